@@ -1,0 +1,263 @@
+"""Pins for the oracle's floating-point parts: RGCN layer fwd/bwd, NC loss, LP scores and
+losses, Adam.  Checked against an independent dense formulation (torch CPU float64
+autograd: a library routine, not the oracle's loops), closed forms printed in the paper /
+SPEC, special cases and central finite differences."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rand_block(rng, n_dst, n_src_extra, R, E):
+    """A random block: dst rows 0..n_dst-1 are the first src rows (dst prefix)."""
+    n_src = n_dst + n_src_extra
+    e_dst = np.sort(rng.integers(0, n_dst, E))
+    e_et = rng.integers(0, R, E).astype(np.int32)
+    e_src = rng.integers(0, n_src, E).astype(np.int32)
+    order = np.lexsort((e_et, e_dst))
+    blk = oracle.Block(dst_gid=np.arange(n_dst), src_gid=np.arange(n_src), seg_cnt=None,
+                       e_src_gid=e_src.astype(np.int64), e_eid=None, e_etype=e_et[order], e_dst=e_dst[order],
+                       e_src=e_src[order], self_row=np.arange(n_dst), src_type_cnt=None)
+    return blk, n_src
+
+
+def _dense_torch(blk, n_src, R, h_src, W, b, relu):
+    """Independent formulation: Z = H_dst W_self + sum_r (D_r^-1 A_r) H_src W_r + b, with a
+    dense row-normalised adjacency per relation (textbook RGCN matrix form)."""
+    n_dst = len(blk.dst_gid)
+    H = torch.tensor(h_src, dtype=torch.float64, requires_grad=True)
+    Wt = torch.tensor(W, dtype=torch.float64, requires_grad=True)
+    bt = torch.tensor(b, dtype=torch.float64, requires_grad=True)
+    Z = H[torch.as_tensor(blk.self_row)] @ Wt[R] + bt
+    for r in range(R):
+        A = torch.zeros(n_dst, n_src, dtype=torch.float64)
+        m = blk.e_etype == r
+        for v, u in zip(blk.e_dst[m], blk.e_src[m]):
+            A[v, u] += 1.0
+        deg = A.sum(1, keepdim=True)
+        A = torch.where(deg > 0, A / deg.clamp(min=1), A)
+        Z = Z + A @ H @ Wt[r]
+    out = torch.relu(Z) if relu else Z
+    return H, Wt, bt, Z, out
+
+
+@pytest.mark.parametrize("relu", [True, False])
+def test_rgcn_fwd_bwd_vs_dense_autograd(relu):
+    rng = np.random.default_rng(10)
+    R, d_in, d_out = 3, 5, 4
+    blk, n_src = _rand_block(rng, 12, 9, R, 60)
+    h = rng.standard_normal((n_src, d_in))
+    W = rng.standard_normal((R + 1, d_in, d_out))
+    b = rng.standard_normal(d_out)
+    z, hd = oracle.rgcn_fwd(blk, R, h, W, b, relu)
+    H, Wt, bt, Z, out = _dense_torch(blk, n_src, R, h, W, b, relu)
+    np.testing.assert_allclose(z, Z.detach().numpy(), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(hd, out.detach().numpy(), rtol=1e-12, atol=1e-12)
+    g = rng.standard_normal(hd.shape)
+    (out * torch.tensor(g)).sum().backward()
+    dW, db, dhs = oracle.rgcn_bwd(blk, R, h, W, z, relu, g, need_dh_src=True)
+    np.testing.assert_allclose(dW, Wt.grad.numpy(), rtol=1e-11, atol=1e-11)
+    np.testing.assert_allclose(db, bt.grad.numpy(), rtol=1e-11, atol=1e-11)
+    np.testing.assert_allclose(dhs, H.grad.numpy(), rtol=1e-11, atol=1e-11)
+
+
+def test_rgcn_finite_differences():
+    """Central differences in double, eps 1e-6."""
+    rng = np.random.default_rng(11)
+    R, d_in, d_out = 2, 3, 3
+    blk, n_src = _rand_block(rng, 5, 4, R, 20)
+    h = rng.standard_normal((n_src, d_in))
+    W = rng.standard_normal((R + 1, d_in, d_out))
+    b = rng.standard_normal(d_out)
+    g = rng.standard_normal((5, d_out))
+
+    def f(h_, W_, b_):
+        return float((oracle.rgcn_fwd(blk, R, h_, W_, b_, False)[1] * g).sum())
+
+    z, _ = oracle.rgcn_fwd(blk, R, h, W, b, False)
+    dW, db, dhs = oracle.rgcn_bwd(blk, R, h, W, z, False, g, need_dh_src=True)
+    eps = 1e-6
+    for arr, grad in ((W, dW), (h, dhs), (b, db)):
+        for idx in list(np.ndindex(arr.shape))[:25]:
+            p = arr.copy(); p[idx] += eps
+            m = arr.copy(); m[idx] -= eps
+            args_p = [h, W, b]; args_m = [h, W, b]
+            k = [h is arr, W is arr, b is arr].index(True)
+            args_p[k] = p; args_m[k] = m
+            fd = (f(*args_p) - f(*args_m)) / (2 * eps)
+            assert abs(fd - grad[idx]) <= 1e-6 * max(1.0, abs(fd))
+
+
+def test_rgcn_special_cases():
+    # isolated node, W_self = I, b = 0, identity act -> h' = h
+    blk = oracle.Block(np.arange(2), np.arange(3), None, np.zeros(0, np.int64), None,
+                       np.zeros(0, np.int32), np.zeros(0, np.int64), np.zeros(0, np.int32), np.arange(2), None)
+    R, d = 2, 4
+    W = np.zeros((R + 1, d, d)); W[R] = np.eye(d)
+    h = np.random.default_rng(0).standard_normal((3, d))
+    _, out = oracle.rgcn_fwd(blk, R, h, W, np.zeros(d), False)
+    np.testing.assert_array_equal(out, h[:2])
+    # one neighbor u, W_self = 0, W_r = I -> h'_v = h_u
+    blk = oracle.Block(np.arange(1), np.arange(3), None, np.array([2]), None,
+                       np.array([1], np.int32), np.array([0]), np.array([2], np.int32), np.arange(1), None)
+    W = np.zeros((R + 1, d, d)); W[1] = np.eye(d)
+    _, out = oracle.rgcn_fwd(blk, R, h, W, np.zeros(d), False)
+    np.testing.assert_array_equal(out[0], h[2])
+    # zero upstream -> zero grads; absent relation -> zero dW_r
+    z, _ = oracle.rgcn_fwd(blk, R, h, W, np.zeros(d), True)
+    dW, db, dhs = oracle.rgcn_bwd(blk, R, h, W, z, True, np.zeros((1, d)), True)
+    assert not dW.any() and not db.any() and not dhs.any()
+    dW, _, _ = oracle.rgcn_bwd(blk, R, h, W, z, False, np.ones((1, d)), True)
+    assert not dW[0].any() and dW[1].any()
+
+
+def test_rgcn_aggregate_then_transform_equals_transform_then_aggregate():
+    """Linearity (R-rgcn order): mean_e(h_u) W == mean_e(h_u W), to 1e-12 in double."""
+    rng = np.random.default_rng(12)
+    R, d_in, d_out = 2, 6, 5
+    blk, n_src = _rand_block(rng, 8, 6, R, 40)
+    h = rng.standard_normal((n_src, d_in))
+    W = rng.standard_normal((R + 1, d_in, d_out))
+    z, _ = oracle.rgcn_fwd(blk, R, h, W, np.zeros(d_out), False)
+    z2 = h[blk.self_row] @ W[R]
+    for v in range(8):
+        for r in range(R):
+            m = (blk.e_dst == v) & (blk.e_etype == r)
+            if m.any():
+                z2[v] += np.mean([h[u] @ W[r] for u in blk.e_src[m]], axis=0)
+    np.testing.assert_allclose(z, z2, rtol=1e-12, atol=1e-12)
+
+
+def test_nc_loss_vs_torch_cross_entropy():
+    rng = np.random.default_rng(13)
+    n, d, C = 17, 6, 9
+    h = rng.standard_normal((n, d)); Wc = rng.standard_normal((d, C)); bc = rng.standard_normal(C)
+    y = rng.integers(0, C, n).astype(np.int32)
+    loss, logits, dh, dWc, dbc = oracle.nc_loss(h, Wc, bc, y)
+    H = torch.tensor(h, requires_grad=True); W = torch.tensor(Wc, requires_grad=True); B = torch.tensor(bc, requires_grad=True)
+    L = torch.nn.functional.cross_entropy(H @ W + B, torch.tensor(y, dtype=torch.long))
+    L.backward()
+    assert abs(loss - L.item()) < 1e-12
+    np.testing.assert_allclose(dh, H.grad.numpy(), rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(dWc, W.grad.numpy(), rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(dbc, B.grad.numpy(), rtol=1e-11, atol=1e-13)
+
+
+def test_nc_loss_uniform_logits_is_ln_C():
+    # uniform logits over C classes -> ln C
+    C = 349
+    loss, *_ = oracle.nc_loss(np.zeros((4, 3)), np.zeros((3, C)), np.full(C, 0.7), np.array([0, 5, 9, 348]))
+    assert abs(loss - np.log(C)) < 1e-12
+
+
+def _golden_lp():
+    rows = []
+    for l in open(os.path.join(GOLDEN, "lp_losses.txt")):
+        if l.strip() and not l.startswith("#"):
+            kind, pos, negs, exp = l.split()[:4]
+            rows.append((kind, float(pos), [] if negs == "-" else [float(x) for x in negs.split(",")], float(exp)))
+    return rows
+
+
+@pytest.mark.parametrize("row", _golden_lp())
+def test_lp_loss_closed_forms(row):
+    """Eq. 7 / Eq. 4 closed forms (tests/golden/lp_losses.txt).  Scores are produced through
+    DistMult with d=1, hu=1, rel=1, hv=pos, hn=neg (Eq. 3 with n=1)."""
+    kind, pos, negs, exp = row
+    if kind == "contrastive":
+        K = len(negs)
+        loss, scores, *_ = oracle.lp_loss(np.ones((1, 1)), np.array([[pos]]), np.array(negs)[:, None],
+                                          np.ones(1), K, 0)
+        assert scores[0, 0] == pos
+        assert abs(loss - exp) < 1e-12
+    else:
+        # single positive edge, y = 1: K=1 negative with score -inf contributes 0 to the mean
+        # only in the limit, so evaluate the per-edge term through a K=1 call and remove the
+        # negative's analytic part: loss = (l_pos + l_neg)/2
+        neg = -50.0
+        loss, *_ = oracle.lp_loss(np.ones((1, 1)), np.array([[pos]]), np.array([[neg]]), np.ones(1), 1, 1)
+        l_neg = np.log1p(np.exp(neg))
+        assert abs(2 * loss - l_neg - exp) < 1e-12
+
+
+def test_lp_distmult_reduces_to_dot_and_zero():
+    # rel = 1 -> dot product (Eq. 2); rel = 0 -> 0
+    rng = np.random.default_rng(14)
+    hu, hv, hn = rng.standard_normal((4, 8)), rng.standard_normal((4, 8)), rng.standard_normal((4, 8))
+    _, sc, *_ = oracle.lp_loss(hu, hv, hn, np.ones(8), 2, 0)
+    np.testing.assert_allclose(sc[:, 0], (hu * hv).sum(1), rtol=1e-13)
+    np.testing.assert_allclose(sc[0, 1:], hu[0] @ hn[0:2].T, rtol=1e-13)
+    np.testing.assert_allclose(sc[3, 1:], hu[3] @ hn[2:4].T, rtol=1e-13)
+    _, sc, *_ = oracle.lp_loss(hu, hv, hn, np.zeros(8), 2, 0)
+    assert not sc.any()
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_lp_loss_grads_vs_torch(kind):
+    rng = np.random.default_rng(15 + kind)
+    B, K, d = 12, 4, 5
+    hu, hv, hn, rel = (rng.standard_normal(s) for s in ((B, d), (B, d), (B, d), (d,)))
+    loss, sc, dhu, dhv, dhn, drel = oracle.lp_loss(hu, hv, hn, rel, K, kind)
+    U, V, N, Rl = (torch.tensor(x, requires_grad=True) for x in (hu, hv, hn, rel))
+    g = torch.arange(B) // K
+    pos = (U * Rl * V).sum(1)
+    neg = torch.einsum("bk,bjk->bj", U * Rl, N.view(-1, K, d)[g])
+    S = torch.cat([pos[:, None], neg], 1)
+    if kind == 0:
+        L = (torch.logsumexp(S, 1) - pos).mean()
+    else:
+        y = torch.zeros_like(S); y[:, 0] = 1
+        L = torch.nn.functional.binary_cross_entropy_with_logits(S, y, reduction="none").mean(1).mean()
+    L.backward()
+    assert abs(loss - L.item()) < 1e-12
+    for a, t in ((dhu, U), (dhv, V), (dhn, N), (drel, Rl)):
+        np.testing.assert_allclose(a, t.grad.numpy(), rtol=1e-11, atol=1e-13)
+
+
+def test_contrastive_shift_invariance():
+    # adding c to all N+1 scores leaves Eq. 7 unchanged (shift through hv/hn with rel=1, hu=1)
+    pos, negs = 0.3, np.array([0.1, -0.4, 1.2])
+    l1, *_ = oracle.lp_loss(np.ones((1, 1)), np.array([[pos]]), negs[:, None], np.ones(1), 3, 0)
+    l2, *_ = oracle.lp_loss(np.ones((1, 1)), np.array([[pos + 7]]), negs[:, None] + 7, np.ones(1), 3, 0)
+    assert abs(l1 - l2) < 1e-12
+
+
+def test_adam_step1_closed_form_and_vs_torch():
+    rng = np.random.default_rng(16)
+    n = 50
+    p0 = rng.standard_normal(n)
+    g = rng.standard_normal(n)
+    p = p0.copy(); m = np.zeros(n); v = np.zeros(n)
+    oracle.adam(p, g, m, v, lr=0.01, t=1)
+    # step 1: delta = -lr g / (|g| + eps)  (bias-corrected moments)
+    np.testing.assert_allclose(p, p0 - 0.01 * g / (np.abs(g) + 1e-8), rtol=1e-12, atol=1e-15)
+    # several steps vs torch.optim.Adam (library routine)
+    P = torch.tensor(p0, requires_grad=True)
+    opt = torch.optim.Adam([P], lr=0.01, betas=(0.9, 0.999), eps=1e-8)
+    p = p0.copy(); m = np.zeros(n); v = np.zeros(n)
+    for t in range(1, 6):
+        gt = rng.standard_normal(n)
+        P.grad = torch.tensor(gt)
+        opt.step()
+        oracle.adam(p, gt, m, v, lr=0.01, t=t)
+    np.testing.assert_allclose(p, P.detach().numpy(), rtol=1e-12, atol=1e-14)
+
+
+def test_nc_step_composition_tiny():
+    """The full NC step on a scaled tiny config: finite, loss near ln C at init, grads for
+    every parameter, and the oracle's composition order (input layer first)."""
+    cfg = synth.scaled(synth.tiny(), 0.2)
+    g = oracle.Graph(cfg)
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    seeds = synth.nc_seeds(cfg, 0)
+    res = oracle.nc_step(g, params, seeds, synth.labels(cfg), step=0, rng_seed=cfg.rng_seed)
+    assert np.isfinite(res.loss) and abs(res.loss - np.log(cfg.num_classes)) < 1.0
+    assert set(res.grads) == set(synth.param_order(cfg))
+    assert res.blocks[-1].dst_gid.tolist() == seeds.tolist()
+    assert res.x0.shape == (len(res.blocks[0].src_gid), cfg.feat_dim)
