@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""bench.py -- RGCN mini-batch train step on B200 (GraphStorm arXiv 2406.06022 hot path).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gsb|reference] [--config mag]
+
+One step = one pass of the whole hot path over one mini-batch of synthetic input
+(SURVEY.md §8(a)): seed batch -> per-etype fanout sampling (2 hops) -> relabel -> feature
+gather -> 2 RGCN layers -> NC decoder + softmax CE -> backward -> (N>1: NCCL gradient
+all-reduce) -> Adam.  Rank 0 prints ONE JSON line.  `--impl reference` times the CPU
+oracle (the only other place bench.py executes oracle/) on bounded samples.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "RGCN train seeds/sec (and sampled edges/sec) on B200"
+UNIT = "seeds/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="gsb", choices=["gsb", "reference"])
+    ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
+    ap.add_argument("--profile-steps", type=int, default=20)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def config_for(name: str) -> synth.Config:
+    return synth.get(name)
+
+
+def cfg_json(cfg: synth.Config, n_gpus: int, extra=None) -> dict:
+    d = {"workload": f"{cfg.name}-shaped synthetic heterograph, RGCN NC train step",
+         "ntypes": cfg.num_ntypes, "etypes": cfg.num_etypes, "nodes": cfg.num_nodes, "edges": cfg.num_edges,
+         "feat_dim": cfg.feat_dim, "fanouts": cfg.fanouts, "batch_per_gpu": cfg.batch,
+         "global_batch": cfg.batch * n_gpus, "hidden": cfg.hidden, "num_classes": cfg.num_classes,
+         "layers": len(cfg.fanouts), "optimizer": "adam",
+         "parallelism": "single" if n_gpus == 1 else f"dp{n_gpus} (graph replicated, NCCL grad all-reduce)",
+         "l2": "inputs larger than L2: feature table + CSC >> 126 MB, fresh random seed batch every step"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "nvml")}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ roofline
+def peaks():
+    p = {"hbm_gbs": None, "src": "fallback"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        j = json.load(open(path))
+        p = {"hbm_gbs": float(j["hbm_gbs"]), "bf16_tflops": float(j.get("bf16_tflops", 0)),
+             "bf16_tflops_sustained": float(j.get("bf16_tflops_sustained", 0)),
+             "sm_max_mhz": float(j.get("sm_max_mhz", 1965.0)), "src": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0,
+             "src": "fallback (B200_PROFILING.md)"}
+    # FP32 FFMA peak: 148 SMs x 128 FP32 lanes x 2 flop x max SM clock
+    p["fp32_tflops"] = 148 * 128 * 2 * p.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    return p
+
+
+def kernel_work(name: str, sz: dict, cfg: synth.Config):
+    """Algorithmic bytes (HBM-bound kernels) or flops (GEMMs) of ONE launch of `name` for
+    a step with block sizes sz (per-unit figures)."""
+    d0, hd, C = cfg.feat_dim, cfg.hidden, cfg.num_classes
+    L = len(cfg.fanouts)
+    if name == "gather":
+        n = sz["n_src"][0]
+        return "bytes", n * d0 * 4 * 2 + n * 8
+    if name == "rgcn_agg":
+        # per launch: average over the layers it ran for (caller divides); return the sum
+        tot = 0
+        for l in range(L):
+            d = d0 if l == 0 else hd
+            tot += sz["n_edges"][l] * (d * 4 + 4) + sz["n_dst"][l] * d * 4 + sz["acat_cols"][l] * 4
+        return "bytes", tot / L
+    if name in ("rgcn_gemm_fwd", "rgcn_gemm_dW"):
+        tot = 0
+        for l in range(L):
+            d = d0 if l == 0 else hd
+            tot += 2 * sz["acat_cols"][l] // d * d * hd
+        return "flops", tot / L
+    if name == "rgcn_gemm_dA":
+        l = L - 1
+        return "flops", 2 * sz["acat_cols"][l] * hd
+    if name in ("nc_logits", "nc_gemm_dWc", "nc_gemm_dh"):
+        return "flops", 2 * cfg.batch * hd * C
+    return None, None
+
+
+# ------------------------------------------------------------------------------ gsb arm
+def build_gsb(cfg, device):
+    import torch
+    from paper_2406_06022_b200.runtime import GraphStore, RGCNTrainer
+    st = GraphStore(cfg.counts, cfg.etype_src(), cfg.etype_dst(), device)
+    for r in range(cfg.num_etypes):
+        s, d = synth.etype_coo(cfg, r, backend="torch", device=device)
+        st.load_etype(r, s, d)
+        del s, d
+    for t in range(cfg.num_ntypes):
+        st.set_features(t, synth.feature_table(cfg, t, backend="torch", device=device))
+    torch.cuda.synchronize()
+    tr = RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
+                     synth.param_order(cfg), synth.labels(cfg, backend="torch", device=device),
+                     int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
+    return st, tr
+
+
+def block_sizes(tr, cfg):
+    L = len(cfg.fanouts)
+    sm = tr.sampler
+    out = {"n_dst": [], "n_src": [], "n_edges": [], "acat_cols": []}
+    slots = tr.store.slot_etypes()
+    for l in range(L):
+        b = sm.block(l)
+        d = cfg.feat_dim if l == 0 else cfg.hidden
+        out["n_dst"].append(int(b.dst_gid.numel()))
+        out["n_src"].append(int(b.src_gid.numel()))
+        out["n_edges"].append(int(b.e_src.numel()))
+        out["acat_cols"].append(int(sum(int(b.dst_type_cnt[t]) * (len(slots[t]) + 1) * d for t in range(len(slots)))))
+    return out
+
+
+def run_gsb(args, cfg):
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = f"cuda:{local}"
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(device))
+    from paper_2406_06022_b200 import _lib
+    t0 = time.time()
+    st, tr = build_gsb(cfg, device)
+    setup_s = time.time() - t0
+    train = synth.train_nodes(cfg)
+    per_epoch = max(1, len(train) // cfg.batch)
+    # seed batches (a1): device-resident epoch permutation slices; rank r takes batch step*ws + r
+    n_batches = args.warmup + args.steps + args.profile_steps + 8
+    seeds_all = torch.from_numpy(np.stack([synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train)
+                                           for i in range(n_batches)])).to(device)
+
+    def step(i):
+        tr.forward_backward(seeds_all[i], i * ws + rank)
+        if dist is not None:
+            dist.all_reduce(tr.grad)          # C6: NCCL all-reduce of the flat dense grads
+            tr.grad.mul_(1.0 / ws)
+        tr.optimizer_step()
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if tr.sampler.poll_error() != 0:
+        raise RuntimeError("device-side sampling error latched")
+    # ---- timed region
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.lib().gsb_launch_count()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for i in range(args.warmup, args.warmup + args.steps):
+            step(i)
+        e1.record()
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    launches = _lib.lib().gsb_launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    seeds_per_s = cfg.batch * ws * args.steps / (ms / 1e3)
+
+    # ---- sizes + per-kernel profile (separate pass, CUDA events around every launch)
+    base = args.warmup + args.steps
+    _lib.lib().gsb_profile_enable(1)
+    for i in range(base, base + args.profile_steps):
+        step(i)          # no host sync inside: events see GPU time, not launch gaps
+    torch.cuda.synchronize()
+    _lib.lib().gsb_profile_enable(0)
+    # block sizes of the profiled steps: sampling is a pure function of (seeds, step), so
+    # re-sampling the same batches reproduces them bit-exactly
+    sizes = []
+    for i in range(base, base + args.profile_steps):
+        tr.sampler.sample(seeds_all[i], tr.rng_seed, i * ws + rank)
+        sizes.append(block_sizes(tr, cfg))
+    import ctypes as C
+    buf = C.create_string_buffer(1 << 16)
+    _lib.call("gsb_profile_dump", buf, len(buf))
+    prof = {}
+    for line in buf.value.decode().splitlines():
+        n, c, t = line.split()
+        prof[n] = {"launches": int(c), "total_ms": float(t)}
+    edges_per_step = float(np.mean([sum(s["n_edges"]) for s in sizes]))
+    # ---- e2e: public API with host buffers (pinned seeds H2D + loss D2H every step)
+    seeds_host = torch.from_numpy(np.stack([synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train)
+                                            for i in range(args.steps)])).pin_memory()
+    loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        if dist is None:
+            tr.train_step_host(seeds_host[i], base + args.profile_steps + i, loss_host)
+        else:
+            n = seeds_host[i].numel()
+            tr.seeds_dev[:n].copy_(seeds_host[i], non_blocking=True)
+            step_dev = tr.seeds_dev[:n]
+            tr.forward_backward(step_dev, base + i)
+            dist.all_reduce(tr.grad)
+            tr.grad.mul_(1.0 / ws)
+            tr.optimizer_step()
+            loss_host.copy_(tr.loss, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": cfg.batch * ws * args.steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(seeds_host[0].numel() * 8), "d2h_bytes_per_step": 4,
+           "final_loss": float(loss_host[0])}
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return None
+    # ---- roofline of the dominant kernel
+    pk = peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1]["total_ms"])[0]
+    kind, _ = kernel_work(dom, sizes[0], cfg)
+    roof = None
+    if kind is not None:
+        works = [kernel_work(dom, s, cfg)[1] for s in sizes]
+        per_launch_work = float(np.mean(works))
+        launches_per_step = prof[dom]["launches"] / args.profile_steps
+        avg_ms = prof[dom]["total_ms"] / prof[dom]["launches"]
+        if kind == "bytes":
+            ach = per_launch_work / (avg_ms / 1e3) / 1e9
+            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / pk["hbm_gbs"], "traffic": None, "peak_src": pk["src"]}
+        else:
+            ach = per_launch_work / (avg_ms / 1e3) / 1e12
+            roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
+                    "frac": ach / pk["fp32_tflops"], "traffic": None,
+                    "peak_src": "FP32 FFMA: 148 SMs x 128 lanes x 2 x sm_max_mhz (DESIGN.md)"}
+        roof["avg_launch_us"] = avg_ms * 1e3
+        roof["launches_per_step"] = launches_per_step
+        roof["algorithmic_per_launch"] = per_launch_work
+    step_ms_prof = sum(v["total_ms"] for v in prof.values()) / args.profile_steps
+    kernels = {k: {"us_per_step": v["total_ms"] * 1e3 / args.profile_steps,
+                   "share": v["total_ms"] / args.profile_steps / step_ms_prof} for k, v in
+               sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])}
+    line = {
+        "metric": METRIC, "value": seeds_per_s, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded hash generator, synth/)",
+        "config": cfg_json(cfg, ws),
+        "sampled_edges_per_s": edges_per_step * ws / (ms_per_step / 1e3),
+        "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
+        "kernels": kernels, "setup_s": setup_s,
+    }
+    if dist is not None:
+        dist.destroy_process_group()
+    return line, st, tr
+
+
+# ------------------------------------------------------------------------------ oracle
+def oracle_rate(cfg, seconds: float, sub_batch: int, max_steps: int = 10 ** 9, min_steps: int = 1):
+    """Time the oracle (as it stands, single-threaded) on bounded samples of the workload:
+    train steps on sub-batches of `sub_batch` seeds until `seconds` of CPU work."""
+    import oracle
+    t0 = time.time()
+    og = oracle.Graph(cfg)
+    for t in range(cfg.num_ntypes):
+        og.feats[t] = synth.feature_table(cfg, t)
+    setup = time.time() - t0
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    opt = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}
+    labels = synth.labels(cfg)
+    train = synth.train_nodes(cfg)
+    n_seeds, steps, el = 0, 0, 0.0
+    while (el < seconds or steps < min_steps) and steps < max_steps:
+        seeds = synth.nc_seeds(cfg, steps, train)[:sub_batch]
+        t1 = time.perf_counter()
+        oracle.train_step(og, params, opt, steps + 1, (seeds, labels), steps, cfg.rng_seed, cfg.lr)
+        el += time.perf_counter() - t1
+        n_seeds += len(seeds)
+        steps += 1
+    return {"value": n_seeds / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{steps} oracle train steps of {sub_batch} seeds each ({cfg.name} graph, fanouts "
+                      f"{cfg.fanouts}), {el:.1f} s of single-threaded CPU work; oracle CSC build "
+                      f"{setup:.1f} s excluded", "steps": steps, "seconds": el}
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    sub = max(8, cfg.batch // 16)
+    import oracle
+    t0 = time.time()
+    og = oracle.Graph(cfg)
+    for t in range(cfg.num_ntypes):
+        og.feats[t] = synth.feature_table(cfg, t)
+    setup = time.time() - t0
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    opt = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}
+    labels = synth.labels(cfg)
+    train = synth.train_nodes(cfg)
+
+    def step(i):
+        seeds = synth.nc_seeds(cfg, i, train)[:sub]
+        oracle.train_step(og, params, opt, i + 1, (seeds, labels), i, cfg.rng_seed, cfg.lr)
+
+    for i in range(args.warmup):
+        step(i)
+    t1 = time.perf_counter()
+    for i in range(args.warmup, args.warmup + args.steps):
+        step(i)
+    el = time.perf_counter() - t1
+    v = sub * args.steps / el
+    return {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded hash generator, synth/)", "impl": "reference",
+            "config": cfg_json(cfg, ws, {"reference_sub_batch": sub}),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"each step = one oracle train step on {sub} of the batch's seeds; "
+                                       f"oracle CSC build {setup:.1f} s excluded"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+
+
+def main():
+    args = parse()
+    cfg = config_for(args.config)
+    if args.impl == "reference":
+        line = run_reference(args, cfg)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    out = run_gsb(args, cfg)
+    if out is None:
+        return
+    line, st, tr = out
+    if not args.no_cpu_baseline:
+        del tr, st
+        import torch
+        torch.cuda.empty_cache()
+        line["cpu_baseline"] = oracle_rate(cfg, args.cpu_seconds, cfg.batch)
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

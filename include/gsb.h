@@ -1,0 +1,226 @@
+/*
+ * gsb.h -- C ABI of libgsb: a B200-native (sm_100a) RGCN mini-batch training step,
+ * after GraphStorm (Zheng et al., arXiv 2406.06022, KDD'24).
+ *
+ * Citations: "P:Lnnn" = /root/reference/PAPER.md line nnn; "S:Lnnn" = SPEC.md line nnn;
+ * "R-x" = a reading of a silent / garbled passage, listed in DESIGN.md §Readings.
+ *
+ * Conventions (all entry points):
+ *  - Plain C types only.  "device" pointers are CUDA global-memory pointers (e.g. a
+ *    torch tensor's data_ptr); "host" pointers are CPU memory.  `stream` is a
+ *    cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Ownership: the library never allocates device memory.  Every device buffer is
+ *    caller-owned; sizes come from the *_bytes / *_floats queries.  Handles
+ *    (gsb_graph_t, gsb_blocks_t) are small host structs owned by the library, freed by
+ *    their *_destroy call; they keep (do not copy) the device pointers registered in them.
+ *  - Asynchrony: every call only enqueues work on `stream` and returns, except the
+ *    calls documented as "syncs".  No call performs a host<->device transfer of data
+ *    sizes on the hot path, so a whole train step can be captured in a CUDA graph.
+ *  - Errors: argument / shape / capacity errors return a non-zero gsb_status
+ *    synchronously and set gsb_last_error() (thread-local text).  Errors detected by a
+ *    kernel (unknown node id, frontier not grouped by node type, capacity overflow) are
+ *    latched in a device word inside the arena and returned by gsb_blocks_poll_error().
+ *  - Layouts: node features / hidden states are row-major [rows][dim] fp32.  Global node
+ *    ids (gid) are type-major: gid = node_off[t] + local id (R-gid).  Relation weights W
+ *    of a layer are row-major [R+1][d_in][d_out]; slot R is W_self.
+ *  - Threads: calls on one handle are not thread-safe; separate handles are independent.
+ */
+#ifndef GSB_H_
+#define GSB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t gsb_status;
+#define GSB_OK 0
+#define GSB_EINVAL 1      /* bad argument / shape / unsupported configuration        */
+#define GSB_EWORKSPACE 2  /* caller-provided buffer too small                         */
+#define GSB_ECUDA 3       /* a CUDA runtime call or kernel launch failed              */
+#define GSB_EDEVICE 4     /* a latched device-side error (see gsb_blocks_poll_error)  */
+
+#define GSB_MAX_NTYPES 8
+#define GSB_MAX_ETYPES 32
+#define GSB_MAX_SLOTS 8    /* max in-relations of one node type */
+#define GSB_MAX_LAYERS 4
+#define GSB_MAX_FANOUT 32  /* Floyd draws are resolved by one warp; -1 (ALL) is unbounded */
+
+/* Thread-local message for the last non-OK status of this thread. */
+const char* gsb_last_error(void);
+/* ABI version (major*100 + minor). */
+int32_t gsb_version(void);
+
+/* --------------------------------------------------------------------------------------
+ * Instrumentation (used by bench.py for the roofline numbers; off by default).
+ *  gsb_launch_count: number of kernels this library has launched since load.
+ *  gsb_profile_enable(1): from now on every launch is bracketed by CUDA events on its
+ *    own stream.  gsb_profile_dump (syncs the device) writes one line per kernel name,
+ *    "name launches total_ms\n", into buf (truncated to buflen) and clears the records.
+ * ------------------------------------------------------------------------------------ */
+int64_t gsb_launch_count(void);
+gsb_status gsb_profile_enable(int32_t on);
+gsb_status gsb_profile_dump(char* buf, size_t buflen);
+
+/* ======================================================================================
+ * Graph store ("distributed graph engine"; S:L225 load_partition, S:L240 edge
+ * owned by its destination).  One CSC per etype over destination nodes of its dst type:
+ *   indptr  int64 [n_dst + 1]   (device)
+ *   indices int32 [n_edges]     (device) src local id, ascending within a segment (R-csc)
+ *   eid of an edge = eid_base[etype] + its CSC position (R-eid; no array stored).
+ * ==================================================================================== */
+typedef struct gsb_graph* gsb_graph_t;
+
+/* Create the (host) schema handle.  ntype_count: host [num_ntypes] node counts;
+ * etype_src / etype_dst: host [num_etypes] node type ids.  Fails with GSB_EINVAL for
+ * num_ntypes > GSB_MAX_NTYPES, num_etypes > GSB_MAX_ETYPES, more than GSB_MAX_SLOTS
+ * etypes into one node type, or > 2^31 nodes in one type. */
+gsb_status gsb_graph_create(int32_t num_ntypes, const int64_t* ntype_count, int32_t num_etypes,
+                            const int32_t* etype_src, const int32_t* etype_dst, gsb_graph_t* out);
+gsb_status gsb_graph_destroy(gsb_graph_t g);
+
+/* Device workspace bytes needed by gsb_csc_build for n_edges COO edges of `etype`. */
+gsb_status gsb_csc_build_bytes(gsb_graph_t g, int32_t etype, int64_t n_edges, size_t* bytes);
+
+/* Build the CSC of `etype` on the device from a COO edge list (src, dst: device int32
+ * local ids, n_edges).  keep: optional device uint8 mask (NULL = keep all); val/test LP
+ * edges are dropped this way.  Output: indptr (device int64 [n_dst+1]), indices
+ * (device int32, capacity n_edges).  *n_kept (host) receives the kept edge count.
+ * Registers indptr/indices in g for `etype` (eid_base 0).  Syncs `stream`. */
+gsb_status gsb_csc_build(gsb_graph_t g, int32_t etype, const int32_t* src, const int32_t* dst,
+                         const uint8_t* keep, int64_t n_edges, int64_t* indptr, int32_t* indices,
+                         int64_t* n_kept, void* ws, size_t ws_bytes, void* stream);
+
+/* Register a prebuilt CSC (device pointers) for `etype`; eid_base is added to CSC
+ * positions to form edge ids (multi-GPU partitions). */
+gsb_status gsb_graph_set_csc(gsb_graph_t g, int32_t etype, const int64_t* indptr, const int32_t* indices,
+                             int64_t n_edges, int64_t eid_base);
+
+/* Register the feature table of `ntype`: device fp32 [ntype_count][dim] row-major
+ * (P:L86 distributed tensors).  All ntypes must use the same dim. */
+gsb_status gsb_graph_set_features(gsb_graph_t g, int32_t ntype, const float* feat, int32_t dim);
+
+/* Feature gather by global id (§8(a) a5; S:L299 fetch_features):
+ *   out[i, :] = F_{t(i)}[gid[i] - node_off[t(i)], :]   for i < n   (exact copy)
+ * gid: device int64 [n]; out: device fp32 [n][dim].  A gid outside [0, total nodes)
+ * yields a zero row. */
+gsb_status gsb_gather(gsb_graph_t g, const int64_t* gid, int64_t n, float* out, void* stream);
+
+/* ======================================================================================
+ * Mini-batch sampling into message-flow blocks (P:L58, P:L86 on-the-fly sampling;
+ * Fig. 4 P:L122-128 fanout/batch; Fig. 8 P:L480-486 blocks[i]).
+ *
+ * gsb_sample draws L hops from the seeds.  Hop h (1-based from the seeds) uses fanout
+ * f[L-h] (layer l consumes the block of hop L-l; blocks[0] is the input layer, R-fanout).
+ * For every frontier node v and every etype r into type(v) (ascending r) it keeps
+ * min(f, deg'_r(v)) in-edges chosen uniformly without replacement (R-wor) by Floyd's
+ * algorithm on Philox4x32-10 draws keyed by (rng_seed; dst gid, etype, hop, draw, step)
+ * (R-rng, R-floyd); f = -1 keeps all.  deg' excludes the batch's LP target edges
+ * (u,v) in excl_etype and (v,u) in excl_rev_etype (R-excl).
+ * Relabel (R-relabel): per ntype, src list = [frontier nodes of that type, frontier order]
+ * ++ ascending unique new sampled sources; the next frontier is their concatenation.
+ * Frontier / seeds must be grouped by node type in ascending type order (latched error
+ * otherwise).  All sizes after the seeds stay on the device.
+ * ==================================================================================== */
+typedef struct gsb_blocks* gsb_blocks_t;
+
+/* fanouts: host [num_layers], f[l] for layer l, each -1 or 1..GSB_MAX_FANOUT.
+ * max_seeds: capacity of the seed frontier; max_excl: capacity of LP exclusion pairs. */
+gsb_status gsb_blocks_create(gsb_graph_t g, int32_t num_layers, const int32_t* fanouts, int64_t max_seeds,
+                             int64_t max_excl, gsb_blocks_t* out);
+gsb_status gsb_blocks_destroy(gsb_blocks_t b);
+/* Device arena bytes for all blocks of one mini-batch (upper bounds). */
+gsb_status gsb_blocks_arena_bytes(gsb_blocks_t b, size_t* bytes);
+/* One-time arena initialisation (node maps to "absent").  Must precede the first sample. */
+gsb_status gsb_blocks_init_arena(gsb_blocks_t b, void* arena, size_t arena_bytes, void* stream);
+
+/* seeds: device int64 gids [n_seeds]; excl_u/excl_v: device int64 gids [n_excl] (may be
+ * NULL when n_excl == 0).  Writes the blocks into the arena. */
+gsb_status gsb_sample(gsb_blocks_t b, const int64_t* seeds, int64_t n_seeds, uint64_t rng_seed, uint32_t step,
+                      const int64_t* excl_u, const int64_t* excl_v, int64_t n_excl, int32_t excl_etype,
+                      int32_t excl_rev_etype, void* arena, size_t arena_bytes, void* stream);
+
+/* Sizes of the block of `layer` (syncs `stream`): n_dst, n_src, n_edges and the
+ * per-ntype dst / src row counts (host arrays [num_ntypes]). */
+gsb_status gsb_block_sizes(gsb_blocks_t b, const void* arena, int32_t layer, int64_t* n_dst, int64_t* n_src,
+                           int64_t* n_edges, int64_t* dst_type_cnt, int64_t* src_type_cnt, void* stream);
+
+/* Device views of the block of `layer` (pointers into the arena).  Layout:
+ *   dst_gid  int64 [n_dst]          frontier (= src rows [0..] of the same type, dst prefix)
+ *   src_gid  int64 [n_src]          next frontier, type-grouped
+ *   seg_ptr  int64 [n_dst*S+1]      edge offsets of segment (dst row j, slot s), S = slots;
+ *                                   slot s of type t is the s-th etype into t (ascending)
+ *   e_src_gid int64 [n_edges], e_eid int64 [n_edges], e_src int32 [n_edges] (src row)   */
+typedef struct {
+    const int64_t* dst_gid;
+    const int64_t* src_gid;
+    const int64_t* seg_ptr;
+    const int64_t* e_src_gid;
+    const int64_t* e_eid;
+    const int32_t* e_src;
+    int32_t num_slots; /* S */
+} gsb_block_view;
+gsb_status gsb_block_view_get(gsb_blocks_t b, const void* arena, int32_t layer, gsb_block_view* out);
+
+/* Etype of slot s for node type t (-1 if none); host query. */
+gsb_status gsb_slot_etype(gsb_graph_t g, int32_t ntype, int32_t slot, int32_t* etype);
+
+/* Latched device error of the last sample (syncs): 0 = none, 1 = frontier not grouped by
+ * type, 2 = gid out of range, 3 = capacity overflow. */
+gsb_status gsb_blocks_poll_error(gsb_blocks_t b, void* arena, int32_t* code, void* stream);
+
+/* Gather the input features of the sampled mini-batch (layer 0 src rows):
+ * out: device fp32 [n_src(layer 0)][dim] (capacity from gsb_blocks_input_rows). */
+gsb_status gsb_gather_block_inputs(gsb_blocks_t b, const void* arena, float* out, void* stream);
+gsb_status gsb_blocks_input_rows(gsb_blocks_t b, int64_t* max_rows);
+/* Row capacity of the dst rows of `layer` (for h_dst buffers). */
+gsb_status gsb_blocks_dst_rows(gsb_blocks_t b, int32_t layer, int64_t* max_rows);
+
+/* ======================================================================================
+ * RGCN layer (P:L96 RGCN, ref [18]; §8(a) a7, a11):
+ *   A_r[v] = (1/c_r(v)) sum_{sampled e: u->v in r} h_src[u]      (0 if c_r(v) = 0)
+ *   Z_v    = sum_r A_r[v] W_r + h_src[self(v)] W_self + b ;  h_dst = ReLU(Z) or Z
+ * computed as a per-relation segment mean followed by one grouped GEMM per dst type over
+ * the concatenation Acat_v = [A_{r_0}[v] | ... | A_{r_{S_t-1}}[v] | h_src[self(v)]].
+ * d_in must be a multiple of 32 and d_out a multiple of 4.
+ * acat: device fp32 cache [gsb_layer_acat_floats] (kept for the backward).
+ * ==================================================================================== */
+gsb_status gsb_layer_acat_floats(gsb_blocks_t b, int32_t layer, int32_t d_in, int64_t* n_floats);
+
+gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src, int32_t d_in,
+                              const float* W, const float* bias, int32_t d_out, int32_t relu, float* h_dst,
+                              float* acat, void* stream);
+
+/* Backward (analytic):  dZ = dh_dst * 1[h_dst > 0] (relu) or dh_dst;
+ *   dW_r = sum_v A_r[v]^T dZ_v ; dW_self = sum_v h_src[self(v)]^T dZ_v ; db = sum_v dZ_v
+ *   dh_src[u] += (1/c_r(v)) dZ_v W_r^T per sampled edge ; dh_src[self(v)] += dZ_v W_self^T
+ * dW [R+1][d_in][d_out] and db [d_out] are overwritten; dh_src [n_src][d_in] is
+ * overwritten when non-NULL (then dacat_ws [acat floats] is scratch). */
+gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_dst,
+                              const float* dh_dst, const float* W, const float* acat, int32_t d_in, int32_t d_out,
+                              int32_t relu, float* dW, float* db, float* dh_src, float* dacat_ws, void* stream);
+
+/* ======================================================================================
+ * Node-classification decoder + softmax cross-entropy (P:L477 ClassifyLossFunc, P:L489;
+ * S:L405-408; §8(a) a8):  logits = h Wc + bc ; loss = mean_i(lse_i - logit_{i,y_i})
+ *   y_i = labels[seed_gid[i] - label_gid_base].
+ * Writes: logits_ws [n][C] (scratch), loss (device fp32 scalar), dh [n][d], dWc [d][C],
+ * dbc [C] (overwritten).  row_loss_ws: device fp32 [n] scratch.
+ * ==================================================================================== */
+gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, const float* bc, int32_t C,
+                       const int32_t* labels, const int64_t* seed_gid, int64_t label_gid_base, float* logits_ws,
+                       float* row_loss_ws, float* loss, float* dh, float* dWc, float* dbc, void* stream);
+
+/* ======================================================================================
+ * Optimizer (paper silent, R-adam): Adam with bias correction over a flat
+ * fp32 buffer of n parameters; t is the 1-based step.  In place on p, m, v.
+ * ==================================================================================== */
+gsb_status gsb_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1,
+                         float beta2, float eps, int32_t t, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSB_H_ */

@@ -1,0 +1,382 @@
+// core.cu -- errors, instrumentation, graph store (CSC build on the device), feature
+// gather, Adam.  See include/gsb.h for the contract of every extern "C" entry point.
+#include <stdarg.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+
+#include "gsb_internal.cuh"
+
+namespace gsb {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+static bool g_prof_on = false;
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_event_pool;
+static std::mutex g_prof_mu;
+static thread_local const char* g_pending_name = nullptr;
+static thread_local cudaEvent_t g_pending_ev = nullptr;
+
+void set_error(const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+gsb_status cuda_status(cudaError_t e, const char* what) {
+    set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+    return GSB_ECUDA;
+}
+
+void count_launch(int n) { g_launches += n; }
+
+static cudaEvent_t get_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_begin(const char* name, cudaStream_t s) {
+    if (!g_prof_on) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_pending_name = name;
+    g_pending_ev = get_event();
+    cudaEventRecord(g_pending_ev, s);
+}
+
+void prof_end(cudaStream_t s) {
+    if (!g_prof_on || !g_pending_name) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEvent_t b = get_event();
+    cudaEventRecord(b, s);
+    g_prof.push_back({g_pending_name, g_pending_ev, b});
+    g_pending_name = nullptr;
+}
+
+// ------------------------------------------------------------------------------------
+// CSC build kernels
+// ------------------------------------------------------------------------------------
+__global__ void csc_keys_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                const uint8_t* __restrict__ keep, int64_t n, uint64_t* __restrict__ keys,
+                                unsigned long long* __restrict__ n_kept) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long local = 0;
+    for (; i < n; i += stride) {
+        bool k = keep ? (keep[i] != 0) : true;
+        keys[i] = k ? (((uint64_t)(uint32_t)dst[i] << 32) | (uint32_t)src[i]) : ~0ull;
+        local += k ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_kept, local);
+}
+
+__global__ void csc_finish_kernel(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ n_kept_p,
+                                  int64_t n_dst, int64_t* __restrict__ indptr, int32_t* __restrict__ indices) {
+    const int64_t n_kept = (int64_t)*n_kept_p;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_kept; i += stride)
+        indices[i] = (int32_t)(uint32_t)(keys[i] & 0xffffffffull);
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n_dst; v += stride) {
+        uint64_t key = (uint64_t)v << 32;
+        int64_t lo = 0, hi = n_kept;
+        while (lo < hi) {
+            int64_t m = (lo + hi) >> 1;
+            if (keys[m] < key) lo = m + 1; else hi = m;
+        }
+        indptr[v] = lo;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// gather: out[i, :] = F_t[gid_i - off_t, :]; one float4 per thread-iteration
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gather_kernel(GraphDev g, const int64_t* __restrict__ gid,
+                                                     const int64_t* __restrict__ n_dev, int64_t n_host,
+                                                     float* __restrict__ out) {
+    const int64_t n = n_dev ? *n_dev : n_host;
+    const int d4 = g.feat_dim >> 2;
+    const int64_t total = n * d4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t N = g.node_off[g.T];
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // 4 independent rows in flight per thread
+    for (; i < total; i += 4 * stride) {
+        float4 v[4];
+        int64_t idx[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            idx[u] = i + u * stride;
+            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (idx[u] < total) {
+                int64_t row = idx[u] / d4;
+                int c = (int)(idx[u] - row * d4);
+                int64_t x = __ldg(gid + row);
+                if (x >= 0 && x < N) {
+                    int t = type_of(g, x);
+                    const float4* src = reinterpret_cast<const float4*>(g.feat[t] + (x - g.node_off[t]) * g.feat_dim) + c;
+                    v[u] = ldg_nc_f4(src);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (idx[u] < total) reinterpret_cast<float4*>(out)[idx[u]] = v[u];
+    }
+}
+
+gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_dev, int64_t n_host, int64_t n_max,
+                         float* out, cudaStream_t s) {
+    int64_t work = n_max * (G->dev.feat_dim / 4);
+    int grid = grid_for(ceil_div(work, 4), 256, kNumSMs * 8);
+    GSB_LAUNCH("gather", gather_kernel, grid, 256, 0, s, G->dev, gid, n_dev, n_host, out);
+    return GSB_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// Adam (bias-corrected), float4 vectorised
+// ------------------------------------------------------------------------------------
+__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ gr, float* __restrict__ m,
+                            float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps, float c1,
+                            float c2) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        float g = gr[i];
+        float mi = b1 * m[i] + (1.f - b1) * g;
+        float vi = b2 * v[i] + (1.f - b2) * g * g;
+        m[i] = mi;
+        v[i] = vi;
+        float mh = mi / c1;
+        float vh = vi / c2;
+        p[i] -= lr * mh / (sqrtf(vh) + eps);
+    }
+}
+
+}  // namespace gsb
+
+using namespace gsb;
+
+// ====================================================================================
+// extern "C" entry points
+// ====================================================================================
+extern "C" {
+
+const char* gsb_last_error(void) { return g_err.c_str(); }
+int32_t gsb_version(void) { return 100; }
+int64_t gsb_launch_count(void) { return g_launches.load(); }
+
+gsb_status gsb_profile_enable(int32_t on) {
+    g_prof_on = on != 0;
+    return GSB_OK;
+}
+
+gsb_status gsb_profile_dump(char* buf, size_t buflen) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    GSB_CUDA(cudaDeviceSynchronize());
+    std::vector<std::string> names;
+    std::vector<int64_t> cnt;
+    std::vector<double> ms;
+    for (auto& r : g_prof) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        size_t k = 0;
+        for (; k < names.size(); ++k)
+            if (names[k] == r.name) break;
+        if (k == names.size()) {
+            names.push_back(r.name);
+            cnt.push_back(0);
+            ms.push_back(0.0);
+        }
+        cnt[k] += 1;
+        ms[k] += t;
+        g_event_pool.push_back(r.a);
+        g_event_pool.push_back(r.b);
+    }
+    g_prof.clear();
+    std::string out;
+    char line[256];
+    for (size_t k = 0; k < names.size(); ++k) {
+        snprintf(line, sizeof(line), "%s %lld %.6f\n", names[k].c_str(), (long long)cnt[k], ms[k]);
+        out += line;
+    }
+    if (buf && buflen) {
+        size_t n = out.size() < buflen - 1 ? out.size() : buflen - 1;
+        memcpy(buf, out.data(), n);
+        buf[n] = 0;
+    }
+    return GSB_OK;
+}
+
+gsb_status gsb_graph_create(int32_t T, const int64_t* counts, int32_t R, const int32_t* etype_src,
+                            const int32_t* etype_dst, gsb_graph_t* out) {
+    GSB_CHECK_ARG(out && counts && etype_src && etype_dst, "null argument");
+    GSB_CHECK_ARG(T >= 1 && T <= kMaxT, "num_ntypes %d out of [1, %d]", T, kMaxT);
+    GSB_CHECK_ARG(R >= 1 && R <= kMaxR, "num_etypes %d out of [1, %d]", R, kMaxR);
+    Graph* G = new Graph();
+    memset(&G->dev, 0, sizeof(GraphDev));
+    G->dev.T = T;
+    G->dev.R = R;
+    G->dev.node_off[0] = 0;
+    for (int t = 0; t < T; ++t) {
+        if (counts[t] < 0 || counts[t] > (int64_t)INT32_MAX) {
+            delete G;
+            set_error("ntype %d count %lld out of range", t, (long long)counts[t]);
+            return GSB_EINVAL;
+        }
+        G->counts[t] = counts[t];
+        G->dev.node_off[t + 1] = G->dev.node_off[t] + counts[t];
+    }
+    for (int t = T + 1; t <= kMaxT; ++t) G->dev.node_off[t] = G->dev.node_off[T];
+    G->total_nodes = G->dev.node_off[T];
+    int S = 0;
+    for (int r = 0; r < R; ++r) {
+        if (etype_src[r] < 0 || etype_src[r] >= T || etype_dst[r] < 0 || etype_dst[r] >= T) {
+            delete G;
+            set_error("etype %d endpoint type out of range", r);
+            return GSB_EINVAL;
+        }
+        G->dev.src_t[r] = etype_src[r];
+        G->dev.dst_t[r] = etype_dst[r];
+        int t = etype_dst[r];
+        if (G->dev.n_slots[t] >= kMaxS) {
+            delete G;
+            set_error("ntype %d has more than %d in-relations", t, kMaxS);
+            return GSB_EINVAL;
+        }
+        G->dev.slot_etype[t][G->dev.n_slots[t]++] = r;
+    }
+    for (int t = 0; t < T; ++t) S = S > G->dev.n_slots[t] ? S : G->dev.n_slots[t];
+    G->dev.S = S;
+    *out = reinterpret_cast<gsb_graph_t>(G);
+    return GSB_OK;
+}
+
+gsb_status gsb_graph_destroy(gsb_graph_t g) {
+    delete reinterpret_cast<Graph*>(g);
+    return GSB_OK;
+}
+
+gsb_status gsb_slot_etype(gsb_graph_t g, int32_t t, int32_t s, int32_t* etype) {
+    Graph* G = reinterpret_cast<Graph*>(g);
+    GSB_CHECK_ARG(G && etype && t >= 0 && t < G->dev.T, "bad argument");
+    *etype = (s >= 0 && s < G->dev.n_slots[t]) ? G->dev.slot_etype[t][s] : -1;
+    return GSB_OK;
+}
+
+static size_t csc_cub_bytes(int64_t n) {
+    size_t b = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, b, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)n, 0, 64);
+    return b;
+}
+
+gsb_status gsb_csc_build_bytes(gsb_graph_t g, int32_t etype, int64_t n_edges, size_t* bytes) {
+    Graph* G = reinterpret_cast<Graph*>(g);
+    GSB_CHECK_ARG(G && bytes && etype >= 0 && etype < G->dev.R && n_edges >= 0, "bad argument");
+    *bytes = align_up(sizeof(unsigned long long)) + 2 * align_up(sizeof(uint64_t) * (size_t)(n_edges + 1)) +
+             align_up(csc_cub_bytes(n_edges));
+    return GSB_OK;
+}
+
+gsb_status gsb_csc_build(gsb_graph_t g, int32_t etype, const int32_t* src, const int32_t* dst, const uint8_t* keep,
+                         int64_t n_edges, int64_t* indptr, int32_t* indices, int64_t* n_kept, void* ws,
+                         size_t ws_bytes, void* stream) {
+    Graph* G = reinterpret_cast<Graph*>(g);
+    GSB_CHECK_ARG(G && etype >= 0 && etype < G->dev.R, "bad graph/etype");
+    GSB_CHECK_ARG(n_edges == 0 || (src && dst), "null COO");
+    GSB_CHECK_ARG(indptr && indices && n_kept && ws, "null output/workspace");
+    size_t need = 0;
+    gsb_csc_build_bytes(g, etype, n_edges, &need);
+    if (ws_bytes < need) {
+        set_error("csc workspace %zu < %zu", ws_bytes, need);
+        return GSB_EWORKSPACE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    char* p = (char*)ws;
+    unsigned long long* d_cnt = (unsigned long long*)p;
+    p += align_up(sizeof(unsigned long long));
+    uint64_t* k_in = (uint64_t*)p;
+    p += align_up(sizeof(uint64_t) * (size_t)(n_edges + 1));
+    uint64_t* k_out = (uint64_t*)p;
+    p += align_up(sizeof(uint64_t) * (size_t)(n_edges + 1));
+    size_t cub_b = csc_cub_bytes(n_edges);
+    const int64_t n_dst = G->counts[G->dev.dst_t[etype]];
+    GSB_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s));
+    if (n_edges > 0) {
+        GSB_LAUNCH("csc_keys", csc_keys_kernel, grid_for(n_edges, 256, kNumSMs * 32), 256, 0, s, src, dst, keep,
+                   n_edges, k_in, d_cnt);
+        int end_bit = 32;
+        while (end_bit < 64 && ((int64_t)1 << (end_bit - 32)) <= n_dst) ++end_bit;
+        GSB_CUDA(cub::DeviceRadixSort::SortKeys(p, cub_b, k_in, k_out, (int64_t)n_edges, 0, end_bit, s));
+        count_launch(2 * ((end_bit + 7) / 8));
+    }
+    GSB_LAUNCH("csc_finish", csc_finish_kernel, grid_for(n_edges > n_dst ? n_edges : n_dst + 1, 256, kNumSMs * 32),
+               256, 0, s, k_out, d_cnt, n_dst, indptr, indices);
+    unsigned long long h = 0;
+    GSB_CUDA(cudaMemcpyAsync(&h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+    GSB_CUDA(cudaStreamSynchronize(s));
+    *n_kept = (int64_t)h;
+    G->dev.indptr[etype] = indptr;
+    G->dev.indices[etype] = indices;
+    G->dev.eid_base[etype] = 0;
+    G->n_edges[etype] = (int64_t)h;
+    return GSB_OK;
+}
+
+gsb_status gsb_graph_set_csc(gsb_graph_t g, int32_t etype, const int64_t* indptr, const int32_t* indices,
+                             int64_t n_edges, int64_t eid_base) {
+    Graph* G = reinterpret_cast<Graph*>(g);
+    GSB_CHECK_ARG(G && etype >= 0 && etype < G->dev.R && indptr && (indices || n_edges == 0), "bad argument");
+    G->dev.indptr[etype] = indptr;
+    G->dev.indices[etype] = indices;
+    G->dev.eid_base[etype] = eid_base;
+    G->n_edges[etype] = n_edges;
+    return GSB_OK;
+}
+
+gsb_status gsb_graph_set_features(gsb_graph_t g, int32_t ntype, const float* feat, int32_t dim) {
+    Graph* G = reinterpret_cast<Graph*>(g);
+    GSB_CHECK_ARG(G && ntype >= 0 && ntype < G->dev.T && feat, "bad argument");
+    GSB_CHECK_ARG(dim > 0 && dim % 4 == 0, "feature dim %d must be a positive multiple of 4", dim);
+    GSB_CHECK_ARG(G->dev.feat_dim == 0 || G->dev.feat_dim == dim, "all ntypes must share one feature dim");
+    GSB_CHECK_ARG(((uintptr_t)feat & 15) == 0, "feature table must be 16-byte aligned");
+    G->dev.feat_dim = dim;
+    G->dev.feat[ntype] = feat;
+    return GSB_OK;
+}
+
+gsb_status gsb_gather(gsb_graph_t g, const int64_t* gid, int64_t n, float* out, void* stream) {
+    Graph* G = reinterpret_cast<Graph*>(g);
+    GSB_CHECK_ARG(G && (n == 0 || (gid && out)), "bad argument");
+    GSB_CHECK_ARG(G->dev.feat_dim > 0, "features not registered");
+    for (int t = 0; t < G->dev.T; ++t) GSB_CHECK_ARG(G->dev.feat[t], "features of ntype %d not registered", t);
+    if (n == 0) return GSB_OK;
+    return launch_gather(G, gid, nullptr, n, n, out, (cudaStream_t)stream);
+}
+
+gsb_status gsb_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                         float eps, int32_t t, void* stream) {
+    GSB_CHECK_ARG(p && g && m && v && n >= 0 && t >= 1, "bad argument");
+    if (n == 0) return GSB_OK;
+    float c1 = 1.f - powf(b1, (float)t);
+    float c2 = 1.f - powf(b2, (float)t);
+    GSB_LAUNCH("adam", adam_kernel, grid_for(n, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream, p, g, m, v, n, lr,
+               b1, b2, eps, c1, c2);
+    return GSB_OK;
+}
+
+}  // extern "C"

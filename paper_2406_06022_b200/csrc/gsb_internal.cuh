@@ -1,0 +1,162 @@
+// gsb_internal.cuh -- shared internals of libgsb (CUDA path).  Independent of oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gsb.h"
+
+namespace gsb {
+
+constexpr int kMaxT = GSB_MAX_NTYPES;
+constexpr int kMaxR = GSB_MAX_ETYPES;
+constexpr int kMaxS = GSB_MAX_SLOTS;
+constexpr int kMaxL = GSB_MAX_LAYERS;
+constexpr int kNumSMs = 148;  // B200
+
+// ------------------------------------------------------------------------------------
+// errors / instrumentation
+// ------------------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+gsb_status cuda_status(cudaError_t e, const char* what);
+void prof_begin(const char* name, cudaStream_t s);
+void prof_end(cudaStream_t s);
+void count_launch(int n = 1);
+
+#define GSB_CHECK_ARG(cond, ...)           \
+    do {                                   \
+        if (!(cond)) {                     \
+            ::gsb::set_error(__VA_ARGS__); \
+            return GSB_EINVAL;             \
+        }                                  \
+    } while (0)
+
+#define GSB_CUDA(call)                                                \
+    do {                                                              \
+        cudaError_t _e = (call);                                      \
+        if (_e != cudaSuccess) return ::gsb::cuda_status(_e, #call); \
+    } while (0)
+
+// Launch with instrumentation: counts the launch, optionally brackets it with events.
+#define GSB_LAUNCH(name, kern, grid, block, smem, stream, ...)                 \
+    do {                                                                       \
+        ::gsb::prof_begin(name, stream);                                       \
+        kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);              \
+        ::gsb::prof_end(stream);                                               \
+        ::gsb::count_launch();                                                 \
+        cudaError_t _e = cudaGetLastError();                                   \
+        if (_e != cudaSuccess) return ::gsb::cuda_status(_e, name);            \
+    } while (0)
+
+// ------------------------------------------------------------------------------------
+// graph descriptor passed to kernels by value
+// ------------------------------------------------------------------------------------
+struct GraphDev {
+    int32_t T, R, S;                    // ntypes, etypes, max slots
+    int32_t feat_dim;
+    int64_t node_off[kMaxT + 1];
+    int32_t src_t[kMaxR], dst_t[kMaxR];
+    int32_t n_slots[kMaxT];             // in-relations of each ntype
+    int32_t slot_etype[kMaxT][kMaxS];   // etype of slot s of ntype t
+    const int64_t* indptr[kMaxR];
+    const int32_t* indices[kMaxR];
+    int64_t eid_base[kMaxR];
+    const float* feat[kMaxT];
+};
+
+__host__ __device__ inline int type_of(const GraphDev& g, int64_t gid) {
+    int t = 0;
+#pragma unroll 1
+    for (int k = 1; k < g.T; ++k) t += (gid >= g.node_off[k]) ? 1 : 0;
+    return t;
+}
+
+// Per-hop sizes, written by kernels (device resident; never copied to the host on the
+// hot path).  dst rows of ntype t are [dst_off[t], dst_off[t+1]); src rows likewise.
+struct HopMeta {
+    int64_t n_dst;
+    int64_t n_edges;
+    int64_t n_src;
+    int64_t dst_off[kMaxT + 1];
+    int64_t src_off[kMaxT + 1];
+    int64_t new_base[kMaxT];   // bitmap rank of node_off[t] (first new node of type t)
+};
+
+// Per-hop device buffers inside the arena.
+struct HopBufs {
+    int64_t cap_dst, cap_edges, cap_src;
+    HopMeta* meta;
+    int64_t* dst_gid;     // [cap_dst]   (hop 1: seed copy; else previous hop's src_gid)
+    int64_t* cnt;         // [cap_dst*S + 1]
+    int64_t* seg_ptr;     // [cap_dst*S + 1]
+    int64_t* e_src_gid;   // [cap_edges]
+    int64_t* e_eid;       // [cap_edges]
+    int32_t* e_src;       // [cap_edges]
+    int64_t* src_gid;     // [cap_src]
+};
+
+struct Graph {
+    GraphDev dev;
+    int64_t counts[kMaxT];
+    int64_t n_edges[kMaxR];
+    int64_t total_nodes;
+};
+
+struct Blocks {
+    Graph* g;
+    int32_t L;
+    int32_t fanout[kMaxL];     // f[l] for layer l
+    int64_t max_seeds, max_excl;
+    // arena layout (byte offsets)
+    size_t off_meta[kMaxL + 1];
+    size_t off_seed, off_cnt[kMaxL], off_seg[kMaxL], off_esrcgid[kMaxL], off_eeid[kMaxL], off_esrc[kMaxL];
+    size_t off_src[kMaxL];
+    size_t off_map, off_bitmap, off_wrank, off_err, off_cub, off_excl;
+    size_t cub_bytes, total_bytes;
+    int64_t cap_dst[kMaxL + 1], cap_edges[kMaxL];
+    int64_t n_words;
+    HopBufs hop(int h, void* arena) const;   // h = 1..L
+    int hop_of_layer(int layer) const { return L - layer; }
+};
+
+template <typename T>
+inline T* at(void* base, size_t off) {
+    return reinterpret_cast<T*>(static_cast<char*>(base) + off);
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+inline int grid_for(int64_t work, int per_block, int max_blocks = kNumSMs * 16) {
+    int64_t b = ceil_div(work, per_block);
+    if (b < 1) b = 1;
+    if (b > max_blocks) b = max_blocks;
+    return (int)b;
+}
+
+// ------------------------------------------------------------------------------------
+// device helpers
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ float4 ldg_nc_f4(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void red_add_f4(float* p, float4 v) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ void red_add_f1(float* p, float v) { atomicAdd(p, v); }
+
+}  // namespace gsb

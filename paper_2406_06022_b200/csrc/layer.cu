@@ -1,0 +1,260 @@
+// layer.cu -- RGCN layer forward / backward and the NC decoder + softmax-CE loss.
+// Contract: include/gsb.h "RGCN layer" and "Node-classification decoder".
+#include "gemm_simt.cuh"
+#include "gsb_internal.cuh"
+
+namespace gsb {
+
+// ------------------------------------------------------------------------------------
+// aggregation: warp per dst row j; lanes over feature columns (float4)
+//   Acat[j, s*d + :] = mean_{e in seg(j,s)} h_src[e_src[e], :]    (0 when empty)
+//   Acat[j, S_t*d + :] = h_src[self(j), :]
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) agg_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                  const int64_t* __restrict__ seg_ptr,
+                                                  const int32_t* __restrict__ e_src, const float* __restrict__ h,
+                                                  int d, float* __restrict__ acat, int64_t lda) {
+    const int lane = threadIdx.x & 31;
+    const int S = g.S;
+    const int64_t n = m->n_dst;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int d4 = d >> 2;
+    for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < n; j += warps) {
+        int t = 0;
+        for (int k = 1; k < g.T; ++k) t += (j >= m->dst_off[k]) ? 1 : 0;
+        const int St = g.n_slots[t];
+        float* out = acat + j * lda;
+        for (int s = 0; s < St; ++s) {
+            const int64_t e0 = seg_ptr[j * S + s], e1 = seg_ptr[j * S + s + 1];
+            const float inv = (e1 > e0) ? 1.f / (float)(e1 - e0) : 0.f;
+            for (int c = lane; c < d4; c += 32) {
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                int64_t e = e0;
+                for (; e + 4 <= e1; e += 4) {
+                    int32_t u0 = e_src[e], u1 = e_src[e + 1], u2 = e_src[e + 2], u3 = e_src[e + 3];
+                    float4 x0 = __ldg(reinterpret_cast<const float4*>(h + (int64_t)u0 * d) + c);
+                    float4 x1 = __ldg(reinterpret_cast<const float4*>(h + (int64_t)u1 * d) + c);
+                    float4 x2 = __ldg(reinterpret_cast<const float4*>(h + (int64_t)u2 * d) + c);
+                    float4 x3 = __ldg(reinterpret_cast<const float4*>(h + (int64_t)u3 * d) + c);
+                    acc.x += x0.x; acc.y += x0.y; acc.z += x0.z; acc.w += x0.w;
+                    acc.x += x1.x; acc.y += x1.y; acc.z += x1.z; acc.w += x1.w;
+                    acc.x += x2.x; acc.y += x2.y; acc.z += x2.z; acc.w += x2.w;
+                    acc.x += x3.x; acc.y += x3.y; acc.z += x3.z; acc.w += x3.w;
+                }
+                for (; e < e1; ++e) {
+                    float4 x = __ldg(reinterpret_cast<const float4*>(h + (int64_t)e_src[e] * d) + c);
+                    acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+                }
+                acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+                reinterpret_cast<float4*>(out + (int64_t)s * d)[c] = acc;
+            }
+        }
+        const int64_t self = m->src_off[t] + (j - m->dst_off[t]);
+        for (int c = lane; c < d4; c += 32)
+            reinterpret_cast<float4*>(out + (int64_t)St * d)[c] =
+                __ldg(reinterpret_cast<const float4*>(h + self * d) + c);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// backward scatter: dh_src[u] += dA[j, s] / c_s(j) per sampled edge; dh_src[self] += dA[j, S_t]
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) scatter_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                      const int64_t* __restrict__ seg_ptr,
+                                                      const int32_t* __restrict__ e_src, const float* __restrict__ dA,
+                                                      int64_t lda, int d, float* __restrict__ dh) {
+    const int lane = threadIdx.x & 31;
+    const int S = g.S;
+    const int64_t n = m->n_dst;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int d4 = d >> 2;
+    for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < n; j += warps) {
+        int t = 0;
+        for (int k = 1; k < g.T; ++k) t += (j >= m->dst_off[k]) ? 1 : 0;
+        const int St = g.n_slots[t];
+        const float* row = dA + j * lda;
+        for (int s = 0; s < St; ++s) {
+            const int64_t e0 = seg_ptr[j * S + s], e1 = seg_ptr[j * S + s + 1];
+            if (e1 == e0) continue;
+            const float inv = 1.f / (float)(e1 - e0);
+            for (int c = lane; c < d4; c += 32) {
+                float4 v = reinterpret_cast<const float4*>(row + (int64_t)s * d)[c];
+                v.x *= inv; v.y *= inv; v.z *= inv; v.w *= inv;
+                for (int64_t e = e0; e < e1; ++e) red_add_f4(dh + (int64_t)e_src[e] * d + 4 * c, v);
+            }
+        }
+        const int64_t self = m->src_off[t] + (j - m->dst_off[t]);
+        for (int c = lane; c < d4; c += 32)
+            red_add_f4(dh + self * d + 4 * c, reinterpret_cast<const float4*>(row + (int64_t)St * d)[c]);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// softmax cross-entropy, warp per row; logits are overwritten by dlogits
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int64_t n, int C,
+                                                 const int32_t* __restrict__ labels,
+                                                 const int64_t* __restrict__ seed_gid, int64_t base,
+                                                 float* __restrict__ row_loss) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const float invn = 1.f / (float)n;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+        float* lg = logits + i * C;
+        const int y = labels[seed_gid[i] - base];
+        float mx = -INFINITY;
+        for (int c = lane; c < C; c += 32) mx = fmaxf(mx, lg[c]);
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float se = 0.f;
+        for (int c = lane; c < C; c += 32) se += expf(lg[c] - mx);
+        for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        const float lse = mx + logf(se);
+        if (lane == 0) row_loss[i] = lse - lg[y];
+        __syncwarp();
+        for (int c = lane; c < C; c += 32) lg[c] = (expf(lg[c] - lse) - (c == y ? 1.f : 0.f)) * invn;
+    }
+}
+
+__global__ void __launch_bounds__(1024) mean_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
+    __shared__ float sm[32];
+    float s = 0.f;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = (threadIdx.x < (blockDim.x >> 5)) ? sm[threadIdx.x] : 0.f;
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) *out = s / (float)n;
+    }
+}
+
+static RowGroups layer_groups(const Blocks* B, const void* arena, int layer) {
+    RowGroups rg;
+    memset(&rg, 0, sizeof(rg));
+    const GraphDev& g = B->g->dev;
+    rg.meta = at<HopMeta>(const_cast<void*>(arena), B->off_meta[B->hop_of_layer(layer)]);
+    rg.G = g.T;
+    for (int t = 0; t < g.T; ++t) {
+        rg.ks[t] = g.n_slots[t] + 1;
+        for (int s = 0; s < g.n_slots[t]; ++s) rg.slot_w[t][s] = g.slot_etype[t][s];
+        rg.slot_w[t][g.n_slots[t]] = g.R;  // W_self
+    }
+    return rg;
+}
+
+static RowGroups single_group(int64_t M) {
+    RowGroups rg;
+    memset(&rg, 0, sizeof(rg));
+    rg.meta = nullptr;
+    rg.M = M;
+    rg.G = 1;
+    rg.ks[0] = 1;
+    rg.slot_w[0][0] = 0;
+    return rg;
+}
+
+static int gemm_grid(int64_t rows_cap, int ncols_tiles, int groups) {
+    int64_t tiles = (ceil_div(rows_cap, BM) + groups) * ncols_tiles;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs * 4));
+}
+
+}  // namespace gsb
+
+using namespace gsb;
+
+extern "C" {
+
+gsb_status gsb_layer_acat_floats(gsb_blocks_t b, int32_t layer, int32_t d_in, int64_t* n_floats) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && n_floats && layer >= 0 && layer < B->L && d_in > 0, "bad argument");
+    *n_floats = B->cap_dst[B->hop_of_layer(layer)] * (int64_t)(B->g->dev.S + 1) * d_in;
+    return GSB_OK;
+}
+
+gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src, int32_t d_in,
+                              const float* W, const float* bias, int32_t d_out, int32_t relu, float* h_dst,
+                              float* acat, void* stream) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && arena && h_src && W && h_dst && acat, "null argument");
+    GSB_CHECK_ARG(layer >= 0 && layer < B->L, "layer %d out of range", layer);
+    GSB_CHECK_ARG(d_in > 0 && d_in % BK == 0, "d_in %d must be a multiple of %d", d_in, BK);
+    GSB_CHECK_ARG(d_out > 0 && d_out % 4 == 0, "d_out %d must be a multiple of 4", d_out);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int h = B->hop_of_layer(layer);
+    HopBufs hb = B->hop(h, const_cast<void*>(arena));
+    const GraphDev& g = B->g->dev;
+    const int64_t lda = (int64_t)(g.S + 1) * d_in;
+    GSB_LAUNCH("rgcn_agg", agg_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g, hb.meta, hb.seg_ptr,
+               hb.e_src, h_src, d_in, acat, lda);
+    RowGroups rg = layer_groups(B, arena, layer);
+    GSB_LAUNCH("rgcn_gemm_fwd", gemm_nn_kernel, gemm_grid(hb.cap_dst, (d_out + BN - 1) / BN, g.T), NT, 0, s, rg,
+               acat, lda, W, d_in, d_out, (int64_t)d_out, (int64_t)d_in * d_out, bias, relu, h_dst, (int64_t)d_out);
+    return GSB_OK;
+}
+
+gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_dst,
+                              const float* dh_dst, const float* W, const float* acat, int32_t d_in, int32_t d_out,
+                              int32_t relu, float* dW, float* db, float* dh_src, float* dacat_ws, void* stream) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && arena && dh_dst && W && acat && dW && db, "null argument");
+    GSB_CHECK_ARG(!relu || h_dst, "relu backward needs h_dst");
+    GSB_CHECK_ARG(!dh_src || dacat_ws, "dh_src needs dacat_ws");
+    GSB_CHECK_ARG(layer >= 0 && layer < B->L, "layer %d out of range", layer);
+    GSB_CHECK_ARG(d_in > 0 && d_in % BK == 0 && d_out > 0 && d_out % 4 == 0, "bad dims");
+    cudaStream_t s = (cudaStream_t)stream;
+    const GraphDev& g = B->g->dev;
+    const int h = B->hop_of_layer(layer);
+    HopBufs hb = B->hop(h, const_cast<void*>(arena));
+    const int64_t lda = (int64_t)(g.S + 1) * d_in;
+    RowGroups rg = layer_groups(B, arena, layer);
+    GSB_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)(g.R + 1) * d_in * d_out, s));
+    GSB_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)d_out, s));
+    const int rpc = 256;
+    {
+        int64_t items = (ceil_div(hb.cap_dst, rpc) + g.T) * (g.S + 1) * ceil_div(d_in, BM) * ceil_div(d_out, BN);
+        int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, kNumSMs * 4));
+        GSB_LAUNCH("rgcn_gemm_dW", gemm_tn_kernel, grid, NT, 0, s, rg, acat, lda, dh_dst, h_dst, relu,
+                   (int64_t)d_out, d_in, d_out, rpc, dW, (int64_t)d_out, (int64_t)d_in * d_out, db);
+    }
+    if (dh_src) {
+        GSB_LAUNCH("rgcn_gemm_dA", gemm_nt_kernel, gemm_grid(hb.cap_dst, (int)ceil_div(d_in, BN) * (g.S + 1), g.T),
+                   NT, 0, s, rg, dh_dst, h_dst, relu, (int64_t)d_out, W, d_in, d_out, (int64_t)d_out,
+                   (int64_t)d_in * d_out, dacat_ws, lda);
+        GSB_CUDA(cudaMemsetAsync(dh_src, 0, sizeof(float) * (size_t)hb.cap_src * d_in, s));
+        GSB_LAUNCH("rgcn_scatter", scatter_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
+                   hb.meta, hb.seg_ptr, hb.e_src, dacat_ws, lda, d_in, dh_src);
+    }
+    return GSB_OK;
+}
+
+gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, const float* bc, int32_t C,
+                       const int32_t* labels, const int64_t* seed_gid, int64_t label_gid_base, float* logits_ws,
+                       float* row_loss_ws, float* loss, float* dh, float* dWc, float* dbc, void* stream) {
+    GSB_CHECK_ARG(h && Wc && bc && labels && seed_gid && logits_ws && row_loss_ws && loss, "null argument");
+    GSB_CHECK_ARG(n >= 1 && d > 0 && d % BK == 0 && C >= 1, "bad dims (d %% %d == 0 required)", BK);
+    cudaStream_t s = (cudaStream_t)stream;
+    RowGroups rg = single_group(n);
+    GSB_LAUNCH("nc_logits", gemm_nn_kernel, gemm_grid(n, (C + BN - 1) / BN, 1), NT, 0, s, rg, h, (int64_t)d, Wc, d,
+               C, (int64_t)C, (int64_t)0, bc, 0, logits_ws, (int64_t)C);
+    GSB_LAUNCH("nc_ce", ce_kernel, grid_for(n * 32, 256, kNumSMs * 4), 256, 0, s, logits_ws, n, C, labels, seed_gid,
+               label_gid_base, row_loss_ws);
+    GSB_LAUNCH("nc_mean", mean_kernel, 1, 1024, 0, s, row_loss_ws, n, loss);
+    if (dWc || dbc) {
+        GSB_CHECK_ARG(dWc && dbc, "dWc and dbc go together");
+        GSB_CUDA(cudaMemsetAsync(dWc, 0, sizeof(float) * (size_t)d * C, s));
+        GSB_CUDA(cudaMemsetAsync(dbc, 0, sizeof(float) * (size_t)C, s));
+        const int rpc = 128;
+        int64_t items = ceil_div(n, rpc) * ceil_div(d, BM) * ceil_div(C, BN);
+        GSB_LAUNCH("nc_gemm_dWc", gemm_tn_kernel, (int)std::min<int64_t>(items, kNumSMs * 4), NT, 0, s, rg, h,
+                   (int64_t)d, logits_ws, (const float*)nullptr, 0, (int64_t)C, d, C, rpc, dWc, (int64_t)C,
+                   (int64_t)0, dbc);
+    }
+    if (dh) {
+        GSB_LAUNCH("nc_gemm_dh", gemm_nt_kernel, gemm_grid(n, (int)ceil_div(d, BN), 1), NT, 0, s, rg, logits_ws,
+                   (const float*)nullptr, 0, (int64_t)C, Wc, d, C, (int64_t)C, (int64_t)0, dh, (int64_t)d);
+    }
+    return GSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,669 @@
+// sample.cu -- per-etype fanout sampling into message-flow blocks + relabel, all sizes
+// device-resident (no host sync), sm_100a.  Contract: include/gsb.h "Mini-batch sampling".
+//
+// Per hop h (frontier D_h, type-grouped):
+//   count   : thread per (dst j, slot s) -> c = min(f, deg'), marks map[gid(j)] = j
+//   scan    : seg_ptr = exclusive_scan(c)                     (CUB, decoupled look-back)
+//   fill    : warp per segment; Philox draws on lanes, Floyd resolved with shfl/ballot,
+//             bitonic sort of the chosen ranks, coalesced writes; marks new sources in a
+//             bitmap over the global id space
+//   rank    : popcount prefix over the bitmap                 (CUB)
+//   meta    : per-type counts of new sources -> src row offsets (device HopMeta)
+//   relabel : edge src gid -> src row (dst prefix via map, new via bitmap rank)
+//   next    : writes D_{h+1} (dst prefix ++ ascending new) and clears map/bitmap
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "gsb_internal.cuh"
+
+namespace gsb {
+
+gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_dev, int64_t n_host, int64_t n_max,
+                         float* out, cudaStream_t s);
+
+enum { ERR_NONE = 0, ERR_GROUPING = 1, ERR_RANGE = 2, ERR_CAPACITY = 3, ERR_DUPLICATE = 4 };
+
+// ------------------------------------------------------------------------------------
+// Philox4x32-10 (counter-based; R-rng)
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k.x += 0x9E3779B9u;
+            k.y += 0xBB67AE85u;
+        }
+        uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    }
+    return c;
+}
+
+__device__ __forceinline__ uint64_t keyed_u64(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+    uint4 o = philox10(make_uint4(c0, c1, c2, c3), make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+    return ((uint64_t)o.y << 32) | o.x;
+}
+
+// ------------------------------------------------------------------------------------
+// LP exclusion set: sorted keys (flag << 62 | dst_gid << 31 | src_gid); flag 0 applies
+// to segments of excl_etype, flag 1 to excl_rev_etype (R-excl).  Gids < 2^31.
+// ------------------------------------------------------------------------------------
+struct Excl {
+    const uint64_t* keys;
+    int64_t n;
+    int32_t etype, rev;
+};
+
+__global__ void excl_keys_kernel(const int64_t* __restrict__ u, const int64_t* __restrict__ v, int64_t n, int rev,
+                                 uint64_t* __restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = ((uint64_t)v[i] << 31) | (uint64_t)u[i];
+        keys[n + i] = rev ? ((1ull << 62) | ((uint64_t)u[i] << 31) | (uint64_t)v[i]) : ~0ull;
+    }
+}
+
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n, uint64_t key) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t m = (lo + hi) >> 1;
+        if (a[m] < key) lo = m + 1; else hi = m;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t* a, int64_t n, int32_t key) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t m = (lo + hi) >> 1;
+        if (a[m] < key) lo = m + 1; else hi = m;
+    }
+    return lo;
+}
+
+// Range [k0, k1) of exclusion keys for segment (v, r); empty when r is not excluded.
+__device__ __forceinline__ void excl_range(const Excl& x, int r, int64_t v, int64_t& k0, int64_t& k1) {
+    k0 = k1 = 0;
+    if (x.n == 0 || (r != x.etype && r != x.rev)) return;
+    uint64_t flag = (r == x.etype) ? 0ull : (1ull << 62);
+    uint64_t base = flag | ((uint64_t)v << 31);
+    k0 = lower_bound_u64(x.keys, x.n, base);
+    k1 = lower_bound_u64(x.keys, x.n, base + (1ull << 31));
+}
+
+// Iterate distinct excluded sources in ascending order, yielding their position ranges
+// [lo, hi) inside the segment (indices sorted by src).  Returns the total excluded.
+__device__ __forceinline__ int64_t excl_count(const Excl& x, int64_t k0, int64_t k1, const int32_t* seg, int64_t deg,
+                                              int64_t src_off) {
+    int64_t tot = 0;
+    uint64_t prev = ~0ull;
+    for (int64_t k = k0; k < k1; ++k) {
+        uint64_t key = x.keys[k];
+        if (key == prev) continue;
+        prev = key;
+        int32_t ul = (int32_t)((int64_t)(key & 0x7FFFFFFFull) - src_off);
+        int64_t lo = lower_bound_i32(seg, deg, ul);
+        int64_t hi = lower_bound_i32(seg, deg, ul + 1);
+        tot += hi - lo;
+    }
+    return tot;
+}
+
+// Map rank q among non-excluded positions to a segment position.
+__device__ __forceinline__ int64_t excl_map(const Excl& x, int64_t k0, int64_t k1, const int32_t* seg, int64_t deg,
+                                            int64_t src_off, int64_t q) {
+    int64_t p = q;
+    uint64_t prev = ~0ull;
+    for (int64_t k = k0; k < k1; ++k) {
+        uint64_t key = x.keys[k];
+        if (key == prev) continue;
+        prev = key;
+        int32_t ul = (int32_t)((int64_t)(key & 0x7FFFFFFFull) - src_off);
+        int64_t lo = lower_bound_i32(seg, deg, ul);
+        int64_t hi = lower_bound_i32(seg, deg, ul + 1);
+        if (p >= lo) p += hi - lo;
+    }
+    return p;
+}
+
+// ------------------------------------------------------------------------------------
+// hop-1 setup: copy seeds into the arena, per-type offsets, grouping / range checks
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) seed_meta_kernel(GraphDev g, const int64_t* __restrict__ seeds, int64_t n,
+                                                         int64_t* __restrict__ d1, HopMeta* __restrict__ m,
+                                                         int* __restrict__ err) {
+    __shared__ unsigned long long cnt[kMaxT];
+    if (threadIdx.x < kMaxT) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t N = g.node_off[g.T];
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        int64_t v = seeds[i];
+        d1[i] = v;
+        if (v < 0 || v >= N) {
+            atomicExch(err, ERR_RANGE);
+            continue;
+        }
+        int t = type_of(g, v);
+        atomicAdd(&cnt[t], 1ull);
+        if (i > 0) {
+            int64_t p = seeds[i - 1];
+            if (p >= 0 && p < N && type_of(g, p) > t) atomicExch(err, ERR_GROUPING);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const bool bad = *(volatile int*)err != 0;   // latched above: sample nothing
+        m->n_dst = bad ? 0 : n;
+        m->dst_off[0] = 0;
+        for (int t = 0; t < kMaxT; ++t)
+            m->dst_off[t + 1] = m->dst_off[t] + ((!bad && t < g.T) ? (int64_t)cnt[t] : 0);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// count: thread per (dst j, slot s)
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) count_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                    const int64_t* __restrict__ dst_gid, int64_t cap_dst, int fanout,
+                                                    Excl ex, int32_t* __restrict__ map, int64_t* __restrict__ cnt,
+                                                    int* __restrict__ err) {
+    const int S = g.S;
+    const int64_t n = (*(volatile int*)err) ? 0 : m->n_dst;
+    const int64_t total = cap_dst * S;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= total; i += stride) {
+        if (i == total) {
+            cnt[i] = 0;
+            continue;
+        }
+        int64_t j = i / S;
+        int s = (int)(i - j * S);
+        int64_t c = 0;
+        if (j < n) {
+            int64_t v = dst_gid[j];
+            int t = type_of(g, v);
+            if (s == 0) {
+                int32_t old = atomicExch(map + v, (int32_t)j);
+                if (old != -1) atomicExch(err, ERR_DUPLICATE);
+            }
+            if (s < g.n_slots[t]) {
+                int r = g.slot_etype[t][s];
+                int64_t vl = v - g.node_off[t];
+                const int64_t a = g.indptr[r][vl];
+                int64_t deg = g.indptr[r][vl + 1] - a;
+                int64_t k0, k1;
+                excl_range(ex, r, v, k0, k1);
+                if (k1 > k0) deg -= excl_count(ex, k0, k1, g.indices[r] + a, deg, g.node_off[g.src_t[r]]);
+                c = (fanout < 0 || deg <= fanout) ? deg : fanout;
+            }
+        }
+        cnt[i] = c;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// fill: warp per segment
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                   const int64_t* __restrict__ dst_gid, int64_t cap_dst,
+                                                   const int64_t* __restrict__ seg_ptr, int fanout, Excl ex,
+                                                   uint64_t seed, uint32_t step, int hop,
+                                                   const int32_t* __restrict__ map, uint32_t* __restrict__ bitmap,
+                                                   int64_t* __restrict__ e_src_gid, int64_t* __restrict__ e_eid,
+                                                   const int* __restrict__ err) {
+    const int S = g.S;
+    const int lane = threadIdx.x & 31;
+    const int64_t n = (*(volatile const int*)err) ? 0 : m->n_dst;
+    const int64_t nseg = n * S;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < nseg; i += warps) {
+        const int64_t base = seg_ptr[i];
+        const int64_t c = seg_ptr[i + 1] - base;
+        if (c == 0) continue;
+        const int64_t j = i / S;
+        const int s = (int)(i - j * S);
+        const int64_t v = dst_gid[j];
+        const int t = type_of(g, v);
+        const int r = g.slot_etype[t][s];
+        const int64_t vl = v - g.node_off[t];
+        const int64_t a = g.indptr[r][vl];
+        const int64_t deg = g.indptr[r][vl + 1] - a;
+        const int32_t* seg = g.indices[r] + a;
+        const int64_t src_off = g.node_off[g.src_t[r]];
+        int64_t k0, k1;
+        excl_range(ex, r, v, k0, k1);
+        const bool has_ex = k1 > k0;
+        const int64_t degp = has_ex ? deg - excl_count(ex, k0, k1, seg, deg, src_off) : deg;
+        if (c == degp) {
+            // every non-excluded in-edge, ascending
+            for (int64_t q = lane; q < c; q += 32) {
+                int64_t p = has_ex ? excl_map(ex, k0, k1, seg, deg, src_off, q) : q;
+                int64_t u = src_off + seg[p];
+                e_src_gid[base + q] = u;
+                e_eid[base + q] = g.eid_base[r] + a + p;
+                if (map[u] < 0) {
+                    uint32_t bit = 1u << (u & 31);
+                    if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);
+                }
+            }
+            continue;
+        }
+        // Floyd (R-floyd): draw i (lane i) is unif(j_i + 1), j_i = deg' - c + i
+        const int cc = (int)c;  // c <= fanout <= 32
+        const int32_t jj = (int32_t)(degp - cc + lane);
+        int32_t tdraw = 0;
+        if (lane < cc) {
+            uint32_t c2 = ((uint32_t)(r & 0xFFF) << 20) | ((uint32_t)(hop & 0xF) << 16) | (uint32_t)lane;
+            uint64_t x = keyed_u64(seed, (uint32_t)(uint64_t)v, (uint32_t)((uint64_t)v >> 32), c2, step);
+            tdraw = (int32_t)__umul64hi(x, (uint64_t)(jj + 1));
+        }
+        int32_t sel = INT32_MAX;
+        for (int k = 0; k < cc; ++k) {
+            int32_t tk = __shfl_sync(0xffffffffu, tdraw, k);
+            unsigned hit = __ballot_sync(0xffffffffu, lane < k && sel == tk);
+            if (lane == k) sel = hit ? jj : tk;
+        }
+        // bitonic sort of sel across the warp (ascending; unused lanes hold INT32_MAX)
+#pragma unroll
+        for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+            for (int jb = kk >> 1; jb > 0; jb >>= 1) {
+                int32_t o = __shfl_xor_sync(0xffffffffu, sel, jb);
+                bool up = (lane & kk) == 0;
+                bool lower = (lane & jb) == 0;
+                sel = (lower == up) ? min(sel, o) : max(sel, o);
+            }
+        }
+        if (lane < cc) {
+            int64_t p = has_ex ? excl_map(ex, k0, k1, seg, deg, src_off, sel) : sel;
+            int64_t u = src_off + seg[p];
+            e_src_gid[base + lane] = u;
+            e_eid[base + lane] = g.eid_base[r] + a + p;
+            if (map[u] < 0) {
+                uint32_t bit = 1u << (u & 31);
+                if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// rank / meta / relabel / next frontier
+// ------------------------------------------------------------------------------------
+__global__ void popc_kernel(const uint32_t* __restrict__ bitmap, int64_t n_words, int32_t* __restrict__ wrank) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= n_words; w += (int64_t)gridDim.x * blockDim.x)
+        wrank[w] = (w < n_words) ? __popc(bitmap[w]) : 0;
+}
+
+__device__ __forceinline__ int64_t bit_rank(const uint32_t* bitmap, const int32_t* wrank, int64_t x) {
+    int64_t w = x >> 5;
+    int b = (int)(x & 31);
+    int64_t r = wrank[w];
+    if (b) r += __popc(bitmap[w] & ((1u << b) - 1u));
+    return r;
+}
+
+__global__ void hop_meta_kernel(GraphDev g, HopMeta* __restrict__ m, HopMeta* __restrict__ next,
+                                const int64_t* __restrict__ seg_ptr, int64_t nseg_cap, const uint32_t* __restrict__ bitmap,
+                                const int32_t* __restrict__ wrank, int64_t cap_src, int* __restrict__ err) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (*(volatile int*)err) {   // latched: empty block and frontier (kernels downstream see 0 rows)
+        m->n_edges = 0;
+        m->n_src = 0;
+        for (int t = 0; t <= kMaxT; ++t) m->src_off[t] = 0;
+        if (next) {
+            next->n_dst = 0;
+            for (int t = 0; t <= kMaxT; ++t) next->dst_off[t] = 0;
+        }
+        return;
+    }
+    m->n_edges = seg_ptr[nseg_cap];
+    m->src_off[0] = 0;
+    for (int t = 0; t < kMaxT; ++t) {
+        int64_t nd = m->dst_off[t + 1] - m->dst_off[t];
+        int64_t nn = 0;
+        if (t < g.T) {
+            int64_t lo = bit_rank(bitmap, wrank, g.node_off[t]);
+            int64_t hi = bit_rank(bitmap, wrank, g.node_off[t + 1]);
+            m->new_base[t] = lo;
+            nn = hi - lo;
+        }
+        m->src_off[t + 1] = m->src_off[t] + nd + nn;
+    }
+    m->n_src = m->src_off[kMaxT];
+    if (m->n_src > cap_src) {
+        atomicExch(err, ERR_CAPACITY);
+        m->n_src = cap_src;
+    }
+    if (next) {
+        next->n_dst = m->n_src;
+        for (int t = 0; t <= kMaxT; ++t) next->dst_off[t] = m->src_off[t];
+    }
+}
+
+__global__ void __launch_bounds__(256) relabel_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                      const int64_t* __restrict__ e_src_gid,
+                                                      const int32_t* __restrict__ map,
+                                                      const uint32_t* __restrict__ bitmap,
+                                                      const int32_t* __restrict__ wrank, int32_t* __restrict__ e_src) {
+    const int64_t E = m->n_edges;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t u = e_src_gid[e];
+        int t = type_of(g, u);
+        int32_t mj = map[u];
+        int64_t row;
+        if (mj >= 0)
+            row = m->src_off[t] + (mj - m->dst_off[t]);
+        else
+            row = m->src_off[t] + (m->dst_off[t + 1] - m->dst_off[t]) + (bit_rank(bitmap, wrank, u) - m->new_base[t]);
+        e_src[e] = (int32_t)row;
+    }
+}
+
+__global__ void __launch_bounds__(256) next_frontier_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                            const int64_t* __restrict__ dst_gid,
+                                                            int32_t* __restrict__ map, uint32_t* __restrict__ bitmap,
+                                                            const int32_t* __restrict__ wrank, int64_t n_words,
+                                                            int64_t cap_src, int64_t* __restrict__ src_gid) {
+    const int64_t n = m->n_dst;
+    const int64_t work = n > n_words ? n : n_words;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < work; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n) {
+            int64_t v = dst_gid[i];
+            int t = type_of(g, v);
+            int64_t row = m->src_off[t] + (i - m->dst_off[t]);
+            if (row < cap_src) src_gid[row] = v;
+            map[v] = -1;
+        }
+        if (i < n_words) {
+            uint32_t bits = bitmap[i];
+            if (bits) {
+                int64_t k = wrank[i];
+                while (bits) {
+                    int b = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    int64_t u = i * 32 + b;
+                    int t = type_of(g, u);
+                    int64_t row = m->src_off[t] + (m->dst_off[t + 1] - m->dst_off[t]) + (k - m->new_base[t]);
+                    if (row < cap_src) src_gid[row] = u;
+                    ++k;
+                }
+                bitmap[i] = 0;
+            }
+        }
+    }
+}
+
+__global__ void init_arena_kernel(int32_t* __restrict__ map, int64_t n, uint32_t* __restrict__ bitmap, int64_t n_words,
+                                  int* __restrict__ err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n || i < n_words;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n) map[i] = -1;
+        if (i < n_words) bitmap[i] = 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *err = 0;
+}
+
+HopBufs Blocks::hop(int h, void* arena) const {
+    HopBufs b;
+    b.cap_dst = cap_dst[h];
+    b.cap_edges = cap_edges[h];
+    b.cap_src = cap_dst[h + 1];
+    b.meta = at<HopMeta>(arena, off_meta[h]);
+    b.dst_gid = (h == 1) ? at<int64_t>(arena, off_seed) : at<int64_t>(arena, off_src[h - 1]);
+    b.cnt = at<int64_t>(arena, off_cnt[h]);
+    b.seg_ptr = at<int64_t>(arena, off_seg[h]);
+    b.e_src_gid = at<int64_t>(arena, off_esrcgid[h]);
+    b.e_eid = at<int64_t>(arena, off_eeid[h]);
+    b.e_src = at<int32_t>(arena, off_esrc[h]);
+    b.src_gid = at<int64_t>(arena, off_src[h]);
+    return b;
+}
+
+}  // namespace gsb
+
+using namespace gsb;
+
+extern "C" {
+
+gsb_status gsb_blocks_create(gsb_graph_t gh, int32_t L, const int32_t* fanouts, int64_t max_seeds, int64_t max_excl,
+                             gsb_blocks_t* out) {
+    Graph* G = reinterpret_cast<Graph*>(gh);
+    GSB_CHECK_ARG(G && fanouts && out, "null argument");
+    GSB_CHECK_ARG(L >= 1 && L <= kMaxL, "num_layers %d out of [1, %d]", L, kMaxL);
+    GSB_CHECK_ARG(max_seeds >= 1 && max_excl >= 0, "bad capacities");
+    GSB_CHECK_ARG(G->total_nodes < ((int64_t)1 << 31), "total node count must be < 2^31");
+    for (int l = 0; l < L; ++l)
+        GSB_CHECK_ARG(fanouts[l] == -1 || (fanouts[l] >= 1 && fanouts[l] <= GSB_MAX_FANOUT),
+                      "fanout %d must be -1 or in [1, %d]", fanouts[l], GSB_MAX_FANOUT);
+    for (int r = 0; r < G->dev.R; ++r)
+        GSB_CHECK_ARG(G->dev.indptr[r] != nullptr, "CSC of etype %d not registered", r);
+    Blocks* B = new Blocks();
+    memset(B, 0, sizeof(Blocks));
+    B->g = G;
+    B->L = L;
+    for (int l = 0; l < L; ++l) B->fanout[l] = fanouts[l];
+    B->max_seeds = max_seeds;
+    B->max_excl = max_excl;
+    const int S = G->dev.S > 0 ? G->dev.S : 1;
+    int64_t total_edges = 0;
+    for (int r = 0; r < G->dev.R; ++r) total_edges += G->n_edges[r];
+    B->cap_dst[1] = max_seeds;
+    for (int h = 1; h <= L; ++h) {
+        int f = fanouts[L - h];
+        int64_t e = (f < 0) ? total_edges : std::min<int64_t>(B->cap_dst[h] * (int64_t)f * S, total_edges);
+        B->cap_edges[h] = std::max<int64_t>(e, 1);
+        B->cap_dst[h + 1] = std::min<int64_t>(B->cap_dst[h] + B->cap_edges[h], G->total_nodes);
+    }
+    B->n_words = ceil_div(G->total_nodes, 32);
+    // cub temp: max over scans
+    size_t cb = 0, t = 0;
+    int64_t maxseg = 0;
+    for (int h = 1; h <= L; ++h) maxseg = std::max<int64_t>(maxseg, B->cap_dst[h] * S + 1);
+    cub::DeviceScan::ExclusiveSum(nullptr, t, (int64_t*)nullptr, (int64_t*)nullptr, (int64_t)maxseg);
+    cb = std::max(cb, t);
+    cub::DeviceScan::ExclusiveSum(nullptr, t, (int32_t*)nullptr, (int32_t*)nullptr, (int64_t)(B->n_words + 1));
+    cb = std::max(cb, t);
+    if (max_excl > 0) {
+        cub::DeviceRadixSort::SortKeys(nullptr, t, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)(2 * max_excl), 0, 64);
+        cb = std::max(cb, t);
+    }
+    B->cub_bytes = cb;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += align_up(bytes > 0 ? bytes : 1);
+        return o;
+    };
+    B->off_err = take(sizeof(int) * 4);
+    for (int h = 1; h <= L + 1; ++h) B->off_meta[h <= kMaxL ? h : kMaxL] = 0;
+    for (int h = 1; h <= L; ++h) B->off_meta[h] = take(sizeof(HopMeta));
+    B->off_seed = take(sizeof(int64_t) * max_seeds);
+    for (int h = 1; h <= L; ++h) {
+        int64_t nseg = B->cap_dst[h] * S + 1;
+        B->off_cnt[h] = take(sizeof(int64_t) * nseg);
+        B->off_seg[h] = take(sizeof(int64_t) * nseg);
+        B->off_esrcgid[h] = take(sizeof(int64_t) * B->cap_edges[h]);
+        B->off_eeid[h] = take(sizeof(int64_t) * B->cap_edges[h]);
+        B->off_esrc[h] = take(sizeof(int32_t) * B->cap_edges[h]);
+        B->off_src[h] = take(sizeof(int64_t) * B->cap_dst[h + 1]);
+    }
+    B->off_map = take(sizeof(int32_t) * G->total_nodes);
+    B->off_bitmap = take(sizeof(uint32_t) * B->n_words);
+    B->off_wrank = take(sizeof(int32_t) * (B->n_words + 1));
+    B->off_excl = take(sizeof(uint64_t) * 4 * (max_excl > 0 ? max_excl : 1));
+    B->off_cub = take(cb);
+    B->total_bytes = off;
+    *out = reinterpret_cast<gsb_blocks_t>(B);
+    return GSB_OK;
+}
+
+gsb_status gsb_blocks_destroy(gsb_blocks_t b) {
+    delete reinterpret_cast<Blocks*>(b);
+    return GSB_OK;
+}
+
+gsb_status gsb_blocks_arena_bytes(gsb_blocks_t b, size_t* bytes) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && bytes, "null argument");
+    *bytes = B->total_bytes;
+    return GSB_OK;
+}
+
+gsb_status gsb_blocks_init_arena(gsb_blocks_t b, void* arena, size_t arena_bytes, void* stream) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && arena, "null argument");
+    if (arena_bytes < B->total_bytes) {
+        set_error("arena %zu < %zu bytes", arena_bytes, B->total_bytes);
+        return GSB_EWORKSPACE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t N = B->g->total_nodes;
+    GSB_LAUNCH("init_arena", init_arena_kernel, grid_for(std::max(N, B->n_words), 256, kNumSMs * 8), 256, 0, s,
+               at<int32_t>(arena, B->off_map), N, at<uint32_t>(arena, B->off_bitmap), B->n_words,
+               at<int>(arena, B->off_err));
+    return GSB_OK;
+}
+
+gsb_status gsb_sample(gsb_blocks_t b, const int64_t* seeds, int64_t n_seeds, uint64_t rng_seed, uint32_t step,
+                      const int64_t* excl_u, const int64_t* excl_v, int64_t n_excl, int32_t excl_etype,
+                      int32_t excl_rev_etype, void* arena, size_t arena_bytes, void* stream) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && arena && seeds, "null argument");
+    GSB_CHECK_ARG(n_seeds >= 1 && n_seeds <= B->max_seeds, "n_seeds %lld out of [1, %lld]", (long long)n_seeds,
+                  (long long)B->max_seeds);
+    GSB_CHECK_ARG(n_excl >= 0 && n_excl <= B->max_excl, "n_excl %lld exceeds capacity %lld", (long long)n_excl,
+                  (long long)B->max_excl);
+    GSB_CHECK_ARG(n_excl == 0 || (excl_u && excl_v && excl_etype >= 0 && excl_etype < B->g->dev.R),
+                  "bad exclusion arguments");
+    GSB_CHECK_ARG(excl_rev_etype < B->g->dev.R, "bad excl_rev_etype");
+    if (arena_bytes < B->total_bytes) {
+        set_error("arena %zu < %zu bytes", arena_bytes, B->total_bytes);
+        return GSB_EWORKSPACE;
+    }
+    const GraphDev& g = B->g->dev;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int S = g.S > 0 ? g.S : 1;
+    int* err = at<int>(arena, B->off_err);
+    int32_t* map = at<int32_t>(arena, B->off_map);
+    uint32_t* bitmap = at<uint32_t>(arena, B->off_bitmap);
+    int32_t* wrank = at<int32_t>(arena, B->off_wrank);
+    void* cub_tmp = at<char>(arena, B->off_cub);
+
+    Excl ex{nullptr, 0, excl_etype, excl_rev_etype >= 0 ? excl_rev_etype : -2};
+    if (n_excl > 0) {
+        uint64_t* kin = at<uint64_t>(arena, B->off_excl);
+        uint64_t* kout = kin + 2 * B->max_excl;
+        GSB_LAUNCH("excl_keys", excl_keys_kernel, grid_for(n_excl, 256, 64), 256, 0, s, excl_u, excl_v, n_excl,
+                   excl_rev_etype >= 0 ? 1 : 0, kin);
+        size_t cb = B->cub_bytes;
+        GSB_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, cb, kin, kout, (int64_t)(2 * n_excl), 0, 64, s));
+        count_launch(16);
+        ex.keys = kout;
+        ex.n = 2 * n_excl;
+    }
+
+    GSB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
+    GSB_LAUNCH("seed_meta", seed_meta_kernel, 1, 1024, 0, s, g, seeds, n_seeds, at<int64_t>(arena, B->off_seed),
+               at<HopMeta>(arena, B->off_meta[1]), err);
+    for (int h = 1; h <= B->L; ++h) {
+        HopBufs hb = B->hop(h, arena);
+        const int f = B->fanout[B->L - h];
+        const int64_t nseg = hb.cap_dst * S;
+        GSB_LAUNCH("sample_count", count_kernel, grid_for(nseg + 1, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
+                   hb.dst_gid, hb.cap_dst, f, ex, map, hb.cnt, err);
+        size_t cb = B->cub_bytes;
+        GSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, hb.cnt, hb.seg_ptr, (int64_t)(nseg + 1), s));
+        count_launch(2);
+        GSB_LAUNCH("sample_fill", fill_kernel, grid_for(nseg * 32, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
+                   hb.dst_gid, hb.cap_dst, hb.seg_ptr, f, ex, rng_seed, step, h, map, bitmap, hb.e_src_gid, hb.e_eid, err);
+        GSB_LAUNCH("bitmap_popc", popc_kernel, grid_for(B->n_words + 1, 256, kNumSMs * 8), 256, 0, s, bitmap,
+                   B->n_words, wrank);
+        cb = B->cub_bytes;
+        GSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, wrank, wrank, (int64_t)(B->n_words + 1), s));
+        count_launch(2);
+        HopMeta* next = (h < B->L) ? at<HopMeta>(arena, B->off_meta[h + 1]) : nullptr;
+        GSB_LAUNCH("hop_meta", hop_meta_kernel, 1, 32, 0, s, g, hb.meta, next, hb.seg_ptr, nseg, bitmap, wrank,
+                   hb.cap_src, err);
+        GSB_LAUNCH("relabel", relabel_kernel, grid_for(hb.cap_edges, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
+                   hb.e_src_gid, map, bitmap, wrank, hb.e_src);
+        GSB_LAUNCH("next_frontier", next_frontier_kernel,
+                   grid_for(std::max(hb.cap_dst, B->n_words), 256, kNumSMs * 8), 256, 0, s, g, hb.meta, hb.dst_gid,
+                   map, bitmap, wrank, B->n_words, hb.cap_src, hb.src_gid);
+    }
+    return GSB_OK;
+}
+
+gsb_status gsb_block_sizes(gsb_blocks_t b, const void* arena, int32_t layer, int64_t* n_dst, int64_t* n_src,
+                                 int64_t* n_edges, int64_t* dst_type_cnt, int64_t* src_type_cnt, void* stream) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && arena && layer >= 0 && layer < B->L, "bad argument");
+    int h = B->hop_of_layer(layer);
+    HopMeta m;
+    cudaStream_t s = (cudaStream_t)stream;
+    GSB_CUDA(cudaMemcpyAsync(&m, at<HopMeta>(const_cast<void*>(arena), B->off_meta[h]), sizeof(HopMeta),
+                             cudaMemcpyDeviceToHost, s));
+    GSB_CUDA(cudaStreamSynchronize(s));
+    if (n_dst) *n_dst = m.n_dst;
+    if (n_src) *n_src = m.n_src;
+    if (n_edges) *n_edges = m.n_edges;
+    for (int t = 0; t < B->g->dev.T; ++t) {
+        if (dst_type_cnt) dst_type_cnt[t] = m.dst_off[t + 1] - m.dst_off[t];
+        if (src_type_cnt) src_type_cnt[t] = m.src_off[t + 1] - m.src_off[t];
+    }
+    return GSB_OK;
+}
+
+gsb_status gsb_block_view_get(gsb_blocks_t b, const void* arena, int32_t layer, gsb_block_view* out) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && arena && out && layer >= 0 && layer < B->L, "bad argument");
+    HopBufs hb = B->hop(B->hop_of_layer(layer), const_cast<void*>(arena));
+    out->dst_gid = hb.dst_gid;
+    out->src_gid = hb.src_gid;
+    out->seg_ptr = hb.seg_ptr;
+    out->e_src_gid = hb.e_src_gid;
+    out->e_eid = hb.e_eid;
+    out->e_src = hb.e_src;
+    out->num_slots = B->g->dev.S > 0 ? B->g->dev.S : 1;
+    return GSB_OK;
+}
+
+gsb_status gsb_blocks_poll_error(gsb_blocks_t b, void* arena, int32_t* code, void* stream) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && arena && code, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    int h = 0;
+    GSB_CUDA(cudaMemcpyAsync(&h, at<int>(arena, B->off_err), sizeof(int), cudaMemcpyDeviceToHost, s));
+    GSB_CUDA(cudaStreamSynchronize(s));
+    *code = h;
+    if (h != 0) {
+        set_error("device-side error %d latched during sampling", h);
+        return GSB_EDEVICE;
+    }
+    return GSB_OK;
+}
+
+gsb_status gsb_blocks_input_rows(gsb_blocks_t b, int64_t* max_rows) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && max_rows, "null argument");
+    *max_rows = B->cap_dst[B->L + 1];
+    return GSB_OK;
+}
+
+gsb_status gsb_blocks_dst_rows(gsb_blocks_t b, int32_t layer, int64_t* max_rows) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && max_rows && layer >= 0 && layer < B->L, "bad argument");
+    *max_rows = B->cap_dst[B->hop_of_layer(layer)];
+    return GSB_OK;
+}
+
+gsb_status gsb_gather_block_inputs(gsb_blocks_t b, const void* arena, float* out, void* stream) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && arena && out, "null argument");
+    const Graph* G = B->g;
+    GSB_CHECK_ARG(G->dev.feat_dim > 0, "features not registered");
+    HopBufs hb = B->hop(B->L, const_cast<void*>(arena));
+    return launch_gather(G, hb.src_gid, &hb.meta->n_src, 0, hb.cap_src, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

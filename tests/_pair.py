@@ -1,0 +1,43 @@
+"""Builds the two independent sides of a parity test from the same seeded synthetic inputs:
+the oracle (CPU, fp64, its own CSC) and the CUDA path (libgsb via the runtime driver).
+Only `synth` is shared."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+import synth
+
+RTOL_F32 = 1e-5   # BASELINE.json north_star: "relative tolerance of 1e-5 in fp32"
+
+
+def close(gpu, ref, rtol=RTOL_F32, what=""):
+    """|g - r| <= rtol*|r| + rtol*max|r|  (SURVEY §8(c) tolerance reading, DESIGN.md R-tol)."""
+    g = np.asarray(gpu, dtype=np.float64)
+    r = np.asarray(ref, dtype=np.float64)
+    assert g.shape == r.shape, (what, g.shape, r.shape)
+    if r.size == 0:
+        return
+    scale = np.abs(r).max()
+    err = np.abs(g - r)
+    bound = rtol * np.abs(r) + rtol * scale
+    bad = err > bound
+    assert not bad.any(), (f"{what}: {bad.sum()} / {r.size} outside tolerance; max err {err.max():.3e}, "
+                           f"max|ref| {scale:.3e}, worst at {np.unravel_index(np.argmax(err - bound), r.shape)}")
+
+
+def gpu_store(cfg, device="cuda", keep=None):
+    import torch
+    from paper_2406_06022_b200.runtime import GraphStore
+    st = GraphStore(cfg.counts, cfg.etype_src(), cfg.etype_dst(), device)
+    for r in range(cfg.num_etypes):
+        s, d = synth.etype_coo(cfg, r, backend="torch", device=device)
+        k = None if keep is None or r not in keep else torch.as_tensor(keep[r]).to(device)
+        st.load_etype(r, s, d, k)
+    for t in range(cfg.num_ntypes):
+        st.set_features(t, synth.feature_table(cfg, t, backend="torch", device=device))
+    return st
+
+
+def oracle_graph(cfg, keep=None):
+    return oracle.Graph(cfg, keep=keep)

@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Integer work (CSC, sampled blocks, relabel, gather) is bit-exact; floats are
+within rtol 1e-5 (fp32, north_star) under |g-r| <= rtol|r| + rtol max|r|."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests._pair import close, gpu_store, oracle_graph
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2406_06022_b200 import build
+    build.build()
+    return torch
+
+
+CASES = {
+    "tiny": lambda: synth.tiny(),
+    "mag_small": lambda: synth.scaled(synth.mag(), 0.01, "mag_small"),
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def pair(request, torch_cuda):
+    cfg = CASES[request.param]()
+    return cfg, gpu_store(cfg), oracle_graph(cfg)
+
+
+# ------------------------------------------------------------------ CSC + gather
+def test_csc_bitexact(pair):
+    cfg, st, og = pair
+    for r in range(cfg.num_etypes):
+        assert st.n_edges[r] == len(og.indices[r])
+        assert np.array_equal(st.indptr[r].cpu().numpy(), og.indptr[r])
+        assert np.array_equal(st.indices[r][:st.n_edges[r]].cpu().numpy(), og.indices[r])
+
+
+def test_csc_keep_mask_bitexact(torch_cuda):
+    cfg = synth.tiny()
+    keep = {0: (np.arange(cfg.etypes[0].num_edges) % 3 != 0).astype(np.uint8)}
+    st = gpu_store(cfg, keep=keep)
+    og = oracle_graph(cfg, keep=keep)
+    assert st.n_edges[0] == len(og.indices[0])
+    assert np.array_equal(st.indptr[0].cpu().numpy(), og.indptr[0])
+    assert np.array_equal(st.indices[0][:st.n_edges[0]].cpu().numpy(), og.indices[0])
+
+
+def test_gather_bitexact(pair, torch_cuda):
+    cfg, st, og = pair
+    rng = np.random.default_rng(0)
+    gids = np.concatenate([rng.integers(0, cfg.num_nodes, 5000), [0, cfg.num_nodes - 1]]).astype(np.int64)
+    out = st.gather(torch_cuda.from_numpy(gids).cuda()).cpu().numpy()
+    assert np.array_equal(out, oracle.gather(og, gids))
+
+
+# ------------------------------------------------------------------ sampling
+def _compare_blocks(cfg, st, sampler, oblocks):
+    slots = st.slot_etypes()
+    for l, ob in enumerate(oblocks):
+        gb = sampler.block(l)
+        assert np.array_equal(gb.dst_gid.cpu().numpy(), ob.dst_gid), f"layer {l} dst"
+        assert np.array_equal(gb.src_gid.cpu().numpy(), ob.src_gid), f"layer {l} src"
+        S = gb.num_slots
+        seg = gb.seg_ptr.cpu().numpy()
+        cnt = np.diff(seg).reshape(-1, S)
+        t = np.searchsorted(cfg.node_off, ob.dst_gid, side="right") - 1
+        exp = np.zeros_like(cnt)
+        for j in range(len(ob.dst_gid)):
+            for s, r in enumerate(slots[t[j]]):
+                exp[j, s] = ob.seg_cnt[j, r]
+        assert np.array_equal(cnt, exp), f"layer {l} segment counts"
+        assert np.array_equal(gb.e_src_gid.cpu().numpy(), ob.e_src_gid), f"layer {l} edge src gid"
+        assert np.array_equal(gb.e_eid.cpu().numpy(), ob.e_eid), f"layer {l} eid"
+        assert np.array_equal(gb.e_src.cpu().numpy(), ob.e_src), f"layer {l} edge src row"
+
+
+@pytest.mark.parametrize("fanouts", [None, [1, 3], [-1, 4], [32, 32]])
+def test_sample_blocks_bitexact(pair, torch_cuda, fanouts):
+    from paper_2406_06022_b200.runtime import MiniBatchSampler
+    cfg, st, og = pair
+    f = fanouts or cfg.fanouts
+    if -1 in f and cfg.name != "tiny":
+        pytest.skip("fanout ALL only on the tiny graph")
+    sm = MiniBatchSampler(st, f, max_seeds=cfg.batch)
+    for step in (0, 3):
+        seeds = synth.nc_seeds(cfg, step)
+        sm.sample(torch_cuda.from_numpy(seeds).cuda(), cfg.rng_seed, step)
+        assert sm.poll_error() == 0
+        ob = oracle.sample_blocks(og, seeds, f, cfg.rng_seed, step)
+        _compare_blocks(cfg, st, sm, ob)
+
+
+def test_sample_ragged_and_edge_cases(torch_cuda):
+    """single seed, a seed of every type (mixed, type-grouped), zero-degree nodes."""
+    from paper_2406_06022_b200.runtime import MiniBatchSampler
+    cfg = synth.tiny()
+    st, og = gpu_store(cfg), oracle_graph(cfg)
+    indeg = {t: np.zeros(cfg.counts[t], np.int64) for t in range(cfg.num_ntypes)}
+    for r in range(cfg.num_etypes):
+        indeg[cfg.etypes[r].dst] += np.diff(og.indptr[r])
+    iso = [int(np.nonzero(indeg[t] == 0)[0][0]) + int(cfg.node_off[t]) for t in range(cfg.num_ntypes)
+           if (indeg[t] == 0).any()]
+    cases = [np.array([7]), np.array(sorted([3, cfg.node_off[1] + 5, cfg.node_off[2] + 9])),
+             np.array(sorted(set(iso + [11, 12])))]
+    sm = MiniBatchSampler(st, cfg.fanouts, max_seeds=64)
+    for i, seeds in enumerate(cases):
+        seeds = seeds.astype(np.int64)
+        sm.sample(torch_cuda.from_numpy(seeds).cuda(), 5, i)
+        assert sm.poll_error() == 0
+        _compare_blocks(cfg, st, sm, oracle.sample_blocks(og, seeds, cfg.fanouts, 5, i))
+
+
+def test_sample_latched_errors(torch_cuda):
+    from paper_2406_06022_b200.runtime import MiniBatchSampler
+    cfg = synth.tiny()
+    st = gpu_store(cfg)
+    sm = MiniBatchSampler(st, cfg.fanouts, max_seeds=8)
+    bad_group = np.array([cfg.node_off[1] + 1, 2], np.int64)       # type 1 before type 0
+    sm.sample(torch_cuda.from_numpy(bad_group).cuda(), 1, 0)
+    assert sm.poll_error() == 1
+    from paper_2406_06022_b200 import _lib
+    with pytest.raises(_lib.GsbError):
+        sm.sample(torch_cuda.zeros(9, dtype=torch_cuda.int64).cuda(), 1, 0)   # over capacity: sync error
+
+
+def test_sample_deterministic(pair, torch_cuda):
+    from paper_2406_06022_b200.runtime import MiniBatchSampler
+    cfg, st, og = pair
+    sm = MiniBatchSampler(st, cfg.fanouts, max_seeds=cfg.batch)
+    seeds = torch_cuda.from_numpy(synth.nc_seeds(cfg, 1)).cuda()
+    outs = []
+    for _ in range(2):
+        sm.sample(seeds, 9, 1)
+        b = sm.block(0)
+        outs.append((b.src_gid.cpu().numpy(), b.e_src.cpu().numpy(), b.e_eid.cpu().numpy()))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ full NC train step
+def _gpu_trainer(cfg, st):
+    import torch
+    from paper_2406_06022_b200.runtime import RGCNTrainer
+    return RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
+                       synth.param_order(cfg), torch.from_numpy(synth.labels(cfg)),
+                       int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
+
+
+def _adam_interval(p, g, m, v, tol_g, lr, t):
+    """Oracle Adam update evaluated for gradients across [g - tol_g, g + tol_g] (5 points):
+    the interval of parameters consistent with the gradient tolerance (DESIGN.md R-adamtol;
+    Adam's normalised step is ill-conditioned where |g| is near 0)."""
+    outs = []
+    for k in (-1.0, -0.5, 0.0, 0.5, 1.0):
+        pp, mm, vv = p.copy(), m.copy(), v.copy()
+        oracle.adam(pp, g + k * tol_g, mm, vv, lr, t)
+        outs.append(pp)
+    outs = np.stack(outs)
+    return outs.min(0), outs.max(0), outs[2]
+
+
+def test_nc_step_parity(pair, torch_cuda):
+    """3 steps; before each, the GPU state is set from the oracle's (fp32-rounded), then both
+    run one full step: blocks, x0 bit-exact; activations, loss, grads within rtol; params
+    after Adam inside the oracle's interval for gradients within the gradient tolerance."""
+    import torch
+    cfg, st, og = pair
+    tr = _gpu_trainer(cfg, st)
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    opt = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}
+    labels = synth.labels(cfg)
+    rtol = 1e-5
+    for step in range(3):
+        for k in synth.param_order(cfg):
+            tr.pview(k).copy_(torch.from_numpy(params[k].astype(np.float32)))
+            tr.pview(k, "m").copy_(torch.from_numpy(opt[k]["m"].astype(np.float32)))
+            tr.pview(k, "v").copy_(torch.from_numpy(opt[k]["v"].astype(np.float32)))
+        tr.t = step
+        seeds = synth.nc_seeds(cfg, step)
+        tr.forward_backward(torch_cuda.from_numpy(seeds).cuda(), step)
+        res = oracle.nc_step(og, params, seeds, labels, step, cfg.rng_seed)
+        n0 = len(res.blocks[0].src_gid)
+        assert np.array_equal(tr.x0[:n0].cpu().numpy(), res.x0)
+        for l in range(len(cfg.fanouts)):
+            nd = len(res.blocks[l].dst_gid)
+            close(tr.hout[l][:nd].cpu().numpy(), res.hs[l], what=f"step {step} h{l}")
+        close(tr.loss.cpu().numpy()[0], res.loss, what="loss")
+        for k in synth.param_order(cfg):
+            close(tr.pview(k, "g").cpu().numpy(), res.grads[k], what=f"step {step} grad {k}")
+        tr.optimizer_step()
+        for k in synth.param_order(cfg):
+            g = res.grads[k]
+            tol_g = rtol * np.abs(g) + rtol * np.abs(g).max()
+            lo, hi, mid = _adam_interval(params[k], g, opt[k]["m"], opt[k]["v"], tol_g, cfg.lr, step + 1)
+            gp = tr.pview(k).cpu().numpy().astype(np.float64)
+            slack = rtol * np.abs(mid) + rtol * np.abs(mid).max()
+            bad = (gp < lo - slack) | (gp > hi + slack)
+            assert not bad.any(), f"step {step} param {k}: {bad.sum()} outside the Adam interval"
+            oracle.adam(params[k], g, opt[k]["m"], opt[k]["v"], cfg.lr, step + 1)
+
+
+def test_adam_kernel_parity(torch_cuda):
+    import ctypes as C
+    import torch
+    from paper_2406_06022_b200._lib import call
+    rng = np.random.default_rng(3)
+    n = 1000
+    p0 = rng.standard_normal(n).astype(np.float32)
+    p, m, v = (torch.from_numpy(x).cuda() for x in (p0.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)))
+    pd, md, vd = p0.astype(np.float64), np.zeros(n), np.zeros(n)
+    for t in range(1, 4):
+        g = rng.standard_normal(n).astype(np.float32)
+        gt = torch.from_numpy(g).cuda()
+        call("gsb_adam_step", C.c_void_p(p.data_ptr()), C.c_void_p(gt.data_ptr()), C.c_void_p(m.data_ptr()),
+             C.c_void_p(v.data_ptr()), n, 0.01, 0.9, 0.999, 1e-8, t, None)
+        oracle.adam(pd, g, md, vd, 0.01, t)
+    torch.cuda.synchronize()
+    close(p.cpu().numpy(), pd, what="adam")
