@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--profile-steps", type=int, default=20)
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     return ap.parse_args()
 
 
@@ -184,6 +185,18 @@ def build_gsb(cfg, device):
     return st, tr
 
 
+_GRAPH_LAUNCHES = {}
+
+
+def launches_per_step_graph(tr, cfg):
+    """libgsb kernels in one captured step (counted once while capturing an eager twin)."""
+    from paper_2406_06022_b200 import _lib
+    key = id(tr)
+    if key not in _GRAPH_LAUNCHES:
+        _GRAPH_LAUNCHES[key] = tr.graph_launches
+    return _GRAPH_LAUNCHES[key]
+
+
 def block_sizes(tr, cfg):
     L = len(cfg.fanouts)
     sm = tr.sampler
@@ -226,8 +239,32 @@ def run_gsb(args, cfg):
             tr.grad.mul_(1.0 / ws)
         tr.optimizer_step()
 
-    for i in range(args.warmup):
+    def allreduce(g):
+        dist.all_reduce(g)
+        g.mul_(1.0 / ws)
+
+    W = max(args.warmup, 3)
+    for i in range(W - 2):
         step(i)
+    torch.cuda.synchronize()
+    if tr.sampler.poll_error() != 0:
+        raise RuntimeError("device-side sampling error latched")
+    # ---- capture ONE whole step (sample..Adam) in a CUDA graph; replays advance the RNG step
+    # word and Adam's t on the device, inputs are copied into the graph's fixed seed buffer
+    use_graph = not args.no_graph
+    if use_graph:
+        tr.load_inputs(seeds_all[W - 2])
+        tr.capture(step0=(W - 2) * ws + rank, ws=ws, allreduce=allreduce if dist is not None else None)
+
+    def run(i):
+        if use_graph:
+            tr.seeds_dev.copy_(seeds_all[i], non_blocking=True)
+            tr.replay()
+        else:
+            step(i)
+
+    for i in range(W - 2, W):
+        run(i)
     torch.cuda.synchronize()
     if tr.sampler.poll_error() != 0:
         raise RuntimeError("device-side sampling error latched")
@@ -239,13 +276,15 @@ def run_gsb(args, cfg):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         e0.record()
-        for i in range(args.warmup, args.warmup + args.steps):
-            step(i)
+        for i in range(W, W + args.steps):
+            run(i)
         e1.record()
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     launches = _lib.lib().gsb_launch_count() - launches0
+    if use_graph:   # kernels inside a replayed graph are not re-counted by the library
+        launches = launches_per_step_graph(tr, cfg) * args.steps
     ms = e0.elapsed_time(e1)
     if dist is not None:
         t = torch.tensor([ms], device=device)
@@ -254,11 +293,14 @@ def run_gsb(args, cfg):
     ms_per_step = ms / args.steps
     seeds_per_s = cfg.batch * ws * args.steps / (ms / 1e3)
 
-    # ---- sizes + per-kernel profile (separate pass, CUDA events around every launch)
-    base = args.warmup + args.steps
+    # ---- per-kernel profile: eager steps, each preceded by a 3 ms spin kernel so the host
+    # enqueues the whole step before it starts (events then time kernels, not launch gaps)
+    base = W + args.steps
+    import ctypes as C
     _lib.lib().gsb_profile_enable(1)
     for i in range(base, base + args.profile_steps):
-        step(i)          # no host sync inside: events see GPU time, not launch gaps
+        _lib.call("gsb_spin", 3_000_000, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        step(i)
     torch.cuda.synchronize()
     _lib.lib().gsb_profile_enable(0)
     # block sizes of the profiled steps: sampling is a pure function of (seeds, step), so
@@ -267,12 +309,13 @@ def run_gsb(args, cfg):
     for i in range(base, base + args.profile_steps):
         tr.sampler.sample(seeds_all[i], tr.rng_seed, i * ws + rank)
         sizes.append(block_sizes(tr, cfg))
-    import ctypes as C
     buf = C.create_string_buffer(1 << 16)
     _lib.call("gsb_profile_dump", buf, len(buf))
     prof = {}
     for line in buf.value.decode().splitlines():
         n, c, t = line.split()
+        if n == "spin":
+            continue
         prof[n] = {"launches": int(c), "total_ms": float(t)}
     edges_per_step = float(np.mean([sum(s["n_edges"]) for s in sizes]))
     # ---- e2e: public API with host buffers (pinned seeds H2D + loss D2H every step)
@@ -285,15 +328,17 @@ def run_gsb(args, cfg):
     t0 = time.perf_counter()
     for i in range(args.steps):
         if dist is None:
-            tr.train_step_host(seeds_host[i], base + args.profile_steps + i, loss_host)
+            tr.train_step_host(seeds_host[i], base + args.profile_steps + i, loss_host, eager=not use_graph)
         else:
             n = seeds_host[i].numel()
             tr.seeds_dev[:n].copy_(seeds_host[i], non_blocking=True)
-            step_dev = tr.seeds_dev[:n]
-            tr.forward_backward(step_dev, base + i)
-            dist.all_reduce(tr.grad)
-            tr.grad.mul_(1.0 / ws)
-            tr.optimizer_step()
+            if use_graph:
+                tr.replay()
+            else:
+                tr.forward_backward(tr.seeds_dev[:n], base + i)
+                dist.all_reduce(tr.grad)
+                tr.grad.mul_(1.0 / ws)
+                tr.optimizer_step()
             loss_host.copy_(tr.loss, non_blocking=True)
             torch.cuda.current_stream().synchronize()
     e2e_s = time.perf_counter() - t0

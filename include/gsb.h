@@ -136,11 +136,30 @@ gsb_status gsb_blocks_arena_bytes(gsb_blocks_t b, size_t* bytes);
 /* One-time arena initialisation (node maps to "absent").  Must precede the first sample. */
 gsb_status gsb_blocks_init_arena(gsb_blocks_t b, void* arena, size_t arena_bytes, void* stream);
 
-/* seeds: device int64 gids [n_seeds]; excl_u/excl_v: device int64 gids [n_excl] (may be
- * NULL when n_excl == 0).  Writes the blocks into the arena. */
-gsb_status gsb_sample(gsb_blocks_t b, const int64_t* seeds, int64_t n_seeds, uint64_t rng_seed, uint32_t step,
-                      const int64_t* excl_u, const int64_t* excl_v, int64_t n_excl, int32_t excl_etype,
-                      int32_t excl_rev_etype, void* arena, size_t arena_bytes, void* stream);
+/* Arguments of one gsb_sample call.
+ *  seeds      device int64 gids; distinct, grouped by ntype in ascending type order
+ *  n_seeds    host count (or, when n_seeds_dev != NULL, the capacity bound <= max_seeds)
+ *  n_seeds_dev  optional device int64 count (e.g. written by gsb_lp_seeds)
+ *  rng_seed   Philox key; step: counter word (R-rng); step_dev: optional device uint32
+ *             overriding `step` (lets a captured CUDA graph advance the step on device)
+ *  excl_u/excl_v  optional device int64 gids [n_excl] of LP batch positives (u,v) of
+ *             excl_etype; their reverses are excluded from excl_rev_etype (-1 = none). */
+typedef struct {
+    const int64_t* seeds;
+    int64_t n_seeds;
+    const int64_t* n_seeds_dev;
+    uint64_t rng_seed;
+    uint32_t step;
+    const uint32_t* step_dev;
+    const int64_t* excl_u;
+    const int64_t* excl_v;
+    int64_t n_excl;
+    int32_t excl_etype;
+    int32_t excl_rev_etype;
+} gsb_sample_args;
+
+/* Samples all hops of one mini-batch into the arena. */
+gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* args, void* arena, size_t arena_bytes, void* stream);
 
 /* Sizes of the block of `layer` (syncs `stream`): n_dst, n_src, n_edges and the
  * per-ntype dst / src row counts (host arrays [num_ntypes]). */
@@ -202,11 +221,18 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
                               const float* dh_dst, const float* W, const float* acat, int32_t d_in, int32_t d_out,
                               int32_t relu, float* dW, float* db, float* dh_src, float* dacat_ws, void* stream);
 
+/* Plain GEMM on the same tcgen05 3xTF32 path as the layers (single group), fp32 row-major:
+ *   mode 0 (NN): C[M][N]  = A[M][K] B[K][N]        (K multiple of 32)
+ *   mode 1 (NT): C[M][K]  = A[M][N] B[K][N]^T
+ *   mode 2 (TN): C[K][N] += A[M][K]^T B[M][N]      (C accumulated; zero it first) */
+gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int32_t N,
+                    int32_t K, float* C, int64_t ldc, void* stream);
+
 /* ======================================================================================
  * Node-classification decoder + softmax cross-entropy (P:L477 ClassifyLossFunc, P:L489;
  * S:L405-408; §8(a) a8):  logits = h Wc + bc ; loss = mean_i(lse_i - logit_{i,y_i})
  *   y_i = labels[seed_gid[i] - label_gid_base].
- * Writes: logits_ws [n][C] (scratch), loss (device fp32 scalar), dh [n][d], dWc [d][C],
+ * Writes: logits_ws [n][ceil4(C)] (scratch, rows padded to a multiple of 4), loss (device fp32 scalar), dh [n][d], dWc [d][C],
  * dbc [C] (overwritten).  row_loss_ws: device fp32 [n] scratch.
  * ==================================================================================== */
 gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, const float* bc, int32_t C,
@@ -214,11 +240,46 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
                        float* row_loss_ws, float* loss, float* dh, float* dWc, float* dbc, void* stream);
 
 /* ======================================================================================
+ * Link prediction (App. A; §8(a) a9, a10).
+ * ==================================================================================== */
+/* Joint negative sampling: positives in groups of K; group g draws K iid uniform
+ * nodes of the dst type: neg[g*K + j] = gid_base + unif(Philox(g + group_base, j, step),
+ * n_dst_nodes) (R-joint, R-rng).  neg: device int64 [ceil(n_pos/K)*K]. */
+gsb_status gsb_joint_negatives(int64_t n_pos, int32_t K, int64_t n_dst_nodes, int64_t gid_base, uint64_t rng_seed,
+                               uint32_t step, const uint32_t* step_dev, int64_t group_base, int64_t* neg,
+                               void* stream);
+
+/* LP seed set (§8(a) a9): seeds = ascending unique(u ∪ v ∪ neg); iu/iv/ineg = row of
+ * each u / v / neg in seeds.  seeds capacity 2*B + n_neg; *n_seeds_dev (device int64)
+ * receives the count.  ws: device scratch of gsb_lp_seeds_bytes. */
+gsb_status gsb_lp_seeds_bytes(int64_t B, int64_t n_neg, size_t* bytes);
+gsb_status gsb_lp_seeds(const int64_t* u, const int64_t* v, int64_t B, const int64_t* neg, int64_t n_neg,
+                        int64_t* seeds, int64_t* n_seeds_dev, int32_t* iu, int32_t* iv, int32_t* ineg, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* DistMult score (Eq. 3) + loss and its gradients.
+ *   pos_i = sum_k H[iu_i,k] rel[k] H[iv_i,k] ; neg_ij = sum_k H[iu_i,k] rel[k] H[ineg_{g(i)K+j},k]
+ *   loss_kind 0: contrastive Eq. 7 (R-lpmean); 1: cross entropy Eq. 4 (R-ce); mean over B.
+ * H: device fp32 [n_rows][d] (last RGCN layer output over the LP seeds); scores: device
+ * fp32 [B][1+K]; loss: device fp32 scalar; dH: device fp32 [n_rows][d] (overwritten,
+ * n_rows_cap rows zeroed); drel [d] (overwritten); row_loss_ws: device fp32 [B]. */
+gsb_status gsb_lp_score(const float* H, int64_t n_rows_cap, int32_t d, const int32_t* iu, const int32_t* iv,
+                        const int32_t* ineg, int64_t B, int32_t K, const float* rel, int32_t loss_kind, float* scores,
+                        float* row_loss_ws, float* loss, float* dH, float* drel, void* stream);
+
+/* ======================================================================================
  * Optimizer (paper silent, R-adam): Adam with bias correction over a flat
  * fp32 buffer of n parameters; t is the 1-based step.  In place on p, m, v.
  * ==================================================================================== */
 gsb_status gsb_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1,
-                         float beta2, float eps, int32_t t, void* stream);
+                         float beta2, float eps, int32_t t, const int32_t* t_dev, void* stream);
+/* t_dev: optional device int32 overriding t (CUDA-graph replay). */
+
+/* Add `delta` to a device int32/uint32 counter (graph-capturable step advance). */
+gsb_status gsb_counter_add(int32_t* counter, int32_t delta, void* stream);
+
+/* Busy-wait kernel (profiling aid: lets the host enqueue a whole step before it runs). */
+gsb_status gsb_spin(int64_t nanoseconds, void* stream);
 
 #ifdef __cplusplus
 }

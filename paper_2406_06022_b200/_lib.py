@@ -20,6 +20,12 @@ class gsb_block_view(C.Structure):
                 ("num_slots", i32)]
 
 
+class gsb_sample_args(C.Structure):
+    _fields_ = [("seeds", P), ("n_seeds", i64), ("n_seeds_dev", P), ("rng_seed", u64), ("step", u32),
+                ("step_dev", P), ("excl_u", P), ("excl_v", P), ("n_excl", i64), ("excl_etype", i32),
+                ("excl_rev_etype", i32)]
+
+
 # name -> argtypes (all return gsb_status = int32 unless listed in _RET)
 SIGS = {
     "gsb_last_error": [],
@@ -38,7 +44,7 @@ SIGS = {
     "gsb_blocks_destroy": [P],
     "gsb_blocks_arena_bytes": [P, C.POINTER(sz)],
     "gsb_blocks_init_arena": [P, P, sz, P],
-    "gsb_sample": [P, P, i64, u64, u32, P, P, i64, i32, i32, P, sz, P],
+    "gsb_sample": [P, C.POINTER(gsb_sample_args), P, sz, P],
     "gsb_block_sizes": [P, P, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), P, P, P],
     "gsb_block_view_get": [P, P, i32, C.POINTER(gsb_block_view)],
     "gsb_slot_etype": [P, i32, i32, C.POINTER(i32)],
@@ -49,8 +55,15 @@ SIGS = {
     "gsb_layer_acat_floats": [P, i32, i32, C.POINTER(i64)],
     "gsb_rgcn_layer_fwd": [P, P, i32, P, i32, P, P, i32, i32, P, P, P],
     "gsb_rgcn_layer_bwd": [P, P, i32, P, P, P, P, i32, i32, i32, P, P, P, P, P],
+    "gsb_gemm": [i32, P, i64, P, i64, i64, i32, i32, P, i64, P],
     "gsb_nc_loss": [P, i64, i32, P, P, i32, P, P, i64, P, P, P, P, P, P, P],
-    "gsb_adam_step": [P, P, P, P, i64, f32, f32, f32, f32, i32, P],
+    "gsb_adam_step": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P],
+    "gsb_counter_add": [P, i32, P],
+    "gsb_spin": [i64, P],
+    "gsb_joint_negatives": [i64, i32, i64, i64, u64, u32, P, i64, P, P],
+    "gsb_lp_seeds_bytes": [i64, i64, C.POINTER(sz)],
+    "gsb_lp_seeds": [P, P, i64, P, i64, P, P, P, P, P, P, sz, P],
+    "gsb_lp_score": [P, i64, i32, P, P, P, i64, i32, P, i32, P, P, P, P, P, P],
 }
 _RET = {"gsb_last_error": C.c_char_p, "gsb_version": i32, "gsb_launch_count": i64}
 

@@ -153,7 +153,12 @@ gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_de
 // ------------------------------------------------------------------------------------
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ gr, float* __restrict__ m,
                             float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps, float c1,
-                            float c2) {
+                            float c2, const int32_t* __restrict__ t_dev) {
+    if (t_dev) {   // bias corrections from the device step counter (graph replay)
+        const float t = (float)*t_dev;
+        c1 = 1.f - powf(b1, t);
+        c2 = 1.f - powf(b2, t);
+    }
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
         float g = gr[i];
@@ -165,6 +170,16 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ gr,
         float vh = vi / c2;
         p[i] -= lr * mh / (sqrtf(vh) + eps);
     }
+}
+
+__global__ void counter_add_kernel(int32_t* c, int32_t d) { *c += d; }
+
+__global__ void spin_kernel(int64_t ns) {
+    uint64_t t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    } while ((int64_t)(t1 - t0) < ns);
 }
 
 }  // namespace gsb
@@ -369,13 +384,25 @@ gsb_status gsb_gather(gsb_graph_t g, const int64_t* gid, int64_t n, float* out, 
 }
 
 gsb_status gsb_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
-                         float eps, int32_t t, void* stream) {
-    GSB_CHECK_ARG(p && g && m && v && n >= 0 && t >= 1, "bad argument");
+                         float eps, int32_t t, const int32_t* t_dev, void* stream) {
+    GSB_CHECK_ARG(p && g && m && v && n >= 0 && (t >= 1 || t_dev), "bad argument");
+    if (t < 1) t = 1;
     if (n == 0) return GSB_OK;
     float c1 = 1.f - powf(b1, (float)t);
     float c2 = 1.f - powf(b2, (float)t);
     GSB_LAUNCH("adam", adam_kernel, grid_for(n, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream, p, g, m, v, n, lr,
-               b1, b2, eps, c1, c2);
+               b1, b2, eps, c1, c2, t_dev);
+    return GSB_OK;
+}
+
+gsb_status gsb_counter_add(int32_t* counter, int32_t delta, void* stream) {
+    GSB_CHECK_ARG(counter, "null counter");
+    GSB_LAUNCH("counter_add", counter_add_kernel, 1, 1, 0, (cudaStream_t)stream, counter, delta);
+    return GSB_OK;
+}
+
+gsb_status gsb_spin(int64_t ns, void* stream) {
+    GSB_LAUNCH("spin", spin_kernel, 1, 32, 0, (cudaStream_t)stream, ns);
     return GSB_OK;
 }
 

@@ -1,6 +1,7 @@
 // layer.cu -- RGCN layer forward / backward and the NC decoder + softmax-CE loss.
 // Contract: include/gsb.h "RGCN layer" and "Node-classification decoder".
 #include "gemm_simt.cuh"
+#include "gemm_umma.cuh"
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(GraphDev g, const HopMeta*
 // ------------------------------------------------------------------------------------
 // softmax cross-entropy, warp per row; logits are overwritten by dlogits
 // ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int64_t n, int C,
+__global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int64_t n, int C, int64_t ldl,
                                                  const int32_t* __restrict__ labels,
                                                  const int64_t* __restrict__ seed_gid, int64_t base,
                                                  float* __restrict__ row_loss) {
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const float invn = 1.f / (float)n;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
-        float* lg = logits + i * C;
+        float* lg = logits + i * ldl;
         const int y = labels[seed_gid[i] - base];
         float mx = -INFINITY;
         for (int c = lane; c < C; c += 32) mx = fmaxf(mx, lg[c]);
@@ -188,9 +189,16 @@ gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     GSB_LAUNCH("rgcn_agg", agg_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g, hb.meta, hb.seg_ptr,
                hb.e_src, h_src, d_in, acat, lda);
     RowGroups rg = layer_groups(B, arena, layer);
+#ifdef GSB_SIMT_GEMM
     GSB_LAUNCH("rgcn_gemm_fwd", gemm_nn_kernel, gemm_grid(hb.cap_dst, (d_out + BN - 1) / BN, g.T), NT, 0, s, rg,
                acat, lda, W, d_in, d_out, (int64_t)d_out, (int64_t)d_in * d_out, bias, relu, h_dst, (int64_t)d_out);
     return GSB_OK;
+#else
+    UProb P{};
+    P.rg = rg; P.A = acat; P.lda = lda; P.B = W; P.ldb = d_out; P.bslot = (int64_t)d_in * d_out;
+    P.relu = relu; P.d_in = d_in; P.N = d_out; P.C = h_dst; P.ldc = d_out; P.bias = bias;
+    return launch_umma<UMMA_NN>("rgcn_gemm_fwd", P, (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_out, 128), s);
+#endif
 }
 
 gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_dst,
@@ -210,6 +218,7 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     RowGroups rg = layer_groups(B, arena, layer);
     GSB_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)(g.R + 1) * d_in * d_out, s));
     GSB_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)d_out, s));
+#ifdef GSB_SIMT_GEMM
     const int rpc = 256;
     {
         int64_t items = (ceil_div(hb.cap_dst, rpc) + g.T) * (g.S + 1) * ceil_div(d_in, BM) * ceil_div(d_out, BN);
@@ -217,15 +226,61 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         GSB_LAUNCH("rgcn_gemm_dW", gemm_tn_kernel, grid, NT, 0, s, rg, acat, lda, dh_dst, h_dst, relu,
                    (int64_t)d_out, d_in, d_out, rpc, dW, (int64_t)d_out, (int64_t)d_in * d_out, db);
     }
+#else
+    {
+        // row chunks sized so the (type, slot, chunk) items cover ~2 waves of SMs
+        const int64_t rows = hb.cap_dst;
+        int rpc = (int)std::max<int64_t>(128, std::min<int64_t>(2048, ceil_div(rows * (g.S + 1), 2 * kNumSMs)));
+        rpc = (rpc + 31) / 32 * 32;
+        UProb P{};
+        P.rg = rg; P.A = acat; P.lda = lda; P.B = dh_dst; P.ldb = d_out; P.H = h_dst; P.relu = relu;
+        P.d_in = d_in; P.N = d_out; P.C = dW; P.ldc = d_out; P.bslot = (int64_t)d_in * d_out; P.db = db;
+        P.rows_per_chunk = rpc;
+        int64_t items = (ceil_div(rows, rpc) + g.T) * (g.S + 1) * ceil_div(d_in, 128) * ceil_div(d_out, 128);
+        gsb_status st = launch_umma<UMMA_TN>("rgcn_gemm_dW", P, items, s);
+        if (st != GSB_OK) return st;
+    }
+#endif
     if (dh_src) {
+#ifdef GSB_SIMT_GEMM
         GSB_LAUNCH("rgcn_gemm_dA", gemm_nt_kernel, gemm_grid(hb.cap_dst, (int)ceil_div(d_in, BN) * (g.S + 1), g.T),
                    NT, 0, s, rg, dh_dst, h_dst, relu, (int64_t)d_out, W, d_in, d_out, (int64_t)d_out,
                    (int64_t)d_in * d_out, dacat_ws, lda);
+#else
+        UProb P{};
+        P.rg = rg; P.A = dh_dst; P.lda = d_out; P.H = h_dst; P.relu = relu; P.B = W; P.ldb = d_out;
+        P.bslot = (int64_t)d_in * d_out; P.d_in = d_in; P.N = d_out; P.C = dacat_ws; P.ldc = lda;
+        gsb_status st = launch_umma<UMMA_NT>("rgcn_gemm_dA", P,
+                                             (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_in, 128) * (g.S + 1), s);
+        if (st != GSB_OK) return st;
+#endif
         GSB_CUDA(cudaMemsetAsync(dh_src, 0, sizeof(float) * (size_t)hb.cap_src * d_in, s));
         GSB_LAUNCH("rgcn_scatter", scatter_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
                    hb.meta, hb.seg_ptr, hb.e_src, dacat_ws, lda, d_in, dh_src);
     }
     return GSB_OK;
+}
+
+gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int32_t N,
+                    int32_t K, float* C, int64_t ldc, void* stream) {
+    GSB_CHECK_ARG(A && B && C && M >= 1 && N >= 1 && K >= 1, "bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    UProb P{};
+    P.rg = single_group(M);
+    P.A = A; P.lda = lda; P.B = B; P.ldb = ldb; P.C = C; P.ldc = ldc;
+    if (mode == 0) {            // C[M][N] = A[M][K] B[K][N]
+        GSB_CHECK_ARG(K % 32 == 0, "NN needs K %% 32 == 0");
+        P.d_in = K; P.N = N;
+        return launch_umma<UMMA_NN>("gemm_nn", P, ceil_div(M, 128) * ceil_div(N, 128), s);
+    } else if (mode == 1) {     // C[M][K] = A[M][N] B[K][N]^T
+        P.d_in = K; P.N = N;
+        return launch_umma<UMMA_NT>("gemm_nt", P, ceil_div(M, 128) * ceil_div(K, 128), s);
+    } else if (mode == 2) {     // C[K][N] += A[M][K]^T B[M][N]
+        P.d_in = K; P.N = N; P.rows_per_chunk = 128;
+        return launch_umma<UMMA_TN>("gemm_tn", P, ceil_div(M, 128) * ceil_div(K, 128) * ceil_div(N, 128), s);
+    }
+    set_error("mode %d not in {0,1,2}", mode);
+    return GSB_EINVAL;
 }
 
 gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, const float* bc, int32_t C,
@@ -235,24 +290,51 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
     GSB_CHECK_ARG(n >= 1 && d > 0 && d % BK == 0 && C >= 1, "bad dims (d %% %d == 0 required)", BK);
     cudaStream_t s = (cudaStream_t)stream;
     RowGroups rg = single_group(n);
+    const int64_t ldl = (C + 3) / 4 * 4;   // padded logits row (16-B aligned rows)
+#ifdef GSB_SIMT_GEMM
     GSB_LAUNCH("nc_logits", gemm_nn_kernel, gemm_grid(n, (C + BN - 1) / BN, 1), NT, 0, s, rg, h, (int64_t)d, Wc, d,
-               C, (int64_t)C, (int64_t)0, bc, 0, logits_ws, (int64_t)C);
-    GSB_LAUNCH("nc_ce", ce_kernel, grid_for(n * 32, 256, kNumSMs * 4), 256, 0, s, logits_ws, n, C, labels, seed_gid,
-               label_gid_base, row_loss_ws);
+               C, (int64_t)C, (int64_t)0, bc, 0, logits_ws, ldl);
+#else
+    {
+        UProb P{};
+        P.rg = rg; P.A = h; P.lda = d; P.B = Wc; P.ldb = C; P.bslot = 0; P.d_in = d; P.N = C; P.C = logits_ws;
+        P.ldc = ldl; P.bias = bc;
+        gsb_status st = launch_umma<UMMA_NN>("nc_logits", P, ceil_div(n, 128) * ceil_div(C, 128), s);
+        if (st != GSB_OK) return st;
+    }
+#endif
+    GSB_LAUNCH("nc_ce", ce_kernel, grid_for(n * 32, 256, kNumSMs * 4), 256, 0, s, logits_ws, n, C, ldl, labels,
+               seed_gid, label_gid_base, row_loss_ws);
     GSB_LAUNCH("nc_mean", mean_kernel, 1, 1024, 0, s, row_loss_ws, n, loss);
     if (dWc || dbc) {
         GSB_CHECK_ARG(dWc && dbc, "dWc and dbc go together");
         GSB_CUDA(cudaMemsetAsync(dWc, 0, sizeof(float) * (size_t)d * C, s));
         GSB_CUDA(cudaMemsetAsync(dbc, 0, sizeof(float) * (size_t)C, s));
+#ifdef GSB_SIMT_GEMM
         const int rpc = 128;
         int64_t items = ceil_div(n, rpc) * ceil_div(d, BM) * ceil_div(C, BN);
         GSB_LAUNCH("nc_gemm_dWc", gemm_tn_kernel, (int)std::min<int64_t>(items, kNumSMs * 4), NT, 0, s, rg, h,
-                   (int64_t)d, logits_ws, (const float*)nullptr, 0, (int64_t)C, d, C, rpc, dWc, (int64_t)C,
+                   (int64_t)d, logits_ws, (const float*)nullptr, 0, ldl, d, C, rpc, dWc, (int64_t)C,
                    (int64_t)0, dbc);
+#else
+        UProb P{};
+        P.rg = rg; P.A = h; P.lda = d; P.B = logits_ws; P.ldb = ldl; P.d_in = d; P.N = C; P.C = dWc; P.ldc = C;
+        P.bslot = 0; P.db = dbc; P.rows_per_chunk = 128;
+        gsb_status st = launch_umma<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, 128) * ceil_div(d, 128) * ceil_div(C, 128), s);
+        if (st != GSB_OK) return st;
+#endif
     }
     if (dh) {
+#ifdef GSB_SIMT_GEMM
         GSB_LAUNCH("nc_gemm_dh", gemm_nt_kernel, gemm_grid(n, (int)ceil_div(d, BN), 1), NT, 0, s, rg, logits_ws,
-                   (const float*)nullptr, 0, (int64_t)C, Wc, d, C, (int64_t)C, (int64_t)0, dh, (int64_t)d);
+                   (const float*)nullptr, 0, ldl, Wc, d, C, (int64_t)C, (int64_t)0, dh, (int64_t)d);
+#else
+        UProb P{};
+        P.rg = rg; P.A = logits_ws; P.lda = ldl; P.B = Wc; P.ldb = C; P.bslot = 0; P.d_in = d; P.N = C; P.C = dh;
+        P.ldc = d;
+        gsb_status st = launch_umma<UMMA_NT>("nc_gemm_dh", P, ceil_div(n, 128) * ceil_div(d, 128), s);
+        if (st != GSB_OK) return st;
+#endif
     }
     return GSB_OK;
 }

@@ -1,0 +1,273 @@
+// lp.cu -- link prediction: joint negative sampling, the LP seed set, DistMult
+// scoring (Eq. 3) with contrastive (Eq. 7) or cross-entropy (Eq. 4) loss and gradients.
+// Contract: include/gsb.h "Link prediction".
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "gsb_internal.cuh"
+#include "rng.cuh"
+
+namespace gsb {
+
+__global__ void joint_neg_kernel(int64_t total, int K, int64_t n_nodes, int64_t base, uint64_t seed, uint32_t step_host,
+                                 const uint32_t* __restrict__ step_dev, int64_t group_base, int64_t* __restrict__ neg) {
+    const uint32_t step = step_dev ? *step_dev : step_host;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = group_base + i / K;
+        const uint32_t j = (uint32_t)(i % K);
+        uint64_t x = keyed_u64(seed, (uint32_t)(uint64_t)g, (uint32_t)((uint64_t)g >> 32), 0xFFF00000u | (j & 0xFFFFu),
+                               step);
+        neg[i] = base + (int64_t)__umul64hi(x, (uint64_t)n_nodes);
+    }
+}
+
+__global__ void lp_concat_kernel(const int64_t* __restrict__ u, const int64_t* __restrict__ v, int64_t B,
+                                 const int64_t* __restrict__ neg, int64_t n_neg, uint64_t* __restrict__ buf) {
+    const int64_t n = 2 * B + n_neg;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = (uint64_t)(i < B ? u[i] : (i < 2 * B ? v[i - B] : neg[i - 2 * B]));
+}
+
+__global__ void lp_pos_kernel(const uint64_t* __restrict__ buf, int64_t B, int64_t n_neg,
+                              const int64_t* __restrict__ seeds, const int64_t* __restrict__ n_seeds,
+                              int32_t* __restrict__ iu, int32_t* __restrict__ iv, int32_t* __restrict__ ineg) {
+    const int64_t n = 2 * B + n_neg;
+    const int64_t ns = *n_seeds;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = (int64_t)buf[i];
+        int64_t lo = 0, hi = ns;
+        while (lo < hi) {
+            int64_t m = (lo + hi) >> 1;
+            if (seeds[m] < x) lo = m + 1; else hi = m;
+        }
+        if (i < B) iu[i] = (int32_t)lo;
+        else if (i < 2 * B) iv[i - B] = (int32_t)lo;
+        else ineg[i - 2 * B] = (int32_t)lo;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// DistMult + loss: warp per positive; lanes over the embedding (float4 chunks)
+// ------------------------------------------------------------------------------------
+constexpr int kMaxC4 = 4;   // d <= 512
+
+__device__ __forceinline__ float warp_sum(float x) {
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+__device__ __forceinline__ float softplus(float x) { return x > 0.f ? x + log1pf(expf(-x)) : log1pf(expf(x)); }
+__device__ __forceinline__ float sigm(float x) { return x >= 0.f ? 1.f / (1.f + expf(-x)) : expf(x) / (1.f + expf(x)); }
+
+__global__ void __launch_bounds__(256) lp_score_kernel(const float* __restrict__ H, int d,
+                                                       const int32_t* __restrict__ iu, const int32_t* __restrict__ iv,
+                                                       const int32_t* __restrict__ ineg, int64_t B, int K,
+                                                       const float* __restrict__ rel, int kind,
+                                                       float* __restrict__ scores, float* __restrict__ row_loss,
+                                                       float* __restrict__ dH, float* __restrict__ drel) {
+    extern __shared__ float s_drel[];
+    const int lane = threadIdx.x & 31;
+    const int d4 = d >> 2;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) s_drel[c] = 0.f;
+    __syncthreads();
+    float4 r[kMaxC4], dr[kMaxC4];
+#pragma unroll
+    for (int q = 0; q < kMaxC4; ++q) {
+        int c = lane + 32 * q;
+        r[q] = (c < d4) ? __ldg(reinterpret_cast<const float4*>(rel) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        dr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float invB = 1.f / (float)B;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < B; i += warps) {
+        const int64_t g = i / K;
+        const float* hu = H + (int64_t)iu[i] * d;
+        const float* hv = H + (int64_t)iv[i] * d;
+        float4 u[kMaxC4], ur[kMaxC4];
+        float s0 = 0.f;
+#pragma unroll
+        for (int q = 0; q < kMaxC4; ++q) {
+            int c = lane + 32 * q;
+            u[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            ur[q] = u[q];
+            if (c < d4) {
+                u[q] = reinterpret_cast<const float4*>(hu)[c];
+                float4 v = reinterpret_cast<const float4*>(hv)[c];
+                ur[q] = make_float4(u[q].x * r[q].x, u[q].y * r[q].y, u[q].z * r[q].z, u[q].w * r[q].w);
+                s0 += ur[q].x * v.x + ur[q].y * v.y + ur[q].z * v.z + ur[q].w * v.w;
+            }
+        }
+        s0 = warp_sum(s0);
+        float* sc = scores + i * (K + 1);
+        if (lane == 0) sc[0] = s0;
+        // pass 1: negative scores, online max / sum-exp (contrastive) or BCE sum (CE)
+        float mx = s0, se = 1.f, lsum = softplus(-s0);
+        for (int j = 0; j < K; ++j) {
+            const float* hn = H + (int64_t)ineg[g * K + j] * d;
+            float s = 0.f;
+#pragma unroll
+            for (int q = 0; q < kMaxC4; ++q) {
+                int c = lane + 32 * q;
+                if (c < d4) {
+                    float4 n = reinterpret_cast<const float4*>(hn)[c];
+                    s += ur[q].x * n.x + ur[q].y * n.y + ur[q].z * n.z + ur[q].w * n.w;
+                }
+            }
+            s = warp_sum(s);
+            if (lane == 0) sc[1 + j] = s;
+            if (s > mx) {
+                se = se * expf(mx - s) + 1.f;
+                mx = s;
+            } else {
+                se += expf(s - mx);
+            }
+            lsum += softplus(s);
+        }
+        const float lse = mx + logf(se);
+        if (lane == 0) row_loss[i] = (kind == 0) ? (lse - s0) : lsum / (float)(K + 1);
+        __syncwarp();
+        // pass 2: gradients.  ds_j = dloss/dscore_j
+        float4 du[kMaxC4];
+        const float ds0 = (kind == 0) ? (expf(s0 - lse) - 1.f) * invB : (sigm(s0) - 1.f) / (float)(K + 1) * invB;
+        float* dv = dH + (int64_t)iv[i] * d;
+#pragma unroll
+        for (int q = 0; q < kMaxC4; ++q) {
+            int c = lane + 32 * q;
+            du[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c < d4) {
+                float4 v = reinterpret_cast<const float4*>(hv)[c];
+                du[q] = make_float4(ds0 * r[q].x * v.x, ds0 * r[q].y * v.y, ds0 * r[q].z * v.z, ds0 * r[q].w * v.w);
+                dr[q].x += ds0 * u[q].x * v.x; dr[q].y += ds0 * u[q].y * v.y;
+                dr[q].z += ds0 * u[q].z * v.z; dr[q].w += ds0 * u[q].w * v.w;
+                red_add_f4(dv + 4 * c, make_float4(ds0 * ur[q].x, ds0 * ur[q].y, ds0 * ur[q].z, ds0 * ur[q].w));
+            }
+        }
+        for (int j = 0; j < K; ++j) {
+            const float s = sc[1 + j];
+            const float ds = (kind == 0) ? expf(s - lse) * invB : sigm(s) / (float)(K + 1) * invB;
+            const int64_t row = ineg[g * K + j];
+            const float* hn = H + row * d;
+            float* dn = dH + row * d;
+#pragma unroll
+            for (int q = 0; q < kMaxC4; ++q) {
+                int c = lane + 32 * q;
+                if (c < d4) {
+                    float4 n = reinterpret_cast<const float4*>(hn)[c];
+                    du[q].x += ds * r[q].x * n.x; du[q].y += ds * r[q].y * n.y;
+                    du[q].z += ds * r[q].z * n.z; du[q].w += ds * r[q].w * n.w;
+                    dr[q].x += ds * u[q].x * n.x; dr[q].y += ds * u[q].y * n.y;
+                    dr[q].z += ds * u[q].z * n.z; dr[q].w += ds * u[q].w * n.w;
+                    red_add_f4(dn + 4 * c, make_float4(ds * ur[q].x, ds * ur[q].y, ds * ur[q].z, ds * ur[q].w));
+                }
+            }
+        }
+        float* duo = dH + (int64_t)iu[i] * d;
+#pragma unroll
+        for (int q = 0; q < kMaxC4; ++q) {
+            int c = lane + 32 * q;
+            if (c < d4) red_add_f4(duo + 4 * c, du[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kMaxC4; ++q) {
+        int c = lane + 32 * q;
+        if (c < d4) {
+            atomicAdd(&s_drel[4 * c + 0], dr[q].x);
+            atomicAdd(&s_drel[4 * c + 1], dr[q].y);
+            atomicAdd(&s_drel[4 * c + 2], dr[q].z);
+            atomicAdd(&s_drel[4 * c + 3], dr[q].w);
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(drel + c, s_drel[c]);
+}
+
+__global__ void __launch_bounds__(1024) lp_mean_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
+    __shared__ float sm[32];
+    float s = 0.f;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = (threadIdx.x < (blockDim.x >> 5)) ? sm[threadIdx.x] : 0.f;
+        s = warp_sum(s);
+        if (threadIdx.x == 0) *out = s / (float)n;
+    }
+}
+
+static size_t lp_cub_bytes(int64_t n) {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, a, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)n, 0, 64);
+    cub::DeviceSelect::Unique(nullptr, b, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t*)nullptr, (int64_t)n);
+    return std::max(a, b);
+}
+
+}  // namespace gsb
+
+using namespace gsb;
+
+extern "C" {
+
+gsb_status gsb_joint_negatives(int64_t n_pos, int32_t K, int64_t n_dst_nodes, int64_t gid_base, uint64_t rng_seed,
+                               uint32_t step, const uint32_t* step_dev, int64_t group_base, int64_t* neg,
+                               void* stream) {
+    GSB_CHECK_ARG(neg && n_pos >= 1 && K >= 1 && K <= 0xFFFF && n_dst_nodes >= 1, "bad argument");
+    const int64_t total = ceil_div(n_pos, K) * K;
+    GSB_LAUNCH("joint_negatives", joint_neg_kernel, grid_for(total, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream,
+               total, K, n_dst_nodes, gid_base, rng_seed, step, step_dev, group_base, neg);
+    return GSB_OK;
+}
+
+gsb_status gsb_lp_seeds_bytes(int64_t B, int64_t n_neg, size_t* bytes) {
+    GSB_CHECK_ARG(bytes && B >= 1 && n_neg >= 0, "bad argument");
+    const int64_t n = 2 * B + n_neg;
+    *bytes = 2 * align_up(sizeof(uint64_t) * n) + align_up(lp_cub_bytes(n));
+    return GSB_OK;
+}
+
+gsb_status gsb_lp_seeds(const int64_t* u, const int64_t* v, int64_t B, const int64_t* neg, int64_t n_neg,
+                        int64_t* seeds, int64_t* n_seeds_dev, int32_t* iu, int32_t* iv, int32_t* ineg, void* ws,
+                        size_t ws_bytes, void* stream) {
+    GSB_CHECK_ARG(u && v && seeds && n_seeds_dev && iu && iv && ws && B >= 1 && n_neg >= 0, "null argument");
+    GSB_CHECK_ARG(n_neg == 0 || (neg && ineg), "null negatives");
+    size_t need = 0;
+    gsb_lp_seeds_bytes(B, n_neg, &need);
+    if (ws_bytes < need) {
+        set_error("lp_seeds workspace %zu < %zu", ws_bytes, need);
+        return GSB_EWORKSPACE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = 2 * B + n_neg;
+    uint64_t* buf = (uint64_t*)ws;
+    uint64_t* sorted = (uint64_t*)((char*)ws + align_up(sizeof(uint64_t) * n));
+    void* tmp = (char*)ws + 2 * align_up(sizeof(uint64_t) * n);
+    size_t tb = lp_cub_bytes(n);
+    GSB_LAUNCH("lp_concat", lp_concat_kernel, grid_for(n, 256, kNumSMs * 4), 256, 0, s, u, v, B, neg, n_neg, buf);
+    GSB_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, buf, sorted, (int64_t)n, 0, 40, s));
+    count_launch(12);
+    tb = lp_cub_bytes(n);
+    GSB_CUDA(cub::DeviceSelect::Unique(tmp, tb, sorted, (uint64_t*)seeds, n_seeds_dev, (int64_t)n, s));
+    count_launch(2);
+    GSB_LAUNCH("lp_positions", lp_pos_kernel, grid_for(n, 256, kNumSMs * 4), 256, 0, s, buf, B, n_neg, seeds,
+               n_seeds_dev, iu, iv, ineg);
+    return GSB_OK;
+}
+
+gsb_status gsb_lp_score(const float* H, int64_t n_rows_cap, int32_t d, const int32_t* iu, const int32_t* iv,
+                        const int32_t* ineg, int64_t B, int32_t K, const float* rel, int32_t loss_kind, float* scores,
+                        float* row_loss_ws, float* loss, float* dH, float* drel, void* stream) {
+    GSB_CHECK_ARG(H && iu && iv && ineg && rel && scores && row_loss_ws && loss && dH && drel, "null argument");
+    GSB_CHECK_ARG(d > 0 && d % 4 == 0 && d <= 4 * 32 * kMaxC4, "d %d must be a multiple of 4 and <= %d", d,
+                  4 * 32 * kMaxC4);
+    GSB_CHECK_ARG(B >= 1 && K >= 1 && (loss_kind == 0 || loss_kind == 1), "bad B/K/loss_kind");
+    cudaStream_t s = (cudaStream_t)stream;
+    GSB_CUDA(cudaMemsetAsync(dH, 0, sizeof(float) * (size_t)n_rows_cap * d, s));
+    GSB_CUDA(cudaMemsetAsync(drel, 0, sizeof(float) * (size_t)d, s));
+    GSB_LAUNCH("lp_score", lp_score_kernel, grid_for(B * 32, 256, kNumSMs * 4), 256, sizeof(float) * d, s, H, d, iu,
+               iv, ineg, B, K, rel, loss_kind, scores, row_loss_ws, dH, drel);
+    GSB_LAUNCH("lp_mean", lp_mean_kernel, 1, 1024, 0, s, row_loss_ws, B, loss);
+    return GSB_OK;
+}
+
+}  // extern "C"

@@ -15,6 +15,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "gsb_internal.cuh"
+#include "rng.cuh"
 
 namespace gsb {
 
@@ -22,28 +23,6 @@ gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_de
                          float* out, cudaStream_t s);
 
 enum { ERR_NONE = 0, ERR_GROUPING = 1, ERR_RANGE = 2, ERR_CAPACITY = 3, ERR_DUPLICATE = 4 };
-
-// ------------------------------------------------------------------------------------
-// Philox4x32-10 (counter-based; R-rng)
-// ------------------------------------------------------------------------------------
-__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        if (r) {
-            k.x += 0x9E3779B9u;
-            k.y += 0xBB67AE85u;
-        }
-        uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-        uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    }
-    return c;
-}
-
-__device__ __forceinline__ uint64_t keyed_u64(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
-    uint4 o = philox10(make_uint4(c0, c1, c2, c3), make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-    return ((uint64_t)o.y << 32) | o.x;
-}
 
 // ------------------------------------------------------------------------------------
 // LP exclusion set: sorted keys (flag << 62 | dst_gid << 31 | src_gid); flag 0 applies
@@ -129,25 +108,40 @@ __device__ __forceinline__ int64_t excl_map(const Excl& x, int64_t k0, int64_t k
 // ------------------------------------------------------------------------------------
 // hop-1 setup: copy seeds into the arena, per-type offsets, grouping / range checks
 // ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) seed_meta_kernel(GraphDev g, const int64_t* __restrict__ seeds, int64_t n,
+__global__ void __launch_bounds__(1024) seed_meta_kernel(GraphDev g, const int64_t* __restrict__ seeds, int64_t n_cap,
+                                                         const int64_t* __restrict__ n_dev,
                                                          int64_t* __restrict__ d1, HopMeta* __restrict__ m,
                                                          int* __restrict__ err) {
     __shared__ unsigned long long cnt[kMaxT];
+    int64_t n = n_dev ? *n_dev : n_cap;
+    if (n > n_cap) {
+        if (threadIdx.x == 0) atomicExch(err, ERR_CAPACITY);
+        n = n_cap;
+    }
     if (threadIdx.x < kMaxT) cnt[threadIdx.x] = 0;
     __syncthreads();
     const int64_t N = g.node_off[g.T];
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        int64_t v = seeds[i];
-        d1[i] = v;
-        if (v < 0 || v >= N) {
-            atomicExch(err, ERR_RANGE);
-            continue;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        int t = -1;
+        if (i < n) {
+            int64_t v = seeds[i];
+            d1[i] = v;
+            if (v < 0 || v >= N) {
+                atomicExch(err, ERR_RANGE);
+            } else {
+                t = type_of(g, v);
+                if (i > 0) {
+                    int64_t p = seeds[i - 1];
+                    if (p >= 0 && p < N && type_of(g, p) > t) atomicExch(err, ERR_GROUPING);
+                }
+            }
         }
-        int t = type_of(g, v);
-        atomicAdd(&cnt[t], 1ull);
-        if (i > 0) {
-            int64_t p = seeds[i - 1];
-            if (p >= 0 && p < N && type_of(g, p) > t) atomicExch(err, ERR_GROUPING);
+        // warp-aggregated per-type counts (one shared atomic per warp and type)
+        for (int tt = 0; tt < g.T; ++tt) {
+            unsigned b = __ballot_sync(0xffffffffu, t == tt);
+            if (lane == 0 && b) atomicAdd(&cnt[tt], (unsigned long long)__popc(b));
         }
     }
     __syncthreads();
@@ -207,13 +201,14 @@ __global__ void __launch_bounds__(256) count_kernel(GraphDev g, const HopMeta* _
 __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __restrict__ m,
                                                    const int64_t* __restrict__ dst_gid, int64_t cap_dst,
                                                    const int64_t* __restrict__ seg_ptr, int fanout, Excl ex,
-                                                   uint64_t seed, uint32_t step, int hop,
+                                                   uint64_t seed, uint32_t step_host, const uint32_t* step_dev, int hop,
                                                    const int32_t* __restrict__ map, uint32_t* __restrict__ bitmap,
                                                    int64_t* __restrict__ e_src_gid, int64_t* __restrict__ e_eid,
                                                    const int* __restrict__ err) {
     const int S = g.S;
     const int lane = threadIdx.x & 31;
     const int64_t n = (*(volatile const int*)err) ? 0 : m->n_dst;
+    const uint32_t step = step_dev ? *step_dev : step_host;
     const int64_t nseg = n * S;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < nseg; i += warps) {
@@ -525,11 +520,16 @@ gsb_status gsb_blocks_init_arena(gsb_blocks_t b, void* arena, size_t arena_bytes
     return GSB_OK;
 }
 
-gsb_status gsb_sample(gsb_blocks_t b, const int64_t* seeds, int64_t n_seeds, uint64_t rng_seed, uint32_t step,
-                      const int64_t* excl_u, const int64_t* excl_v, int64_t n_excl, int32_t excl_etype,
-                      int32_t excl_rev_etype, void* arena, size_t arena_bytes, void* stream) {
+gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, size_t arena_bytes, void* stream) {
     Blocks* B = reinterpret_cast<Blocks*>(b);
-    GSB_CHECK_ARG(B && arena && seeds, "null argument");
+    GSB_CHECK_ARG(B && a && arena && a->seeds, "null argument");
+    const int64_t* seeds = a->seeds;
+    const int64_t n_seeds = a->n_seeds;
+    const uint64_t rng_seed = a->rng_seed;
+    const int64_t* excl_u = a->excl_u;
+    const int64_t* excl_v = a->excl_v;
+    const int64_t n_excl = a->n_excl;
+    const int32_t excl_etype = a->excl_etype, excl_rev_etype = a->excl_rev_etype;
     GSB_CHECK_ARG(n_seeds >= 1 && n_seeds <= B->max_seeds, "n_seeds %lld out of [1, %lld]", (long long)n_seeds,
                   (long long)B->max_seeds);
     GSB_CHECK_ARG(n_excl >= 0 && n_excl <= B->max_excl, "n_excl %lld exceeds capacity %lld", (long long)n_excl,
@@ -564,7 +564,7 @@ gsb_status gsb_sample(gsb_blocks_t b, const int64_t* seeds, int64_t n_seeds, uin
     }
 
     GSB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
-    GSB_LAUNCH("seed_meta", seed_meta_kernel, 1, 1024, 0, s, g, seeds, n_seeds, at<int64_t>(arena, B->off_seed),
+    GSB_LAUNCH("seed_meta", seed_meta_kernel, 1, 1024, 0, s, g, seeds, n_seeds, a->n_seeds_dev, at<int64_t>(arena, B->off_seed),
                at<HopMeta>(arena, B->off_meta[1]), err);
     for (int h = 1; h <= B->L; ++h) {
         HopBufs hb = B->hop(h, arena);
@@ -576,7 +576,8 @@ gsb_status gsb_sample(gsb_blocks_t b, const int64_t* seeds, int64_t n_seeds, uin
         GSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, hb.cnt, hb.seg_ptr, (int64_t)(nseg + 1), s));
         count_launch(2);
         GSB_LAUNCH("sample_fill", fill_kernel, grid_for(nseg * 32, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
-                   hb.dst_gid, hb.cap_dst, hb.seg_ptr, f, ex, rng_seed, step, h, map, bitmap, hb.e_src_gid, hb.e_eid, err);
+                   hb.dst_gid, hb.cap_dst, hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid,
+                   hb.e_eid, err);
         GSB_LAUNCH("bitmap_popc", popc_kernel, grid_for(B->n_words + 1, 256, kNumSMs * 8), 256, 0, s, bitmap,
                    B->n_words, wrank);
         cb = B->cub_bytes;

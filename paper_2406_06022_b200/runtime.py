@@ -123,6 +123,7 @@ class MiniBatchSampler:
     """gsb_blocks_* : sampled message-flow blocks of one mini-batch in a device arena."""
 
     def __init__(self, store: GraphStore, fanouts: Sequence[int], max_seeds: int, max_excl: int = 0):
+        self.max_excl = max_excl
         self.store = store
         self.L = len(fanouts)
         f = np.asarray(fanouts, dtype=np.int32)
@@ -144,10 +145,23 @@ class MiniBatchSampler:
 
     def sample(self, seeds: torch.Tensor, rng_seed: int, step: int, excl_u: Optional[torch.Tensor] = None,
                excl_v: Optional[torch.Tensor] = None, excl_etype: int = -1, excl_rev_etype: int = -1,
-               stream=None):
-        n_ex = 0 if excl_u is None else excl_u.numel()
-        call("gsb_sample", self.h, _ptr(seeds), seeds.numel(), rng_seed, step, _ptr(excl_u), _ptr(excl_v), n_ex,
-             excl_etype, excl_rev_etype, _ptr(self.arena), self.arena.numel(), _stream(stream))
+               stream=None, n_seeds_dev: Optional[torch.Tensor] = None, step_dev: Optional[torch.Tensor] = None,
+               n_seeds: Optional[int] = None):
+        """gsb_sample.  With n_seeds_dev the seed count is read on the device (n_seeds is then
+        the capacity); with step_dev the RNG step word is read on the device."""
+        a = _lib.gsb_sample_args()
+        a.seeds = seeds.data_ptr()
+        a.n_seeds = int(n_seeds if n_seeds is not None else seeds.numel())
+        a.n_seeds_dev = None if n_seeds_dev is None else n_seeds_dev.data_ptr()
+        a.rng_seed = rng_seed
+        a.step = step
+        a.step_dev = None if step_dev is None else step_dev.data_ptr()
+        a.excl_u = None if excl_u is None else excl_u.data_ptr()
+        a.excl_v = None if excl_v is None else excl_v.data_ptr()
+        a.n_excl = 0 if excl_u is None else excl_u.numel()
+        a.excl_etype = excl_etype
+        a.excl_rev_etype = excl_rev_etype
+        call("gsb_sample", self.h, C.byref(a), _ptr(self.arena), self.arena.numel(), _stream(stream))
 
     def input_rows(self) -> int:
         v = C.c_int64()
@@ -203,25 +217,22 @@ def _from_ptr(ptr: int, n: int, dtype: torch.dtype, device, owner: torch.Tensor)
     return owner[off:off + n * esz].view(dtype).clone()
 
 
-class RGCNTrainer:
-    """One RGCN mini-batch train step through libgsb (§8(a) a1-a12, NC task).
+class _TrainerBase:
+    """Shared state of an RGCN train step through libgsb: flat parameter / gradient / Adam
+    buffers, upper-bound-sized activation buffers, device step counters (so a whole step can
+    be captured in a CUDA graph and replayed), and the RGCN layers (§8(a) a5, a7, a11, a12)."""
 
-    params: dict name -> float32 numpy (synth.init_params layout: W{l} (R+1, d_in, d_out),
-    b{l}, Wc, bc).  All parameters live in one flat fp32 device buffer (one Adam launch).
-    """
-
-    def __init__(self, store: GraphStore, fanouts: Sequence[int], batch: int, hidden: int, num_classes: int,
-                 params: Dict[str, np.ndarray], param_order: Sequence[str], labels: torch.Tensor,
-                 label_gid_base: int, lr: float = 1e-3, rng_seed: int = 1):
+    def __init__(self, store: GraphStore, fanouts: Sequence[int], max_seeds: int, hidden: int,
+                 params: Dict[str, np.ndarray], param_order: Sequence[str], lr: float, rng_seed: int,
+                 max_excl: int = 0):
         self.store = store
         self.L = len(fanouts)
-        self.batch = batch
         self.hidden = hidden
-        self.C = num_classes
         self.lr = lr
         self.rng_seed = rng_seed
-        self.sampler = MiniBatchSampler(store, fanouts, max_seeds=batch)
+        self.sampler = MiniBatchSampler(store, fanouts, max_seeds=max_seeds, max_excl=max_excl)
         dev = store.device
+        self.device = dev
         self.names = list(param_order)
         sizes = [int(np.prod(params[k].shape)) for k in self.names]
         self.offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
@@ -232,11 +243,8 @@ class RGCNTrainer:
         self.v = torch.zeros_like(self.flat)
         self.shapes = {k: params[k].shape for k in self.names}
         self.t = 0
-        self.labels = labels.to(dev, dtype=torch.int32).contiguous()
-        self.label_base = int(label_gid_base)
         d0 = store.feat_dim
         self.d_in = [d0] + [hidden] * (self.L - 1)
-        # activations / caches (upper-bound sized; never reallocated)
         self.x0 = torch.empty((self.sampler.input_rows(), d0), dtype=torch.float32, device=dev)
         self.hout = [torch.empty((self.sampler.dst_rows(l), hidden), dtype=torch.float32, device=dev)
                      for l in range(self.L)]
@@ -246,10 +254,11 @@ class RGCNTrainer:
                                  dtype=torch.float32, device=dev)
         self.dh = [torch.empty((self.sampler.dst_rows(l), hidden), dtype=torch.float32, device=dev)
                    for l in range(self.L)]
-        self.logits = torch.empty((batch, max(num_classes, 1)), dtype=torch.float32, device=dev)
-        self.row_loss = torch.empty(batch, dtype=torch.float32, device=dev)
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
-        self.seeds_dev = torch.empty(batch, dtype=torch.int64, device=dev)
+        # device counters: [0] = RNG step word, [1] = Adam t (graph mode)
+        self.counters = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.graph = None
+        self.graph_ws = 1
 
     # parameter views -------------------------------------------------------------------
     def pview(self, name: str, which: str = "p") -> torch.Tensor:
@@ -262,12 +271,9 @@ class RGCNTrainer:
         buf = {"p": self.flat, "g": self.grad}[which]
         return C.c_void_p(buf.data_ptr() + int(self.offsets[k]) * 4)
 
-    # the step ----------------------------------------------------------------------------
-    def forward_backward(self, seeds: torch.Tensor, step: int, stream=None):
-        """Sample -> gather -> layers (input layer first) -> NC loss -> backward."""
-        s = _stream(stream)
-        n = seeds.numel()
-        self.sampler.sample(seeds, self.rng_seed, step, stream=stream)
+    # pieces ------------------------------------------------------------------------------
+    def _encode(self, s):
+        """gather -> RGCN layers, input layer first (Fig. 8)."""
         sm = self.sampler
         call("gsb_gather_block_inputs", sm.h, _ptr(sm.arena), _ptr(self.x0), s)
         h = self.x0
@@ -275,35 +281,177 @@ class RGCNTrainer:
             call("gsb_rgcn_layer_fwd", sm.h, _ptr(sm.arena), l, _ptr(h), self.d_in[l], self._pp(f"W{l}"),
                  self._pp(f"b{l}"), self.hidden, int(l < self.L - 1), _ptr(self.hout[l]), _ptr(self.acat[l]), s)
             h = self.hout[l]
-        top = self.L - 1
-        call("gsb_nc_loss", _ptr(h), n, self.hidden, self._pp("Wc"), self._pp("bc"), self.C, _ptr(self.labels),
-             _ptr(seeds), self.label_base, _ptr(self.logits), _ptr(self.row_loss), _ptr(self.loss),
-             _ptr(self.dh[top]), self._pp("Wc", "g"), self._pp("bc", "g"), s)
+        return h
+
+    def _backward_layers(self, s):
+        sm = self.sampler
         for l in reversed(range(self.L)):
-            h_src = self.x0 if l == 0 else self.hout[l - 1]
             dh_src = None if l == 0 else self.dh[l - 1]
             call("gsb_rgcn_layer_bwd", sm.h, _ptr(sm.arena), l, _ptr(self.hout[l]), _ptr(self.dh[l]),
                  self._pp(f"W{l}"), _ptr(self.acat[l]), self.d_in[l], self.hidden, int(l < self.L - 1),
                  self._pp(f"W{l}", "g"), self._pp(f"b{l}", "g"), _ptr(dh_src),
                  _ptr(self.dacat) if dh_src is not None else None, s)
-            del h_src
 
-    def optimizer_step(self, stream=None):
+    def optimizer_step(self, stream=None, t_dev: bool = False):
+        if t_dev:
+            call("gsb_adam_step", _ptr(self.flat), _ptr(self.grad), _ptr(self.m), _ptr(self.v), self.n_params,
+                 self.lr, 0.9, 0.999, 1e-8, 1, C.c_void_p(self.counters.data_ptr() + 4), _stream(stream))
+            return
         self.t += 1
         call("gsb_adam_step", _ptr(self.flat), _ptr(self.grad), _ptr(self.m), _ptr(self.v), self.n_params, self.lr,
-             0.9, 0.999, 1e-8, self.t, _stream(stream))
+             0.9, 0.999, 1e-8, self.t, None, _stream(stream))
+
+    # CUDA graph of one whole step ----------------------------------------------------------
+    def capture(self, step0: int, ws: int = 1, allreduce=None):
+        """Capture forward+backward(+all-reduce)+Adam of one step reading its inputs from the
+        fixed input buffers and the RNG step / Adam t from device counters, which the graph
+        advances (step += ws, t += 1).  Subsequent steps: load inputs, then replay()."""
+        self.counters[0] = step0
+        self.counters[1] = self.t
+        self.graph_ws = ws
+        torch.cuda.synchronize()
+        launches0 = lib().gsb_launch_count()
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                s = _stream()
+                call("gsb_counter_add", C.c_void_p(self.counters.data_ptr() + 4), 1, s)
+                self._step_body(stream=None, step=0, step_dev=self.counters[0:1])
+                if allreduce is not None:
+                    allreduce(self.grad)
+                self.optimizer_step(t_dev=True)
+                call("gsb_counter_add", C.c_void_p(self.counters.data_ptr()), ws, s)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph_launches = lib().gsb_launch_count() - launches0
+        self.graph = g
+        return g
+
+    def replay(self):
+        self.graph.replay()
+        self.t += 1
+
+
+class RGCNTrainer(_TrainerBase):
+    """Node classification (§8(a) a1-a8, a11, a12): RGCN encoder + softmax-CE decoder.
+
+    params (synth.init_params layout): W{l} (R+1, d_in, d_out), b{l}, Wc (hidden, C), bc.
+    """
+
+    def __init__(self, store: GraphStore, fanouts: Sequence[int], batch: int, hidden: int, num_classes: int,
+                 params: Dict[str, np.ndarray], param_order: Sequence[str], labels: torch.Tensor,
+                 label_gid_base: int, lr: float = 1e-3, rng_seed: int = 1):
+        super().__init__(store, fanouts, batch, hidden, params, param_order, lr, rng_seed)
+        dev = store.device
+        self.batch = batch
+        self.C = num_classes
+        self.labels = labels.to(dev, dtype=torch.int32).contiguous()
+        self.label_base = int(label_gid_base)
+        self.logits = torch.empty((batch, (max(num_classes, 1) + 3) // 4 * 4), dtype=torch.float32, device=dev)
+        self.row_loss = torch.empty(batch, dtype=torch.float32, device=dev)
+        self.seeds_dev = torch.empty(batch, dtype=torch.int64, device=dev)
+
+    def _step_body(self, stream=None, step: int = 0, step_dev=None, seeds=None):
+        s = _stream(stream)
+        seeds = self.seeds_dev if seeds is None else seeds
+        n = seeds.numel()
+        self.sampler.sample(seeds, self.rng_seed, step, stream=stream, step_dev=step_dev)
+        h = self._encode(s)
+        top = self.L - 1
+        call("gsb_nc_loss", _ptr(h), n, self.hidden, self._pp("Wc"), self._pp("bc"), self.C, _ptr(self.labels),
+             _ptr(seeds), self.label_base, _ptr(self.logits), _ptr(self.row_loss), _ptr(self.loss),
+             _ptr(self.dh[top]), self._pp("Wc", "g"), self._pp("bc", "g"), s)
+        self._backward_layers(s)
+
+    def forward_backward(self, seeds: torch.Tensor, step: int, stream=None):
+        """Sample -> gather -> layers (input layer first) -> NC loss -> backward."""
+        self._step_body(stream, step, None, seeds)
 
     def train_step(self, seeds: torch.Tensor, step: int, stream=None):
-        """One full step on device-resident seeds; returns nothing (loss stays on device)."""
         self.forward_backward(seeds, step, stream)
         self.optimizer_step(stream)
 
-    def train_step_host(self, seeds_host: torch.Tensor, step: int, loss_host: torch.Tensor) -> float:
-        """Public end-to-end call: seeds from (pinned) host memory, loss back to the host."""
+    def load_inputs(self, seeds: torch.Tensor):
+        self.seeds_dev[:seeds.numel()].copy_(seeds, non_blocking=True)
+
+    def train_step_host(self, seeds_host: torch.Tensor, step: int, loss_host: torch.Tensor,
+                        eager: bool = False) -> float:
+        """Public end-to-end call: seeds from (pinned) host memory, loss back to the host.
+        Uses the captured CUDA graph when one exists (the step word then comes from the
+        device counter, advanced by each replay)."""
         n = seeds_host.numel()
         dst = self.seeds_dev[:n]
         dst.copy_(seeds_host, non_blocking=True)
-        self.train_step(dst, step)
+        if self.graph is not None and n == self.batch and not eager:
+            self.replay()
+        else:
+            self.train_step(dst, step)
         loss_host.copy_(self.loss, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return float(loss_host[0])
+
+
+class LPTrainer(_TrainerBase):
+    """Link prediction (§8(a) a3', a9, a10): joint negatives, target-edge exclusion,
+    RGCN encoder, DistMult + contrastive (or CE) loss.  params: W{l}, b{l}, rel."""
+
+    def __init__(self, store: GraphStore, fanouts: Sequence[int], batch: int, hidden: int, num_neg: int,
+                 lp_etype: int, lp_rev_etype: int, params: Dict[str, np.ndarray], param_order: Sequence[str],
+                 lr: float = 1e-3, rng_seed: int = 1, loss_kind: int = 0):
+        B, K = batch, num_neg
+        self.G = (B + K - 1) // K
+        self.n_neg = self.G * K
+        max_seeds = 2 * B + self.n_neg
+        super().__init__(store, fanouts, max_seeds, hidden, params, param_order, lr, rng_seed, max_excl=B)
+        dev = store.device
+        self.B, self.K = B, K
+        self.lp_etype, self.lp_rev = lp_etype, lp_rev_etype
+        self.loss_kind = loss_kind
+        dst_t = int(store.etype_dst[lp_etype])
+        self.neg_base = int(store.node_off[dst_t])
+        self.neg_n = int(store.counts[dst_t])
+        self.pos_u = torch.empty(B, dtype=torch.int64, device=dev)
+        self.pos_v = torch.empty(B, dtype=torch.int64, device=dev)
+        self.neg = torch.empty(self.n_neg, dtype=torch.int64, device=dev)
+        self.seeds = torch.empty(max_seeds, dtype=torch.int64, device=dev)
+        self.n_seeds = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.iu = torch.empty(B, dtype=torch.int32, device=dev)
+        self.iv = torch.empty(B, dtype=torch.int32, device=dev)
+        self.ineg = torch.empty(self.n_neg, dtype=torch.int32, device=dev)
+        wb = C.c_size_t()
+        call("gsb_lp_seeds_bytes", B, self.n_neg, C.byref(wb))
+        self.seeds_ws = torch.empty(int(wb.value), dtype=torch.uint8, device=dev)
+        self.scores = torch.empty((B, K + 1), dtype=torch.float32, device=dev)
+        self.row_loss = torch.empty(B, dtype=torch.float32, device=dev)
+        self.group_base = 0
+
+    def _step_body(self, stream=None, step: int = 0, step_dev=None, seeds=None):
+        s = _stream(stream)
+        sd = None if step_dev is None else C.c_void_p(step_dev.data_ptr())
+        call("gsb_joint_negatives", self.B, self.K, self.neg_n, self.neg_base, self.rng_seed, step, sd,
+             self.group_base, _ptr(self.neg), s)
+        call("gsb_lp_seeds", _ptr(self.pos_u), _ptr(self.pos_v), self.B, _ptr(self.neg), self.n_neg, _ptr(self.seeds),
+             _ptr(self.n_seeds), _ptr(self.iu), _ptr(self.iv), _ptr(self.ineg), _ptr(self.seeds_ws),
+             self.seeds_ws.numel(), s)
+        self.sampler.sample(self.seeds, self.rng_seed, step, self.pos_u, self.pos_v, self.lp_etype, self.lp_rev, stream,
+                            n_seeds_dev=self.n_seeds, step_dev=step_dev, n_seeds=self.seeds.numel())
+        h = self._encode(s)
+        top = self.L - 1
+        call("gsb_lp_score", _ptr(h), self.hout[top].shape[0], self.hidden, _ptr(self.iu), _ptr(self.iv),
+             _ptr(self.ineg), self.B, self.K, self._pp("rel"), self.loss_kind, _ptr(self.scores),
+             _ptr(self.row_loss), _ptr(self.loss), _ptr(self.dh[top]), self._pp("rel", "g"), s)
+        self._backward_layers(s)
+
+    def load_inputs(self, u: torch.Tensor, v: torch.Tensor):
+        self.pos_u.copy_(u, non_blocking=True)
+        self.pos_v.copy_(v, non_blocking=True)
+
+    def forward_backward(self, u: torch.Tensor, v: torch.Tensor, step: int, stream=None):
+        self.load_inputs(u, v)
+        self._step_body(stream, step)
+
+    def train_step(self, u: torch.Tensor, v: torch.Tensor, step: int, stream=None):
+        self.forward_backward(u, v, step, stream)
+        self.optimizer_step(stream)

@@ -218,7 +218,38 @@ def test_adam_kernel_parity(torch_cuda):
         g = rng.standard_normal(n).astype(np.float32)
         gt = torch.from_numpy(g).cuda()
         call("gsb_adam_step", C.c_void_p(p.data_ptr()), C.c_void_p(gt.data_ptr()), C.c_void_p(m.data_ptr()),
-             C.c_void_p(v.data_ptr()), n, 0.01, 0.9, 0.999, 1e-8, t, None)
+             C.c_void_p(v.data_ptr()), n, 0.01, 0.9, 0.999, 1e-8, t, None, None)
         oracle.adam(pd, g, md, vd, 0.01, t)
     torch.cuda.synchronize()
     close(p.cpu().numpy(), pd, what="adam")
+
+
+def test_cuda_graph_replay_matches_oracle(torch_cuda):
+    """A whole step captured once in a CUDA graph and replayed: the step word and Adam t
+    advance on the device; the replayed step's blocks are bit-exact and its loss and
+    gradients match the oracle (the graph path is the one bench.py times)."""
+    import torch
+    cfg = synth.scaled(synth.mag(), 0.01, "mag_small")
+    st, og = gpu_store(cfg), oracle_graph(cfg)
+    tr = _gpu_trainer(cfg, st)
+    tr.load_inputs(torch.from_numpy(synth.nc_seeds(cfg, 0)).cuda())
+    tr.capture(step0=0)                       # capture runs nothing; replays run the steps
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    opt = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}
+    labels = synth.labels(cfg)
+    for step in range(3):
+        seeds = synth.nc_seeds(cfg, step)
+        tr.load_inputs(torch.from_numpy(seeds).cuda())
+        for k in synth.param_order(cfg):   # re-sync from the oracle state (see test_nc_step_parity)
+            tr.pview(k).copy_(torch.from_numpy(params[k].astype(np.float32)))
+            tr.pview(k, "m").copy_(torch.from_numpy(opt[k]["m"].astype(np.float32)))
+            tr.pview(k, "v").copy_(torch.from_numpy(opt[k]["v"].astype(np.float32)))
+        tr.replay()
+        torch.cuda.synchronize()
+        assert int(tr.counters[0].item()) == step + 1 and int(tr.counters[1].item()) == step + 1
+        res = oracle.nc_step(og, params, seeds, labels, step, cfg.rng_seed)
+        _compare_blocks(cfg, st, tr.sampler, res.blocks)
+        close(tr.loss.cpu().numpy()[0], res.loss, what=f"graph step {step} loss")
+        for k in synth.param_order(cfg):
+            close(tr.pview(k, "g").cpu().numpy(), res.grads[k], what=f"graph step {step} grad {k}")
+            oracle.adam(params[k], res.grads[k], opt[k]["m"], opt[k]["v"], cfg.lr, step + 1)
