@@ -139,29 +139,26 @@ def peaks():
 
 
 def kernel_work(name: str, sz: dict, cfg: synth.Config):
-    """Algorithmic bytes (HBM-bound kernels) or flops (GEMMs) of ONE launch of `name` for
-    a step with block sizes sz (per-unit figures)."""
+    """Algorithmic bytes (HBM-bound kernels) or flops (GEMMs) of ONE launch of `name` for a
+    step with block sizes sz (DESIGN.md §6 per-unit figures x units of the launch)."""
     d0, hd, C = cfg.feat_dim, cfg.hidden, cfg.num_classes
     L = len(cfg.fanouts)
+    lay = None
+    if name[-3:-1] == "_l" and name[-1].isdigit():
+        lay = int(name[-1])
+        name = name[:-3]
     if name == "gather":
         n = sz["n_src"][0]
         return "bytes", n * d0 * 4 * 2 + n * 8
-    if name == "rgcn_agg":
-        # per launch: average over the layers it ran for (caller divides); return the sum
-        tot = 0
-        for l in range(L):
-            d = d0 if l == 0 else hd
-            tot += sz["n_edges"][l] * (d * 4 + 4) + sz["n_dst"][l] * d * 4 + sz["acat_cols"][l] * 4
-        return "bytes", tot / L
-    if name in ("rgcn_gemm_fwd", "rgcn_gemm_dW"):
-        tot = 0
-        for l in range(L):
-            d = d0 if l == 0 else hd
-            tot += 2 * sz["acat_cols"][l] // d * d * hd
-        return "flops", tot / L
-    if name == "rgcn_gemm_dA":
-        l = L - 1
-        return "flops", 2 * sz["acat_cols"][l] * hd
+    if name == "rgcn_agg" and lay is not None:
+        d = d0 if lay == 0 else hd
+        # per sampled edge: one d-float source row + its index; per dst row: self row + Acat row
+        idx = 12 if lay == 0 else 4
+        return "bytes", sz["n_edges"][lay] * (d * 4 + idx) + sz["n_dst"][lay] * d * 4 + sz["acat_cols"][lay] * 4
+    if name in ("rgcn_gemm_fwd", "rgcn_gemm_dW") and lay is not None:
+        return "flops", 2 * sz["acat_cols"][lay] * hd
+    if name == "rgcn_gemm_dA" and lay is not None:
+        return "flops", 2 * sz["acat_cols"][lay] * hd
     if name in ("nc_logits", "nc_gemm_dWc", "nc_gemm_dh"):
         return "flops", 2 * cfg.batch * hd * C
     return None, None

@@ -204,6 +204,8 @@ gsb_status gsb_blocks_dst_rows(gsb_blocks_t b, int32_t layer, int64_t* max_rows)
  * computed as a per-relation segment mean followed by one grouped GEMM per dst type over
  * the concatenation Acat_v = [A_{r_0}[v] | ... | A_{r_{S_t-1}}[v] | h_src[self(v)]].
  * d_in must be a multiple of 32 and d_out a multiple of 4.
+ * h_src == NULL (layer 0 only): source rows are read straight from the registered feature
+ * tables by global id -- the feature gather (§8(a) a5) fused into the aggregation.
  * acat: device fp32 cache [gsb_layer_acat_floats] (kept for the backward).
  * ==================================================================================== */
 gsb_status gsb_layer_acat_floats(gsb_blocks_t b, int32_t layer, int32_t d_in, int64_t* n_floats);
@@ -216,9 +218,10 @@ gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, 
  *   dW_r = sum_v A_r[v]^T dZ_v ; dW_self = sum_v h_src[self(v)]^T dZ_v ; db = sum_v dZ_v
  *   dh_src[u] += (1/c_r(v)) dZ_v W_r^T per sampled edge ; dh_src[self(v)] += dZ_v W_self^T
  * dW [R+1][d_in][d_out] and db [d_out] are overwritten; dh_src [n_src][d_in] is
- * overwritten when non-NULL (then dacat_ws [acat floats] is scratch). */
+ * overwritten when non-NULL (then dacat_ws [acat floats] is scratch).  With relu, dh_dst
+ * is overwritten in place by dZ. */
 gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_dst,
-                              const float* dh_dst, const float* W, const float* acat, int32_t d_in, int32_t d_out,
+                              float* dh_dst, const float* W, const float* acat, int32_t d_in, int32_t d_out,
                               int32_t relu, float* dW, float* db, float* dh_src, float* dacat_ws, void* stream);
 
 /* Plain GEMM on the same tcgen05 3xTF32 path as the layers (single group), fp32 row-major:

@@ -54,6 +54,7 @@ def lib():
             "oracle_sample_hop": (i64, [P, P, i64, i32, u64, u32, i32, P, P, i64, i32, i32, P, P, P, P, P, i64]),
             "oracle_relabel": (i64, [P, P, i64, P, i64, P, P, P, P, i64]),
             "oracle_gather": (None, [P, P, i32, P, i64, P]),
+            "oracle_rgcn_means": (None, [i64, i32, i32, P, P, P, i64, P, P, P]),
             "oracle_rgcn_fwd": (None, [i64, i32, i32, i32, P, P, P, i64, P, P, P, P, i32, P, P]),
             "oracle_rgcn_bwd": (None, [i64, i64, i32, i32, i32, P, P, P, i64, P, P, P, P, i32, P, P, P, P]),
             "oracle_nc_loss": (dbl, [i64, i32, i32, P, P, P, P, P, P, P, P]),
@@ -244,6 +245,18 @@ def rgcn_fwd(blk: Block, R: int, h_src: np.ndarray, W: np.ndarray, b: np.ndarray
     return z, h
 
 
+def rgcn_means(blk: Block, R: int, h_src):
+    """Per-relation sampled means A (n_dst, R, d_in) and counts c (n_dst, R)."""
+    h_src = _c(h_src, np.float64)
+    n = len(blk.dst_gid)
+    d_in = h_src.shape[1]
+    c = np.zeros((n, R), np.int64)
+    A = np.zeros((n, R, d_in))
+    lib().oracle_rgcn_means(n, R, d_in, _p(_c(blk.e_dst, np.int64)), _p(_c(blk.e_etype, np.int32)),
+                            _p(_c(blk.e_src, np.int32)), len(blk.e_dst), _p(h_src), _p(c), _p(A))
+    return A, c
+
+
 def rgcn_bwd(blk: Block, R: int, h_src, W, z, relu: bool, dh_dst, need_dh_src: bool):
     h_src = _c(h_src, np.float64)
     W = _c(W, np.float64)
@@ -332,12 +345,14 @@ def nc_step(g: Graph, params: Dict[str, np.ndarray], seeds: np.ndarray, labels: 
     y = labels[seeds - g.node_off[cfg.target_ntype]]
     loss, logits, dh, dWc, dbc = nc_loss(h, params["Wc"], params["bc"], y)
     grads = {"Wc": dWc, "bc": dbc}
+    dhs = [None] * L
     for l in reversed(range(L)):
+        dhs[l] = dh
         dW, db, dh = rgcn_bwd(blocks[l], g.R, ins[l], params[f"W{l}"], zs[l], relu=(l < L - 1),
                               dh_dst=dh, need_dh_src=(l > 0))
         grads[f"W{l}"] = dW
         grads[f"b{l}"] = db
-    return StepResult(loss, blocks, x0, hs, zs, grads, {"logits": logits})
+    return StepResult(loss, blocks, x0, hs, zs, grads, {"logits": logits, "dh": dhs, "ins": ins})
 
 
 def lp_seeds(u: np.ndarray, v: np.ndarray, neg: np.ndarray) -> np.ndarray:
@@ -371,12 +386,15 @@ def lp_step(g: Graph, params: Dict[str, np.ndarray], u: np.ndarray, v: np.ndarra
     np.add.at(dh, iv, dhv)
     np.add.at(dh, ineg, dhn)
     grads = {"rel": drel}
+    dhs = [None] * L
     for l in reversed(range(L)):
+        dhs[l] = dh
         dW, db, dh = rgcn_bwd(blocks[l], g.R, ins[l], params[f"W{l}"], zs[l], relu=(l < L - 1),
                               dh_dst=dh, need_dh_src=(l > 0))
         grads[f"W{l}"] = dW
         grads[f"b{l}"] = db
-    return StepResult(loss, blocks, x0, hs, zs, grads, {"neg": neg, "seeds": seeds, "scores": scores})
+    return StepResult(loss, blocks, x0, hs, zs, grads, {"neg": neg, "seeds": seeds, "scores": scores, "dh": dhs,
+                                                        "ins": ins})
 
 
 def train_step(g: Graph, params: Dict[str, np.ndarray], opt: Dict[str, Dict[str, np.ndarray]], t: int,

@@ -381,6 +381,13 @@ static void rel_means(int64_t n_dst, int32_t R, int32_t d_in, const int64_t* e_d
         }
 }
 
+/* Exposed for tests: the per-relation means A[v][r][:] and counts c[v][r] (section 6). */
+void oracle_rgcn_means(int64_t n_dst, int32_t R, int32_t d_in, const int64_t* e_dst, const int32_t* e_et,
+                       const int32_t* e_src, int64_t E, const double* h_src, int64_t* c, double* A) {
+    rel_counts(n_dst, R, e_dst, e_et, E, c);
+    rel_means(n_dst, R, d_in, e_dst, e_et, e_src, E, c, h_src, A);
+}
+
 void oracle_rgcn_fwd(int64_t n_dst, int32_t R, int32_t d_in, int32_t d_out,
                      const int64_t* e_dst, const int32_t* e_et, const int32_t* e_src, int64_t E,
                      const int64_t* self_row, const double* h_src, const double* W, const double* b,

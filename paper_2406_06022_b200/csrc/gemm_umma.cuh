@@ -41,16 +41,38 @@ struct UProb {
 
 constexpr int UM_THREADS = 256;
 constexpr int UM_PANEL = 16384;            // bytes of one 128 x 32 fp32/tf32 panel
-constexpr int UM_STAGE = 4 * UM_PANEL;     // A_hi, A_lo, B_hi, B_lo
-constexpr int UM_STAGES = 2;
+constexpr int UM_STAGE = 4 * UM_PANEL;     // A_hi(raw), A_lo, B_hi(raw), B_lo
+constexpr int UM_STAGES = 3;
 constexpr int UM_SMEM = UM_STAGES * UM_STAGE + 1024;
 
-__device__ __forceinline__ float4 ld4(const float* p, bool vec) {
-    if (vec) return __ldg(reinterpret_cast<const float4*>(p));
-    return make_float4(__ldg(p), __ldg(p + 1), __ldg(p + 2), __ldg(p + 3));
+// ---- cp.async (LDGSTS) with zero fill ------------------------------------------------
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp4(uint32_t dst, const void* src, int bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Copy the 4 elements [c, c+4) of row `row` (cols >= ncols, rows out of range -> 0) to dst.
+__device__ __forceinline__ void cp_chunk(uint32_t dst, const float* base, int64_t ld, int64_t row, bool row_ok,
+                                         int64_t c, int64_t ncols, bool vec) {
+    const float* src = base + (row_ok ? row * ld : 0);
+    const int64_t valid = row_ok ? max((int64_t)0, min((int64_t)4, ncols - c)) : 0;
+    if (vec) {
+        cp16(dst, valid > 0 ? (const void*)(src + c) : (const void*)base, (int)(4 * valid));
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cp4(dst + 4 * q, q < valid ? (const void*)(src + c + q) : (const void*)base,
+                                        q < valid ? 4 : 0);
+    }
 }
 
-__device__ __forceinline__ void st_split(uint8_t* hi, uint8_t* lo, uint32_t off, float4 v) {
+// in-place split of one staged 16-B chunk: hi (rna tf32) overwrites the raw value, lo goes to lo
+__device__ __forceinline__ float4 split_chunk(uint8_t* hi, uint8_t* lo, uint32_t off) {
+    float4 v = *reinterpret_cast<float4*>(hi + off);
     uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
     umma::split_tf32(v.x, h0, l0);
     umma::split_tf32(v.y, h1, l1);
@@ -58,29 +80,142 @@ __device__ __forceinline__ void st_split(uint8_t* hi, uint8_t* lo, uint32_t off,
     umma::split_tf32(v.w, h3, l3);
     *reinterpret_cast<uint4*>(hi + off) = make_uint4(h0, h1, h2, h3);
     *reinterpret_cast<uint4*>(lo + off) = make_uint4(l0, l1, l2, l3);
+    return v;
 }
 
-// masked load of 4 consecutive elements [c, c+4) of row `row` (cols >= ncols -> 0)
-__device__ __forceinline__ float4 load4(const float* base, int64_t ld, int64_t row, int64_t c, int64_t ncols, bool vec,
-                                        const float* mask) {
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (c + 3 < ncols) {
-        v = ld4(base + row * ld + c, vec);
-        if (mask) {
-            float4 h = ld4(mask + row * ld + c, vec);
-            v.x = h.x > 0.f ? v.x : 0.f; v.y = h.y > 0.f ? v.y : 0.f;
-            v.z = h.z > 0.f ? v.z : 0.f; v.w = h.w > 0.f ? v.w : 0.f;
-        }
-    } else if (c < ncols) {
-        float e[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int q = 0; q < 4 && c + q < ncols; ++q) {
-            float x = __ldg(base + row * ld + c + q);
-            if (mask && __ldg(mask + row * ld + c + q) <= 0.f) x = 0.f;
-            e[q] = x;
-        }
-        v = make_float4(e[0], e[1], e[2], e[3]);
+// One (tile, panel) position of this CTA's persistent schedule.
+struct UCursor {
+    int64_t tile;          // >= total: exhausted
+    int p, KP;
+    int t, s, c0, n0;
+    int64_t row0, rlim;
+};
+
+template <int MODE>
+__device__ __forceinline__ int64_t tiles_of_group(const UProb& P, int t, int64_t r0, int64_t r1, int nct, int kct) {
+    if (MODE == UMMA_NN) return ((r1 - r0 + 127) / 128) * nct;
+    if (MODE == UMMA_NT) return ((r1 - r0 + 127) / 128) * kct * P.rg.ks[t];
+    return ((r1 - r0 + P.rows_per_chunk - 1) / P.rows_per_chunk) * P.rg.ks[t] * kct * nct;
+}
+
+template <int MODE>
+__device__ __forceinline__ void decode_tile(const UProb& P, int64_t tile, int nct, int kct, UCursor& c) {
+    const RowGroups& rg = P.rg;
+    int t = 0;
+    int64_t rem = tile, r0 = 0, r1 = 0;
+    for (;; ++t) {
+        group_rows(rg, t, r0, r1);
+        const int64_t nt = tiles_of_group<MODE>(P, t, r0, r1, nct, kct);
+        if (rem < nt) break;
+        rem -= nt;
     }
-    return v;
+    c.t = t;
+    c.s = 0; c.c0 = 0; c.n0 = 0;
+    if (MODE == UMMA_NN) {
+        c.row0 = r0 + (rem / nct) * 128;
+        c.rlim = r1;
+        c.n0 = (int)(rem % nct) * 128;
+        c.KP = rg.ks[t] * (P.d_in / 32);
+    } else if (MODE == UMMA_NT) {
+        const int per = kct * rg.ks[t];
+        c.row0 = r0 + (rem / per) * 128;
+        c.rlim = r1;
+        const int q = (int)(rem % per);
+        c.s = q / kct;
+        c.c0 = (q % kct) * 128;
+        c.KP = (P.N + 31) / 32;
+    } else {
+        const int per = rg.ks[t] * kct * nct;
+        c.row0 = r0 + (rem / per) * P.rows_per_chunk;
+        c.rlim = min(r1, c.row0 + (int64_t)P.rows_per_chunk);
+        int q = (int)(rem % per);
+        c.s = q / (kct * nct);
+        q -= c.s * kct * nct;
+        c.c0 = (q / nct) * 128;
+        c.n0 = (q % nct) * 128;
+        c.KP = (int)((c.rlim - c.row0 + 31) / 32);
+    }
+    c.p = 0;
+}
+
+// issue this thread's cp.async copies of panel c.p into stage buffers (A: 4 chunks, B: 4 chunks)
+template <int MODE>
+__device__ __forceinline__ void issue_panel(const UProb& P, const UCursor& c, uint8_t* stage, int tid, bool vecA,
+                                            bool vecB) {
+    const uint32_t Ahi = umma::smem_u32(stage), Bhi = umma::smem_u32(stage + 2 * UM_PANEL);
+    if (MODE == UMMA_NN) {
+        const int per = P.d_in / 32;
+        const int sp = c.p / per;
+        const int kk = (c.p - sp * per) * 32;
+        const int64_t acol = (int64_t)sp * P.d_in + kk;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = (tid >> 3) + 32 * i, ch = tid & 7;
+            const int64_t row = c.row0 + r;
+            cp_chunk(Ahi + umma::kmajor_off(r, 4 * ch), P.A, P.lda, row, row < c.rlim, acol + 4 * ch, acol + 32, vecA);
+        }
+        const float* W = P.B + (int64_t)P.rg.slot_w[c.t][sp] * P.bslot;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int kr = (tid >> 5) + 8 * i, j = tid & 31;
+            cp_chunk(Bhi + umma::mnmajor_off(4 * j, kr), W, P.ldb, kk + kr, true, c.n0 + 4 * j, P.N, vecB);
+        }
+    } else if (MODE == UMMA_NT) {
+        const int nn = c.p * 32;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = (tid >> 3) + 32 * i, ch = tid & 7;
+            const int64_t row = c.row0 + r;
+            cp_chunk(Ahi + umma::kmajor_off(r, 4 * ch), P.A, P.lda, row, row < c.rlim, nn + 4 * ch, P.N, vecA);
+        }
+        const float* W = P.B + (int64_t)P.rg.slot_w[c.t][c.s] * P.bslot;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = (tid >> 3) + 32 * i, ch = tid & 7;
+            const int k = c.c0 + r;
+            cp_chunk(Bhi + umma::kmajor_off(r, 4 * ch), W, P.ldb, k, k < P.d_in, nn + 4 * ch, P.N, vecB);
+        }
+    } else {
+        const int64_t rb = c.row0 + (int64_t)c.p * 32;
+        const int64_t acol = (int64_t)c.s * P.d_in + c.c0;
+        const int64_t alim = (int64_t)c.s * P.d_in + P.d_in;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int kr = (tid >> 5) + 8 * i, j = tid & 31;
+            const int64_t row = rb + kr;
+            cp_chunk(Ahi + umma::mnmajor_off(4 * j, kr), P.A, P.lda, row, row < c.rlim, acol + 4 * j, alim, vecA);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int kr = (tid >> 5) + 8 * i, j = tid & 31;
+            const int64_t row = rb + kr;
+            cp_chunk(Bhi + umma::mnmajor_off(4 * j, kr), P.B, P.ldb, row, row < c.rlim, c.n0 + 4 * j, P.N, vecB);
+        }
+    }
+}
+
+// split this thread's own chunks (the ones it issued) of a landed stage
+template <int MODE>
+__device__ __forceinline__ float4 split_panel(uint8_t* stage, int tid) {
+    uint8_t* Ahi = stage;
+    uint8_t* Alo = stage + UM_PANEL;
+    uint8_t* Bhi = stage + 2 * UM_PANEL;
+    uint8_t* Blo = stage + 3 * UM_PANEL;
+    float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t oa = (MODE == UMMA_TN) ? umma::mnmajor_off(4 * (tid & 31), (tid >> 5) + 8 * i)
+                                              : umma::kmajor_off((tid >> 3) + 32 * i, 4 * (tid & 7));
+        split_chunk(Ahi, Alo, oa);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t ob = (MODE == UMMA_NT) ? umma::kmajor_off((tid >> 3) + 32 * i, 4 * (tid & 7))
+                                              : umma::mnmajor_off(4 * (tid & 31), (tid >> 5) + 8 * i);
+        float4 v = split_chunk(Bhi, Blo, ob);
+        cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w;
+    }
+    return cs;
 }
 
 template <int MODE>
@@ -109,166 +244,96 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
     const bool vecA = ((P.lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(P.A) & 15) == 0);
     const bool vecB = ((P.ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(P.B) & 15) == 0);
 
-    // ---- tile enumeration
-    const int nct = (P.N + 127) / 128;          // NN/TN: output col tiles over N
-    const int kct = (P.d_in + 127) / 128;       // NT: col tiles per slot; TN: row tiles over d_in
+    const int nct = (P.N + 127) / 128;
+    const int kct = (P.d_in + 127) / 128;
     int64_t total = 0;
     for (int t = 0; t < rg.G; ++t) {
         int64_t r0, r1;
         group_rows(rg, t, r0, r1);
-        if (MODE == UMMA_NN) total += ((r1 - r0 + 127) / 128) * nct;
-        else if (MODE == UMMA_NT) total += ((r1 - r0 + 127) / 128) * kct * rg.ks[t];
-        else total += ((r1 - r0 + P.rows_per_chunk - 1) / P.rows_per_chunk) * rg.ks[t] * kct * nct;
+        total += tiles_of_group<MODE>(P, t, r0, r1, nct, kct);
     }
 
-    uint32_t phase[UM_STAGES] = {0, 0};
-    bool pend[UM_STAGES] = {false, false};
-    int64_t it = 0;
-
-    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        // ---- decode
-        int t = 0;
-        int64_t rem = tile, r0 = 0, r1 = 0;
-        for (;; ++t) {
-            group_rows(rg, t, r0, r1);
-            int64_t nt;
-            if (MODE == UMMA_NN) nt = ((r1 - r0 + 127) / 128) * nct;
-            else if (MODE == UMMA_NT) nt = ((r1 - r0 + 127) / 128) * kct * rg.ks[t];
-            else nt = ((r1 - r0 + P.rows_per_chunk - 1) / P.rows_per_chunk) * rg.ks[t] * kct * nct;
-            if (rem < nt) break;
-            rem -= nt;
+    // two cursors over the same (tile, panel) sequence: loads run UM_STAGES-1 panels ahead
+    UCursor ld, cp;
+    ld.tile = blockIdx.x;
+    if (ld.tile < total) decode_tile<MODE>(P, ld.tile, nct, kct, ld);
+    cp = ld;
+    auto advance = [&](UCursor& c) {
+        if (c.tile >= total) return;
+        if (++c.p >= c.KP) {
+            c.tile += gridDim.x;
+            if (c.tile < total) decode_tile<MODE>(P, c.tile, nct, kct, c);
         }
-        int64_t row0 = 0, rlim = 0;   // NN/NT: output rows [row0, rlim); TN: reduction rows
-        int s = 0, c0 = 0, n0 = 0, KP = 0;
-        if (MODE == UMMA_NN) {
-            row0 = r0 + (rem / nct) * 128;
-            rlim = r1;
-            n0 = (int)(rem % nct) * 128;
-            KP = rg.ks[t] * (P.d_in / 32);
-        } else if (MODE == UMMA_NT) {
-            const int per = kct * rg.ks[t];
-            row0 = r0 + (rem / per) * 128;
-            rlim = r1;
-            const int q = (int)(rem % per);
-            s = q / kct;
-            c0 = (q % kct) * 128;
-            KP = (P.N + 31) / 32;
-        } else {
-            const int per = rg.ks[t] * kct * nct;
-            row0 = r0 + (rem / per) * P.rows_per_chunk;
-            rlim = min(r1, row0 + (int64_t)P.rows_per_chunk);
-            int q = (int)(rem % per);
-            s = q / (kct * nct);
-            q -= s * kct * nct;
-            c0 = (q / nct) * 128;   // k offset inside the slot
-            n0 = (q % nct) * 128;
-            KP = (int)((rlim - row0 + 31) / 32);
+    };
+    uint32_t phase[UM_STAGES] = {0, 0, 0};
+    bool pend[UM_STAGES] = {false, false, false};
+    int64_t it_ld = 0, it_cp = 0;
+    auto wait_stage = [&](int st) {
+        if (pend[st]) {
+            umma::mbar_wait(&bars[st], phase[st]);
+            phase[st] ^= 1;
+            pend[st] = false;
         }
-        const bool do_db = (MODE == UMMA_TN) && P.db && (s == rg.ks[t] - 1) && c0 == 0;
-        float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
-
-        for (int p = 0; p < KP; ++p, ++it) {
-            const int st = (int)(it & 1);
-            if (pend[st]) {
-                umma::mbar_wait(&bars[st], phase[st]);
-                phase[st] ^= 1;
-                pend[st] = false;
-            }
-            uint8_t* Ahi = smem + st * UM_STAGE;
-            uint8_t* Alo = Ahi + UM_PANEL;
-            uint8_t* Bhi = Alo + UM_PANEL;
-            uint8_t* Blo = Bhi + UM_PANEL;
-            // ---- stage operands
-            if (MODE == UMMA_NN) {
-                const int sp = p / (P.d_in / 32);
-                const int kk = (p - sp * (P.d_in / 32)) * 32;
-                const int64_t acol = (int64_t)sp * P.d_in + kk;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {           // A: 128 rows x 8 chunks, K-major
-                    const int r = (tid >> 3) + 32 * i, c = tid & 7;
-                    const int64_t row = row0 + r;
-                    float4 v = (row < rlim) ? load4(P.A, P.lda, row, acol + 4 * c, acol + 32, vecA, nullptr)
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-                    st_split(Ahi, Alo, umma::kmajor_off(r, 4 * c), v);
-                }
-                const float* W = P.B + (int64_t)rg.slot_w[t][sp] * P.bslot;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {           // B: rows k of W, MN = n, MN-major
-                    const int kr = (tid >> 5) + 8 * i, j = tid & 31;
-                    float4 v = load4(W, P.ldb, kk + kr, n0 + 4 * j, P.N, vecB, nullptr);
-                    st_split(Bhi, Blo, umma::mnmajor_off(4 * j, kr), v);
-                }
-            } else if (MODE == UMMA_NT) {
-                const int nn = p * 32;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {           // A: dZ rows, K = n, K-major
-                    const int r = (tid >> 3) + 32 * i, c = tid & 7;
-                    const int64_t row = row0 + r;
-                    float4 v = (row < rlim) ? load4(P.A, P.lda, row, nn + 4 * c, P.N, vecA, P.relu ? P.H : nullptr)
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-                    st_split(Ahi, Alo, umma::kmajor_off(r, 4 * c), v);
-                }
-                const float* W = P.B + (int64_t)rg.slot_w[t][s] * P.bslot;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {           // B: rows k of W (N' = k), K = n, K-major
-                    const int r = (tid >> 3) + 32 * i, c = tid & 7;
-                    const int k = c0 + r;
-                    float4 v = (k < P.d_in) ? load4(W, P.ldb, k, nn + 4 * c, P.N, vecB, nullptr)
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-                    st_split(Bhi, Blo, umma::kmajor_off(r, 4 * c), v);
-                }
-            } else {
-                const int64_t rb = row0 + (int64_t)p * 32;
-                const int64_t acol = (int64_t)s * P.d_in + c0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {           // A': MN = k (Acat cols), K = rows, MN-major
-                    const int kr = (tid >> 5) + 8 * i, j = tid & 31;
-                    const int64_t row = rb + kr;
-                    float4 v = (row < rlim) ? load4(P.A, P.lda, row, acol + 4 * j, (int64_t)s * P.d_in + P.d_in, vecA,
-                                                    nullptr)
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-                    st_split(Ahi, Alo, umma::mnmajor_off(4 * j, kr), v);
-                }
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {           // B': MN = n (dZ cols), K = rows, MN-major
-                    const int kr = (tid >> 5) + 8 * i, j = tid & 31;
-                    const int64_t row = rb + kr;
-                    float4 v = (row < rlim) ? load4(P.B, P.ldb, row, n0 + 4 * j, P.N, vecB, P.relu ? P.H : nullptr)
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (do_db) { cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w; }
-                    st_split(Bhi, Blo, umma::mnmajor_off(4 * j, kr), v);
-                }
-            }
-            umma::fence_proxy_async_smem();
-            __syncthreads();
-            if (tid == 0) {
-                umma::tc_fence_after();
-                const uint32_t a_hi = umma::smem_u32(Ahi), a_lo = umma::smem_u32(Alo);
-                const uint32_t b_hi = umma::smem_u32(Bhi), b_lo = umma::smem_u32(Blo);
-#pragma unroll
-                for (int ks = 0; ks < 4; ++ks) {
-                    const uint32_t oa = A_MN ? ks * 4096u : ks * 32u;
-                    const uint32_t ob = B_MN ? ks * 4096u : ks * 32u;
-                    const uint64_t dah = A_MN ? umma::desc_mnmajor(a_hi + oa) : umma::desc_kmajor(a_hi + oa);
-                    const uint64_t dal = A_MN ? umma::desc_mnmajor(a_lo + oa) : umma::desc_kmajor(a_lo + oa);
-                    const uint64_t dbh = B_MN ? umma::desc_mnmajor(b_hi + ob) : umma::desc_kmajor(b_hi + ob);
-                    const uint64_t dbl = B_MN ? umma::desc_mnmajor(b_lo + ob) : umma::desc_kmajor(b_lo + ob);
-                    umma::mma_tf32(tmem, dal, dbh, IDESC, (p > 0 || ks > 0) ? 1u : 0u);
-                    umma::mma_tf32(tmem, dah, dbl, IDESC, 1u);
-                    umma::mma_tf32(tmem, dah, dbh, IDESC, 1u);
-                }
-                umma::mma_commit(&bars[st]);
-            }
-            pend[st] = true;
+    };
+    // prologue
+    for (int k = 0; k < UM_STAGES - 1; ++k) {
+        if (ld.tile < total) {
+            issue_panel<MODE>(P, ld, smem + (it_ld % UM_STAGES) * UM_STAGE, tid, vecA, vecB);
+            advance(ld);
         }
-        // ---- drain the MMAs of this tile (older stage first)
+        cp_commit();
+        ++it_ld;
+    }
+    float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
+    while (cp.tile < total) {
+        // keep the copy engine UM_STAGES-1 panels ahead (stage reuse waits for its MMAs)
         {
-            const int last = (int)((it - 1) & 1), other = last ^ 1;
-            if (pend[other]) { umma::mbar_wait(&bars[other], phase[other]); phase[other] ^= 1; pend[other] = false; }
-            if (pend[last]) { umma::mbar_wait(&bars[last], phase[last]); phase[last] ^= 1; pend[last] = false; }
+            const int st = (int)(it_ld % UM_STAGES);
+            wait_stage(st);
+            if (ld.tile < total) {
+                issue_panel<MODE>(P, ld, smem + st * UM_STAGE, tid, vecA, vecB);
+                advance(ld);
+            }
+            cp_commit();
+            ++it_ld;
         }
+        cp_wait<UM_STAGES - 1>();
+        const int st = (int)(it_cp % UM_STAGES);
+        uint8_t* stage = smem + st * UM_STAGE;
+        const bool do_db = (MODE == UMMA_TN) && P.db && (cp.s == rg.ks[cp.t] - 1) && cp.c0 == 0;
+        {
+            float4 v = split_panel<MODE>(stage, tid);
+            if (do_db) { cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w; }
+        }
+        umma::fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            umma::tc_fence_after();
+            const uint32_t a_hi = umma::smem_u32(stage), a_lo = a_hi + UM_PANEL;
+            const uint32_t b_hi = a_hi + 2 * UM_PANEL, b_lo = a_hi + 3 * UM_PANEL;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const uint32_t oa = A_MN ? ks * 4096u : ks * 32u;
+                const uint32_t ob = B_MN ? ks * 4096u : ks * 32u;
+                const uint64_t dah = A_MN ? umma::desc_mnmajor(a_hi + oa) : umma::desc_kmajor(a_hi + oa);
+                const uint64_t dal = A_MN ? umma::desc_mnmajor(a_lo + oa) : umma::desc_kmajor(a_lo + oa);
+                const uint64_t dbh = B_MN ? umma::desc_mnmajor(b_hi + ob) : umma::desc_kmajor(b_hi + ob);
+                const uint64_t dbl = B_MN ? umma::desc_mnmajor(b_lo + ob) : umma::desc_kmajor(b_lo + ob);
+                umma::mma_tf32(tmem, dal, dbh, IDESC, (cp.p > 0 || ks > 0) ? 1u : 0u);
+                umma::mma_tf32(tmem, dah, dbl, IDESC, 1u);
+                umma::mma_tf32(tmem, dah, dbh, IDESC, 1u);
+            }
+            umma::mma_commit(&bars[st]);
+        }
+        pend[st] = true;
+        ++it_cp;
+        if (cp.p + 1 < cp.KP) {
+            advance(cp);
+            continue;
+        }
+        // ---- last panel of the tile: drain its MMAs, then the epilogue
+        for (int k = 1; k <= UM_STAGES; ++k) wait_stage((int)((it_cp - 1 + k) % UM_STAGES));   // oldest first
         umma::tc_fence_after();
-        // ---- epilogue: warp w reads TMEM lanes 32*(w&3).., columns half (w>>2)*64
         {
             const int q = warp & 3, half = warp >> 2;
             const int r = q * 32 + lane;
@@ -278,13 +343,13 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
                 float v[32];
                 umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)col, v);
                 if (MODE == UMMA_NN) {
-                    const int64_t row = row0 + r;
-                    if (row < rlim) {
+                    const int64_t row = cp.row0 + r;
+                    if (row < cp.rlim) {
                         float* out = P.C + row * P.ldc;
                         const bool vec = ((P.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(P.C) & 15) == 0);
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
-                            const int n = n0 + col + e;
+                            const int n = cp.n0 + col + e;
                             float x[4];
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
@@ -300,23 +365,30 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
                         }
                     }
                 } else if (MODE == UMMA_NT) {
-                    const int64_t row = row0 + r;
-                    if (row < rlim) {
-                        float* out = P.C + row * P.ldc + (int64_t)s * P.d_in;
+                    const int64_t row = cp.row0 + r;
+                    if (row < cp.rlim) {
+                        float* out = P.C + row * P.ldc + (int64_t)cp.s * P.d_in;
+                        const bool vec = ((P.ldc & 3) == 0) && ((P.d_in & 3) == 0) &&
+                                         ((reinterpret_cast<uintptr_t>(P.C) & 15) == 0);
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) {
-                            const int k = c0 + col + e;
-                            if (k < P.d_in) out[k] = v[e];
+                        for (int e = 0; e < 32; e += 4) {
+                            const int k = cp.c0 + col + e;
+                            if (vec && k + 3 < P.d_in) {
+                                *reinterpret_cast<float4*>(out + k) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                            } else {
+                                for (int u = 0; u < 4; ++u)
+                                    if (k + u < P.d_in) out[k + u] = v[e + u];
+                            }
                         }
                     }
                 } else {
-                    const int k = c0 + r;
+                    const int k = cp.c0 + r;
                     if (k < P.d_in) {
-                        float* out = P.C + (int64_t)rg.slot_w[t][s] * P.bslot + (int64_t)k * P.ldc;
+                        float* out = P.C + (int64_t)rg.slot_w[cp.t][cp.s] * P.bslot + (int64_t)k * P.ldc;
                         const bool vec = ((P.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
-                            const int n = n0 + col + e;
+                            const int n = cp.n0 + col + e;
                             if (vec && n + 3 < P.N) {
                                 red_add_f4(out + n, make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
                             } else {
@@ -328,7 +400,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
                 }
             }
         }
-        if (do_db) {   // column sums of dZ over the chunk (each thread owns 4 columns of 128)
+        if (do_db) {   // column sums of dZ over the chunk (thread owns columns 4*(tid&31)..+3)
             if (tid < 128) dbred[tid] = 0.f;
             __syncthreads();
             const int j = tid & 31;
@@ -337,11 +409,14 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
             atomicAdd(&dbred[4 * j + 2], cs.z);
             atomicAdd(&dbred[4 * j + 3], cs.w);
             __syncthreads();
-            if (tid < 128 && n0 + tid < P.N) atomicAdd(P.db + n0 + tid, dbred[tid]);
+            if (tid < 128 && cp.n0 + tid < P.N) atomicAdd(P.db + cp.n0 + tid, dbred[tid]);
         }
+        cs = make_float4(0.f, 0.f, 0.f, 0.f);
         umma::tc_fence_before();
         __syncthreads();
+        advance(cp);
     }
+    cp_wait<0>();
     umma::tc_fence_after();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc<128>(tmem);

@@ -11,9 +11,22 @@ namespace gsb {
 //   Acat[j, s*d + :] = mean_{e in seg(j,s)} h_src[e_src[e], :]    (0 when empty)
 //   Acat[j, S_t*d + :] = h_src[self(j), :]
 // ------------------------------------------------------------------------------------
+template <bool FEAT>
+__device__ __forceinline__ const float4* src_row(const GraphDev& g, const float* h, int d, int64_t row, int64_t gid) {
+    if (FEAT) {   // layer 0 reads the feature table by global id (fused gather, §8(a) a5)
+        const int t = type_of(g, gid);
+        return reinterpret_cast<const float4*>(g.feat[t] + (gid - g.node_off[t]) * d);
+    }
+    return reinterpret_cast<const float4*>(h + row * d);
+}
+
+// FEAT: h_src rows come from the feature tables via e_src_gid / dst_gid (no x0 buffer)
+template <bool FEAT>
 __global__ void __launch_bounds__(256) agg_kernel(GraphDev g, const HopMeta* __restrict__ m,
                                                   const int64_t* __restrict__ seg_ptr,
-                                                  const int32_t* __restrict__ e_src, const float* __restrict__ h,
+                                                  const int32_t* __restrict__ e_src,
+                                                  const int64_t* __restrict__ e_src_gid,
+                                                  const int64_t* __restrict__ dst_gid, const float* __restrict__ h,
                                                   int d, float* __restrict__ acat, int64_t lda) {
     const int lane = threadIdx.x & 31;
     const int S = g.S;
@@ -32,18 +45,18 @@ __global__ void __launch_bounds__(256) agg_kernel(GraphDev g, const HopMeta* __r
                 float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
                 int64_t e = e0;
                 for (; e + 4 <= e1; e += 4) {
-                    int32_t u0 = e_src[e], u1 = e_src[e + 1], u2 = e_src[e + 2], u3 = e_src[e + 3];
-                    float4 x0 = __ldg(reinterpret_cast<const float4*>(h + (int64_t)u0 * d) + c);
-                    float4 x1 = __ldg(reinterpret_cast<const float4*>(h + (int64_t)u1 * d) + c);
-                    float4 x2 = __ldg(reinterpret_cast<const float4*>(h + (int64_t)u2 * d) + c);
-                    float4 x3 = __ldg(reinterpret_cast<const float4*>(h + (int64_t)u3 * d) + c);
+                    const float4* p0 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e], FEAT ? e_src_gid[e] : 0);
+                    const float4* p1 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 1], FEAT ? e_src_gid[e + 1] : 0);
+                    const float4* p2 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 2], FEAT ? e_src_gid[e + 2] : 0);
+                    const float4* p3 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 3], FEAT ? e_src_gid[e + 3] : 0);
+                    float4 x0 = __ldg(p0 + c), x1 = __ldg(p1 + c), x2 = __ldg(p2 + c), x3 = __ldg(p3 + c);
                     acc.x += x0.x; acc.y += x0.y; acc.z += x0.z; acc.w += x0.w;
                     acc.x += x1.x; acc.y += x1.y; acc.z += x1.z; acc.w += x1.w;
                     acc.x += x2.x; acc.y += x2.y; acc.z += x2.z; acc.w += x2.w;
                     acc.x += x3.x; acc.y += x3.y; acc.z += x3.z; acc.w += x3.w;
                 }
                 for (; e < e1; ++e) {
-                    float4 x = __ldg(reinterpret_cast<const float4*>(h + (int64_t)e_src[e] * d) + c);
+                    float4 x = __ldg(src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e], FEAT ? e_src_gid[e] : 0) + c);
                     acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
                 }
                 acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
@@ -51,9 +64,8 @@ __global__ void __launch_bounds__(256) agg_kernel(GraphDev g, const HopMeta* __r
             }
         }
         const int64_t self = m->src_off[t] + (j - m->dst_off[t]);
-        for (int c = lane; c < d4; c += 32)
-            reinterpret_cast<float4*>(out + (int64_t)St * d)[c] =
-                __ldg(reinterpret_cast<const float4*>(h + self * d) + c);
+        const float4* ps = src_row<FEAT>(g, h, d, self, FEAT ? dst_gid[j] : 0);
+        for (int c = lane; c < d4; c += 32) reinterpret_cast<float4*>(out + (int64_t)St * d)[c] = __ldg(ps + c);
     }
 }
 
@@ -130,6 +142,34 @@ __global__ void __launch_bounds__(1024) mean_kernel(const float* __restrict__ x,
     }
 }
 
+// dZ = dh * 1[h > 0] in place (ReLU backward, ReLU'(0) = 0), rows = device dst count
+__global__ void __launch_bounds__(256) relu_bwd_kernel(const HopMeta* __restrict__ m, float* __restrict__ dh,
+                                                       const float* __restrict__ h, int d) {
+    const int64_t n4 = m->n_dst * (int64_t)d / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 g = reinterpret_cast<float4*>(dh)[i];
+        const float4 x = __ldg(reinterpret_cast<const float4*>(h) + i);
+        g.x = x.x > 0.f ? g.x : 0.f; g.y = x.y > 0.f ? g.y : 0.f;
+        g.z = x.z > 0.f ? g.z : 0.f; g.w = x.w > 0.f ? g.w : 0.f;
+        reinterpret_cast<float4*>(dh)[i] = g;
+    }
+}
+
+static const char* lname(const char* base, int layer) {
+    static const char* names[][4] = {
+        {"rgcn_agg_l0", "rgcn_agg_l1", "rgcn_agg_l2", "rgcn_agg_l3"},
+        {"rgcn_gemm_fwd_l0", "rgcn_gemm_fwd_l1", "rgcn_gemm_fwd_l2", "rgcn_gemm_fwd_l3"},
+        {"rgcn_gemm_dW_l0", "rgcn_gemm_dW_l1", "rgcn_gemm_dW_l2", "rgcn_gemm_dW_l3"},
+        {"rgcn_gemm_dA_l0", "rgcn_gemm_dA_l1", "rgcn_gemm_dA_l2", "rgcn_gemm_dA_l3"},
+        {"rgcn_scatter_l0", "rgcn_scatter_l1", "rgcn_scatter_l2", "rgcn_scatter_l3"},
+        {"relu_bwd_l0", "relu_bwd_l1", "relu_bwd_l2", "relu_bwd_l3"}};
+    int k = 0;
+    const char* keys[] = {"rgcn_agg", "rgcn_gemm_fwd", "rgcn_gemm_dW", "rgcn_gemm_dA", "rgcn_scatter", "relu_bwd"};
+    for (; k < 6; ++k)
+        if (strcmp(base, keys[k]) == 0) break;
+    return (k < 6 && layer >= 0 && layer < 4) ? names[k][layer] : base;
+}
+
 static RowGroups layer_groups(const Blocks* B, const void* arena, int layer) {
     RowGroups rg;
     memset(&rg, 0, sizeof(rg));
@@ -177,7 +217,8 @@ gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, 
                               const float* W, const float* bias, int32_t d_out, int32_t relu, float* h_dst,
                               float* acat, void* stream) {
     Blocks* B = reinterpret_cast<Blocks*>(b);
-    GSB_CHECK_ARG(B && arena && h_src && W && h_dst && acat, "null argument");
+    GSB_CHECK_ARG(B && arena && W && h_dst && acat, "null argument");
+    GSB_CHECK_ARG(h_src || layer == 0, "h_src may be NULL only for layer 0 (features read by gid)");
     GSB_CHECK_ARG(layer >= 0 && layer < B->L, "layer %d out of range", layer);
     GSB_CHECK_ARG(d_in > 0 && d_in % BK == 0, "d_in %d must be a multiple of %d", d_in, BK);
     GSB_CHECK_ARG(d_out > 0 && d_out % 4 == 0, "d_out %d must be a multiple of 4", d_out);
@@ -186,23 +227,30 @@ gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     HopBufs hb = B->hop(h, const_cast<void*>(arena));
     const GraphDev& g = B->g->dev;
     const int64_t lda = (int64_t)(g.S + 1) * d_in;
-    GSB_LAUNCH("rgcn_agg", agg_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g, hb.meta, hb.seg_ptr,
-               hb.e_src, h_src, d_in, acat, lda);
+    if (h_src) {
+        GSB_LAUNCH(lname("rgcn_agg", layer), agg_kernel<false>, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
+                   hb.seg_ptr, hb.e_src, hb.e_src_gid, hb.dst_gid, h_src, d_in, acat, lda);
+    } else {
+        GSB_CHECK_ARG(g.feat_dim == d_in, "layer 0 with features: d_in %d != feature dim %d", d_in, g.feat_dim);
+        for (int t = 0; t < g.T; ++t) GSB_CHECK_ARG(g.feat[t], "features of ntype %d not registered", t);
+        GSB_LAUNCH(lname("rgcn_agg", layer), agg_kernel<true>, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
+                   hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid, hb.dst_gid, (const float*)nullptr, d_in, acat, lda);
+    }
     RowGroups rg = layer_groups(B, arena, layer);
 #ifdef GSB_SIMT_GEMM
-    GSB_LAUNCH("rgcn_gemm_fwd", gemm_nn_kernel, gemm_grid(hb.cap_dst, (d_out + BN - 1) / BN, g.T), NT, 0, s, rg,
+    GSB_LAUNCH(lname("rgcn_gemm_fwd", layer), gemm_nn_kernel, gemm_grid(hb.cap_dst, (d_out + BN - 1) / BN, g.T), NT, 0, s, rg,
                acat, lda, W, d_in, d_out, (int64_t)d_out, (int64_t)d_in * d_out, bias, relu, h_dst, (int64_t)d_out);
     return GSB_OK;
 #else
     UProb P{};
     P.rg = rg; P.A = acat; P.lda = lda; P.B = W; P.ldb = d_out; P.bslot = (int64_t)d_in * d_out;
     P.relu = relu; P.d_in = d_in; P.N = d_out; P.C = h_dst; P.ldc = d_out; P.bias = bias;
-    return launch_umma<UMMA_NN>("rgcn_gemm_fwd", P, (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_out, 128), s);
+    return launch_umma<UMMA_NN>(lname("rgcn_gemm_fwd", layer), P, (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_out, 128), s);
 #endif
 }
 
 gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_dst,
-                              const float* dh_dst, const float* W, const float* acat, int32_t d_in, int32_t d_out,
+                              float* dh_dst, const float* W, const float* acat, int32_t d_in, int32_t d_out,
                               int32_t relu, float* dW, float* db, float* dh_src, float* dacat_ws, void* stream) {
     Blocks* B = reinterpret_cast<Blocks*>(b);
     GSB_CHECK_ARG(B && arena && dh_dst && W && acat && dW && db, "null argument");
@@ -218,12 +266,18 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     RowGroups rg = layer_groups(B, arena, layer);
     GSB_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)(g.R + 1) * d_in * d_out, s));
     GSB_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)d_out, s));
+#ifndef GSB_SIMT_GEMM
+    if (relu) {   // dZ once, in place; the GEMMs below then read dZ directly
+        GSB_LAUNCH(lname("relu_bwd", layer), relu_bwd_kernel, grid_for(hb.cap_dst * d_out / 4, 256, kNumSMs * 8), 256, 0, s,
+                   hb.meta, dh_dst, h_dst, d_out);
+    }
+#endif
 #ifdef GSB_SIMT_GEMM
     const int rpc = 256;
     {
         int64_t items = (ceil_div(hb.cap_dst, rpc) + g.T) * (g.S + 1) * ceil_div(d_in, BM) * ceil_div(d_out, BN);
         int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, kNumSMs * 4));
-        GSB_LAUNCH("rgcn_gemm_dW", gemm_tn_kernel, grid, NT, 0, s, rg, acat, lda, dh_dst, h_dst, relu,
+        GSB_LAUNCH(lname("rgcn_gemm_dW", layer), gemm_tn_kernel, grid, NT, 0, s, rg, acat, lda, dh_dst, h_dst, relu,
                    (int64_t)d_out, d_in, d_out, rpc, dW, (int64_t)d_out, (int64_t)d_in * d_out, db);
     }
 #else
@@ -233,29 +287,29 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         int rpc = (int)std::max<int64_t>(128, std::min<int64_t>(2048, ceil_div(rows * (g.S + 1), 2 * kNumSMs)));
         rpc = (rpc + 31) / 32 * 32;
         UProb P{};
-        P.rg = rg; P.A = acat; P.lda = lda; P.B = dh_dst; P.ldb = d_out; P.H = h_dst; P.relu = relu;
+        P.rg = rg; P.A = acat; P.lda = lda; P.B = dh_dst; P.ldb = d_out;
         P.d_in = d_in; P.N = d_out; P.C = dW; P.ldc = d_out; P.bslot = (int64_t)d_in * d_out; P.db = db;
         P.rows_per_chunk = rpc;
         int64_t items = (ceil_div(rows, rpc) + g.T) * (g.S + 1) * ceil_div(d_in, 128) * ceil_div(d_out, 128);
-        gsb_status st = launch_umma<UMMA_TN>("rgcn_gemm_dW", P, items, s);
+        gsb_status st = launch_umma<UMMA_TN>(lname("rgcn_gemm_dW", layer), P, items, s);
         if (st != GSB_OK) return st;
     }
 #endif
     if (dh_src) {
 #ifdef GSB_SIMT_GEMM
-        GSB_LAUNCH("rgcn_gemm_dA", gemm_nt_kernel, gemm_grid(hb.cap_dst, (int)ceil_div(d_in, BN) * (g.S + 1), g.T),
+        GSB_LAUNCH(lname("rgcn_gemm_dA", layer), gemm_nt_kernel, gemm_grid(hb.cap_dst, (int)ceil_div(d_in, BN) * (g.S + 1), g.T),
                    NT, 0, s, rg, dh_dst, h_dst, relu, (int64_t)d_out, W, d_in, d_out, (int64_t)d_out,
                    (int64_t)d_in * d_out, dacat_ws, lda);
 #else
         UProb P{};
-        P.rg = rg; P.A = dh_dst; P.lda = d_out; P.H = h_dst; P.relu = relu; P.B = W; P.ldb = d_out;
+        P.rg = rg; P.A = dh_dst; P.lda = d_out; P.B = W; P.ldb = d_out;
         P.bslot = (int64_t)d_in * d_out; P.d_in = d_in; P.N = d_out; P.C = dacat_ws; P.ldc = lda;
-        gsb_status st = launch_umma<UMMA_NT>("rgcn_gemm_dA", P,
+        gsb_status st = launch_umma<UMMA_NT>(lname("rgcn_gemm_dA", layer), P,
                                              (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_in, 128) * (g.S + 1), s);
         if (st != GSB_OK) return st;
 #endif
         GSB_CUDA(cudaMemsetAsync(dh_src, 0, sizeof(float) * (size_t)hb.cap_src * d_in, s));
-        GSB_LAUNCH("rgcn_scatter", scatter_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
+        GSB_LAUNCH(lname("rgcn_scatter", layer), scatter_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
                    hb.meta, hb.seg_ptr, hb.e_src, dacat_ws, lda, d_in, dh_src);
     }
     return GSB_OK;

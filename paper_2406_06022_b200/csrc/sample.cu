@@ -301,38 +301,46 @@ __device__ __forceinline__ int64_t bit_rank(const uint32_t* bitmap, const int32_
 __global__ void hop_meta_kernel(GraphDev g, HopMeta* __restrict__ m, HopMeta* __restrict__ next,
                                 const int64_t* __restrict__ seg_ptr, int64_t nseg_cap, const uint32_t* __restrict__ bitmap,
                                 const int32_t* __restrict__ wrank, int64_t cap_src, int* __restrict__ err) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (*(volatile int*)err) {   // latched: empty block and frontier (kernels downstream see 0 rows)
+    __shared__ int64_t nn_s[kMaxT];
+    const int t = threadIdx.x;
+    const bool bad = *(volatile int*)err != 0;
+    if (!bad && t < kMaxT) {   // one thread per node type: new-source count via bitmap ranks
+        int64_t nn = 0;
+        if (t < g.T) {
+            const int64_t lo = bit_rank(bitmap, wrank, g.node_off[t]);
+            const int64_t hi = bit_rank(bitmap, wrank, g.node_off[t + 1]);
+            m->new_base[t] = lo;
+            nn = hi - lo;
+        }
+        nn_s[t] = nn;
+    }
+    __syncthreads();
+    if (t != 0) return;
+    if (bad) {   // latched: empty block and frontier (kernels downstream see 0 rows)
         m->n_edges = 0;
         m->n_src = 0;
-        for (int t = 0; t <= kMaxT; ++t) m->src_off[t] = 0;
+        for (int k = 0; k <= kMaxT; ++k) m->src_off[k] = 0;
         if (next) {
             next->n_dst = 0;
-            for (int t = 0; t <= kMaxT; ++t) next->dst_off[t] = 0;
+            for (int k = 0; k <= kMaxT; ++k) next->dst_off[k] = 0;
         }
         return;
     }
     m->n_edges = seg_ptr[nseg_cap];
+    int64_t off = 0;
     m->src_off[0] = 0;
-    for (int t = 0; t < kMaxT; ++t) {
-        int64_t nd = m->dst_off[t + 1] - m->dst_off[t];
-        int64_t nn = 0;
-        if (t < g.T) {
-            int64_t lo = bit_rank(bitmap, wrank, g.node_off[t]);
-            int64_t hi = bit_rank(bitmap, wrank, g.node_off[t + 1]);
-            m->new_base[t] = lo;
-            nn = hi - lo;
-        }
-        m->src_off[t + 1] = m->src_off[t] + nd + nn;
+    for (int k = 0; k < kMaxT; ++k) {
+        off += (m->dst_off[k + 1] - m->dst_off[k]) + nn_s[k];
+        m->src_off[k + 1] = off;
     }
-    m->n_src = m->src_off[kMaxT];
+    m->n_src = off;
     if (m->n_src > cap_src) {
         atomicExch(err, ERR_CAPACITY);
         m->n_src = cap_src;
     }
     if (next) {
         next->n_dst = m->n_src;
-        for (int t = 0; t <= kMaxT; ++t) next->dst_off[t] = m->src_off[t];
+        for (int k = 0; k <= kMaxT; ++k) next->dst_off[k] = m->src_off[k];
     }
 }
 

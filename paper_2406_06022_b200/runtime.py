@@ -259,6 +259,7 @@ class _TrainerBase:
         self.counters = torch.zeros(2, dtype=torch.int32, device=dev)
         self.graph = None
         self.graph_ws = 1
+        self.fuse_gather = True
 
     # parameter views -------------------------------------------------------------------
     def pview(self, name: str, which: str = "p") -> torch.Tensor:
@@ -273,10 +274,14 @@ class _TrainerBase:
 
     # pieces ------------------------------------------------------------------------------
     def _encode(self, s):
-        """gather -> RGCN layers, input layer first (Fig. 8)."""
+        """gather -> RGCN layers, input layer first (Fig. 8).  With fuse_gather
+        (default) layer 0 reads the feature rows by gid inside its aggregation kernel."""
         sm = self.sampler
-        call("gsb_gather_block_inputs", sm.h, _ptr(sm.arena), _ptr(self.x0), s)
-        h = self.x0
+        if self.fuse_gather:
+            h = None
+        else:
+            call("gsb_gather_block_inputs", sm.h, _ptr(sm.arena), _ptr(self.x0), s)
+            h = self.x0
         for l in range(self.L):
             call("gsb_rgcn_layer_fwd", sm.h, _ptr(sm.arena), l, _ptr(h), self.d_in[l], self._pp(f"W{l}"),
                  self._pp(f"b{l}"), self.hidden, int(l < self.L - 1), _ptr(self.hout[l]), _ptr(self.acat[l]), s)

@@ -41,3 +41,35 @@ def gpu_store(cfg, device="cuda", keep=None):
 
 def oracle_graph(cfg, keep=None):
     return oracle.Graph(cfg, keep=keep)
+
+
+def relu_tie_slack(res, R, layer, rtol=RTOL_F32):
+    """Gradient slack from ambiguous ReLU decisions (DESIGN.md R-relutie).
+
+    A pre-activation z whose oracle value lies within the forward tolerance of 0 may take
+    either side of the ReLU on the GPU; flipping it changes dW[r][k][n] by at most
+    |A_r[i][k] * dh[i][n]| and db[n] by |dh[i][n]| (first order, exact for one flip).
+    Returns (slack_W (R+1, d_in, d_out), slack_b (d_out,), n_ambiguous)."""
+    import oracle as _o
+    z = res.zs[layer]
+    dh = res.extra["dh"][layer]
+    amb = np.abs(z) <= rtol * np.abs(z) + rtol * np.abs(z).max()
+    blk = res.blocks[layer]
+    h_src = res.extra["ins"][layer]
+    A, c = _o.rgcn_means(blk, R, h_src)
+    d_in = h_src.shape[1]
+    d_out = z.shape[1]
+    g = np.abs(dh) * amb
+    sW = np.zeros((R + 1, d_in, d_out))
+    for r in range(R):
+        sW[r] = np.abs(A[:, r, :]).T @ g
+    sW[R] = np.abs(h_src[blk.self_row]).T @ g
+    return sW, g.sum(0), int(amb.sum())
+
+
+def close_slack(gpu, ref, slack, rtol=RTOL_F32, what=""):
+    g = np.asarray(gpu, dtype=np.float64)
+    r = np.asarray(ref, dtype=np.float64)
+    bound = rtol * np.abs(r) + rtol * np.abs(r).max() + slack
+    bad = np.abs(g - r) > bound
+    assert not bad.any(), f"{what}: {bad.sum()} / {r.size} outside tolerance (+ReLU-tie slack)"
