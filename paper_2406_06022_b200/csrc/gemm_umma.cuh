@@ -37,6 +37,7 @@ struct UProb {
     const float* bias;     // NN
     float* db;             // TN (optional)
     int rows_per_chunk;    // TN
+    int ksplit;            // NN/NT: K-panel splits per tile (>1: partials red.add into a zeroed C; no relu)
 };
 
 constexpr int UM_THREADS = 256;
@@ -86,15 +87,16 @@ __device__ __forceinline__ float4 split_chunk(uint8_t* hi, uint8_t* lo, uint32_t
 // One (tile, panel) position of this CTA's persistent schedule.
 struct UCursor {
     int64_t tile;          // >= total: exhausted
-    int p, KP;
+    int p, KP;             // panels [p0, KP) of this (split) tile; p runs from p0
+    int p0, split;
     int t, s, c0, n0;
     int64_t row0, rlim;
 };
 
 template <int MODE>
 __device__ __forceinline__ int64_t tiles_of_group(const UProb& P, int t, int64_t r0, int64_t r1, int nct, int kct) {
-    if (MODE == UMMA_NN) return ((r1 - r0 + 127) / 128) * nct;
-    if (MODE == UMMA_NT) return ((r1 - r0 + 127) / 128) * kct * P.rg.ks[t];
+    if (MODE == UMMA_NN) return ((r1 - r0 + 127) / 128) * nct * P.ksplit;
+    if (MODE == UMMA_NT) return ((r1 - r0 + 127) / 128) * kct * P.rg.ks[t] * P.ksplit;
     return ((r1 - r0 + P.rows_per_chunk - 1) / P.rows_per_chunk) * P.rg.ks[t] * kct * nct;
 }
 
@@ -111,6 +113,11 @@ __device__ __forceinline__ void decode_tile(const UProb& P, int64_t tile, int nc
     }
     c.t = t;
     c.s = 0; c.c0 = 0; c.n0 = 0;
+    c.split = 0;
+    if (MODE != UMMA_TN) {
+        c.split = (int)(rem % P.ksplit);
+        rem /= P.ksplit;
+    }
     if (MODE == UMMA_NN) {
         c.row0 = r0 + (rem / nct) * 128;
         c.rlim = r1;
@@ -135,7 +142,13 @@ __device__ __forceinline__ void decode_tile(const UProb& P, int64_t tile, int nc
         c.n0 = (q % nct) * 128;
         c.KP = (int)((c.rlim - c.row0 + 31) / 32);
     }
-    c.p = 0;
+    c.p0 = 0;
+    if (MODE != UMMA_TN && P.ksplit > 1) {
+        const int per = (c.KP + P.ksplit - 1) / P.ksplit;
+        c.p0 = min(c.KP, c.split * per);
+        c.KP = min(c.KP, c.p0 + per);
+    }
+    c.p = c.p0;
 }
 
 // issue this thread's cp.async copies of panel c.p into stage buffers (A: 4 chunks, B: 4 chunks)
@@ -319,7 +332,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
                 const uint64_t dal = A_MN ? umma::desc_mnmajor(a_lo + oa) : umma::desc_kmajor(a_lo + oa);
                 const uint64_t dbh = B_MN ? umma::desc_mnmajor(b_hi + ob) : umma::desc_kmajor(b_hi + ob);
                 const uint64_t dbl = B_MN ? umma::desc_mnmajor(b_lo + ob) : umma::desc_kmajor(b_lo + ob);
-                umma::mma_tf32(tmem, dal, dbh, IDESC, (cp.p > 0 || ks > 0) ? 1u : 0u);
+                umma::mma_tf32(tmem, dal, dbh, IDESC, (cp.p > cp.p0 || ks > 0) ? 1u : 0u);
                 umma::mma_tf32(tmem, dah, dbl, IDESC, 1u);
                 umma::mma_tf32(tmem, dah, dbh, IDESC, 1u);
             }
@@ -342,7 +355,27 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
                 const int col = half * 64 + cc * 32;
                 float v[32];
                 umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)col, v);
-                if (MODE == UMMA_NN) {
+                if (MODE == UMMA_NN && P.ksplit > 1) {
+                    const int64_t row = cp.row0 + r;
+                    if (row < cp.rlim) {
+                        float* out = P.C + row * P.ldc;
+                        const bool vec = ((P.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(P.C) & 15) == 0);
+#pragma unroll
+                        for (int e = 0; e < 32; e += 4) {
+                            const int n = cp.n0 + col + e;
+                            float x[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                x[u] = v[e + u] + ((cp.split == 0 && P.bias && n + u < P.N) ? __ldg(P.bias + n + u) : 0.f);
+                            if (vec && n + 3 < P.N) {
+                                red_add_f4(out + n, make_float4(x[0], x[1], x[2], x[3]));
+                            } else {
+                                for (int u = 0; u < 4; ++u)
+                                    if (n + u < P.N) atomicAdd(out + n + u, x[u]);
+                            }
+                        }
+                    }
+                } else if (MODE == UMMA_NN) {
                     const int64_t row = cp.row0 + r;
                     if (row < cp.rlim) {
                         float* out = P.C + row * P.ldc;
@@ -373,7 +406,14 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
 #pragma unroll
                         for (int e = 0; e < 32; e += 4) {
                             const int k = cp.c0 + col + e;
-                            if (vec && k + 3 < P.d_in) {
+                            if (P.ksplit > 1) {
+                                if (vec && k + 3 < P.d_in) {
+                                    red_add_f4(out + k, make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]));
+                                } else {
+                                    for (int u = 0; u < 4; ++u)
+                                        if (k + u < P.d_in) atomicAdd(out + k + u, v[e + u]);
+                                }
+                            } else if (vec && k + 3 < P.d_in) {
                                 *reinterpret_cast<float4*>(out + k) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
                             } else {
                                 for (int u = 0; u < 4; ++u)
@@ -422,14 +462,24 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
     if (warp == 0) umma::tmem_dealloc<128>(tmem);
 }
 
+// Split-K choice for NN/NT: when a problem has too few output tiles to fill the SMs, split
+// each tile's K panels (>= 3 panels per split) across CTAs.  Split outputs are accumulated
+// with red.add, so C must be zeroed first and relu is not allowed (callers check).
+inline int choose_ksplit(int64_t tiles_upper, int kp, bool allowed) {
+    if (!allowed || tiles_upper * 2 > kNumSMs) return 1;
+    int k = (int)std::min<int64_t>(kNumSMs / std::max<int64_t>(tiles_upper, 1), (kp + 2) / 3);
+    return std::max(1, k);
+}
+
 template <int MODE>
-inline gsb_status launch_umma(const char* name, const UProb& P, int64_t tiles_upper, cudaStream_t s) {
+inline gsb_status launch_umma(const char* name, UProb P, int64_t tiles_upper, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
         GSB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, UM_SMEM));
         attr_set = true;
     }
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_upper, kNumSMs));
+    if (P.ksplit < 1) P.ksplit = 1;
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_upper * P.ksplit, kNumSMs));
     GSB_LAUNCH(name, umma_gemm_kernel<MODE>, grid, UM_THREADS, UM_SMEM, s, P);
     return GSB_OK;
 }

@@ -245,7 +245,10 @@ gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     UProb P{};
     P.rg = rg; P.A = acat; P.lda = lda; P.B = W; P.ldb = d_out; P.bslot = (int64_t)d_in * d_out;
     P.relu = relu; P.d_in = d_in; P.N = d_out; P.C = h_dst; P.ldc = d_out; P.bias = bias;
-    return launch_umma<UMMA_NN>(lname("rgcn_gemm_fwd", layer), P, (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_out, 128), s);
+    const int64_t tiles = (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_out, 128);
+    P.ksplit = choose_ksplit(tiles, (g.S + 1) * (d_in / 32), !relu);
+    if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(h_dst, 0, sizeof(float) * (size_t)hb.cap_dst * d_out, s));
+    return launch_umma<UMMA_NN>(lname("rgcn_gemm_fwd", layer), P, tiles, s);
 #endif
 }
 
@@ -284,7 +287,7 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     {
         // row chunks sized so the (type, slot, chunk) items cover ~2 waves of SMs
         const int64_t rows = hb.cap_dst;
-        int rpc = (int)std::max<int64_t>(128, std::min<int64_t>(2048, ceil_div(rows * (g.S + 1), 2 * kNumSMs)));
+        int rpc = (int)std::max<int64_t>(64, std::min<int64_t>(2048, ceil_div(rows * (g.S + 1), 2 * kNumSMs)));
         rpc = (rpc + 31) / 32 * 32;
         UProb P{};
         P.rg = rg; P.A = acat; P.lda = lda; P.B = dh_dst; P.ldb = d_out;
@@ -304,8 +307,10 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         UProb P{};
         P.rg = rg; P.A = dh_dst; P.lda = d_out; P.B = W; P.ldb = d_out;
         P.bslot = (int64_t)d_in * d_out; P.d_in = d_in; P.N = d_out; P.C = dacat_ws; P.ldc = lda;
-        gsb_status st = launch_umma<UMMA_NT>(lname("rgcn_gemm_dA", layer), P,
-                                             (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_in, 128) * (g.S + 1), s);
+        const int64_t tiles = (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_in, 128) * (g.S + 1);
+        P.ksplit = choose_ksplit(tiles, (d_out + 31) / 32, true);
+        if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(dacat_ws, 0, sizeof(float) * (size_t)hb.cap_dst * lda, s));
+        gsb_status st = launch_umma<UMMA_NT>(lname("rgcn_gemm_dA", layer), P, tiles, s);
         if (st != GSB_OK) return st;
 #endif
         GSB_CUDA(cudaMemsetAsync(dh_src, 0, sizeof(float) * (size_t)hb.cap_src * d_in, s));
@@ -353,7 +358,10 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         UProb P{};
         P.rg = rg; P.A = h; P.lda = d; P.B = Wc; P.ldb = C; P.bslot = 0; P.d_in = d; P.N = C; P.C = logits_ws;
         P.ldc = ldl; P.bias = bc;
-        gsb_status st = launch_umma<UMMA_NN>("nc_logits", P, ceil_div(n, 128) * ceil_div(C, 128), s);
+        const int64_t tiles = ceil_div(n, 128) * ceil_div(C, 128);
+        P.ksplit = choose_ksplit(tiles, d / 32, true);
+        if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(logits_ws, 0, sizeof(float) * (size_t)n * ldl, s));
+        gsb_status st = launch_umma<UMMA_NN>("nc_logits", P, tiles, s);
         if (st != GSB_OK) return st;
     }
 #endif
@@ -373,8 +381,8 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
 #else
         UProb P{};
         P.rg = rg; P.A = h; P.lda = d; P.B = logits_ws; P.ldb = ldl; P.d_in = d; P.N = C; P.C = dWc; P.ldc = C;
-        P.bslot = 0; P.db = dbc; P.rows_per_chunk = 128;
-        gsb_status st = launch_umma<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, 128) * ceil_div(d, 128) * ceil_div(C, 128), s);
+        P.bslot = 0; P.db = dbc; P.rows_per_chunk = 64;
+        gsb_status st = launch_umma<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, 64) * ceil_div(d, 128) * ceil_div(C, 128), s);
         if (st != GSB_OK) return st;
 #endif
     }
@@ -386,7 +394,10 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         UProb P{};
         P.rg = rg; P.A = logits_ws; P.lda = ldl; P.B = Wc; P.ldb = C; P.bslot = 0; P.d_in = d; P.N = C; P.C = dh;
         P.ldc = d;
-        gsb_status st = launch_umma<UMMA_NT>("nc_gemm_dh", P, ceil_div(n, 128) * ceil_div(d, 128), s);
+        const int64_t tiles = ceil_div(n, 128) * ceil_div(d, 128);
+        P.ksplit = choose_ksplit(tiles, (C + 31) / 32, true);
+        if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(dh, 0, sizeof(float) * (size_t)n * d, s));
+        gsb_status st = launch_umma<UMMA_NT>("nc_gemm_dh", P, tiles, s);
         if (st != GSB_OK) return st;
 #endif
     }
