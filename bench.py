@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--replicate-features", action="store_true",
+                    help="N>1: replicate the feature tables instead of partitioning them by node ID")
     return ap.parse_args()
 
 
@@ -165,7 +167,8 @@ def kernel_work(name: str, sz: dict, cfg: synth.Config):
 
 
 # ------------------------------------------------------------------------------ gsb arm
-def build_gsb(cfg, device):
+def build_gsb(cfg, device, partition=None):
+    """partition = (world, rank) -> features partitioned by node ID (FeatureExchange)."""
     import torch
     from paper_2406_06022_b200.runtime import GraphStore, RGCNTrainer
     st = GraphStore(cfg.counts, cfg.etype_src(), cfg.etype_dst(), device)
@@ -173,12 +176,23 @@ def build_gsb(cfg, device):
         s, d = synth.etype_coo(cfg, r, backend="torch", device=device)
         st.load_etype(r, s, d)
         del s, d
-    for t in range(cfg.num_ntypes):
-        st.set_features(t, synth.feature_table(cfg, t, backend="torch", device=device))
+    ex = None
+    if partition is None:
+        for t in range(cfg.num_ntypes):
+            st.set_features(t, synth.feature_table(cfg, t, backend="torch", device=device))
+    else:
+        from paper_2406_06022_b200.dist import FeatureExchange, balanced_bounds
+        world, rank = partition
+        b = balanced_bounds(cfg.counts, world)
+        shards = [synth.feature_rows(cfg, t, torch.arange(int(b[t][rank]), int(b[t][rank + 1]), device=device),
+                                     "torch", device) for t in range(cfg.num_ntypes)]
+        ex = FeatureExchange(cfg.counts, world, rank, shards, cfg.feat_dim)
+        st.feat_dim = cfg.feat_dim
     torch.cuda.synchronize()
     tr = RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
                      synth.param_order(cfg), synth.labels(cfg, backend="torch", device=device),
                      int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
+    tr.exchange = ex
     return st, tr
 
 
@@ -220,7 +234,8 @@ def run_gsb(args, cfg):
         dist.init_process_group("nccl", device_id=torch.device(device))
     from paper_2406_06022_b200 import _lib
     t0 = time.time()
-    st, tr = build_gsb(cfg, device)
+    partitioned = dist is not None and not args.replicate_features
+    st, tr = build_gsb(cfg, device, (ws, rank) if partitioned else None)
     setup_s = time.time() - t0
     train = synth.train_nodes(cfg)
     per_epoch = max(1, len(train) // cfg.batch)
@@ -248,7 +263,7 @@ def run_gsb(args, cfg):
         raise RuntimeError("device-side sampling error latched")
     # ---- capture ONE whole step (sample..Adam) in a CUDA graph; replays advance the RNG step
     # word and Adam's t on the device, inputs are copied into the graph's fixed seed buffer
-    use_graph = not args.no_graph
+    use_graph = not args.no_graph and not partitioned   # all-to-all sizes are host-synced
     if use_graph:
         tr.load_inputs(seeds_all[W - 2])
         tr.capture(step0=(W - 2) * ws + rank, ws=ws, allreduce=allreduce if dist is not None else None)
@@ -268,6 +283,8 @@ def run_gsb(args, cfg):
     # ---- timed region
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _lib.lib().gsb_launch_count()
+    if tr.exchange is not None:
+        tr.exchange.bytes_sent = 0
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -280,6 +297,7 @@ def run_gsb(args, cfg):
     if dist is not None:
         dist.barrier()
     launches = _lib.lib().gsb_launch_count() - launches0
+    nv_bytes = tr.exchange.bytes_sent / args.steps if tr.exchange is not None else 0
     if use_graph:   # kernels inside a replayed graph are not re-counted by the library
         launches = launches_per_step_graph(tr, cfg) * args.steps
     ms = e0.elapsed_time(e1)
@@ -376,15 +394,20 @@ def run_gsb(args, cfg):
     kernels = {k: {"us_per_step": v["total_ms"] * 1e3 / args.profile_steps,
                    "share": v["total_ms"] / args.profile_steps / step_ms_prof} for k, v in
                sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])}
+    par = ("single" if ws == 1 else
+           (f"dp{ws}: features partitioned by node ID (NCCL all-to-all fetch), topology replicated, "
+            f"NCCL grad all-reduce" if partitioned else f"dp{ws}: graph + features replicated, NCCL grad all-reduce"))
     line = {
         "metric": METRIC, "value": seeds_per_s, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded hash generator, synth/)",
-        "config": cfg_json(cfg, ws),
+        "config": cfg_json(cfg, ws, {"parallelism": par, "cuda_graph": use_graph}),
         "sampled_edges_per_s": edges_per_step * ws / (ms_per_step / 1e3),
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
         "kernels": kernels, "setup_s": setup_s,
     }
+    if tr.exchange is not None:
+        line["nvlink_bytes_per_step_rank0"] = nv_bytes
     if dist is not None:
         dist.destroy_process_group()
     return line, st, tr

@@ -271,6 +271,32 @@ gsb_status gsb_lp_score(const float* H, int64_t n_rows_cap, int32_t d, const int
                         float* row_loss_ws, float* loss, float* dH, float* drel, void* stream);
 
 /* ======================================================================================
+ * Partitioned feature store across GPUs (§8(e); P:L86 distributed tensors, P:L90 random
+ * partitioning, P:L172 remote data movement).  Rank r owns local ids
+ * [bounds[t][r], bounds[t][r+1]) of every ntype t and holds only those feature rows.  A
+ * gather of arbitrary gids = bucket by owner -> NCCL all-to-all of ids (caller) ->
+ * gsb_shard_gather on the owner -> all-to-all of rows (caller) -> gsb_rows_permute.
+ * ==================================================================================== */
+typedef struct gsb_partition* gsb_partition_t;
+/* bounds: host int64 [num_ntypes][world+1], bounds[t][0] = 0, bounds[t][world] = count[t].
+ * world <= 8. */
+gsb_status gsb_partition_create(int32_t num_ntypes, const int64_t* ntype_count, int32_t world, int32_t rank,
+                                const int64_t* bounds, gsb_partition_t* out);
+gsb_status gsb_partition_destroy(gsb_partition_t p);
+/* Register this rank's shard of ntype t: device fp32 rows for its owned local ids. */
+gsb_status gsb_partition_set_shard(gsb_partition_t p, int32_t ntype, const float* rows, int32_t dim);
+/* Owner bucketing (K11): for i < n (n = *n_dev if non-NULL, else n_cap): send_gid[perm[i]] =
+ * gid[i] grouped by owner rank in rank order; send_counts: device int64 [world] (overwritten);
+ * ws: device scratch of 8*world bytes.  Order inside a bucket is unspecified; perm is exact. */
+gsb_status gsb_bucket_by_owner(gsb_partition_t p, const int64_t* gid, const int64_t* n_dev, int64_t n_cap,
+                               int64_t* send_gid, int32_t* perm, int64_t* send_counts, void* ws, void* stream);
+/* out[i, :] = own shard row of gid[i] (every gid must be owned by this rank). */
+gsb_status gsb_shard_gather(gsb_partition_t p, const int64_t* gid, int64_t n, float* out, void* stream);
+/* out[i, :] = rows[perm[i], :] for i < n (n = *n_dev if non-NULL, else n_cap). */
+gsb_status gsb_rows_permute(const float* rows, int32_t d, const int32_t* perm, const int64_t* n_dev, int64_t n_cap,
+                            float* out, void* stream);
+
+/* ======================================================================================
  * Optimizer (paper silent, R-adam): Adam with bias correction over a flat
  * fp32 buffer of n parameters; t is the 1-based step.  In place on p, m, v.
  * ==================================================================================== */

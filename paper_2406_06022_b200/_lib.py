@@ -55,6 +55,12 @@ SIGS = {
     "gsb_layer_acat_floats": [P, i32, i32, C.POINTER(i64)],
     "gsb_rgcn_layer_fwd": [P, P, i32, P, i32, P, P, i32, i32, P, P, P],
     "gsb_rgcn_layer_bwd": [P, P, i32, P, P, P, P, i32, i32, i32, P, P, P, P, P],
+    "gsb_partition_create": [i32, P, i32, i32, P, C.POINTER(P)],
+    "gsb_partition_destroy": [P],
+    "gsb_partition_set_shard": [P, i32, P, i32],
+    "gsb_bucket_by_owner": [P, P, P, i64, P, P, P, P, P],
+    "gsb_shard_gather": [P, P, i64, P, P],
+    "gsb_rows_permute": [P, i32, P, P, i64, P, P],
     "gsb_gemm": [i32, P, i64, P, i64, i64, i32, i32, P, i64, P],
     "gsb_nc_loss": [P, i64, i32, P, P, i32, P, P, i64, P, P, P, P, P, P, P],
     "gsb_adam_step": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P],

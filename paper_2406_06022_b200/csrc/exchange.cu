@@ -1,0 +1,184 @@
+// exchange.cu -- node-ID partitioning of the feature store across GPUs (SURVEY §8(e), §2.4
+// C4/C5): owner bucketing of requested gids (K11), gather from the local shard on the owner,
+// and unpacking of the returned rows.  The collectives themselves (NCCL all-to-all) are issued
+// by the caller between these calls.  Contract: include/gsb.h "Partitioned feature store".
+#include <cub/device/device_scan.cuh>
+
+#include "gsb_internal.cuh"
+
+namespace gsb {
+
+struct PartDev {
+    int32_t world, rank, T;
+    int64_t lo[kMaxT][9];   // local-id boundaries of each rank per ntype (world <= 8)
+    int64_t node_off[kMaxT + 1];
+    const float* shard[kMaxT];   // local shard rows [lo[t][rank], lo[t][rank+1])
+    int32_t dim;
+};
+
+__device__ __forceinline__ int part_type(const PartDev& p, int64_t gid) {
+    int t = 0;
+    for (int k = 1; k < p.T; ++k) t += (gid >= p.node_off[k]) ? 1 : 0;
+    return t;
+}
+__device__ __forceinline__ int part_owner(const PartDev& p, int t, int64_t local) {
+    int r = 0;
+    for (int k = 1; k < p.world; ++k) r += (local >= p.lo[t][k]) ? 1 : 0;
+    return r;
+}
+
+__global__ void owner_count_kernel(PartDev p, const int64_t* __restrict__ gid, const int64_t* __restrict__ n_dev,
+                                   int64_t n_cap, unsigned long long* __restrict__ cnt) {
+    __shared__ unsigned long long sc[8];
+    if (threadIdx.x < 8) sc[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t n = n_dev ? min(*n_dev, n_cap) : n_cap;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = gid[i];
+        const int t = part_type(p, x);
+        atomicAdd(&sc[part_owner(p, t, x - p.node_off[t])], 1ull);
+    }
+    __syncthreads();
+    if (threadIdx.x < p.world && sc[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], sc[threadIdx.x]);
+}
+
+// cursor[w] starts at the exclusive prefix of the counts; positions via atomics (the order
+// inside an owner's bucket does not affect the unpacked result: perm maps every row back)
+__global__ void owner_scatter_kernel(PartDev p, const int64_t* __restrict__ gid, const int64_t* __restrict__ n_dev,
+                                     int64_t n_cap, const unsigned long long* __restrict__ cnt,
+                                     unsigned long long* __restrict__ cursor, int64_t* __restrict__ send_gid,
+                                     int32_t* __restrict__ perm) {
+    __shared__ unsigned long long base[8];
+    if (threadIdx.x == 0) {
+        unsigned long long a = 0;
+        for (int w = 0; w < p.world; ++w) {
+            base[w] = a;
+            a += cnt[w];
+        }
+    }
+    __syncthreads();
+    const int64_t n = n_dev ? min(*n_dev, n_cap) : n_cap;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = gid[i];
+        const int t = part_type(p, x);
+        const int w = part_owner(p, t, x - p.node_off[t]);
+        const int64_t pos = (int64_t)(base[w] + atomicAdd(&cursor[w], 1ull));
+        send_gid[pos] = x;
+        perm[i] = (int32_t)pos;
+    }
+}
+
+__global__ void shard_gather_kernel(PartDev p, const int64_t* __restrict__ gid, int64_t n, float* __restrict__ out) {
+    const int d4 = p.dim >> 2;
+    const int64_t total = n * d4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / d4;
+        const int c = (int)(i - row * d4);
+        const int64_t x = gid[row];
+        const int t = part_type(p, x);
+        const int64_t local = x - p.node_off[t] - p.lo[t][p.rank];
+        reinterpret_cast<float4*>(out)[i] = __ldg(reinterpret_cast<const float4*>(p.shard[t] + local * p.dim) + c);
+    }
+}
+
+__global__ void rows_permute_kernel(const float* __restrict__ rows, int d, const int32_t* __restrict__ perm,
+                                    const int64_t* __restrict__ n_dev, int64_t n_cap, float* __restrict__ out) {
+    const int64_t n = n_dev ? min(*n_dev, n_cap) : n_cap;
+    const int d4 = d >> 2;
+    const int64_t total = n * d4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / d4;
+        const int c = (int)(i - row * d4);
+        reinterpret_cast<float4*>(out)[i] = __ldg(reinterpret_cast<const float4*>(rows + (int64_t)perm[row] * d) + c);
+    }
+}
+
+struct Part {
+    PartDev dev;
+};
+
+}  // namespace gsb
+
+using namespace gsb;
+
+extern "C" {
+
+gsb_status gsb_partition_create(int32_t num_ntypes, const int64_t* ntype_count, int32_t world, int32_t rank,
+                                const int64_t* bounds, gsb_partition_t* out) {
+    GSB_CHECK_ARG(out && ntype_count && bounds, "null argument");
+    GSB_CHECK_ARG(num_ntypes >= 1 && num_ntypes <= kMaxT, "bad num_ntypes");
+    GSB_CHECK_ARG(world >= 1 && world <= 8 && rank >= 0 && rank < world, "world %d / rank %d unsupported", world, rank);
+    Part* P = new Part();
+    memset(&P->dev, 0, sizeof(PartDev));
+    P->dev.world = world;
+    P->dev.rank = rank;
+    P->dev.T = num_ntypes;
+    P->dev.node_off[0] = 0;
+    for (int t = 0; t < num_ntypes; ++t) {
+        P->dev.node_off[t + 1] = P->dev.node_off[t] + ntype_count[t];
+        for (int w = 0; w <= world; ++w) P->dev.lo[t][w] = bounds[t * (world + 1) + w];
+        if (P->dev.lo[t][0] != 0 || P->dev.lo[t][world] != ntype_count[t]) {
+            delete P;
+            set_error("bounds of ntype %d must span [0, %lld]", t, (long long)ntype_count[t]);
+            return GSB_EINVAL;
+        }
+    }
+    for (int t = num_ntypes + 1; t <= kMaxT; ++t) P->dev.node_off[t] = P->dev.node_off[num_ntypes];
+    *out = reinterpret_cast<gsb_partition_t>(P);
+    return GSB_OK;
+}
+
+gsb_status gsb_partition_destroy(gsb_partition_t p) {
+    delete reinterpret_cast<Part*>(p);
+    return GSB_OK;
+}
+
+gsb_status gsb_partition_set_shard(gsb_partition_t p, int32_t ntype, const float* rows, int32_t dim) {
+    Part* P = reinterpret_cast<Part*>(p);
+    GSB_CHECK_ARG(P && ntype >= 0 && ntype < P->dev.T && dim > 0 && dim % 4 == 0, "bad argument");
+    GSB_CHECK_ARG(P->dev.dim == 0 || P->dev.dim == dim, "all shards must share one dim");
+    P->dev.dim = dim;
+    P->dev.shard[ntype] = rows;
+    return GSB_OK;
+}
+
+gsb_status gsb_bucket_by_owner(gsb_partition_t p, const int64_t* gid, const int64_t* n_dev, int64_t n_cap,
+                               int64_t* send_gid, int32_t* perm, int64_t* send_counts, void* ws, void* stream) {
+    Part* P = reinterpret_cast<Part*>(p);
+    GSB_CHECK_ARG(P && gid && send_gid && perm && send_counts && ws && n_cap >= 0, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(send_counts);
+    unsigned long long* cursor = reinterpret_cast<unsigned long long*>(ws);
+    GSB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * P->dev.world, s));
+    GSB_CUDA(cudaMemsetAsync(cursor, 0, sizeof(int64_t) * P->dev.world, s));
+    if (n_cap == 0) return GSB_OK;
+    const int grid = grid_for(n_cap, 256, kNumSMs * 4);
+    GSB_LAUNCH("owner_count", owner_count_kernel, grid, 256, 0, s, P->dev, gid, n_dev, n_cap, cnt);
+    GSB_LAUNCH("owner_scatter", owner_scatter_kernel, grid, 256, 0, s, P->dev, gid, n_dev, n_cap, cnt, cursor,
+               send_gid, perm);
+    return GSB_OK;
+}
+
+gsb_status gsb_shard_gather(gsb_partition_t p, const int64_t* gid, int64_t n, float* out, void* stream) {
+    Part* P = reinterpret_cast<Part*>(p);
+    GSB_CHECK_ARG(P && (n == 0 || (gid && out)), "null argument");
+    GSB_CHECK_ARG(P->dev.dim > 0, "no shard registered");
+    for (int t = 0; t < P->dev.T; ++t)
+        GSB_CHECK_ARG(P->dev.shard[t] || P->dev.lo[t][P->dev.rank + 1] == P->dev.lo[t][P->dev.rank],
+                      "shard of ntype %d not registered", t);
+    if (n == 0) return GSB_OK;
+    GSB_LAUNCH("shard_gather", shard_gather_kernel, grid_for(n * (P->dev.dim / 4), 256, kNumSMs * 8), 256, 0,
+               (cudaStream_t)stream, P->dev, gid, n, out);
+    return GSB_OK;
+}
+
+gsb_status gsb_rows_permute(const float* rows, int32_t d, const int32_t* perm, const int64_t* n_dev, int64_t n_cap,
+                            float* out, void* stream) {
+    GSB_CHECK_ARG(rows && perm && out && d > 0 && d % 4 == 0 && n_cap >= 0, "bad argument");
+    if (n_cap == 0) return GSB_OK;
+    GSB_LAUNCH("rows_permute", rows_permute_kernel, grid_for(n_cap * (d / 4), 256, kNumSMs * 8), 256, 0,
+               (cudaStream_t)stream, rows, d, perm, n_dev, n_cap, out);
+    return GSB_OK;
+}
+
+}  // extern "C"

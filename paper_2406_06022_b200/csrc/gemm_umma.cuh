@@ -299,22 +299,12 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
     }
     float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
     while (cp.tile < total) {
-        // keep the copy engine UM_STAGES-1 panels ahead (stage reuse waits for its MMAs)
-        {
-            const int st = (int)(it_ld % UM_STAGES);
-            wait_stage(st);
-            if (ld.tile < total) {
-                issue_panel<MODE>(P, ld, smem + st * UM_STAGE, tid, vecA, vecB);
-                advance(ld);
-            }
-            cp_commit();
-            ++it_ld;
-        }
-        cp_wait<UM_STAGES - 1>();
+        // data of panel it_cp landed (the one newer group may still be in flight)
+        cp_wait<UM_STAGES - 2>();
         const int st = (int)(it_cp % UM_STAGES);
         uint8_t* stage = smem + st * UM_STAGE;
         const bool do_db = (MODE == UMMA_TN) && P.db && (cp.s == rg.ks[cp.t] - 1) && cp.c0 == 0;
-        {
+        {   // split overlaps the tensor pipe still working on the previous panel
             float4 v = split_panel<MODE>(stage, tid);
             if (do_db) { cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w; }
         }
@@ -339,6 +329,17 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
             umma::mma_commit(&bars[st]);
         }
         pend[st] = true;
+        // refill: the stage of panel it_cp-1 receives panel it_cp+2 once its MMAs are done
+        {
+            const int fst = (int)(it_ld % UM_STAGES);
+            wait_stage(fst);
+            if (ld.tile < total) {
+                issue_panel<MODE>(P, ld, smem + fst * UM_STAGE, tid, vecA, vecB);
+                advance(ld);
+            }
+            cp_commit();
+            ++it_ld;
+        }
         ++it_cp;
         if (cp.p + 1 < cp.KP) {
             advance(cp);

@@ -53,9 +53,13 @@ __device__ __forceinline__ uint32_t to_tf32(float x) {
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return r;
 }
+// rna tf32 rounding with integer ops (same result as cvt.rna.tf32.f32 for finite x): add half
+// an ulp of the kept 10-bit mantissa, then drop the 13 low bits.  Runs on the ALU pipes
+// instead of the narrower conversion pipe.
+__device__ __forceinline__ uint32_t rna_tf32_bits(uint32_t b) { return (b + 0x1000u) & 0xFFFFE000u; }
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-    hi = to_tf32(x);
-    lo = to_tf32(x - __uint_as_float(hi));
+    hi = rna_tf32_bits(__float_as_uint(x));
+    lo = rna_tf32_bits(__float_as_uint(x - __uint_as_float(hi)));
 }
 
 // ---- mbarrier ------------------------------------------------------------------------

@@ -25,3 +25,67 @@ def rank_step(step: int, rank: int, world: int) -> int:
     union over ranks of one step is `world` consecutive batches (a round-robin split of a
     global batch) and the RNG step word (keyed sampling) stays globally unique."""
     return step * world + rank
+
+
+def balanced_bounds(counts, world: int):
+    """Contiguous node-ID ranges per ntype (random partition: the generator scatters node
+    ranks by an affine bijection).  bounds[t][w] = floor(N_t * w / world)."""
+    import numpy as np
+    return np.array([[(int(n) * w) // world for w in range(world + 1)] for n in counts], dtype=np.int64)
+
+
+class FeatureExchange:
+    """Partitioned feature store (§8(e)): this rank holds only its node-ID range of every
+    ntype; `gather(gids)` returns the rows of arbitrary gids via owner bucketing (libgsb),
+    NCCL all-to-all of ids, a shard gather on the owners (libgsb), an all-to-all of rows back
+    and an unpack (libgsb).  Collectives are issued from the current stream."""
+
+    def __init__(self, counts, world: int, rank: int, shards, dim: int, group=None):
+        import ctypes as C
+        import numpy as np
+        from ._lib import call
+        self.world, self.rank, self.group, self.dim = world, rank, group, dim
+        self.counts = np.asarray(counts, dtype=np.int64)
+        self.bounds = balanced_bounds(self.counts, world)
+        h = C.c_void_p()
+        call("gsb_partition_create", len(self.counts), self.counts.ctypes.data_as(C.c_void_p), world, rank,
+             self.bounds.ctypes.data_as(C.c_void_p), C.byref(h))
+        self.h = h
+        self.shards = [s.contiguous() for s in shards]
+        for t, sh in enumerate(self.shards):
+            call("gsb_partition_set_shard", self.h, t, C.c_void_p(sh.data_ptr()), dim)
+        dev = self.shards[0].device
+        self.counts_dev = torch.zeros(world, dtype=torch.int64, device=dev)
+        self.ws = torch.zeros(world, dtype=torch.int64, device=dev)
+        self.bytes_sent = 0
+
+    def __del__(self):
+        try:
+            from ._lib import lib
+            lib().gsb_partition_destroy(self.h)
+        except Exception:
+            pass
+
+    def gather(self, gids: torch.Tensor, n: int, out: torch.Tensor):
+        import ctypes as C
+        import torch.distributed as dist
+        from ._lib import call
+        P = lambda x: C.c_void_p(x.data_ptr())
+        s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        dev = gids.device
+        send_gid = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        call("gsb_bucket_by_owner", self.h, P(gids), None, n, P(send_gid), P(perm), P(self.counts_dev), P(self.ws), s)
+        recv_counts = torch.empty_like(self.counts_dev)
+        dist.all_to_all_single(recv_counts, self.counts_dev, group=self.group)          # C1
+        both = torch.cat([self.counts_dev, recv_counts]).cpu().tolist()
+        send_splits, recv_splits = both[:self.world], both[self.world:]
+        recv_gid = torch.empty(sum(recv_splits), dtype=torch.int64, device=dev)
+        dist.all_to_all_single(recv_gid, send_gid[:n], recv_splits, send_splits, group=self.group)   # C4
+        rows = torch.empty((max(sum(recv_splits), 1), self.dim), dtype=torch.float32, device=dev)
+        call("gsb_shard_gather", self.h, P(recv_gid), recv_gid.numel(), P(rows), s)
+        back = torch.empty((max(n, 1), self.dim), dtype=torch.float32, device=dev)
+        dist.all_to_all_single(back[:n], rows[:sum(recv_splits)], send_splits, recv_splits, group=self.group)  # C5
+        call("gsb_rows_permute", P(back), self.dim, P(perm), None, n, P(out), s)
+        self.bytes_sent += (n - send_splits[self.rank]) * 8 + (sum(recv_splits) - recv_splits[self.rank]) * self.dim * 4
+        return out

@@ -163,6 +163,17 @@ class MiniBatchSampler:
         a.excl_rev_etype = excl_rev_etype
         call("gsb_sample", self.h, C.byref(a), _ptr(self.arena), self.arena.numel(), _stream(stream))
 
+    def input_gids(self):
+        """(device view of the input-layer gids, their count) -- syncs to read the count."""
+        nd, ns, ne = C.c_int64(), C.c_int64(), C.c_int64()
+        call("gsb_block_sizes", self.h, _ptr(self.arena), 0, C.byref(nd), C.byref(ns), C.byref(ne), None, None,
+             _stream())
+        v = _lib.gsb_block_view()
+        call("gsb_block_view_get", self.h, _ptr(self.arena), 0, C.byref(v))
+        off = v.src_gid - self.arena.data_ptr()
+        n = int(ns.value)
+        return self.arena[off:off + max(n, 1) * 8].view(torch.int64), n
+
     def input_rows(self) -> int:
         v = C.c_int64()
         call("gsb_blocks_input_rows", self.h, C.byref(v))
@@ -260,6 +271,7 @@ class _TrainerBase:
         self.graph = None
         self.graph_ws = 1
         self.fuse_gather = True
+        self.exchange = None      # dist.FeatureExchange when features are partitioned across GPUs
 
     # parameter views -------------------------------------------------------------------
     def pview(self, name: str, which: str = "p") -> torch.Tensor:
@@ -277,7 +289,11 @@ class _TrainerBase:
         """gather -> RGCN layers, input layer first (Fig. 8).  With fuse_gather
         (default) layer 0 reads the feature rows by gid inside its aggregation kernel."""
         sm = self.sampler
-        if self.fuse_gather:
+        if self.exchange is not None:   # partitioned features: NCCL all-to-all fetch (C4/C5)
+            gids, n = sm.input_gids()
+            self.exchange.gather(gids, n, self.x0)
+            h = self.x0
+        elif self.fuse_gather:
             h = None
         else:
             call("gsb_gather_block_inputs", sm.h, _ptr(sm.arena), _ptr(self.x0), s)

@@ -1,0 +1,102 @@
+"""2-GPU test of the partitioned feature store (§8(e)): ranks own node-ID ranges, rows of
+arbitrary gids come back through owner bucketing + NCCL all-to-all + shard gather + unpack,
+bit-exact against the generator's closed form; and one partitioned NC train step whose
+all-reduced gradients equal the mean of the per-rank oracle gradients.
+Skipped unless >= 2 GPUs are visible (run with `gpurun --gpus 2`)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device(f"cuda:{rank}"))
+    import synth
+    from paper_2406_06022_b200 import build
+    build.build()
+    from paper_2406_06022_b200.dist import FeatureExchange, allreduce_mean, balanced_bounds, rank_step
+    from paper_2406_06022_b200.runtime import GraphStore, RGCNTrainer
+    cfg = synth.scaled(synth.mag(), 0.01, "mag_small")
+    dev = f"cuda:{rank}"
+    bounds = balanced_bounds(cfg.counts, world)
+    shards = [synth.feature_rows(cfg, t, torch.arange(int(bounds[t][rank]), int(bounds[t][rank + 1]), device=dev),
+                                 "torch", dev) for t in range(cfg.num_ntypes)]
+    ex = FeatureExchange(cfg.counts, world, rank, shards, cfg.feat_dim)
+    rng = np.random.default_rng(rank)
+    gids = np.sort(rng.integers(0, cfg.num_nodes, 3000)).astype(np.int64)
+    outt = torch.empty((len(gids), cfg.feat_dim), device=dev)
+    ex.gather(torch.from_numpy(gids).to(dev), len(gids), outt)
+    exp = np.concatenate([synth.feature_rows(cfg, int(np.searchsorted(cfg.node_off, g, side="right") - 1),
+                                             [g - cfg.node_off[np.searchsorted(cfg.node_off, g, side="right") - 1]])
+                          for g in gids])
+    out["rows_ok%d" % rank] = bool(np.array_equal(outt.cpu().numpy(), exp))
+    # partitioned NC step: CSC replicated, features partitioned
+    st = GraphStore(cfg.counts, cfg.etype_src(), cfg.etype_dst(), dev)
+    for r in range(cfg.num_etypes):
+        s_, d_ = synth.etype_coo(cfg, r, backend="torch", device=dev)
+        st.load_etype(r, s_, d_)
+    st.feat_dim = cfg.feat_dim
+    tr = RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
+                     synth.param_order(cfg), torch.from_numpy(synth.labels(cfg)),
+                     int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
+    tr.exchange = ex
+    step = rank_step(0, rank, world)
+    tr.forward_backward(torch.from_numpy(synth.nc_seeds(cfg, step)).to(dev), step)
+    allreduce_mean(tr.grad)
+    torch.cuda.synchronize()
+    out["grad%d" % rank] = tr.grad.cpu().numpy().copy()
+    out["loss%d" % rank] = float(tr.loss.item())
+    dist.destroy_process_group()
+
+
+def test_two_gpu_partitioned_features():
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    import torch.multiprocessing as mp
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert out["rows_ok0"] and out["rows_ok1"]
+    import oracle
+    import synth
+    from paper_2406_06022_b200.dist import rank_step
+    from tests._pair import close
+    cfg = synth.scaled(synth.mag(), 0.01, "mag_small")
+    og = oracle.Graph(cfg)
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    flats, losses, slW, slb = [], [], [], []
+    from tests._pair import close_slack, relu_tie_slack
+    for r in range(2):
+        step = rank_step(0, r, 2)
+        res = oracle.nc_step(og, params, synth.nc_seeds(cfg, step), synth.labels(cfg), step, cfg.rng_seed)
+        flats.append(np.concatenate([res.grads[k].reshape(-1) for k in synth.param_order(cfg)]))
+        losses.append(res.loss)
+        sW, sb, _ = relu_tie_slack(res, cfg.num_etypes, 0)
+        slW.append(sW)
+        slb.append(sb)
+    exp = np.mean(flats, axis=0)
+    for r in range(2):
+        close(out["loss%d" % r], losses[r], what=f"rank {r} loss")
+    # layer 0 (ReLU) gets the mean of the ranks' ReLU-tie slack (R-relutie); the rest rtol only
+    slack = np.zeros_like(exp)
+    nW = slW[0].size
+    slack[:nW] = (0.5 * (slW[0] + slW[1])).reshape(-1)
+    slack[nW:nW + slb[0].size] = 0.5 * (slb[0] + slb[1])
+    close_slack(out["grad0"], exp, slack, what="all-reduced grads")
+    np.testing.assert_array_equal(out["grad0"], out["grad1"])
