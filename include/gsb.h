@@ -213,6 +213,11 @@ gsb_status gsb_layer_acat_floats(gsb_blocks_t b, int32_t layer, int32_t d_in, in
 gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src, int32_t d_in,
                               const float* W, const float* bias, int32_t d_out, int32_t relu, float* h_dst,
                               float* acat, void* stream);
+/* Same, with h_src row r read at h_src[rowmap[r]] (rows delivered in exchange order by
+ * gsb_bucket_by_owner's perm: the unpack is folded into the aggregation). */
+gsb_status gsb_rgcn_layer_fwd_rowmap(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src,
+                                     const int32_t* rowmap, int32_t d_in, const float* W, const float* bias,
+                                     int32_t d_out, int32_t relu, float* h_dst, float* acat, void* stream);
 
 /* Backward (analytic):  dZ = dh_dst * 1[h_dst > 0] (relu) or dh_dst;
  *   dW_r = sum_v A_r[v]^T dZ_v ; dW_self = sum_v h_src[self(v)]^T dZ_v ; db = sum_v dZ_v

@@ -27,23 +27,35 @@ __device__ __forceinline__ int part_owner(const PartDev& p, int t, int64_t local
     return r;
 }
 
+// Warp-aggregated: one shared-memory atomic per (warp, owner) instead of one per id.
 __global__ void owner_count_kernel(PartDev p, const int64_t* __restrict__ gid, const int64_t* __restrict__ n_dev,
                                    int64_t n_cap, unsigned long long* __restrict__ cnt) {
     __shared__ unsigned long long sc[8];
     if (threadIdx.x < 8) sc[threadIdx.x] = 0;
     __syncthreads();
+    const int lane = threadIdx.x & 31;
     const int64_t n = n_dev ? min(*n_dev, n_cap) : n_cap;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t x = gid[i];
-        const int t = part_type(p, x);
-        atomicAdd(&sc[part_owner(p, t, x - p.node_off[t])], 1ull);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += stride) {
+        const int64_t i = b + threadIdx.x;
+        int w = -1;
+        if (i < n) {
+            const int64_t x = gid[i];
+            const int t = part_type(p, x);
+            w = part_owner(p, t, x - p.node_off[t]);
+        }
+        for (int o = 0; o < p.world; ++o) {
+            const unsigned bal = __ballot_sync(0xffffffffu, w == o);
+            if (lane == 0 && bal) atomicAdd(&sc[o], (unsigned long long)__popc(bal));
+        }
     }
     __syncthreads();
     if (threadIdx.x < p.world && sc[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], sc[threadIdx.x]);
 }
 
-// cursor[w] starts at the exclusive prefix of the counts; positions via atomics (the order
-// inside an owner's bucket does not affect the unpacked result: perm maps every row back)
+// cursor[w] counts positions handed out inside owner w's bucket; one global atomic per
+// (warp, owner), lanes take consecutive slots by their rank inside the ballot.  The order
+// inside a bucket does not affect the result: perm maps every row back.
 __global__ void owner_scatter_kernel(PartDev p, const int64_t* __restrict__ gid, const int64_t* __restrict__ n_dev,
                                      int64_t n_cap, const unsigned long long* __restrict__ cnt,
                                      unsigned long long* __restrict__ cursor, int64_t* __restrict__ send_gid,
@@ -57,14 +69,32 @@ __global__ void owner_scatter_kernel(PartDev p, const int64_t* __restrict__ gid,
         }
     }
     __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
     const int64_t n = n_dev ? min(*n_dev, n_cap) : n_cap;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t x = gid[i];
-        const int t = part_type(p, x);
-        const int w = part_owner(p, t, x - p.node_off[t]);
-        const int64_t pos = (int64_t)(base[w] + atomicAdd(&cursor[w], 1ull));
-        send_gid[pos] = x;
-        perm[i] = (int32_t)pos;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += stride) {
+        const int64_t i = b + threadIdx.x;
+        int w = -1;
+        int64_t x = 0;
+        if (i < n) {
+            x = gid[i];
+            const int t = part_type(p, x);
+            w = part_owner(p, t, x - p.node_off[t]);
+        }
+        for (int o = 0; o < p.world; ++o) {
+            const unsigned bal = __ballot_sync(0xffffffffu, w == o);
+            if (!bal) continue;
+            const int leader = __ffs(bal) - 1;
+            unsigned long long start = 0;
+            if (lane == leader) start = atomicAdd(&cursor[o], (unsigned long long)__popc(bal));
+            start = __shfl_sync(0xffffffffu, start, leader);
+            if (w == o) {
+                const int64_t pos = (int64_t)(base[o] + start + __popc(bal & lt));
+                send_gid[pos] = x;
+                perm[i] = (int32_t)pos;
+            }
+        }
     }
 }
 

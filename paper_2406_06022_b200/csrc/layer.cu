@@ -12,7 +12,9 @@ namespace gsb {
 //   Acat[j, S_t*d + :] = h_src[self(j), :]
 // ------------------------------------------------------------------------------------
 template <bool FEAT>
-__device__ __forceinline__ const float4* src_row(const GraphDev& g, const float* h, int d, int64_t row, int64_t gid) {
+__device__ __forceinline__ const float4* src_row(const GraphDev& g, const float* h, int d, int64_t row, int64_t gid,
+                                                 const int32_t* rowmap = nullptr) {
+    if (!FEAT && rowmap) row = rowmap[row];   // rows delivered in exchange order (partitioned features)
     if (FEAT) {   // layer 0 reads the feature table by global id (fused gather, §8(a) a5)
         const int t = type_of(g, gid);
         return reinterpret_cast<const float4*>(g.feat[t] + (gid - g.node_off[t]) * d);
@@ -27,7 +29,8 @@ __global__ void __launch_bounds__(256) agg_kernel(GraphDev g, const HopMeta* __r
                                                   const int32_t* __restrict__ e_src,
                                                   const int64_t* __restrict__ e_src_gid,
                                                   const int64_t* __restrict__ dst_gid, const float* __restrict__ h,
-                                                  int d, float* __restrict__ acat, int64_t lda) {
+                                                  int d, float* __restrict__ acat, int64_t lda,
+                                                  const int32_t* __restrict__ rowmap) {
     const int lane = threadIdx.x & 31;
     const int S = g.S;
     const int64_t n = m->n_dst;
@@ -45,10 +48,10 @@ __global__ void __launch_bounds__(256) agg_kernel(GraphDev g, const HopMeta* __r
                 float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
                 int64_t e = e0;
                 for (; e + 4 <= e1; e += 4) {
-                    const float4* p0 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e], FEAT ? e_src_gid[e] : 0);
-                    const float4* p1 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 1], FEAT ? e_src_gid[e + 1] : 0);
-                    const float4* p2 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 2], FEAT ? e_src_gid[e + 2] : 0);
-                    const float4* p3 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 3], FEAT ? e_src_gid[e + 3] : 0);
+                    const float4* p0 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e], FEAT ? e_src_gid[e] : 0, rowmap);
+                    const float4* p1 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 1], FEAT ? e_src_gid[e + 1] : 0, rowmap);
+                    const float4* p2 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 2], FEAT ? e_src_gid[e + 2] : 0, rowmap);
+                    const float4* p3 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 3], FEAT ? e_src_gid[e + 3] : 0, rowmap);
                     float4 x0 = __ldg(p0 + c), x1 = __ldg(p1 + c), x2 = __ldg(p2 + c), x3 = __ldg(p3 + c);
                     acc.x += x0.x; acc.y += x0.y; acc.z += x0.z; acc.w += x0.w;
                     acc.x += x1.x; acc.y += x1.y; acc.z += x1.z; acc.w += x1.w;
@@ -56,7 +59,7 @@ __global__ void __launch_bounds__(256) agg_kernel(GraphDev g, const HopMeta* __r
                     acc.x += x3.x; acc.y += x3.y; acc.z += x3.z; acc.w += x3.w;
                 }
                 for (; e < e1; ++e) {
-                    float4 x = __ldg(src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e], FEAT ? e_src_gid[e] : 0) + c);
+                    float4 x = __ldg(src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e], FEAT ? e_src_gid[e] : 0, rowmap) + c);
                     acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
                 }
                 acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(256) agg_kernel(GraphDev g, const HopMeta* __r
             }
         }
         const int64_t self = m->src_off[t] + (j - m->dst_off[t]);
-        const float4* ps = src_row<FEAT>(g, h, d, self, FEAT ? dst_gid[j] : 0);
+        const float4* ps = src_row<FEAT>(g, h, d, self, FEAT ? dst_gid[j] : 0, rowmap);
         for (int c = lane; c < d4; c += 32) reinterpret_cast<float4*>(out + (int64_t)St * d)[c] = __ldg(ps + c);
     }
 }
@@ -213,9 +216,19 @@ gsb_status gsb_layer_acat_floats(gsb_blocks_t b, int32_t layer, int32_t d_in, in
     return GSB_OK;
 }
 
+gsb_status gsb_rgcn_layer_fwd_rowmap(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src,
+                                     const int32_t* rowmap, int32_t d_in, const float* W, const float* bias,
+                                     int32_t d_out, int32_t relu, float* h_dst, float* acat, void* stream);
+
 gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src, int32_t d_in,
                               const float* W, const float* bias, int32_t d_out, int32_t relu, float* h_dst,
                               float* acat, void* stream) {
+    return gsb_rgcn_layer_fwd_rowmap(b, arena, layer, h_src, nullptr, d_in, W, bias, d_out, relu, h_dst, acat, stream);
+}
+
+gsb_status gsb_rgcn_layer_fwd_rowmap(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src,
+                                     const int32_t* rowmap, int32_t d_in, const float* W, const float* bias,
+                                     int32_t d_out, int32_t relu, float* h_dst, float* acat, void* stream) {
     Blocks* B = reinterpret_cast<Blocks*>(b);
     GSB_CHECK_ARG(B && arena && W && h_dst && acat, "null argument");
     GSB_CHECK_ARG(h_src || layer == 0, "h_src may be NULL only for layer 0 (features read by gid)");
@@ -229,12 +242,13 @@ gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     const int64_t lda = (int64_t)(g.S + 1) * d_in;
     if (h_src) {
         GSB_LAUNCH(lname("rgcn_agg", layer), agg_kernel<false>, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
-                   hb.seg_ptr, hb.e_src, hb.e_src_gid, hb.dst_gid, h_src, d_in, acat, lda);
+                   hb.seg_ptr, hb.e_src, hb.e_src_gid, hb.dst_gid, h_src, d_in, acat, lda, rowmap);
     } else {
         GSB_CHECK_ARG(g.feat_dim == d_in, "layer 0 with features: d_in %d != feature dim %d", d_in, g.feat_dim);
         for (int t = 0; t < g.T; ++t) GSB_CHECK_ARG(g.feat[t], "features of ntype %d not registered", t);
         GSB_LAUNCH(lname("rgcn_agg", layer), agg_kernel<true>, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
-                   hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid, hb.dst_gid, (const float*)nullptr, d_in, acat, lda);
+                   hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid, hb.dst_gid, (const float*)nullptr, d_in, acat, lda,
+                   (const int32_t*)nullptr);
     }
     RowGroups rg = layer_groups(B, arena, layer);
 #ifdef GSB_SIMT_GEMM

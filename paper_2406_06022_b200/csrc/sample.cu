@@ -196,8 +196,9 @@ __global__ void __launch_bounds__(256) count_kernel(GraphDev g, const HopMeta* _
 }
 
 // ------------------------------------------------------------------------------------
-// fill: warp per segment
+// fill: one group of G lanes per segment (G >= fanout: 8, 16 or 32)
 // ------------------------------------------------------------------------------------
+template <int G>
 __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __restrict__ m,
                                                    const int64_t* __restrict__ dst_gid, int64_t cap_dst,
                                                    const int64_t* __restrict__ seg_ptr, int fanout, Excl ex,
@@ -207,11 +208,13 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
                                                    const int* __restrict__ err) {
     const int S = g.S;
     const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);                       // lane inside the group
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const int64_t n = (*(volatile const int*)err) ? 0 : m->n_dst;
     const uint32_t step = step_dev ? *step_dev : step_host;
     const int64_t nseg = n * S;
-    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < nseg; i += warps) {
+    const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / G;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; i < nseg; i += groups) {
         const int64_t base = seg_ptr[i];
         const int64_t c = seg_ptr[i + 1] - base;
         if (c == 0) continue;
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
         const int64_t degp = has_ex ? deg - excl_count(ex, k0, k1, seg, deg, src_off) : deg;
         if (c == degp) {
             // every non-excluded in-edge, ascending
-            for (int64_t q = lane; q < c; q += 32) {
+            for (int64_t q = gl; q < c; q += G) {
                 int64_t p = has_ex ? excl_map(ex, k0, k1, seg, deg, src_off, q) : q;
                 int64_t u = src_off + seg[p];
                 e_src_gid[base + q] = u;
@@ -243,37 +246,37 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
             }
             continue;
         }
-        // Floyd (R-floyd): draw i (lane i) is unif(j_i + 1), j_i = deg' - c + i
-        const int cc = (int)c;  // c <= fanout <= 32
-        const int32_t jj = (int32_t)(degp - cc + lane);
+        // Floyd (R-floyd): draw i (group lane i) is unif(j_i + 1), j_i = deg' - c + i
+        const int cc = (int)c;  // c <= fanout <= G
+        const int32_t jj = (int32_t)(degp - cc + gl);
         int32_t tdraw = 0;
-        if (lane < cc) {
-            uint32_t c2 = ((uint32_t)(r & 0xFFF) << 20) | ((uint32_t)(hop & 0xF) << 16) | (uint32_t)lane;
+        if (gl < cc) {
+            uint32_t c2 = ((uint32_t)(r & 0xFFF) << 20) | ((uint32_t)(hop & 0xF) << 16) | (uint32_t)gl;
             uint64_t x = keyed_u64(seed, (uint32_t)(uint64_t)v, (uint32_t)((uint64_t)v >> 32), c2, step);
             tdraw = (int32_t)__umul64hi(x, (uint64_t)(jj + 1));
         }
         int32_t sel = INT32_MAX;
         for (int k = 0; k < cc; ++k) {
-            int32_t tk = __shfl_sync(0xffffffffu, tdraw, k);
-            unsigned hit = __ballot_sync(0xffffffffu, lane < k && sel == tk);
-            if (lane == k) sel = hit ? jj : tk;
+            int32_t tk = __shfl_sync(gmask, tdraw, k, G);
+            unsigned hit = __ballot_sync(gmask, gl < k && sel == tk) & gmask;
+            if (gl == k) sel = hit ? jj : tk;
         }
-        // bitonic sort of sel across the warp (ascending; unused lanes hold INT32_MAX)
+        // bitonic sort of sel across the group (ascending; unused lanes hold INT32_MAX)
 #pragma unroll
-        for (int kk = 2; kk <= 32; kk <<= 1) {
+        for (int kk = 2; kk <= G; kk <<= 1) {
 #pragma unroll
             for (int jb = kk >> 1; jb > 0; jb >>= 1) {
-                int32_t o = __shfl_xor_sync(0xffffffffu, sel, jb);
-                bool up = (lane & kk) == 0;
-                bool lower = (lane & jb) == 0;
+                int32_t o = __shfl_xor_sync(gmask, sel, jb, G);
+                bool up = (gl & kk) == 0 || kk == G;
+                bool lower = (gl & jb) == 0;
                 sel = (lower == up) ? min(sel, o) : max(sel, o);
             }
         }
-        if (lane < cc) {
+        if (gl < cc) {
             int64_t p = has_ex ? excl_map(ex, k0, k1, seg, deg, src_off, sel) : sel;
             int64_t u = src_off + seg[p];
-            e_src_gid[base + lane] = u;
-            e_eid[base + lane] = g.eid_base[r] + a + p;
+            e_src_gid[base + gl] = u;
+            e_eid[base + gl] = g.eid_base[r] + a + p;
             if (map[u] < 0) {
                 uint32_t bit = 1u << (u & 31);
                 if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);
@@ -583,9 +586,22 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
         size_t cb = B->cub_bytes;
         GSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, hb.cnt, hb.seg_ptr, (int64_t)(nseg + 1), s));
         count_launch(2);
-        GSB_LAUNCH("sample_fill", fill_kernel, grid_for(nseg * 32, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
-                   hb.dst_gid, hb.cap_dst, hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid,
-                   hb.e_eid, err);
+        {
+            const int G = (f >= 1 && f <= 8) ? 8 : ((f >= 1 && f <= 16) ? 16 : 32);
+            const int grid = grid_for(nseg * G, 256, kNumSMs * 8);
+            if (G == 8)
+                GSB_LAUNCH("sample_fill", fill_kernel<8>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
+                           hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
+                           err);
+            else if (G == 16)
+                GSB_LAUNCH("sample_fill", fill_kernel<16>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
+                           hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
+                           err);
+            else
+                GSB_LAUNCH("sample_fill", fill_kernel<32>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
+                           hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
+                           err);
+        }
         GSB_LAUNCH("bitmap_popc", popc_kernel, grid_for(B->n_words + 1, 256, kNumSMs * 8), 256, 0, s, bitmap,
                    B->n_words, wrank);
         cb = B->cub_bytes;

@@ -66,7 +66,10 @@ class FeatureExchange:
         except Exception:
             pass
 
-    def gather(self, gids: torch.Tensor, n: int, out: torch.Tensor):
+    def gather(self, gids: torch.Tensor, n: int, out: Optional[torch.Tensor] = None):
+        """Rows of gids[:n].  With `out`, unpacks into out (gid order) and returns it; without,
+        returns (rows in exchange order, perm) so that row i of the request is rows[perm[i]]
+        (the consumer reads through perm -- no unpack pass)."""
         import ctypes as C
         import torch.distributed as dist
         from ._lib import call
@@ -86,6 +89,8 @@ class FeatureExchange:
         call("gsb_shard_gather", self.h, P(recv_gid), recv_gid.numel(), P(rows), s)
         back = torch.empty((max(n, 1), self.dim), dtype=torch.float32, device=dev)
         dist.all_to_all_single(back[:n], rows[:sum(recv_splits)], send_splits, recv_splits, group=self.group)  # C5
-        call("gsb_rows_permute", P(back), self.dim, P(perm), None, n, P(out), s)
         self.bytes_sent += (n - send_splits[self.rank]) * 8 + (sum(recv_splits) - recv_splits[self.rank]) * self.dim * 4
+        if out is None:
+            return back, perm
+        call("gsb_rows_permute", P(back), self.dim, P(perm), None, n, P(out), s)
         return out

@@ -289,18 +289,20 @@ class _TrainerBase:
         """gather -> RGCN layers, input layer first (Fig. 8).  With fuse_gather
         (default) layer 0 reads the feature rows by gid inside its aggregation kernel."""
         sm = self.sampler
+        rowmap = None
         if self.exchange is not None:   # partitioned features: NCCL all-to-all fetch (C4/C5)
             gids, n = sm.input_gids()
-            self.exchange.gather(gids, n, self.x0)
-            h = self.x0
+            h, rowmap = self.exchange.gather(gids, n)   # layer 0 reads rows through perm
+            self._keep = (h, rowmap)
         elif self.fuse_gather:
             h = None
         else:
             call("gsb_gather_block_inputs", sm.h, _ptr(sm.arena), _ptr(self.x0), s)
             h = self.x0
         for l in range(self.L):
-            call("gsb_rgcn_layer_fwd", sm.h, _ptr(sm.arena), l, _ptr(h), self.d_in[l], self._pp(f"W{l}"),
-                 self._pp(f"b{l}"), self.hidden, int(l < self.L - 1), _ptr(self.hout[l]), _ptr(self.acat[l]), s)
+            call("gsb_rgcn_layer_fwd_rowmap", sm.h, _ptr(sm.arena), l, _ptr(h), _ptr(rowmap if l == 0 else None),
+                 self.d_in[l], self._pp(f"W{l}"), self._pp(f"b{l}"), self.hidden, int(l < self.L - 1),
+                 _ptr(self.hout[l]), _ptr(self.acat[l]), s)
             h = self.hout[l]
         return h
 
