@@ -36,7 +36,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="gsb", choices=["gsb", "reference"])
-    ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b"])
+    ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b", "amazon_lp", "tiny_lp"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--profile-steps", type=int, default=20)
@@ -58,7 +58,8 @@ def config_for(name: str) -> synth.Config:
 
 
 def cfg_json(cfg: synth.Config, n_gpus: int, extra=None) -> dict:
-    d = {"workload": f"{cfg.name}-shaped synthetic heterograph, RGCN NC train step",
+    task = "RGCN NC train step" if cfg.task == "nc" else f"RGCN + DistMult LP train step (joint-{cfg.num_neg} negatives, contrastive)"
+    d = {"workload": f"{cfg.name}-shaped synthetic heterograph, {task}",
          "ntypes": cfg.num_ntypes, "etypes": cfg.num_etypes, "nodes": cfg.num_nodes, "edges": cfg.num_edges,
          "feat_dim": cfg.feat_dim, "fanouts": cfg.fanouts, "batch_per_gpu": cfg.batch,
          "global_batch": cfg.batch * n_gpus, "hidden": cfg.hidden, "num_classes": cfg.num_classes,
@@ -170,11 +171,17 @@ def kernel_work(name: str, sz: dict, cfg: synth.Config):
 def build_gsb(cfg, device, partition=None):
     """partition = (world, rank) -> features partitioned by node ID (FeatureExchange)."""
     import torch
-    from paper_2406_06022_b200.runtime import GraphStore, RGCNTrainer
+    from paper_2406_06022_b200.runtime import GraphStore, LPTrainer, RGCNTrainer
     st = GraphStore(cfg.counts, cfg.etype_src(), cfg.etype_dst(), device)
+    keep = None
+    if cfg.task == "lp":   # val/test edges of the target etype (and its reverse) leave the graph, P:L170
+        k = torch.from_numpy(synth.lp_keep_mask(cfg).astype(np.uint8)).to(device)
+        keep = {cfg.lp_etype: k}
+        if cfg.lp_rev_etype >= 0:
+            keep[cfg.lp_rev_etype] = k
     for r in range(cfg.num_etypes):
         s, d = synth.etype_coo(cfg, r, backend="torch", device=device)
-        st.load_etype(r, s, d)
+        st.load_etype(r, s, d, None if keep is None else keep.get(r))
         del s, d
     ex = None
     if partition is None:
@@ -189,9 +196,13 @@ def build_gsb(cfg, device, partition=None):
         ex = FeatureExchange(cfg.counts, world, rank, shards, cfg.feat_dim)
         st.feat_dim = cfg.feat_dim
     torch.cuda.synchronize()
-    tr = RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
-                     synth.param_order(cfg), synth.labels(cfg, backend="torch", device=device),
-                     int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
+    if cfg.task == "lp":
+        tr = LPTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_neg, cfg.lp_etype, cfg.lp_rev_etype,
+                       synth.init_params(cfg), synth.param_order(cfg), lr=cfg.lr, rng_seed=cfg.rng_seed)
+    else:
+        tr = RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
+                         synth.param_order(cfg), synth.labels(cfg, backend="torch", device=device),
+                         int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
     tr.exchange = ex
     return st, tr
 
@@ -237,15 +248,35 @@ def run_gsb(args, cfg):
     partitioned = dist is not None and not args.replicate_features
     st, tr = build_gsb(cfg, device, (ws, rank) if partitioned else None)
     setup_s = time.time() - t0
-    train = synth.train_nodes(cfg)
-    per_epoch = max(1, len(train) // cfg.batch)
-    # seed batches (a1): device-resident epoch permutation slices; rank r takes batch step*ws + r
     n_batches = args.warmup + args.steps + args.profile_steps + 8
-    seeds_all = torch.from_numpy(np.stack([synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train)
-                                           for i in range(n_batches)])).to(device)
+    if cfg.task == "lp":
+        lpb = synth.LPBatcher(cfg)
+        uv = [lpb.batch((i * ws + rank) % 100000) for i in range(n_batches)]
+        us_all = torch.from_numpy(np.stack([x[0] for x in uv])).to(device)
+        vs_all = torch.from_numpy(np.stack([x[1] for x in uv])).to(device)
+        host_batches = [np.stack([x[0], x[1]]) for x in uv[:args.steps]]
+    else:
+        train = synth.train_nodes(cfg)
+        per_epoch = max(1, len(train) // cfg.batch)
+        # seed batches (a1): device-resident epoch permutation slices; rank r takes batch step*ws + r
+        seeds_all = torch.from_numpy(np.stack([synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train)
+                                               for i in range(n_batches)])).to(device)
+        host_batches = [synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train) for i in range(args.steps)]
+
+    def fb(i):
+        if cfg.task == "lp":
+            tr.forward_backward(us_all[i], vs_all[i], i * ws + rank)
+        else:
+            tr.forward_backward(seeds_all[i], i * ws + rank)
+
+    def load(i):
+        if cfg.task == "lp":
+            tr.load_inputs(us_all[i], vs_all[i])
+        else:
+            tr.load_inputs(seeds_all[i])
 
     def step(i):
-        tr.forward_backward(seeds_all[i], i * ws + rank)
+        fb(i)
         if dist is not None:
             dist.all_reduce(tr.grad)          # C6: NCCL all-reduce of the flat dense grads
             tr.grad.mul_(1.0 / ws)
@@ -265,12 +296,12 @@ def run_gsb(args, cfg):
     # word and Adam's t on the device, inputs are copied into the graph's fixed seed buffer
     use_graph = not args.no_graph and not partitioned   # all-to-all sizes are host-synced
     if use_graph:
-        tr.load_inputs(seeds_all[W - 2])
+        load(W - 2)
         tr.capture(step0=(W - 2) * ws + rank, ws=ws, allreduce=allreduce if dist is not None else None)
 
     def run(i):
         if use_graph:
-            tr.seeds_dev.copy_(seeds_all[i], non_blocking=True)
+            load(i)
             tr.replay()
         else:
             step(i)
@@ -306,7 +337,7 @@ def run_gsb(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    seeds_per_s = cfg.batch * ws * args.steps / (ms / 1e3)
+    seeds_per_s = cfg.batch * ws * args.steps / (ms / 1e3)   # NC: seeds; LP: positive edges
 
     # ---- per-kernel profile: eager steps, each preceded by a 3 ms spin kernel so the host
     # enqueues the whole step before it starts (events then time kernels, not launch gaps)
@@ -322,7 +353,10 @@ def run_gsb(args, cfg):
     # re-sampling the same batches reproduces them bit-exactly
     sizes = []
     for i in range(base, base + args.profile_steps):
-        tr.sampler.sample(seeds_all[i], tr.rng_seed, i * ws + rank)
+        if cfg.task == "lp":
+            fb(i)          # sampling inputs depend on the negatives/seeds of the step
+        else:
+            tr.sampler.sample(seeds_all[i], tr.rng_seed, i * ws + rank)
         sizes.append(block_sizes(tr, cfg))
     buf = C.create_string_buffer(1 << 16)
     _lib.call("gsb_profile_dump", buf, len(buf))
@@ -334,35 +368,39 @@ def run_gsb(args, cfg):
         prof[n] = {"launches": int(c), "total_ms": float(t)}
     edges_per_step = float(np.mean([sum(s["n_edges"]) for s in sizes]))
     # ---- e2e: public API with host buffers (pinned seeds H2D + loss D2H every step)
-    seeds_host = torch.from_numpy(np.stack([synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train)
-                                            for i in range(args.steps)])).pin_memory()
+    host_pinned = [torch.from_numpy(b).pin_memory() for b in host_batches]
     loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for i in range(args.steps):
-        if dist is None:
-            tr.train_step_host(seeds_host[i], base + args.profile_steps + i, loss_host, eager=not use_graph)
+        hb = host_pinned[i]
+        if cfg.task == "lp":
+            tr.pos_u.copy_(hb[0], non_blocking=True)
+            tr.pos_v.copy_(hb[1], non_blocking=True)
         else:
-            n = seeds_host[i].numel()
-            tr.seeds_dev[:n].copy_(seeds_host[i], non_blocking=True)
-            if use_graph:
-                tr.replay()
+            tr.seeds_dev[:hb.numel()].copy_(hb, non_blocking=True)
+        if use_graph:
+            tr.replay()
+        else:
+            if cfg.task == "lp":
+                tr._step_body(None, base + i)
             else:
-                tr.forward_backward(tr.seeds_dev[:n], base + i)
+                tr.forward_backward(tr.seeds_dev[:hb.numel()], base + i)
+            if dist is not None:
                 dist.all_reduce(tr.grad)
                 tr.grad.mul_(1.0 / ws)
-                tr.optimizer_step()
-            loss_host.copy_(tr.loss, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            tr.optimizer_step()
+        loss_host.copy_(tr.loss, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
     e2e_s = time.perf_counter() - t0
     if dist is not None:
         t = torch.tensor([e2e_s], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": cfg.batch * ws * args.steps / e2e_s, "unit": UNIT,
-           "h2d_bytes_per_step": int(seeds_host[0].numel() * 8), "d2h_bytes_per_step": 4,
+    e2e = {"value": cfg.batch * ws * args.steps / e2e_s, "unit": UNIT if cfg.task == "nc" else "pos_edges/s",
+           "h2d_bytes_per_step": int(host_pinned[0].numel() * 8), "d2h_bytes_per_step": 4,
            "final_loss": float(loss_host[0])}
     if rank != 0:
         if dist is not None:
@@ -387,6 +425,13 @@ def run_gsb(args, cfg):
             roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
                     "frac": ach / pk["fp32_tflops"], "traffic": None,
                     "peak_src": "FP32 FFMA: 148 SMs x 128 lanes x 2 x sm_max_mhz (DESIGN.md)"}
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+            if dom in tj:
+                roof["traffic"] = tj[dom]["bytes"]
+                roof["traffic_src"] = tj[dom]["capture"]
+        except Exception:
+            pass
         roof["avg_launch_us"] = avg_ms * 1e3
         roof["launches_per_step"] = launches_per_step
         roof["algorithmic_per_launch"] = per_launch_work
@@ -397,8 +442,10 @@ def run_gsb(args, cfg):
     par = ("single" if ws == 1 else
            (f"dp{ws}: features partitioned by node ID (NCCL all-to-all fetch), topology replicated, "
             f"NCCL grad all-reduce" if partitioned else f"dp{ws}: graph + features replicated, NCCL grad all-reduce"))
+    unit = UNIT if cfg.task == "nc" else "pos_edges/s"
+    metric = METRIC if cfg.task == "nc" else "RGCN+DistMult LP train positive edges/sec (joint negatives) on B200"
     line = {
-        "metric": METRIC, "value": seeds_per_s, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "metric": metric, "value": seeds_per_s, "unit": unit, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded hash generator, synth/)",
         "config": cfg_json(cfg, ws, {"parallelism": par, "cuda_graph": use_graph}),
@@ -491,7 +538,7 @@ def main():
     if out is None:
         return
     line, st, tr = out
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and cfg.task == "nc":
         del tr, st
         import torch
         torch.cuda.empty_cache()

@@ -24,7 +24,7 @@ __device__ __forceinline__ const float4* src_row(const GraphDev& g, const float*
 
 // FEAT: h_src rows come from the feature tables via e_src_gid / dst_gid (no x0 buffer)
 template <bool FEAT>
-__global__ void __launch_bounds__(256) agg_kernel(GraphDev g, const HopMeta* __restrict__ m,
+__global__ void __launch_bounds__(256, 6) agg_kernel(GraphDev g, const HopMeta* __restrict__ m,
                                                   const int64_t* __restrict__ seg_ptr,
                                                   const int32_t* __restrict__ e_src,
                                                   const int64_t* __restrict__ e_src_gid,
@@ -46,21 +46,28 @@ __global__ void __launch_bounds__(256) agg_kernel(GraphDev g, const HopMeta* __r
             const float inv = (e1 > e0) ? 1.f / (float)(e1 - e0) : 0.f;
             for (int c = lane; c < d4; c += 32) {
                 float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                int64_t e = e0;
-                for (; e + 4 <= e1; e += 4) {
-                    const float4* p0 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e], FEAT ? e_src_gid[e] : 0, rowmap);
-                    const float4* p1 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 1], FEAT ? e_src_gid[e + 1] : 0, rowmap);
-                    const float4* p2 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 2], FEAT ? e_src_gid[e + 2] : 0, rowmap);
-                    const float4* p3 = src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e + 3], FEAT ? e_src_gid[e + 3] : 0, rowmap);
-                    float4 x0 = __ldg(p0 + c), x1 = __ldg(p1 + c), x2 = __ldg(p2 + c), x3 = __ldg(p3 + c);
-                    acc.x += x0.x; acc.y += x0.y; acc.z += x0.z; acc.w += x0.w;
-                    acc.x += x1.x; acc.y += x1.y; acc.z += x1.z; acc.w += x1.w;
-                    acc.x += x2.x; acc.y += x2.y; acc.z += x2.z; acc.w += x2.w;
-                    acc.x += x3.x; acc.y += x3.y; acc.z += x3.z; acc.w += x3.w;
-                }
-                for (; e < e1; ++e) {
-                    float4 x = __ldg(src_row<FEAT>(g, h, d, FEAT ? 0 : e_src[e], FEAT ? e_src_gid[e] : 0, rowmap) + c);
-                    acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+                for (int64_t cb = e0; cb < e1; cb += 32) {
+                    // one coalesced load of up to 32 source keys, broadcast by shuffle
+                    const int64_t key = (cb + lane < e1) ? (FEAT ? e_src_gid[cb + lane] : (int64_t)e_src[cb + lane]) : 0;
+                    const int cnt = (int)min((int64_t)32, e1 - cb);
+                    int k = 0;
+                    for (; k + 4 <= cnt; k += 4) {
+                        const int64_t k0 = __shfl_sync(0xffffffffu, key, k), k1 = __shfl_sync(0xffffffffu, key, k + 1);
+                        const int64_t k2 = __shfl_sync(0xffffffffu, key, k + 2), k3 = __shfl_sync(0xffffffffu, key, k + 3);
+                        float4 x0 = __ldg(src_row<FEAT>(g, h, d, k0, k0, rowmap) + c);
+                        float4 x1 = __ldg(src_row<FEAT>(g, h, d, k1, k1, rowmap) + c);
+                        float4 x2 = __ldg(src_row<FEAT>(g, h, d, k2, k2, rowmap) + c);
+                        float4 x3 = __ldg(src_row<FEAT>(g, h, d, k3, k3, rowmap) + c);
+                        acc.x += x0.x; acc.y += x0.y; acc.z += x0.z; acc.w += x0.w;
+                        acc.x += x1.x; acc.y += x1.y; acc.z += x1.z; acc.w += x1.w;
+                        acc.x += x2.x; acc.y += x2.y; acc.z += x2.z; acc.w += x2.w;
+                        acc.x += x3.x; acc.y += x3.y; acc.z += x3.z; acc.w += x3.w;
+                    }
+                    for (; k < cnt; ++k) {
+                        const int64_t kk = __shfl_sync(0xffffffffu, key, k);
+                        float4 x = __ldg(src_row<FEAT>(g, h, d, kk, kk, rowmap) + c);
+                        acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+                    }
                 }
                 acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
                 reinterpret_cast<float4*>(out + (int64_t)s * d)[c] = acc;

@@ -355,6 +355,29 @@ def lp_train_edges(cfg: Config, step: int) -> Tuple[np.ndarray, np.ndarray]:
     return (s[ids].astype(np.int64) + off[e.src], d[ids].astype(np.int64) + off[e.dst])
 
 
+class LPBatcher:
+    """Cached LP batch source (same batches as lp_train_edges, without regenerating the COO)."""
+
+    def __init__(self, cfg: Config):
+        self.cfg = cfg
+        e = cfg.etypes[cfg.lp_etype]
+        h = hash32(cfg.gen_seed, 4000, np.arange(e.num_edges, dtype=np.uint64))
+        self.tr = np.nonzero((h % np.uint64(1000)) < np.uint64(int(cfg.train_frac * 1000)))[0]
+        self.s, self.d = etype_coo(cfg, cfg.lp_etype)
+        self.off = cfg.node_off
+        self.e = e
+        self._perm = {}
+
+    def batch(self, step: int):
+        B = self.cfg.batch
+        per_epoch = max(1, len(self.tr) // B)
+        ep, k = divmod(step, per_epoch)
+        if ep not in self._perm:
+            self._perm = {ep: epoch_perm(len(self.tr), ep, self.cfg.gen_seed + 1)}
+        ids = self.tr[self._perm[ep][k * B:(k + 1) * B]]
+        return (self.s[ids].astype(np.int64) + self.off[self.e.src], self.d[ids].astype(np.int64) + self.off[self.e.dst])
+
+
 def lp_keep_mask(cfg: Config) -> np.ndarray:
     """Val/test LP edges are removed from the training graph: keep = train split."""
     e = cfg.etypes[cfg.lp_etype]
