@@ -408,7 +408,9 @@ def run_gsb(args, cfg):
         return None
     # ---- roofline of the dominant kernel
     pk = peaks()
-    dom = max(prof.items(), key=lambda kv: kv[1]["total_ms"])[0]
+    # dominant kernel = the most expensive one with an algorithmic-work model
+    ranked = [k for k, _ in sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])]
+    dom = next((k for k in ranked if kernel_work(k, sizes[0], cfg)[0] is not None), ranked[0])
     kind, _ = kernel_work(dom, sizes[0], cfg)
     roof = None
     if kind is not None:

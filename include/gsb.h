@@ -241,7 +241,8 @@ gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, i
  * S:L405-408; §8(a) a8):  logits = h Wc + bc ; loss = mean_i(lse_i - logit_{i,y_i})
  *   y_i = labels[seed_gid[i] - label_gid_base].
  * Writes: logits_ws [n][ceil4(C)] (scratch, rows padded to a multiple of 4), loss (device fp32 scalar), dh [n][d], dWc [d][C],
- * dbc [C] (overwritten).  row_loss_ws: device fp32 [n] scratch.
+ * dbc [C] (overwritten).  row_loss_ws: device fp32 [n + 640] scratch (row losses, then the
+ * fused mean's block partials and ticket word); zero-fill it once before the first call.
  * ==================================================================================== */
 gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, const float* bc, int32_t C,
                        const int32_t* labels, const int64_t* seed_gid, int64_t label_gid_base, float* logits_ws,

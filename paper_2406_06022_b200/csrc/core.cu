@@ -151,24 +151,46 @@ gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_de
 // ------------------------------------------------------------------------------------
 // Adam (bias-corrected), float4 vectorised
 // ------------------------------------------------------------------------------------
-__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ gr, float* __restrict__ m,
-                            float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps, float c1,
-                            float c2, const int32_t* __restrict__ t_dev) {
-    if (t_dev) {   // bias corrections from the device step counter (graph replay)
-        const float t = (float)*t_dev;
-        c1 = 1.f - powf(b1, t);
-        c2 = 1.f - powf(b2, t);
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const float* __restrict__ gr,
+                                                   float* __restrict__ m, float* __restrict__ v, int64_t n, float lr,
+                                                   float b1, float b2, float eps, float c1, float c2,
+                                                   const int32_t* __restrict__ t_dev) {
+    __shared__ float sc[2];
+    if (t_dev) {   // bias corrections from the device step counter (graph replay), once per block
+        if (threadIdx.x == 0) {
+            const float t = (float)*t_dev;
+            sc[0] = 1.f - powf(b1, t);
+            sc[1] = 1.f - powf(b2, t);
+        }
+        __syncthreads();
+        c1 = sc[0];
+        c2 = sc[1];
     }
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-        float g = gr[i];
-        float mi = b1 * m[i] + (1.f - b1) * g;
-        float vi = b2 * v[i] + (1.f - b2) * g * g;
+    const float a1 = lr / c1, r2 = 1.f / c2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n4 = n >> 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 g = reinterpret_cast<const float4*>(gr)[i];
+        float4 mi = reinterpret_cast<float4*>(m)[i];
+        float4 vi = reinterpret_cast<float4*>(v)[i];
+        float4 pi = reinterpret_cast<float4*>(p)[i];
+#define ADAM1(c)                                         \
+        mi.c = b1 * mi.c + (1.f - b1) * g.c;             \
+        vi.c = b2 * vi.c + (1.f - b2) * g.c * g.c;       \
+        pi.c -= a1 * mi.c / (sqrtf(vi.c * r2) + eps);
+        ADAM1(x) ADAM1(y) ADAM1(z) ADAM1(w)
+#undef ADAM1
+        reinterpret_cast<float4*>(m)[i] = mi;
+        reinterpret_cast<float4*>(v)[i] = vi;
+        reinterpret_cast<float4*>(p)[i] = pi;
+    }
+    for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float g = gr[i];
+        const float mi = b1 * m[i] + (1.f - b1) * g;
+        const float vi = b2 * v[i] + (1.f - b2) * g * g;
         m[i] = mi;
         v[i] = vi;
-        float mh = mi / c1;
-        float vh = vi / c2;
-        p[i] -= lr * mh / (sqrtf(vh) + eps);
+        p[i] -= a1 * mi / (sqrtf(vi * r2) + eps);
     }
 }
 
@@ -390,7 +412,9 @@ gsb_status gsb_adam_step(float* p, const float* g, float* m, float* v, int64_t n
     if (n == 0) return GSB_OK;
     float c1 = 1.f - powf(b1, (float)t);
     float c2 = 1.f - powf(b2, (float)t);
-    GSB_LAUNCH("adam", adam_kernel, grid_for(n, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream, p, g, m, v, n, lr,
+    GSB_CHECK_ARG(((uintptr_t)p & 15) == 0 && ((uintptr_t)g & 15) == 0 && ((uintptr_t)m & 15) == 0 &&
+                      ((uintptr_t)v & 15) == 0, "adam buffers must be 16-byte aligned");
+    GSB_LAUNCH("adam", adam_kernel, grid_for((n + 3) / 4, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream, p, g, m, v, n, lr,
                b1, b2, eps, c1, c2, t_dev);
     return GSB_OK;
 }

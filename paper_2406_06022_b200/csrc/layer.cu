@@ -115,11 +115,18 @@ __global__ void __launch_bounds__(256) scatter_kernel(GraphDev g, const HopMeta*
 // ------------------------------------------------------------------------------------
 // softmax cross-entropy, warp per row; logits are overwritten by dlogits
 // ------------------------------------------------------------------------------------
+// Softmax CE, warp per row.  The batch mean is fused: every block writes the sum of its rows'
+// losses to part[blockIdx]; the last block to finish (ticket) adds the partials in block order
+// (deterministic) and resets the ticket for the next launch / graph replay.
 __global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int64_t n, int C, int64_t ldl,
                                                  const int32_t* __restrict__ labels,
                                                  const int64_t* __restrict__ seed_gid, int64_t base,
-                                                 float* __restrict__ row_loss) {
+                                                 float* __restrict__ row_loss, float* __restrict__ part,
+                                                 unsigned* __restrict__ ticket, float* __restrict__ loss) {
+    __shared__ float wsum[8];
+    __shared__ bool last;
     const int lane = threadIdx.x & 31;
+    float mine = 0.f;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const float invn = 1.f / (float)n;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
@@ -132,9 +139,28 @@ __global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int
         for (int c = lane; c < C; c += 32) se += expf(lg[c] - mx);
         for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
         const float lse = mx + logf(se);
-        if (lane == 0) row_loss[i] = lse - lg[y];
+        const float li = lse - lg[y];
+        if (lane == 0) row_loss[i] = li;
+        mine += li;
         __syncwarp();
         for (int c = lane; c < C; c += 32) lg[c] = (expf(lg[c] - lse) - (c == y ? 1.f : 0.f)) * invn;
+    }
+    if (lane == 0) wsum[threadIdx.x >> 5] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float b = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += wsum[w];
+        part[blockIdx.x] = b;
+        __threadfence();
+        last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        float tot = 0.f;
+        for (unsigned b = 0; b < gridDim.x; ++b) tot += ((volatile float*)part)[b];
+        *loss = tot / (float)n;
+        *ticket = 0u;
     }
 }
 
@@ -386,9 +412,15 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         if (st != GSB_OK) return st;
     }
 #endif
-    GSB_LAUNCH("nc_ce", ce_kernel, grid_for(n * 32, 256, kNumSMs * 4), 256, 0, s, logits_ws, n, C, ldl, labels,
-               seed_gid, label_gid_base, row_loss_ws);
-    GSB_LAUNCH("nc_mean", mean_kernel, 1, 1024, 0, s, row_loss_ws, n, loss);
+    {
+        // fused batch mean: partials and the ticket word live in row_loss_ws after the n row
+        // losses (caller-owned scratch of n + 640 floats, zero-filled before first use)
+        const int grid = grid_for(n * 32, 256, kNumSMs * 4);
+        float* part = row_loss_ws + ((n + 31) / 32) * 32;
+        unsigned* ticket = reinterpret_cast<unsigned*>(part + kNumSMs * 4);
+        GSB_LAUNCH("nc_ce", ce_kernel, grid, 256, 0, s, logits_ws, n, C, ldl, labels, seed_gid, label_gid_base,
+                   row_loss_ws, part, ticket, loss);
+    }
     if (dWc || dbc) {
         GSB_CHECK_ARG(dWc && dbc, "dWc and dbc go together");
         GSB_CUDA(cudaMemsetAsync(dWc, 0, sizeof(float) * (size_t)d * C, s));

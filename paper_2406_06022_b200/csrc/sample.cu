@@ -32,7 +32,44 @@ struct Excl {
     const uint64_t* keys;
     int64_t n;
     int32_t etype, rev;
+    const int64_t* lo;    // [n] first excluded position of key k inside its dst segment
+    const int64_t* cum;   // [n+1] exclusive prefix of the range lengths (duplicates: length 0)
 };
+
+// Position range of every sorted exclusion key inside its destination's CSC segment
+// (one binary search pair per key, once per batch).  Duplicate keys get an empty range at the
+// previous key's end so that (lo - cum) stays non-decreasing within a segment.
+__global__ void excl_ranges_kernel(GraphDev g, const uint64_t* __restrict__ keys, int64_t n, int32_t etype,
+                                   int32_t rev, int64_t* __restrict__ lo_out, int64_t* __restrict__ len_out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= n; k += (int64_t)gridDim.x * blockDim.x) {
+        if (k == n) {
+            len_out[k] = 0;
+            continue;
+        }
+        const uint64_t key = keys[k];
+        int64_t lo = 0, hi = 0;
+        if (key != ~0ull) {
+            const int r = (key >> 62) ? rev : etype;
+            const int64_t v = (int64_t)((key >> 31) & 0x7FFFFFFFull);
+            const int64_t u = (int64_t)(key & 0x7FFFFFFFull);
+            const int t = type_of(g, v);
+            const int64_t vl = v - g.node_off[t];
+            const int64_t a = g.indptr[r][vl];
+            const int64_t deg = g.indptr[r][vl + 1] - a;
+            const int32_t ul = (int32_t)(u - g.node_off[g.src_t[r]]);
+            const int32_t* seg = g.indices[r] + a;
+            int64_t l = 0, h = deg;
+            while (l < h) { int64_t m = (l + h) >> 1; if (seg[m] < ul) l = m + 1; else h = m; }
+            lo = l;
+            h = deg;
+            while (l < h) { int64_t m = (l + h) >> 1; if (seg[m] < ul + 1) l = m + 1; else h = m; }
+            hi = l;
+            if (k > 0 && keys[k - 1] == key) lo = hi;   // duplicate pair: empty range
+        }
+        lo_out[k] = lo;
+        len_out[k] = hi - lo;
+    }
+}
 
 __global__ void excl_keys_kernel(const int64_t* __restrict__ u, const int64_t* __restrict__ v, int64_t n, int rev,
                                  uint64_t* __restrict__ keys) {
@@ -70,39 +107,25 @@ __device__ __forceinline__ void excl_range(const Excl& x, int r, int64_t v, int6
     k1 = lower_bound_u64(x.keys, x.n, base + (1ull << 31));
 }
 
-// Iterate distinct excluded sources in ascending order, yielding their position ranges
-// [lo, hi) inside the segment (indices sorted by src).  Returns the total excluded.
-__device__ __forceinline__ int64_t excl_count(const Excl& x, int64_t k0, int64_t k1, const int32_t* seg, int64_t deg,
-                                              int64_t src_off) {
-    int64_t tot = 0;
-    uint64_t prev = ~0ull;
-    for (int64_t k = k0; k < k1; ++k) {
-        uint64_t key = x.keys[k];
-        if (key == prev) continue;
-        prev = key;
-        int32_t ul = (int32_t)((int64_t)(key & 0x7FFFFFFFull) - src_off);
-        int64_t lo = lower_bound_i32(seg, deg, ul);
-        int64_t hi = lower_bound_i32(seg, deg, ul + 1);
-        tot += hi - lo;
-    }
-    return tot;
+// Excluded positions of the segment whose keys are [k0, k1): their ranges are disjoint and
+// ascending (keys sorted by src, segment sorted by src).
+__device__ __forceinline__ int64_t excl_count(const Excl& x, int64_t k0, int64_t k1, const int32_t*, int64_t,
+                                              int64_t) {
+    return x.cum[k1] - x.cum[k0];
 }
 
-// Map rank q among non-excluded positions to a segment position.
-__device__ __forceinline__ int64_t excl_map(const Excl& x, int64_t k0, int64_t k1, const int32_t* seg, int64_t deg,
-                                            int64_t src_off, int64_t q) {
-    int64_t p = q;
-    uint64_t prev = ~0ull;
-    for (int64_t k = k0; k < k1; ++k) {
-        uint64_t key = x.keys[k];
-        if (key == prev) continue;
-        prev = key;
-        int32_t ul = (int32_t)((int64_t)(key & 0x7FFFFFFFull) - src_off);
-        int64_t lo = lower_bound_i32(seg, deg, ul);
-        int64_t hi = lower_bound_i32(seg, deg, ul + 1);
-        if (p >= lo) p += hi - lo;
+// Map rank q among non-excluded positions to a segment position: p = q + (lengths of the
+// ranges starting at or before the q-th non-excluded position); binary search over
+// nonexcl_before(k) = lo_k - (cum_k - cum_k0), which is non-decreasing in k.
+__device__ __forceinline__ int64_t excl_map(const Excl& x, int64_t k0, int64_t k1, const int32_t*, int64_t, int64_t,
+                                            int64_t q) {
+    const int64_t c0 = x.cum[k0];
+    int64_t l = k0, h = k1;   // first k with nonexcl_before(k) > q
+    while (l < h) {
+        const int64_t m = (l + h) >> 1;
+        if (x.lo[m] - (x.cum[m] - c0) <= q) l = m + 1; else h = m;
     }
-    return p;
+    return q + (x.cum[l] - c0);
 }
 
 // ------------------------------------------------------------------------------------
@@ -473,6 +496,8 @@ gsb_status gsb_blocks_create(gsb_graph_t gh, int32_t L, const int32_t* fanouts, 
     if (max_excl > 0) {
         cub::DeviceRadixSort::SortKeys(nullptr, t, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)(2 * max_excl), 0, 64);
         cb = std::max(cb, t);
+        cub::DeviceScan::ExclusiveSum(nullptr, t, (int64_t*)nullptr, (int64_t*)nullptr, (int64_t)(2 * max_excl + 1));
+        cb = std::max(cb, t);
     }
     B->cub_bytes = cb;
     size_t off = 0;
@@ -497,7 +522,7 @@ gsb_status gsb_blocks_create(gsb_graph_t gh, int32_t L, const int32_t* fanouts, 
     B->off_map = take(sizeof(int32_t) * G->total_nodes);
     B->off_bitmap = take(sizeof(uint32_t) * B->n_words);
     B->off_wrank = take(sizeof(int32_t) * (B->n_words + 1));
-    B->off_excl = take(sizeof(uint64_t) * 4 * (max_excl > 0 ? max_excl : 1));
+    B->off_excl = take(sizeof(uint64_t) * (8 * (max_excl > 0 ? max_excl : 1) + 2));
     B->off_cub = take(cb);
     B->total_bytes = off;
     *out = reinterpret_cast<gsb_blocks_t>(B);
@@ -561,17 +586,26 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
     int32_t* wrank = at<int32_t>(arena, B->off_wrank);
     void* cub_tmp = at<char>(arena, B->off_cub);
 
-    Excl ex{nullptr, 0, excl_etype, excl_rev_etype >= 0 ? excl_rev_etype : -2};
+    Excl ex{nullptr, 0, excl_etype, excl_rev_etype >= 0 ? excl_rev_etype : -2, nullptr, nullptr};
     if (n_excl > 0) {
         uint64_t* kin = at<uint64_t>(arena, B->off_excl);
         uint64_t* kout = kin + 2 * B->max_excl;
+        int64_t* elo = reinterpret_cast<int64_t*>(kout + 2 * B->max_excl);
+        int64_t* ecum = elo + 2 * B->max_excl;
         GSB_LAUNCH("excl_keys", excl_keys_kernel, grid_for(n_excl, 256, 64), 256, 0, s, excl_u, excl_v, n_excl,
                    excl_rev_etype >= 0 ? 1 : 0, kin);
         size_t cb = B->cub_bytes;
         GSB_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, cb, kin, kout, (int64_t)(2 * n_excl), 0, 64, s));
         count_launch(16);
+        GSB_LAUNCH("excl_ranges", excl_ranges_kernel, grid_for(2 * n_excl + 1, 256, kNumSMs * 4), 256, 0, s, g, kout,
+                   2 * n_excl, excl_etype, excl_rev_etype >= 0 ? excl_rev_etype : -2, elo, ecum);
+        cb = B->cub_bytes;
+        GSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, ecum, ecum, (int64_t)(2 * n_excl + 1), s));
+        count_launch(2);
         ex.keys = kout;
         ex.n = 2 * n_excl;
+        ex.lo = elo;
+        ex.cum = ecum;
     }
 
     GSB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));

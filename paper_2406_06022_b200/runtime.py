@@ -373,7 +373,7 @@ class RGCNTrainer(_TrainerBase):
         self.labels = labels.to(dev, dtype=torch.int32).contiguous()
         self.label_base = int(label_gid_base)
         self.logits = torch.empty((batch, (max(num_classes, 1) + 3) // 4 * 4), dtype=torch.float32, device=dev)
-        self.row_loss = torch.empty(batch, dtype=torch.float32, device=dev)
+        self.row_loss = torch.zeros(batch + 640, dtype=torch.float32, device=dev)   # + fused-mean scratch
         self.seeds_dev = torch.empty(batch, dtype=torch.int64, device=dev)
 
     def _step_body(self, stream=None, step: int = 0, step_dev=None, seeds=None):

@@ -322,8 +322,16 @@ def train_nodes(cfg: Config) -> np.ndarray:
     return np.nonzero((h % np.uint64(1000)) < np.uint64(int(cfg.train_frac * 1000)))[0].astype(np.int64)
 
 
+_PERM_CACHE = {}
+
+
 def epoch_perm(n: int, epoch: int, seed: int) -> np.ndarray:
-    return np.random.Generator(np.random.PCG64([seed, epoch])).permutation(n)
+    key = (n, epoch, seed)
+    if key not in _PERM_CACHE:
+        if len(_PERM_CACHE) > 8:
+            _PERM_CACHE.clear()
+        _PERM_CACHE[key] = np.random.Generator(np.random.PCG64([seed, epoch])).permutation(n)
+    return _PERM_CACHE[key]
 
 
 def nc_seeds(cfg: Config, step: int, train: Optional[np.ndarray] = None) -> np.ndarray:
