@@ -41,8 +41,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
-    ap.add_argument("--replicate-features", action="store_true",
-                    help="N>1: replicate the feature tables instead of partitioning them by node ID")
+    ap.add_argument("--features", default="peer", choices=["peer", "alltoall", "replicate"],
+                    help="N>1 feature store: partitioned by node ID and read over NVLink inside the kernels "
+                         "(peer, default), partitioned + NCCL all-to-all fetch (alltoall), or replicated")
     return ap.parse_args()
 
 
@@ -168,8 +169,9 @@ def kernel_work(name: str, sz: dict, cfg: synth.Config):
 
 
 # ------------------------------------------------------------------------------ gsb arm
-def build_gsb(cfg, device, partition=None):
-    """partition = (world, rank) -> features partitioned by node ID (FeatureExchange)."""
+def build_gsb(cfg, device, partition=None, mode="peer"):
+    """partition = (world, rank) -> features partitioned by node ID: mode "peer" maps every
+    rank's shard over NVLink (PeerFeatures), "alltoall" fetches rows with NCCL (FeatureExchange)."""
     import torch
     from paper_2406_06022_b200.runtime import GraphStore, LPTrainer, RGCNTrainer
     st = GraphStore(cfg.counts, cfg.etype_src(), cfg.etype_dst(), device)
@@ -188,13 +190,16 @@ def build_gsb(cfg, device, partition=None):
         for t in range(cfg.num_ntypes):
             st.set_features(t, synth.feature_table(cfg, t, backend="torch", device=device))
     else:
-        from paper_2406_06022_b200.dist import FeatureExchange, balanced_bounds
+        from paper_2406_06022_b200.dist import FeatureExchange, PeerFeatures, balanced_bounds
         world, rank = partition
         b = balanced_bounds(cfg.counts, world)
         shards = [synth.feature_rows(cfg, t, torch.arange(int(b[t][rank]), int(b[t][rank + 1]), device=device),
                                      "torch", device) for t in range(cfg.num_ntypes)]
-        ex = FeatureExchange(cfg.counts, world, rank, shards, cfg.feat_dim)
-        st.feat_dim = cfg.feat_dim
+        if mode == "peer":
+            st._peer = PeerFeatures(st, cfg.counts, world, rank, shards, cfg.feat_dim)
+        else:
+            ex = FeatureExchange(cfg.counts, world, rank, shards, cfg.feat_dim)
+            st.feat_dim = cfg.feat_dim
     torch.cuda.synchronize()
     if cfg.task == "lp":
         tr = LPTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_neg, cfg.lp_etype, cfg.lp_rev_etype,
@@ -245,8 +250,8 @@ def run_gsb(args, cfg):
         dist.init_process_group("nccl", device_id=torch.device(device))
     from paper_2406_06022_b200 import _lib
     t0 = time.time()
-    partitioned = dist is not None and not args.replicate_features
-    st, tr = build_gsb(cfg, device, (ws, rank) if partitioned else None)
+    partitioned = dist is not None and args.features != "replicate"
+    st, tr = build_gsb(cfg, device, (ws, rank) if partitioned else None, args.features)
     setup_s = time.time() - t0
     n_batches = args.warmup + args.steps + args.profile_steps + 8
     if cfg.task == "lp":
@@ -294,7 +299,7 @@ def run_gsb(args, cfg):
         raise RuntimeError("device-side sampling error latched")
     # ---- capture ONE whole step (sample..Adam) in a CUDA graph; replays advance the RNG step
     # word and Adam's t on the device, inputs are copied into the graph's fixed seed buffer
-    use_graph = not args.no_graph and not partitioned   # all-to-all sizes are host-synced
+    use_graph = not args.no_graph and tr.exchange is None   # all-to-all sizes are host-synced
     if use_graph:
         load(W - 2)
         tr.capture(step0=(W - 2) * ws + rank, ws=ws, allreduce=allreduce if dist is not None else None)
@@ -441,9 +446,12 @@ def run_gsb(args, cfg):
     kernels = {k: {"us_per_step": v["total_ms"] * 1e3 / args.profile_steps,
                    "share": v["total_ms"] / args.profile_steps / step_ms_prof} for k, v in
                sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])}
-    par = ("single" if ws == 1 else
-           (f"dp{ws}: features partitioned by node ID (NCCL all-to-all fetch), topology replicated, "
-            f"NCCL grad all-reduce" if partitioned else f"dp{ws}: graph + features replicated, NCCL grad all-reduce"))
+    par = ("single" if ws == 1 else {
+        "peer": f"dp{ws}: features partitioned by node ID, read over NVLink (CUDA IPC) inside the fused "
+                f"gather+aggregation kernel; topology replicated; NCCL grad all-reduce in the CUDA graph",
+        "alltoall": f"dp{ws}: features partitioned by node ID, NCCL all-to-all fetch; topology replicated; "
+                    f"NCCL grad all-reduce",
+        "replicate": f"dp{ws}: graph + features replicated, NCCL grad all-reduce"}[args.features])
     unit = UNIT if cfg.task == "nc" else "pos_edges/s"
     metric = METRIC if cfg.task == "nc" else "RGCN+DistMult LP train positive edges/sec (joint negatives) on B200"
     line = {

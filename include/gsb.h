@@ -303,6 +303,24 @@ gsb_status gsb_rows_permute(const float* rows, int32_t d, const int32_t* perm, c
                             float* out, void* stream);
 
 /* ======================================================================================
+ * Peer feature access over NVLink (§8(e); P:L86 distributed tensors).  Each rank keeps only
+ * its node-ID range of every ntype; the other ranks' shards are mapped with CUDA IPC and the
+ * fused layer-0 gather+aggregation (gsb_rgcn_layer_fwd with h_src = NULL) and gsb_gather read
+ * every row from its owner's HBM directly -- no all-to-all, no host-synced sizes.
+ * ==================================================================================== */
+/* handle_out: 64 bytes (cudaIpcMemHandle_t of the allocation containing dev_ptr);
+ * offset_out: dev_ptr's byte offset inside that allocation. */
+gsb_status gsb_ipc_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out);
+/* Map another process's allocation (peer access enabled lazily); *dev_ptr_out = base + offset. */
+gsb_status gsb_ipc_open(const void* handle, int64_t offset, void** dev_ptr_out);
+gsb_status gsb_ipc_close(void* base_ptr);
+/* Register ntype t's partitioned table: bounds host int64 [world+1] (local-id ranges, bounds[0]
+ * = 0, bounds[world] = count), ptrs host [world] device pointers (own shard + IPC-mapped peer
+ * shards), row-major [bounds[w+1]-bounds[w]][dim] fp32.  world <= 8. */
+gsb_status gsb_graph_set_feature_peers(gsb_graph_t g, int32_t ntype, int32_t world, const int64_t* bounds,
+                                       const float* const* ptrs, int32_t dim);
+
+/* ======================================================================================
  * Optimizer (paper silent, R-adam): Adam with bias correction over a flat
  * fp32 buffer of n parameters; t is the 1-based step.  In place on p, m, v.
  * ==================================================================================== */

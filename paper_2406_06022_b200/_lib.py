@@ -62,6 +62,10 @@ SIGS = {
     "gsb_bucket_by_owner": [P, P, P, i64, P, P, P, P, P],
     "gsb_shard_gather": [P, P, i64, P, P],
     "gsb_rows_permute": [P, i32, P, P, i64, P, P],
+    "gsb_ipc_handle": [P, P, C.POINTER(i64)],
+    "gsb_ipc_open": [P, i64, C.POINTER(P)],
+    "gsb_ipc_close": [P],
+    "gsb_graph_set_feature_peers": [P, i32, i32, P, P, i32],
     "gsb_gemm": [i32, P, i64, P, i64, i64, i32, i32, P, i64, P],
     "gsb_nc_loss": [P, i64, i32, P, P, i32, P, P, i64, P, P, P, P, P, P, P],
     "gsb_adam_step": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P],

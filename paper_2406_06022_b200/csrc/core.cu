@@ -127,11 +127,7 @@ __global__ void __launch_bounds__(256) gather_kernel(GraphDev g, const int64_t* 
                 int64_t row = idx[u] / d4;
                 int c = (int)(idx[u] - row * d4);
                 int64_t x = __ldg(gid + row);
-                if (x >= 0 && x < N) {
-                    int t = type_of(g, x);
-                    const float4* src = reinterpret_cast<const float4*>(g.feat[t] + (x - g.node_off[t]) * g.feat_dim) + c;
-                    v[u] = ldg_nc_f4(src);
-                }
+                if (x >= 0 && x < N) v[u] = ldg_nc_f4(reinterpret_cast<const float4*>(feat_row(g, x)) + c);
             }
         }
 #pragma unroll

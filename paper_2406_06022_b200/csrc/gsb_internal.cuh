@@ -19,6 +19,7 @@ constexpr int kMaxR = GSB_MAX_ETYPES;
 constexpr int kMaxS = GSB_MAX_SLOTS;
 constexpr int kMaxL = GSB_MAX_LAYERS;
 constexpr int kNumSMs = 148;  // B200
+constexpr int kMaxPeers = 8;  // GPUs of one NVSwitch box
 
 // ------------------------------------------------------------------------------------
 // errors / instrumentation
@@ -68,6 +69,11 @@ struct GraphDev {
     const int32_t* indices[kMaxR];
     int64_t eid_base[kMaxR];
     const float* feat[kMaxT];
+    // node-ID partitioned features read over NVLink (peer.cu): rank w owns local ids
+    // [plo[t][w], plo[t][w+1]) of ntype t at peer[t][w] (an IPC-mapped pointer for w != self)
+    int32_t nparts;
+    int64_t plo[kMaxT][kMaxPeers + 1];
+    const float* peer[kMaxT][kMaxPeers];
 };
 
 __host__ __device__ inline int type_of(const GraphDev& g, int64_t gid) {
@@ -75,6 +81,19 @@ __host__ __device__ inline int type_of(const GraphDev& g, int64_t gid) {
 #pragma unroll 1
     for (int k = 1; k < g.T; ++k) t += (gid >= g.node_off[k]) ? 1 : 0;
     return t;
+}
+
+// Row of node gid in its feature table: local table, or the owner's (possibly peer) shard.
+__device__ __forceinline__ const float* feat_row(const GraphDev& g, int64_t gid) {
+    const int t = type_of(g, gid);
+    const int64_t local = gid - g.node_off[t];
+    if (g.nparts > 1) {
+        int w = 0;
+#pragma unroll 1
+        for (int k = 1; k < g.nparts; ++k) w += (local >= g.plo[t][k]) ? 1 : 0;
+        return g.peer[t][w] + (local - g.plo[t][w]) * g.feat_dim;
+    }
+    return g.feat[t] + local * g.feat_dim;
 }
 
 // Per-hop sizes, written by kernels (device resident; never copied to the host on the

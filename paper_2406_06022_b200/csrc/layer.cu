@@ -15,10 +15,7 @@ template <bool FEAT>
 __device__ __forceinline__ const float4* src_row(const GraphDev& g, const float* h, int d, int64_t row, int64_t gid,
                                                  const int32_t* rowmap = nullptr) {
     if (!FEAT && rowmap) row = rowmap[row];   // rows delivered in exchange order (partitioned features)
-    if (FEAT) {   // layer 0 reads the feature table by global id (fused gather, §8(a) a5)
-        const int t = type_of(g, gid);
-        return reinterpret_cast<const float4*>(g.feat[t] + (gid - g.node_off[t]) * d);
-    }
+    if (FEAT) return reinterpret_cast<const float4*>(feat_row(g, gid));   // layer 0: fused gather (a5)
     return reinterpret_cast<const float4*>(h + row * d);
 }
 
@@ -44,7 +41,11 @@ __global__ void __launch_bounds__(256, 6) agg_kernel(GraphDev g, const HopMeta* 
         for (int s = 0; s < St; ++s) {
             const int64_t e0 = seg_ptr[j * S + s], e1 = seg_ptr[j * S + s + 1];
             const float inv = (e1 > e0) ? 1.f / (float)(e1 - e0) : 0.f;
-            for (int c = lane; c < d4; c += 32) {
+            // every lane runs every column chunk (the shuffles below need the whole warp);
+            // lanes past the row width only predicate their loads and stores
+            for (int c0 = 0; c0 < d4; c0 += 32) {
+                const int c = c0 + lane;
+                const bool cl = c < d4;
                 float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
                 for (int64_t cb = e0; cb < e1; cb += 32) {
                     // one coalesced load of up to 32 source keys, broadcast by shuffle
@@ -54,23 +55,29 @@ __global__ void __launch_bounds__(256, 6) agg_kernel(GraphDev g, const HopMeta* 
                     for (; k + 4 <= cnt; k += 4) {
                         const int64_t k0 = __shfl_sync(0xffffffffu, key, k), k1 = __shfl_sync(0xffffffffu, key, k + 1);
                         const int64_t k2 = __shfl_sync(0xffffffffu, key, k + 2), k3 = __shfl_sync(0xffffffffu, key, k + 3);
-                        float4 x0 = __ldg(src_row<FEAT>(g, h, d, k0, k0, rowmap) + c);
-                        float4 x1 = __ldg(src_row<FEAT>(g, h, d, k1, k1, rowmap) + c);
-                        float4 x2 = __ldg(src_row<FEAT>(g, h, d, k2, k2, rowmap) + c);
-                        float4 x3 = __ldg(src_row<FEAT>(g, h, d, k3, k3, rowmap) + c);
-                        acc.x += x0.x; acc.y += x0.y; acc.z += x0.z; acc.w += x0.w;
-                        acc.x += x1.x; acc.y += x1.y; acc.z += x1.z; acc.w += x1.w;
-                        acc.x += x2.x; acc.y += x2.y; acc.z += x2.z; acc.w += x2.w;
-                        acc.x += x3.x; acc.y += x3.y; acc.z += x3.z; acc.w += x3.w;
+                        if (cl) {
+                            float4 x0 = __ldg(src_row<FEAT>(g, h, d, k0, k0, rowmap) + c);
+                            float4 x1 = __ldg(src_row<FEAT>(g, h, d, k1, k1, rowmap) + c);
+                            float4 x2 = __ldg(src_row<FEAT>(g, h, d, k2, k2, rowmap) + c);
+                            float4 x3 = __ldg(src_row<FEAT>(g, h, d, k3, k3, rowmap) + c);
+                            acc.x += x0.x; acc.y += x0.y; acc.z += x0.z; acc.w += x0.w;
+                            acc.x += x1.x; acc.y += x1.y; acc.z += x1.z; acc.w += x1.w;
+                            acc.x += x2.x; acc.y += x2.y; acc.z += x2.z; acc.w += x2.w;
+                            acc.x += x3.x; acc.y += x3.y; acc.z += x3.z; acc.w += x3.w;
+                        }
                     }
                     for (; k < cnt; ++k) {
                         const int64_t kk = __shfl_sync(0xffffffffu, key, k);
-                        float4 x = __ldg(src_row<FEAT>(g, h, d, kk, kk, rowmap) + c);
-                        acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+                        if (cl) {
+                            float4 x = __ldg(src_row<FEAT>(g, h, d, kk, kk, rowmap) + c);
+                            acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+                        }
                     }
                 }
-                acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
-                reinterpret_cast<float4*>(out + (int64_t)s * d)[c] = acc;
+                if (cl) {
+                    acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+                    reinterpret_cast<float4*>(out + (int64_t)s * d)[c] = acc;
+                }
             }
         }
         const int64_t self = m->src_off[t] + (j - m->dst_off[t]);

@@ -1,0 +1,84 @@
+// peer.cu -- NVLink peer access to other GPUs' feature shards (CUDA IPC).  With the shards
+// registered, the fused layer-0 gather+aggregation reads every source row straight from its
+// owner's HBM over NVLink/NVSwitch: the feature fetch of §8(e) happens inside the compute
+// kernel (no all-to-all, no host-synced sizes, CUDA-graph capturable).
+// Contract: include/gsb.h "Peer feature access".
+#include <cuda.h>
+
+#include "gsb_internal.cuh"
+
+namespace gsb {
+
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+static PFN_getAddressRange address_range_fn() {
+    static PFN_getAddressRange fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_getAddressRange>(p);
+    }
+    return fn;
+}
+
+}  // namespace gsb
+
+using namespace gsb;
+
+extern "C" {
+
+gsb_status gsb_ipc_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out) {
+    GSB_CHECK_ARG(dev_ptr && handle_out && offset_out, "null argument");
+    PFN_getAddressRange fn = address_range_fn();
+    GSB_CHECK_ARG(fn, "cuMemGetAddressRange entry point unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) {
+        set_error("cuMemGetAddressRange failed");
+        return GSB_ECUDA;
+    }
+    cudaIpcMemHandle_t h;
+    GSB_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (int64_t)((CUdeviceptr)dev_ptr - base);
+    return GSB_OK;
+}
+
+gsb_status gsb_ipc_open(const void* handle, int64_t offset, void** dev_ptr_out) {
+    GSB_CHECK_ARG(handle && dev_ptr_out && offset >= 0, "bad argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    GSB_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr_out = static_cast<char*>(base) + offset;
+    return GSB_OK;
+}
+
+gsb_status gsb_ipc_close(void* base_ptr) {
+    GSB_CUDA(cudaIpcCloseMemHandle(base_ptr));
+    return GSB_OK;
+}
+
+gsb_status gsb_graph_set_feature_peers(gsb_graph_t g, int32_t ntype, int32_t world, const int64_t* bounds,
+                                       const float* const* ptrs, int32_t dim) {
+    Graph* G = reinterpret_cast<Graph*>(g);
+    GSB_CHECK_ARG(G && bounds && ptrs && ntype >= 0 && ntype < G->dev.T, "bad argument");
+    GSB_CHECK_ARG(world >= 1 && world <= kMaxPeers, "world %d out of [1, %d]", world, kMaxPeers);
+    GSB_CHECK_ARG(dim > 0 && dim % 4 == 0, "dim must be a positive multiple of 4");
+    GSB_CHECK_ARG(G->dev.feat_dim == 0 || G->dev.feat_dim == dim, "all ntypes must share one feature dim");
+    GSB_CHECK_ARG(bounds[0] == 0 && bounds[world] == G->counts[ntype], "bounds must span [0, count)");
+    G->dev.feat_dim = dim;
+    G->dev.nparts = world;
+    for (int w = 0; w <= world; ++w) G->dev.plo[ntype][w] = bounds[w];
+    for (int w = 0; w < world; ++w) {
+        GSB_CHECK_ARG(ptrs[w] || bounds[w + 1] == bounds[w], "null shard pointer for rank %d", w);
+        G->dev.peer[ntype][w] = ptrs[w];
+    }
+    // the local-table pointer is unused in partitioned mode but marks the ntype as registered
+    G->dev.feat[ntype] = ptrs[0] ? ptrs[0] : reinterpret_cast<const float*>(16);
+    return GSB_OK;
+}
+
+}  // extern "C"

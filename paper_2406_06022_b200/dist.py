@@ -94,3 +94,47 @@ class FeatureExchange:
             return back, perm
         call("gsb_rows_permute", P(back), self.dim, P(perm), None, n, P(out), s)
         return out
+
+
+class PeerFeatures:
+    """Partitioned features read over NVLink (§8(e)): this rank allocates only its node-ID
+    range of every ntype; the shards of all ranks are mapped into every process with CUDA IPC
+    and registered in the graph store, so the fused layer-0 gather+aggregation (and
+    gsb_gather) load each row straight from its owner's HBM.  No collective on the data path."""
+
+    def __init__(self, store, counts, world: int, rank: int, shards, dim: int, group=None):
+        import ctypes as C
+        import numpy as np
+        import torch.distributed as dist
+        from ._lib import call
+        self.bounds = balanced_bounds(counts, world)
+        self.shards = [s.contiguous() for s in shards]
+        mine = []
+        for sh in self.shards:
+            if sh.numel() == 0:
+                mine.append(None)
+                continue
+            h = (C.c_char * 64)()
+            off = C.c_int64()
+            call("gsb_ipc_handle", C.c_void_p(sh.data_ptr()), h, C.byref(off))
+            mine.append((bytes(h), int(off.value)))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self.mapped = []
+        for t in range(len(self.shards)):
+            ptrs = (C.c_void_p * world)()
+            for w in range(world):
+                if w == rank:
+                    ptrs[w] = self.shards[t].data_ptr() if self.shards[t].numel() else None
+                elif allh[w][t] is None:
+                    ptrs[w] = None
+                else:
+                    hb, off = allh[w][t]
+                    p = C.c_void_p()
+                    call("gsb_ipc_open", (C.c_char * 64).from_buffer_copy(hb), off, C.byref(p))
+                    ptrs[w] = p.value
+                    self.mapped.append(p.value - off)
+            b = np.ascontiguousarray(self.bounds[t])
+            call("gsb_graph_set_feature_peers", store.h, t, world, b.ctypes.data_as(C.c_void_p), ptrs, dim)
+        store.feat_dim = dim
+        self.store = store

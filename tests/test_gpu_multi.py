@@ -61,6 +61,27 @@ def _worker(rank, world, port, out):
     torch.cuda.synchronize()
     out["grad%d" % rank] = tr.grad.cpu().numpy().copy()
     out["loss%d" % rank] = float(tr.loss.item())
+    # peer mode: shards mapped over NVLink (CUDA IPC), rows read inside the kernels
+    from paper_2406_06022_b200.dist import PeerFeatures
+    st2 = GraphStore(cfg.counts, cfg.etype_src(), cfg.etype_dst(), dev)
+    for r in range(cfg.num_etypes):
+        s_, d_ = synth.etype_coo(cfg, r, backend="torch", device=dev)
+        st2.load_etype(r, s_, d_)
+    pf = PeerFeatures(st2, cfg.counts, world, rank, shards, cfg.feat_dim)
+    g2 = st2.gather(torch.from_numpy(gids).to(dev)).cpu().numpy()
+    out["peer_rows_ok%d" % rank] = bool(np.array_equal(g2, exp))
+    tr2 = RGCNTrainer(st2, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
+                      synth.param_order(cfg), torch.from_numpy(synth.labels(cfg)),
+                      int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
+    tr2.load_inputs(torch.from_numpy(synth.nc_seeds(cfg, step)).to(dev))
+    tr2.capture(step0=step, ws=world, allreduce=lambda gr: allreduce_mean(gr))   # whole step in one graph
+    tr2.replay()
+    torch.cuda.synchronize()
+    out["peer_grad%d" % rank] = tr2.pview("W1", "g").cpu().numpy().copy()
+    out["peer_W1_%d" % rank] = tr2.pview("W1").cpu().numpy().copy()
+    out["peer_loss%d" % rank] = float(tr2.loss.item())
+    dist.barrier()
+    del pf
     dist.destroy_process_group()
 
 
@@ -100,3 +121,13 @@ def test_two_gpu_partitioned_features():
     slack[nW:nW + slb[0].size] = 0.5 * (slb[0] + slb[1])
     close_slack(out["grad0"], exp, slack, what="all-reduced grads")
     np.testing.assert_array_equal(out["grad0"], out["grad1"])
+    # peer (NVLink) mode inside one captured CUDA graph incl. the NCCL all-reduce
+    assert out["peer_rows_ok0"] and out["peer_rows_ok1"]
+    for r in range(2):
+        close(out["peer_loss%d" % r], losses[r], what=f"peer rank {r} loss")
+    names = synth.param_order(cfg)
+    shapes = {k: synth.init_params(cfg)[k].size for k in names}
+    o = int(np.cumsum([0] + [shapes[k] for k in names])[names.index("W1")])
+    expW1 = exp[o:o + shapes["W1"]].reshape(out["peer_grad0"].shape)
+    close(out["peer_grad0"], expW1, what="peer all-reduced grad W1")
+    np.testing.assert_array_equal(out["peer_W1_0"], out["peer_W1_1"])
