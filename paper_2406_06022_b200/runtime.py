@@ -270,6 +270,7 @@ class _TrainerBase:
         self.counters = torch.zeros(2, dtype=torch.int32, device=dev)
         self.graph = None
         self.graph_ws = 1
+        self.graph_allreduce = None
         self.fuse_gather = True
         self.exchange = None      # dist.FeatureExchange when features are partitioned across GPUs
 
@@ -326,9 +327,12 @@ class _TrainerBase:
 
     # CUDA graph of one whole step ----------------------------------------------------------
     def capture(self, step0: int, ws: int = 1, allreduce=None):
-        """Capture forward+backward(+all-reduce)+Adam of one step reading its inputs from the
-        fixed input buffers and the RNG step / Adam t from device counters, which the graph
-        advances (step += ws, t += 1).  Subsequent steps: load inputs, then replay()."""
+        """Capture one step in a CUDA graph reading its inputs from the fixed input buffers and
+        the RNG step / Adam t from device counters, which the graph advances (step += ws,
+        t += 1).  Single GPU: sample..Adam in the graph.  With `allreduce` (N>1) the graph
+        ends at the gradients; replay() then runs the NCCL all-reduce and Adam eagerly (NCCL
+        is kept out of graph capture).  Subsequent steps: load inputs, then replay()."""
+        self.graph_allreduce = allreduce
         self.counters[0] = step0
         self.counters[1] = self.t
         self.graph_ws = ws
@@ -342,9 +346,8 @@ class _TrainerBase:
                 s = _stream()
                 call("gsb_counter_add", C.c_void_p(self.counters.data_ptr() + 4), 1, s)
                 self._step_body(stream=None, step=0, step_dev=self.counters[0:1])
-                if allreduce is not None:
-                    allreduce(self.grad)
-                self.optimizer_step(t_dev=True)
+                if allreduce is None:
+                    self.optimizer_step(t_dev=True)
                 call("gsb_counter_add", C.c_void_p(self.counters.data_ptr()), ws, s)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
@@ -354,6 +357,9 @@ class _TrainerBase:
 
     def replay(self):
         self.graph.replay()
+        if self.graph_allreduce is not None:
+            self.graph_allreduce(self.grad)
+            self.optimizer_step(t_dev=True)
         self.t += 1
 
 
