@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--peer-gather", default="unique", choices=["unique", "fused"],
+                    help="peer mode: gather the unique input rows over NVLink first (unique) or read them per "
+                         "edge inside the fused aggregation (fused)")
     ap.add_argument("--features", default="peer", choices=["peer", "alltoall", "replicate"],
                     help="N>1 feature store: partitioned by node ID and read over NVLink inside the kernels "
                          "(peer, default), partitioned + NCCL all-to-all fetch (alltoall), or replicated")
@@ -252,6 +255,8 @@ def run_gsb(args, cfg):
     t0 = time.time()
     partitioned = dist is not None and args.features != "replicate"
     st, tr = build_gsb(cfg, device, (ws, rank) if partitioned else None, args.features)
+    if partitioned and args.features == "peer" and args.peer_gather == "unique":
+        tr.fuse_gather = False   # unique rows over NVLink once (peer loads bypass L2), then local aggregation
     setup_s = time.time() - t0
     n_batches = args.warmup + args.steps + args.profile_steps + 8
     if cfg.task == "lp":
@@ -447,8 +452,8 @@ def run_gsb(args, cfg):
                    "share": v["total_ms"] / args.profile_steps / step_ms_prof} for k, v in
                sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])}
     par = ("single" if ws == 1 else {
-        "peer": f"dp{ws}: features partitioned by node ID, read over NVLink (CUDA IPC) inside the fused "
-                f"gather+aggregation kernel; topology replicated; NCCL grad all-reduce in the CUDA graph",
+        "peer": f"dp{ws}: features partitioned by node ID, read over NVLink (CUDA IPC) by libgsb kernels "
+                f"({args.peer_gather} gather); topology replicated; NCCL grad all-reduce after the CUDA graph",
         "alltoall": f"dp{ws}: features partitioned by node ID, NCCL all-to-all fetch; topology replicated; "
                     f"NCCL grad all-reduce",
         "replicate": f"dp{ws}: graph + features replicated, NCCL grad all-reduce"}[args.features])
