@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--pipeline", default="on", choices=["on", "off"],
+                    help="sample batch i+1 on a side stream while batch i computes (double-buffered)")
     ap.add_argument("--peer-gather", default="unique", choices=["unique", "fused"],
                     help="peer mode: gather the unique input rows over NVLink first (unique) or read them per "
                          "edge inside the fused aggregation (fused)")
@@ -264,14 +266,14 @@ def run_gsb(args, cfg):
         uv = [lpb.batch((i * ws + rank) % 100000) for i in range(n_batches)]
         us_all = torch.from_numpy(np.stack([x[0] for x in uv])).to(device)
         vs_all = torch.from_numpy(np.stack([x[1] for x in uv])).to(device)
-        host_batches = [np.stack([x[0], x[1]]) for x in uv[:args.steps]]
+        host_batches = [np.stack([x[0], x[1]]) for x in uv[:args.steps + 1]]
     else:
         train = synth.train_nodes(cfg)
         per_epoch = max(1, len(train) // cfg.batch)
         # seed batches (a1): device-resident epoch permutation slices; rank r takes batch step*ws + r
         seeds_all = torch.from_numpy(np.stack([synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train)
                                                for i in range(n_batches)])).to(device)
-        host_batches = [synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train) for i in range(args.steps)]
+        host_batches = [synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train) for i in range(args.steps + 1)]
 
     def fb(i):
         if cfg.task == "lp":
@@ -302,15 +304,27 @@ def run_gsb(args, cfg):
     torch.cuda.synchronize()
     if tr.sampler.poll_error() != 0:
         raise RuntimeError("device-side sampling error latched")
-    # ---- capture ONE whole step (sample..Adam) in a CUDA graph; replays advance the RNG step
-    # word and Adam's t on the device, inputs are copied into the graph's fixed seed buffer
+    # ---- CUDA graphs.  Pipelined (default): per-buffer graphs of the sample phase (side
+    # stream, batch i+1) and of the compute phase (+ Adam) of batch i; otherwise ONE graph of
+    # the whole step.  Replays advance the RNG step word and Adam's t on the device; inputs
+    # are copied into the graphs' fixed buffers.
     use_graph = not args.no_graph and tr.exchange is None   # all-to-all sizes are host-synced
-    if use_graph:
+    pipelined = use_graph and args.pipeline == "on"
+
+    def inputs(i):
+        return (us_all[i], vs_all[i]) if cfg.task == "lp" else (seeds_all[i],)
+
+    ar = allreduce if dist is not None else None
+    if pipelined:
+        tr.pipeline_start(inputs(W - 2), (W - 2) * ws + rank, ws=ws, allreduce=ar)
+    elif use_graph:
         load(W - 2)
-        tr.capture(step0=(W - 2) * ws + rank, ws=ws, allreduce=allreduce if dist is not None else None)
+        tr.capture(step0=(W - 2) * ws + rank, ws=ws, allreduce=ar)
 
     def run(i):
-        if use_graph:
+        if pipelined:
+            tr.pipeline_step(*inputs(i + 1))
+        elif use_graph:
             load(i)
             tr.replay()
         else:
@@ -333,6 +347,8 @@ def run_gsb(args, cfg):
         e0.record()
         for i in range(W, W + args.steps):
             run(i)
+        if pipelined:
+            tr.pipeline_sync()    # the sampling of batch W+steps (issued in the last step) is inside
         e1.record()
         torch.cuda.synchronize()
     if dist is not None:
@@ -384,14 +400,22 @@ def run_gsb(args, cfg):
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    if pipelined:   # prologue (first batch H2D + sampling) inside the timed region
+        tr.pipeline_start(tuple(host_pinned[0]) if cfg.task == "lp" else (host_pinned[0],), base * ws + rank,
+                          ws=ws, allreduce=ar)
     for i in range(args.steps):
         hb = host_pinned[i]
-        if cfg.task == "lp":
+        if pipelined:
+            nb = host_pinned[i + 1]
+            tr.pipeline_step(*(tuple(nb) if cfg.task == "lp" else (nb,)))
+        elif cfg.task == "lp":
             tr.pos_u.copy_(hb[0], non_blocking=True)
             tr.pos_v.copy_(hb[1], non_blocking=True)
         else:
             tr.seeds_dev[:hb.numel()].copy_(hb, non_blocking=True)
-        if use_graph:
+        if pipelined:
+            pass
+        elif use_graph:
             tr.replay()
         else:
             if cfg.task == "lp":
@@ -404,6 +428,9 @@ def run_gsb(args, cfg):
             tr.optimizer_step()
         loss_host.copy_(tr.loss, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+    if pipelined:
+        tr.pipeline_sync()
+        torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist is not None:
         t = torch.tensor([e2e_s], device=device)
@@ -463,7 +490,9 @@ def run_gsb(args, cfg):
         "metric": metric, "value": seeds_per_s, "unit": unit, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded hash generator, synth/)",
-        "config": cfg_json(cfg, ws, {"parallelism": par, "cuda_graph": use_graph}),
+        "config": cfg_json(cfg, ws, {"parallelism": par, "cuda_graph": use_graph,
+                                     "pipeline": "sample i+1 on a side stream during compute i" if pipelined
+                                     else "off"}),
         "sampled_edges_per_s": edges_per_step * ws / (ms_per_step / 1e3),
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
         "kernels": kernels, "setup_s": setup_s,

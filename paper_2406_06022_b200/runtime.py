@@ -135,6 +135,11 @@ class MiniBatchSampler:
         self.arena = torch.empty(int(b.value), dtype=torch.uint8, device=store.device)
         call("gsb_blocks_init_arena", self.h, _ptr(self.arena), self.arena.numel(), _stream())
         self.max_seeds = max_seeds
+        self.fanouts = list(fanouts)
+
+    def twin(self) -> "MiniBatchSampler":
+        """A second sampler of the same shape (own handle + arena), for double buffering."""
+        return MiniBatchSampler(self.store, self.fanouts, self.max_seeds, self.max_excl)
 
     def __del__(self):
         try:
@@ -273,6 +278,9 @@ class _TrainerBase:
         self.graph_allreduce = None
         self.fuse_gather = True
         self.exchange = None      # dist.FeatureExchange when features are partitioned across GPUs
+        self._bufs = None         # double-buffered per-batch state (enable_prefetch)
+        self.pipe_graphs = None
+        self.pipe_k = 0
 
     # parameter views -------------------------------------------------------------------
     def pview(self, name: str, which: str = "p") -> torch.Tensor:
@@ -286,9 +294,17 @@ class _TrainerBase:
         return C.c_void_p(buf.data_ptr() + int(self.offsets[k]) * 4)
 
     # pieces ------------------------------------------------------------------------------
+    def _gather_inputs(self, s):
+        """Explicit input-row gather into x0 (unfused mode; with peer shards registered this is
+        the unique-row NVLink fetch).  Part of the sample phase: it depends only on the blocks."""
+        if not self.fuse_gather and self.exchange is None:
+            sm = self.sampler
+            call("gsb_gather_block_inputs", sm.h, _ptr(sm.arena), _ptr(self.x0), s)
+
     def _encode(self, s):
         """gather -> RGCN layers, input layer first (Fig. 8).  With fuse_gather
-        (default) layer 0 reads the feature rows by gid inside its aggregation kernel."""
+        (default) layer 0 reads the feature rows by gid inside its aggregation kernel;
+        otherwise x0 was filled by _gather_inputs in the sample phase."""
         sm = self.sampler
         rowmap = None
         if self.exchange is not None:   # partitioned features: NCCL all-to-all fetch (C4/C5)
@@ -298,7 +314,6 @@ class _TrainerBase:
         elif self.fuse_gather:
             h = None
         else:
-            call("gsb_gather_block_inputs", sm.h, _ptr(sm.arena), _ptr(self.x0), s)
             h = self.x0
         for l in range(self.L):
             call("gsb_rgcn_layer_fwd_rowmap", sm.h, _ptr(sm.arena), l, _ptr(h), _ptr(rowmap if l == 0 else None),
@@ -306,6 +321,11 @@ class _TrainerBase:
                  _ptr(self.hout[l]), _ptr(self.acat[l]), s)
             h = self.hout[l]
         return h
+
+    def _step_body(self, stream=None, step: int = 0, step_dev=None, seeds=None):
+        """One step without the optimizer: sample phase, then compute phase."""
+        self._sample_phase(stream, step, step_dev, seeds)
+        self._compute_phase(stream, seeds)
 
     def _backward_layers(self, s):
         sm = self.sampler
@@ -362,6 +382,113 @@ class _TrainerBase:
             self.optimizer_step(t_dev=True)
         self.t += 1
 
+    # double-buffered pipeline: sample batch i+1 while batch i computes ---------------------
+    _BUFFERED = ("sampler", "x0")     # per-batch state; subclasses add their input buffers
+
+    def enable_prefetch(self):
+        """Allocate a second copy of every per-batch buffer (sampler handle + arena, input
+        rows, the task's input tensors) so the sample phase of batch i+1 -- sampling,
+        relabel and, in unique-gather mode, the input-row fetch; none of it reads the
+        parameters -- runs on a side stream while batch i computes."""
+        if self._bufs is not None:
+            return
+        cur = {k: getattr(self, k) for k in self._BUFFERED}
+        nxt = {k: (v.twin() if isinstance(v, MiniBatchSampler) else torch.zeros_like(v)) for k, v in cur.items()}
+        self._bufs = [cur, nxt]
+        self.side = torch.cuda.Stream(device=self.device)
+        self.ev_s = [torch.cuda.Event(), torch.cuda.Event()]
+        self.ev_c = torch.cuda.Event()
+
+    def _use(self, b: int):
+        for k, v in self._bufs[b].items():
+            setattr(self, k, v)
+
+    def _sample_ops(self):
+        """Sample phase of the batch in the active buffer, RNG step word read from (and then
+        advanced on) the device counter."""
+        self._sample_phase(None, 0, self.counters[0:1])
+        call("gsb_counter_add", C.c_void_p(self.counters.data_ptr()), self.pipe_ws, _stream())
+
+    def _compute_ops(self):
+        call("gsb_counter_add", C.c_void_p(self.counters.data_ptr() + 4), 1, _stream())
+        self._compute_phase(None)
+        if self.pipe_allreduce is None:
+            self.optimizer_step(t_dev=True)
+
+    def pipeline_start(self, inputs, step: int, ws: int = 1, allreduce=None, use_graph: bool = True):
+        """Start a pipelined run: capture (once) per-buffer CUDA graphs of the sample phase
+        and of the compute phase (+ Adam unless `allreduce`, which then runs eagerly after
+        each compute graph, NCCL being kept out of capture), then load `inputs` (the first
+        batch) into buffer 0 and sample it with RNG step word `step`.  Each pipeline_step()
+        computes the pending batch and samples the next one (step word + ws)."""
+        if self.exchange is not None:
+            raise GsbError("pipeline needs device-resident sizes (no all-to-all exchange mode)")
+        self.enable_prefetch()
+        self.pipe_ws, self.pipe_allreduce = ws, allreduce
+        if use_graph and self.pipe_graphs is None:
+            torch.cuda.synchronize()
+            launches0 = lib().gsb_launch_count()
+            cap = torch.cuda.Stream(device=self.device)
+            graphs = {"sample": [], "compute": []}
+            for kind, fn in (("sample", self._sample_ops), ("compute", self._compute_ops)):
+                for b in (0, 1):
+                    g = torch.cuda.CUDAGraph()
+                    cap.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(cap):
+                        with torch.cuda.graph(g, stream=cap):
+                            self._use(b)
+                            fn()
+                    torch.cuda.current_stream().wait_stream(cap)
+                    graphs[kind].append(g)
+            torch.cuda.synchronize()
+            # kernels per step = one sample graph + one compute graph
+            self.graph_launches = (lib().gsb_launch_count() - launches0) // 2
+            self.pipe_graphs = graphs
+        elif not use_graph:
+            self.pipe_graphs = None
+        self.pipe_k = 0
+        self.counters[0] = step + ws
+        self.counters[1] = self.t
+        self._use(0)
+        self._load_inputs(self._bufs[0], *inputs)
+        self._sample_phase(None, step, None)
+        self.ev_s[0].record()
+        self.ev_c.record()
+
+    def pipeline_step(self, *next_inputs):
+        """Compute the pending batch (loss, grads, Adam) on the current stream while the side
+        stream loads `next_inputs` into the other buffer and samples them.  Afterwards
+        self.loss is the computed batch's loss (read it on the current stream)."""
+        b = self.pipe_k & 1
+        nb = b ^ 1
+        main = torch.cuda.current_stream()
+        self.side.wait_event(self.ev_c)          # buffer nb is free once batch k-1 computed
+        with torch.cuda.stream(self.side):
+            self._load_inputs(self._bufs[nb], *next_inputs)
+            if self.pipe_graphs is not None:
+                self.pipe_graphs["sample"][nb].replay()
+            else:
+                self._use(nb)
+                self._sample_ops()
+            self.ev_s[nb].record(self.side)
+        main.wait_event(self.ev_s[b])
+        self._use(b)
+        if self.pipe_graphs is not None:
+            self.pipe_graphs["compute"][b].replay()
+        else:
+            self._compute_ops()
+        self.ev_c.record(main)
+        if self.pipe_allreduce is not None:
+            self.pipe_allreduce(self.grad)
+            self.optimizer_step(t_dev=True)
+        self.t += 1
+        self.pipe_k += 1
+
+    def pipeline_sync(self):
+        """Join the side stream into the current stream (end of a pipelined run)."""
+        if self._bufs is not None:
+            torch.cuda.current_stream().wait_stream(self.side)
+
 
 class RGCNTrainer(_TrainerBase):
     """Node classification (§8(a) a1-a8, a11, a12): RGCN encoder + softmax-CE decoder.
@@ -382,11 +509,20 @@ class RGCNTrainer(_TrainerBase):
         self.row_loss = torch.zeros(batch + 640, dtype=torch.float32, device=dev)   # + fused-mean scratch
         self.seeds_dev = torch.empty(batch, dtype=torch.int64, device=dev)
 
-    def _step_body(self, stream=None, step: int = 0, step_dev=None, seeds=None):
+    _BUFFERED = ("sampler", "x0", "seeds_dev")
+
+    def _load_inputs(self, d, seeds: torch.Tensor):
+        d["seeds_dev"][:seeds.numel()].copy_(seeds, non_blocking=True)
+
+    def _sample_phase(self, stream=None, step: int = 0, step_dev=None, seeds=None):
+        seeds = self.seeds_dev if seeds is None else seeds
+        self.sampler.sample(seeds, self.rng_seed, step, stream=stream, step_dev=step_dev)
+        self._gather_inputs(_stream(stream))
+
+    def _compute_phase(self, stream=None, seeds=None):
         s = _stream(stream)
         seeds = self.seeds_dev if seeds is None else seeds
         n = seeds.numel()
-        self.sampler.sample(seeds, self.rng_seed, step, stream=stream, step_dev=step_dev)
         h = self._encode(s)
         top = self.L - 1
         call("gsb_nc_loss", _ptr(h), n, self.hidden, self._pp("Wc"), self._pp("bc"), self.C, _ptr(self.labels),
@@ -456,7 +592,14 @@ class LPTrainer(_TrainerBase):
         self.row_loss = torch.empty(B, dtype=torch.float32, device=dev)
         self.group_base = 0
 
-    def _step_body(self, stream=None, step: int = 0, step_dev=None, seeds=None):
+    _BUFFERED = ("sampler", "x0", "pos_u", "pos_v", "neg", "seeds", "n_seeds", "iu", "iv", "ineg", "seeds_ws")
+
+    def _load_inputs(self, d, u: torch.Tensor, v: torch.Tensor):
+        d["pos_u"].copy_(u, non_blocking=True)
+        d["pos_v"].copy_(v, non_blocking=True)
+
+    def _sample_phase(self, stream=None, step: int = 0, step_dev=None, seeds=None):
+        """Joint negatives -> LP seed set -> exclusion-aware sampling (-> input rows)."""
         s = _stream(stream)
         sd = None if step_dev is None else C.c_void_p(step_dev.data_ptr())
         call("gsb_joint_negatives", self.B, self.K, self.neg_n, self.neg_base, self.rng_seed, step, sd,
@@ -466,6 +609,10 @@ class LPTrainer(_TrainerBase):
              self.seeds_ws.numel(), s)
         self.sampler.sample(self.seeds, self.rng_seed, step, self.pos_u, self.pos_v, self.lp_etype, self.lp_rev, stream,
                             n_seeds_dev=self.n_seeds, step_dev=step_dev, n_seeds=self.seeds.numel())
+        self._gather_inputs(s)
+
+    def _compute_phase(self, stream=None, seeds=None):
+        s = _stream(stream)
         h = self._encode(s)
         top = self.L - 1
         call("gsb_lp_score", _ptr(h), self.hout[top].shape[0], self.hidden, _ptr(self.iu), _ptr(self.iv),

@@ -182,3 +182,37 @@ def test_lp_step_parity(lp_pair, torch_cuda):
             pslack = rtol * np.abs(mid) + rtol * np.abs(mid).max()
             assert not ((gp < lo - pslack) | (gp > hi + pslack)).any(), f"step {step} param {k}"
             oracle.adam(params[k], g, opt[k]["m"], opt[k]["v"], cfg.lr, step + 1)
+
+
+def test_lp_pipelined_matches_oracle(lp_pair, torch_cuda):
+    """LP through the double-buffered graph pipeline: negatives, seed set, loss and grads of
+    every computed batch match the oracle (batch k+1's negatives/sampling run on the side
+    stream during batch k's compute)."""
+    import torch
+    from paper_2406_06022_b200.runtime import LPTrainer
+    from tests.test_gpu_parity import check_grads
+    cfg, st, og = lp_pair
+    tr = LPTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_neg, cfg.lp_etype, cfg.lp_rev_etype,
+                   synth.init_params(cfg), synth.param_order(cfg), lr=cfg.lr, rng_seed=cfg.rng_seed)
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    opt = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}
+    dev = lambda a: torch.from_numpy(np.asarray(a, np.int64)).cuda()
+    batches = [synth.lp_train_edges(cfg, i) for i in range(4)]
+    tr.pipeline_start((dev(batches[0][0]), dev(batches[0][1])), 0)
+    for step in range(3):
+        for k in synth.param_order(cfg):
+            tr.pview(k).copy_(torch.from_numpy(params[k].astype(np.float32)))
+            tr.pview(k, "m").copy_(torch.from_numpy(opt[k]["m"].astype(np.float32)))
+            tr.pview(k, "v").copy_(torch.from_numpy(opt[k]["v"].astype(np.float32)))
+        tr.pipeline_step(dev(batches[step + 1][0]), dev(batches[step + 1][1]))
+        tr.pipeline_sync()
+        torch.cuda.synchronize()
+        u, v = batches[step]
+        res = oracle.lp_step(og, params, u, v, step, cfg.rng_seed)
+        assert np.array_equal(tr.neg.cpu().numpy(), res.extra["neg"])
+        ns = int(tr.n_seeds.item())
+        assert np.array_equal(tr.seeds[:ns].cpu().numpy(), res.extra["seeds"])
+        close(tr.loss.cpu().numpy()[0], res.loss, what=f"pipelined step {step} loss")
+        check_grads(tr, res, cfg, step)
+        for k in synth.param_order(cfg):
+            oracle.adam(params[k], res.grads[k], opt[k]["m"], opt[k]["v"], cfg.lr, step + 1)

@@ -272,3 +272,36 @@ def test_cuda_graph_replay_matches_oracle(torch_cuda):
         check_grads(tr, res, cfg, step)
         for k in synth.param_order(cfg):
             oracle.adam(params[k], res.grads[k], opt[k]["m"], opt[k]["v"], cfg.lr, step + 1)
+
+
+@pytest.mark.parametrize("use_graph,fuse", [(True, True), (True, False), (False, True)])
+def test_pipelined_steps_match_oracle(torch_cuda, use_graph, fuse):
+    """Double-buffered pipeline (bench.py's default): batch k+1 is sampled on a side stream
+    while batch k computes.  Every computed batch's blocks are bit-exact, its loss and grads
+    match the oracle, and the device step / t counters advance as in the serial graph."""
+    import torch
+    cfg = synth.scaled(synth.mag(), 0.01, "mag_small")
+    st, og = gpu_store(cfg), oracle_graph(cfg)
+    tr = _gpu_trainer(cfg, st)
+    tr.fuse_gather = fuse
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    opt = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}
+    labels = synth.labels(cfg)
+    dev_seeds = [torch.from_numpy(synth.nc_seeds(cfg, i)).cuda() for i in range(5)]
+    tr.pipeline_start((dev_seeds[0],), 0, use_graph=use_graph)
+    for step in range(4):
+        for k in synth.param_order(cfg):   # re-sync from the oracle state (see test_nc_step_parity)
+            tr.pview(k).copy_(torch.from_numpy(params[k].astype(np.float32)))
+            tr.pview(k, "m").copy_(torch.from_numpy(opt[k]["m"].astype(np.float32)))
+            tr.pview(k, "v").copy_(torch.from_numpy(opt[k]["v"].astype(np.float32)))
+        tr.pipeline_step(dev_seeds[step + 1])
+        tr.pipeline_sync()
+        torch.cuda.synchronize()
+        assert int(tr.counters[0].item()) == step + 2 and int(tr.counters[1].item()) == step + 1
+        seeds = synth.nc_seeds(cfg, step)
+        res = oracle.nc_step(og, params, seeds, labels, step, cfg.rng_seed)
+        _compare_blocks(cfg, st, tr.sampler, res.blocks)
+        close(tr.loss.cpu().numpy()[0], res.loss, what=f"pipelined step {step} loss")
+        check_grads(tr, res, cfg, step)
+        for k in synth.param_order(cfg):
+            oracle.adam(params[k], res.grads[k], opt[k]["m"], opt[k]["v"], cfg.lr, step + 1)
