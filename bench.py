@@ -37,6 +37,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="gsb", choices=["gsb", "reference"])
     ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b", "amazon_lp", "tiny_lp"])
+    ap.add_argument("--feat-dtype", default=None, choices=["f32", "bf16"],
+                    help="feature storage type (default: the config's; compute stays fp32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--profile-steps", type=int, default=20)
@@ -156,14 +158,16 @@ def kernel_work(name: str, sz: dict, cfg: synth.Config):
     if name[-3:-1] == "_l" and name[-1].isdigit():
         lay = int(name[-1])
         name = name[:-3]
+    fe = 2 if cfg.feat_dtype == "bf16" else 4      # feature element bytes (layer-0 inputs)
     if name == "gather":
         n = sz["n_src"][0]
-        return "bytes", n * d0 * 4 * 2 + n * 8
+        return "bytes", n * d0 * fe * 2 + n * 8
     if name == "rgcn_agg" and lay is not None:
         d = d0 if lay == 0 else hd
-        # per sampled edge: one d-float source row + its index; per dst row: self row + Acat row
+        es = fe if lay == 0 else 4
+        # per sampled edge: one d-wide source row + its index; per dst row: self row + fp32 Acat row
         idx = 12 if lay == 0 else 4
-        return "bytes", sz["n_edges"][lay] * (d * 4 + idx) + sz["n_dst"][lay] * d * 4 + sz["acat_cols"][lay] * 4
+        return "bytes", sz["n_edges"][lay] * (d * es + idx) + sz["n_dst"][lay] * d * es + sz["acat_cols"][lay] * 4
     if name in ("rgcn_gemm_fwd", "rgcn_gemm_dW") and lay is not None:
         return "flops", 2 * sz["acat_cols"][lay] * hd
     if name == "rgcn_gemm_dA" and lay is not None:
@@ -198,13 +202,15 @@ def build_gsb(cfg, device, partition=None, mode="peer"):
         from paper_2406_06022_b200.dist import FeatureExchange, PeerFeatures, balanced_bounds
         world, rank = partition
         b = balanced_bounds(cfg.counts, world)
+        tdt = torch.bfloat16 if cfg.feat_dtype == "bf16" else torch.float32
         shards = [synth.feature_rows(cfg, t, torch.arange(int(b[t][rank]), int(b[t][rank + 1]), device=device),
-                                     "torch", device) for t in range(cfg.num_ntypes)]
+                                     "torch", device).to(tdt) for t in range(cfg.num_ntypes)]
         if mode == "peer":
             st._peer = PeerFeatures(st, cfg.counts, world, rank, shards, cfg.feat_dim)
         else:
             ex = FeatureExchange(cfg.counts, world, rank, shards, cfg.feat_dim)
             st.feat_dim = cfg.feat_dim
+            st.feat_dtype = tdt
     torch.cuda.synchronize()
     if cfg.task == "lp":
         tr = LPTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_neg, cfg.lp_etype, cfg.lp_rev_etype,
@@ -489,7 +495,7 @@ def run_gsb(args, cfg):
     line = {
         "metric": metric, "value": seeds_per_s, "unit": unit, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded hash generator, synth/)",
+        "vs_baseline": None, "dtype": "f32" if cfg.feat_dtype == "f32" else "f32 (bf16 feature storage)", "data": "synthetic (seeded hash generator, synth/)",
         "config": cfg_json(cfg, ws, {"parallelism": par, "cuda_graph": use_graph,
                                      "pipeline": "sample i+1 on a side stream during compute i" if pipelined
                                      else "off"}),
@@ -573,6 +579,8 @@ def run_reference(args, cfg):
 def main():
     args = parse()
     cfg = config_for(args.config)
+    if args.feat_dtype:
+        cfg = synth.with_dtype(cfg, args.feat_dtype)
     if args.impl == "reference":
         line = run_reference(args, cfg)
         if line is not None:

@@ -20,7 +20,9 @@
  *    synchronously and set gsb_last_error() (thread-local text).  Errors detected by a
  *    kernel (unknown node id, frontier not grouped by node type, capacity overflow) are
  *    latched in a device word inside the arena and returned by gsb_blocks_poll_error().
- *  - Layouts: node features / hidden states are row-major [rows][dim] fp32.  Global node
+ *  - Layouts: node features are row-major [rows][dim] fp32 or bf16 (GSB_F32 / GSB_BF16,
+ *    one format for all node types; bf16 values are widened exactly to fp32 when read);
+ *    hidden states, activations and parameters are row-major fp32.  Global node
  *    ids (gid) are type-major: gid = node_off[t] + local id (R-gid).  Relation weights W
  *    of a layer are row-major [R+1][d_in][d_out]; slot R is W_self.
  *  - Threads: calls on one handle are not thread-safe; separate handles are independent.
@@ -41,6 +43,10 @@ typedef int32_t gsb_status;
 #define GSB_EWORKSPACE 2  /* caller-provided buffer too small                         */
 #define GSB_ECUDA 3       /* a CUDA runtime call or kernel launch failed              */
 #define GSB_EDEVICE 4     /* a latched device-side error (see gsb_blocks_poll_error)  */
+
+/* feature element types */
+#define GSB_F32 0
+#define GSB_BF16 1
 
 #define GSB_MAX_NTYPES 8
 #define GSB_MAX_ETYPES 32
@@ -98,15 +104,17 @@ gsb_status gsb_csc_build(gsb_graph_t g, int32_t etype, const int32_t* src, const
 gsb_status gsb_graph_set_csc(gsb_graph_t g, int32_t etype, const int64_t* indptr, const int32_t* indices,
                              int64_t n_edges, int64_t eid_base);
 
-/* Register the feature table of `ntype`: device fp32 [ntype_count][dim] row-major
- * (P:L86 distributed tensors).  All ntypes must use the same dim. */
-gsb_status gsb_graph_set_features(gsb_graph_t g, int32_t ntype, const float* feat, int32_t dim);
+/* Register the feature table of `ntype`: device [ntype_count][dim] row-major, element type
+ * dtype (GSB_F32 / GSB_BF16), 16-byte aligned, dim * element size a multiple of 16
+ * (P:L86 distributed tensors).  All ntypes share one dtype; widths may differ per ntype
+ * (input-encoder graphs), but the fused layer-0 path and the gathers need one width. */
+gsb_status gsb_graph_set_features(gsb_graph_t g, int32_t ntype, const void* feat, int32_t dim, int32_t dtype);
 
 /* Feature gather by global id (§8(a) a5; S:L299 fetch_features):
  *   out[i, :] = F_{t(i)}[gid[i] - node_off[t(i)], :]   for i < n   (exact copy)
- * gid: device int64 [n]; out: device fp32 [n][dim].  A gid outside [0, total nodes)
- * yields a zero row. */
-gsb_status gsb_gather(gsb_graph_t g, const int64_t* gid, int64_t n, float* out, void* stream);
+ * gid: device int64 [n]; out: device [n][dim] in the feature dtype.  A gid outside
+ * [0, total nodes) yields a zero row. */
+gsb_status gsb_gather(gsb_graph_t g, const int64_t* gid, int64_t n, void* out, void* stream);
 
 /* ======================================================================================
  * Mini-batch sampling into message-flow blocks (P:L58, P:L86 on-the-fly sampling;
@@ -191,8 +199,9 @@ gsb_status gsb_slot_etype(gsb_graph_t g, int32_t ntype, int32_t slot, int32_t* e
 gsb_status gsb_blocks_poll_error(gsb_blocks_t b, void* arena, int32_t* code, void* stream);
 
 /* Gather the input features of the sampled mini-batch (layer 0 src rows):
- * out: device fp32 [n_src(layer 0)][dim] (capacity from gsb_blocks_input_rows). */
-gsb_status gsb_gather_block_inputs(gsb_blocks_t b, const void* arena, float* out, void* stream);
+ * out: device [n_src(layer 0)][dim] in the feature dtype (capacity from
+ * gsb_blocks_input_rows). */
+gsb_status gsb_gather_block_inputs(gsb_blocks_t b, const void* arena, void* out, void* stream);
 gsb_status gsb_blocks_input_rows(gsb_blocks_t b, int64_t* max_rows);
 /* Row capacity of the dst rows of `layer` (for h_dst buffers). */
 gsb_status gsb_blocks_dst_rows(gsb_blocks_t b, int32_t layer, int64_t* max_rows);
@@ -205,19 +214,20 @@ gsb_status gsb_blocks_dst_rows(gsb_blocks_t b, int32_t layer, int64_t* max_rows)
  * the concatenation Acat_v = [A_{r_0}[v] | ... | A_{r_{S_t-1}}[v] | h_src[self(v)]].
  * d_in must be a multiple of 32 and d_out a multiple of 4.
  * h_src == NULL (layer 0 only): source rows are read straight from the registered feature
- * tables by global id -- the feature gather (§8(a) a5) fused into the aggregation.
- * acat: device fp32 cache [gsb_layer_acat_floats] (kept for the backward).
+ * tables by global id (in their dtype) -- the feature gather (§8(a) a5) fused into the
+ * aggregation.  acat: device fp32 cache [gsb_layer_acat_floats] (kept for the backward).
  * ==================================================================================== */
 gsb_status gsb_layer_acat_floats(gsb_blocks_t b, int32_t layer, int32_t d_in, int64_t* n_floats);
 
 gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src, int32_t d_in,
                               const float* W, const float* bias, int32_t d_out, int32_t relu, float* h_dst,
                               float* acat, void* stream);
-/* Same, with h_src row r read at h_src[rowmap[r]] (rows delivered in exchange order by
- * gsb_bucket_by_owner's perm: the unpack is folded into the aggregation). */
-gsb_status gsb_rgcn_layer_fwd_rowmap(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src,
-                                     const int32_t* rowmap, int32_t d_in, const float* W, const float* bias,
-                                     int32_t d_out, int32_t relu, float* h_dst, float* acat, void* stream);
+/* Same, with h_src of element type h_dtype (GSB_F32, or GSB_BF16 for gathered bf16 input
+ * rows) and, when rowmap != NULL, source row r read at h_src[rowmap[r]] (rows delivered in
+ * exchange order by gsb_bucket_by_owner's perm: the unpack is folded into the aggregation). */
+gsb_status gsb_rgcn_layer_fwd_ex(gsb_blocks_t b, const void* arena, int32_t layer, const void* h_src, int32_t h_dtype,
+                                 const int32_t* rowmap, int32_t d_in, const float* W, const float* bias, int32_t d_out,
+                                 int32_t relu, float* h_dst, float* acat, void* stream);
 
 /* Backward (analytic):  dZ = dh_dst * 1[h_dst > 0] (relu) or dh_dst;
  *   dW_r = sum_v A_r[v]^T dZ_v ; dW_self = sum_v h_src[self(v)]^T dZ_v ; db = sum_v dZ_v
@@ -228,6 +238,27 @@ gsb_status gsb_rgcn_layer_fwd_rowmap(gsb_blocks_t b, const void* arena, int32_t 
 gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_dst,
                               float* dh_dst, const float* W, const float* acat, int32_t d_in, int32_t d_out,
                               int32_t relu, float* dW, float* db, float* dh_src, float* dacat_ws, void* stream);
+
+/* ======================================================================================
+ * Input encoder (§8(a) a6; "node input encoders handle node features"
+ * featureless nodes) over the input rows of the sampled mini-batch (layer-0 src rows i,
+ * type-grouped, count on the device):
+ *   H0[i, :] = F_t[local(i), :] W_t     ntype t with W_in[t] != NULL: W_t device fp32
+ *                                       [dim_t][d_out], features bf16, dim_t % 128 == 0
+ *   H0[i, :] = F_t[local(i), :]         W_in[t] == NULL: frozen table, dim_t == d_out
+ * W_in: host array [num_ntypes] of device pointers.  d_out % 128 == 0.  H0: device fp32
+ * [gsb_blocks_input_rows][d_out] (the layer-0 h_src, GSB_F32).  The products run on tcgen05
+ * bf16 MMAs with W (forward) / dH0 (backward) split into bf16 hi + lo (fp32-class accuracy).
+ * ws: device scratch of gsb_encoder_ws_bytes (same W_in non-NULL pattern in every call).
+ * Backward: dW_in[t] (device fp32 [dim_t][d_out], overwritten) = sum over input rows i of
+ * type t of F_t[local(i)]^T dH0[i], for every t with W_in[t] != NULL; dH0 is layer 0's
+ * dh_src (gsb_rgcn_layer_bwd).
+ * ==================================================================================== */
+gsb_status gsb_encoder_ws_bytes(gsb_blocks_t b, const float* const* W_in, int32_t d_out, size_t* bytes);
+gsb_status gsb_encoder_fwd(gsb_blocks_t b, const void* arena, const float* const* W_in, int32_t d_out, float* H0,
+                           void* ws, size_t ws_bytes, void* stream);
+gsb_status gsb_encoder_bwd(gsb_blocks_t b, const void* arena, const float* const* W_in, const float* dH0,
+                           int32_t d_out, float* const* dW_in, void* ws, size_t ws_bytes, void* stream);
 
 /* Plain GEMM on the same tcgen05 3xTF32 path as the layers (single group), fp32 row-major:
  *   mode 0 (NN): C[M][N]  = A[M][K] B[K][N]        (K multiple of 32)
@@ -289,18 +320,20 @@ typedef struct gsb_partition* gsb_partition_t;
 gsb_status gsb_partition_create(int32_t num_ntypes, const int64_t* ntype_count, int32_t world, int32_t rank,
                                 const int64_t* bounds, gsb_partition_t* out);
 gsb_status gsb_partition_destroy(gsb_partition_t p);
-/* Register this rank's shard of ntype t: device fp32 rows for its owned local ids. */
-gsb_status gsb_partition_set_shard(gsb_partition_t p, int32_t ntype, const float* rows, int32_t dim);
+/* Register this rank's shard of ntype t: device rows (dim elements of dtype, 16-byte
+ * aligned, row bytes a multiple of 16) for its owned local ids. */
+gsb_status gsb_partition_set_shard(gsb_partition_t p, int32_t ntype, const void* rows, int32_t dim, int32_t dtype);
 /* Owner bucketing (K11): for i < n (n = *n_dev if non-NULL, else n_cap): send_gid[perm[i]] =
  * gid[i] grouped by owner rank in rank order; send_counts: device int64 [world] (overwritten);
  * ws: device scratch of 8*world bytes.  Order inside a bucket is unspecified; perm is exact. */
 gsb_status gsb_bucket_by_owner(gsb_partition_t p, const int64_t* gid, const int64_t* n_dev, int64_t n_cap,
                                int64_t* send_gid, int32_t* perm, int64_t* send_counts, void* ws, void* stream);
-/* out[i, :] = own shard row of gid[i] (every gid must be owned by this rank). */
-gsb_status gsb_shard_gather(gsb_partition_t p, const int64_t* gid, int64_t n, float* out, void* stream);
-/* out[i, :] = rows[perm[i], :] for i < n (n = *n_dev if non-NULL, else n_cap). */
-gsb_status gsb_rows_permute(const float* rows, int32_t d, const int32_t* perm, const int64_t* n_dev, int64_t n_cap,
-                            float* out, void* stream);
+/* out[i, :] = own shard row of gid[i] (every gid must be owned by this rank); exact copy. */
+gsb_status gsb_shard_gather(gsb_partition_t p, const int64_t* gid, int64_t n, void* out, void* stream);
+/* out[i, :] = rows[perm[i], :] for i < n (n = *n_dev if non-NULL, else n_cap); rows of
+ * row_bytes bytes (a multiple of 16), copied exactly. */
+gsb_status gsb_rows_permute(const void* rows, int32_t row_bytes, const int32_t* perm, const int64_t* n_dev,
+                            int64_t n_cap, void* out, void* stream);
 
 /* ======================================================================================
  * Peer feature access over NVLink (§8(e); P:L86 distributed tensors).  Each rank keeps only
@@ -316,9 +349,9 @@ gsb_status gsb_ipc_open(const void* handle, int64_t offset, void** dev_ptr_out);
 gsb_status gsb_ipc_close(void* base_ptr);
 /* Register ntype t's partitioned table: bounds host int64 [world+1] (local-id ranges, bounds[0]
  * = 0, bounds[world] = count), ptrs host [world] device pointers (own shard + IPC-mapped peer
- * shards), row-major [bounds[w+1]-bounds[w]][dim] fp32.  world <= 8. */
+ * shards), row-major [bounds[w+1]-bounds[w]][dim] of dtype (GSB_F32 / GSB_BF16).  world <= 8. */
 gsb_status gsb_graph_set_feature_peers(gsb_graph_t g, int32_t ntype, int32_t world, const int64_t* bounds,
-                                       const float* const* ptrs, int32_t dim);
+                                       const void* const* ptrs, int32_t dim, int32_t dtype);
 
 /* ======================================================================================
  * Optimizer (paper silent, R-adam): Adam with bias correction over a flat

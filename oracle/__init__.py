@@ -231,6 +231,47 @@ def gather(g: Graph, gids: np.ndarray) -> np.ndarray:
     return out
 
 
+def input_rows(g: Graph, t: int, local_ids: np.ndarray) -> np.ndarray:
+    """Raw feature rows F_t[local_ids] (per-ntype width), widened to float64 (exact)."""
+    import synth
+    if g.feats[t] is None:
+        g.feats[t] = synth.feature_table(g.cfg, t)
+    return g.feats[t][np.asarray(local_ids, np.int64)].astype(np.float64)
+
+
+def encoder_fwd(g: Graph, params: Dict[str, np.ndarray], gids: np.ndarray) -> np.ndarray:
+    """Input encoder (§8(a) a6; "node input encoders handle node features"
+    featureless nodes): H0[i] = F_t[local(i)] Win_t for an ntype t with a projection,
+    H0[i] = F_t[local(i)] (frozen table of width feat_dim) otherwise.  fp64."""
+    cfg = g.cfg
+    gids = np.asarray(gids, np.int64)
+    ty = g.type_of(gids)
+    H0 = np.zeros((len(gids), cfg.feat_dim))
+    for t in range(g.T):
+        rows = np.nonzero(ty == t)[0]
+        if len(rows) == 0:
+            continue
+        X = input_rows(g, t, gids[rows] - g.node_off[t])
+        H0[rows] = X @ params[f"Win{t}"].astype(np.float64) if cfg.project[t] else X
+    return H0
+
+
+def encoder_bwd(g: Graph, params: Dict[str, np.ndarray], gids: np.ndarray, dH0: np.ndarray) -> Dict[str, np.ndarray]:
+    """dWin_t = sum over input rows i of type t of F_t[local(i)]^T dH0[i] (H0 = X Win_t is
+    linear in Win_t); frozen tables get no gradient."""
+    cfg = g.cfg
+    gids = np.asarray(gids, np.int64)
+    ty = g.type_of(gids)
+    out = {}
+    for t in range(g.T):
+        if not cfg.project[t]:
+            continue
+        rows = np.nonzero(ty == t)[0]
+        X = input_rows(g, t, gids[rows] - g.node_off[t])
+        out[f"Win{t}"] = X.T @ np.asarray(dH0, np.float64)[rows]
+    return out
+
+
 def rgcn_fwd(blk: Block, R: int, h_src: np.ndarray, W: np.ndarray, b: np.ndarray, relu: bool):
     h_src = _c(h_src, np.float64)
     W = _c(W, np.float64)
@@ -334,8 +375,12 @@ def nc_step(g: Graph, params: Dict[str, np.ndarray], seeds: np.ndarray, labels: 
     cfg = g.cfg
     L = len(cfg.fanouts)
     blocks = sample_blocks(g, seeds, cfg.fanouts, rng_seed, step)
-    x0 = gather(g, blocks[0].src_gid)
-    h = x0.astype(np.float64)
+    if cfg.has_encoder:      # a6: projected / frozen input rows
+        x0 = None
+        h = encoder_fwd(g, params, blocks[0].src_gid)
+    else:
+        x0 = gather(g, blocks[0].src_gid)
+        h = x0.astype(np.float64)
     hs, zs, ins = [], [], []
     for l in range(L):
         ins.append(h)
@@ -349,10 +394,14 @@ def nc_step(g: Graph, params: Dict[str, np.ndarray], seeds: np.ndarray, labels: 
     for l in reversed(range(L)):
         dhs[l] = dh
         dW, db, dh = rgcn_bwd(blocks[l], g.R, ins[l], params[f"W{l}"], zs[l], relu=(l < L - 1),
-                              dh_dst=dh, need_dh_src=(l > 0))
+                              dh_dst=dh, need_dh_src=(l > 0 or cfg.has_encoder))
         grads[f"W{l}"] = dW
         grads[f"b{l}"] = db
-    return StepResult(loss, blocks, x0, hs, zs, grads, {"logits": logits, "dh": dhs, "ins": ins})
+    extra = {"logits": logits, "dh": dhs, "ins": ins}
+    if cfg.has_encoder:
+        grads.update(encoder_bwd(g, params, blocks[0].src_gid, dh))
+        extra["dH0"] = dh
+    return StepResult(loss, blocks, x0, hs, zs, grads, extra)
 
 
 def lp_seeds(u: np.ndarray, v: np.ndarray, neg: np.ndarray) -> np.ndarray:

@@ -38,7 +38,7 @@ SIGS = {
     "gsb_csc_build_bytes": [P, i32, i64, C.POINTER(sz)],
     "gsb_csc_build": [P, i32, P, P, P, i64, P, P, C.POINTER(i64), P, sz, P],
     "gsb_graph_set_csc": [P, i32, P, P, i64, i64],
-    "gsb_graph_set_features": [P, i32, P, i32],
+    "gsb_graph_set_features": [P, i32, P, i32, i32],
     "gsb_gather": [P, P, i64, P, P],
     "gsb_blocks_create": [P, i32, P, i64, i64, C.POINTER(P)],
     "gsb_blocks_destroy": [P],
@@ -54,18 +54,21 @@ SIGS = {
     "gsb_blocks_dst_rows": [P, i32, C.POINTER(i64)],
     "gsb_layer_acat_floats": [P, i32, i32, C.POINTER(i64)],
     "gsb_rgcn_layer_fwd": [P, P, i32, P, i32, P, P, i32, i32, P, P, P],
-    "gsb_rgcn_layer_fwd_rowmap": [P, P, i32, P, P, i32, P, P, i32, i32, P, P, P],
+    "gsb_rgcn_layer_fwd_ex": [P, P, i32, P, i32, P, i32, P, P, i32, i32, P, P, P],
     "gsb_rgcn_layer_bwd": [P, P, i32, P, P, P, P, i32, i32, i32, P, P, P, P, P],
     "gsb_partition_create": [i32, P, i32, i32, P, C.POINTER(P)],
     "gsb_partition_destroy": [P],
-    "gsb_partition_set_shard": [P, i32, P, i32],
+    "gsb_partition_set_shard": [P, i32, P, i32, i32],
     "gsb_bucket_by_owner": [P, P, P, i64, P, P, P, P, P],
     "gsb_shard_gather": [P, P, i64, P, P],
     "gsb_rows_permute": [P, i32, P, P, i64, P, P],
     "gsb_ipc_handle": [P, P, C.POINTER(i64)],
     "gsb_ipc_open": [P, i64, C.POINTER(P)],
     "gsb_ipc_close": [P],
-    "gsb_graph_set_feature_peers": [P, i32, i32, P, P, i32],
+    "gsb_encoder_ws_bytes": [P, P, i32, P],
+    "gsb_encoder_fwd": [P, P, P, i32, P, P, sz, P],
+    "gsb_encoder_bwd": [P, P, P, P, i32, P, P, sz, P],
+    "gsb_graph_set_feature_peers": [P, i32, i32, P, P, i32, i32],
     "gsb_gemm": [i32, P, i64, P, i64, i64, i32, i32, P, i64, P],
     "gsb_nc_loss": [P, i64, i32, P, P, i32, P, P, i64, P, P, P, P, P, P, P],
     "gsb_adam_step": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P],

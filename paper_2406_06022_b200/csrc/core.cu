@@ -104,43 +104,44 @@ __global__ void csc_finish_kernel(const uint64_t* __restrict__ keys, const unsig
 }
 
 // ------------------------------------------------------------------------------------
-// gather: out[i, :] = F_t[gid_i - off_t, :]; one float4 per thread-iteration
+// gather: out[i, :] = F_t[gid_i - off_t, :]; one 16-byte chunk per thread-iteration
+// (dtype-agnostic exact copy: fp32 or bf16 rows)
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) gather_kernel(GraphDev g, const int64_t* __restrict__ gid,
                                                      const int64_t* __restrict__ n_dev, int64_t n_host,
-                                                     float* __restrict__ out) {
+                                                     uint4* __restrict__ out) {
     const int64_t n = n_dev ? *n_dev : n_host;
-    const int d4 = g.feat_dim >> 2;
-    const int64_t total = n * d4;
+    const int d16 = g.feat_row_bytes >> 4;
+    const int64_t total = n * d16;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t N = g.node_off[g.T];
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     // 4 independent rows in flight per thread
     for (; i < total; i += 4 * stride) {
-        float4 v[4];
+        uint4 v[4];
         int64_t idx[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             idx[u] = i + u * stride;
-            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            v[u] = make_uint4(0u, 0u, 0u, 0u);
             if (idx[u] < total) {
-                int64_t row = idx[u] / d4;
-                int c = (int)(idx[u] - row * d4);
+                int64_t row = idx[u] / d16;
+                int c = (int)(idx[u] - row * d16);
                 int64_t x = __ldg(gid + row);
-                if (x >= 0 && x < N) v[u] = ldg_nc_f4(reinterpret_cast<const float4*>(feat_row(g, x)) + c);
+                if (x >= 0 && x < N) v[u] = ldg_nc_u4(feat_row(g, x) + c);
             }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (idx[u] < total) reinterpret_cast<float4*>(out)[idx[u]] = v[u];
+            if (idx[u] < total) out[idx[u]] = v[u];
     }
 }
 
 gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_dev, int64_t n_host, int64_t n_max,
-                         float* out, cudaStream_t s) {
-    int64_t work = n_max * (G->dev.feat_dim / 4);
+                         void* out, cudaStream_t s) {
+    int64_t work = n_max * (G->dev.feat_row_bytes / 16);
     int grid = grid_for(ceil_div(work, 4), 256, kNumSMs * 8);
-    GSB_LAUNCH("gather", gather_kernel, grid, 256, 0, s, G->dev, gid, n_dev, n_host, out);
+    GSB_LAUNCH("gather", gather_kernel, grid, 256, 0, s, G->dev, gid, n_dev, n_host, static_cast<uint4*>(out));
     return GSB_OK;
 }
 
@@ -198,6 +199,27 @@ __global__ void spin_kernel(int64_t ns) {
     do {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     } while ((int64_t)(t1 - t0) < ns);
+}
+
+gsb_status set_feature_format(Graph* G, int32_t ntype, int32_t dim, int32_t dtype) {
+    const int es = dtype_size(dtype);
+    GSB_CHECK_ARG(es > 0, "dtype %d not GSB_F32 / GSB_BF16", dtype);
+    GSB_CHECK_ARG(dim > 0 && (dim * es) % 16 == 0, "feature rows must be a positive multiple of 16 bytes "
+                  "(dim %d x %d B)", dim, es);
+    GSB_CHECK_ARG(!G->dtype_set || G->dev.feat_dtype == dtype, "all ntypes must share one feature dtype");
+    G->dtype_set = true;
+    G->dev.feat_dtype = dtype;
+    G->dev.dim_t[ntype] = dim;
+    G->dev.row_bytes_t[ntype] = dim * es;
+    // uniform width over the registered ntypes (required by the fused layer-0 path and gathers)
+    int u = 0;
+    for (int t = 0; t < G->dev.T; ++t) {
+        if (!G->dev.dim_t[t]) continue;
+        u = (u == 0 || u == G->dev.dim_t[t]) ? G->dev.dim_t[t] : -1;
+    }
+    G->dev.feat_dim = u > 0 ? u : 0;
+    G->dev.feat_row_bytes = u > 0 ? u * es : 0;
+    return GSB_OK;
 }
 
 }  // namespace gsb
@@ -381,22 +403,21 @@ gsb_status gsb_graph_set_csc(gsb_graph_t g, int32_t etype, const int64_t* indptr
     return GSB_OK;
 }
 
-gsb_status gsb_graph_set_features(gsb_graph_t g, int32_t ntype, const float* feat, int32_t dim) {
+gsb_status gsb_graph_set_features(gsb_graph_t g, int32_t ntype, const void* feat, int32_t dim, int32_t dtype) {
     Graph* G = reinterpret_cast<Graph*>(g);
     GSB_CHECK_ARG(G && ntype >= 0 && ntype < G->dev.T && feat, "bad argument");
-    GSB_CHECK_ARG(dim > 0 && dim % 4 == 0, "feature dim %d must be a positive multiple of 4", dim);
-    GSB_CHECK_ARG(G->dev.feat_dim == 0 || G->dev.feat_dim == dim, "all ntypes must share one feature dim");
     GSB_CHECK_ARG(((uintptr_t)feat & 15) == 0, "feature table must be 16-byte aligned");
-    G->dev.feat_dim = dim;
-    G->dev.feat[ntype] = feat;
+    gsb_status st = set_feature_format(G, ntype, dim, dtype);
+    if (st != GSB_OK) return st;
+    G->dev.feat[ntype] = static_cast<const char*>(feat);
     return GSB_OK;
 }
 
-gsb_status gsb_gather(gsb_graph_t g, const int64_t* gid, int64_t n, float* out, void* stream) {
+gsb_status gsb_gather(gsb_graph_t g, const int64_t* gid, int64_t n, void* out, void* stream) {
     Graph* G = reinterpret_cast<Graph*>(g);
     GSB_CHECK_ARG(G && (n == 0 || (gid && out)), "bad argument");
-    GSB_CHECK_ARG(G->dev.feat_dim > 0, "features not registered");
     for (int t = 0; t < G->dev.T; ++t) GSB_CHECK_ARG(G->dev.feat[t], "features of ntype %d not registered", t);
+    GSB_CHECK_ARG(G->dev.feat_dim > 0, "gather needs one feature width for all ntypes");
     if (n == 0) return GSB_OK;
     return launch_gather(G, gid, nullptr, n, n, out, (cudaStream_t)stream);
 }

@@ -12,8 +12,8 @@ struct PartDev {
     int32_t world, rank, T;
     int64_t lo[kMaxT][9];   // local-id boundaries of each rank per ntype (world <= 8)
     int64_t node_off[kMaxT + 1];
-    const float* shard[kMaxT];   // local shard rows [lo[t][rank], lo[t][rank+1])
-    int32_t dim;
+    const char* shard[kMaxT];    // local shard rows [lo[t][rank], lo[t][rank+1])
+    int32_t dim, row_bytes;      // elements / bytes per row (fp32 or bf16)
 };
 
 __device__ __forceinline__ int part_type(const PartDev& p, int64_t gid) {
@@ -98,28 +98,29 @@ __global__ void owner_scatter_kernel(PartDev p, const int64_t* __restrict__ gid,
     }
 }
 
-__global__ void shard_gather_kernel(PartDev p, const int64_t* __restrict__ gid, int64_t n, float* __restrict__ out) {
-    const int d4 = p.dim >> 2;
-    const int64_t total = n * d4;
+// row copies in 16-byte chunks (dtype-agnostic)
+__global__ void shard_gather_kernel(PartDev p, const int64_t* __restrict__ gid, int64_t n, uint4* __restrict__ out) {
+    const int d16 = p.row_bytes >> 4;
+    const int64_t total = n * d16;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = i / d4;
-        const int c = (int)(i - row * d4);
+        const int64_t row = i / d16;
+        const int c = (int)(i - row * d16);
         const int64_t x = gid[row];
         const int t = part_type(p, x);
         const int64_t local = x - p.node_off[t] - p.lo[t][p.rank];
-        reinterpret_cast<float4*>(out)[i] = __ldg(reinterpret_cast<const float4*>(p.shard[t] + local * p.dim) + c);
+        out[i] = __ldg(reinterpret_cast<const uint4*>(p.shard[t] + local * p.row_bytes) + c);
     }
 }
 
-__global__ void rows_permute_kernel(const float* __restrict__ rows, int d, const int32_t* __restrict__ perm,
-                                    const int64_t* __restrict__ n_dev, int64_t n_cap, float* __restrict__ out) {
+__global__ void rows_permute_kernel(const char* __restrict__ rows, int row_bytes, const int32_t* __restrict__ perm,
+                                    const int64_t* __restrict__ n_dev, int64_t n_cap, uint4* __restrict__ out) {
     const int64_t n = n_dev ? min(*n_dev, n_cap) : n_cap;
-    const int d4 = d >> 2;
-    const int64_t total = n * d4;
+    const int d16 = row_bytes >> 4;
+    const int64_t total = n * d16;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = i / d4;
-        const int c = (int)(i - row * d4);
-        reinterpret_cast<float4*>(out)[i] = __ldg(reinterpret_cast<const float4*>(rows + (int64_t)perm[row] * d) + c);
+        const int64_t row = i / d16;
+        const int c = (int)(i - row * d16);
+        out[i] = __ldg(reinterpret_cast<const uint4*>(rows + (int64_t)perm[row] * row_bytes) + c);
     }
 }
 
@@ -163,12 +164,16 @@ gsb_status gsb_partition_destroy(gsb_partition_t p) {
     return GSB_OK;
 }
 
-gsb_status gsb_partition_set_shard(gsb_partition_t p, int32_t ntype, const float* rows, int32_t dim) {
+gsb_status gsb_partition_set_shard(gsb_partition_t p, int32_t ntype, const void* rows, int32_t dim, int32_t dtype) {
     Part* P = reinterpret_cast<Part*>(p);
-    GSB_CHECK_ARG(P && ntype >= 0 && ntype < P->dev.T && dim > 0 && dim % 4 == 0, "bad argument");
-    GSB_CHECK_ARG(P->dev.dim == 0 || P->dev.dim == dim, "all shards must share one dim");
+    const int es = dtype_size(dtype);
+    GSB_CHECK_ARG(P && ntype >= 0 && ntype < P->dev.T && es > 0 && dim > 0 && (dim * es) % 16 == 0,
+                  "bad argument (rows must be a positive multiple of 16 bytes)");
+    GSB_CHECK_ARG(P->dev.dim == 0 || P->dev.row_bytes == dim * es, "all shards must share one row format");
+    GSB_CHECK_ARG(((uintptr_t)rows & 15) == 0, "shard must be 16-byte aligned");
     P->dev.dim = dim;
-    P->dev.shard[ntype] = rows;
+    P->dev.row_bytes = dim * es;
+    P->dev.shard[ntype] = static_cast<const char*>(rows);
     return GSB_OK;
 }
 
@@ -189,7 +194,7 @@ gsb_status gsb_bucket_by_owner(gsb_partition_t p, const int64_t* gid, const int6
     return GSB_OK;
 }
 
-gsb_status gsb_shard_gather(gsb_partition_t p, const int64_t* gid, int64_t n, float* out, void* stream) {
+gsb_status gsb_shard_gather(gsb_partition_t p, const int64_t* gid, int64_t n, void* out, void* stream) {
     Part* P = reinterpret_cast<Part*>(p);
     GSB_CHECK_ARG(P && (n == 0 || (gid && out)), "null argument");
     GSB_CHECK_ARG(P->dev.dim > 0, "no shard registered");
@@ -197,17 +202,18 @@ gsb_status gsb_shard_gather(gsb_partition_t p, const int64_t* gid, int64_t n, fl
         GSB_CHECK_ARG(P->dev.shard[t] || P->dev.lo[t][P->dev.rank + 1] == P->dev.lo[t][P->dev.rank],
                       "shard of ntype %d not registered", t);
     if (n == 0) return GSB_OK;
-    GSB_LAUNCH("shard_gather", shard_gather_kernel, grid_for(n * (P->dev.dim / 4), 256, kNumSMs * 8), 256, 0,
-               (cudaStream_t)stream, P->dev, gid, n, out);
+    GSB_LAUNCH("shard_gather", shard_gather_kernel, grid_for(n * (P->dev.row_bytes / 16), 256, kNumSMs * 8), 256, 0,
+               (cudaStream_t)stream, P->dev, gid, n, static_cast<uint4*>(out));
     return GSB_OK;
 }
 
-gsb_status gsb_rows_permute(const float* rows, int32_t d, const int32_t* perm, const int64_t* n_dev, int64_t n_cap,
-                            float* out, void* stream) {
-    GSB_CHECK_ARG(rows && perm && out && d > 0 && d % 4 == 0 && n_cap >= 0, "bad argument");
+gsb_status gsb_rows_permute(const void* rows, int32_t row_bytes, const int32_t* perm, const int64_t* n_dev,
+                            int64_t n_cap, void* out, void* stream) {
+    GSB_CHECK_ARG(rows && perm && out && row_bytes > 0 && row_bytes % 16 == 0 && n_cap >= 0, "bad argument");
     if (n_cap == 0) return GSB_OK;
-    GSB_LAUNCH("rows_permute", rows_permute_kernel, grid_for(n_cap * (d / 4), 256, kNumSMs * 8), 256, 0,
-               (cudaStream_t)stream, rows, d, perm, n_dev, n_cap, out);
+    GSB_LAUNCH("rows_permute", rows_permute_kernel, grid_for(n_cap * (row_bytes / 16), 256, kNumSMs * 8), 256, 0,
+               (cudaStream_t)stream, static_cast<const char*>(rows), row_bytes, perm, n_dev, n_cap,
+               static_cast<uint4*>(out));
     return GSB_OK;
 }
 

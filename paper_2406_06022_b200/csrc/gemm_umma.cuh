@@ -19,6 +19,11 @@
 
 namespace gsb {
 
+using umma::cp16;
+using umma::cp4;
+using umma::cp_commit;
+using umma::cp_wait;
+
 enum { UMMA_NN = 0, UMMA_NT = 1, UMMA_TN = 2 };
 
 struct UProb {
@@ -45,17 +50,6 @@ constexpr int UM_PANEL = 16384;            // bytes of one 128 x 32 fp32/tf32 pa
 constexpr int UM_STAGE = 4 * UM_PANEL;     // A_hi(raw), A_lo, B_hi(raw), B_lo
 constexpr int UM_STAGES = 3;
 constexpr int UM_SMEM = UM_STAGES * UM_STAGE + 1024;
-
-// ---- cp.async (LDGSTS) with zero fill ------------------------------------------------
-__device__ __forceinline__ void cp16(uint32_t dst, const void* src, int bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp4(uint32_t dst, const void* src, int bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Copy the 4 elements [c, c+4) of row `row` (cols >= ncols, rows out of range -> 0) to dst.
 __device__ __forceinline__ void cp_chunk(uint32_t dst, const float* base, int64_t ld, int64_t row, bool row_ok,

@@ -60,7 +60,11 @@ void count_launch(int n = 1);
 // ------------------------------------------------------------------------------------
 struct GraphDev {
     int32_t T, R, S;                    // ntypes, etypes, max slots
-    int32_t feat_dim;
+    int32_t feat_dim;                   // elements per feature row when uniform over ntypes, else 0
+    int32_t feat_dtype;                 // GSB_F32 / GSB_BF16 (one element type for all ntypes)
+    int32_t feat_row_bytes;             // feat_dim * element size (uniform case)
+    int32_t dim_t[kMaxT];               // per-ntype row width (elements; 0 = not registered)
+    int32_t row_bytes_t[kMaxT];         // per-ntype row bytes (multiple of 16)
     int64_t node_off[kMaxT + 1];
     int32_t src_t[kMaxR], dst_t[kMaxR];
     int32_t n_slots[kMaxT];             // in-relations of each ntype
@@ -68,12 +72,12 @@ struct GraphDev {
     const int64_t* indptr[kMaxR];
     const int32_t* indices[kMaxR];
     int64_t eid_base[kMaxR];
-    const float* feat[kMaxT];
+    const char* feat[kMaxT];
     // node-ID partitioned features read over NVLink (peer.cu): rank w owns local ids
     // [plo[t][w], plo[t][w+1]) of ntype t at peer[t][w] (an IPC-mapped pointer for w != self)
     int32_t nparts;
     int64_t plo[kMaxT][kMaxPeers + 1];
-    const float* peer[kMaxT][kMaxPeers];
+    const char* peer[kMaxT][kMaxPeers];
 };
 
 __host__ __device__ inline int type_of(const GraphDev& g, int64_t gid) {
@@ -83,18 +87,27 @@ __host__ __device__ inline int type_of(const GraphDev& g, int64_t gid) {
     return t;
 }
 
-// Row of node gid in its feature table: local table, or the owner's (possibly peer) shard.
-__device__ __forceinline__ const float* feat_row(const GraphDev& g, int64_t gid) {
+// Row of node gid in its feature table (16-byte chunks): local table, or the owner's
+// (possibly peer) shard.
+__device__ __forceinline__ const uint4* feat_row(const GraphDev& g, int64_t gid) {
     const int t = type_of(g, gid);
     const int64_t local = gid - g.node_off[t];
     if (g.nparts > 1) {
         int w = 0;
 #pragma unroll 1
         for (int k = 1; k < g.nparts; ++k) w += (local >= g.plo[t][k]) ? 1 : 0;
-        return g.peer[t][w] + (local - g.plo[t][w]) * g.feat_dim;
+        return reinterpret_cast<const uint4*>(g.peer[t][w] + (local - g.plo[t][w]) * g.row_bytes_t[t]);
     }
-    return g.feat[t] + local * g.feat_dim;
+    return reinterpret_cast<const uint4*>(g.feat[t] + local * g.row_bytes_t[t]);
 }
+
+inline int dtype_size(int32_t dtype) { return dtype == GSB_BF16 ? 2 : (dtype == GSB_F32 ? 4 : 0); }
+
+struct Graph;
+// feature row format shared by all ntypes (core.cu)
+gsb_status set_feature_format(Graph* G, int32_t ntype, int32_t dim, int32_t dtype);
+gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_dev, int64_t n_host, int64_t n_max,
+                         void* out, cudaStream_t s);
 
 // Per-hop sizes, written by kernels (device resident; never copied to the host on the
 // hot path).  dst rows of ntype t are [dst_off[t], dst_off[t+1]); src rows likewise.
@@ -122,6 +135,7 @@ struct HopBufs {
 
 struct Graph {
     GraphDev dev;
+    bool dtype_set = false;
     int64_t counts[kMaxT];
     int64_t n_edges[kMaxR];
     int64_t total_nodes;
@@ -168,6 +182,33 @@ __device__ __forceinline__ float4 ldg_nc_f4(const float4* p) {
                  : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                  : "l"(p));
     return r;
+}
+
+__device__ __forceinline__ uint4 ldg_nc_u4(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// 16-byte chunk -> fp32 values: 4 floats (fp32 rows) or 8 bf16 widened exactly
+template <bool BF16>
+struct Chunk {
+    static constexpr int kVec = BF16 ? 8 : 4;
+};
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+template <bool BF16>
+__device__ __forceinline__ void chunk_acc(float* acc, const uint4 x) {
+    if (BF16) {
+        acc[0] += bf16_lo(x.x); acc[1] += bf16_hi(x.x); acc[2] += bf16_lo(x.y); acc[3] += bf16_hi(x.y);
+        acc[4] += bf16_lo(x.z); acc[5] += bf16_hi(x.z); acc[6] += bf16_lo(x.w); acc[7] += bf16_hi(x.w);
+    } else {
+        acc[0] += __uint_as_float(x.x); acc[1] += __uint_as_float(x.y);
+        acc[2] += __uint_as_float(x.z); acc[3] += __uint_as_float(x.w);
+    }
 }
 
 __device__ __forceinline__ void red_add_f4(float* p, float4 v) {

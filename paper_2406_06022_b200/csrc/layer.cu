@@ -7,32 +7,39 @@
 namespace gsb {
 
 // ------------------------------------------------------------------------------------
-// aggregation: warp per dst row j; lanes over feature columns (float4)
+// aggregation: warp per dst row j
 //   Acat[j, s*d + :] = mean_{e in seg(j,s)} h_src[e_src[e], :]    (0 when empty)
 //   Acat[j, S_t*d + :] = h_src[self(j), :]
+// Source rows are read in 16-byte chunks (4 fp32 or 8 bf16 values, widened exactly to
+// fp32); LPE lanes cover one row's chunks and the warp's 32/LPE lane groups take
+// different edges of the segment (4 rows in flight per lane), reduced by shuffles at the
+// end -- so narrow rows (64-d fp32, 128-d bf16) still keep every lane loading.
 // ------------------------------------------------------------------------------------
 template <bool FEAT>
-__device__ __forceinline__ const float4* src_row(const GraphDev& g, const float* h, int d, int64_t row, int64_t gid,
-                                                 const int32_t* rowmap = nullptr) {
-    if (!FEAT && rowmap) row = rowmap[row];   // rows delivered in exchange order (partitioned features)
-    if (FEAT) return reinterpret_cast<const float4*>(feat_row(g, gid));   // layer 0: fused gather (a5)
-    return reinterpret_cast<const float4*>(h + row * d);
+__device__ __forceinline__ const uint4* src_row(const GraphDev& g, const char* h, int row_bytes, int64_t key,
+                                                const int32_t* rowmap) {
+    if (FEAT) return feat_row(g, key);              // layer 0: fused gather by gid (a5)
+    const int64_t row = rowmap ? (int64_t)rowmap[key] : key;   // exchange order (partitioned features)
+    return reinterpret_cast<const uint4*>(h + row * row_bytes);
 }
 
-// FEAT: h_src rows come from the feature tables via e_src_gid / dst_gid (no x0 buffer)
-template <bool FEAT>
+// FEAT: source rows come from the feature tables via e_src_gid / dst_gid (no x0 buffer)
+template <bool FEAT, bool BF16, int LPE>
 __global__ void __launch_bounds__(256, 6) agg_kernel(GraphDev g, const HopMeta* __restrict__ m,
                                                   const int64_t* __restrict__ seg_ptr,
                                                   const int32_t* __restrict__ e_src,
                                                   const int64_t* __restrict__ e_src_gid,
-                                                  const int64_t* __restrict__ dst_gid, const float* __restrict__ h,
-                                                  int d, float* __restrict__ acat, int64_t lda,
+                                                  const int64_t* __restrict__ dst_gid, const char* __restrict__ h,
+                                                  int row_bytes, int d, float* __restrict__ acat, int64_t lda,
                                                   const int32_t* __restrict__ rowmap) {
+    constexpr int V = Chunk<BF16>::kVec;
+    constexpr int G = 32 / LPE;                  // edges per warp pass
     const int lane = threadIdx.x & 31;
+    const int grp = lane / LPE, sub = lane % LPE;
     const int S = g.S;
     const int64_t n = m->n_dst;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int d4 = d >> 2;
+    const int cpr = row_bytes >> 4;              // 16-byte chunks per row
     for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < n; j += warps) {
         int t = 0;
         for (int k = 1; k < g.T; ++k) t += (j >= m->dst_off[k]) ? 1 : 0;
@@ -41,49 +48,87 @@ __global__ void __launch_bounds__(256, 6) agg_kernel(GraphDev g, const HopMeta* 
         for (int s = 0; s < St; ++s) {
             const int64_t e0 = seg_ptr[j * S + s], e1 = seg_ptr[j * S + s + 1];
             const float inv = (e1 > e0) ? 1.f / (float)(e1 - e0) : 0.f;
-            // every lane runs every column chunk (the shuffles below need the whole warp);
-            // lanes past the row width only predicate their loads and stores
-            for (int c0 = 0; c0 < d4; c0 += 32) {
-                const int c = c0 + lane;
-                const bool cl = c < d4;
-                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            // every lane runs every chunk pass (the shuffles need the whole warp); lanes past
+            // the row width or the segment end only predicate their loads and stores
+            for (int c0 = 0; c0 < cpr; c0 += LPE) {
+                const int c = c0 + sub;
+                const bool cl = c < cpr;
+                float acc[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] = 0.f;
                 for (int64_t cb = e0; cb < e1; cb += 32) {
                     // one coalesced load of up to 32 source keys, broadcast by shuffle
                     const int64_t key = (cb + lane < e1) ? (FEAT ? e_src_gid[cb + lane] : (int64_t)e_src[cb + lane]) : 0;
                     const int cnt = (int)min((int64_t)32, e1 - cb);
-                    int k = 0;
-                    for (; k + 4 <= cnt; k += 4) {
-                        const int64_t k0 = __shfl_sync(0xffffffffu, key, k), k1 = __shfl_sync(0xffffffffu, key, k + 1);
-                        const int64_t k2 = __shfl_sync(0xffffffffu, key, k + 2), k3 = __shfl_sync(0xffffffffu, key, k + 3);
-                        if (cl) {
-                            float4 x0 = __ldg(src_row<FEAT>(g, h, d, k0, k0, rowmap) + c);
-                            float4 x1 = __ldg(src_row<FEAT>(g, h, d, k1, k1, rowmap) + c);
-                            float4 x2 = __ldg(src_row<FEAT>(g, h, d, k2, k2, rowmap) + c);
-                            float4 x3 = __ldg(src_row<FEAT>(g, h, d, k3, k3, rowmap) + c);
-                            acc.x += x0.x; acc.y += x0.y; acc.z += x0.z; acc.w += x0.w;
-                            acc.x += x1.x; acc.y += x1.y; acc.z += x1.z; acc.w += x1.w;
-                            acc.x += x2.x; acc.y += x2.y; acc.z += x2.z; acc.w += x2.w;
-                            acc.x += x3.x; acc.y += x3.y; acc.z += x3.z; acc.w += x3.w;
+                    for (int k = 0; k < cnt; k += 4 * G) {
+                        uint4 x[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int idx = k + grp + G * u;
+                            const int64_t kk = __shfl_sync(0xffffffffu, key, idx & 31);
+                            x[u] = make_uint4(0u, 0u, 0u, 0u);
+                            if (cl && idx < cnt) x[u] = __ldg(src_row<FEAT>(g, h, row_bytes, kk, rowmap) + c);
                         }
-                    }
-                    for (; k < cnt; ++k) {
-                        const int64_t kk = __shfl_sync(0xffffffffu, key, k);
-                        if (cl) {
-                            float4 x = __ldg(src_row<FEAT>(g, h, d, kk, kk, rowmap) + c);
-                            acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
-                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) chunk_acc<BF16>(acc, x[u]);
                     }
                 }
-                if (cl) {
-                    acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
-                    reinterpret_cast<float4*>(out + (int64_t)s * d)[c] = acc;
+#pragma unroll
+                for (int o = LPE; o < 32; o <<= 1)
+#pragma unroll
+                    for (int v = 0; v < V; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], o);
+                if (cl && grp == 0) {
+                    float4* o4 = reinterpret_cast<float4*>(out + (int64_t)s * d + (int64_t)c * V);
+#pragma unroll
+                    for (int v = 0; v < V; v += 4)
+                        o4[v / 4] = make_float4(acc[v] * inv, acc[v + 1] * inv, acc[v + 2] * inv, acc[v + 3] * inv);
                 }
             }
         }
         const int64_t self = m->src_off[t] + (j - m->dst_off[t]);
-        const float4* ps = src_row<FEAT>(g, h, d, self, FEAT ? dst_gid[j] : 0, rowmap);
-        for (int c = lane; c < d4; c += 32) reinterpret_cast<float4*>(out + (int64_t)St * d)[c] = __ldg(ps + c);
+        const uint4* ps = src_row<FEAT>(g, h, row_bytes, FEAT ? dst_gid[j] : self, rowmap);
+        for (int c = lane; c < cpr; c += 32) {
+            float r[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) r[v] = 0.f;
+            chunk_acc<BF16>(r, __ldg(ps + c));
+            float4* o4 = reinterpret_cast<float4*>(out + (int64_t)St * d + (int64_t)c * V);
+#pragma unroll
+            for (int v = 0; v < V; v += 4) o4[v / 4] = make_float4(r[v], r[v + 1], r[v + 2], r[v + 3]);
+        }
     }
+}
+
+template <bool FEAT, bool BF16>
+static gsb_status launch_agg_lpe(const char* name, int grid, cudaStream_t s, const GraphDev& g, const HopBufs& hb,
+                                 const char* h, int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap) {
+    const int cpr = row_bytes / 16;
+    if (cpr <= 4) {
+        GSB_LAUNCH(name, (agg_kernel<FEAT, BF16, 4>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
+                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap);
+    } else if (cpr <= 8) {
+        GSB_LAUNCH(name, (agg_kernel<FEAT, BF16, 8>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
+                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap);
+    } else if (cpr <= 16) {
+        GSB_LAUNCH(name, (agg_kernel<FEAT, BF16, 16>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
+                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap);
+    } else {
+        GSB_LAUNCH(name, (agg_kernel<FEAT, BF16, 32>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
+                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap);
+    }
+    return GSB_OK;
+}
+
+static gsb_status launch_agg(const char* name, bool feat, int dtype, cudaStream_t s, const GraphDev& g,
+                             const HopBufs& hb, const void* h, int d, float* acat, int64_t lda, const int32_t* rowmap) {
+    const int grid = grid_for(hb.cap_dst * 32, 256, kNumSMs * 8);
+    const int rb = d * dtype_size(dtype);
+    const char* hc = static_cast<const char*>(h);
+    if (feat)
+        return dtype == GSB_BF16 ? launch_agg_lpe<true, true>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap)
+                                 : launch_agg_lpe<true, false>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap);
+    return dtype == GSB_BF16 ? launch_agg_lpe<false, true>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap)
+                             : launch_agg_lpe<false, false>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap);
 }
 
 // ------------------------------------------------------------------------------------
@@ -256,40 +301,38 @@ gsb_status gsb_layer_acat_floats(gsb_blocks_t b, int32_t layer, int32_t d_in, in
     return GSB_OK;
 }
 
-gsb_status gsb_rgcn_layer_fwd_rowmap(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src,
-                                     const int32_t* rowmap, int32_t d_in, const float* W, const float* bias,
-                                     int32_t d_out, int32_t relu, float* h_dst, float* acat, void* stream);
-
 gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src, int32_t d_in,
                               const float* W, const float* bias, int32_t d_out, int32_t relu, float* h_dst,
                               float* acat, void* stream) {
-    return gsb_rgcn_layer_fwd_rowmap(b, arena, layer, h_src, nullptr, d_in, W, bias, d_out, relu, h_dst, acat, stream);
+    return gsb_rgcn_layer_fwd_ex(b, arena, layer, h_src, GSB_F32, nullptr, d_in, W, bias, d_out, relu, h_dst, acat,
+                                 stream);
 }
 
-gsb_status gsb_rgcn_layer_fwd_rowmap(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_src,
-                                     const int32_t* rowmap, int32_t d_in, const float* W, const float* bias,
-                                     int32_t d_out, int32_t relu, float* h_dst, float* acat, void* stream) {
+gsb_status gsb_rgcn_layer_fwd_ex(gsb_blocks_t b, const void* arena, int32_t layer, const void* h_src, int32_t h_dtype,
+                                 const int32_t* rowmap, int32_t d_in, const float* W, const float* bias, int32_t d_out,
+                                 int32_t relu, float* h_dst, float* acat, void* stream) {
     Blocks* B = reinterpret_cast<Blocks*>(b);
     GSB_CHECK_ARG(B && arena && W && h_dst && acat, "null argument");
     GSB_CHECK_ARG(h_src || layer == 0, "h_src may be NULL only for layer 0 (features read by gid)");
     GSB_CHECK_ARG(layer >= 0 && layer < B->L, "layer %d out of range", layer);
     GSB_CHECK_ARG(d_in > 0 && d_in % BK == 0, "d_in %d must be a multiple of %d", d_in, BK);
     GSB_CHECK_ARG(d_out > 0 && d_out % 4 == 0, "d_out %d must be a multiple of 4", d_out);
+    GSB_CHECK_ARG(!rowmap || h_src, "rowmap needs h_src");
     cudaStream_t s = (cudaStream_t)stream;
     const int h = B->hop_of_layer(layer);
     HopBufs hb = B->hop(h, const_cast<void*>(arena));
     const GraphDev& g = B->g->dev;
     const int64_t lda = (int64_t)(g.S + 1) * d_in;
+    gsb_status st;
     if (h_src) {
-        GSB_LAUNCH(lname("rgcn_agg", layer), agg_kernel<false>, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
-                   hb.seg_ptr, hb.e_src, hb.e_src_gid, hb.dst_gid, h_src, d_in, acat, lda, rowmap);
+        GSB_CHECK_ARG(dtype_size(h_dtype) > 0, "h_dtype %d not GSB_F32 / GSB_BF16", h_dtype);
+        st = launch_agg(lname("rgcn_agg", layer), false, h_dtype, s, g, hb, h_src, d_in, acat, lda, rowmap);
     } else {
         GSB_CHECK_ARG(g.feat_dim == d_in, "layer 0 with features: d_in %d != feature dim %d", d_in, g.feat_dim);
         for (int t = 0; t < g.T; ++t) GSB_CHECK_ARG(g.feat[t], "features of ntype %d not registered", t);
-        GSB_LAUNCH(lname("rgcn_agg", layer), agg_kernel<true>, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
-                   hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid, hb.dst_gid, (const float*)nullptr, d_in, acat, lda,
-                   (const int32_t*)nullptr);
+        st = launch_agg(lname("rgcn_agg", layer), true, g.feat_dtype, s, g, hb, nullptr, d_in, acat, lda, nullptr);
     }
+    if (st != GSB_OK) return st;
     RowGroups rg = layer_groups(B, arena, layer);
 #ifdef GSB_SIMT_GEMM
     GSB_LAUNCH(lname("rgcn_gemm_fwd", layer), gemm_nn_kernel, gemm_grid(hb.cap_dst, (d_out + BN - 1) / BN, g.T), NT, 0, s, rg,

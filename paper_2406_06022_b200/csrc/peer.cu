@@ -62,22 +62,22 @@ gsb_status gsb_ipc_close(void* base_ptr) {
 }
 
 gsb_status gsb_graph_set_feature_peers(gsb_graph_t g, int32_t ntype, int32_t world, const int64_t* bounds,
-                                       const float* const* ptrs, int32_t dim) {
+                                       const void* const* ptrs, int32_t dim, int32_t dtype) {
     Graph* G = reinterpret_cast<Graph*>(g);
     GSB_CHECK_ARG(G && bounds && ptrs && ntype >= 0 && ntype < G->dev.T, "bad argument");
     GSB_CHECK_ARG(world >= 1 && world <= kMaxPeers, "world %d out of [1, %d]", world, kMaxPeers);
-    GSB_CHECK_ARG(dim > 0 && dim % 4 == 0, "dim must be a positive multiple of 4");
-    GSB_CHECK_ARG(G->dev.feat_dim == 0 || G->dev.feat_dim == dim, "all ntypes must share one feature dim");
     GSB_CHECK_ARG(bounds[0] == 0 && bounds[world] == G->counts[ntype], "bounds must span [0, count)");
-    G->dev.feat_dim = dim;
+    gsb_status st = set_feature_format(G, ntype, dim, dtype);
+    if (st != GSB_OK) return st;
     G->dev.nparts = world;
     for (int w = 0; w <= world; ++w) G->dev.plo[ntype][w] = bounds[w];
     for (int w = 0; w < world; ++w) {
         GSB_CHECK_ARG(ptrs[w] || bounds[w + 1] == bounds[w], "null shard pointer for rank %d", w);
-        G->dev.peer[ntype][w] = ptrs[w];
+        GSB_CHECK_ARG(((uintptr_t)ptrs[w] & 15) == 0, "shard of rank %d not 16-byte aligned", w);
+        G->dev.peer[ntype][w] = static_cast<const char*>(ptrs[w]);
     }
     // the local-table pointer is unused in partitioned mode but marks the ntype as registered
-    G->dev.feat[ntype] = ptrs[0] ? ptrs[0] : reinterpret_cast<const float*>(16);
+    G->dev.feat[ntype] = ptrs[0] ? static_cast<const char*>(ptrs[0]) : reinterpret_cast<const char*>(16);
     return GSB_OK;
 }
 

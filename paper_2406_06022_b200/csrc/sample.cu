@@ -19,8 +19,6 @@
 
 namespace gsb {
 
-gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_dev, int64_t n_host, int64_t n_max,
-                         float* out, cudaStream_t s);
 
 enum { ERR_NONE = 0, ERR_GROUPING = 1, ERR_RANGE = 2, ERR_CAPACITY = 3, ERR_DUPLICATE = 4 };
 
@@ -716,11 +714,11 @@ gsb_status gsb_blocks_dst_rows(gsb_blocks_t b, int32_t layer, int64_t* max_rows)
     return GSB_OK;
 }
 
-gsb_status gsb_gather_block_inputs(gsb_blocks_t b, const void* arena, float* out, void* stream) {
+gsb_status gsb_gather_block_inputs(gsb_blocks_t b, const void* arena, void* out, void* stream) {
     Blocks* B = reinterpret_cast<Blocks*>(b);
     GSB_CHECK_ARG(B && arena && out, "null argument");
     const Graph* G = B->g;
-    GSB_CHECK_ARG(G->dev.feat_dim > 0, "features not registered");
+    GSB_CHECK_ARG(G->dev.feat_dim > 0, "features not registered (or not one width for all ntypes)");
     HopBufs hb = B->hop(B->L, const_cast<void*>(arena));
     return launch_gather(G, hb.src_gid, &hb.meta->n_src, 0, hb.cap_src, out, (cudaStream_t)stream);
 }

@@ -37,6 +37,27 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn, bool b_mn) {
            ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
 }
 
+// kind::f16 with bf16 A and B, fp32 accumulate, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_bf16(int n, bool a_mn, bool b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+           ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+}
+
+// 16-bit operand panels, SWIZZLE_128B (bf16; input encoder):
+//   K-major  (128 rows x 64 K): row r at r*128 B, 16-B chunk c at chunk c ^ (r&7); SBO 1024;
+//            one MMA (K = 16 = 32 B) starts at base + ks*32.
+//   MN-major (128 MN x 64 K): atoms of 64 MN (128 B) x 8 K rows (1024 B), 16-B chunk c of K
+//            row kk at chunk c ^ kk; MN atoms 1024 B apart (LBO), 8-row K groups 2048 B apart
+//            (SBO); one MMA (K = 16 rows) starts at base + ks*4096.
+__device__ __forceinline__ uint32_t kmaj16_chunk(int r, int c) {
+    return (uint32_t)(r * 128 + (((c ^ (r & 7)) & 7) << 4));
+}
+__device__ __forceinline__ uint32_t mnmaj16_chunk(int mn, int k) {   // mn multiple of 8
+    const int kk = k & 7, c = (mn & 63) >> 3;
+    return (uint32_t)((k >> 3) * 2048 + (mn >> 6) * 1024 + kk * 128 + (((c ^ kk) & 7) << 4));
+}
+__device__ __forceinline__ uint64_t desc_mnmajor16(uint32_t addr) { return desc_encode(addr, 1024, 2048, 2); }
+
 // byte offset of element (r, k) inside a K-major panel (k in [0,32))
 __device__ __forceinline__ uint32_t kmajor_off(int r, int k) {
     return (uint32_t)(r * 128 + ((((k >> 2) ^ (r & 7)) & 7) << 4) + ((k & 3) << 2));
@@ -61,6 +82,17 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
     hi = rna_tf32_bits(__float_as_uint(x));
     lo = rna_tf32_bits(__float_as_uint(x - __uint_as_float(hi)));
 }
+
+// ---- cp.async (LDGSTS) with zero fill ------------------------------------------------
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp4(uint32_t dst, const void* src, int bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // ---- mbarrier ------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -108,6 +140,14 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(idesc), "r"(accum)
         : "memory");
 }

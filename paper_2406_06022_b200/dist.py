@@ -52,8 +52,11 @@ class FeatureExchange:
              self.bounds.ctypes.data_as(C.c_void_p), C.byref(h))
         self.h = h
         self.shards = [s.contiguous() for s in shards]
+        from .runtime import DTYPE_CODE
+        self.dtype = self.shards[0].dtype
+        self.esize = self.shards[0].element_size()
         for t, sh in enumerate(self.shards):
-            call("gsb_partition_set_shard", self.h, t, C.c_void_p(sh.data_ptr()), dim)
+            call("gsb_partition_set_shard", self.h, t, C.c_void_p(sh.data_ptr()), dim, DTYPE_CODE[sh.dtype])
         dev = self.shards[0].device
         self.counts_dev = torch.zeros(world, dtype=torch.int64, device=dev)
         self.ws = torch.zeros(world, dtype=torch.int64, device=dev)
@@ -85,14 +88,14 @@ class FeatureExchange:
         send_splits, recv_splits = both[:self.world], both[self.world:]
         recv_gid = torch.empty(sum(recv_splits), dtype=torch.int64, device=dev)
         dist.all_to_all_single(recv_gid, send_gid[:n], recv_splits, send_splits, group=self.group)   # C4
-        rows = torch.empty((max(sum(recv_splits), 1), self.dim), dtype=torch.float32, device=dev)
+        rows = torch.empty((max(sum(recv_splits), 1), self.dim), dtype=self.dtype, device=dev)
         call("gsb_shard_gather", self.h, P(recv_gid), recv_gid.numel(), P(rows), s)
-        back = torch.empty((max(n, 1), self.dim), dtype=torch.float32, device=dev)
+        back = torch.empty((max(n, 1), self.dim), dtype=self.dtype, device=dev)
         dist.all_to_all_single(back[:n], rows[:sum(recv_splits)], send_splits, recv_splits, group=self.group)  # C5
-        self.bytes_sent += (n - send_splits[self.rank]) * 8 + (sum(recv_splits) - recv_splits[self.rank]) * self.dim * 4
+        self.bytes_sent += (n - send_splits[self.rank]) * 8 + (sum(recv_splits) - recv_splits[self.rank]) * self.dim * self.esize
         if out is None:
             return back, perm
-        call("gsb_rows_permute", P(back), self.dim, P(perm), None, n, P(out), s)
+        call("gsb_rows_permute", P(back), self.dim * self.esize, P(perm), None, n, P(out), s)
         return out
 
 
@@ -107,6 +110,7 @@ class PeerFeatures:
         import numpy as np
         import torch.distributed as dist
         from ._lib import call
+        from .runtime import DTYPE_CODE
         self.bounds = balanced_bounds(counts, world)
         self.shards = [s.contiguous() for s in shards]
         mine = []
@@ -135,6 +139,8 @@ class PeerFeatures:
                     ptrs[w] = p.value
                     self.mapped.append(p.value - off)
             b = np.ascontiguousarray(self.bounds[t])
-            call("gsb_graph_set_feature_peers", store.h, t, world, b.ctypes.data_as(C.c_void_p), ptrs, dim)
+            call("gsb_graph_set_feature_peers", store.h, t, world, b.ctypes.data_as(C.c_void_p), ptrs, dim,
+                 DTYPE_CODE[self.shards[t].dtype])
         store.feat_dim = dim
+        store.feat_dtype = self.shards[0].dtype
         self.store = store

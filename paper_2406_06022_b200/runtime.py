@@ -15,6 +15,9 @@ import torch
 from . import _lib
 from ._lib import call, lib
 
+# feature element types of the C ABI (GSB_F32 / GSB_BF16)
+DTYPE_CODE = {torch.float32: 0, torch.bfloat16: 1}
+
 
 def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else C.c_void_p(t.data_ptr())
@@ -51,6 +54,7 @@ class GraphStore:
         self.n_edges = [0] * self.R
         self.feats: List[Optional[torch.Tensor]] = [None] * self.T
         self.feat_dim = 0
+        self.feat_dtype = torch.float32
 
     def __del__(self):
         try:
@@ -80,15 +84,18 @@ class GraphStore:
         self.n_edges[r] = int(kept.value)
 
     def set_features(self, t: int, feat: torch.Tensor):
-        f = feat.to(self.device, dtype=torch.float32).contiguous()
-        call("gsb_graph_set_features", self.h, t, _ptr(f), f.shape[1])
+        """Register ntype t's feature table (fp32 or bf16 rows; one format for all ntypes)."""
+        dt = feat.dtype if feat.dtype in DTYPE_CODE else torch.float32
+        f = feat.to(self.device, dtype=dt).contiguous()
+        call("gsb_graph_set_features", self.h, t, _ptr(f), f.shape[1], DTYPE_CODE[dt])
         self.feats[t] = f
         self.feat_dim = f.shape[1]
+        self.feat_dtype = dt
 
     def gather(self, gids: torch.Tensor) -> torch.Tensor:
-        """gsb_gather: out[i] = F_{t(i)}[gid_i - off_t]."""
+        """gsb_gather: out[i] = F_{t(i)}[gid_i - off_t] (exact copy, feature dtype)."""
         g = gids.to(self.device, dtype=torch.int64).contiguous()
-        out = torch.empty((g.numel(), self.feat_dim), dtype=torch.float32, device=self.device)
+        out = torch.empty((g.numel(), self.feat_dim), dtype=self.feat_dtype, device=self.device)
         call("gsb_gather", self.h, _ptr(g), g.numel(), _ptr(out), _stream())
         return out
 
@@ -261,7 +268,7 @@ class _TrainerBase:
         self.t = 0
         d0 = store.feat_dim
         self.d_in = [d0] + [hidden] * (self.L - 1)
-        self.x0 = torch.empty((self.sampler.input_rows(), d0), dtype=torch.float32, device=dev)
+        self.x0 = torch.empty((self.sampler.input_rows(), d0), dtype=store.feat_dtype, device=dev)
         self.hout = [torch.empty((self.sampler.dst_rows(l), hidden), dtype=torch.float32, device=dev)
                      for l in range(self.L)]
         self.acat = [torch.empty(self.sampler.acat_floats(l, self.d_in[l]), dtype=torch.float32, device=dev)
@@ -316,7 +323,8 @@ class _TrainerBase:
         else:
             h = self.x0
         for l in range(self.L):
-            call("gsb_rgcn_layer_fwd_rowmap", sm.h, _ptr(sm.arena), l, _ptr(h), _ptr(rowmap if l == 0 else None),
+            hdt = DTYPE_CODE[h.dtype] if h is not None else 0
+            call("gsb_rgcn_layer_fwd_ex", sm.h, _ptr(sm.arena), l, _ptr(h), hdt, _ptr(rowmap if l == 0 else None),
                  self.d_in[l], self._pp(f"W{l}"), self._pp(f"b{l}"), self.hidden, int(l < self.L - 1),
                  _ptr(self.hout[l]), _ptr(self.acat[l]), s)
             h = self.hout[l]

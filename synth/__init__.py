@@ -96,6 +96,12 @@ class Config:
     gen_seed: int = 2406060220
     rng_seed: int = 1           # the sampler's Philox key (method RNG input)
     lr: float = 1e-3
+    feat_dtype: str = "f32"     # "f32" | "bf16": storage type of the node features (c.8)
+    # input encoder (§8(a) a6): per-ntype raw feature width (None = feat_dim for
+    # all) and which ntypes get a trainable projection Win{t} (dims[t] -> feat_dim); the
+    # others are frozen tables of width feat_dim (featureless ntypes)
+    feat_dims: Optional[List[int]] = None
+    project: Optional[List[bool]] = None
 
     @property
     def num_ntypes(self) -> int:
@@ -116,6 +122,14 @@ class Config:
     @property
     def num_edges(self) -> int:
         return int(sum(e.num_edges for e in self.etypes))
+
+    def dim_of(self, t: int) -> int:
+        """Raw feature width of ntype t."""
+        return self.feat_dims[t] if self.feat_dims else self.feat_dim
+
+    @property
+    def has_encoder(self) -> bool:
+        return bool(self.project) and any(self.project)
 
     @property
     def feat_seed(self) -> int:
@@ -197,8 +211,45 @@ def synth_1b(scale: float = 1.0) -> Config:
         gen_seed=2406060220 + 5)
 
 
+def mag240m(scale: float = 1.0) -> Config:
+    """configs[3]: MAG240M-shaped (OGB-LSC counts [EXT], SURVEY §8(d) cfg 4): paper 768-d bf16
+    features with a trainable input projection 768 -> 128 (a6); author / institution are
+    featureless -> frozen 128-d bf16 tables; 3 forward + 2 reverse etypes
+    (2.16B stored at full scale), [15,10], b1024/GPU, NC on paper, C = 153."""
+    c = [int(121_751_666 * scale), int(122_383_112 * scale), int(25_721 * scale)]
+    et = [EType("writes", 1, 0, int(386_022_720 * scale)), EType("cites", 0, 0, int(1_297_748_926 * scale)),
+          EType("affiliated_with", 1, 2, int(44_592_586 * scale))]
+    et += [EType("rev_writes", 0, 1, int(386_022_720 * scale), reverse_of=0),
+           EType("rev_affiliated_with", 2, 1, int(44_592_586 * scale), reverse_of=2)]
+    return Config(
+        name="mag240m" if scale == 1.0 else f"mag240m_x{scale:g}", ntypes=["paper", "author", "institution"],
+        counts=c, etypes=et, feat_dim=128, fanouts=[15, 10], batch=1024, hidden=128, num_classes=153,
+        target_ntype=0, gen_seed=2406060220 + 4, feat_dtype="bf16", feat_dims=[768, 128, 128],
+        project=[True, False, False])
+
+
+def tiny_enc() -> Config:
+    """Small input-encoder case for parity: tiny graph, ntype A with 96-d raw features and a
+    projection, B / C frozen 64-d tables (bf16 storage)."""
+    cfg = tiny()
+    cfg.name = "tiny_enc"
+    cfg.feat_dtype = "bf16"
+    cfg.feat_dims = [192, 64, 64]
+    cfg.project = [True, False, False]
+    cfg.gen_seed = 2406060220 + 12
+    return cfg
+
+
+def with_dtype(cfg: Config, feat_dtype: str) -> Config:
+    """The same workload with features stored as `feat_dtype` ("f32" | "bf16")."""
+    if feat_dtype == cfg.feat_dtype:
+        return cfg
+    return dataclasses.replace(cfg, feat_dtype=feat_dtype, name=f"{cfg.name}_{feat_dtype}")
+
+
 CONFIGS = {"tiny": tiny, "mag": mag, "amazon_lp": amazon_lp, "tiny_lp": tiny_lp,
-           "synth_1b": synth_1b}
+           "synth_1b": synth_1b, "mag240m": mag240m, "mag240m_1_16": lambda: mag240m(1.0 / 16),
+           "tiny_enc": tiny_enc}
 
 
 def get(name: str) -> Config:
@@ -272,34 +323,55 @@ def etype_coo(cfg: Config, r: int, backend: str = "np", device=None, lo: int = 0
 # --------------------------------------------------------------------------------------
 # Features, labels, splits
 # --------------------------------------------------------------------------------------
+def _round_bf16_bits(bits):
+    """fp32 bit patterns -> nearest-even bf16 bit patterns (kept in the high 16 bits).
+    Integer-only so numpy and torch give identical values (finite inputs)."""
+    return (bits + 0x7FFF + ((bits >> 16) & 1)) & 0xFFFF0000
+
+
 def feature_rows(cfg: Config, t: int, local_ids, backend: str = "np", device=None):
-    """F_t[i, k] = (h >> 8) * 2^-23 - 1, exactly representable in fp32, in [-1, 1)."""
-    d = cfg.feat_dim
+    """F_t[i, k] = (h >> 8) * 2^-23 - 1, exactly representable in fp32, in [-1, 1).  With
+    cfg.feat_dtype == "bf16" each value is rounded to the nearest bf16 (ties to even), so the
+    returned fp32 values are exactly representable in bf16."""
+    d = cfg.dim_of(t)
+    bf = cfg.feat_dtype == "bf16"
     if backend == "np":
         ids = np.asarray(local_ids, dtype=np.uint64)
         idx = ids[:, None] * np.uint64(d) + np.arange(d, dtype=np.uint64)[None, :]
         h = hash32(cfg.feat_seed, 1000 + t, idx)
-        return ((h >> 8).astype(np.float32) * np.float32(2.0 ** -23) - np.float32(1.0)).astype(np.float32)
+        f = ((h >> 8).astype(np.float32) * np.float32(2.0 ** -23) - np.float32(1.0)).astype(np.float32)
+        if bf:
+            b = f.view(np.uint32).astype(np.uint64)
+            f = (_round_bf16_bits(b) & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(np.float32)
+        return f
     import torch
     ids = torch.as_tensor(local_ids, dtype=torch.int64, device=device)
     idx = ids[:, None] * d + torch.arange(d, dtype=torch.int64, device=device)[None, :]
     h = hash32(cfg.feat_seed, 1000 + t, idx)
-    return (h >> 8).to(torch.float32) * (2.0 ** -23) - 1.0
+    f = (h >> 8).to(torch.float32) * (2.0 ** -23) - 1.0
+    if bf:
+        b = f.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        f = (_round_bf16_bits(b) & 0xFFFFFFFF).to(torch.int64)
+        f = torch.where(f >= 2 ** 31, f - 2 ** 32, f).to(torch.int32).view(torch.float32)
+    return f
 
 
 def feature_table(cfg: Config, t: int, backend: str = "np", device=None, chunk: int = 1 << 20):
+    """Whole table of ntype t: numpy float32 (values exact in the config's dtype), or a torch
+    tensor of the config's storage dtype (float32 / bfloat16; the conversion is exact)."""
     n = cfg.counts[t]
     if backend == "np":
-        out = np.empty((n, cfg.feat_dim), dtype=np.float32)
+        out = np.empty((n, cfg.dim_of(t)), dtype=np.float32)
         for lo in range(0, n, chunk):
             hi = min(n, lo + chunk)
             out[lo:hi] = feature_rows(cfg, t, np.arange(lo, hi), "np")
         return out
     import torch
-    out = torch.empty((n, cfg.feat_dim), dtype=torch.float32, device=device)
+    dt = torch.bfloat16 if cfg.feat_dtype == "bf16" else torch.float32
+    out = torch.empty((n, cfg.dim_of(t)), dtype=dt, device=device)
     for lo in range(0, n, chunk):
         hi = min(n, lo + chunk)
-        out[lo:hi] = feature_rows(cfg, t, torch.arange(lo, hi, device=device), "torch", device)
+        out[lo:hi] = feature_rows(cfg, t, torch.arange(lo, hi, device=device), "torch", device).to(dt)
     return out
 
 
@@ -408,6 +480,9 @@ def init_params(cfg: Config) -> dict:
     L = len(cfg.fanouts)
     R = cfg.num_etypes
     p = {}
+    for t in range(cfg.num_ntypes):   # input encoder projections (a6)
+        if cfg.project and cfg.project[t]:
+            p[f"Win{t}"] = glorot((cfg.dim_of(t), cfg.feat_dim), cfg.dim_of(t), cfg.feat_dim, cfg.gen_seed * 31 + 50 + t)
     d_in = cfg.feat_dim
     for l in range(L):
         d_out = cfg.hidden
@@ -425,7 +500,7 @@ def init_params(cfg: Config) -> dict:
 
 def param_order(cfg: Config) -> List[str]:
     L = len(cfg.fanouts)
-    names = []
+    names = [f"Win{t}" for t in range(cfg.num_ntypes) if cfg.project and cfg.project[t]]
     for l in range(L):
         names += [f"W{l}", f"b{l}"]
     names += ["Wc", "bc"] if cfg.task == "nc" else ["rel"]

@@ -20,7 +20,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, feat_dtype):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -31,26 +31,28 @@ def _worker(rank, world, port, out):
     build.build()
     from paper_2406_06022_b200.dist import FeatureExchange, allreduce_mean, balanced_bounds, rank_step
     from paper_2406_06022_b200.runtime import GraphStore, RGCNTrainer
-    cfg = synth.scaled(synth.mag(), 0.01, "mag_small")
+    cfg = synth.with_dtype(synth.scaled(synth.mag(), 0.01, "mag_small"), feat_dtype)
+    tdt = torch.bfloat16 if feat_dtype == "bf16" else torch.float32
     dev = f"cuda:{rank}"
     bounds = balanced_bounds(cfg.counts, world)
     shards = [synth.feature_rows(cfg, t, torch.arange(int(bounds[t][rank]), int(bounds[t][rank + 1]), device=dev),
-                                 "torch", dev) for t in range(cfg.num_ntypes)]
+                                 "torch", dev).to(tdt) for t in range(cfg.num_ntypes)]
     ex = FeatureExchange(cfg.counts, world, rank, shards, cfg.feat_dim)
     rng = np.random.default_rng(rank)
     gids = np.sort(rng.integers(0, cfg.num_nodes, 3000)).astype(np.int64)
-    outt = torch.empty((len(gids), cfg.feat_dim), device=dev)
+    outt = torch.empty((len(gids), cfg.feat_dim), dtype=tdt, device=dev)
     ex.gather(torch.from_numpy(gids).to(dev), len(gids), outt)
     exp = np.concatenate([synth.feature_rows(cfg, int(np.searchsorted(cfg.node_off, g, side="right") - 1),
                                              [g - cfg.node_off[np.searchsorted(cfg.node_off, g, side="right") - 1]])
                           for g in gids])
-    out["rows_ok%d" % rank] = bool(np.array_equal(outt.cpu().numpy(), exp))
+    out["rows_ok%d" % rank] = bool(np.array_equal(outt.float().cpu().numpy(), exp))
     # partitioned NC step: CSC replicated, features partitioned
     st = GraphStore(cfg.counts, cfg.etype_src(), cfg.etype_dst(), dev)
     for r in range(cfg.num_etypes):
         s_, d_ = synth.etype_coo(cfg, r, backend="torch", device=dev)
         st.load_etype(r, s_, d_)
     st.feat_dim = cfg.feat_dim
+    st.feat_dtype = tdt
     tr = RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
                      synth.param_order(cfg), torch.from_numpy(synth.labels(cfg)),
                      int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
@@ -68,7 +70,7 @@ def _worker(rank, world, port, out):
         s_, d_ = synth.etype_coo(cfg, r, backend="torch", device=dev)
         st2.load_etype(r, s_, d_)
     pf = PeerFeatures(st2, cfg.counts, world, rank, shards, cfg.feat_dim)
-    g2 = st2.gather(torch.from_numpy(gids).to(dev)).cpu().numpy()
+    g2 = st2.gather(torch.from_numpy(gids).to(dev)).float().cpu().numpy()
     out["peer_rows_ok%d" % rank] = bool(np.array_equal(g2, exp))
     tr2 = RGCNTrainer(st2, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
                       synth.param_order(cfg), torch.from_numpy(synth.labels(cfg)),
@@ -85,20 +87,21 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_two_gpu_partitioned_features():
+@pytest.mark.parametrize("feat_dtype", ["f32", "bf16"])
+def test_two_gpu_partitioned_features(feat_dtype):
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
     import torch.multiprocessing as mp
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), out, feat_dtype), nprocs=2, join=True)
     assert out["rows_ok0"] and out["rows_ok1"]
     import oracle
     import synth
     from paper_2406_06022_b200.dist import rank_step
     from tests._pair import close
-    cfg = synth.scaled(synth.mag(), 0.01, "mag_small")
+    cfg = synth.with_dtype(synth.scaled(synth.mag(), 0.01, "mag_small"), feat_dtype)
     og = oracle.Graph(cfg)
     params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
     flats, losses, slW, slb = [], [], [], []

@@ -21,8 +21,10 @@ def torch_cuda():
 
 
 CASES = {
-    "tiny": lambda: synth.tiny(),
-    "mag_small": lambda: synth.scaled(synth.mag(), 0.01, "mag_small"),
+    "tiny": lambda: synth.tiny(),                                          # 64-d fp32 rows
+    "mag_small": lambda: synth.scaled(synth.mag(), 0.01, "mag_small"),     # 128-d fp32
+    "tiny_bf16": lambda: synth.with_dtype(synth.tiny(), "bf16"),           # 64-d bf16
+    "mag_small_bf16": lambda: synth.with_dtype(synth.scaled(synth.mag(), 0.01, "mag_small"), "bf16"),
 }
 
 
@@ -55,8 +57,9 @@ def test_gather_bitexact(pair, torch_cuda):
     cfg, st, og = pair
     rng = np.random.default_rng(0)
     gids = np.concatenate([rng.integers(0, cfg.num_nodes, 5000), [0, cfg.num_nodes - 1]]).astype(np.int64)
-    out = st.gather(torch_cuda.from_numpy(gids).cuda()).cpu().numpy()
-    assert np.array_equal(out, oracle.gather(og, gids))
+    out = st.gather(torch_cuda.from_numpy(gids).cuda())
+    assert out.dtype == (torch_cuda.bfloat16 if cfg.feat_dtype == "bf16" else torch_cuda.float32)
+    assert np.array_equal(out.float().cpu().numpy(), oracle.gather(og, gids))
 
 
 # ------------------------------------------------------------------ sampling
@@ -206,7 +209,7 @@ def test_nc_step_parity(pair, torch_cuda, fuse_gather):
         res = oracle.nc_step(og, params, seeds, labels, step, cfg.rng_seed)
         n0 = len(res.blocks[0].src_gid)
         if not fuse_gather:
-            assert np.array_equal(tr.x0[:n0].cpu().numpy(), res.x0)
+            assert np.array_equal(tr.x0[:n0].float().cpu().numpy(), res.x0)
         for l in range(len(cfg.fanouts)):
             nd = len(res.blocks[l].dst_gid)
             close(tr.hout[l][:nd].cpu().numpy(), res.hs[l], what=f"step {step} h{l}")

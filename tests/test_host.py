@@ -29,6 +29,26 @@ def test_generator_numpy_torch_bit_identical():
         assert np.array_equal(synth.labels(cfg), synth.labels(cfg, backend="torch").numpy())
 
 
+def test_bf16_features_are_rne_rounded_fp32_features():
+    """bf16 feature storage: every value is the fp32 feature rounded to the
+    nearest bf16 (ties to even) -- checked against torch's own conversion -- numpy and torch
+    agree bit for bit, and the torch table converts to bfloat16 exactly."""
+    cfg = synth.with_dtype(synth.tiny(), "bf16")
+    ids = np.arange(0, 4000, 3)
+    f32 = synth.feature_rows(synth.tiny(), 2, ids)
+    bf = synth.feature_rows(cfg, 2, ids)
+    assert np.array_equal(bf, torch.from_numpy(f32).to(torch.bfloat16).float().numpy())
+    assert np.array_equal(bf, synth.feature_rows(cfg, 2, torch.from_numpy(ids), backend="torch").numpy())
+    assert np.abs(bf - f32).max() <= 2.0 ** -8          # half an ulp of bf16 on [-1, 1)
+    tab = synth.feature_table(cfg, 2, backend="torch")
+    assert tab.dtype == torch.bfloat16
+    assert np.array_equal(tab.float().numpy(), synth.feature_table(cfg, 2))
+    # ties round to even: 1 + 2^-8 is halfway between bf16 neighbours 1 and 1 + 2^-7
+    x = np.array([1.0 + 2.0 ** -8, 1.0 + 3 * 2.0 ** -8], np.float32).view(np.uint32).astype(np.uint64)
+    r = (synth._round_bf16_bits(x) & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(np.float32)
+    assert r[0] == 1.0 and r[1] == 1.0 + 2.0 ** -6
+
+
 def test_reverse_etypes_mirror_forward():
     cfg = synth.mag()
     s, d = synth.etype_coo(cfg, 0, hi=1000)

