@@ -36,7 +36,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="gsb", choices=["gsb", "reference"])
-    ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b", "amazon_lp", "tiny_lp"])
+    ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b", "amazon_lp", "tiny_lp", "mag240m",
+                                                        "mag240m_1_16"])
     ap.add_argument("--feat-dtype", default=None, choices=["f32", "bf16"],
                     help="feature storage type (default: the config's; compute stays fp32)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -172,6 +173,12 @@ def kernel_work(name: str, sz: dict, cfg: synth.Config):
         return "flops", 2 * sz["acat_cols"][lay] * hd
     if name == "rgcn_gemm_dA" and lay is not None:
         return "flops", 2 * sz["acat_cols"][lay] * hd
+    if name in ("enc_gemm_fwd", "enc_gemm_dW") and cfg.has_encoder:
+        # a6: HBM bytes of the gathered bf16 rows of projected ntypes (+ the fp32 H0 rows written
+        # by the forward / the split dH0 rows read by the backward)
+        rows = sum(sz["src_type_cnt0"][t] for t in range(cfg.num_ntypes) if cfg.project[t])
+        dims = max(cfg.dim_of(t) for t in range(cfg.num_ntypes) if cfg.project[t])
+        return "bytes", rows * dims * 2 + rows * cfg.feat_dim * 4
     if name in ("nc_logits", "nc_gemm_dWc", "nc_gemm_dh"):
         return "flops", 2 * cfg.batch * hd * C
     return None, None
@@ -203,8 +210,8 @@ def build_gsb(cfg, device, partition=None, mode="peer"):
         world, rank = partition
         b = balanced_bounds(cfg.counts, world)
         tdt = torch.bfloat16 if cfg.feat_dtype == "bf16" else torch.float32
-        shards = [synth.feature_rows(cfg, t, torch.arange(int(b[t][rank]), int(b[t][rank + 1]), device=device),
-                                     "torch", device).to(tdt) for t in range(cfg.num_ntypes)]
+        shards = [synth.feature_table(cfg, t, "torch", device, lo=int(b[t][rank]), hi=int(b[t][rank + 1]))
+                  for t in range(cfg.num_ntypes)]
         if mode == "peer":
             st._peer = PeerFeatures(st, cfg.counts, world, rank, shards, cfg.feat_dim)
         else:
@@ -238,7 +245,7 @@ def launches_per_step_graph(tr, cfg):
 def block_sizes(tr, cfg):
     L = len(cfg.fanouts)
     sm = tr.sampler
-    out = {"n_dst": [], "n_src": [], "n_edges": [], "acat_cols": []}
+    out = {"n_dst": [], "n_src": [], "n_edges": [], "acat_cols": [], "src_type_cnt0": None}
     slots = tr.store.slot_etypes()
     for l in range(L):
         b = sm.block(l)
@@ -247,6 +254,8 @@ def block_sizes(tr, cfg):
         out["n_src"].append(int(b.src_gid.numel()))
         out["n_edges"].append(int(b.e_src.numel()))
         out["acat_cols"].append(int(sum(int(b.dst_type_cnt[t]) * (len(slots[t]) + 1) * d for t in range(len(slots)))))
+        if l == 0:
+            out["src_type_cnt0"] = [int(x) for x in b.src_type_cnt]
     return out
 
 
@@ -517,8 +526,9 @@ def oracle_rate(cfg, seconds: float, sub_batch: int, max_steps: int = 10 ** 9, m
     import oracle
     t0 = time.time()
     og = oracle.Graph(cfg)
-    for t in range(cfg.num_ntypes):
-        og.feats[t] = synth.feature_table(cfg, t)
+    if not cfg.has_encoder:   # encoder configs read rows from the generator's closed form
+        for t in range(cfg.num_ntypes):
+            og.feats[t] = synth.feature_table(cfg, t)
     setup = time.time() - t0
     params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
     opt = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}
@@ -546,8 +556,9 @@ def run_reference(args, cfg):
     import oracle
     t0 = time.time()
     og = oracle.Graph(cfg)
-    for t in range(cfg.num_ntypes):
-        og.feats[t] = synth.feature_table(cfg, t)
+    if not cfg.has_encoder:   # encoder configs read rows from the generator's closed form
+        for t in range(cfg.num_ntypes):
+            og.feats[t] = synth.feature_table(cfg, t)
     setup = time.time() - t0
     params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
     opt = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}

@@ -232,11 +232,13 @@ def gather(g: Graph, gids: np.ndarray) -> np.ndarray:
 
 
 def input_rows(g: Graph, t: int, local_ids: np.ndarray) -> np.ndarray:
-    """Raw feature rows F_t[local_ids] (per-ntype width), widened to float64 (exact)."""
+    """Raw feature rows F_t[local_ids] (per-ntype width), widened to float64 (exact): from the
+    materialised table if present, else from the generator's closed form row by row."""
     import synth
-    if g.feats[t] is None:
-        g.feats[t] = synth.feature_table(g.cfg, t)
-    return g.feats[t][np.asarray(local_ids, np.int64)].astype(np.float64)
+    ids = np.asarray(local_ids, np.int64)
+    if g.feats[t] is not None:
+        return g.feats[t][ids].astype(np.float64)
+    return synth.feature_rows(g.cfg, t, ids).astype(np.float64)
 
 
 def encoder_fwd(g: Graph, params: Dict[str, np.ndarray], gids: np.ndarray) -> np.ndarray:

@@ -22,7 +22,6 @@ using umma::cp4;
 using umma::cp_commit;
 using umma::cp_wait;
 
-constexpr int EN_THREADS = 256;
 constexpr int EN_PANEL = 16384;            // 128 x 64 bf16 (fwd) / 128 MN x 64 K bf16 (dW)
 constexpr int EN_STAGE = 3 * EN_PANEL;     // A, B_hi, B_lo
 constexpr int EN_STAGES = 4;
@@ -115,184 +114,201 @@ __device__ __forceinline__ void dw_decode(const EncDev& e, const HopMeta* m, int
     }
 }
 
-// ---- the pipelined kernel (BWD = false: forward, true: weight gradient) -----------------
+// ---- the warp-specialized pipelined kernel (BWD = false: forward, true: weight gradient) --
+// warps 0-3: producers (cp.async gathers of operand panels into a ring of EN_STAGES stages;
+//            completion is signalled per stage with cp.async.mbarrier.arrive.noinc)
+// warps 4-7: epilogue (TMEM -> registers -> H0 rows / red.add into dW), warp w drains TMEM
+//            lanes 32*(w%4)..; two TMEM accumulators so a tile's epilogue overlaps the next
+//            tile's MMAs
+// warp 8:    one thread issues the tcgen05 MMAs and commits stage / accumulator barriers
+constexpr int EN_WS_THREADS = 288;
+
+__device__ __forceinline__ void cp_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(umma::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(umma::smem_u32(bar))
+                 : "memory");
+}
+
 template <bool BWD>
-__global__ void __launch_bounds__(EN_THREADS, 1) enc_umma_kernel(GraphDev g, EncDev e, const HopMeta* __restrict__ m,
-                                                                 const int64_t* __restrict__ src_gid, float* __restrict__ H0,
-                                                                 EncOut out) {
+__global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, EncDev e, const HopMeta* __restrict__ m,
+                                                                    const int64_t* __restrict__ src_gid,
+                                                                    float* __restrict__ H0, EncOut out) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t bars[EN_STAGES];
+    __shared__ __align__(8) uint64_t full[EN_STAGES], empty[EN_STAGES], tfull[2], tempty[2];
     __shared__ uint32_t tmem_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (warp == 0) umma::tmem_alloc<128>(&tmem_sh);
+    if (warp == 0) umma::tmem_alloc<256>(&tmem_sh);
     if (tid == 0) {
-        for (int s = 0; s < EN_STAGES; ++s) umma::mbar_init(&bars[s], 1);
+        for (int s = 0; s < EN_STAGES; ++s) {
+            umma::mbar_init(&full[s], 128);
+            umma::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            umma::mbar_init(&tfull[a], 1);
+            umma::mbar_init(&tempty[a], 128);
+        }
         umma::fence_barrier_init();
     }
     umma::tc_fence_before();
     __syncthreads();
     umma::tc_fence_after();
     const uint32_t tmem = tmem_sh;
-    constexpr uint32_t IDESC = umma::idesc_bf16(128, BWD, BWD);
-
     const int nct = e.d_out / 128;
     const int grid = gridDim.x;
     const int64_t total = BWD ? dw_total(e, m, nct, grid) : fwd_total(e, m, nct);
-    EnCursor ld, cp;
-    ld.tile = blockIdx.x;
     auto decode = [&](EnCursor& c) {
         if (BWD) dw_decode(e, m, nct, grid, c);
         else fwd_decode(e, m, nct, c);
     };
-    // forward: the 4 A rows this thread copies are fixed per tile -> resolve them once
-    const char* arow[4] = {nullptr, nullptr, nullptr, nullptr};
-    auto rows_of = [&](const EnCursor& c) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t row = c.row0 + (tid >> 3) + 32 * i;
-            arow[i] = row < c.rlim ? reinterpret_cast<const char*>(feat_row(g, __ldg(src_gid + row))) : nullptr;
-        }
-    };
-    if (ld.tile < total) {
-        decode(ld);
-        if (!BWD) rows_of(ld);
-    }
-    cp = ld;
-    auto advance_ld = [&]() {
-        if (ld.tile >= total) return;
-        if (++ld.p >= ld.KP) {
-            ld.tile += grid;
-            if (ld.tile < total) {
-                decode(ld);
-                if (!BWD) rows_of(ld);
-            }
-        }
-    };
-    auto issue = [&](uint8_t* stage) {
-        const uint32_t sA = umma::smem_u32(stage), sBh = sA + EN_PANEL, sBl = sA + 2 * EN_PANEL;
-        if (!BWD) {
-            const int ch = tid & 7;
-            const __nv_bfloat16* whi = e.wt_hi[ld.t];
-            const __nv_bfloat16* wlo = e.wt_lo[ld.t];
-            const int dim = e.dim[ld.t];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int r = (tid >> 3) + 32 * i;
-                const char* src = arow[i] ? arow[i] + ld.p * 128 + ch * 16 : reinterpret_cast<const char*>(whi);
-                cp16(sA + umma::kmaj16_chunk(r, ch), src, arow[i] ? 16 : 0);
-                const size_t off = (size_t)(ld.n0 + r) * dim + ld.p * 64 + ch * 8;
-                cp16(sBh + umma::kmaj16_chunk(r, ch), whi + off, 16);
-                cp16(sBl + umma::kmaj16_chunk(r, ch), wlo + off, 16);
-            }
-        } else {
-            const int c = tid & 15;
-            const int64_t rb = ld.row0 + (int64_t)ld.p * 64;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int k = (tid >> 4) + 16 * i;
-                const int64_t row = rb + k;
-                const bool ok = row < ld.rlim;
-                const uint32_t o = umma::mnmaj16_chunk(c * 8, k);
-                const char* src = ok ? reinterpret_cast<const char*>(feat_row(g, __ldg(src_gid + row))) +
-                                           (size_t)(ld.m0 + c * 8) * 2
-                                     : reinterpret_cast<const char*>(e.d_hi);
-                cp16(sA + o, src, ok ? 16 : 0);
-                const size_t off = (size_t)(ok ? row : 0) * e.d_out + ld.n0 + c * 8;
-                cp16(sBh + o, e.d_hi + off, ok ? 16 : 0);
-                cp16(sBl + o, e.d_lo + off, ok ? 16 : 0);
-            }
-        }
-    };
 
-    uint32_t phase[EN_STAGES] = {0, 0, 0, 0};
-    bool pend[EN_STAGES] = {false, false, false, false};
-    auto wait_stage = [&](int st) {
-        if (pend[st]) {
-            umma::mbar_wait(&bars[st], phase[st]);
-            phase[st] ^= 1;
-            pend[st] = false;
-        }
-    };
-    int64_t it_ld = 0, it_cp = 0;
-    for (int k = 0; k < EN_STAGES - 1; ++k) {
-        if (ld.tile < total) {
-            issue(smem + (it_ld % EN_STAGES) * EN_STAGE);
-            advance_ld();
-        }
-        cp_commit();
-        ++it_ld;
-    }
-    while (cp.tile < total) {
-        cp_wait<EN_STAGES - 2>();
-        const int st = (int)(it_cp % EN_STAGES);
-        uint8_t* stage = smem + st * EN_STAGE;
-        umma::fence_proxy_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-            umma::tc_fence_after();
-            const uint32_t a = umma::smem_u32(stage), bh = a + EN_PANEL, bl = a + 2 * EN_PANEL;
+    if (warp < 4) {
+        // ------------------------------------------------------------------ producers
+        const int p = tid;                       // 0..127
+        int64_t it = 0;
+        for (int64_t tile = blockIdx.x; tile < total; tile += grid) {
+            EnCursor c;
+            c.tile = tile;
+            decode(c);
+            if (!BWD) {
+                // rows rg + 16 i (i < 8), 16-B chunk ch of each 128-B K slice: a warp covers 4 whole rows
+                const int ch = p & 7, rg = p >> 3;
+                const char* arow[8];
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-                const uint32_t o = BWD ? ks * 4096u : ks * 32u;
-                const uint64_t da = BWD ? umma::desc_mnmajor16(a + o) : umma::desc_kmajor(a + o);
-                const uint64_t dbh = BWD ? umma::desc_mnmajor16(bh + o) : umma::desc_kmajor(bh + o);
-                const uint64_t dbl = BWD ? umma::desc_mnmajor16(bl + o) : umma::desc_kmajor(bl + o);
-                umma::mma_f16(tmem, da, dbh, IDESC, (cp.p > 0 || ks > 0) ? 1u : 0u);
-                umma::mma_f16(tmem, da, dbl, IDESC, 1u);
-            }
-            umma::mma_commit(&bars[st]);
-        }
-        pend[st] = true;
-        {   // refill the stage of panel it_cp-1 (its MMAs done) with panel it_cp+STAGES-1
-            const int fst = (int)(it_ld % EN_STAGES);
-            wait_stage(fst);
-            if (ld.tile < total) {
-                issue(smem + fst * EN_STAGE);
-                advance_ld();
-            }
-            cp_commit();
-            ++it_ld;
-        }
-        ++it_cp;
-        if (cp.p + 1 < cp.KP) {
-            ++cp.p;
-            continue;
-        }
-        for (int k = 1; k <= EN_STAGES; ++k) wait_stage((int)((it_cp - 1 + k) % EN_STAGES));
-        umma::tc_fence_after();
-        {
-            const int q = warp & 3, half = warp >> 2;
-            const int r = q * 32 + lane;
+                for (int i = 0; i < 8; ++i) {
+                    const int64_t row = c.row0 + rg + 16 * i;
+                    arow[i] = row < c.rlim ? reinterpret_cast<const char*>(feat_row(g, __ldg(src_gid + row))) : nullptr;
+                }
+                const __nv_bfloat16* whi = e.wt_hi[c.t];
+                const __nv_bfloat16* wlo = e.wt_lo[c.t];
+                const int dim = e.dim[c.t];
+                for (int pn = 0; pn < c.KP; ++pn, ++it) {
+                    const int st = (int)(it % EN_STAGES);
+                    if (it >= EN_STAGES) umma::mbar_wait(&empty[st], (uint32_t)((it / EN_STAGES) - 1) & 1u);
+                    const uint32_t sA = umma::smem_u32(smem + st * EN_STAGE), sBh = sA + EN_PANEL, sBl = sA + 2 * EN_PANEL;
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-                const int col = half * 64 + cc * 32;
-                float v[32];
-                umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)col, v);
-                if (!BWD) {
-                    const int64_t row = cp.row0 + r;
-                    if (row < cp.rlim) {
-                        float4* o4 = reinterpret_cast<float4*>(H0 + row * e.d_out + cp.n0 + col);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    for (int i = 0; i < 8; ++i) {
+                        const int r = rg + 16 * i;
+                        const uint32_t o = umma::kmaj16_chunk(r, ch);
+                        cp16(sA + o, arow[i] ? arow[i] + pn * 128 + ch * 16 : reinterpret_cast<const char*>(whi),
+                             arow[i] ? 16 : 0);
+                        const size_t off = (size_t)(c.n0 + r) * dim + pn * 64 + ch * 8;
+                        cp16(sBh + o, whi + off, 16);
+                        cp16(sBl + o, wlo + off, 16);
                     }
-                } else {   // dW_t[m0 + r][n0 + col ..] += D (row chunks of other CTAs add in)
-                    float* o = out.dW[cp.t] + (int64_t)(cp.m0 + r) * e.d_out + cp.n0 + col;
+                    cp_arrive_noinc(&full[st]);
+                }
+            } else {
+                // K rows kr = (p >> 4) + 8 i (i < 8) of the 64-row panel, 16-B chunk c of the 128-wide slice
+                const int cc = p & 15, kb = p >> 4;
+                int64_t gid_next[8];
+                auto load_gids = [&](int pn) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        red_add_f4(o + 4 * j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+                    for (int i = 0; i < 8; ++i) {
+                        const int64_t row = c.row0 + (int64_t)pn * 64 + kb + 8 * i;
+                        gid_next[i] = row < c.rlim ? __ldg(src_gid + row) : -1;
+                    }
+                };
+                load_gids(0);
+                for (int pn = 0; pn < c.KP; ++pn, ++it) {
+                    int64_t gid[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) gid[i] = gid_next[i];
+                    if (pn + 1 < c.KP) load_gids(pn + 1);       // prefetch the next panel's ids
+                    const int st = (int)(it % EN_STAGES);
+                    if (it >= EN_STAGES) umma::mbar_wait(&empty[st], (uint32_t)((it / EN_STAGES) - 1) & 1u);
+                    const uint32_t sA = umma::smem_u32(smem + st * EN_STAGE), sBh = sA + EN_PANEL, sBl = sA + 2 * EN_PANEL;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int kr = kb + 8 * i;
+                        const int64_t row = c.row0 + (int64_t)pn * 64 + kr;
+                        const bool ok = gid[i] >= 0;
+                        const uint32_t o = umma::mnmaj16_chunk(cc * 8, kr);
+                        const char* src = ok ? reinterpret_cast<const char*>(feat_row(g, gid[i])) + (size_t)(c.m0 + cc * 8) * 2
+                                             : reinterpret_cast<const char*>(e.d_hi);
+                        cp16(sA + o, src, ok ? 16 : 0);
+                        const size_t off = (size_t)(ok ? row : 0) * e.d_out + c.n0 + cc * 8;
+                        cp16(sBh + o, e.d_hi + off, ok ? 16 : 0);
+                        cp16(sBl + o, e.d_lo + off, ok ? 16 : 0);
+                    }
+                    cp_arrive_noinc(&full[st]);
                 }
             }
         }
-        umma::tc_fence_before();
-        __syncthreads();
-        cp.tile += grid;
-        if (cp.tile < total) decode(cp);
+    } else if (warp == 8) {
+        // ------------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t IDESC = umma::idesc_bf16(128, BWD, BWD);
+            int64_t it = 0, j = 0;
+            for (int64_t tile = blockIdx.x; tile < total; tile += grid, ++j) {
+                EnCursor c;
+                c.tile = tile;
+                decode(c);
+                const int acc = (int)(j & 1);
+                if (j >= 2) umma::mbar_wait(&tempty[acc], (uint32_t)((j >> 1) - 1) & 1u);
+                umma::tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * 128);
+                for (int pn = 0; pn < c.KP; ++pn, ++it) {
+                    const int st = (int)(it % EN_STAGES);
+                    umma::mbar_wait(&full[st], (uint32_t)(it / EN_STAGES) & 1u);
+                    umma::fence_proxy_async_smem();
+                    umma::tc_fence_after();
+                    const uint32_t a = umma::smem_u32(smem + st * EN_STAGE), bh = a + EN_PANEL, bl = a + 2 * EN_PANEL;
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                        const uint32_t o = BWD ? ks * 4096u : ks * 32u;
+                        const uint64_t da = BWD ? umma::desc_mnmajor16(a + o) : umma::desc_kmajor(a + o);
+                        const uint64_t dbh = BWD ? umma::desc_mnmajor16(bh + o) : umma::desc_kmajor(bh + o);
+                        const uint64_t dbl = BWD ? umma::desc_mnmajor16(bl + o) : umma::desc_kmajor(bl + o);
+                        umma::mma_f16(d, da, dbh, IDESC, (pn > 0 || ks > 0) ? 1u : 0u);
+                        umma::mma_f16(d, da, dbl, IDESC, 1u);
+                    }
+                    umma::mma_commit(&empty[st]);
+                }
+                umma::mma_commit(&tfull[acc]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------------ epilogue (warps 4-7)
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        int64_t j = 0;
+        for (int64_t tile = blockIdx.x; tile < total; tile += grid, ++j) {
+            EnCursor c;
+            c.tile = tile;
+            decode(c);
+            const int acc = (int)(j & 1);
+            umma::mbar_wait(&tfull[acc], (uint32_t)(j >> 1) & 1u);
+            umma::tc_fence_after();
+#pragma unroll 1
+            for (int cc = 0; cc < 4; ++cc) {
+                float v[32];
+                umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 128 + cc * 32), v);
+                if (!BWD) {
+                    const int64_t row = c.row0 + r;
+                    if (row < c.rlim) {
+                        float4* o4 = reinterpret_cast<float4*>(H0 + row * e.d_out + c.n0 + cc * 32);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) o4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                    }
+                } else {   // dW_t[m0 + r][n0 + ..] += D (row chunks of other CTAs add in)
+                    float* o = out.dW[c.t] + (int64_t)(c.m0 + r) * e.d_out + c.n0 + cc * 32;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        red_add_f4(o + 4 * k, make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+                }
+            }
+            umma::tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
     }
-    cp_wait<0>();
-    umma::tc_fence_after();
     __syncthreads();
-    if (warp == 0) umma::tmem_dealloc<128>(tmem);
+    if (warp == 0) {
+        umma::tc_fence_after();
+        umma::tmem_dealloc<256>(tmem);
+    }
 }
 
 }  // namespace gsb
@@ -418,7 +434,7 @@ static gsb_status launch_enc(const char* name, const GraphDev& g, const EncDev& 
         GSB_CUDA(cudaFuncSetAttribute(enc_umma_kernel<BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, EN_SMEM));
         attr = true;
     }
-    GSB_LAUNCH(name, enc_umma_kernel<BWD>, kNumSMs, EN_THREADS, EN_SMEM, s, g, e, m, src_gid, H0, out);
+    GSB_LAUNCH(name, enc_umma_kernel<BWD>, kNumSMs, EN_WS_THREADS, EN_SMEM, s, g, e, m, src_gid, H0, out);
     return GSB_OK;
 }
 

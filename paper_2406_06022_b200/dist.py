@@ -139,8 +139,8 @@ class PeerFeatures:
                     ptrs[w] = p.value
                     self.mapped.append(p.value - off)
             b = np.ascontiguousarray(self.bounds[t])
-            call("gsb_graph_set_feature_peers", store.h, t, world, b.ctypes.data_as(C.c_void_p), ptrs, dim,
-                 DTYPE_CODE[self.shards[t].dtype])
+            call("gsb_graph_set_feature_peers", store.h, t, world, b.ctypes.data_as(C.c_void_p), ptrs,
+                 int(self.shards[t].shape[1]) if self.shards[t].dim() == 2 else dim, DTYPE_CODE[self.shards[t].dtype])
         store.feat_dim = dim
         store.feat_dtype = self.shards[0].dtype
         self.store = store

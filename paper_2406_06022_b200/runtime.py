@@ -266,9 +266,22 @@ class _TrainerBase:
         self.v = torch.zeros_like(self.flat)
         self.shapes = {k: params[k].shape for k in self.names}
         self.t = 0
-        d0 = store.feat_dim
+        d0 = int(params["W0"].shape[1])      # layer-0 input width (= encoder output width)
         self.d_in = [d0] + [hidden] * (self.L - 1)
-        self.x0 = torch.empty((self.sampler.input_rows(), d0), dtype=store.feat_dtype, device=dev)
+        # input encoder (a6): ntypes with a projection Win{t}; the others are frozen tables
+        self.enc_types = [t for t in range(store.T) if f"Win{t}" in self.names]
+        nin = self.sampler.input_rows()
+        self.x0 = torch.empty((0 if self.enc_types else nin, d0), dtype=store.feat_dtype, device=dev)
+        if self.enc_types:
+            self.H0 = torch.empty((nin, d0), dtype=torch.float32, device=dev)
+            self.dH0 = torch.empty((nin, d0), dtype=torch.float32, device=dev)
+            self._win = (C.c_void_p * store.T)(*[self._pp(f"Win{t}").value if t in self.enc_types else None
+                                                  for t in range(store.T)])
+            self._dwin = (C.c_void_p * store.T)(*[self._pp(f"Win{t}", "g").value if t in self.enc_types else None
+                                                   for t in range(store.T)])
+            wb = C.c_size_t()
+            call("gsb_encoder_ws_bytes", self.sampler.h, self._win, d0, C.byref(wb))
+            self.enc_ws = torch.empty(max(int(wb.value), 1), dtype=torch.uint8, device=dev)
         self.hout = [torch.empty((self.sampler.dst_rows(l), hidden), dtype=torch.float32, device=dev)
                      for l in range(self.L)]
         self.acat = [torch.empty(self.sampler.acat_floats(l, self.d_in[l]), dtype=torch.float32, device=dev)
@@ -304,7 +317,7 @@ class _TrainerBase:
     def _gather_inputs(self, s):
         """Explicit input-row gather into x0 (unfused mode; with peer shards registered this is
         the unique-row NVLink fetch).  Part of the sample phase: it depends only on the blocks."""
-        if not self.fuse_gather and self.exchange is None:
+        if not self.fuse_gather and self.exchange is None and not self.enc_types:
             sm = self.sampler
             call("gsb_gather_block_inputs", sm.h, _ptr(sm.arena), _ptr(self.x0), s)
 
@@ -314,7 +327,11 @@ class _TrainerBase:
         otherwise x0 was filled by _gather_inputs in the sample phase."""
         sm = self.sampler
         rowmap = None
-        if self.exchange is not None:   # partitioned features: NCCL all-to-all fetch (C4/C5)
+        if self.enc_types:              # a6: projected / frozen input rows by gid -> H0 (fp32)
+            call("gsb_encoder_fwd", sm.h, _ptr(sm.arena), self._win, self.d_in[0], _ptr(self.H0), _ptr(self.enc_ws),
+                 self.enc_ws.numel(), s)
+            h = self.H0
+        elif self.exchange is not None:   # partitioned features: NCCL all-to-all fetch (C4/C5)
             gids, n = sm.input_gids()
             h, rowmap = self.exchange.gather(gids, n)   # layer 0 reads rows through perm
             self._keep = (h, rowmap)
@@ -338,11 +355,14 @@ class _TrainerBase:
     def _backward_layers(self, s):
         sm = self.sampler
         for l in reversed(range(self.L)):
-            dh_src = None if l == 0 else self.dh[l - 1]
+            dh_src = (self.dH0 if self.enc_types else None) if l == 0 else self.dh[l - 1]
             call("gsb_rgcn_layer_bwd", sm.h, _ptr(sm.arena), l, _ptr(self.hout[l]), _ptr(self.dh[l]),
                  self._pp(f"W{l}"), _ptr(self.acat[l]), self.d_in[l], self.hidden, int(l < self.L - 1),
                  self._pp(f"W{l}", "g"), self._pp(f"b{l}", "g"), _ptr(dh_src),
                  _ptr(self.dacat) if dh_src is not None else None, s)
+        if self.enc_types:   # a6 backward: dWin_t = X_t^T dH0 (frozen tables get no gradient)
+            call("gsb_encoder_bwd", sm.h, _ptr(sm.arena), self._win, _ptr(self.dH0), self.d_in[0], self._dwin,
+                 _ptr(self.enc_ws), self.enc_ws.numel(), s)
 
     def optimizer_step(self, stream=None, t_dev: bool = False):
         if t_dev:

@@ -229,12 +229,13 @@ def mag240m(scale: float = 1.0) -> Config:
 
 
 def tiny_enc() -> Config:
-    """Small input-encoder case for parity: tiny graph, ntype A with 96-d raw features and a
-    projection, B / C frozen 64-d tables (bf16 storage)."""
+    """Small input-encoder case for parity: tiny graph, ntype A with 256-d raw features and a
+    projection to 128, B / C frozen 128-d tables (bf16 storage)."""
     cfg = tiny()
     cfg.name = "tiny_enc"
     cfg.feat_dtype = "bf16"
-    cfg.feat_dims = [192, 64, 64]
+    cfg.feat_dim = 128
+    cfg.feat_dims = [256, 128, 128]
     cfg.project = [True, False, False]
     cfg.gen_seed = 2406060220 + 12
     return cfg
@@ -356,22 +357,27 @@ def feature_rows(cfg: Config, t: int, local_ids, backend: str = "np", device=Non
     return f
 
 
-def feature_table(cfg: Config, t: int, backend: str = "np", device=None, chunk: int = 1 << 20):
-    """Whole table of ntype t: numpy float32 (values exact in the config's dtype), or a torch
-    tensor of the config's storage dtype (float32 / bfloat16; the conversion is exact)."""
-    n = cfg.counts[t]
+def feature_table(cfg: Config, t: int, backend: str = "np", device=None, chunk: Optional[int] = None,
+                  lo: int = 0, hi: Optional[int] = None):
+    """Rows [lo, hi) (default: all) of ntype t's table: numpy float32 (values exact in the
+    config's dtype), or a torch tensor of the config's storage dtype (float32 / bfloat16;
+    the conversion is exact)."""
+    hi = cfg.counts[t] if hi is None else hi
+    n = hi - lo
+    d = cfg.dim_of(t)
+    chunk = chunk or max(1, (1 << 26) // d)          # ~64M elements per generation chunk
     if backend == "np":
-        out = np.empty((n, cfg.dim_of(t)), dtype=np.float32)
-        for lo in range(0, n, chunk):
-            hi = min(n, lo + chunk)
-            out[lo:hi] = feature_rows(cfg, t, np.arange(lo, hi), "np")
+        out = np.empty((n, d), dtype=np.float32)
+        for a in range(lo, hi, chunk):
+            b = min(hi, a + chunk)
+            out[a - lo:b - lo] = feature_rows(cfg, t, np.arange(a, b), "np")
         return out
     import torch
     dt = torch.bfloat16 if cfg.feat_dtype == "bf16" else torch.float32
-    out = torch.empty((n, cfg.dim_of(t)), dtype=dt, device=device)
-    for lo in range(0, n, chunk):
-        hi = min(n, lo + chunk)
-        out[lo:hi] = feature_rows(cfg, t, torch.arange(lo, hi, device=device), "torch", device).to(dt)
+    out = torch.empty((n, d), dtype=dt, device=device)
+    for a in range(lo, hi, chunk):
+        b = min(hi, a + chunk)
+        out[a - lo:b - lo] = feature_rows(cfg, t, torch.arange(a, b, device=device), "torch", device).to(dt)
     return out
 
 

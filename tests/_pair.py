@@ -73,3 +73,25 @@ def close_slack(gpu, ref, slack, rtol=RTOL_F32, what=""):
     bound = rtol * np.abs(r) + rtol * np.abs(r).max() + slack
     bad = np.abs(g - r) > bound
     assert not bad.any(), f"{what}: {bad.sum()} / {r.size} outside tolerance (+ReLU-tie slack)"
+
+
+def dsrc_tie_slack(res, R, layer, W, rtol=RTOL_F32):
+    """Slack of a layer's input-row gradient dh_src from its ambiguous ReLU units (R-relutie):
+    flipping unit (i, n) changes dZ[i, n] by dh[i, n], hence dh_src[u, k] by at most
+    |dh[i, n] W_r[k, n]| / c_r(i) for every sampled edge u -> i of relation r, and by
+    |dh[i, n] W_self[k, n]| for i's own source row (first order, exact for one flip)."""
+    z = res.zs[layer]
+    dh = res.extra["dh"][layer]
+    amb = np.abs(z) <= rtol * np.abs(z) + rtol * np.abs(z).max()
+    G = np.abs(dh) * amb
+    blk = res.blocks[layer]
+    Wa = np.abs(np.asarray(W, np.float64))
+    out = np.zeros((len(blk.src_gid), Wa.shape[1]))
+    for r in range(R):
+        e = np.nonzero(blk.e_etype == r)[0]
+        if len(e) == 0:
+            continue
+        M = G @ Wa[r].T
+        np.add.at(out, blk.e_src[e], M[blk.e_dst[e]] / blk.seg_cnt[blk.e_dst[e], r][:, None])
+    np.add.at(out, blk.self_row, G @ Wa[R].T)
+    return out

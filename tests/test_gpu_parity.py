@@ -155,11 +155,12 @@ def _gpu_trainer(cfg, st):
                        int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
 
 
-def check_grads(tr, res, cfg, step):
+def check_grads(tr, res, cfg, step, extra_slack=None):
     """Gradients within rtol; the hidden ReLU layers' dW/db additionally get the slack of
-    their ambiguous (|z| within tolerance of 0) activations (R-relutie)."""
+    their ambiguous (|z| within tolerance of 0) activations (R-relutie); extra_slack adds
+    per-parameter slack (e.g. input-encoder weights behind layer 0's ReLU)."""
     L = len(cfg.fanouts)
-    slack = {}
+    slack = dict(extra_slack or {})
     for l in range(L - 1):
         sW, sb, _ = relu_tie_slack(res, cfg.num_etypes, l)
         slack[f"W{l}"], slack[f"b{l}"] = sW, sb

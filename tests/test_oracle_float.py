@@ -276,6 +276,7 @@ def test_encoder_identity_projection_reduces_to_plain_step():
     dWin equals X^T dH0 of the plain step's input-layer gradient."""
     base = synth.with_dtype(synth.scaled(synth.tiny(), 0.2), "bf16")
     enc = synth.dataclasses.replace(base, feat_dims=[64, 64, 64], project=[True, False, False])
+    # (widths need not be GPU-friendly here: this pins the oracle alone)
     g0, g1 = oracle.Graph(base), oracle.Graph(enc)
     p0 = {k: v.astype(np.float64) for k, v in synth.init_params(base).items()}
     p1 = dict(p0)
