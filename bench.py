@@ -38,8 +38,9 @@ def parse():
     ap.add_argument("--impl", default="gsb", choices=["gsb", "reference"])
     ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b", "amazon_lp", "tiny_lp", "mag240m",
                                                         "mag240m_1_16"])
-    ap.add_argument("--feat-dtype", default=None, choices=["f32", "bf16"],
-                    help="feature storage type (default: the config's; compute stays fp32)")
+    ap.add_argument("--feat-dtype", default="auto", choices=["auto", "f32", "bf16"],
+                    help="feature storage type; compute stays fp32 (auto: bf16 for the large configs, as "
+                         "SURVEY §8(d) plans, fp32 for tiny)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--profile-steps", type=int, default=20)
@@ -182,6 +183,41 @@ def kernel_work(name: str, sz: dict, cfg: synth.Config):
     if name in ("nc_logits", "nc_gemm_dWc", "nc_gemm_dh"):
         return "flops", 2 * cfg.batch * hd * C
     return None, None
+
+
+def roofline_of(name, prof, sizes, cfg, pk, profile_steps):
+    """Roofline entry of kernel `name`: algorithmic work per launch (kernel_work) / its mean
+    CUDA-event launch time, against the measured peak; DRAM traffic from the ncu capture
+    recorded in profiles/roofline_traffic.json for this config (null if none)."""
+    kind, _ = kernel_work(name, sizes[0], cfg)
+    if kind is None or name not in prof:
+        return None
+    per_launch_work = float(np.mean([kernel_work(name, s, cfg)[1] for s in sizes]))
+    avg_ms = prof[name]["total_ms"] / prof[name]["launches"]
+    if kind == "bytes":
+        ach = per_launch_work / (avg_ms / 1e3) / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / pk["hbm_gbs"], "traffic": None, "peak_src": pk["src"]}
+    else:
+        # tcgen05 kind::tf32 (3xTF32: 3 MMAs per fp32 product; achieved counts the algorithmic
+        # 2*M*N*K once) against the dense TF32 peak = measured bf16 burst x 1/2 (guide ratio)
+        ach = per_launch_work / (avg_ms / 1e3) / 1e12
+        tf32 = pk.get("bf16_tflops", 1590.0) * 0.5
+        roof = {"kernel": name, "bound": "tensor", "achieved": ach, "peak": tf32, "unit": "TFLOP/s",
+                "frac": ach / tf32, "traffic": None,
+                "peak_src": "dense TF32 = measured bf16 burst (MEASURED_PEAKS.json) x 0.5 (nominal ratio)"}
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+        key = f"{cfg.name}:{name}"
+        if key in tj:
+            roof["traffic"] = tj[key]["bytes"]
+            roof["traffic_src"] = tj[key]["capture"]
+    except Exception:
+        pass
+    roof["avg_launch_us"] = avg_ms * 1e3
+    roof["launches_per_step"] = prof[name]["launches"] / profile_steps
+    roof["algorithmic_per_launch"] = per_launch_work
+    return roof
 
 
 # ------------------------------------------------------------------------------ gsb arm
@@ -458,37 +494,13 @@ def run_gsb(args, cfg):
         if dist is not None:
             dist.destroy_process_group()
         return None
-    # ---- roofline of the dominant kernel
+    # ---- roofline of the dominant kernel (the most expensive one with an algorithmic-work
+    # model) and, separately, of the fused gather + aggregation (north_star target)
     pk = peaks()
-    # dominant kernel = the most expensive one with an algorithmic-work model
     ranked = [k for k, _ in sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])]
     dom = next((k for k in ranked if kernel_work(k, sizes[0], cfg)[0] is not None), ranked[0])
-    kind, _ = kernel_work(dom, sizes[0], cfg)
-    roof = None
-    if kind is not None:
-        works = [kernel_work(dom, s, cfg)[1] for s in sizes]
-        per_launch_work = float(np.mean(works))
-        launches_per_step = prof[dom]["launches"] / args.profile_steps
-        avg_ms = prof[dom]["total_ms"] / prof[dom]["launches"]
-        if kind == "bytes":
-            ach = per_launch_work / (avg_ms / 1e3) / 1e9
-            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": ach / pk["hbm_gbs"], "traffic": None, "peak_src": pk["src"]}
-        else:
-            ach = per_launch_work / (avg_ms / 1e3) / 1e12
-            roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
-                    "frac": ach / pk["fp32_tflops"], "traffic": None,
-                    "peak_src": "FP32 FFMA: 148 SMs x 128 lanes x 2 x sm_max_mhz (DESIGN.md)"}
-        try:
-            tj = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
-            if dom in tj:
-                roof["traffic"] = tj[dom]["bytes"]
-                roof["traffic_src"] = tj[dom]["capture"]
-        except Exception:
-            pass
-        roof["avg_launch_us"] = avg_ms * 1e3
-        roof["launches_per_step"] = launches_per_step
-        roof["algorithmic_per_launch"] = per_launch_work
+    roof = roofline_of(dom, prof, sizes, cfg, pk, args.profile_steps)
+    roof_agg = roofline_of("rgcn_agg_l0", prof, sizes, cfg, pk, args.profile_steps) if "rgcn_agg_l0" in prof else None
     step_ms_prof = sum(v["total_ms"] for v in prof.values()) / args.profile_steps
     kernels = {k: {"us_per_step": v["total_ms"] * 1e3 / args.profile_steps,
                    "share": v["total_ms"] / args.profile_steps / step_ms_prof} for k, v in
@@ -510,6 +522,7 @@ def run_gsb(args, cfg):
                                      else "off"}),
         "sampled_edges_per_s": edges_per_step * ws / (ms_per_step / 1e3),
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
+        "roofline_gather_aggregation": roof_agg,
         "kernels": kernels, "setup_s": setup_s,
     }
     if tr.exchange is not None:
@@ -590,8 +603,10 @@ def run_reference(args, cfg):
 def main():
     args = parse()
     cfg = config_for(args.config)
-    if args.feat_dtype:
-        cfg = synth.with_dtype(cfg, args.feat_dtype)
+    fd = args.feat_dtype
+    if fd == "auto":
+        fd = cfg.feat_dtype if cfg.name in ("tiny", "tiny_lp") or cfg.feat_dtype == "bf16" else "bf16"
+    cfg = synth.with_dtype(cfg, fd)
     if args.impl == "reference":
         line = run_reference(args, cfg)
         if line is not None:

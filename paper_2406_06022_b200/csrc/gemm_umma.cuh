@@ -225,6 +225,94 @@ __device__ __forceinline__ float4 split_panel(uint8_t* stage, int tid) {
     return cs;
 }
 
+// Per-thread source pointers of the tile being loaded, resolved once per tile so that a panel's
+// copies are a pointer add + cp.async each (the generic issue_panel recomputes row bases,
+// slot weights and bounds for every chunk of every panel).  Used when all chunks are whole
+// 16-B copies (aligned operands, N / d_in multiples of 4 or 32 as below).
+struct FastSrc {
+    const float* a[4];
+    const float* b[4];
+    int64_t arow[4];     // TN: first row of this thread's A/B chunk rows (row0 + kr)
+    int64_t boff[4];     // NN: element offset of this thread's B chunks inside a W slot panel
+    bool bok;            // NN: this thread's B columns exist
+};
+
+template <int MODE>
+__device__ __forceinline__ void fast_setup(const UProb& P, const UCursor& c, int tid, FastSrc& f) {
+    if (MODE == UMMA_NN) {
+        const int ch = tid & 7, j = tid & 31;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t row = c.row0 + (tid >> 3) + 32 * i;
+            f.a[i] = row < c.rlim ? P.A + row * P.lda + 4 * ch : nullptr;
+            const int kr = (tid >> 5) + 8 * i;
+            f.boff[i] = (int64_t)kr * P.ldb + c.n0 + 4 * j;
+        }
+        f.bok = c.n0 + 4 * j < P.N;
+    } else if (MODE == UMMA_NT) {
+        const int ch = tid & 7;
+        const float* W = P.B + (int64_t)P.rg.slot_w[c.t][c.s] * P.bslot;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = (tid >> 3) + 32 * i;
+            const int64_t row = c.row0 + r;
+            f.a[i] = row < c.rlim ? P.A + row * P.lda + 4 * ch : nullptr;
+            const int k = c.c0 + r;
+            f.b[i] = k < P.d_in ? W + (int64_t)k * P.ldb + 4 * ch : nullptr;
+        }
+    } else {
+        const int j = tid & 31;
+        const int64_t acol = (int64_t)c.s * P.d_in + c.c0 + 4 * j;
+        const bool aok = c.c0 + 4 * j < P.d_in, bok = c.n0 + 4 * j < P.N;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t row = c.row0 + (tid >> 5) + 8 * i;
+            f.arow[i] = row;
+            f.a[i] = aok ? P.A + row * P.lda + acol : nullptr;
+            f.b[i] = bok ? P.B + row * P.ldb + c.n0 + 4 * j : nullptr;
+        }
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void issue_panel_fast(const UProb& P, const UCursor& c, const FastSrc& f, uint8_t* stage,
+                                                 int tid) {
+    const uint32_t Ahi = umma::smem_u32(stage), Bhi = umma::smem_u32(stage + 2 * UM_PANEL);
+    if (MODE == UMMA_NN) {
+        const int per = P.d_in / 32;
+        const int sp = c.p / per;
+        const int kk = (c.p - sp * per) * 32;
+        const float* W = P.B + (int64_t)P.rg.slot_w[c.t][sp] * P.bslot + (int64_t)kk * P.ldb;
+        const int ch = tid & 7, j = tid & 31;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = (tid >> 3) + 32 * i;
+            cp16(Ahi + umma::kmajor_off(r, 4 * ch), f.a[i] ? f.a[i] + c.p * 32 : P.A, f.a[i] ? 16 : 0);
+            const int kr = (tid >> 5) + 8 * i;
+            cp16(Bhi + umma::mnmajor_off(4 * j, kr), f.bok ? W + f.boff[i] : P.B, f.bok ? 16 : 0);
+        }
+    } else if (MODE == UMMA_NT) {
+        const int ch = tid & 7;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = (tid >> 3) + 32 * i;
+            cp16(Ahi + umma::kmajor_off(r, 4 * ch), f.a[i] ? f.a[i] + c.p * 32 : P.A, f.a[i] ? 16 : 0);
+            cp16(Bhi + umma::kmajor_off(r, 4 * ch), f.b[i] ? f.b[i] + c.p * 32 : P.B, f.b[i] ? 16 : 0);
+        }
+    } else {
+        const int j = tid & 31;
+        const int64_t dr = (int64_t)c.p * 32;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int kr = (tid >> 5) + 8 * i;
+            const bool rok = f.arow[i] + dr < c.rlim;
+            const bool oa = rok && f.a[i], ob = rok && f.b[i];
+            cp16(Ahi + umma::mnmajor_off(4 * j, kr), oa ? f.a[i] + dr * P.lda : P.A, oa ? 16 : 0);
+            cp16(Bhi + umma::mnmajor_off(4 * j, kr), ob ? f.b[i] + dr * P.ldb : P.B, ob ? 16 : 0);
+        }
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
     extern __shared__ uint8_t smem_raw[];
@@ -250,6 +338,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
     constexpr uint32_t IDESC = umma::idesc_tf32(128, A_MN, B_MN);
     const bool vecA = ((P.lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(P.A) & 15) == 0);
     const bool vecB = ((P.ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(P.B) & 15) == 0);
+    const bool fast = vecA && vecB && ((P.bslot & 3) == 0) &&
+                      (MODE == UMMA_NN ? (P.N & 3) == 0 : MODE == UMMA_NT ? (P.N & 31) == 0
+                                                                          : ((P.N & 3) == 0 && (P.d_in & 3) == 0));
+    FastSrc fs;
 
     const int nct = (P.N + 127) / 128;
     const int kct = (P.d_in + 127) / 128;
@@ -263,39 +355,49 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
     // two cursors over the same (tile, panel) sequence: loads run UM_STAGES-1 panels ahead
     UCursor ld, cp;
     ld.tile = blockIdx.x;
-    if (ld.tile < total) decode_tile<MODE>(P, ld.tile, nct, kct, ld);
+    if (ld.tile < total) {
+        decode_tile<MODE>(P, ld.tile, nct, kct, ld);
+        if (fast) fast_setup<MODE>(P, ld, tid, fs);
+    }
     cp = ld;
-    auto advance = [&](UCursor& c) {
+    auto advance = [&](UCursor& c, bool is_ld) {
         if (c.tile >= total) return;
         if (++c.p >= c.KP) {
             c.tile += gridDim.x;
-            if (c.tile < total) decode_tile<MODE>(P, c.tile, nct, kct, c);
+            if (c.tile < total) {
+                decode_tile<MODE>(P, c.tile, nct, kct, c);
+                if (is_ld && fast) fast_setup<MODE>(P, c, tid, fs);
+            }
         }
     };
-    uint32_t phase[UM_STAGES] = {0, 0, 0};
-    bool pend[UM_STAGES] = {false, false, false};
-    int64_t it_ld = 0, it_cp = 0;
+    auto issue = [&](uint8_t* stage) {
+        if (fast) issue_panel_fast<MODE>(P, ld, fs, stage, tid);
+        else issue_panel<MODE>(P, ld, stage, tid, vecA, vecB);
+    };
+    uint32_t phase = 0, pend = 0;          // per-stage bits
+    int st_ld = 0, st_cp = 0;              // stage of the next load / of the panel being computed
     auto wait_stage = [&](int st) {
-        if (pend[st]) {
-            umma::mbar_wait(&bars[st], phase[st]);
-            phase[st] ^= 1;
-            pend[st] = false;
+        if (pend & (1u << st)) {
+            umma::mbar_wait(&bars[st], (phase >> st) & 1u);
+            phase ^= 1u << st;
+            pend &= ~(1u << st);
         }
     };
+    auto next_st = [](int s) { return s + 1 == UM_STAGES ? 0 : s + 1; };
     // prologue
     for (int k = 0; k < UM_STAGES - 1; ++k) {
         if (ld.tile < total) {
-            issue_panel<MODE>(P, ld, smem + (it_ld % UM_STAGES) * UM_STAGE, tid, vecA, vecB);
-            advance(ld);
+            issue(smem + st_ld * UM_STAGE);
+            advance(ld, true);
         }
         cp_commit();
-        ++it_ld;
+        st_ld = next_st(st_ld);
     }
     float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
     while (cp.tile < total) {
         // data of panel it_cp landed (the one newer group may still be in flight)
         cp_wait<UM_STAGES - 2>();
-        const int st = (int)(it_cp % UM_STAGES);
+        const int st = st_cp;
         uint8_t* stage = smem + st * UM_STAGE;
         const bool do_db = (MODE == UMMA_TN) && P.db && (cp.s == rg.ks[cp.t] - 1) && cp.c0 == 0;
         {   // split overlaps the tensor pipe still working on the previous panel
@@ -322,25 +424,28 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
             }
             umma::mma_commit(&bars[st]);
         }
-        pend[st] = true;
+        pend |= 1u << st;
         // refill: the stage of panel it_cp-1 receives panel it_cp+2 once its MMAs are done
         {
-            const int fst = (int)(it_ld % UM_STAGES);
+            const int fst = st_ld;
             wait_stage(fst);
             if (ld.tile < total) {
-                issue_panel<MODE>(P, ld, smem + fst * UM_STAGE, tid, vecA, vecB);
-                advance(ld);
+                issue(smem + fst * UM_STAGE);
+                advance(ld, true);
             }
             cp_commit();
-            ++it_ld;
+            st_ld = next_st(st_ld);
         }
-        ++it_cp;
+        st_cp = next_st(st_cp);
         if (cp.p + 1 < cp.KP) {
-            advance(cp);
+            advance(cp, false);
             continue;
         }
         // ---- last panel of the tile: drain its MMAs, then the epilogue
-        for (int k = 1; k <= UM_STAGES; ++k) wait_stage((int)((it_cp - 1 + k) % UM_STAGES));   // oldest first
+        {
+            int w = st_cp;                                   // oldest pending stage first
+            for (int k = 0; k < UM_STAGES; ++k, w = next_st(w)) wait_stage(w);
+        }
         umma::tc_fence_after();
         {
             const int q = warp & 3, half = warp >> 2;
@@ -449,7 +554,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
         cs = make_float4(0.f, 0.f, 0.f, 0.f);
         umma::tc_fence_before();
         __syncthreads();
-        advance(cp);
+        advance(cp, false);
     }
     cp_wait<0>();
     umma::tc_fence_after();
