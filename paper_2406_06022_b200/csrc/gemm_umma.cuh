@@ -65,18 +65,44 @@ __device__ __forceinline__ void cp_chunk(uint32_t dst, const float* base, int64_
     }
 }
 
-// in-place split of one staged 16-B chunk: hi (rna tf32) overwrites the raw value, lo goes to lo
-__device__ __forceinline__ float4 split_chunk(uint8_t* hi, uint8_t* lo, uint32_t off) {
-    float4 v = *reinterpret_cast<float4*>(hi + off);
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+// in-place split through 32-bit shared addresses (LDS/STS, not generic loads/stores)
+__device__ __forceinline__ float4 split_chunk_s(uint32_t hi, uint32_t lo, uint32_t off) {
+    const float4 v = lds128(hi + off);
     uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
     umma::split_tf32(v.x, h0, l0);
     umma::split_tf32(v.y, h1, l1);
     umma::split_tf32(v.z, h2, l2);
     umma::split_tf32(v.w, h3, l3);
-    *reinterpret_cast<uint4*>(hi + off) = make_uint4(h0, h1, h2, h3);
-    *reinterpret_cast<uint4*>(lo + off) = make_uint4(l0, l1, l2, l3);
+    sts128(hi + off, h0, h1, h2, h3);
+    sts128(lo + off, l0, l1, l2, l3);
     return v;
 }
+
+// per-thread shared-memory offsets of its 4 A and 4 B chunks (constant for the kernel)
+struct SmemOff {
+    uint32_t a[4], b[4];
+};
+template <int MODE>
+__device__ __forceinline__ SmemOff smem_offsets(int tid) {
+    SmemOff o;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t kmA = umma::kmajor_off((tid >> 3) + 32 * i, 4 * (tid & 7));
+        const uint32_t mnA = umma::mnmajor_off(4 * (tid & 31), (tid >> 5) + 8 * i);
+        o.a[i] = (MODE == UMMA_TN) ? mnA : kmA;
+        o.b[i] = (MODE == UMMA_NT) ? kmA : mnA;
+    }
+    return o;
+}
+
 
 // One (tile, panel) position of this CTA's persistent schedule.
 struct UCursor {
@@ -201,30 +227,6 @@ __device__ __forceinline__ void issue_panel(const UProb& P, const UCursor& c, ui
     }
 }
 
-// split this thread's own chunks (the ones it issued) of a landed stage
-template <int MODE>
-__device__ __forceinline__ float4 split_panel(uint8_t* stage, int tid) {
-    uint8_t* Ahi = stage;
-    uint8_t* Alo = stage + UM_PANEL;
-    uint8_t* Bhi = stage + 2 * UM_PANEL;
-    uint8_t* Blo = stage + 3 * UM_PANEL;
-    float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t oa = (MODE == UMMA_TN) ? umma::mnmajor_off(4 * (tid & 31), (tid >> 5) + 8 * i)
-                                              : umma::kmajor_off((tid >> 3) + 32 * i, 4 * (tid & 7));
-        split_chunk(Ahi, Alo, oa);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t ob = (MODE == UMMA_NT) ? umma::kmajor_off((tid >> 3) + 32 * i, 4 * (tid & 7))
-                                              : umma::mnmajor_off(4 * (tid & 31), (tid >> 5) + 8 * i);
-        float4 v = split_chunk(Bhi, Blo, ob);
-        cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w;
-    }
-    return cs;
-}
-
 // Per-thread source pointers of the tile being loaded, resolved once per tile so that a panel's
 // copies are a pointer add + cp.async each (the generic issue_panel recomputes row bases,
 // slot weights and bounds for every chunk of every panel).  Used when all chunks are whole
@@ -275,42 +277,49 @@ __device__ __forceinline__ void fast_setup(const UProb& P, const UCursor& c, int
 }
 
 template <int MODE>
-__device__ __forceinline__ void issue_panel_fast(const UProb& P, const UCursor& c, const FastSrc& f, uint8_t* stage,
-                                                 int tid) {
-    const uint32_t Ahi = umma::smem_u32(stage), Bhi = umma::smem_u32(stage + 2 * UM_PANEL);
+__device__ __forceinline__ void issue_panel_fast(const UProb& P, const UCursor& c, const FastSrc& f,
+                                                 const SmemOff& so, uint32_t Ahi) {
+    const uint32_t Bhi = Ahi + 2 * UM_PANEL;
     if (MODE == UMMA_NN) {
         const int per = P.d_in / 32;
         const int sp = c.p / per;
         const int kk = (c.p - sp * per) * 32;
         const float* W = P.B + (int64_t)P.rg.slot_w[c.t][sp] * P.bslot + (int64_t)kk * P.ldb;
-        const int ch = tid & 7, j = tid & 31;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int r = (tid >> 3) + 32 * i;
-            cp16(Ahi + umma::kmajor_off(r, 4 * ch), f.a[i] ? f.a[i] + c.p * 32 : P.A, f.a[i] ? 16 : 0);
-            const int kr = (tid >> 5) + 8 * i;
-            cp16(Bhi + umma::mnmajor_off(4 * j, kr), f.bok ? W + f.boff[i] : P.B, f.bok ? 16 : 0);
+            cp16(Ahi + so.a[i], f.a[i] ? f.a[i] + c.p * 32 : P.A, f.a[i] ? 16 : 0);
+            cp16(Bhi + so.b[i], f.bok ? W + f.boff[i] : P.B, f.bok ? 16 : 0);
         }
     } else if (MODE == UMMA_NT) {
-        const int ch = tid & 7;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int r = (tid >> 3) + 32 * i;
-            cp16(Ahi + umma::kmajor_off(r, 4 * ch), f.a[i] ? f.a[i] + c.p * 32 : P.A, f.a[i] ? 16 : 0);
-            cp16(Bhi + umma::kmajor_off(r, 4 * ch), f.b[i] ? f.b[i] + c.p * 32 : P.B, f.b[i] ? 16 : 0);
+            cp16(Ahi + so.a[i], f.a[i] ? f.a[i] + c.p * 32 : P.A, f.a[i] ? 16 : 0);
+            cp16(Bhi + so.b[i], f.b[i] ? f.b[i] + c.p * 32 : P.B, f.b[i] ? 16 : 0);
         }
     } else {
-        const int j = tid & 31;
         const int64_t dr = (int64_t)c.p * 32;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int kr = (tid >> 5) + 8 * i;
             const bool rok = f.arow[i] + dr < c.rlim;
             const bool oa = rok && f.a[i], ob = rok && f.b[i];
-            cp16(Ahi + umma::mnmajor_off(4 * j, kr), oa ? f.a[i] + dr * P.lda : P.A, oa ? 16 : 0);
-            cp16(Bhi + umma::mnmajor_off(4 * j, kr), ob ? f.b[i] + dr * P.ldb : P.B, ob ? 16 : 0);
+            cp16(Ahi + so.a[i], oa ? f.a[i] + dr * P.lda : P.A, oa ? 16 : 0);
+            cp16(Bhi + so.b[i], ob ? f.b[i] + dr * P.ldb : P.B, ob ? 16 : 0);
         }
     }
+}
+
+// split this thread's own chunks of a landed stage (shared addresses, precomputed offsets)
+template <int MODE>
+__device__ __forceinline__ float4 split_panel_s(uint32_t stage, const SmemOff& so) {
+    float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split_chunk_s(stage, stage + UM_PANEL, so.a[i]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float4 v = split_chunk_s(stage + 2 * UM_PANEL, stage + 3 * UM_PANEL, so.b[i]);
+        cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w;
+    }
+    return cs;
 }
 
 template <int MODE>
@@ -370,8 +379,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
             }
         }
     };
+    const SmemOff so = smem_offsets<MODE>(tid);
     auto issue = [&](uint8_t* stage) {
-        if (fast) issue_panel_fast<MODE>(P, ld, fs, stage, tid);
+        if (fast) issue_panel_fast<MODE>(P, ld, fs, so, umma::smem_u32(stage));
         else issue_panel<MODE>(P, ld, stage, tid, vecA, vecB);
     };
     uint32_t phase = 0, pend = 0;          // per-stage bits
@@ -401,7 +411,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
         uint8_t* stage = smem + st * UM_STAGE;
         const bool do_db = (MODE == UMMA_TN) && P.db && (cp.s == rg.ks[cp.t] - 1) && cp.c0 == 0;
         {   // split overlaps the tensor pipe still working on the previous panel
-            float4 v = split_panel<MODE>(stage, tid);
+            float4 v = split_panel_s<MODE>(umma::smem_u32(stage), so);
             if (do_db) { cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w; }
         }
         umma::fence_proxy_async_smem();

@@ -283,10 +283,12 @@ static RowGroups single_group(int64_t M) {
     return rg;
 }
 
+#ifdef GSB_SIMT_GEMM
 static int gemm_grid(int64_t rows_cap, int ncols_tiles, int groups) {
     int64_t tiles = (ceil_div(rows_cap, BM) + groups) * ncols_tiles;
     return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs * 4));
 }
+#endif
 
 }  // namespace gsb
 
