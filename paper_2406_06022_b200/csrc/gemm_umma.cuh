@@ -45,7 +45,13 @@ struct UProb {
     int ksplit;            // NN/NT: K-panel splits per tile (>1: partials red.add into a zeroed C; no relu)
 };
 
-constexpr int UM_THREADS = 256;
+#ifndef GSB_UM_THREADS
+#define GSB_UM_THREADS 256
+#endif
+constexpr int UM_THREADS = GSB_UM_THREADS;
+constexpr int UM_NI = 1024 / UM_THREADS;      // 16-B chunks per thread per operand panel
+constexpr int UM_RS = UM_THREADS / 8;         // K-major: row stride between a thread's chunks
+constexpr int UM_KS = UM_THREADS / 32;        // MN-major: K-row stride between a thread's chunks
 constexpr int UM_PANEL = 16384;            // bytes of one 128 x 32 fp32/tf32 panel
 constexpr int UM_STAGE = 4 * UM_PANEL;     // A_hi(raw), A_lo, B_hi(raw), B_lo
 constexpr int UM_STAGES = 3;
@@ -88,15 +94,15 @@ __device__ __forceinline__ float4 split_chunk_s(uint32_t hi, uint32_t lo, uint32
 
 // per-thread shared-memory offsets of its 4 A and 4 B chunks (constant for the kernel)
 struct SmemOff {
-    uint32_t a[4], b[4];
+    uint32_t a[UM_NI], b[UM_NI];
 };
 template <int MODE>
 __device__ __forceinline__ SmemOff smem_offsets(int tid) {
     SmemOff o;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t kmA = umma::kmajor_off((tid >> 3) + 32 * i, 4 * (tid & 7));
-        const uint32_t mnA = umma::mnmajor_off(4 * (tid & 31), (tid >> 5) + 8 * i);
+    for (int i = 0; i < UM_NI; ++i) {
+        const uint32_t kmA = umma::kmajor_off((tid >> 3) + UM_RS * i, 4 * (tid & 7));
+        const uint32_t mnA = umma::mnmajor_off(4 * (tid & 31), (tid >> 5) + UM_KS * i);
         o.a[i] = (MODE == UMMA_TN) ? mnA : kmA;
         o.b[i] = (MODE == UMMA_NT) ? kmA : mnA;
     }
@@ -182,29 +188,29 @@ __device__ __forceinline__ void issue_panel(const UProb& P, const UCursor& c, ui
         const int kk = (c.p - sp * per) * 32;
         const int64_t acol = (int64_t)sp * P.d_in + kk;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = (tid >> 3) + 32 * i, ch = tid & 7;
+        for (int i = 0; i < UM_NI; ++i) {
+            const int r = (tid >> 3) + UM_RS * i, ch = tid & 7;
             const int64_t row = c.row0 + r;
             cp_chunk(Ahi + umma::kmajor_off(r, 4 * ch), P.A, P.lda, row, row < c.rlim, acol + 4 * ch, acol + 32, vecA);
         }
         const float* W = P.B + (int64_t)P.rg.slot_w[c.t][sp] * P.bslot;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int kr = (tid >> 5) + 8 * i, j = tid & 31;
+        for (int i = 0; i < UM_NI; ++i) {
+            const int kr = (tid >> 5) + UM_KS * i, j = tid & 31;
             cp_chunk(Bhi + umma::mnmajor_off(4 * j, kr), W, P.ldb, kk + kr, true, c.n0 + 4 * j, P.N, vecB);
         }
     } else if (MODE == UMMA_NT) {
         const int nn = c.p * 32;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = (tid >> 3) + 32 * i, ch = tid & 7;
+        for (int i = 0; i < UM_NI; ++i) {
+            const int r = (tid >> 3) + UM_RS * i, ch = tid & 7;
             const int64_t row = c.row0 + r;
             cp_chunk(Ahi + umma::kmajor_off(r, 4 * ch), P.A, P.lda, row, row < c.rlim, nn + 4 * ch, P.N, vecA);
         }
         const float* W = P.B + (int64_t)P.rg.slot_w[c.t][c.s] * P.bslot;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = (tid >> 3) + 32 * i, ch = tid & 7;
+        for (int i = 0; i < UM_NI; ++i) {
+            const int r = (tid >> 3) + UM_RS * i, ch = tid & 7;
             const int k = c.c0 + r;
             cp_chunk(Bhi + umma::kmajor_off(r, 4 * ch), W, P.ldb, k, k < P.d_in, nn + 4 * ch, P.N, vecB);
         }
@@ -213,14 +219,14 @@ __device__ __forceinline__ void issue_panel(const UProb& P, const UCursor& c, ui
         const int64_t acol = (int64_t)c.s * P.d_in + c.c0;
         const int64_t alim = (int64_t)c.s * P.d_in + P.d_in;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int kr = (tid >> 5) + 8 * i, j = tid & 31;
+        for (int i = 0; i < UM_NI; ++i) {
+            const int kr = (tid >> 5) + UM_KS * i, j = tid & 31;
             const int64_t row = rb + kr;
             cp_chunk(Ahi + umma::mnmajor_off(4 * j, kr), P.A, P.lda, row, row < c.rlim, acol + 4 * j, alim, vecA);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int kr = (tid >> 5) + 8 * i, j = tid & 31;
+        for (int i = 0; i < UM_NI; ++i) {
+            const int kr = (tid >> 5) + UM_KS * i, j = tid & 31;
             const int64_t row = rb + kr;
             cp_chunk(Bhi + umma::mnmajor_off(4 * j, kr), P.B, P.ldb, row, row < c.rlim, c.n0 + 4 * j, P.N, vecB);
         }
@@ -232,10 +238,10 @@ __device__ __forceinline__ void issue_panel(const UProb& P, const UCursor& c, ui
 // slot weights and bounds for every chunk of every panel).  Used when all chunks are whole
 // 16-B copies (aligned operands, N / d_in multiples of 4 or 32 as below).
 struct FastSrc {
-    const float* a[4];
-    const float* b[4];
-    int64_t arow[4];     // TN: first row of this thread's A/B chunk rows (row0 + kr)
-    int64_t boff[4];     // NN: element offset of this thread's B chunks inside a W slot panel
+    const float* a[UM_NI];
+    const float* b[UM_NI];
+    int64_t arow[UM_NI];     // TN: first row of this thread's A/B chunk rows (row0 + kr)
+    int64_t boff[UM_NI];     // NN: element offset of this thread's B chunks inside a W slot panel
     bool bok;            // NN: this thread's B columns exist
 };
 
@@ -244,10 +250,10 @@ __device__ __forceinline__ void fast_setup(const UProb& P, const UCursor& c, int
     if (MODE == UMMA_NN) {
         const int ch = tid & 7, j = tid & 31;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t row = c.row0 + (tid >> 3) + 32 * i;
+        for (int i = 0; i < UM_NI; ++i) {
+            const int64_t row = c.row0 + (tid >> 3) + UM_RS * i;
             f.a[i] = row < c.rlim ? P.A + row * P.lda + 4 * ch : nullptr;
-            const int kr = (tid >> 5) + 8 * i;
+            const int kr = (tid >> 5) + UM_KS * i;
             f.boff[i] = (int64_t)kr * P.ldb + c.n0 + 4 * j;
         }
         f.bok = c.n0 + 4 * j < P.N;
@@ -255,8 +261,8 @@ __device__ __forceinline__ void fast_setup(const UProb& P, const UCursor& c, int
         const int ch = tid & 7;
         const float* W = P.B + (int64_t)P.rg.slot_w[c.t][c.s] * P.bslot;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = (tid >> 3) + 32 * i;
+        for (int i = 0; i < UM_NI; ++i) {
+            const int r = (tid >> 3) + UM_RS * i;
             const int64_t row = c.row0 + r;
             f.a[i] = row < c.rlim ? P.A + row * P.lda + 4 * ch : nullptr;
             const int k = c.c0 + r;
@@ -267,8 +273,8 @@ __device__ __forceinline__ void fast_setup(const UProb& P, const UCursor& c, int
         const int64_t acol = (int64_t)c.s * P.d_in + c.c0 + 4 * j;
         const bool aok = c.c0 + 4 * j < P.d_in, bok = c.n0 + 4 * j < P.N;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t row = c.row0 + (tid >> 5) + 8 * i;
+        for (int i = 0; i < UM_NI; ++i) {
+            const int64_t row = c.row0 + (tid >> 5) + UM_KS * i;
             f.arow[i] = row;
             f.a[i] = aok ? P.A + row * P.lda + acol : nullptr;
             f.b[i] = bok ? P.B + row * P.ldb + c.n0 + 4 * j : nullptr;
@@ -286,20 +292,20 @@ __device__ __forceinline__ void issue_panel_fast(const UProb& P, const UCursor& 
         const int kk = (c.p - sp * per) * 32;
         const float* W = P.B + (int64_t)P.rg.slot_w[c.t][sp] * P.bslot + (int64_t)kk * P.ldb;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < UM_NI; ++i) {
             cp16(Ahi + so.a[i], f.a[i] ? f.a[i] + c.p * 32 : P.A, f.a[i] ? 16 : 0);
             cp16(Bhi + so.b[i], f.bok ? W + f.boff[i] : P.B, f.bok ? 16 : 0);
         }
     } else if (MODE == UMMA_NT) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < UM_NI; ++i) {
             cp16(Ahi + so.a[i], f.a[i] ? f.a[i] + c.p * 32 : P.A, f.a[i] ? 16 : 0);
             cp16(Bhi + so.b[i], f.b[i] ? f.b[i] + c.p * 32 : P.B, f.b[i] ? 16 : 0);
         }
     } else {
         const int64_t dr = (int64_t)c.p * 32;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < UM_NI; ++i) {
             const bool rok = f.arow[i] + dr < c.rlim;
             const bool oa = rok && f.a[i], ob = rok && f.b[i];
             cp16(Ahi + so.a[i], oa ? f.a[i] + dr * P.lda : P.A, oa ? 16 : 0);
@@ -313,9 +319,9 @@ template <int MODE>
 __device__ __forceinline__ float4 split_panel_s(uint32_t stage, const SmemOff& so) {
     float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) split_chunk_s(stage, stage + UM_PANEL, so.a[i]);
+    for (int i = 0; i < UM_NI; ++i) split_chunk_s(stage, stage + UM_PANEL, so.a[i]);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < UM_NI; ++i) {
         const float4 v = split_chunk_s(stage + 2 * UM_PANEL, stage + 3 * UM_PANEL, so.b[i]);
         cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w;
     }
@@ -458,11 +464,12 @@ __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
         }
         umma::tc_fence_after();
         {
+            constexpr int CW = 128 / (UM_THREADS / 128);   // columns drained per warp
             const int q = warp & 3, half = warp >> 2;
             const int r = q * 32 + lane;
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-                const int col = half * 64 + cc * 32;
+            for (int cc = 0; cc < CW / 32; ++cc) {
+                const int col = half * CW + cc * 32;
                 float v[32];
                 umma::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)col, v);
                 if (MODE == UMMA_NN && P.ksplit > 1) {
