@@ -25,7 +25,7 @@ __device__ __forceinline__ const uint4* src_row(const GraphDev& g, const char* h
 
 // FEAT: source rows come from the feature tables via e_src_gid / dst_gid (no x0 buffer)
 template <bool FEAT, bool BF16, int LPE>
-__global__ void __launch_bounds__(256, 6) agg_kernel(GraphDev g, const HopMeta* __restrict__ m,
+__global__ void __launch_bounds__(256, 4) agg_kernel(GraphDev g, const HopMeta* __restrict__ m,
                                                   const int64_t* __restrict__ seg_ptr,
                                                   const int32_t* __restrict__ e_src,
                                                   const int64_t* __restrict__ e_src_gid,
@@ -34,19 +34,29 @@ __global__ void __launch_bounds__(256, 6) agg_kernel(GraphDev g, const HopMeta* 
                                                   const int32_t* __restrict__ rowmap) {
     constexpr int V = Chunk<BF16>::kVec;
     constexpr int G = 32 / LPE;                  // edges per warp pass
+    __shared__ int64_t s_dst_off[kMaxT + 1], s_src_off[kMaxT + 1];
+    if (threadIdx.x <= (unsigned)g.T) {
+        s_dst_off[threadIdx.x] = m->dst_off[threadIdx.x];
+        s_src_off[threadIdx.x] = m->src_off[threadIdx.x];
+    }
+    const int64_t n = m->n_dst;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int grp = lane / LPE, sub = lane % LPE;
     const int S = g.S;
-    const int64_t n = m->n_dst;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int cpr = row_bytes >> 4;              // 16-byte chunks per row
     for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < n; j += warps) {
         int t = 0;
-        for (int k = 1; k < g.T; ++k) t += (j >= m->dst_off[k]) ? 1 : 0;
+        for (int k = 1; k < g.T; ++k) t += (j >= s_dst_off[k]) ? 1 : 0;
         const int St = g.n_slots[t];
         float* out = acat + j * lda;
+        // all St+1 slot boundaries of row j with one load (lane s = start of slot s)
+        const int64_t bl = (lane <= St) ? seg_ptr[j * S + lane] : 0;
+        // the self row's address, resolved while the segments load
+        const uint4* ps = src_row<FEAT>(g, h, row_bytes, FEAT ? dst_gid[j] : s_src_off[t] + (j - s_dst_off[t]), rowmap);
         for (int s = 0; s < St; ++s) {
-            const int64_t e0 = seg_ptr[j * S + s], e1 = seg_ptr[j * S + s + 1];
+            const int64_t e0 = __shfl_sync(0xffffffffu, bl, s), e1 = __shfl_sync(0xffffffffu, bl, s + 1);
             const float inv = (e1 > e0) ? 1.f / (float)(e1 - e0) : 0.f;
             // every lane runs every chunk pass (the shuffles need the whole warp); lanes past
             // the row width or the segment end only predicate their loads and stores
@@ -57,17 +67,20 @@ __global__ void __launch_bounds__(256, 6) agg_kernel(GraphDev g, const HopMeta* 
 #pragma unroll
                 for (int v = 0; v < V; ++v) acc[v] = 0.f;
                 for (int64_t cb = e0; cb < e1; cb += 32) {
-                    // one coalesced load of up to 32 source keys, broadcast by shuffle
-                    const int64_t key = (cb + lane < e1) ? (FEAT ? e_src_gid[cb + lane] : (int64_t)e_src[cb + lane]) : 0;
+                    // one coalesced load of up to 32 source keys; lane i resolves the row
+                    // address of edge cb+i once, the warp takes the addresses by shuffle
+                    const uint4* prow = (cb + lane < e1)
+                        ? src_row<FEAT>(g, h, row_bytes, FEAT ? e_src_gid[cb + lane] : (int64_t)e_src[cb + lane], rowmap)
+                        : nullptr;
                     const int cnt = (int)min((int64_t)32, e1 - cb);
                     for (int k = 0; k < cnt; k += 4 * G) {
                         uint4 x[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int idx = k + grp + G * u;
-                            const int64_t kk = __shfl_sync(0xffffffffu, key, idx & 31);
+                            const uint64_t pu = __shfl_sync(0xffffffffu, (uint64_t)prow, idx & 31);
                             x[u] = make_uint4(0u, 0u, 0u, 0u);
-                            if (cl && idx < cnt) x[u] = __ldg(src_row<FEAT>(g, h, row_bytes, kk, rowmap) + c);
+                            if (cl && idx < cnt) x[u] = __ldg(reinterpret_cast<const uint4*>(pu) + c);
                         }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) chunk_acc<BF16>(acc, x[u]);
@@ -85,8 +98,6 @@ __global__ void __launch_bounds__(256, 6) agg_kernel(GraphDev g, const HopMeta* 
                 }
             }
         }
-        const int64_t self = m->src_off[t] + (j - m->dst_off[t]);
-        const uint4* ps = src_row<FEAT>(g, h, row_bytes, FEAT ? dst_gid[j] : self, rowmap);
         for (int c = lane; c < cpr; c += 32) {
             float r[V];
 #pragma unroll
