@@ -60,6 +60,8 @@ def lib():
             "oracle_nc_loss": (dbl, [i64, i32, i32, P, P, P, P, P, P, P, P]),
             "oracle_joint_negatives": (i64, [i64, i32, i64, i64, u64, u32, i64, P]),
             "oracle_lp_loss": (dbl, [i64, i32, i32, P, P, P, P, i32, P, P, P, P, P]),
+            "oracle_uniform_negatives": (i64, [i64, i32, i64, i64, u64, u32, i64, P]),
+            "oracle_lp_loss_ex": (dbl, [i64, i32, i32, i32, i32, P, P, P, i64, P, i32, P, P, P, P, P, P]),
             "oracle_adam": (None, [i64, P, P, P, P, dbl, dbl, dbl, dbl, i32]),
             "oracle_sgd": (None, [i64, P, P, dbl]),
         }
@@ -350,6 +352,37 @@ def lp_loss(hu, hv, hn, rel, K: int, loss_kind: int = 0):
     return loss, scores, dhu, dhv, dhn, drel
 
 
+def uniform_negatives(n_pos: int, K: int, n_dst_nodes: int, gid_base: int, seed: int, step: int,
+                      pos_base: int = 0):
+    """Uniform negatives (App. A.2.1): K iid draws per positive, n_pos*K in total."""
+    neg = np.zeros(n_pos * K, np.int64)
+    lib().oracle_uniform_negatives(n_pos, K, n_dst_nodes, gid_base, seed, step, pos_base, _p(neg))
+    return neg
+
+
+# negative samplers (App. A.2.1): name -> (mode, group(K)) for oracle_lp_loss_ex
+NEG_SAMPLERS = ("joint", "uniform", "local_joint", "in_batch")
+
+
+def lp_loss_ex(hu, hv, hn, rel, K: int, group: int, mode: int, loss_kind: int = 0, w=None):
+    """General LP score + loss (oracle_lp_loss_ex): mode 0 = sampled negatives shared by
+    `group` positives (hn rows), mode 1 = in-batch (K = B-1, hn unused); rel None = dot
+    product (Eq. 2); loss_kind 2 = weighted CE with per-positive weights w."""
+    hu, hv = _c(hu, np.float64), _c(hv, np.float64)
+    B, d = hu.shape
+    hn = _c(hn, np.float64) if mode == 0 else None
+    n_hn = hn.shape[0] if hn is not None else 0
+    rel = _c(rel, np.float64) if rel is not None else None
+    w = _c(w, np.float64) if w is not None else None
+    scores = np.zeros((B, K + 1))
+    dhu, dhv = np.zeros_like(hu), np.zeros_like(hv)
+    dhn = np.zeros((n_hn, d)) if hn is not None else None
+    drel = np.zeros(d) if rel is not None else None
+    loss = lib().oracle_lp_loss_ex(B, K, group, mode, d, _p(hu), _p(hv), _p(hn), n_hn, _p(rel), loss_kind, _p(w),
+                                   _p(scores), _p(dhu), _p(dhv), _p(dhn), _p(drel))
+    return loss, scores, dhu, dhv, dhn, drel
+
+
 def adam(p, g, m, v, lr, t, b1=0.9, b2=0.999, eps=1e-8):
     """In place on float64 arrays p, m, v."""
     g = _c(g, np.float64)
@@ -412,12 +445,34 @@ def lp_seeds(u: np.ndarray, v: np.ndarray, neg: np.ndarray) -> np.ndarray:
 
 
 def lp_step(g: Graph, params: Dict[str, np.ndarray], u: np.ndarray, v: np.ndarray, step: int,
-            rng_seed: int, loss_kind: int = 0) -> StepResult:
+            rng_seed: int, loss_kind: int = 0, neg_sampler: str = "joint", score: str = "distmult",
+            local_range=None, w=None, pos_base: int = 0, group_base: int = 0) -> StepResult:
+    """One LP step (§8(a) a3', a9, a10) in the paper's order.  neg_sampler (App. A.2.1):
+    joint / uniform / local_joint (joint draws over local_range = (first local id, count) of
+    the dst type) / in_batch; score: distmult (Eq. 3) or dot (Eq. 2); loss_kind 2 uses the
+    per-positive weights w (Eq. 5)."""
     cfg = g.cfg
     L = len(cfg.fanouts)
     et = cfg.etypes[cfg.lp_etype]
+    B = len(u)
     K = cfg.num_neg
-    neg = joint_negatives(len(u), K, cfg.counts[et.dst], int(g.node_off[et.dst]), rng_seed, step)
+    base, n_dst = int(g.node_off[et.dst]), int(cfg.counts[et.dst])
+    if neg_sampler == "joint":
+        neg = joint_negatives(B, K, n_dst, base, rng_seed, step, group_base)
+        mode, group = 0, K
+    elif neg_sampler == "local_joint":
+        lo, cnt = local_range if local_range is not None else (0, n_dst)
+        neg = joint_negatives(B, K, cnt, base + lo, rng_seed, step, group_base)
+        mode, group = 0, K
+    elif neg_sampler == "uniform":
+        neg = uniform_negatives(B, K, n_dst, base, rng_seed, step, pos_base)
+        mode, group = 0, 1
+    elif neg_sampler == "in_batch":
+        neg = np.zeros(0, np.int64)
+        K = B - 1
+        mode, group = 1, 1
+    else:
+        raise ValueError(neg_sampler)
     seeds = lp_seeds(u, v, neg)
     blocks = sample_blocks(g, seeds, cfg.fanouts, rng_seed, step, u, v, cfg.lp_etype, cfg.lp_rev_etype)
     x0 = gather(g, blocks[0].src_gid)
@@ -431,12 +486,15 @@ def lp_step(g: Graph, params: Dict[str, np.ndarray], u: np.ndarray, v: np.ndarra
     iu = np.searchsorted(seeds, u)
     iv = np.searchsorted(seeds, v)
     ineg = np.searchsorted(seeds, neg)
-    loss, scores, dhu, dhv, dhn, drel = lp_loss(h[iu], h[iv], h[ineg], params["rel"], K, loss_kind)
+    rel = params["rel"] if score == "distmult" else None
+    loss, scores, dhu, dhv, dhn, drel = lp_loss_ex(h[iu], h[iv], h[ineg] if mode == 0 else None, rel, K, group,
+                                                   mode, loss_kind, w)
     dh = np.zeros_like(h)
     np.add.at(dh, iu, dhu)
     np.add.at(dh, iv, dhv)
-    np.add.at(dh, ineg, dhn)
-    grads = {"rel": drel}
+    if mode == 0:
+        np.add.at(dh, ineg, dhn)
+    grads = {"rel": drel} if rel is not None else {}
     dhs = [None] * L
     for l in reversed(range(L)):
         dhs[l] = dh

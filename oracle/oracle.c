@@ -537,40 +537,71 @@ int64_t oracle_joint_negatives(int64_t n_pos, int32_t K, int64_t n_dst_nodes, in
 }
 
 /* ======================================================================================
- * 9. DistMult score (Eq. 3) and LP losses (App. A.2):
- *    pos_i = sum_k hu_i[k] rel[k] hv_i[k] ; neg_ij = sum_k hu_i[k] rel[k] hn_{g(i),j}[k]
+ * 8b. Uniform negative sampling (App. A.2.1): every positive i draws K nodes of
+ *     dst_t uniformly (iid, with replacement): N*K draws in total.  Draw j of positive p =
+ *     pos_base + i uses counter (p lo, p hi, 0xFFE00000 | j, step) (R-rng; etype id 0xFFE
+ *     is reserved for uniform negatives as 0xFFF is for joint ones).
+ *     neg[i*K + j] = gid_base + index.
+ *     Local joint negative sampling is joint sampling with gid_base / n_dst_nodes
+ *     restricted to the local partition's range of dst_t: no separate routine.
+ *     In-batch negative sampling draws nothing (see oracle_lp_loss_ex, mode 1).
+ * ==================================================================================== */
+int64_t oracle_uniform_negatives(int64_t n_pos, int32_t K, int64_t n_dst_nodes, int64_t gid_base,
+                                 uint64_t seed, uint32_t step, int64_t pos_base, int64_t* neg) {
+    for (int64_t i = 0; i < n_pos; ++i) {
+        int64_t p = pos_base + i;
+        for (int32_t j = 0; j < K; ++j) {
+            uint64_t x = oracle_keyed_u64(seed, (uint32_t)(uint64_t)p, (uint32_t)((uint64_t)p >> 32),
+                                          0xFFE00000u | ((uint32_t)j & 0xFFFFu), step);
+            neg[i * K + j] = gid_base + (int64_t)oracle_unif_index(x, (uint64_t)n_dst_nodes);
+        }
+    }
+    return n_pos * K;
+}
+
+/* ======================================================================================
+ * 9. Link-prediction score (App. A.1) and losses (App. A.2):
+ *    score(u, x) = sum_k u[k] rel[k] x[k]   DistMult, Eq. 3
+ *                = sum_k u[k] x[k]          dot product, Eq. 2, rel == NULL
+ *    Positive i scores (hu_i, hv_i); its K negatives replace the destination:
+ *      mode 0 (sampled negatives, shared by groups of `group` positives): negative j of
+ *             positive i is hn row (i / group) * K + j.  Joint / local joint: group = K
+ *             (P:L356-357); uniform: group = 1.
+ *      mode 1 (in-batch): the negatives of positive i are the destinations of the
+ *             other positives, in batch order: j -> hv row (j < i ? j : j + 1); K = B - 1.
  *    loss_kind 0: contrastive Eq. 7: l_i = -log(exp(pos_i)/sum_{all 1+K} exp(s))
  *    loss_kind 1: cross entropy Eq. 4 (garbled; R-ce): per edge
  *       -[y ln sigma(s) + (1-y) ln(1 - sigma(s))], mean over the 1+K edges, then over i.
+ *    loss_kind 2: weighted cross entropy Eq. 5 (R-wce): as 1 with the positive
+ *       edge's term multiplied by its weight w[i]; negatives weigh 1.
  *    Batch mean over positives (R-lpmean).  scores[i*(1+K)+0] = pos, [1+j] = neg_ij.
- *    Gradients: dhu (B,d), dhv (B,d), dhn (G*K,d) (negatives accumulate over the group),
- *    drel (d).
+ *    Gradients: dhu (B,d), dhv (B,d), dhn (rows of hn, d; mode 0 only; a row accumulates
+ *    over the positives that share it), drel (d; DistMult only).
  * ==================================================================================== */
 static double log_sigmoid(double s) { return s >= 0 ? -log1p(exp(-s)) : s - log1p(exp(s)); }
 static double sigmoid(double s) { return s >= 0 ? 1.0 / (1.0 + exp(-s)) : exp(s) / (1.0 + exp(s)); }
 
-double oracle_lp_loss(int64_t B, int32_t K, int32_t d, const double* hu, const double* hv, const double* hn,
-                      const double* rel, int32_t loss_kind, double* scores,
-                      double* dhu, double* dhv, double* dhn, double* drel) {
-    int64_t G = (B + K - 1) / K;
+double oracle_lp_loss_ex(int64_t B, int32_t K, int32_t group, int32_t mode, int32_t d, const double* hu,
+                         const double* hv, const double* hn, int64_t n_hn, const double* rel, int32_t loss_kind,
+                         const double* w, double* scores, double* dhu, double* dhv, double* dhn, double* drel) {
     double loss = 0.0;
     double* ds = (double*)malloc(sizeof(double) * (size_t)(K + 1));
     memset(dhu, 0, sizeof(double) * (size_t)(B * d));
     memset(dhv, 0, sizeof(double) * (size_t)(B * d));
-    memset(dhn, 0, sizeof(double) * (size_t)(G * K * d));
-    memset(drel, 0, sizeof(double) * (size_t)d);
+    if (dhn) memset(dhn, 0, sizeof(double) * (size_t)(n_hn * d));
+    if (drel) memset(drel, 0, sizeof(double) * (size_t)d);
     for (int64_t i = 0; i < B; ++i) {
-        int64_t g = i / K;
         double* sc = scores + (size_t)i * (K + 1);
         const double* u = hu + (size_t)i * d;
         const double* v = hv + (size_t)i * d;
         double s = 0.0;
-        for (int32_t k = 0; k < d; ++k) s += u[k] * rel[k] * v[k];
+        for (int32_t k = 0; k < d; ++k) s += u[k] * (rel ? rel[k] : 1.0) * v[k];
         sc[0] = s;
         for (int32_t j = 0; j < K; ++j) {
-            const double* nn = hn + ((size_t)g * K + j) * d;
+            const double* nn = mode == 0 ? hn + ((size_t)(i / group) * K + j) * d
+                                         : hv + (size_t)(j < i ? j : j + 1) * d;
             double t = 0.0;
-            for (int32_t k = 0; k < d; ++k) t += u[k] * rel[k] * nn[k];
+            for (int32_t k = 0; k < d; ++k) t += u[k] * (rel ? rel[k] : 1.0) * nn[k];
             sc[1 + j] = t;
         }
         if (loss_kind == 0) {
@@ -582,8 +613,9 @@ double oracle_lp_loss(int64_t B, int32_t K, int32_t d, const double* hu, const d
             loss += lse - sc[0];
             for (int32_t j = 0; j <= K; ++j) ds[j] = (exp(sc[j] - lse) - (j == 0 ? 1.0 : 0.0)) / (double)B;
         } else {
-            double li = -log_sigmoid(sc[0]);
-            ds[0] = (sigmoid(sc[0]) - 1.0) / (double)(K + 1) / (double)B;
+            double wi = (loss_kind == 2) ? w[i] : 1.0;
+            double li = -wi * log_sigmoid(sc[0]);
+            ds[0] = wi * (sigmoid(sc[0]) - 1.0) / (double)(K + 1) / (double)B;
             for (int32_t j = 1; j <= K; ++j) {
                 li += -log_sigmoid(-sc[j]);
                 ds[j] = sigmoid(sc[j]) / (double)(K + 1) / (double)B;
@@ -592,22 +624,39 @@ double oracle_lp_loss(int64_t B, int32_t K, int32_t d, const double* hu, const d
         }
         /* chain rule through s = sum_k u r x */
         for (int32_t k = 0; k < d; ++k) {
-            dhu[(size_t)i * d + k] += ds[0] * rel[k] * v[k];
-            dhv[(size_t)i * d + k] += ds[0] * u[k] * rel[k];
-            drel[k] += ds[0] * u[k] * v[k];
+            double r = rel ? rel[k] : 1.0;
+            dhu[(size_t)i * d + k] += ds[0] * r * v[k];
+            dhv[(size_t)i * d + k] += ds[0] * u[k] * r;
+            if (drel) drel[k] += ds[0] * u[k] * v[k];
         }
         for (int32_t j = 0; j < K; ++j) {
-            const double* nn = hn + ((size_t)g * K + j) * d;
-            double* dn = dhn + ((size_t)g * K + j) * d;
+            const double* nn;
+            double* dn;
+            if (mode == 0) {
+                nn = hn + ((size_t)(i / group) * K + j) * d;
+                dn = dhn + ((size_t)(i / group) * K + j) * d;
+            } else {
+                nn = hv + (size_t)(j < i ? j : j + 1) * d;
+                dn = dhv + (size_t)(j < i ? j : j + 1) * d;
+            }
             for (int32_t k = 0; k < d; ++k) {
-                dhu[(size_t)i * d + k] += ds[1 + j] * rel[k] * nn[k];
-                dn[k] += ds[1 + j] * u[k] * rel[k];
-                drel[k] += ds[1 + j] * u[k] * nn[k];
+                double r = rel ? rel[k] : 1.0;
+                dhu[(size_t)i * d + k] += ds[1 + j] * r * nn[k];
+                dn[k] += ds[1 + j] * u[k] * r;
+                if (drel) drel[k] += ds[1 + j] * u[k] * nn[k];
             }
         }
     }
     free(ds);
     return loss / (double)B;
+}
+
+/* Joint negatives + DistMult (the §8(a) a10 default): oracle_lp_loss_ex with group = K. */
+double oracle_lp_loss(int64_t B, int32_t K, int32_t d, const double* hu, const double* hv, const double* hn,
+                      const double* rel, int32_t loss_kind, double* scores,
+                      double* dhu, double* dhv, double* dhn, double* drel) {
+    int64_t G = (B + K - 1) / K;
+    return oracle_lp_loss_ex(B, K, K, 0, d, hu, hv, hn, G * K, rel, loss_kind, NULL, scores, dhu, dhv, dhn, drel);
 }
 
 /* ======================================================================================
