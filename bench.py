@@ -42,6 +42,9 @@ def parse():
                     help="feature storage type; compute stays fp32 (auto: bf16 for the large configs, as "
                          "SURVEY §8(d) plans, fp32 for tiny)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--neg", default="joint", choices=["joint", "uniform", "local_joint", "in_batch"],
+                    help="LP negative sampler (App. A.2.1)")
+    ap.add_argument("--score", default="distmult", choices=["distmult", "dot"], help="LP score function (App. A.1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--profile-steps", type=int, default=20)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
@@ -67,8 +70,18 @@ def config_for(name: str) -> synth.Config:
     return synth.get(name)
 
 
+LP_OPTS = {"neg": "joint", "score": "distmult"}
+
+
+def lp_task(cfg: synth.Config) -> str:
+    neg = LP_OPTS["neg"]
+    negs = "in-batch" if neg == "in_batch" else f"{neg.replace('_', '-')}-{cfg.num_neg}"
+    score = "DistMult" if LP_OPTS["score"] == "distmult" else "dot-product"
+    return f"RGCN + {score} LP train step ({negs} negatives, contrastive)"
+
+
 def cfg_json(cfg: synth.Config, n_gpus: int, extra=None) -> dict:
-    task = "RGCN NC train step" if cfg.task == "nc" else f"RGCN + DistMult LP train step (joint-{cfg.num_neg} negatives, contrastive)"
+    task = "RGCN NC train step" if cfg.task == "nc" else lp_task(cfg)
     d = {"workload": f"{cfg.name}-shaped synthetic heterograph, {task}",
          "ntypes": cfg.num_ntypes, "etypes": cfg.num_etypes, "nodes": cfg.num_nodes, "edges": cfg.num_edges,
          "feat_dim": cfg.feat_dim, "fanouts": cfg.fanouts, "batch_per_gpu": cfg.batch,
@@ -256,8 +269,17 @@ def build_gsb(cfg, device, partition=None, mode="peer"):
             st.feat_dtype = tdt
     torch.cuda.synchronize()
     if cfg.task == "lp":
+        local = None
+        if LP_OPTS["neg"] == "local_joint" and partition is not None:
+            from paper_2406_06022_b200.dist import balanced_bounds
+            world, rank = partition
+            dt = cfg.etypes[cfg.lp_etype].dst
+            b = balanced_bounds(cfg.counts, world)
+            local = (int(b[dt][rank]), int(b[dt][rank + 1] - b[dt][rank]))
+        names = [k for k in synth.param_order(cfg) if LP_OPTS["score"] == "distmult" or k != "rel"]
         tr = LPTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_neg, cfg.lp_etype, cfg.lp_rev_etype,
-                       synth.init_params(cfg), synth.param_order(cfg), lr=cfg.lr, rng_seed=cfg.rng_seed)
+                       {k: v for k, v in synth.init_params(cfg).items() if k in names}, names, lr=cfg.lr,
+                       rng_seed=cfg.rng_seed, neg_sampler=LP_OPTS["neg"], score=LP_OPTS["score"], local_range=local)
     else:
         tr = RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
                          synth.param_order(cfg), synth.labels(cfg, backend="torch", device=device),
@@ -512,7 +534,7 @@ def run_gsb(args, cfg):
                     f"NCCL grad all-reduce",
         "replicate": f"dp{ws}: graph + features replicated, NCCL grad all-reduce"}[args.features])
     unit = UNIT if cfg.task == "nc" else "pos_edges/s"
-    metric = METRIC if cfg.task == "nc" else "RGCN+DistMult LP train positive edges/sec (joint negatives) on B200"
+    metric = METRIC if cfg.task == "nc" else "RGCN LP train positive edges/sec on B200"
     line = {
         "metric": metric, "value": seeds_per_s, "unit": unit, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -603,6 +625,7 @@ def run_reference(args, cfg):
 def main():
     args = parse()
     cfg = config_for(args.config)
+    LP_OPTS.update(neg=args.neg, score=args.score)
     fd = args.feat_dtype
     if fd == "auto":
         fd = cfg.feat_dtype if cfg.name in ("tiny", "tiny_lp") or cfg.feat_dtype == "bf16" else "bf16"

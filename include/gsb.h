@@ -289,6 +289,16 @@ gsb_status gsb_joint_negatives(int64_t n_pos, int32_t K, int64_t n_dst_nodes, in
                                uint32_t step, const uint32_t* step_dev, int64_t group_base, int64_t* neg,
                                void* stream);
 
+/* Uniform negative sampling (App. A.2.1): every positive draws K
+ * iid uniform nodes of the dst type: neg[i*K + j] = gid_base + unif(Philox(pos_base + i,
+ * 0xFFE00000 | j, step), n_dst_nodes) (R-rng).  neg: device int64 [n_pos*K].
+ * Local joint negative sampling is gsb_joint_negatives over the local partition's
+ * range of the dst type (gid_base = first local gid, n_dst_nodes = local count).
+ * In-batch negative sampling draws nothing: gsb_lp_score_ex neg_mode 1. */
+gsb_status gsb_uniform_negatives(int64_t n_pos, int32_t K, int64_t n_dst_nodes, int64_t gid_base, uint64_t rng_seed,
+                                 uint32_t step, const uint32_t* step_dev, int64_t pos_base, int64_t* neg,
+                                 void* stream);
+
 /* LP seed set (§8(a) a9): seeds = ascending unique(u ∪ v ∪ neg); iu/iv/ineg = row of
  * each u / v / neg in seeds.  seeds capacity 2*B + n_neg; *n_seeds_dev (device int64)
  * receives the count.  ws: device scratch of gsb_lp_seeds_bytes. */
@@ -306,6 +316,24 @@ gsb_status gsb_lp_seeds(const int64_t* u, const int64_t* v, int64_t B, const int
 gsb_status gsb_lp_score(const float* H, int64_t n_rows_cap, int32_t d, const int32_t* iu, const int32_t* iv,
                         const int32_t* ineg, int64_t B, int32_t K, const float* rel, int32_t loss_kind, float* scores,
                         float* row_loss_ws, float* loss, float* dH, float* drel, void* stream);
+
+/* General LP score + loss (App. A).  Negative j of positive i is
+ *   neg_mode 0 (sampled): row ineg[(i / group) * K + j]   (joint / local joint: group = K;
+ *                          uniform: group = 1)
+ *   neg_mode 1 (in-batch): row iv[j < i ? j : j + 1], K = B - 1 (ineg unused).
+ * rel: DistMult relation vector (Eq. 3) or NULL for the dot product (Eq. 2; drel unused).
+ * loss_kind 0 contrastive (Eq. 7), 1 cross entropy (Eq. 4, R-ce), 2 weighted cross entropy
+ * (Eq. 5, R-wce): positive i's term times w[i] (device fp32 [B]); negatives weigh 1.
+ * Other arguments and outputs as gsb_lp_score; scores: [B][1+K].
+ * In-batch with B a multiple of 32 runs as dense contractions on the tensor cores:
+ * S = (H[iu] o rel) H[iv]^T (B x B), the loss row-wise on S, then dS H[iv] and
+ * dS^T (H[iu] o rel) (gsb_gemm, 3xTF32); ws: device scratch of gsb_lp_score_ws_bytes
+ * (0 bytes otherwise; then ws may be NULL). */
+gsb_status gsb_lp_score_ws_bytes(int64_t B, int32_t d, int32_t neg_mode, size_t* bytes);
+gsb_status gsb_lp_score_ex(const float* H, int64_t n_rows_cap, int32_t d, const int32_t* iu, const int32_t* iv,
+                           const int32_t* ineg, int64_t B, int32_t K, int32_t group, int32_t neg_mode,
+                           const float* rel, int32_t loss_kind, const float* w, float* scores, float* row_loss_ws,
+                           float* loss, float* dH, float* drel, void* ws, size_t ws_bytes, void* stream);
 
 /* ======================================================================================
  * Partitioned feature store across GPUs (§8(e); P:L86 distributed tensors, P:L90 random

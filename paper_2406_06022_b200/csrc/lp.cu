@@ -9,14 +9,16 @@
 
 namespace gsb {
 
+// Draw i = (key k = key_base + i / K, j = i % K): joint negatives key by group (tag 0xFFF),
+// uniform negatives by positive (tag 0xFFE); R-rng.
 __global__ void joint_neg_kernel(int64_t total, int K, int64_t n_nodes, int64_t base, uint64_t seed, uint32_t step_host,
-                                 const uint32_t* __restrict__ step_dev, int64_t group_base, int64_t* __restrict__ neg) {
+                                 const uint32_t* __restrict__ step_dev, int64_t group_base, int64_t* __restrict__ neg,
+                                 uint32_t tag) {
     const uint32_t step = step_dev ? *step_dev : step_host;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t g = group_base + i / K;
         const uint32_t j = (uint32_t)(i % K);
-        uint64_t x = keyed_u64(seed, (uint32_t)(uint64_t)g, (uint32_t)((uint64_t)g >> 32), 0xFFF00000u | (j & 0xFFFFu),
-                               step);
+        uint64_t x = keyed_u64(seed, (uint32_t)(uint64_t)g, (uint32_t)((uint64_t)g >> 32), tag | (j & 0xFFFFu), step);
         neg[i] = base + (int64_t)__umul64hi(x, (uint64_t)n_nodes);
     }
 }
@@ -62,7 +64,8 @@ __device__ __forceinline__ float sigm(float x) { return x >= 0.f ? 1.f / (1.f + 
 __global__ void __launch_bounds__(256) lp_score_kernel(const float* __restrict__ H, int d,
                                                        const int32_t* __restrict__ iu, const int32_t* __restrict__ iv,
                                                        const int32_t* __restrict__ ineg, int64_t B, int K,
-                                                       const float* __restrict__ rel, int kind,
+                                                       int group, int mode, const float* __restrict__ rel, int kind,
+                                                       const float* __restrict__ wpos,
                                                        float* __restrict__ scores, float* __restrict__ row_loss,
                                                        float* __restrict__ dH, float* __restrict__ drel) {
     extern __shared__ float s_drel[];
@@ -74,13 +77,17 @@ __global__ void __launch_bounds__(256) lp_score_kernel(const float* __restrict__
 #pragma unroll
     for (int q = 0; q < kMaxC4; ++q) {
         int c = lane + 32 * q;
-        r[q] = (c < d4) ? __ldg(reinterpret_cast<const float4*>(rel) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        r[q] = (c >= d4) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                         : (rel ? __ldg(reinterpret_cast<const float4*>(rel) + c) : make_float4(1.f, 1.f, 1.f, 1.f));
         dr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const float invB = 1.f / (float)B;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < B; i += warps) {
-        const int64_t g = i / K;
+        // row of negative j of positive i: sampled (mode 0, shared by `group` positives) or the
+        // destination of another positive of the batch (mode 1, in-batch)
+        const int64_t nb = (i / group) * K;
+        auto neg_row = [&](int j) -> int64_t { return mode == 0 ? ineg[nb + j] : iv[j < i ? j : j + 1]; };
         const float* hu = H + (int64_t)iu[i] * d;
         const float* hv = H + (int64_t)iv[i] * d;
         float4 u[kMaxC4], ur[kMaxC4];
@@ -101,9 +108,10 @@ __global__ void __launch_bounds__(256) lp_score_kernel(const float* __restrict__
         float* sc = scores + i * (K + 1);
         if (lane == 0) sc[0] = s0;
         // pass 1: negative scores, online max / sum-exp (contrastive) or BCE sum (CE)
-        float mx = s0, se = 1.f, lsum = softplus(-s0);
+        const float wi = (kind == 2) ? wpos[i] : 1.f;
+        float mx = s0, se = 1.f, lsum = wi * softplus(-s0);
         for (int j = 0; j < K; ++j) {
-            const float* hn = H + (int64_t)ineg[g * K + j] * d;
+            const float* hn = H + neg_row(j) * d;
             float s = 0.f;
 #pragma unroll
             for (int q = 0; q < kMaxC4; ++q) {
@@ -128,7 +136,7 @@ __global__ void __launch_bounds__(256) lp_score_kernel(const float* __restrict__
         __syncwarp();
         // pass 2: gradients.  ds_j = dloss/dscore_j
         float4 du[kMaxC4];
-        const float ds0 = (kind == 0) ? (expf(s0 - lse) - 1.f) * invB : (sigm(s0) - 1.f) / (float)(K + 1) * invB;
+        const float ds0 = (kind == 0) ? (expf(s0 - lse) - 1.f) * invB : wi * (sigm(s0) - 1.f) / (float)(K + 1) * invB;
         float* dv = dH + (int64_t)iv[i] * d;
 #pragma unroll
         for (int q = 0; q < kMaxC4; ++q) {
@@ -145,7 +153,7 @@ __global__ void __launch_bounds__(256) lp_score_kernel(const float* __restrict__
         for (int j = 0; j < K; ++j) {
             const float s = sc[1 + j];
             const float ds = (kind == 0) ? expf(s - lse) * invB : sigm(s) / (float)(K + 1) * invB;
-            const int64_t row = ineg[g * K + j];
+            const int64_t row = neg_row(j);
             const float* hn = H + row * d;
             float* dn = dH + row * d;
 #pragma unroll
@@ -179,7 +187,8 @@ __global__ void __launch_bounds__(256) lp_score_kernel(const float* __restrict__
         }
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(drel + c, s_drel[c]);
+    if (rel)
+        for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(drel + c, s_drel[c]);
 }
 
 __global__ void __launch_bounds__(1024) lp_mean_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
@@ -195,6 +204,98 @@ __global__ void __launch_bounds__(1024) lp_mean_kernel(const float* __restrict__
         if (threadIdx.x == 0) *out = s / (float)n;
     }
 }
+
+
+// ------------------------------------------------------------------------------------
+// In-batch negatives as dense contractions (App. A.2.1): with U = H[iu], V = H[iv]
+// and Ur = U o r, every score of the batch is S = Ur V^T (B x B; S_ii the positive, row i's
+// other entries its B-1 negatives in batch order).  Backward: M = dS V, dU = M o r,
+// drel = sum_i U_i o M_i, dV = dS^T Ur.  The three products run on the tcgen05 3xTF32 GEMM
+// (gsb_gemm); these kernels do the row-wise loss and the gathers / scatters.
+// ------------------------------------------------------------------------------------
+__global__ void ib_gather_kernel(const float* __restrict__ H, int d, const int32_t* __restrict__ iu,
+                                 const int32_t* __restrict__ iv, int64_t B, const float* __restrict__ rel,
+                                 float* __restrict__ U, float* __restrict__ V, float* __restrict__ Ur) {
+    const int d4 = d >> 2;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < B * d4; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = x / d4;
+        const int c = (int)(x % d4);
+        const float4 u = reinterpret_cast<const float4*>(H + (int64_t)iu[i] * d)[c];
+        const float4 v = reinterpret_cast<const float4*>(H + (int64_t)iv[i] * d)[c];
+        const float4 r = rel ? reinterpret_cast<const float4*>(rel)[c] : make_float4(1.f, 1.f, 1.f, 1.f);
+        reinterpret_cast<float4*>(U)[x] = u;
+        reinterpret_cast<float4*>(V)[x] = v;
+        reinterpret_cast<float4*>(Ur)[x] = make_float4(u.x * r.x, u.y * r.y, u.z * r.z, u.w * r.w);
+    }
+}
+
+// warp per row i of S: loss_i, scores row [S_ii, S_i0 .. (skipping i) .. S_i,B-1], dS row in place
+__global__ void __launch_bounds__(256) ib_rows_kernel(float* __restrict__ S, int64_t B, int kind,
+                                                      const float* __restrict__ wpos, float* __restrict__ scores,
+                                                      float* __restrict__ row_loss) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const float invB = 1.f / (float)B;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < B; i += warps) {
+        float* row = S + i * B;
+        float* sc = scores + i * B;
+        const float s0 = row[i];
+        float mx = -INFINITY, lsum = 0.f;
+        const float wi = (kind == 2) ? wpos[i] : 1.f;
+        for (int64_t j = lane; j < B; j += 32) {
+            const float x = row[j];
+            mx = fmaxf(mx, x);
+            lsum += (j == i) ? wi * softplus(-x) : softplus(x);
+            sc[j < i ? j + 1 : (j == i ? 0 : j)] = x;
+        }
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float se = 0.f;
+        for (int64_t j = lane; j < B; j += 32) se += expf(row[j] - mx);
+        se = warp_sum(se);
+        lsum = warp_sum(lsum);
+        const float lse = mx + logf(se);
+        if (lane == 0) row_loss[i] = (kind == 0) ? (lse - s0) : lsum / (float)B;
+        for (int64_t j = lane; j < B; j += 32) {
+            const float x = row[j];
+            float g;
+            if (kind == 0) g = (expf(x - lse) - (j == i ? 1.f : 0.f)) * invB;
+            else g = (j == i ? wi * (sigm(x) - 1.f) : sigm(x)) / (float)B * invB;
+            row[j] = g;
+        }
+    }
+}
+
+// dU = M o r scattered to dH[iu], dV scattered to dH[iv], drel = sum_i U_i o M_i
+__global__ void __launch_bounds__(256) ib_finish_kernel(const float* __restrict__ U, const float* __restrict__ M,
+                                                        const float* __restrict__ dV, const int32_t* __restrict__ iu,
+                                                        const int32_t* __restrict__ iv, int64_t B, int d,
+                                                        const float* __restrict__ rel, float* __restrict__ dH,
+                                                        float* __restrict__ drel) {
+    extern __shared__ float s_dr[];
+    for (int c = threadIdx.x; c < d; c += blockDim.x) s_dr[c] = 0.f;
+    __syncthreads();
+    const int d4 = d >> 2;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < B * d4; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = x / d4;
+        const int c = (int)(x % d4);
+        const float4 m = reinterpret_cast<const float4*>(M)[x];
+        const float4 r = rel ? reinterpret_cast<const float4*>(rel)[c] : make_float4(1.f, 1.f, 1.f, 1.f);
+        red_add_f4(dH + (int64_t)iu[i] * d + 4 * c, make_float4(m.x * r.x, m.y * r.y, m.z * r.z, m.w * r.w));
+        red_add_f4(dH + (int64_t)iv[i] * d + 4 * c, reinterpret_cast<const float4*>(dV)[x]);
+        if (rel) {
+            const float4 u = reinterpret_cast<const float4*>(U)[x];
+            atomicAdd(&s_dr[4 * c + 0], u.x * m.x);
+            atomicAdd(&s_dr[4 * c + 1], u.y * m.y);
+            atomicAdd(&s_dr[4 * c + 2], u.z * m.z);
+            atomicAdd(&s_dr[4 * c + 3], u.w * m.w);
+        }
+    }
+    __syncthreads();
+    if (rel)
+        for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(drel + c, s_dr[c]);
+}
+
+static bool inbatch_gemm_ok(int64_t B) { return B % 32 == 0 && B >= 32; }
 
 static size_t lp_cub_bytes(int64_t n) {
     size_t a = 0, b = 0;
@@ -215,7 +316,17 @@ gsb_status gsb_joint_negatives(int64_t n_pos, int32_t K, int64_t n_dst_nodes, in
     GSB_CHECK_ARG(neg && n_pos >= 1 && K >= 1 && K <= 0xFFFF && n_dst_nodes >= 1, "bad argument");
     const int64_t total = ceil_div(n_pos, K) * K;
     GSB_LAUNCH("joint_negatives", joint_neg_kernel, grid_for(total, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream,
-               total, K, n_dst_nodes, gid_base, rng_seed, step, step_dev, group_base, neg);
+               total, K, n_dst_nodes, gid_base, rng_seed, step, step_dev, group_base, neg, 0xFFF00000u);
+    return GSB_OK;
+}
+
+gsb_status gsb_uniform_negatives(int64_t n_pos, int32_t K, int64_t n_dst_nodes, int64_t gid_base, uint64_t rng_seed,
+                                 uint32_t step, const uint32_t* step_dev, int64_t pos_base, int64_t* neg,
+                                 void* stream) {
+    GSB_CHECK_ARG(neg && n_pos >= 1 && K >= 1 && K <= 0xFFFF && n_dst_nodes >= 1, "bad argument");
+    const int64_t total = n_pos * K;
+    GSB_LAUNCH("uniform_negatives", joint_neg_kernel, grid_for(total, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream,
+               total, K, n_dst_nodes, gid_base, rng_seed, step, step_dev, pos_base, neg, 0xFFE00000u);
     return GSB_OK;
 }
 
@@ -254,20 +365,71 @@ gsb_status gsb_lp_seeds(const int64_t* u, const int64_t* v, int64_t B, const int
     return GSB_OK;
 }
 
+gsb_status gsb_lp_score_ws_bytes(int64_t B, int32_t d, int32_t neg_mode, size_t* bytes) {
+    GSB_CHECK_ARG(bytes && B >= 1 && d > 0, "bad argument");
+    *bytes = (neg_mode == 1 && inbatch_gemm_ok(B))
+                 ? sizeof(float) * (size_t)(5 * B * (int64_t)d + B * B) : 0;
+    return GSB_OK;
+}
+
+gsb_status gsb_lp_score_ex(const float* H, int64_t n_rows_cap, int32_t d, const int32_t* iu, const int32_t* iv,
+                           const int32_t* ineg, int64_t B, int32_t K, int32_t group, int32_t neg_mode,
+                           const float* rel, int32_t loss_kind, const float* w, float* scores, float* row_loss_ws,
+                           float* loss, float* dH, float* drel, void* ws, size_t ws_bytes, void* stream) {
+    GSB_CHECK_ARG(H && iu && iv && scores && row_loss_ws && loss && dH, "null argument");
+    GSB_CHECK_ARG(d > 0 && d % 4 == 0 && d <= 4 * 32 * kMaxC4, "d %d must be a multiple of 4 and <= %d", d,
+                  4 * 32 * kMaxC4);
+    GSB_CHECK_ARG(B >= 1 && K >= 1 && loss_kind >= 0 && loss_kind <= 2, "bad B/K/loss_kind");
+    GSB_CHECK_ARG(neg_mode == 0 || neg_mode == 1, "neg_mode must be 0 (sampled) or 1 (in-batch)");
+    GSB_CHECK_ARG(neg_mode == 1 || (ineg && group >= 1), "sampled negatives need ineg and group >= 1");
+    GSB_CHECK_ARG(neg_mode == 0 || K == B - 1, "in-batch negatives need K = B - 1 (K %d, B %lld)", K, (long long)B);
+    GSB_CHECK_ARG(!rel || drel, "DistMult needs drel");
+    GSB_CHECK_ARG(loss_kind != 2 || w, "weighted cross entropy needs w");
+    size_t need = 0;
+    gsb_lp_score_ws_bytes(B, d, neg_mode, &need);
+    if (ws_bytes < need || (need && !ws)) {
+        set_error("lp_score workspace %zu < %zu", ws_bytes, need);
+        return GSB_EWORKSPACE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    GSB_CUDA(cudaMemsetAsync(dH, 0, sizeof(float) * (size_t)n_rows_cap * d, s));
+    if (rel) GSB_CUDA(cudaMemsetAsync(drel, 0, sizeof(float) * (size_t)d, s));
+    if (need) {   // in-batch on the tensor cores
+        float* U = (float*)ws;
+        float* V = U + B * d;
+        float* Ur = V + B * d;
+        float* M = Ur + B * d;
+        float* dV = M + B * d;
+        float* S = dV + B * d;
+        const int64_t n4 = B * (d / 4);
+        GSB_LAUNCH("lp_ib_gather", ib_gather_kernel, grid_for(n4, 256, kNumSMs * 8), 256, 0, s, H, d, iu, iv, B, rel,
+                   U, V, Ur);
+        gsb_status st = gsb_gemm(1, Ur, d, V, d, B, d, (int32_t)B, S, B, s);          // S = Ur V^T
+        if (st != GSB_OK) return st;
+        GSB_LAUNCH("lp_ib_rows", ib_rows_kernel, grid_for(B * 32, 256, kNumSMs * 8), 256, 0, s, S, B, loss_kind, w,
+                   scores, row_loss_ws);
+        st = gsb_gemm(0, S, B, V, d, B, d, (int32_t)B, M, d, s);                     // M = dS V
+        if (st != GSB_OK) return st;
+        GSB_CUDA(cudaMemsetAsync(dV, 0, sizeof(float) * (size_t)(B * d), s));
+        st = gsb_gemm(2, S, B, Ur, d, B, d, (int32_t)B, dV, d, s);                   // dV = dS^T Ur
+        if (st != GSB_OK) return st;
+        GSB_LAUNCH("lp_ib_finish", ib_finish_kernel, grid_for(n4, 256, kNumSMs * 4), 256, sizeof(float) * d, s, U, M,
+                   dV, iu, iv, B, d, rel, dH, drel);
+    } else {
+        GSB_LAUNCH("lp_score", lp_score_kernel, grid_for(B * 32, 256, kNumSMs * 4), 256, sizeof(float) * d, s, H, d,
+                   iu, iv, ineg, B, K, neg_mode == 0 ? group : 1, neg_mode, rel, loss_kind, w, scores, row_loss_ws,
+                   dH, drel);
+    }
+    GSB_LAUNCH("lp_mean", lp_mean_kernel, 1, 1024, 0, s, row_loss_ws, B, loss);
+    return GSB_OK;
+}
+
 gsb_status gsb_lp_score(const float* H, int64_t n_rows_cap, int32_t d, const int32_t* iu, const int32_t* iv,
                         const int32_t* ineg, int64_t B, int32_t K, const float* rel, int32_t loss_kind, float* scores,
                         float* row_loss_ws, float* loss, float* dH, float* drel, void* stream) {
-    GSB_CHECK_ARG(H && iu && iv && ineg && rel && scores && row_loss_ws && loss && dH && drel, "null argument");
-    GSB_CHECK_ARG(d > 0 && d % 4 == 0 && d <= 4 * 32 * kMaxC4, "d %d must be a multiple of 4 and <= %d", d,
-                  4 * 32 * kMaxC4);
-    GSB_CHECK_ARG(B >= 1 && K >= 1 && (loss_kind == 0 || loss_kind == 1), "bad B/K/loss_kind");
-    cudaStream_t s = (cudaStream_t)stream;
-    GSB_CUDA(cudaMemsetAsync(dH, 0, sizeof(float) * (size_t)n_rows_cap * d, s));
-    GSB_CUDA(cudaMemsetAsync(drel, 0, sizeof(float) * (size_t)d, s));
-    GSB_LAUNCH("lp_score", lp_score_kernel, grid_for(B * 32, 256, kNumSMs * 4), 256, sizeof(float) * d, s, H, d, iu,
-               iv, ineg, B, K, rel, loss_kind, scores, row_loss_ws, dH, drel);
-    GSB_LAUNCH("lp_mean", lp_mean_kernel, 1, 1024, 0, s, row_loss_ws, B, loss);
-    return GSB_OK;
+    GSB_CHECK_ARG(rel && ineg && (loss_kind == 0 || loss_kind == 1), "gsb_lp_score: DistMult + joint negatives");
+    return gsb_lp_score_ex(H, n_rows_cap, d, iu, iv, ineg, B, K, K, 0, rel, loss_kind, nullptr, scores, row_loss_ws,
+                           loss, dH, drel, nullptr, 0, stream);
 }
 
 }  // extern "C"

@@ -587,15 +587,35 @@ class RGCNTrainer(_TrainerBase):
 
 
 class LPTrainer(_TrainerBase):
-    """Link prediction (§8(a) a3', a9, a10): joint negatives, target-edge exclusion,
-    RGCN encoder, DistMult + contrastive (or CE) loss.  params: W{l}, b{l}, rel."""
+    """Link prediction (§8(a) a3', a9, a10; §8(f) f2): negatives, target-edge exclusion,
+    RGCN encoder, DistMult / dot-product score, contrastive / CE / weighted CE loss.
+    params: W{l}, b{l}, rel (DistMult).
+
+    neg_sampler (App. A.2.1): "joint" (K nodes per group of K positives),
+    "uniform" (K per positive), "local_joint" (joint over local_range = (first local id,
+    count) of the dst type: this rank's partition), "in_batch" (the other positives'
+    destinations, K = B - 1, nothing drawn)."""
 
     def __init__(self, store: GraphStore, fanouts: Sequence[int], batch: int, hidden: int, num_neg: int,
                  lp_etype: int, lp_rev_etype: int, params: Dict[str, np.ndarray], param_order: Sequence[str],
-                 lr: float = 1e-3, rng_seed: int = 1, loss_kind: int = 0):
-        B, K = batch, num_neg
+                 lr: float = 1e-3, rng_seed: int = 1, loss_kind: int = 0, neg_sampler: str = "joint",
+                 score: str = "distmult", local_range=None):
+        B = batch
+        if neg_sampler not in ("joint", "uniform", "local_joint", "in_batch"):
+            raise _lib.GsbError(f"unknown negative sampler {neg_sampler!r}")
+        if score not in ("distmult", "dot"):
+            raise _lib.GsbError(f"unknown score {score!r}")
+        K = B - 1 if neg_sampler == "in_batch" else num_neg
+        self.neg_sampler, self.score = neg_sampler, score
+        self.neg_mode = 1 if neg_sampler == "in_batch" else 0
+        self.group = 1 if neg_sampler == "uniform" else K
+        if neg_sampler == "in_batch":
+            self.n_neg = 0
+        elif neg_sampler == "uniform":
+            self.n_neg = B * K
+        else:
+            self.n_neg = ((B + K - 1) // K) * K
         self.G = (B + K - 1) // K
-        self.n_neg = self.G * K
         max_seeds = 2 * B + self.n_neg
         super().__init__(store, fanouts, max_seeds, hidden, params, param_order, lr, rng_seed, max_excl=B)
         dev = store.device
@@ -605,20 +625,27 @@ class LPTrainer(_TrainerBase):
         dst_t = int(store.etype_dst[lp_etype])
         self.neg_base = int(store.node_off[dst_t])
         self.neg_n = int(store.counts[dst_t])
+        if neg_sampler == "local_joint" and local_range is not None:
+            self.neg_base += int(local_range[0])
+            self.neg_n = int(local_range[1])
         self.pos_u = torch.empty(B, dtype=torch.int64, device=dev)
         self.pos_v = torch.empty(B, dtype=torch.int64, device=dev)
-        self.neg = torch.empty(self.n_neg, dtype=torch.int64, device=dev)
+        self.neg = torch.empty(max(self.n_neg, 1), dtype=torch.int64, device=dev)
         self.seeds = torch.empty(max_seeds, dtype=torch.int64, device=dev)
         self.n_seeds = torch.zeros(1, dtype=torch.int64, device=dev)
         self.iu = torch.empty(B, dtype=torch.int32, device=dev)
         self.iv = torch.empty(B, dtype=torch.int32, device=dev)
-        self.ineg = torch.empty(self.n_neg, dtype=torch.int32, device=dev)
+        self.ineg = torch.empty(max(self.n_neg, 1), dtype=torch.int32, device=dev)
+        self.pos_w = torch.ones(B, dtype=torch.float32, device=dev)    # Eq. 5 weights (loss_kind 2)
         wb = C.c_size_t()
         call("gsb_lp_seeds_bytes", B, self.n_neg, C.byref(wb))
         self.seeds_ws = torch.empty(int(wb.value), dtype=torch.uint8, device=dev)
         self.scores = torch.empty((B, K + 1), dtype=torch.float32, device=dev)
         self.row_loss = torch.empty(B, dtype=torch.float32, device=dev)
+        call("gsb_lp_score_ws_bytes", B, hidden, self.neg_mode, C.byref(wb))
+        self.score_ws = torch.empty(max(int(wb.value), 1), dtype=torch.uint8, device=dev)
         self.group_base = 0
+        self.pos_base = 0
 
     _BUFFERED = ("sampler", "x0", "pos_u", "pos_v", "neg", "seeds", "n_seeds", "iu", "iv", "ineg", "seeds_ws")
 
@@ -630,11 +657,16 @@ class LPTrainer(_TrainerBase):
         """Joint negatives -> LP seed set -> exclusion-aware sampling (-> input rows)."""
         s = _stream(stream)
         sd = None if step_dev is None else C.c_void_p(step_dev.data_ptr())
-        call("gsb_joint_negatives", self.B, self.K, self.neg_n, self.neg_base, self.rng_seed, step, sd,
-             self.group_base, _ptr(self.neg), s)
-        call("gsb_lp_seeds", _ptr(self.pos_u), _ptr(self.pos_v), self.B, _ptr(self.neg), self.n_neg, _ptr(self.seeds),
-             _ptr(self.n_seeds), _ptr(self.iu), _ptr(self.iv), _ptr(self.ineg), _ptr(self.seeds_ws),
-             self.seeds_ws.numel(), s)
+        if self.neg_sampler in ("joint", "local_joint"):
+            call("gsb_joint_negatives", self.B, self.K, self.neg_n, self.neg_base, self.rng_seed, step, sd,
+                 self.group_base, _ptr(self.neg), s)
+        elif self.neg_sampler == "uniform":
+            call("gsb_uniform_negatives", self.B, self.K, self.neg_n, self.neg_base, self.rng_seed, step, sd,
+                 self.pos_base, _ptr(self.neg), s)
+        has_neg = self.n_neg > 0
+        call("gsb_lp_seeds", _ptr(self.pos_u), _ptr(self.pos_v), self.B, _ptr(self.neg) if has_neg else None,
+             self.n_neg, _ptr(self.seeds), _ptr(self.n_seeds), _ptr(self.iu), _ptr(self.iv),
+             _ptr(self.ineg) if has_neg else None, _ptr(self.seeds_ws), self.seeds_ws.numel(), s)
         self.sampler.sample(self.seeds, self.rng_seed, step, self.pos_u, self.pos_v, self.lp_etype, self.lp_rev, stream,
                             n_seeds_dev=self.n_seeds, step_dev=step_dev, n_seeds=self.seeds.numel())
         self._gather_inputs(s)
@@ -643,9 +675,12 @@ class LPTrainer(_TrainerBase):
         s = _stream(stream)
         h = self._encode(s)
         top = self.L - 1
-        call("gsb_lp_score", _ptr(h), self.hout[top].shape[0], self.hidden, _ptr(self.iu), _ptr(self.iv),
-             _ptr(self.ineg), self.B, self.K, self._pp("rel"), self.loss_kind, _ptr(self.scores),
-             _ptr(self.row_loss), _ptr(self.loss), _ptr(self.dh[top]), self._pp("rel", "g"), s)
+        dm = self.score == "distmult"
+        call("gsb_lp_score_ex", _ptr(h), self.hout[top].shape[0], self.hidden, _ptr(self.iu), _ptr(self.iv),
+             _ptr(self.ineg) if self.n_neg > 0 else None, self.B, self.K, self.group, self.neg_mode,
+             self._pp("rel") if dm else None, self.loss_kind, _ptr(self.pos_w), _ptr(self.scores),
+             _ptr(self.row_loss), _ptr(self.loss), _ptr(self.dh[top]), self._pp("rel", "g") if dm else None,
+             _ptr(self.score_ws), self.score_ws.numel(), s)
         self._backward_layers(s)
 
     def load_inputs(self, u: torch.Tensor, v: torch.Tensor):
