@@ -334,6 +334,30 @@ def nc_loss(h, Wc, bc, y, need_grads: bool = True):
     return loss, logits, dh, dWc, dbc
 
 
+def construct_features(g: Graph, ntype: int, featured, feats=None, first: int = 0, count: Optional[int] = None):
+    """Eq. 1 with f = average (R-eq1): for node v of the featureless ntype,
+    F'_v = mean of F_u over every in-edge u -> v (every stored etype r with dst_t = ntype
+    whose src type is in `featured`), each edge counted once; 0 when v has no such edge.
+    feats[t]: float array (N_t, dim) of ntype t's rows (default: the generator's table).
+    Returns float64 (count, dim) for local ids [first, first + count).  Plain loops."""
+    import synth
+    count = g.counts[ntype] - first if count is None else count
+    feats = {t: (feats[t] if feats is not None and t in feats else synth.feature_table(g.cfg, t)) for t in featured}
+    dim = feats[featured[0]].shape[1]
+    rels = [r for r in range(g.R) if g.dst_t[r] == ntype and g.src_t[r] in featured]
+    out = np.zeros((count, dim))
+    for i in range(count):
+        v = first + i
+        acc, n = np.zeros(dim), 0
+        for r in rels:
+            for e in range(g.indptr[r][v], g.indptr[r][v + 1]):
+                acc += feats[g.src_t[r]][g.indices[r][e]].astype(np.float64)
+                n += 1
+        if n:
+            out[i] = acc / n
+    return out
+
+
 def joint_negatives(n_pos: int, K: int, n_dst_nodes: int, gid_base: int, seed: int, step: int, group_base: int = 0):
     G = (n_pos + K - 1) // K
     neg = np.zeros(G * K, np.int64)
