@@ -280,6 +280,17 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
                        float* row_loss_ws, float* loss, float* dh, float* dWc, float* dbc, void* stream);
 
 /* ======================================================================================
+ * Feature construction for featureless nodes (Eq. 1).
+ *   F'_v = f(F_u, u in N(v)) with f = average (R-eq1): every in-edge u -> v of every stored
+ *   etype whose dst type is `ntype` and whose src type is set in featured_mask (bit t = ntype
+ *   t) counts once; F'_v = 0 when v has no such edge.  Local ids [first, first + count) of
+ *   ntype; out: device fp32 [count][dim] (row-major), dim = the featured types' common width.
+ *   A full sweep over the CSC (no sampling); features may be local or NVLink peer shards.
+ * ==================================================================================== */
+gsb_status gsb_construct_features(gsb_graph_t g, int32_t ntype, uint32_t featured_mask, int64_t first,
+                                  int64_t count, float* out, int32_t dim, void* stream);
+
+/* ======================================================================================
  * Link prediction (App. A; §8(a) a9, a10).
  * ==================================================================================== */
 /* Joint negative sampling: positives in groups of K; group g draws K iid uniform

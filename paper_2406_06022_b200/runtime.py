@@ -63,6 +63,18 @@ class GraphStore:
         except Exception:
             pass
 
+    def construct_features(self, ntype: int, featured: Sequence[int], dim: int, first: int = 0,
+                           count: Optional[int] = None, stream=None) -> torch.Tensor:
+        """Eq. 1 (§8(f) f4): fp32 rows [first, first+count) of ntype built as the
+        average of its featured in-neighbours' rows (gsb_construct_features)."""
+        count = int(self.counts[ntype]) - first if count is None else count
+        out = torch.empty((count, dim), dtype=torch.float32, device=self.device)
+        mask = 0
+        for t in featured:
+            mask |= 1 << int(t)
+        call("gsb_construct_features", self.h, ntype, mask, first, count, _ptr(out), dim, _stream(stream))
+        return out
+
     def load_etype(self, r: int, src: torch.Tensor, dst: torch.Tensor, keep: Optional[torch.Tensor] = None):
         """gsb_csc_build from a device COO (int32 local ids)."""
         s = torch.as_tensor(src, dtype=torch.int32).to(self.device).contiguous()
