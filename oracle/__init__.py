@@ -63,6 +63,7 @@ def lib():
             "oracle_uniform_negatives": (i64, [i64, i32, i64, i64, u64, u32, i64, P]),
             "oracle_lp_loss_ex": (dbl, [i64, i32, i32, i32, i32, P, P, P, i64, P, i32, P, P, P, P, P, P]),
             "oracle_adam": (None, [i64, P, P, P, P, dbl, dbl, dbl, dbl, i32]),
+            "oracle_sparse_adagrad": (None, [i64, i32, P, P, P, P, dbl, dbl]),
             "oracle_sgd": (None, [i64, P, P, dbl]),
         }
         for name, (res, args) in sig.items():
@@ -255,9 +256,35 @@ def encoder_fwd(g: Graph, params: Dict[str, np.ndarray], gids: np.ndarray) -> np
         rows = np.nonzero(ty == t)[0]
         if len(rows) == 0:
             continue
+        if f"Emb{t}" in params:   # learnable embedding table (§8(f) f1): H0 rows are its rows
+            H0[rows] = np.asarray(params[f"Emb{t}"], np.float64)[gids[rows] - g.node_off[t]]
+            continue
         X = input_rows(g, t, gids[rows] - g.node_off[t])
         H0[rows] = X @ params[f"Win{t}"].astype(np.float64) if cfg.project[t] else X
     return H0
+
+
+def emb_grads(g: Graph, params: Dict[str, np.ndarray], gids: np.ndarray, dH0: np.ndarray):
+    """Sparse gradients of the learnable embedding tables (§8(f) f1): H0[i] = Emb_t[local(i)]
+    is a row copy, so dEmb_t[local(i)] = dH0[i] for every input row i of type t (input rows
+    are unique, so no row is hit twice).  Returns {t: (local rows, gradient rows)}."""
+    gids = np.asarray(gids, np.int64)
+    ty = g.type_of(gids)
+    out = {}
+    for t in range(g.T):
+        if f"Emb{t}" in params:
+            rows = np.nonzero(ty == t)[0]
+            out[t] = (gids[rows] - g.node_off[t], np.asarray(dH0, np.float64)[rows])
+    return out
+
+
+def sparse_adagrad(E: np.ndarray, state: np.ndarray, rows: np.ndarray, grad: np.ndarray, lr: float,
+                   eps: float = 1e-10):
+    """In place on float64 E, state: Adagrad on the touched rows only (R-sparseopt)."""
+    rows = _c(rows, np.int64)
+    grad = _c(grad, np.float64)
+    assert E.dtype == np.float64 and state.dtype == np.float64 and E.flags.c_contiguous
+    lib().oracle_sparse_adagrad(len(rows), E.shape[1], _p(rows), _p(grad), _p(E), _p(state), lr, eps)
 
 
 def encoder_bwd(g: Graph, params: Dict[str, np.ndarray], gids: np.ndarray, dH0: np.ndarray) -> Dict[str, np.ndarray]:

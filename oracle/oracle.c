@@ -676,6 +676,23 @@ void oracle_adam(int64_t n, double* p, const double* g, double* m, double* v,
     }
 }
 
+/* Sparse Adagrad for learnable embedding tables (paper silent on the
+ * optimizer, R-sparseopt): for each touched row r with gradient row g (rows distinct):
+ *    state[r] += g*g ;  E[r] -= lr * g / (sqrt(state[r]) + eps)    (elementwise)
+ * Untouched rows and their state are left as they are. */
+void oracle_sparse_adagrad(int64_t n_rows, int32_t d, const int64_t* rows, const double* g, double* E,
+                           double* state, double lr, double eps) {
+    for (int64_t i = 0; i < n_rows; ++i) {
+        double* e = E + (size_t)rows[i] * d;
+        double* st = state + (size_t)rows[i] * d;
+        const double* gi = g + (size_t)i * d;
+        for (int32_t k = 0; k < d; ++k) {
+            st[k] += gi[k] * gi[k];
+            e[k] -= lr * gi[k] / (sqrt(st[k]) + eps);
+        }
+    }
+}
+
 void oracle_sgd(int64_t n, double* p, const double* g, double lr) {
     for (int64_t i = 0; i < n; ++i) p[i] -= lr * g[i];
 }
