@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--neg", default="joint", choices=["joint", "uniform", "local_joint", "in_batch"],
                     help="LP negative sampler (App. A.2.1)")
+    ap.add_argument("--learnable-emb", action="store_true",
+                    help="featureless ntypes (encoder configs) get learnable tables + sparse Adagrad (§8(f) f1)")
     ap.add_argument("--score", default="distmult", choices=["distmult", "dot"], help="LP score function (App. A.1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
     ap.add_argument("--profile-steps", type=int, default=20)
@@ -70,7 +72,7 @@ def config_for(name: str) -> synth.Config:
     return synth.get(name)
 
 
-LP_OPTS = {"neg": "joint", "score": "distmult"}
+LP_OPTS = {"neg": "joint", "score": "distmult", "learnable_emb": False}
 
 
 def lp_task(cfg: synth.Config) -> str:
@@ -89,6 +91,8 @@ def cfg_json(cfg: synth.Config, n_gpus: int, extra=None) -> dict:
          "layers": len(cfg.fanouts), "optimizer": "adam",
          "parallelism": "single" if n_gpus == 1 else f"dp{n_gpus} (graph replicated, NCCL grad all-reduce)",
          "l2": "inputs larger than L2: feature table + CSC >> 126 MB, fresh random seed batch every step"}
+    if LP_OPTS["learnable_emb"] and any(getattr(cfg, "project", None) or []):
+        d["featureless_inputs"] = "learnable tables, sparse Adagrad on touched rows"
     if extra:
         d.update(extra)
     return d
@@ -284,6 +288,10 @@ def build_gsb(cfg, device, partition=None, mode="peer"):
         tr = RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
                          synth.param_order(cfg), synth.labels(cfg, backend="torch", device=device),
                          int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
+    if LP_OPTS["learnable_emb"] and getattr(tr, "enc_types", None):
+        for t in range(cfg.num_ntypes):
+            if not cfg.project[t]:     # init = the frozen table, widened to fp32
+                tr.set_embedding(t, synth.feature_table(cfg, t, backend="torch", device=device).float())
     tr.exchange = ex
     return st, tr
 
@@ -625,7 +633,7 @@ def run_reference(args, cfg):
 def main():
     args = parse()
     cfg = config_for(args.config)
-    LP_OPTS.update(neg=args.neg, score=args.score)
+    LP_OPTS.update(neg=args.neg, score=args.score, learnable_emb=args.learnable_emb)
     fd = args.feat_dtype
     if fd == "auto":
         fd = cfg.feat_dtype if cfg.name in ("tiny", "tiny_lp") or cfg.feat_dtype == "bf16" else "bf16"

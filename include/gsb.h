@@ -280,6 +280,22 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
                        float* row_loss_ws, float* loss, float* dh, float* dWc, float* dbc, void* stream);
 
 /* ======================================================================================
+ * Learnable sparse embeddings for featureless ntypes ("GraphStorm
+ * by default adds learnable embeddings on author nodes").  E: device fp32 [N_t][d] table of
+ * ntype t (this GPU holds all of it), 16-byte aligned; d % 4 == 0.
+ * gsb_sparse_emb_fwd: H0[i] = E[local(i)] for every layer-0 input row i of type t (run after
+ *   gsb_encoder_fwd, which leaves those rows to the table).  H0 as in gsb_encoder_fwd.
+ * gsb_sparse_adagrad: the gradient of E is dH0 on the touched rows only (a row copy; the
+ *   input rows of one ntype are distinct); for each: state[r] += g^2,
+ *   E[r] -= lr g / (sqrt(state[r]) + eps) (R-sparseopt: Adagrad, paper silent).  state:
+ *   device fp32 [N_t][d], zero-initialised by the caller.  Untouched rows do not move.
+ * ==================================================================================== */
+gsb_status gsb_sparse_emb_fwd(gsb_blocks_t b, const void* arena, int32_t ntype, const float* E, int32_t d, float* H0,
+                              void* stream);
+gsb_status gsb_sparse_adagrad(gsb_blocks_t b, const void* arena, int32_t ntype, float* E, float* state,
+                              const float* dH0, int32_t d, float lr, float eps, void* stream);
+
+/* ======================================================================================
  * Feature construction for featureless nodes (Eq. 1).
  *   F'_v = f(F_u, u in N(v)) with f = average (R-eq1): every in-edge u -> v of every stored
  *   etype whose dst type is `ntype` and whose src type is set in featured_mask (bit t = ntype

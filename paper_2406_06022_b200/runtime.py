@@ -281,7 +281,9 @@ class _TrainerBase:
         d0 = int(params["W0"].shape[1])      # layer-0 input width (= encoder output width)
         self.d_in = [d0] + [hidden] * (self.L - 1)
         # input encoder (a6): ntypes with a projection Win{t}; the others are frozen tables
+        # unless set_embedding() makes them learnable (f1)
         self.enc_types = [t for t in range(store.T) if f"Win{t}" in self.names]
+        self.emb: Dict[int, tuple] = {}
         nin = self.sampler.input_rows()
         self.x0 = torch.empty((0 if self.enc_types else nin, d0), dtype=store.feat_dtype, device=dev)
         if self.enc_types:
@@ -342,6 +344,8 @@ class _TrainerBase:
         if self.enc_types:              # a6: projected / frozen input rows by gid -> H0 (fp32)
             call("gsb_encoder_fwd", sm.h, _ptr(sm.arena), self._win, self.d_in[0], _ptr(self.H0), _ptr(self.enc_ws),
                  self.enc_ws.numel(), s)
+            for t, (E, _) in self.emb.items():     # f1: learnable tables replace the frozen rows
+                call("gsb_sparse_emb_fwd", sm.h, _ptr(sm.arena), t, _ptr(E), self.d_in[0], _ptr(self.H0), s)
             h = self.H0
         elif self.exchange is not None:   # partitioned features: NCCL all-to-all fetch (C4/C5)
             gids, n = sm.input_gids()
@@ -376,7 +380,26 @@ class _TrainerBase:
             call("gsb_encoder_bwd", sm.h, _ptr(sm.arena), self._win, _ptr(self.dH0), self.d_in[0], self._dwin,
                  _ptr(self.enc_ws), self.enc_ws.numel(), s)
 
+    def set_embedding(self, ntype: int, E: torch.Tensor, lr: float = 0.01, eps: float = 1e-10):
+        """Make ntype's input rows a learnable table (§8(f) f1): E fp32 [N_t][d_in0] (copied),
+        trained by sparse Adagrad on the rows each mini-batch touches (gsb_sparse_adagrad).
+        Needs the input-encoder path (H0) and a non-projected ntype; one GPU holds the table."""
+        if not self.enc_types or ntype in self.enc_types:
+            raise _lib.GsbError("learnable embeddings need the encoder path and a non-projected ntype")
+        E = E.to(self.device, torch.float32).contiguous().clone()
+        if E.shape != (int(self.store.counts[ntype]), self.d_in[0]):
+            raise _lib.GsbError(f"embedding table shape {tuple(E.shape)}")
+        self.emb[ntype] = (E, torch.zeros_like(E))
+        self.emb_lr, self.emb_eps = lr, eps
+
+    def _sparse_update(self, stream=None):
+        sm = self.sampler
+        for t, (E, st) in self.emb.items():
+            call("gsb_sparse_adagrad", sm.h, _ptr(sm.arena), t, _ptr(E), _ptr(st), _ptr(self.dH0), self.d_in[0],
+                 self.emb_lr, self.emb_eps, _stream(stream))
+
     def optimizer_step(self, stream=None, t_dev: bool = False):
+        self._sparse_update(stream)
         if t_dev:
             call("gsb_adam_step", _ptr(self.flat), _ptr(self.grad), _ptr(self.m), _ptr(self.v), self.n_params,
                  self.lr, 0.9, 0.999, 1e-8, 1, C.c_void_p(self.counters.data_ptr() + 4), _stream(stream))
