@@ -490,6 +490,33 @@ def nc_step(g: Graph, params: Dict[str, np.ndarray], seeds: np.ndarray, labels: 
     return StepResult(loss, blocks, x0, hs, zs, grads, extra)
 
 
+def full_graph_infer(g: Graph, params: Dict[str, np.ndarray]) -> List[np.ndarray]:
+    """Full-graph layer-wise inference (P:L393, P:L403 --inference /
+    --save-embed-path): layer l maps every node's h_{l-1} (h_{-1} = input features) to h_l
+    over its whole in-neighbourhood (fanout ALL, R-fanout ALL), i.e. the RGCN layer (R-rgcn)
+    on one block whose dst and src lists are all nodes in gid order.  Returns [h_0 .. h_{L-1}],
+    each (N_total, d) float64."""
+    cfg = g.cfg
+    L = len(cfg.fanouts)
+    allg = np.arange(int(g.node_off[-1]), dtype=np.int64)
+    blk = sample_blocks(g, allg, [-1], 0, 0)[0]
+    assert np.array_equal(blk.src_gid, allg)          # every src is already a dst: no new nodes
+    h = encoder_fwd(g, params, allg) if cfg.has_encoder else gather(g, allg).astype(np.float64)
+    hs = []
+    for l in range(L):
+        _, h = rgcn_fwd(blk, g.R, h, params[f"W{l}"], params[f"b{l}"], relu=(l < L - 1))
+        hs.append(h)
+    return hs
+
+
+def nc_predict(h: np.ndarray, Wc: np.ndarray, bc: np.ndarray):
+    """Decoder logits (R-ncloss) and their argmax (lowest class on ties) and top-2 margin."""
+    logits = np.asarray(h, np.float64) @ np.asarray(Wc, np.float64) + np.asarray(bc, np.float64)
+    pred = np.argmax(logits, axis=1)
+    top2 = np.sort(logits, axis=1)[:, -2:]
+    return logits, pred, top2[:, 1] - top2[:, 0]
+
+
 def lp_seeds(u: np.ndarray, v: np.ndarray, neg: np.ndarray) -> np.ndarray:
     """LP seed set (§8(a) a9): S0 = ascending unique(u ∪ v ∪ neg)."""
     return np.unique(np.concatenate([u, v, neg]).astype(np.int64))
