@@ -280,6 +280,25 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
                        float* row_loss_ws, float* loss, float* dh, float* dWc, float* dbc, void* stream);
 
 /* ======================================================================================
+ * Full-graph inference (P:L393 layer-wise inference, P:L403 embedding
+ * export).  Layer l of every node = the RGCN layer over its whole in-neighbourhood: sample a
+ * chunk of consecutive gids with fanout ALL (gsb_sample, one layer), run gsb_rgcn_layer_fwd_ex
+ * with h_src = the all-node table of layer l-1 and rowmap from gsb_blocks_input_rowmap (layer
+ * 0: h_src NULL, the features are read by gid), writing the chunk's rows of layer l.
+ * gsb_blocks_input_rowmap: rowmap[i] = src_gid[i] - gid_base for the first layer's input rows
+ *   (device count); rowmap: device int32 [gsb_blocks_input_rows]; ids must fit int32.
+ * gsb_nc_predict: logits = h Wc + bc (tcgen05 GEMM into logits_ws, device fp32 [n][C rounded up
+ *   to 4]), pred[i] = argmax (lowest class on ties; pred nullable), and, when correct != NULL,
+ *   *correct += #{i : pred[i] == labels[seed_gid[i] - label_gid_base]} (device uint64).
+ *   d % 32 == 0.
+ * ==================================================================================== */
+gsb_status gsb_blocks_input_rowmap(gsb_blocks_t b, const void* arena, int64_t gid_base, int32_t* rowmap,
+                                   void* stream);
+gsb_status gsb_nc_predict(const float* h, int64_t n, int32_t d, const float* Wc, const float* bc, int32_t C,
+                          const int32_t* labels, const int64_t* seed_gid, int64_t label_gid_base, float* logits_ws,
+                          int32_t* pred, unsigned long long* correct, void* stream);
+
+/* ======================================================================================
  * Learnable sparse embeddings for featureless ntypes ("GraphStorm
  * by default adds learnable embeddings on author nodes").  E: device fp32 [N_t][d] table of
  * ntype t (this GPU holds all of it), 16-byte aligned; d % 4 == 0.

@@ -81,6 +81,8 @@ SIGS = {
     "gsb_uniform_negatives": [i64, i32, i64, i64, u64, u32, P, i64, P, P],
     "gsb_construct_features": [P, i32, u32, i64, i64, P, i32, P],
     "gsb_sparse_emb_fwd": [P, P, i32, P, i32, P, P],
+    "gsb_blocks_input_rowmap": [P, P, i64, P, P],
+    "gsb_nc_predict": [P, i64, i32, P, P, i32, P, P, i64, P, P, P, P],
     "gsb_sparse_adagrad": [P, P, i32, P, P, P, i32, f32, f32, P],
     "gsb_lp_score_ex": [P, i64, i32, P, P, P, i64, i32, i32, i32, P, i32, P, P, P, P, P, P, P, C.c_size_t, P],
     "gsb_lp_score_ws_bytes": [i64, i32, i32, P],

@@ -729,3 +729,71 @@ class LPTrainer(_TrainerBase):
     def train_step(self, u: torch.Tensor, v: torch.Tensor, step: int, stream=None):
         self.forward_backward(u, v, step, stream)
         self.optimizer_step(stream)
+
+
+class FullGraphInference:
+    """Full-graph layer-wise inference (P:L393 --inference, P:L403
+    --save-embed-path): h_l of every node over its whole in-neighbourhood, layer by layer, in
+    chunks of consecutive gids (fanout ALL, one-layer blocks).  Every arithmetic step runs in
+    libgsb (gsb_sample, gsb_rgcn_layer_fwd_ex, gsb_blocks_input_rowmap, gsb_nc_predict);
+    torch holds the all-node tables.  params: W{l}, b{l} (and Wc, bc for predict)."""
+
+    def __init__(self, store: GraphStore, params: Dict[str, np.ndarray], num_layers: int, hidden: int,
+                 chunk: int = 1 << 16):
+        if any(k.startswith("Win") for k in params):
+            raise _lib.GsbError("full-graph inference with an input encoder is not supported yet")
+        self.store, self.L, self.hidden = store, num_layers, hidden
+        self.chunk = int(min(chunk, int(store.node_off[-1])))
+        dev = store.device
+        self.p = {k: torch.from_numpy(np.ascontiguousarray(v, np.float32)).to(dev) for k, v in params.items()}
+        self.sampler = MiniBatchSampler(store, [-1], self.chunk)
+        self.N = int(store.node_off[-1])
+        self.d_in = [int(params["W0"].shape[1])] + [hidden] * (num_layers - 1)
+        nin = self.sampler.input_rows()
+        self.rowmap = torch.empty(nin, dtype=torch.int32, device=dev)
+        self.acat = torch.empty(max(self.sampler.acat_floats(0, d) for d in self.d_in), dtype=torch.float32,
+                                device=dev)
+        self.H: List[torch.Tensor] = []
+
+    def run(self, stream=None) -> torch.Tensor:
+        """All layers; returns the last layer's table [N_total][hidden] (fp32, device)."""
+        s = _stream(stream)
+        sm = self.sampler
+        dev = self.store.device
+        self.H = []
+        h_prev = None
+        for l in range(self.L):
+            H = torch.empty((self.N, self.hidden), dtype=torch.float32, device=dev)
+            for a in range(0, self.N, self.chunk):
+                b = min(a + self.chunk, self.N)
+                seeds = torch.arange(a, b, dtype=torch.int64, device=dev)
+                sm.sample(seeds, 0, 0, stream=stream)
+                rm = None
+                if h_prev is not None:
+                    call("gsb_blocks_input_rowmap", sm.h, _ptr(sm.arena), 0, _ptr(self.rowmap), s)
+                    rm = self.rowmap
+                call("gsb_rgcn_layer_fwd_ex", sm.h, _ptr(sm.arena), 0, _ptr(h_prev),
+                     0 if h_prev is None else DTYPE_CODE[torch.float32], _ptr(rm), self.d_in[l],
+                     _ptr(self.p[f"W{l}"]), _ptr(self.p[f"b{l}"]), self.hidden, int(l < self.L - 1),
+                     _ptr(H[a:b]), _ptr(self.acat), s)
+            self.H.append(H)
+            h_prev = H
+        return self.H[-1]
+
+    def predict(self, gids: torch.Tensor, labels: torch.Tensor, label_gid_base: int, num_classes: int,
+                stream=None):
+        """NC decoder over the given nodes' final embeddings: (pred int32 [n], #correct)."""
+        h = self.H[-1].index_select(0, gids)     # row selection (plumbing)
+        n = int(gids.numel())
+        C_pad = (num_classes + 3) // 4 * 4
+        logits = torch.empty((max(n, 1), C_pad), dtype=torch.float32, device=h.device)
+        pred = torch.empty(max(n, 1), dtype=torch.int32, device=h.device)
+        correct = torch.zeros(1, dtype=torch.int64, device=h.device)
+        lab = labels.to(h.device, torch.int32).contiguous()
+        call("gsb_nc_predict", _ptr(h), n, self.hidden, _ptr(self.p["Wc"]), _ptr(self.p["bc"]), num_classes,
+             _ptr(lab), _ptr(gids), label_gid_base, _ptr(logits), _ptr(pred), _ptr(correct), _stream(stream))
+        return pred[:n], int(correct.item())
+
+    def save(self, path: str):
+        """Embedding export (P:L403 --save-embed-path): the last layer's table as .npy."""
+        np.save(path, self.H[-1].cpu().numpy())
