@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256, 4) agg_kernel(GraphDev g, const HopMeta* 
                                                   const int64_t* __restrict__ e_src_gid,
                                                   const int64_t* __restrict__ dst_gid, const char* __restrict__ h,
                                                   int row_bytes, int d, float* __restrict__ acat, int64_t lda,
-                                                  const int32_t* __restrict__ rowmap) {
+                                                  const int32_t* __restrict__ rowmap, int64_t seg_cap) {
     constexpr int V = Chunk<BF16>::kVec;
     constexpr int G = 32 / LPE;                  // edges per warp pass
     __shared__ int64_t s_dst_off[kMaxT + 1], s_src_off[kMaxT + 1];
@@ -66,13 +66,15 @@ __global__ void __launch_bounds__(256, 4) agg_kernel(GraphDev g, const HopMeta* 
                 float acc[V];
 #pragma unroll
                 for (int v = 0; v < V; ++v) acc[v] = 0.f;
-                for (int64_t cb = e0; cb < e1; cb += 32) {
+                // a segment longer than seg_cap (fanout ALL hubs) leaves its tail to heavy_kernel
+                const int64_t ec = (e1 - e0 > seg_cap) ? e0 + seg_cap : e1;
+                for (int64_t cb = e0; cb < ec; cb += 32) {
                     // one coalesced load of up to 32 source keys; lane i resolves the row
                     // address of edge cb+i once, the warp takes the addresses by shuffle
-                    const uint4* prow = (cb + lane < e1)
+                    const uint4* prow = (cb + lane < ec)
                         ? src_row<FEAT>(g, h, row_bytes, FEAT ? e_src_gid[cb + lane] : (int64_t)e_src[cb + lane], rowmap)
                         : nullptr;
-                    const int cnt = (int)min((int64_t)32, e1 - cb);
+                    const int cnt = (int)min((int64_t)32, ec - cb);
                     for (int k = 0; k < cnt; k += 4 * G) {
                         uint4 x[4];
 #pragma unroll
@@ -112,34 +114,147 @@ __global__ void __launch_bounds__(256, 4) agg_kernel(GraphDev g, const HopMeta* 
 
 template <bool FEAT, bool BF16>
 static gsb_status launch_agg_lpe(const char* name, int grid, cudaStream_t s, const GraphDev& g, const HopBufs& hb,
-                                 const char* h, int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap) {
+                                 const char* h, int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap,
+                                 int64_t seg_cap) {
     const int cpr = row_bytes / 16;
     if (cpr <= 4) {
         GSB_LAUNCH(name, (agg_kernel<FEAT, BF16, 4>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
-                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap);
+                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
     } else if (cpr <= 8) {
         GSB_LAUNCH(name, (agg_kernel<FEAT, BF16, 8>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
-                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap);
+                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
     } else if (cpr <= 16) {
         GSB_LAUNCH(name, (agg_kernel<FEAT, BF16, 16>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
-                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap);
+                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
     } else {
         GSB_LAUNCH(name, (agg_kernel<FEAT, BF16, 32>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
-                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap);
+                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
     }
     return GSB_OK;
 }
 
+// ------------------------------------------------------------------------------------
+// Heavy segments (fanout ALL, e.g. full-graph inference over hub nodes): agg_kernel sums the
+// first kSegCap edges of every segment; the (row, slot) segments with more edges are listed
+// here, and one block per listed segment spreads the remaining edges over its 8 warps, each
+// adding its scaled partial sum into the Acat slot row (red.add; agg_kernel's store of the
+// head precedes it in stream order).
+// ------------------------------------------------------------------------------------
+constexpr int64_t kSegCap = 256;
+
+__global__ void heavy_list_kernel(GraphDev g, const HopMeta* __restrict__ m, const int64_t* __restrict__ seg_ptr,
+                                  int64_t* __restrict__ list) {
+    const int S = g.S;
+    const int64_t nq = m->n_dst * S;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+        if (seg_ptr[q + 1] - seg_ptr[q] > kSegCap) {
+            const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(list), 1ull);
+            list[1 + k] = q;
+        }
+    }
+}
+
+template <bool FEAT, bool BF16, int LPE>
+__global__ void __launch_bounds__(256) heavy_kernel(GraphDev g, const int64_t* __restrict__ list,
+                                                    const int64_t* __restrict__ seg_ptr,
+                                                    const int32_t* __restrict__ e_src,
+                                                    const int64_t* __restrict__ e_src_gid, const char* __restrict__ h,
+                                                    int row_bytes, int d, float* __restrict__ acat, int64_t lda,
+                                                    const int32_t* __restrict__ rowmap) {
+    constexpr int V = Chunk<BF16>::kVec;
+    constexpr int G = 32 / LPE;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int grp = lane / LPE, sub = lane % LPE;
+    const int cpr = row_bytes >> 4;
+    const int64_t n = list[0];
+    for (int64_t k = blockIdx.x; k < n; k += gridDim.x) {
+        const int64_t q = list[1 + k];
+        const int64_t j = q / g.S;
+        const int sl = (int)(q - j * g.S);
+        const int64_t e0 = seg_ptr[q], e1 = seg_ptr[q + 1];
+        const float inv = 1.f / (float)(e1 - e0);
+        for (int c0 = 0; c0 < cpr; c0 += LPE) {
+            const int c = c0 + sub;
+            const bool cl = c < cpr;
+            float acc[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] = 0.f;
+            for (int64_t cb = e0 + kSegCap + 32 * warp; cb < e1; cb += 32 * nw) {
+                const uint4* prow = (cb + lane < e1)
+                    ? src_row<FEAT>(g, h, row_bytes, FEAT ? e_src_gid[cb + lane] : (int64_t)e_src[cb + lane], rowmap)
+                    : nullptr;
+                const int cnt = (int)min((int64_t)32, e1 - cb);
+                for (int kk = 0; kk < cnt; kk += 4 * G) {
+                    uint4 x[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int idx = kk + grp + G * u;
+                        const uint64_t pu = __shfl_sync(0xffffffffu, (uint64_t)prow, idx & 31);
+                        x[u] = make_uint4(0u, 0u, 0u, 0u);
+                        if (cl && idx < cnt) x[u] = __ldg(reinterpret_cast<const uint4*>(pu) + c);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) chunk_acc<BF16>(acc, x[u]);
+                }
+            }
+#pragma unroll
+            for (int o = LPE; o < 32; o <<= 1)
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], o);
+            if (cl && grp == 0) {
+                float* o = acat + j * lda + (int64_t)sl * d + (int64_t)c * V;
+#pragma unroll
+                for (int v = 0; v < V; v += 4)
+                    red_add_f4(o + v, make_float4(acc[v] * inv, acc[v + 1] * inv, acc[v + 2] * inv, acc[v + 3] * inv));
+            }
+        }
+    }
+}
+
+template <bool FEAT, bool BF16>
+static gsb_status launch_heavy(cudaStream_t s, const GraphDev& g, const HopBufs& hb, const char* h, int row_bytes,
+                               int d, float* acat, int64_t lda, const int32_t* rowmap) {
+    const int cpr = row_bytes / 16;
+    const int grid = kNumSMs * 4;
+    if (cpr <= 8) {
+        GSB_LAUNCH("rgcn_agg_heavy", (heavy_kernel<FEAT, BF16, 8>), grid, 256, 0, s, g, hb.cnt, hb.seg_ptr, hb.e_src,
+                   hb.e_src_gid, h, row_bytes, d, acat, lda, rowmap);
+    } else if (cpr <= 16) {
+        GSB_LAUNCH("rgcn_agg_heavy", (heavy_kernel<FEAT, BF16, 16>), grid, 256, 0, s, g, hb.cnt, hb.seg_ptr, hb.e_src,
+                   hb.e_src_gid, h, row_bytes, d, acat, lda, rowmap);
+    } else {
+        GSB_LAUNCH("rgcn_agg_heavy", (heavy_kernel<FEAT, BF16, 32>), grid, 256, 0, s, g, hb.cnt, hb.seg_ptr, hb.e_src,
+                   hb.e_src_gid, h, row_bytes, d, acat, lda, rowmap);
+    }
+    return GSB_OK;
+}
+
+// fanout: the hop's fanout (-1 = ALL); segments can exceed kSegCap only when it does
 static gsb_status launch_agg(const char* name, bool feat, int dtype, cudaStream_t s, const GraphDev& g,
-                             const HopBufs& hb, const void* h, int d, float* acat, int64_t lda, const int32_t* rowmap) {
+                             const HopBufs& hb, const void* h, int d, float* acat, int64_t lda, const int32_t* rowmap,
+                             int fanout) {
     const int grid = grid_for(hb.cap_dst * 32, 256, kNumSMs * 8);
     const int rb = d * dtype_size(dtype);
     const char* hc = static_cast<const char*>(h);
+    const bool heavy = fanout < 0 || fanout > kSegCap;
+    const int64_t cap = heavy ? kSegCap : INT64_MAX;
+    gsb_status st;
     if (feat)
-        return dtype == GSB_BF16 ? launch_agg_lpe<true, true>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap)
-                                 : launch_agg_lpe<true, false>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap);
-    return dtype == GSB_BF16 ? launch_agg_lpe<false, true>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap)
-                             : launch_agg_lpe<false, false>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap);
+        st = dtype == GSB_BF16 ? launch_agg_lpe<true, true>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
+                               : launch_agg_lpe<true, false>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
+    else
+        st = dtype == GSB_BF16 ? launch_agg_lpe<false, true>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
+                               : launch_agg_lpe<false, false>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
+    if (st != GSB_OK || !heavy) return st;
+    // the sampler's per-segment count buffer is dead after its scan: reuse it as the list
+    GSB_CUDA(cudaMemsetAsync(hb.cnt, 0, sizeof(int64_t), s));
+    GSB_LAUNCH("rgcn_agg_heavy_list", heavy_list_kernel, grid_for(hb.cap_dst * g.S, 256, kNumSMs * 8), 256, 0, s, g,
+               hb.meta, hb.seg_ptr, hb.cnt);
+    if (feat)
+        return dtype == GSB_BF16 ? launch_heavy<true, true>(s, g, hb, hc, rb, d, acat, lda, rowmap)
+                                 : launch_heavy<true, false>(s, g, hb, hc, rb, d, acat, lda, rowmap);
+    return dtype == GSB_BF16 ? launch_heavy<false, true>(s, g, hb, hc, rb, d, acat, lda, rowmap)
+                             : launch_heavy<false, false>(s, g, hb, hc, rb, d, acat, lda, rowmap);
 }
 
 // ------------------------------------------------------------------------------------
@@ -339,11 +454,13 @@ gsb_status gsb_rgcn_layer_fwd_ex(gsb_blocks_t b, const void* arena, int32_t laye
     gsb_status st;
     if (h_src) {
         GSB_CHECK_ARG(dtype_size(h_dtype) > 0, "h_dtype %d not GSB_F32 / GSB_BF16", h_dtype);
-        st = launch_agg(lname("rgcn_agg", layer), false, h_dtype, s, g, hb, h_src, d_in, acat, lda, rowmap);
+        st = launch_agg(lname("rgcn_agg", layer), false, h_dtype, s, g, hb, h_src, d_in, acat, lda, rowmap,
+                        B->fanout[layer]);
     } else {
         GSB_CHECK_ARG(g.feat_dim == d_in, "layer 0 with features: d_in %d != feature dim %d", d_in, g.feat_dim);
         for (int t = 0; t < g.T; ++t) GSB_CHECK_ARG(g.feat[t], "features of ntype %d not registered", t);
-        st = launch_agg(lname("rgcn_agg", layer), true, g.feat_dtype, s, g, hb, nullptr, d_in, acat, lda, nullptr);
+        st = launch_agg(lname("rgcn_agg", layer), true, g.feat_dtype, s, g, hb, nullptr, d_in, acat, lda, nullptr,
+                        B->fanout[layer]);
     }
     if (st != GSB_OK) return st;
     RowGroups rg = layer_groups(B, arena, layer);

@@ -35,3 +35,20 @@ l1 = E * (cfg.hidden * 4 + 12) + N * (cfg.hidden * 4 + (S + 1) * cfg.hidden * 4)
 print(json.dumps({"what": f"full-graph inference, {name}-shaped (bf16 features), {len(cfg.fanouts)} RGCN layers, "
                           f"chunk {inf.chunk}", "nodes": N, "edges": E, "ms": ms, "nodes_per_s": N / ms * 1e3,
                   "agg_alg_GB": (l0 + l1) / 1e9, "agg_alg_GBps_over_whole_run": (l0 + l1) / ms / 1e6}))
+
+# per-kernel breakdown of one more run (events around every launch; serialised)
+import ctypes as C  # noqa: E402
+from paper_2406_06022_b200 import _lib  # noqa: E402
+_lib.lib().gsb_profile_enable(1)
+inf.run()
+torch.cuda.synchronize()
+_lib.lib().gsb_profile_enable(0)
+buf = C.create_string_buffer(1 << 16)
+_lib.call("gsb_profile_dump", buf, len(buf))
+rows = []
+for line in buf.value.decode().splitlines():
+    n, c, t = line.split()
+    rows.append((float(t), n, int(c)))
+rows.sort(reverse=True)
+print(json.dumps({"profile_ms": {n: round(t, 3) for t, n, c in rows[:12]},
+                  "launches": {n: c for t, n, c in rows[:12]}}))
