@@ -229,6 +229,45 @@ using namespace gsb;
 // ====================================================================================
 // extern "C" entry points
 // ====================================================================================
+namespace gsb {
+namespace {
+struct ForkState {
+    bool init = false, enabled = true;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+};
+ForkState g_fork[16];
+}  // namespace
+
+cudaStream_t fork_begin(cudaStream_t s) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return s;
+    ForkState& f = g_fork[dev];
+    if (!f.init) {
+        f.init = true;
+        const char* e = getenv("GSB_NO_FORK");
+        f.enabled = !(e && atoi(e) != 0) &&
+                    cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&f.ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&f.ev_join, cudaEventDisableTiming) == cudaSuccess;
+    }
+    if (!f.enabled) return s;
+    if (cudaEventRecord(f.ev_fork, s) != cudaSuccess || cudaStreamWaitEvent(f.side, f.ev_fork, 0) != cudaSuccess)
+        return s;
+    return f.side;
+}
+
+gsb_status fork_end(cudaStream_t s, cudaStream_t side) {
+    if (side == s) return GSB_OK;
+    int dev = 0;
+    GSB_CUDA(cudaGetDevice(&dev));
+    ForkState& f = g_fork[dev];
+    GSB_CUDA(cudaEventRecord(f.ev_join, side));
+    GSB_CUDA(cudaStreamWaitEvent(s, f.ev_join, 0));
+    return GSB_OK;
+}
+}  // namespace gsb
+
 extern "C" {
 
 const char* gsb_last_error(void) { return g_err.c_str(); }

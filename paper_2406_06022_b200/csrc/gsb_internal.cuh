@@ -56,6 +56,16 @@ void count_launch(int n = 1);
     } while (0)
 
 // ------------------------------------------------------------------------------------
+// Fork / join onto a library-owned side stream (one per device), so independent kernels of
+// one call (e.g. a weight gradient and the input gradient) overlap.  Works inside CUDA graph
+// capture: the side stream joins the capture through the fork event and is joined back
+// before the call returns.  fork_begin returns the side stream (or s itself when forking is
+// disabled with GSB_NO_FORK=1).
+// ------------------------------------------------------------------------------------
+cudaStream_t fork_begin(cudaStream_t s);
+gsb_status fork_end(cudaStream_t s, cudaStream_t side);
+
+// ------------------------------------------------------------------------------------
 // graph descriptor passed to kernels by value
 // ------------------------------------------------------------------------------------
 struct GraphDev {

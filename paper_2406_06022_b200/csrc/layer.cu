@@ -494,14 +494,17 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     HopBufs hb = B->hop(h, const_cast<void*>(arena));
     const int64_t lda = (int64_t)(g.S + 1) * d_in;
     RowGroups rg = layer_groups(B, arena, layer);
-    GSB_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)(g.R + 1) * d_in * d_out, s));
-    GSB_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)d_out, s));
 #ifndef GSB_SIMT_GEMM
     if (relu) {   // dZ once, in place; the GEMMs below then read dZ directly
         GSB_LAUNCH(lname("relu_bwd", layer), relu_bwd_kernel, grid_for(hb.cap_dst * d_out / 4, 256, kNumSMs * 8), 256, 0, s,
                    hb.meta, dh_dst, h_dst, d_out);
     }
+    // the weight gradient runs on the side stream, overlapping dA + scatter (joined below)
+    cudaStream_t s_main = s;
+    if (dh_src) s = fork_begin(s_main);
 #endif
+    GSB_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)(g.R + 1) * d_in * d_out, s));
+    GSB_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)d_out, s));
 #ifdef GSB_SIMT_GEMM
     const int rpc = 256;
     {
@@ -524,6 +527,8 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         gsb_status st = launch_umma<UMMA_TN>(lname("rgcn_gemm_dW", layer), P, items, s);
         if (st != GSB_OK) return st;
     }
+    cudaStream_t s_side = s;
+    s = s_main;
 #endif
     if (dh_src) {
 #ifdef GSB_SIMT_GEMM
@@ -544,7 +549,11 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         GSB_LAUNCH(lname("rgcn_scatter", layer), scatter_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
                    hb.meta, hb.seg_ptr, hb.e_src, dacat_ws, lda, d_in, dh_src);
     }
+#ifndef GSB_SIMT_GEMM
+    return fork_end(s_main, s_side);
+#else
     return GSB_OK;
+#endif
 }
 
 gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int32_t N,
@@ -601,6 +610,8 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         GSB_LAUNCH("nc_ce", ce_kernel, grid, 256, 0, s, logits_ws, n, C, ldl, labels, seed_gid, label_gid_base,
                    row_loss_ws, part, ticket, loss);
     }
+    cudaStream_t s_main = s;
+    if (dWc && dh) s = fork_begin(s_main);   // dWc on the side stream, overlapping dh
     if (dWc || dbc) {
         GSB_CHECK_ARG(dWc && dbc, "dWc and dbc go together");
         GSB_CUDA(cudaMemsetAsync(dWc, 0, sizeof(float) * (size_t)d * C, s));
@@ -619,6 +630,8 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         if (st != GSB_OK) return st;
 #endif
     }
+    cudaStream_t s_side = s;
+    s = s_main;
     if (dh) {
 #ifdef GSB_SIMT_GEMM
         GSB_LAUNCH("nc_gemm_dh", gemm_nt_kernel, gemm_grid(n, (int)ceil_div(d, BN), 1), NT, 0, s, rg, logits_ws,
@@ -634,7 +647,7 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         if (st != GSB_OK) return st;
 #endif
     }
-    return GSB_OK;
+    return fork_end(s_main, s_side);
 }
 
 }  // extern "C"
