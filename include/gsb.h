@@ -228,6 +228,15 @@ gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, 
 gsb_status gsb_rgcn_layer_fwd_ex(gsb_blocks_t b, const void* arena, int32_t layer, const void* h_src, int32_t h_dtype,
                                  const int32_t* rowmap, int32_t d_in, const float* W, const float* bias, int32_t d_out,
                                  int32_t relu, float* h_dst, float* acat, void* stream);
+/* The two halves of gsb_rgcn_layer_fwd_ex, for callers that schedule them apart:
+ * gsb_rgcn_layer_agg fills acat (per-relation means + self rows; reads no parameter, so a
+ *   pipelined caller runs it with the sampling of the next batch), gsb_rgcn_layer_gemm
+ *   computes h_dst from acat.  fwd_ex = agg then gemm on one stream. */
+gsb_status gsb_rgcn_layer_agg(gsb_blocks_t b, const void* arena, int32_t layer, const void* h_src, int32_t h_dtype,
+                              const int32_t* rowmap, int32_t d_in, float* acat, void* stream);
+gsb_status gsb_rgcn_layer_gemm(gsb_blocks_t b, const void* arena, int32_t layer, const float* acat, int32_t d_in,
+                               const float* W, const float* bias, int32_t d_out, int32_t relu, float* h_dst,
+                               void* stream);
 
 /* Backward (analytic):  dZ = dh_dst * 1[h_dst > 0] (relu) or dh_dst;
  *   dW_r = sum_v A_r[v]^T dZ_v ; dW_self = sum_v h_src[self(v)]^T dZ_v ; db = sum_v dZ_v

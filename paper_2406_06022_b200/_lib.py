@@ -55,6 +55,8 @@ SIGS = {
     "gsb_layer_acat_floats": [P, i32, i32, C.POINTER(i64)],
     "gsb_rgcn_layer_fwd": [P, P, i32, P, i32, P, P, i32, i32, P, P, P],
     "gsb_rgcn_layer_fwd_ex": [P, P, i32, P, i32, P, i32, P, P, i32, i32, P, P, P],
+    "gsb_rgcn_layer_agg": [P, P, i32, P, i32, P, i32, P, P],
+    "gsb_rgcn_layer_gemm": [P, P, i32, P, i32, P, P, i32, i32, P, P],
     "gsb_rgcn_layer_bwd": [P, P, i32, P, P, P, P, i32, i32, i32, P, P, P, P, P],
     "gsb_partition_create": [i32, P, i32, i32, P, C.POINTER(P)],
     "gsb_partition_destroy": [P],

@@ -436,33 +436,43 @@ gsb_status gsb_rgcn_layer_fwd(gsb_blocks_t b, const void* arena, int32_t layer, 
                                  stream);
 }
 
-gsb_status gsb_rgcn_layer_fwd_ex(gsb_blocks_t b, const void* arena, int32_t layer, const void* h_src, int32_t h_dtype,
-                                 const int32_t* rowmap, int32_t d_in, const float* W, const float* bias, int32_t d_out,
-                                 int32_t relu, float* h_dst, float* acat, void* stream) {
+gsb_status gsb_rgcn_layer_agg(gsb_blocks_t b, const void* arena, int32_t layer, const void* h_src, int32_t h_dtype,
+                              const int32_t* rowmap, int32_t d_in, float* acat, void* stream) {
     Blocks* B = reinterpret_cast<Blocks*>(b);
-    GSB_CHECK_ARG(B && arena && W && h_dst && acat, "null argument");
+    GSB_CHECK_ARG(B && arena && acat, "null argument");
     GSB_CHECK_ARG(h_src || layer == 0, "h_src may be NULL only for layer 0 (features read by gid)");
     GSB_CHECK_ARG(layer >= 0 && layer < B->L, "layer %d out of range", layer);
     GSB_CHECK_ARG(d_in > 0 && d_in % BK == 0, "d_in %d must be a multiple of %d", d_in, BK);
-    GSB_CHECK_ARG(d_out > 0 && d_out % 4 == 0, "d_out %d must be a multiple of 4", d_out);
     GSB_CHECK_ARG(!rowmap || h_src, "rowmap needs h_src");
     cudaStream_t s = (cudaStream_t)stream;
     const int h = B->hop_of_layer(layer);
     HopBufs hb = B->hop(h, const_cast<void*>(arena));
     const GraphDev& g = B->g->dev;
     const int64_t lda = (int64_t)(g.S + 1) * d_in;
-    gsb_status st;
     if (h_src) {
         GSB_CHECK_ARG(dtype_size(h_dtype) > 0, "h_dtype %d not GSB_F32 / GSB_BF16", h_dtype);
-        st = launch_agg(lname("rgcn_agg", layer), false, h_dtype, s, g, hb, h_src, d_in, acat, lda, rowmap,
-                        B->fanout[layer]);
-    } else {
-        GSB_CHECK_ARG(g.feat_dim == d_in, "layer 0 with features: d_in %d != feature dim %d", d_in, g.feat_dim);
-        for (int t = 0; t < g.T; ++t) GSB_CHECK_ARG(g.feat[t], "features of ntype %d not registered", t);
-        st = launch_agg(lname("rgcn_agg", layer), true, g.feat_dtype, s, g, hb, nullptr, d_in, acat, lda, nullptr,
-                        B->fanout[layer]);
+        return launch_agg(lname("rgcn_agg", layer), false, h_dtype, s, g, hb, h_src, d_in, acat, lda, rowmap,
+                          B->fanout[layer]);
     }
-    if (st != GSB_OK) return st;
+    GSB_CHECK_ARG(g.feat_dim == d_in, "layer 0 with features: d_in %d != feature dim %d", d_in, g.feat_dim);
+    for (int t = 0; t < g.T; ++t) GSB_CHECK_ARG(g.feat[t], "features of ntype %d not registered", t);
+    return launch_agg(lname("rgcn_agg", layer), true, g.feat_dtype, s, g, hb, nullptr, d_in, acat, lda, nullptr,
+                      B->fanout[layer]);
+}
+
+gsb_status gsb_rgcn_layer_gemm(gsb_blocks_t b, const void* arena, int32_t layer, const float* acat, int32_t d_in,
+                               const float* W, const float* bias, int32_t d_out, int32_t relu, float* h_dst,
+                               void* stream) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && arena && W && h_dst && acat, "null argument");
+    GSB_CHECK_ARG(layer >= 0 && layer < B->L, "layer %d out of range", layer);
+    GSB_CHECK_ARG(d_in > 0 && d_in % BK == 0, "d_in %d must be a multiple of %d", d_in, BK);
+    GSB_CHECK_ARG(d_out > 0 && d_out % 4 == 0, "d_out %d must be a multiple of 4", d_out);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int h = B->hop_of_layer(layer);
+    HopBufs hb = B->hop(h, const_cast<void*>(arena));
+    const GraphDev& g = B->g->dev;
+    const int64_t lda = (int64_t)(g.S + 1) * d_in;
     RowGroups rg = layer_groups(B, arena, layer);
 #ifdef GSB_SIMT_GEMM
     GSB_LAUNCH(lname("rgcn_gemm_fwd", layer), gemm_nn_kernel, gemm_grid(hb.cap_dst, (d_out + BN - 1) / BN, g.T), NT, 0, s, rg,
@@ -477,6 +487,15 @@ gsb_status gsb_rgcn_layer_fwd_ex(gsb_blocks_t b, const void* arena, int32_t laye
     if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(h_dst, 0, sizeof(float) * (size_t)hb.cap_dst * d_out, s));
     return launch_umma<UMMA_NN>(lname("rgcn_gemm_fwd", layer), P, tiles, s);
 #endif
+}
+
+gsb_status gsb_rgcn_layer_fwd_ex(gsb_blocks_t b, const void* arena, int32_t layer, const void* h_src, int32_t h_dtype,
+                                 const int32_t* rowmap, int32_t d_in, const float* W, const float* bias, int32_t d_out,
+                                 int32_t relu, float* h_dst, float* acat, void* stream) {
+    GSB_CHECK_ARG(W && h_dst, "null argument");
+    gsb_status st = gsb_rgcn_layer_agg(b, arena, layer, h_src, h_dtype, rowmap, d_in, acat, stream);
+    if (st != GSB_OK) return st;
+    return gsb_rgcn_layer_gemm(b, arena, layer, acat, d_in, W, bias, d_out, relu, h_dst, stream);
 }
 
 gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, const float* h_dst,

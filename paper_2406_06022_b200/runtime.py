@@ -300,6 +300,8 @@ class _TrainerBase:
                      for l in range(self.L)]
         self.acat = [torch.empty(self.sampler.acat_floats(l, self.d_in[l]), dtype=torch.float32, device=dev)
                      for l in range(self.L)]
+        self.acat0 = self.acat[0]      # per-batch (double-buffered with the pipeline)
+        self.early_agg = True
         self.dacat = torch.empty(max(self.sampler.acat_floats(l, self.d_in[l]) for l in range(self.L)),
                                  dtype=torch.float32, device=dev)
         self.dh = [torch.empty((self.sampler.dst_rows(l), hidden), dtype=torch.float32, device=dev)
@@ -330,10 +332,20 @@ class _TrainerBase:
     # pieces ------------------------------------------------------------------------------
     def _gather_inputs(self, s):
         """Explicit input-row gather into x0 (unfused mode; with peer shards registered this is
-        the unique-row NVLink fetch).  Part of the sample phase: it depends only on the blocks."""
+        the unique-row NVLink fetch).  Part of the sample phase: it depends only on the blocks.
+        With early_agg the input layer's aggregation (feature gather + per-relation means,
+        parameter-free) runs here too, into this buffer's acat0."""
         if not self.fuse_gather and self.exchange is None and not self.enc_types:
             sm = self.sampler
             call("gsb_gather_block_inputs", sm.h, _ptr(sm.arena), _ptr(self.x0), s)
+        if self._early():
+            sm = self.sampler
+            h = None if self.fuse_gather else self.x0
+            hdt = DTYPE_CODE[h.dtype] if h is not None else 0
+            call("gsb_rgcn_layer_agg", sm.h, _ptr(sm.arena), 0, _ptr(h), hdt, None, self.d_in[0], _ptr(self.acat0), s)
+
+    def _early(self) -> bool:
+        return self.early_agg and not self.enc_types and self.exchange is None
 
     def _encode(self, s):
         """gather -> RGCN layers, input layer first (Fig. 8).  With fuse_gather
@@ -355,11 +367,16 @@ class _TrainerBase:
             h = None
         else:
             h = self.x0
+        self.acat[0] = self.acat0
         for l in range(self.L):
-            hdt = DTYPE_CODE[h.dtype] if h is not None else 0
-            call("gsb_rgcn_layer_fwd_ex", sm.h, _ptr(sm.arena), l, _ptr(h), hdt, _ptr(rowmap if l == 0 else None),
-                 self.d_in[l], self._pp(f"W{l}"), self._pp(f"b{l}"), self.hidden, int(l < self.L - 1),
-                 _ptr(self.hout[l]), _ptr(self.acat[l]), s)
+            if l == 0 and self._early():   # acat0 was filled in the sample phase
+                call("gsb_rgcn_layer_gemm", sm.h, _ptr(sm.arena), 0, _ptr(self.acat0), self.d_in[0],
+                     self._pp("W0"), self._pp("b0"), self.hidden, int(self.L > 1), _ptr(self.hout[0]), s)
+            else:
+                hdt = DTYPE_CODE[h.dtype] if h is not None else 0
+                call("gsb_rgcn_layer_fwd_ex", sm.h, _ptr(sm.arena), l, _ptr(h), hdt, _ptr(rowmap if l == 0 else None),
+                     self.d_in[l], self._pp(f"W{l}"), self._pp(f"b{l}"), self.hidden, int(l < self.L - 1),
+                     _ptr(self.hout[l]), _ptr(self.acat[l]), s)
             h = self.hout[l]
         return h
 
@@ -446,7 +463,7 @@ class _TrainerBase:
         self.t += 1
 
     # double-buffered pipeline: sample batch i+1 while batch i computes ---------------------
-    _BUFFERED = ("sampler", "x0")     # per-batch state; subclasses add their input buffers
+    _BUFFERED = ("sampler", "x0", "acat0")     # per-batch state; subclasses add their input buffers
 
     def enable_prefetch(self):
         """Allocate a second copy of every per-batch buffer (sampler handle + arena, input
@@ -465,6 +482,7 @@ class _TrainerBase:
     def _use(self, b: int):
         for k, v in self._bufs[b].items():
             setattr(self, k, v)
+        self.acat[0] = self.acat0
 
     def _sample_ops(self):
         """Sample phase of the batch in the active buffer, RNG step word read from (and then
@@ -572,7 +590,7 @@ class RGCNTrainer(_TrainerBase):
         self.row_loss = torch.zeros(batch + 640, dtype=torch.float32, device=dev)   # + fused-mean scratch
         self.seeds_dev = torch.empty(batch, dtype=torch.int64, device=dev)
 
-    _BUFFERED = ("sampler", "x0", "seeds_dev")
+    _BUFFERED = ("sampler", "x0", "acat0", "seeds_dev")
 
     def _load_inputs(self, d, seeds: torch.Tensor):
         d["seeds_dev"][:seeds.numel()].copy_(seeds, non_blocking=True)
@@ -672,6 +690,9 @@ class LPTrainer(_TrainerBase):
         self.iv = torch.empty(B, dtype=torch.int32, device=dev)
         self.ineg = torch.empty(max(self.n_neg, 1), dtype=torch.int32, device=dev)
         self.pos_w = torch.ones(B, dtype=torch.float32, device=dev)    # Eq. 5 weights (loss_kind 2)
+        # the LP sample phase (negatives, seed set, exclusion-aware sampling) is already the
+        # longer of the two pipelined streams: keep the input aggregation in the compute phase
+        self.early_agg = False
         wb = C.c_size_t()
         call("gsb_lp_seeds_bytes", B, self.n_neg, C.byref(wb))
         self.seeds_ws = torch.empty(int(wb.value), dtype=torch.uint8, device=dev)
@@ -682,7 +703,8 @@ class LPTrainer(_TrainerBase):
         self.group_base = 0
         self.pos_base = 0
 
-    _BUFFERED = ("sampler", "x0", "pos_u", "pos_v", "neg", "seeds", "n_seeds", "iu", "iv", "ineg", "seeds_ws")
+    _BUFFERED = ("sampler", "x0", "acat0", "pos_u", "pos_v", "neg", "seeds", "n_seeds", "iu", "iv", "ineg",
+                 "seeds_ws")
 
     def _load_inputs(self, d, u: torch.Tensor, v: torch.Tensor):
         d["pos_u"].copy_(u, non_blocking=True)
