@@ -74,6 +74,7 @@ void prof_end(cudaStream_t s) {
 __global__ void csc_keys_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                                 const uint8_t* __restrict__ keep, int64_t n, uint64_t* __restrict__ keys,
                                 unsigned long long* __restrict__ n_kept) {
+    GSB_PDL_ENTRY();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
     unsigned long long local = 0;
@@ -88,6 +89,7 @@ __global__ void csc_keys_kernel(const int32_t* __restrict__ src, const int32_t* 
 
 __global__ void csc_finish_kernel(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ n_kept_p,
                                   int64_t n_dst, int64_t* __restrict__ indptr, int32_t* __restrict__ indices) {
+    GSB_PDL_ENTRY();
     const int64_t n_kept = (int64_t)*n_kept_p;
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_kept; i += stride)
@@ -110,6 +112,7 @@ __global__ void csc_finish_kernel(const uint64_t* __restrict__ keys, const unsig
 __global__ void __launch_bounds__(256) gather_kernel(GraphDev g, const int64_t* __restrict__ gid,
                                                      const int64_t* __restrict__ n_dev, int64_t n_host,
                                                      uint4* __restrict__ out) {
+    GSB_PDL_ENTRY();
     const int64_t n = n_dev ? *n_dev : n_host;
     const int d16 = g.feat_row_bytes >> 4;
     const int64_t total = n * d16;
@@ -152,6 +155,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
                                                    float* __restrict__ m, float* __restrict__ v, int64_t n, float lr,
                                                    float b1, float b2, float eps, float c1, float c2,
                                                    const int32_t* __restrict__ t_dev) {
+    GSB_PDL_ENTRY();
     __shared__ float sc[2];
     if (t_dev) {   // bias corrections from the device step counter (graph replay), once per block
         if (threadIdx.x == 0) {
@@ -191,9 +195,11 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
     }
 }
 
-__global__ void counter_add_kernel(int32_t* c, int32_t d) { *c += d; }
+__global__ void counter_add_kernel(int32_t* c, int32_t d) {
+    GSB_PDL_ENTRY(); *c += d; }
 
 __global__ void spin_kernel(int64_t ns) {
+    GSB_PDL_ENTRY();
     uint64_t t0, t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     do {
@@ -230,6 +236,14 @@ using namespace gsb;
 // extern "C" entry points
 // ====================================================================================
 namespace gsb {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("GSB_PDL");   // opt-in: measured neutral to -4 % under CUDA graphs
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+
 namespace {
 struct ForkState {
     bool init = false, enabled = true;

@@ -135,6 +135,7 @@ template <bool BWD>
 __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, EncDev e, const HopMeta* __restrict__ m,
                                                                     const int64_t* __restrict__ src_gid,
                                                                     float* __restrict__ H0, EncOut out) {
+    GSB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ __align__(8) uint64_t full[EN_STAGES], empty[EN_STAGES], tfull[2], tempty[2];
@@ -318,6 +319,7 @@ namespace gsb {
 // W_t [dim][d_out] fp32 -> transposed bf16 hi / lo [d_out][dim]
 __global__ void enc_wsplit_kernel(const float* __restrict__ W, int dim, int d_out, __nv_bfloat16* __restrict__ hi,
                                   __nv_bfloat16* __restrict__ lo) {
+    GSB_PDL_ENTRY();
     const int64_t n = (int64_t)dim * d_out;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int k = (int)(i / d_out), j = (int)(i % d_out);
@@ -331,6 +333,7 @@ __global__ void enc_wsplit_kernel(const float* __restrict__ W, int dim, int d_ou
 // dH0 rows of projected types -> bf16 hi / lo (same layout [rows][d_out])
 __global__ void enc_dsplit_kernel(EncDev e, const HopMeta* __restrict__ m, const float* __restrict__ dH0,
                                   __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
+    GSB_PDL_ENTRY();
     const int64_t n4 = m->n_src * (int64_t)e.d_out / 4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t row = i * 4 / e.d_out;
@@ -354,6 +357,7 @@ __global__ void enc_dsplit_kernel(EncDev e, const HopMeta* __restrict__ m, const
 template <bool BF16>
 __global__ void enc_copy_kernel(GraphDev g, EncDev e, const HopMeta* __restrict__ m, const int64_t* __restrict__ src_gid,
                                 float* __restrict__ H0) {
+    GSB_PDL_ENTRY();
     constexpr int V = Chunk<BF16>::kVec;
     const int cpr = e.d_out / V;                        // chunks per row (dim_t == d_out)
     const int64_t n = m->n_src * (int64_t)cpr;

@@ -30,6 +30,7 @@ __device__ __forceinline__ int part_owner(const PartDev& p, int t, int64_t local
 // Warp-aggregated: one shared-memory atomic per (warp, owner) instead of one per id.
 __global__ void owner_count_kernel(PartDev p, const int64_t* __restrict__ gid, const int64_t* __restrict__ n_dev,
                                    int64_t n_cap, unsigned long long* __restrict__ cnt) {
+    GSB_PDL_ENTRY();
     __shared__ unsigned long long sc[8];
     if (threadIdx.x < 8) sc[threadIdx.x] = 0;
     __syncthreads();
@@ -60,6 +61,7 @@ __global__ void owner_scatter_kernel(PartDev p, const int64_t* __restrict__ gid,
                                      int64_t n_cap, const unsigned long long* __restrict__ cnt,
                                      unsigned long long* __restrict__ cursor, int64_t* __restrict__ send_gid,
                                      int32_t* __restrict__ perm) {
+    GSB_PDL_ENTRY();
     __shared__ unsigned long long base[8];
     if (threadIdx.x == 0) {
         unsigned long long a = 0;
@@ -100,6 +102,7 @@ __global__ void owner_scatter_kernel(PartDev p, const int64_t* __restrict__ gid,
 
 // row copies in 16-byte chunks (dtype-agnostic)
 __global__ void shard_gather_kernel(PartDev p, const int64_t* __restrict__ gid, int64_t n, uint4* __restrict__ out) {
+    GSB_PDL_ENTRY();
     const int d16 = p.row_bytes >> 4;
     const int64_t total = n * d16;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -114,6 +117,7 @@ __global__ void shard_gather_kernel(PartDev p, const int64_t* __restrict__ gid, 
 
 __global__ void rows_permute_kernel(const char* __restrict__ rows, int row_bytes, const int32_t* __restrict__ perm,
                                     const int64_t* __restrict__ n_dev, int64_t n_cap, uint4* __restrict__ out) {
+    GSB_PDL_ENTRY();
     const int64_t n = n_dev ? min(*n_dev, n_cap) : n_cap;
     const int d16 = row_bytes >> 4;
     const int64_t total = n * d16;

@@ -11,6 +11,7 @@ namespace gsb {
 template <bool BF16>
 __global__ void __launch_bounds__(256) featcon_kernel(GraphDev g, int ntype, uint32_t rel_mask, int64_t first,
                                                       int64_t count, int dim, float* __restrict__ out) {
+    GSB_PDL_ENTRY();
     constexpr int V = Chunk<BF16>::kVec;
     const int lane = threadIdx.x & 31;
     const int cpr = dim / V;                       // 16-byte chunks per row

@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(NT) gemm_nn_kernel(RowGroups rg, const float* 
                                                      const float* __restrict__ W, int d_in, int N, int64_t ldw,
                                                      int64_t wslot_stride, const float* __restrict__ bias, int relu,
                                                      float* __restrict__ C, int64_t ldc) {
+    GSB_PDL_ENTRY();
     __shared__ __align__(16) float As[BK][BM + APAD];
     __shared__ __align__(16) float Bs[BK][BN];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(NT) gemm_nt_kernel(RowGroups rg, const float* 
                                                      const float* __restrict__ H, int relu, int64_t ldh,
                                                      const float* __restrict__ W, int d_in, int N, int64_t ldw,
                                                      int64_t wslot_stride, float* __restrict__ C, int64_t ldc) {
+    GSB_PDL_ENTRY();
     __shared__ __align__(16) float As[BK][BM + APAD];
     __shared__ __align__(16) float Bs[BK][BN];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(NT) gemm_tn_kernel(RowGroups rg, const float* 
                                                      int relu, int64_t ldh, int d_in, int N, int rows_per_chunk,
                                                      float* __restrict__ dW, int64_t ldw, int64_t wslot_stride,
                                                      float* __restrict__ db) {
+    GSB_PDL_ENTRY();
     __shared__ __align__(16) float As[BK][BM + APAD];
     __shared__ __align__(16) float Bs[BK][BN];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;

@@ -330,6 +330,7 @@ __device__ __forceinline__ float4 split_panel_s(uint32_t stage, const SmemOff& s
 
 template <int MODE>
 __global__ void __launch_bounds__(UM_THREADS, 1) umma_gemm_kernel(UProb P) {
+    GSB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ __align__(8) uint64_t bars[UM_STAGES];

@@ -8,6 +8,7 @@ namespace gsb {
 
 __global__ void input_rowmap_kernel(const HopMeta* __restrict__ m, const int64_t* __restrict__ src_gid, int64_t base,
                                     int32_t* __restrict__ rowmap) {
+    GSB_PDL_ENTRY();
     const int64_t n = m->n_src;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         rowmap[i] = (int32_t)(src_gid[i] - base);
@@ -20,6 +21,7 @@ __global__ void __launch_bounds__(256) nc_argmax_kernel(const float* __restrict_
                                                         const int64_t* __restrict__ seed_gid, int64_t base,
                                                         int32_t* __restrict__ pred,
                                                         unsigned long long* __restrict__ correct) {
+    GSB_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {

@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(256, 4) agg_kernel(GraphDev g, const HopMeta* 
                                                   const int64_t* __restrict__ dst_gid, const char* __restrict__ h,
                                                   int row_bytes, int d, float* __restrict__ acat, int64_t lda,
                                                   const int32_t* __restrict__ rowmap, int64_t seg_cap) {
+    GSB_PDL_ENTRY();
     constexpr int V = Chunk<BF16>::kVec;
     constexpr int G = 32 / LPE;                  // edges per warp pass
     __shared__ int64_t s_dst_off[kMaxT + 1], s_src_off[kMaxT + 1];
@@ -144,6 +145,7 @@ constexpr int64_t kSegCap = 256;
 
 __global__ void heavy_list_kernel(GraphDev g, const HopMeta* __restrict__ m, const int64_t* __restrict__ seg_ptr,
                                   int64_t* __restrict__ list) {
+    GSB_PDL_ENTRY();
     const int S = g.S;
     const int64_t nq = m->n_dst * S;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
@@ -161,6 +163,7 @@ __global__ void __launch_bounds__(256) heavy_kernel(GraphDev g, const int64_t* _
                                                     const int64_t* __restrict__ e_src_gid, const char* __restrict__ h,
                                                     int row_bytes, int d, float* __restrict__ acat, int64_t lda,
                                                     const int32_t* __restrict__ rowmap) {
+    GSB_PDL_ENTRY();
     constexpr int V = Chunk<BF16>::kVec;
     constexpr int G = 32 / LPE;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -264,6 +267,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(GraphDev g, const HopMeta*
                                                       const int64_t* __restrict__ seg_ptr,
                                                       const int32_t* __restrict__ e_src, const float* __restrict__ dA,
                                                       int64_t lda, int d, float* __restrict__ dh) {
+    GSB_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const int S = g.S;
     const int64_t n = m->n_dst;
@@ -301,6 +305,7 @@ __global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int
                                                  const int64_t* __restrict__ seed_gid, int64_t base,
                                                  float* __restrict__ row_loss, float* __restrict__ part,
                                                  unsigned* __restrict__ ticket, float* __restrict__ loss) {
+    GSB_PDL_ENTRY();
     __shared__ float wsum[8];
     __shared__ bool last;
     const int lane = threadIdx.x & 31;
@@ -343,6 +348,7 @@ __global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int
 }
 
 __global__ void __launch_bounds__(1024) mean_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
+    GSB_PDL_ENTRY();
     __shared__ float sm[32];
     float s = 0.f;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
@@ -359,6 +365,7 @@ __global__ void __launch_bounds__(1024) mean_kernel(const float* __restrict__ x,
 // dZ = dh * 1[h > 0] in place (ReLU backward, ReLU'(0) = 0), rows = device dst count
 __global__ void __launch_bounds__(256) relu_bwd_kernel(const HopMeta* __restrict__ m, float* __restrict__ dh,
                                                        const float* __restrict__ h, int d) {
+    GSB_PDL_ENTRY();
     const int64_t n4 = m->n_dst * (int64_t)d / 4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
         float4 g = reinterpret_cast<float4*>(dh)[i];

@@ -14,6 +14,7 @@ namespace gsb {
 __global__ void joint_neg_kernel(int64_t total, int K, int64_t n_nodes, int64_t base, uint64_t seed, uint32_t step_host,
                                  const uint32_t* __restrict__ step_dev, int64_t group_base, int64_t* __restrict__ neg,
                                  uint32_t tag) {
+    GSB_PDL_ENTRY();
     const uint32_t step = step_dev ? *step_dev : step_host;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t g = group_base + i / K;
@@ -25,6 +26,7 @@ __global__ void joint_neg_kernel(int64_t total, int K, int64_t n_nodes, int64_t 
 
 __global__ void lp_concat_kernel(const int64_t* __restrict__ u, const int64_t* __restrict__ v, int64_t B,
                                  const int64_t* __restrict__ neg, int64_t n_neg, uint64_t* __restrict__ buf) {
+    GSB_PDL_ENTRY();
     const int64_t n = 2 * B + n_neg;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         buf[i] = (uint64_t)(i < B ? u[i] : (i < 2 * B ? v[i - B] : neg[i - 2 * B]));
@@ -33,6 +35,7 @@ __global__ void lp_concat_kernel(const int64_t* __restrict__ u, const int64_t* _
 __global__ void lp_pos_kernel(const uint64_t* __restrict__ buf, int64_t B, int64_t n_neg,
                               const int64_t* __restrict__ seeds, const int64_t* __restrict__ n_seeds,
                               int32_t* __restrict__ iu, int32_t* __restrict__ iv, int32_t* __restrict__ ineg) {
+    GSB_PDL_ENTRY();
     const int64_t n = 2 * B + n_neg;
     const int64_t ns = *n_seeds;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -68,6 +71,7 @@ __global__ void __launch_bounds__(256) lp_score_kernel(const float* __restrict__
                                                        const float* __restrict__ wpos,
                                                        float* __restrict__ scores, float* __restrict__ row_loss,
                                                        float* __restrict__ dH, float* __restrict__ drel) {
+    GSB_PDL_ENTRY();
     extern __shared__ float s_drel[];
     const int lane = threadIdx.x & 31;
     const int d4 = d >> 2;
@@ -192,6 +196,7 @@ __global__ void __launch_bounds__(256) lp_score_kernel(const float* __restrict__
 }
 
 __global__ void __launch_bounds__(1024) lp_mean_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
+    GSB_PDL_ENTRY();
     __shared__ float sm[32];
     float s = 0.f;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
@@ -216,6 +221,7 @@ __global__ void __launch_bounds__(1024) lp_mean_kernel(const float* __restrict__
 __global__ void ib_gather_kernel(const float* __restrict__ H, int d, const int32_t* __restrict__ iu,
                                  const int32_t* __restrict__ iv, int64_t B, const float* __restrict__ rel,
                                  float* __restrict__ U, float* __restrict__ V, float* __restrict__ Ur) {
+    GSB_PDL_ENTRY();
     const int d4 = d >> 2;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < B * d4; x += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = x / d4;
@@ -233,6 +239,7 @@ __global__ void ib_gather_kernel(const float* __restrict__ H, int d, const int32
 __global__ void __launch_bounds__(256) ib_rows_kernel(float* __restrict__ S, int64_t B, int kind,
                                                       const float* __restrict__ wpos, float* __restrict__ scores,
                                                       float* __restrict__ row_loss) {
+    GSB_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const float invB = 1.f / (float)B;
@@ -271,6 +278,7 @@ __global__ void __launch_bounds__(256) ib_finish_kernel(const float* __restrict_
                                                         const int32_t* __restrict__ iv, int64_t B, int d,
                                                         const float* __restrict__ rel, float* __restrict__ dH,
                                                         float* __restrict__ drel) {
+    GSB_PDL_ENTRY();
     extern __shared__ float s_dr[];
     for (int c = threadIdx.x; c < d; c += blockDim.x) s_dr[c] = 0.f;
     __syncthreads();

@@ -39,6 +39,7 @@ struct Excl {
 // previous key's end so that (lo - cum) stays non-decreasing within a segment.
 __global__ void excl_ranges_kernel(GraphDev g, const uint64_t* __restrict__ keys, int64_t n, int32_t etype,
                                    int32_t rev, int64_t* __restrict__ lo_out, int64_t* __restrict__ len_out) {
+    GSB_PDL_ENTRY();
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= n; k += (int64_t)gridDim.x * blockDim.x) {
         if (k == n) {
             len_out[k] = 0;
@@ -71,6 +72,7 @@ __global__ void excl_ranges_kernel(GraphDev g, const uint64_t* __restrict__ keys
 
 __global__ void excl_keys_kernel(const int64_t* __restrict__ u, const int64_t* __restrict__ v, int64_t n, int rev,
                                  uint64_t* __restrict__ keys) {
+    GSB_PDL_ENTRY();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         keys[i] = ((uint64_t)v[i] << 31) | (uint64_t)u[i];
         keys[n + i] = rev ? ((1ull << 62) | ((uint64_t)u[i] << 31) | (uint64_t)v[i]) : ~0ull;
@@ -133,6 +135,7 @@ __global__ void __launch_bounds__(1024) seed_meta_kernel(GraphDev g, const int64
                                                          const int64_t* __restrict__ n_dev,
                                                          int64_t* __restrict__ d1, HopMeta* __restrict__ m,
                                                          int* __restrict__ err) {
+    GSB_PDL_ENTRY();
     __shared__ unsigned long long cnt[kMaxT];
     int64_t n = n_dev ? *n_dev : n_cap;
     if (n > n_cap) {
@@ -182,6 +185,7 @@ __global__ void __launch_bounds__(256) count_kernel(GraphDev g, const HopMeta* _
                                                     const int64_t* __restrict__ dst_gid, int64_t cap_dst, int fanout,
                                                     Excl ex, int32_t* __restrict__ map, int64_t* __restrict__ cnt,
                                                     int* __restrict__ err) {
+    GSB_PDL_ENTRY();
     const int S = g.S;
     const int64_t n = (*(volatile int*)err) ? 0 : m->n_dst;
     const int64_t total = cap_dst * S;
@@ -227,6 +231,7 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
                                                    const int32_t* __restrict__ map, uint32_t* __restrict__ bitmap,
                                                    int64_t* __restrict__ e_src_gid, int64_t* __restrict__ e_eid,
                                                    const int* __restrict__ err) {
+    GSB_PDL_ENTRY();
     const int S = g.S;
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);                       // lane inside the group
@@ -310,6 +315,7 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
 // rank / meta / relabel / next frontier
 // ------------------------------------------------------------------------------------
 __global__ void popc_kernel(const uint32_t* __restrict__ bitmap, int64_t n_words, int32_t* __restrict__ wrank) {
+    GSB_PDL_ENTRY();
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= n_words; w += (int64_t)gridDim.x * blockDim.x)
         wrank[w] = (w < n_words) ? __popc(bitmap[w]) : 0;
 }
@@ -325,6 +331,7 @@ __device__ __forceinline__ int64_t bit_rank(const uint32_t* bitmap, const int32_
 __global__ void hop_meta_kernel(GraphDev g, HopMeta* __restrict__ m, HopMeta* __restrict__ next,
                                 const int64_t* __restrict__ seg_ptr, int64_t nseg_cap, const uint32_t* __restrict__ bitmap,
                                 const int32_t* __restrict__ wrank, int64_t cap_src, int* __restrict__ err) {
+    GSB_PDL_ENTRY();
     __shared__ int64_t nn_s[kMaxT];
     const int t = threadIdx.x;
     const bool bad = *(volatile int*)err != 0;
@@ -373,6 +380,7 @@ __global__ void __launch_bounds__(256) relabel_kernel(GraphDev g, const HopMeta*
                                                       const int32_t* __restrict__ map,
                                                       const uint32_t* __restrict__ bitmap,
                                                       const int32_t* __restrict__ wrank, int32_t* __restrict__ e_src) {
+    GSB_PDL_ENTRY();
     const int64_t E = m->n_edges;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
         int64_t u = e_src_gid[e];
@@ -392,6 +400,7 @@ __global__ void __launch_bounds__(256) next_frontier_kernel(GraphDev g, const Ho
                                                             int32_t* __restrict__ map, uint32_t* __restrict__ bitmap,
                                                             const int32_t* __restrict__ wrank, int64_t n_words,
                                                             int64_t cap_src, int64_t* __restrict__ src_gid) {
+    GSB_PDL_ENTRY();
     const int64_t n = m->n_dst;
     const int64_t work = n > n_words ? n : n_words;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < work; i += (int64_t)gridDim.x * blockDim.x) {
@@ -423,6 +432,7 @@ __global__ void __launch_bounds__(256) next_frontier_kernel(GraphDev g, const Ho
 
 __global__ void init_arena_kernel(int32_t* __restrict__ map, int64_t n, uint32_t* __restrict__ bitmap, int64_t n_words,
                                   int* __restrict__ err) {
+    GSB_PDL_ENTRY();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n || i < n_words;
          i += (int64_t)gridDim.x * blockDim.x) {
         if (i < n) map[i] = -1;

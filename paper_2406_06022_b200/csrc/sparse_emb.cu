@@ -10,6 +10,7 @@ namespace gsb {
 // thread per 16-byte chunk of an input row of type t:  H0[row] = E[gid - node_off[t]]
 __global__ void emb_fwd_kernel(const HopMeta* __restrict__ m, const int64_t* __restrict__ src_gid, int t,
                                int64_t node_off_t, const float* __restrict__ E, int d, float* __restrict__ H0) {
+    GSB_PDL_ENTRY();
     const int c4 = d >> 2;
     const int64_t r0 = m->src_off[t], n = (m->src_off[t + 1] - r0) * c4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -25,6 +26,7 @@ __global__ void emb_fwd_kernel(const HopMeta* __restrict__ m, const int64_t* __r
 __global__ void emb_adagrad_kernel(const HopMeta* __restrict__ m, const int64_t* __restrict__ src_gid, int t,
                                    int64_t node_off_t, float* __restrict__ E, float* __restrict__ state,
                                    const float* __restrict__ dH0, int d, float lr, float eps) {
+    GSB_PDL_ENTRY();
     const int c4 = d >> 2;
     const int64_t r0 = m->src_off[t], n = (m->src_off[t + 1] - r0) * c4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
