@@ -312,9 +312,43 @@ __global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int
     float mine = 0.f;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const float invn = 1.f / (float)n;
+    constexpr int kR = 16;                         // row values held per lane (C <= 512)
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
         float* lg = logits + i * ldl;
         const int y = labels[seed_gid[i] - base];
+        if (C <= 32 * kR) {   // one read of the row into registers
+            float x[kR];
+            float mx = -INFINITY, ly = 0.f;
+#pragma unroll
+            for (int k = 0; k < kR; ++k) {
+                const int c = lane + 32 * k;
+                x[k] = c < C ? lg[c] : -INFINITY;
+                mx = fmaxf(mx, x[k]);
+                if (c == y) ly = x[k];
+            }
+            for (int o = 16; o; o >>= 1) {
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                ly += __shfl_xor_sync(0xffffffffu, ly, o);     // one lane holds logit_y
+            }
+            float se = 0.f;
+#pragma unroll
+            for (int k = 0; k < kR; ++k) {
+                const int c = lane + 32 * k;
+                x[k] = c < C ? expf(x[k] - mx) : 0.f;
+                se += x[k];
+            }
+            for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+            const float inv_se = 1.f / se;
+#pragma unroll
+            for (int k = 0; k < kR; ++k) {
+                const int c = lane + 32 * k;
+                if (c < C) lg[c] = (x[k] * inv_se - (c == y ? 1.f : 0.f)) * invn;
+            }
+            const float li = mx + logf(se) - ly;          // lse - logit_y
+            if (lane == 0) row_loss[i] = li;
+            mine += li;
+            continue;
+        }
         float mx = -INFINITY;
         for (int c = lane; c < C; c += 32) mx = fmaxf(mx, lg[c]);
         for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -338,12 +372,15 @@ __global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int
         last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last && threadIdx.x < 32) {   // one warp adds the block partials (fixed order per lane)
         __threadfence();
         float tot = 0.f;
-        for (unsigned b = 0; b < gridDim.x; ++b) tot += ((volatile float*)part)[b];
-        *loss = tot / (float)n;
-        *ticket = 0u;
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) tot += ((volatile float*)part)[b];
+        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (threadIdx.x == 0) {
+            *loss = tot / (float)n;
+            *ticket = 0u;
+        }
     }
 }
 
