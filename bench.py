@@ -446,6 +446,30 @@ def run_gsb(args, cfg):
     ms_per_step = ms / args.steps
     seeds_per_s = cfg.batch * ws * args.steps / (ms / 1e3)   # NC: seeds; LP: positive edges
 
+    # ---- phase diagnostic: the pipelined step overlaps a sample-phase graph (side stream)
+    # with a compute-phase graph; replayed alone, each one's time shows which bounds the step
+    phase_ms = None
+    if pipelined and getattr(tr, "pipe_graphs", None):
+        torch.cuda.synchronize()
+        phase_ms = {}
+        for kind in ("sample", "compute"):
+            g = tr.pipe_graphs[kind][0]
+            tr._use(0)
+            g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(20):
+                g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            phase_ms[kind] = a.elapsed_time(b) / 20
+        if dist is not None:
+            for k in list(phase_ms):
+                t = torch.tensor([phase_ms[k]], device=device)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                phase_ms[k] = float(t.item())
+
     # ---- per-kernel profile: eager steps, each preceded by a 3 ms spin kernel so the host
     # enqueues the whole step before it starts (events then time kernels, not launch gaps)
     base = W + args.steps
@@ -554,6 +578,7 @@ def run_gsb(args, cfg):
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
         "roofline_gather_aggregation": roof_agg,
         "kernels": kernels, "setup_s": setup_s,
+        "phase_ms_alone": phase_ms,
     }
     if tr.exchange is not None:
         line["nvlink_bytes_per_step_rank0"] = nv_bytes
