@@ -426,11 +426,13 @@ def run_gsb(args, cfg):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         e0.record()
+        th0 = time.perf_counter()
         for i in range(W, W + args.steps):
             run(i)
         if pipelined:
             tr.pipeline_sync()    # the sampling of batch W+steps (issued in the last step) is inside
         e1.record()
+        host_enqueue_ms = (time.perf_counter() - th0) * 1e3
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
@@ -579,6 +581,7 @@ def run_gsb(args, cfg):
         "roofline_gather_aggregation": roof_agg,
         "kernels": kernels, "setup_s": setup_s,
         "phase_ms_alone": phase_ms,
+        "host_enqueue_ms_per_step": host_enqueue_ms / args.steps,
     }
     if tr.exchange is not None:
         line["nvlink_bytes_per_step_rank0"] = nv_bytes
