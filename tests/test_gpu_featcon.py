@@ -41,3 +41,43 @@ def test_construct_features_wide_bf16(torch_cuda):
     exp = oracle.construct_features(og, author, [paper], first=5, count=700)
     close(got, exp, what="F' author from papers")
     assert np.abs(exp).sum() > 0
+
+
+@pytest.mark.parametrize("dtype,dim", [("f32", 64), ("bf16", 768), ("bf16", 128)])
+def test_construct_features_hubs(torch_cuda, dtype, dim):
+    """Hub in-degrees around the head/tail split (featcon.cu kFeatconCap = 128): segments of
+    0, 1, 127, 128, 129, 255, 256, 257, 1000 and 40 000 edges over two featured relations, in
+    a range that starts and ends mid-graph.  Expected rows: the mean of the in-neighbours'
+    rows (Eq. 1), written out in float64 from the COO."""
+    torch = torch_cuda
+    rng = np.random.default_rng(2406)
+    nA, nB = 5000, 64
+    degs = [0, 1, 127, 128, 129, 255, 256, 257, 1000, 40000, 3, 0, 129, 2]
+    src, dst = [], []
+    for r in range(2):
+        s_r, d_r = [], []
+        for v in range(nB):
+            k = degs[(v + 5 * r) % len(degs)] if v % 3 else int(rng.integers(0, 6))
+            s_r.append(rng.integers(0, nA, size=k))
+            d_r.append(np.full(k, v))
+        src.append(np.concatenate(s_r).astype(np.int32))
+        dst.append(np.concatenate(d_r).astype(np.int32))
+    from paper_2406_06022_b200.runtime import GraphStore
+    st = GraphStore([nA, nB], [0, 0], [1, 1], "cuda")
+    for r in range(2):
+        st.load_etype(r, torch.from_numpy(src[r]), torch.from_numpy(dst[r]))
+    F = rng.uniform(-1, 1, size=(nA, dim)).astype(np.float32)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    Ft = torch.from_numpy(F).to(tdt)
+    st.set_features(0, Ft)
+    st.set_features(1, torch.zeros((nB, dim), dtype=tdt))
+    Fx = Ft.float().numpy().astype(np.float64)      # the stored (rounded) rows
+    first, count = 3, nB - 7
+    got = st.construct_features(1, [0], dim, first, count).cpu().numpy()
+    s_all, d_all = np.concatenate(src), np.concatenate(dst)
+    exp = np.zeros((count, dim))
+    for i in range(count):
+        nb = s_all[d_all == first + i]
+        if nb.size:
+            exp[i] = Fx[nb].mean(axis=0)
+    close(got, exp, what=f"F' hubs {dtype} {dim}")
