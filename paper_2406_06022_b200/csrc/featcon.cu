@@ -92,20 +92,6 @@ __global__ void __launch_bounds__(256) featcon_kernel(GraphDev g, uint32_t rel_m
     }
 }
 
-// last v in [lo, hi) with indptr[v] <= a (indptr[lo] <= a < indptr[hi]); 32 probes per round
-__device__ __forceinline__ int64_t featcon_find(const int64_t* __restrict__ indptr, int64_t lo, int64_t hi, int64_t a,
-                                                int lane) {
-    while (hi - lo > 1) {
-        const int64_t step = (hi - lo + 31) / 32;
-        const int64_t p = lo + (int64_t)(lane + 1) * step;
-        const bool le = p < hi && indptr[p] <= a;
-        const int k = __popc(__ballot_sync(0xffffffffu, le));
-        lo += (int64_t)k * step;
-        hi = min(hi, lo + step);
-    }
-    return lo;
-}
-
 template <bool BF16, int NP>
 __global__ void __launch_bounds__(256) featcon_tail_kernel(GraphDev g, int r, uint32_t rel_mask, int64_t first,
                                                            int64_t count, int dim, float* __restrict__ out) {
@@ -119,8 +105,8 @@ __global__ void __launch_bounds__(256) featcon_tail_kernel(GraphDev g, int r, ui
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < pieces; k += warps) {
         const int64_t a = E0 + k * kFeatconCap, b = min(E1, a + kFeatconCap);
-        const int64_t va = featcon_find(ip, first, first + count, a, lane);
-        const int64_t vb = featcon_find(ip, va, first + count, b - 1, lane);
+        const int64_t va = seg_find(ip, first, first + count, a, lane);
+        const int64_t vb = seg_find(ip, va, first + count, b - 1, lane);
         for (int64_t v = va;; v = vb) {
             const int64_t t0 = max(a, ip[v] + kFeatconCap), t1 = min(b, ip[v + 1]);
             if (t0 < t1) {

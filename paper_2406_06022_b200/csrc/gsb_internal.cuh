@@ -253,6 +253,23 @@ __device__ __forceinline__ void chunk_acc(float* acc, const uint4 x) {
     }
 }
 
+// Warp-cooperative search in a non-decreasing offset array: the last i in [lo, hi) with
+// ptr[i] <= a, given ptr[lo] <= a < ptr[hi]; 32 probes per round (log32 rounds).  Used to cut
+// long (fanout ALL / full-CSC) segments into fixed-size edge pieces: the warp owning piece
+// [a, b) finds the segments holding its first and last edge.
+__device__ __forceinline__ int64_t seg_find(const int64_t* __restrict__ ptr, int64_t lo, int64_t hi, int64_t a,
+                                            int lane) {
+    while (hi - lo > 1) {
+        const int64_t step = (hi - lo + 31) / 32;
+        const int64_t p = lo + (int64_t)(lane + 1) * step;
+        const bool le = p < hi && ptr[p] <= a;
+        const int k = __popc(__ballot_sync(0xffffffffu, le));
+        lo += (int64_t)k * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+
 __device__ __forceinline__ void red_add_f4(float* p, float4 v) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
                  "f"(v.w)

@@ -136,28 +136,17 @@ static gsb_status launch_agg_lpe(const char* name, int grid, cudaStream_t s, con
 
 // ------------------------------------------------------------------------------------
 // Heavy segments (fanout ALL, e.g. full-graph inference over hub nodes): agg_kernel sums the
-// first kSegCap edges of every segment; the (row, slot) segments with more edges are listed
-// here, and one block per listed segment spreads the remaining edges over its 8 warps, each
-// adding its scaled partial sum into the Acat slot row (red.add; agg_kernel's store of the
-// head precedes it in stream order).
+// first kSegCap edges of every segment.  The hop's flat edge range is cut into pieces of
+// kSegCap edges; a warp per piece adds the scaled sum of the edges in it that lie beyond
+// kSegCap of their (row, slot) segment into the Acat slot row (red.add; agg_kernel's store of
+// the head precedes it in stream order).  A segment wholly inside a piece has <= kSegCap
+// edges, so only the segments holding the piece's first and last edge qualify: a hub's tail
+// is spread over (len - kSegCap) / kSegCap warps, with no list and no workspace.
 // ------------------------------------------------------------------------------------
 constexpr int64_t kSegCap = 256;
 
-__global__ void heavy_list_kernel(GraphDev g, const HopMeta* __restrict__ m, const int64_t* __restrict__ seg_ptr,
-                                  int64_t* __restrict__ list) {
-    GSB_PDL_ENTRY();
-    const int S = g.S;
-    const int64_t nq = m->n_dst * S;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-        if (seg_ptr[q + 1] - seg_ptr[q] > kSegCap) {
-            const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(list), 1ull);
-            list[1 + k] = q;
-        }
-    }
-}
-
 template <bool FEAT, bool BF16, int LPE>
-__global__ void __launch_bounds__(256) heavy_kernel(GraphDev g, const int64_t* __restrict__ list,
+__global__ void __launch_bounds__(256) heavy_kernel(GraphDev g, const HopMeta* __restrict__ m,
                                                     const int64_t* __restrict__ seg_ptr,
                                                     const int32_t* __restrict__ e_src,
                                                     const int64_t* __restrict__ e_src_gid, const char* __restrict__ h,
@@ -166,50 +155,68 @@ __global__ void __launch_bounds__(256) heavy_kernel(GraphDev g, const int64_t* _
     GSB_PDL_ENTRY();
     constexpr int V = Chunk<BF16>::kVec;
     constexpr int G = 32 / LPE;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int grp = lane / LPE, sub = lane % LPE;
     const int cpr = row_bytes >> 4;
-    const int64_t n = list[0];
-    for (int64_t k = blockIdx.x; k < n; k += gridDim.x) {
-        const int64_t q = list[1 + k];
-        const int64_t j = q / g.S;
-        const int sl = (int)(q - j * g.S);
-        const int64_t e0 = seg_ptr[q], e1 = seg_ptr[q + 1];
-        const float inv = 1.f / (float)(e1 - e0);
-        for (int c0 = 0; c0 < cpr; c0 += LPE) {
-            const int c = c0 + sub;
-            const bool cl = c < cpr;
-            float acc[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) acc[v] = 0.f;
-            for (int64_t cb = e0 + kSegCap + 32 * warp; cb < e1; cb += 32 * nw) {
-                const uint4* prow = (cb + lane < e1)
-                    ? src_row<FEAT>(g, h, row_bytes, FEAT ? e_src_gid[cb + lane] : (int64_t)e_src[cb + lane], rowmap)
+    const int64_t nseg = m->n_dst * g.S;
+    const int64_t E = seg_ptr[nseg];
+    const int64_t pieces = (E + kSegCap - 1) / kSegCap;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < pieces; k += warps) {
+        const int64_t pa = k * kSegCap, pb = min(E, pa + kSegCap);
+        const int64_t qa = seg_find(seg_ptr, 0, nseg, pa, lane);
+        const int64_t qb = seg_find(seg_ptr, qa, nseg, pb - 1, lane);
+        for (int64_t q = qa;; q = qb) {
+            const int64_t e0 = seg_ptr[q], e1 = seg_ptr[q + 1];
+            const int64_t t0 = max(pa, e0 + kSegCap), t1 = min(pb, e1);
+            if (t0 < t1) {
+                const int64_t j = q / g.S;
+                const int sl = (int)(q - j * g.S);
+                const float inv = 1.f / (float)(e1 - e0);
+                const uint4* prow = (t0 + lane < t1)
+                    ? src_row<FEAT>(g, h, row_bytes, FEAT ? e_src_gid[t0 + lane] : (int64_t)e_src[t0 + lane], rowmap)
                     : nullptr;
-                const int cnt = (int)min((int64_t)32, e1 - cb);
-                for (int kk = 0; kk < cnt; kk += 4 * G) {
-                    uint4 x[4];
+                for (int c0 = 0; c0 < cpr; c0 += LPE) {
+                    const int c = c0 + sub;
+                    const bool cl = c < cpr;
+                    float acc[V];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int idx = kk + grp + G * u;
-                        const uint64_t pu = __shfl_sync(0xffffffffu, (uint64_t)prow, idx & 31);
-                        x[u] = make_uint4(0u, 0u, 0u, 0u);
-                        if (cl && idx < cnt) x[u] = __ldg(reinterpret_cast<const uint4*>(pu) + c);
+                    for (int v = 0; v < V; ++v) acc[v] = 0.f;
+                    for (int64_t cb = t0; cb < t1; cb += 32) {
+                        const uint4* pr = prow;
+                        if (cb != t0)
+                            pr = (cb + lane < t1) ? src_row<FEAT>(g, h, row_bytes,
+                                                                  FEAT ? e_src_gid[cb + lane] : (int64_t)e_src[cb + lane],
+                                                                  rowmap)
+                                                  : nullptr;
+                        const int cnt = (int)min((int64_t)32, t1 - cb);
+                        for (int kk = 0; kk < cnt; kk += 4 * G) {
+                            uint4 x[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int idx = kk + grp + G * u;
+                                const uint64_t pu = __shfl_sync(0xffffffffu, (uint64_t)pr, idx & 31);
+                                x[u] = make_uint4(0u, 0u, 0u, 0u);
+                                if (cl && idx < cnt) x[u] = __ldg(reinterpret_cast<const uint4*>(pu) + c);
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) chunk_acc<BF16>(acc, x[u]);
+                        }
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) chunk_acc<BF16>(acc, x[u]);
+                    for (int o = LPE; o < 32; o <<= 1)
+#pragma unroll
+                        for (int v = 0; v < V; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], o);
+                    if (cl && grp == 0) {
+                        float* o = acat + j * lda + (int64_t)sl * d + (int64_t)c * V;
+#pragma unroll
+                        for (int v = 0; v < V; v += 4)
+                            red_add_f4(o + v, make_float4(acc[v] * inv, acc[v + 1] * inv, acc[v + 2] * inv,
+                                                          acc[v + 3] * inv));
+                    }
                 }
             }
-#pragma unroll
-            for (int o = LPE; o < 32; o <<= 1)
-#pragma unroll
-                for (int v = 0; v < V; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], o);
-            if (cl && grp == 0) {
-                float* o = acat + j * lda + (int64_t)sl * d + (int64_t)c * V;
-#pragma unroll
-                for (int v = 0; v < V; v += 4)
-                    red_add_f4(o + v, make_float4(acc[v] * inv, acc[v + 1] * inv, acc[v + 2] * inv, acc[v + 3] * inv));
-            }
+            if (q == qb) break;
         }
     }
 }
@@ -218,15 +225,15 @@ template <bool FEAT, bool BF16>
 static gsb_status launch_heavy(cudaStream_t s, const GraphDev& g, const HopBufs& hb, const char* h, int row_bytes,
                                int d, float* acat, int64_t lda, const int32_t* rowmap) {
     const int cpr = row_bytes / 16;
-    const int grid = kNumSMs * 4;
+    const int grid = kNumSMs * 8;
     if (cpr <= 8) {
-        GSB_LAUNCH("rgcn_agg_heavy", (heavy_kernel<FEAT, BF16, 8>), grid, 256, 0, s, g, hb.cnt, hb.seg_ptr, hb.e_src,
+        GSB_LAUNCH("rgcn_agg_heavy", (heavy_kernel<FEAT, BF16, 8>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,
                    hb.e_src_gid, h, row_bytes, d, acat, lda, rowmap);
     } else if (cpr <= 16) {
-        GSB_LAUNCH("rgcn_agg_heavy", (heavy_kernel<FEAT, BF16, 16>), grid, 256, 0, s, g, hb.cnt, hb.seg_ptr, hb.e_src,
+        GSB_LAUNCH("rgcn_agg_heavy", (heavy_kernel<FEAT, BF16, 16>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,
                    hb.e_src_gid, h, row_bytes, d, acat, lda, rowmap);
     } else {
-        GSB_LAUNCH("rgcn_agg_heavy", (heavy_kernel<FEAT, BF16, 32>), grid, 256, 0, s, g, hb.cnt, hb.seg_ptr, hb.e_src,
+        GSB_LAUNCH("rgcn_agg_heavy", (heavy_kernel<FEAT, BF16, 32>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,
                    hb.e_src_gid, h, row_bytes, d, acat, lda, rowmap);
     }
     return GSB_OK;
@@ -249,10 +256,6 @@ static gsb_status launch_agg(const char* name, bool feat, int dtype, cudaStream_
         st = dtype == GSB_BF16 ? launch_agg_lpe<false, true>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
                                : launch_agg_lpe<false, false>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
     if (st != GSB_OK || !heavy) return st;
-    // the sampler's per-segment count buffer is dead after its scan: reuse it as the list
-    GSB_CUDA(cudaMemsetAsync(hb.cnt, 0, sizeof(int64_t), s));
-    GSB_LAUNCH("rgcn_agg_heavy_list", heavy_list_kernel, grid_for(hb.cap_dst * g.S, 256, kNumSMs * 8), 256, 0, s, g,
-               hb.meta, hb.seg_ptr, hb.cnt);
     if (feat)
         return dtype == GSB_BF16 ? launch_heavy<true, true>(s, g, hb, hc, rb, d, acat, lda, rowmap)
                                  : launch_heavy<true, false>(s, g, hb, hc, rb, d, acat, lda, rowmap);

@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
                                                    uint64_t seed, uint32_t step_host, const uint32_t* step_dev, int hop,
                                                    const int32_t* __restrict__ map, uint32_t* __restrict__ bitmap,
                                                    int64_t* __restrict__ e_src_gid, int64_t* __restrict__ e_eid,
-                                                   const int* __restrict__ err) {
+                                                   const int* __restrict__ err, int64_t cap) {
     GSB_PDL_ENTRY();
     const int S = g.S;
     const int lane = threadIdx.x & 31;
@@ -259,8 +259,9 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
         const bool has_ex = k1 > k0;
         const int64_t degp = has_ex ? deg - excl_count(ex, k0, k1, seg, deg, src_off) : deg;
         if (c == degp) {
-            // every non-excluded in-edge, ascending
-            for (int64_t q = gl; q < c; q += G) {
+            // every non-excluded in-edge, ascending; beyond cap: fill_tail_kernel
+            const int64_t ce = min(c, cap);
+            for (int64_t q = gl; q < ce; q += G) {
                 int64_t p = has_ex ? excl_map(ex, k0, k1, seg, deg, src_off, q) : q;
                 int64_t u = src_off + seg[p];
                 e_src_gid[base + q] = u;
@@ -307,6 +308,65 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
                 uint32_t bit = 1u << (u & 31);
                 if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);
             }
+        }
+    }
+}
+
+// Fanout ALL (and fanouts above kFillCap) copy whole neighbourhoods; a power-law hub's
+// segment (10^5 edges) would serialise one lane group.  fill_kernel copies the first kFillCap
+// edges of each segment; here the hop's flat edge range is cut into pieces of kFillCap edges
+// and a warp per piece copies the edges in it that lie beyond kFillCap of their segment.  A
+// segment wholly inside a piece has <= kFillCap edges, so only the segments holding the
+// piece's first and last edge qualify.  Segments longer than kFillCap are never Floyd draws
+// (those hold c <= fanout <= 32 edges), so every such edge is the copy rule's.
+constexpr int64_t kFillCap = 256;
+
+__global__ void __launch_bounds__(256) fill_tail_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                        const int64_t* __restrict__ dst_gid,
+                                                        const int64_t* __restrict__ seg_ptr, Excl ex,
+                                                        const int32_t* __restrict__ map, uint32_t* __restrict__ bitmap,
+                                                        int64_t* __restrict__ e_src_gid, int64_t* __restrict__ e_eid,
+                                                        const int* __restrict__ err) {
+    GSB_PDL_ENTRY();
+    const int S = g.S;
+    const int lane = threadIdx.x & 31;
+    const int64_t nseg = ((*(volatile const int*)err) ? 0 : m->n_dst) * S;
+    const int64_t E = seg_ptr[nseg];
+    const int64_t pieces = (E + kFillCap - 1) / kFillCap;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < pieces; k += warps) {
+        const int64_t pa = k * kFillCap, pb = min(E, pa + kFillCap);
+        const int64_t ia = seg_find(seg_ptr, 0, nseg, pa, lane);
+        const int64_t ib = seg_find(seg_ptr, ia, nseg, pb - 1, lane);
+        for (int64_t i = ia;; i = ib) {
+            const int64_t base = seg_ptr[i];
+            const int64_t q0 = max(pa, base + kFillCap) - base, q1 = min(pb, seg_ptr[i + 1]) - base;
+            if (q0 < q1) {
+                const int64_t j = i / S;
+                const int s = (int)(i - j * S);
+                const int64_t v = dst_gid[j];
+                const int t = type_of(g, v);
+                const int r = g.slot_etype[t][s];
+                const int64_t vl = v - g.node_off[t];
+                const int64_t a = g.indptr[r][vl];
+                const int64_t deg = g.indptr[r][vl + 1] - a;
+                const int32_t* seg = g.indices[r] + a;
+                const int64_t src_off = g.node_off[g.src_t[r]];
+                int64_t k0, k1;
+                excl_range(ex, r, v, k0, k1);
+                const bool has_ex = k1 > k0;
+                for (int64_t q = q0 + lane; q < q1; q += 32) {
+                    const int64_t p = has_ex ? excl_map(ex, k0, k1, seg, deg, src_off, q) : q;
+                    const int64_t u = src_off + seg[p];
+                    e_src_gid[base + q] = u;
+                    e_eid[base + q] = g.eid_base[r] + a + p;
+                    if (map[u] < 0) {
+                        const uint32_t bit = 1u << (u & 31);
+                        if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);
+                    }
+                }
+            }
+            if (i == ib) break;
         }
     }
 }
@@ -631,18 +691,23 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
         {
             const int G = (f >= 1 && f <= 8) ? 8 : ((f >= 1 && f <= 16) ? 16 : 32);
             const int grid = grid_for(nseg * G, 256, kNumSMs * 8);
+            const bool tail = f < 0 || f > kFillCap;
+            const int64_t cap = tail ? kFillCap : INT64_MAX;
             if (G == 8)
                 GSB_LAUNCH("sample_fill", fill_kernel<8>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
                            hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
-                           err);
+                           err, cap);
             else if (G == 16)
                 GSB_LAUNCH("sample_fill", fill_kernel<16>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
                            hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
-                           err);
+                           err, cap);
             else
                 GSB_LAUNCH("sample_fill", fill_kernel<32>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
                            hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
-                           err);
+                           err, cap);
+            if (tail)
+                GSB_LAUNCH("sample_fill_tail", fill_tail_kernel, kNumSMs * 8, 256, 0, s, g, hb.meta, hb.dst_gid,
+                           hb.seg_ptr, ex, map, bitmap, hb.e_src_gid, hb.e_eid, err);
         }
         GSB_LAUNCH("bitmap_popc", popc_kernel, grid_for(B->n_words + 1, 256, kNumSMs * 8), 256, 0, s, bitmap,
                    B->n_words, wrank);
