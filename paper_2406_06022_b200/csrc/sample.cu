@@ -178,6 +178,66 @@ __global__ void __launch_bounds__(1024) seed_meta_kernel(GraphDev g, const int64
     }
 }
 
+// Large seed sets (full-graph inference chunks of 10^5-10^6 nodes): the same copy, checks and
+// per-type counts over the whole grid (block counts added into the zeroed dst_off[t + 1]),
+// then one thread turns the counts into offsets.  One block of seed_meta_kernel walked a
+// 262k-seed chunk in 0.28 ms.
+__global__ void __launch_bounds__(256) seed_scan_kernel(GraphDev g, const int64_t* __restrict__ seeds, int64_t n_cap,
+                                                        const int64_t* __restrict__ n_dev, int64_t* __restrict__ d1,
+                                                        HopMeta* __restrict__ m, int* __restrict__ err) {
+    GSB_PDL_ENTRY();
+    __shared__ unsigned long long cnt[kMaxT];
+    int64_t n = n_dev ? *n_dev : n_cap;
+    if (n > n_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(err, ERR_CAPACITY);
+        n = n_cap;
+    }
+    if (threadIdx.x < kMaxT) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t N = g.node_off[g.T];
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        int t = -1;
+        if (i < n) {
+            const int64_t v = seeds[i];
+            d1[i] = v;
+            if (v < 0 || v >= N) {
+                atomicExch(err, ERR_RANGE);
+            } else {
+                t = type_of(g, v);
+                if (i > 0) {
+                    const int64_t p = seeds[i - 1];
+                    if (p >= 0 && p < N && type_of(g, p) > t) atomicExch(err, ERR_GROUPING);
+                }
+            }
+        }
+        for (int tt = 0; tt < g.T; ++tt) {
+            const unsigned b = __ballot_sync(0xffffffffu, t == tt);
+            if (lane == 0 && b) atomicAdd(&cnt[tt], (unsigned long long)__popc(b));
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < g.T && cnt[threadIdx.x])
+        atomicAdd(reinterpret_cast<unsigned long long*>(&m->dst_off[threadIdx.x + 1]), cnt[threadIdx.x]);
+}
+
+__global__ void seed_fin_kernel(int T, int64_t n_cap, const int64_t* __restrict__ n_dev, HopMeta* __restrict__ m,
+                                const int* __restrict__ err) {
+    GSB_PDL_ENTRY();
+    if (threadIdx.x != 0) return;
+    int64_t n = n_dev ? *n_dev : n_cap;
+    if (n > n_cap) n = n_cap;
+    const bool bad = *(volatile const int*)err != 0;
+    m->n_dst = bad ? 0 : n;
+    m->dst_off[0] = 0;
+    for (int t = 0; t < kMaxT; ++t) {
+        const int64_t c = (!bad && t < T) ? m->dst_off[t + 1] : 0;
+        m->dst_off[t + 1] = m->dst_off[t] + c;
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // count: thread per (dst j, slot s)
 // ------------------------------------------------------------------------------------
@@ -677,8 +737,16 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
     }
 
     GSB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
-    GSB_LAUNCH("seed_meta", seed_meta_kernel, 1, 1024, 0, s, g, seeds, n_seeds, a->n_seeds_dev, at<int64_t>(arena, B->off_seed),
-               at<HopMeta>(arena, B->off_meta[1]), err);
+    if (n_seeds <= 8192) {
+        GSB_LAUNCH("seed_meta", seed_meta_kernel, 1, 1024, 0, s, g, seeds, n_seeds, a->n_seeds_dev,
+                   at<int64_t>(arena, B->off_seed), at<HopMeta>(arena, B->off_meta[1]), err);
+    } else {
+        HopMeta* m1 = at<HopMeta>(arena, B->off_meta[1]);
+        GSB_CUDA(cudaMemsetAsync(m1, 0, sizeof(HopMeta), s));
+        GSB_LAUNCH("seed_meta", seed_scan_kernel, grid_for(n_seeds, 256, kNumSMs * 8), 256, 0, s, g, seeds, n_seeds,
+                   a->n_seeds_dev, at<int64_t>(arena, B->off_seed), m1, err);
+        GSB_LAUNCH("seed_meta_fin", seed_fin_kernel, 1, 32, 0, s, g.T, n_seeds, a->n_seeds_dev, m1, err);
+    }
     for (int h = 1; h <= B->L; ++h) {
         HopBufs hb = B->hop(h, arena);
         const int f = B->fanout[B->L - h];

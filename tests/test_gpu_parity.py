@@ -132,6 +132,25 @@ def test_sample_latched_errors(torch_cuda):
         sm.sample(torch_cuda.zeros(9, dtype=torch_cuda.int64).cuda(), 1, 0)   # over capacity: sync error
 
 
+def test_sample_large_seed_set(torch_cuda):
+    """Seed sets above 8192 take the grid-wide seed scan (sample.cu seed_scan_kernel): every
+    node of the tiny graph as seeds (all ntypes, ragged type boundaries) matches the oracle's
+    blocks bit for bit, and a grouping error deep inside the set is still latched."""
+    from paper_2406_06022_b200.runtime import MiniBatchSampler
+    cfg = synth.tiny()
+    st, og = gpu_store(cfg), oracle_graph(cfg)
+    n = int(cfg.node_off[-1])
+    sm = MiniBatchSampler(st, cfg.fanouts, max_seeds=n)
+    seeds = np.arange(n, dtype=np.int64)
+    sm.sample(torch_cuda.from_numpy(seeds).cuda(), 5, 3)
+    assert sm.poll_error() == 0
+    _compare_blocks(cfg, st, sm, oracle.sample_blocks(og, seeds, cfg.fanouts, 5, 3))
+    bad = seeds.copy()
+    bad[9001] = int(cfg.node_off[1]) - 1          # a type-0 node after type-2 nodes
+    sm.sample(torch_cuda.from_numpy(bad).cuda(), 5, 3)
+    assert sm.poll_error() == 1
+
+
 def test_sample_deterministic(pair, torch_cuda):
     from paper_2406_06022_b200.runtime import MiniBatchSampler
     cfg, st, og = pair
