@@ -517,6 +517,28 @@ def nc_predict(h: np.ndarray, Wc: np.ndarray, bc: np.ndarray):
     return logits, pred, top2[:, 1] - top2[:, 0]
 
 
+def lp_mrr(scores: np.ndarray):
+    """MRR of link prediction (the paper's LP metric, Table 2, Table 6
+    P:L249-259), reading R-mrr: row i of scores is [pos_i, neg_i1 .. neg_iK]; the positive's
+    rank is 1 + #(negatives scoring higher) + #(negatives scoring equal) / 2 -- its expected
+    rank under a uniformly random order of tied scores; MRR = mean over rows of 1 / rank.
+    Returns (reciprocal ranks [B] float64, MRR)."""
+    S = np.asarray(scores)
+    B = S.shape[0]
+    rr = np.zeros(B)
+    for i in range(B):
+        pos = S[i, 0]
+        greater = 0
+        equal = 0
+        for x in S[i, 1:]:
+            if x > pos:
+                greater += 1
+            elif x == pos:
+                equal += 1
+        rr[i] = 1.0 / (1.0 + greater + 0.5 * equal)
+    return rr, (float(rr.mean()) if B else 0.0)
+
+
 def lp_seeds(u: np.ndarray, v: np.ndarray, neg: np.ndarray) -> np.ndarray:
     """LP seed set (§8(a) a9): S0 = ascending unique(u ∪ v ∪ neg)."""
     return np.unique(np.concatenate([u, v, neg]).astype(np.int64))
