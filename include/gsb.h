@@ -372,6 +372,14 @@ gsb_status gsb_lp_score(const float* H, int64_t n_rows_cap, int32_t d, const int
                         const int32_t* ineg, int64_t B, int32_t K, const float* rel, int32_t loss_kind, float* scores,
                         float* row_loss_ws, float* loss, float* dH, float* drel, void* stream);
 
+/* LP evaluation metric MRR (Tables 2 and 6 report it), reading R-mrr.
+ *   scores: device fp32 [B][ld], row i = [pos_i, neg_i1 .. neg_iK] (the layout gsb_lp_score /
+ *   gsb_lp_score_ex write, ld = 1 + K); rank_i = 1 + #{j: neg_ij > pos_i} + #{j: neg_ij ==
+ *   pos_i} / 2 (compared in fp32); rr: device fp32 [B] receives 1 / rank_i; mrr: device fp32
+ *   scalar, the mean of rr.  B >= 1, K >= 1, ld >= K + 1 (else GSB_ERR_ARG).  Caller-owned
+ *   memory, asynchronous on stream. */
+gsb_status gsb_lp_mrr(const float* scores, int64_t ld, int64_t B, int32_t K, float* rr, float* mrr, void* stream);
+
 /* General LP score + loss (App. A).  Negative j of positive i is
  *   neg_mode 0 (sampled): row ineg[(i / group) * K + j]   (joint / local joint: group = K;
  *                          uniform: group = 1)

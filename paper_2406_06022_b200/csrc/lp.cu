@@ -210,6 +210,31 @@ __global__ void __launch_bounds__(1024) lp_mean_kernel(const float* __restrict__
     }
 }
 
+// MRR (R-mrr): warp per positive, lanes over its K negatives; rank = 1 + #higher +
+// #equal / 2 (counts exact, compared in the scores' own fp32), rr = 1 / rank
+__global__ void __launch_bounds__(256) lp_rr_kernel(const float* __restrict__ scores, int64_t ld, int64_t B, int K,
+                                                    float* __restrict__ rr) {
+    GSB_PDL_ENTRY();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < B; i += warps) {
+        const float* row = scores + i * ld;
+        const float pos = row[0];
+        int gt = 0, eq = 0;
+        for (int j = 1 + lane; j <= K; j += 32) {
+            const float x = row[j];
+            gt += x > pos;
+            eq += x == pos;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            gt += __shfl_xor_sync(0xffffffffu, gt, o);
+            eq += __shfl_xor_sync(0xffffffffu, eq, o);
+        }
+        if (lane == 0) rr[i] = 1.f / (1.f + (float)gt + 0.5f * (float)eq);
+    }
+}
+
 
 // ------------------------------------------------------------------------------------
 // In-batch negatives as dense contractions (App. A.2.1): with U = H[iu], V = H[iv]
@@ -429,6 +454,15 @@ gsb_status gsb_lp_score_ex(const float* H, int64_t n_rows_cap, int32_t d, const 
                    dH, drel);
     }
     GSB_LAUNCH("lp_mean", lp_mean_kernel, 1, 1024, 0, s, row_loss_ws, B, loss);
+    return GSB_OK;
+}
+
+gsb_status gsb_lp_mrr(const float* scores, int64_t ld, int64_t B, int32_t K, float* rr, float* mrr, void* stream) {
+    GSB_CHECK_ARG(scores && rr && mrr, "null argument");
+    GSB_CHECK_ARG(B >= 1 && K >= 1 && ld >= (int64_t)K + 1, "B %lld, K %d, ld %lld", (long long)B, K, (long long)ld);
+    cudaStream_t s = (cudaStream_t)stream;
+    GSB_LAUNCH("lp_rr", lp_rr_kernel, grid_for(B * 32, 256, kNumSMs * 8), 256, 0, s, scores, ld, B, (int)K, rr);
+    GSB_LAUNCH("lp_mean", lp_mean_kernel, 1, 1024, 0, s, rr, B, mrr);
     return GSB_OK;
 }
 

@@ -740,6 +740,17 @@ class LPTrainer(_TrainerBase):
              _ptr(self.score_ws), self.score_ws.numel(), s)
         self._backward_layers(s)
 
+    def mrr(self, stream=None) -> torch.Tensor:
+        """MRR (R-mrr) of the last step's scores (each positive ranked among its K
+        negatives; gsb_lp_mrr).  Returns a device fp32 scalar; per-positive reciprocal
+        ranks in self.rr."""
+        if not hasattr(self, "rr"):
+            self.rr = torch.empty(self.B, dtype=torch.float32, device=self.scores.device)
+            self.mrr_dev = torch.empty(1, dtype=torch.float32, device=self.scores.device)
+        call("gsb_lp_mrr", _ptr(self.scores), self.scores.shape[1], self.B, self.K, _ptr(self.rr),
+             _ptr(self.mrr_dev), _stream(stream))
+        return self.mrr_dev
+
     def load_inputs(self, u: torch.Tensor, v: torch.Tensor):
         self.pos_u.copy_(u, non_blocking=True)
         self.pos_v.copy_(v, non_blocking=True)

@@ -172,6 +172,10 @@ def test_lp_step_parity(lp_pair, torch_cuda):
         assert np.array_equal(tr.seeds[:ns].cpu().numpy(), res.extra["seeds"])
         close(tr.scores.cpu().numpy(), res.extra["scores"], what=f"step {step} scores")
         close(tr.loss.cpu().numpy()[0], res.loss, what="loss")
+        # MRR of this step's scores: the same fp32 scores on both sides (R-mrr)
+        rr_o, mrr_o = oracle.lp_mrr(tr.scores.cpu().numpy())
+        close(tr.mrr().cpu().numpy()[0], mrr_o, what="MRR")
+        assert np.array_equal(np.rint(2 / tr.rr.cpu().numpy()), np.rint(2 / rr_o))
         slack = check_grads(tr, res, cfg, step)
         tr.optimizer_step()
         for k in synth.param_order(cfg):
@@ -216,3 +220,24 @@ def test_lp_pipelined_matches_oracle(lp_pair, torch_cuda):
         check_grads(tr, res, cfg, step)
         for k in synth.param_order(cfg):
             oracle.adam(params[k], res.grads[k], opt[k]["m"], opt[k]["v"], cfg.lr, step + 1)
+
+
+@pytest.mark.parametrize("B,K,ld", [(1, 1, 2), (1000, 32, 33), (77, 100, 104), (4096, 4095, 4096)])
+def test_lp_mrr_parity(torch_cuda, B, K, ld):
+    """gsb_lp_mrr vs oracle.lp_mrr (R-mrr) on scores with many exact ties (small integers)
+    and ragged widths; ranks compared exactly (2 * rank is an integer), MRR within 1e-5."""
+    import torch
+    from paper_2406_06022_b200._lib import GsbError, call
+    rng = np.random.default_rng(B + K)
+    S = rng.integers(-3, 4, size=(B, ld)).astype(np.float32)
+    S[: B // 2] += rng.normal(size=(B // 2, ld)).astype(np.float32)     # half the rows tie-free
+    St = torch.from_numpy(S).cuda()
+    rr = torch.empty(B, dtype=torch.float32, device="cuda")
+    m = torch.empty(1, dtype=torch.float32, device="cuda")
+    call("gsb_lp_mrr", C.c_void_p(St.data_ptr()), ld, B, K, C.c_void_p(rr.data_ptr()), C.c_void_p(m.data_ptr()), None)
+    rr_o, m_o = oracle.lp_mrr(S[:, : K + 1])
+    assert np.array_equal(np.rint(2 / rr.cpu().numpy()), np.rint(2 / rr_o))
+    close(m.cpu().numpy()[0], m_o, what="MRR")
+    with pytest.raises(GsbError):
+        call("gsb_lp_mrr", C.c_void_p(St.data_ptr()), K, B, K, C.c_void_p(rr.data_ptr()), C.c_void_p(m.data_ptr()),
+             None)
