@@ -287,6 +287,27 @@ def sparse_adagrad(E: np.ndarray, state: np.ndarray, rows: np.ndarray, grad: np.
     lib().oracle_sparse_adagrad(len(rows), E.shape[1], _p(rows), _p(grad), _p(E), _p(state), lr, eps)
 
 
+def sparse_adagrad_dist(E: np.ndarray, state: np.ndarray, rows_per_rank, grads_per_rank, lr: float,
+                        eps: float = 1e-10):
+    """Data-parallel sparse update of a table partitioned over N ranks (§8(f) f1 with §8(e);
+    reading R-sparsedist): the gradient of row x is the mean over ranks of the rank's dEmb row
+    (a rank that did not touch x contributes 0; dense gradients are mean-all-reduced the same
+    way), and each touched row takes ONE Adagrad step (sparse_adagrad) with it.  Row
+    ownership does not enter the result.  rows_per_rank[r]: distinct local rows of rank r."""
+    N = len(rows_per_rank)
+    acc: Dict[int, np.ndarray] = {}
+    for rows, grads in zip(rows_per_rank, grads_per_rank):
+        rows = np.asarray(rows, np.int64)
+        assert len(np.unique(rows)) == len(rows)
+        for x, gr in zip(rows, np.asarray(grads, np.float64)):
+            acc[int(x)] = acc.get(int(x), 0.0) + gr
+    if not acc:
+        return
+    touched = np.array(sorted(acc), np.int64)
+    g = np.stack([acc[int(x)] / N for x in touched])
+    sparse_adagrad(E, state, touched, g, lr, eps)
+
+
 def encoder_bwd(g: Graph, params: Dict[str, np.ndarray], gids: np.ndarray, dH0: np.ndarray) -> Dict[str, np.ndarray]:
     """dWin_t = sum over input rows i of type t of F_t[local(i)]^T dH0[i] (H0 = X Win_t is
     linear in Win_t); frozen tables get no gradient."""

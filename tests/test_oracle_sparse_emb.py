@@ -64,3 +64,41 @@ def test_embedding_gradient_is_dH0_rows_by_finite_differences():
             E[rows[r], k] = old
             fd = (lp - lm) / (2 * h)
             assert abs(fd - g[r, k]) <= 1e-6 * max(1.0, abs(g[r, k])) + 1e-9, (t, r, k, fd, g[r, k])
+
+
+def test_sparse_adagrad_dist_pins():
+    """R-sparsedist: N ranks' sparse gradients -> one Adagrad step per touched row with the
+    mean over ranks.  Pinned by (a) N = 1 equals sparse_adagrad, (b) N identical ranks equal
+    one rank, (c) torch.optim.Adagrad on the dense table fed the mean of the ranks' dense
+    gradients (zero rows elsewhere), over three steps with overlapping row sets."""
+    rng = np.random.default_rng(11)
+    N, d, lr, eps = 50, 8, 0.1, 1e-10
+    E0 = rng.normal(size=(N, d))
+    rows = np.array([4, 9, 33])
+    g = rng.normal(size=(3, d))
+    Ea, sa = E0.copy(), np.zeros((N, d))
+    Eb, sb = E0.copy(), np.zeros((N, d))
+    oracle.sparse_adagrad(Ea, sa, rows, g, lr, eps)
+    oracle.sparse_adagrad_dist(Eb, sb, [rows], [g], lr, eps)
+    assert np.array_equal(Ea, Eb) and np.array_equal(sa, sb)
+    Ec, sc = E0.copy(), np.zeros((N, d))
+    oracle.sparse_adagrad_dist(Ec, sc, [rows] * 4, [g] * 4, lr, eps)
+    assert np.allclose(Ec, Ea, rtol=0, atol=1e-15) and np.allclose(sc, sa, rtol=0, atol=1e-15)
+
+    W = 3
+    E, st = E0.copy(), np.zeros((N, d))
+    T = torch.tensor(E0.copy(), requires_grad=True)
+    opt = torch.optim.Adagrad([T], lr=lr, eps=eps)
+    for step in range(3):
+        rr = [rng.choice(N, size=int(rng.integers(5, 20)), replace=False) for _ in range(W)]
+        gg = [rng.normal(size=(len(r), d)) for r in rr]
+        dense = np.zeros((N, d))
+        for r, x in zip(rr, gg):
+            dense[r] += x / W
+        oracle.sparse_adagrad_dist(E, st, rr, gg, lr, eps)
+        opt.zero_grad()
+        T.grad = torch.tensor(dense)
+        opt.step()
+        assert np.allclose(E, T.detach().numpy(), rtol=1e-12, atol=1e-12), step
+    untouched = np.setdiff1d(np.arange(N), np.concatenate(rr))
+    assert untouched.size == 0 or np.isfinite(E[untouched]).all()
