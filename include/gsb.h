@@ -323,6 +323,30 @@ gsb_status gsb_sparse_emb_fwd(gsb_blocks_t b, const void* arena, int32_t ntype, 
 gsb_status gsb_sparse_adagrad(gsb_blocks_t b, const void* arena, int32_t ntype, float* E, float* state,
                               const float* dH0, int32_t d, float lr, float eps, void* stream);
 
+/* Tables partitioned over the N GPUs of one box (§8(e) with §8(f) f1; reading R-sparsedist:
+ * the gradient of a row is the mean over ranks of the ranks' dEmb rows, and the owner takes
+ * one Adagrad step with it).  bounds: host int64 [world+1], rank w owns local rows
+ * [bounds[w], bounds[w+1]) of ntype t (bounds[0] = 0, bounds[world] = count of t), world <= 8.
+ * Pointer arrays are host arrays of world device pointers: this rank's own buffers and the
+ * peers' (IPC-mapped, gsb_ipc_open), each shard row-major [bounds[w+1]-bounds[w]][d] fp32.
+ * gsb_sparse_emb_fwd_peers: H0[i] = E_w[x - bounds[w]] for every layer-0 input row i of type t
+ *   (x its local id, w its owner): loads over NVLink.
+ * gsb_sparse_emb_push: G_w[x - bounds[w]] += scale * dH0[i] (fp32 atomics, over NVLink for
+ *   peers) and bit (x - bounds[w]) set in touched_w (uint32 words, bit k of word j = row
+ *   32 j + k).  scale = 1 / world for the mean.  G and touched are zero between steps.
+ * gsb_sparse_adagrad_apply (owner, on its own shard of n_rows rows): for every set bit,
+ *   state += g^2, E -= lr g / (sqrt(state) + eps) with g the G row; then the G row and the bit
+ *   are zeroed.  Untouched rows do not move.
+ * Ordering: every rank's push must complete before any owner's apply, and every apply before
+ * the next fwd reads the shards: the caller puts a cross-rank barrier (NCCL) between them. */
+gsb_status gsb_sparse_emb_fwd_peers(gsb_blocks_t b, const void* arena, int32_t ntype, int32_t world,
+                                    const int64_t* bounds, void* const* E, int32_t d, float* H0, void* stream);
+gsb_status gsb_sparse_emb_push(gsb_blocks_t b, const void* arena, int32_t ntype, int32_t world, const int64_t* bounds,
+                               void* const* G, void* const* touched, const float* dH0, int32_t d, float scale,
+                               void* stream);
+gsb_status gsb_sparse_adagrad_apply(float* E, float* state, float* G, uint32_t* touched, int64_t n_rows, int32_t d,
+                                    float lr, float eps, void* stream);
+
 /* ======================================================================================
  * Feature construction for featureless nodes (Eq. 1).
  *   F'_v = f(F_u, u in N(v)) with f = average (R-eq1): every in-edge u -> v of every stored

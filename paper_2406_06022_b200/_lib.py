@@ -89,6 +89,9 @@ SIGS = {
     "gsb_lp_score_ex": [P, i64, i32, P, P, P, i64, i32, i32, i32, P, i32, P, P, P, P, P, P, P, C.c_size_t, P],
     "gsb_lp_score_ws_bytes": [i64, i32, i32, P],
     "gsb_lp_mrr": [P, i64, i64, i32, P, P, P],
+    "gsb_sparse_emb_fwd_peers": [P, P, i32, i32, P, P, i32, P, P],
+    "gsb_sparse_emb_push": [P, P, i32, i32, P, P, P, P, i32, f32, P],
+    "gsb_sparse_adagrad_apply": [P, P, P, P, i64, i32, f32, f32, P],
 }
 _RET = {"gsb_last_error": C.c_char_p, "gsb_version": i32, "gsb_launch_count": i64}
 

@@ -88,3 +88,59 @@ def test_sparse_embedding_steps(torch_cuda, use_graph):
             # continue both sides from the GPU's table / state (steps compared one at a time)
             params[f"Emb{t}"] = E_gpu.copy()
             state[t] = tr.emb[t][1].cpu().numpy().astype(np.float64)
+
+
+def test_partitioned_embedding_two_ranks_one_gpu(torch_cuda):
+    """R-sparsedist on one GPU: two samplers play two ranks, the table of ntype 0 is split in two
+    shards (separate allocations, as two ranks would hold them); forward reads each input row
+    from its owner's shard, both ranks push 1/2 of their dH0 rows into the owners' accumulators,
+    each owner applies Adagrad.  Expected: oracle.sparse_adagrad_dist over the two ranks' rows,
+    two steps (the second on the updated table)."""
+    import ctypes as C
+    import torch
+    from paper_2406_06022_b200._lib import call
+    from paper_2406_06022_b200.runtime import MiniBatchSampler
+    cfg = synth.tiny()
+    st = gpu_store(cfg)
+    t, d, W = 0, 64, 2
+    n = int(cfg.counts[t])
+    bounds = np.array([0, 2077, n], np.int64)
+    rng = np.random.default_rng(5)
+    E_full = rng.normal(size=(n, d)).astype(np.float32)
+    E = [torch.from_numpy(E_full[bounds[w]:bounds[w + 1]].copy()).cuda() for w in range(W)]
+    S = [torch.zeros_like(e) for e in E]
+    G = [torch.zeros_like(e) for e in E]
+    bits = [torch.zeros((int(bounds[w + 1] - bounds[w]) + 31) // 32, dtype=torch.int32, device="cuda")
+            for w in range(W)]
+    ptrs = lambda ts: (C.c_void_p * W)(*[t_.data_ptr() for t_ in ts])
+    bnd = bounds.ctypes.data_as(C.c_void_p)
+    sms = [MiniBatchSampler(st, cfg.fanouts, max_seeds=cfg.batch) for _ in range(W)]
+    E64, S64 = E_full.astype(np.float64), np.zeros((n, d))
+    for step in range(2):
+        rows_r, grads_r, dH0s = [], [], []
+        E_cur = torch.cat(E).cpu().numpy()          # the sharded table as the GPU holds it
+        for r, sm in enumerate(sms):
+            sm.sample(torch.from_numpy(synth.nc_seeds(cfg, 2 * step + r)).cuda(), cfg.rng_seed, step)
+            gid = sm.block(0).src_gid.cpu().numpy()
+            pos = np.nonzero((gid >= cfg.node_off[t]) & (gid < cfg.node_off[t + 1]))[0]
+            H0 = torch.zeros((sm.input_rows(), d), dtype=torch.float32, device="cuda")
+            call("gsb_sparse_emb_fwd_peers", sm.h, C.c_void_p(sm.arena.data_ptr()), t, W, bnd, ptrs(E), d,
+                 C.c_void_p(H0.data_ptr()), None)
+            assert np.array_equal(H0.cpu().numpy()[pos], E_cur[gid[pos] - cfg.node_off[t]]), step
+            dH0 = rng.normal(size=(sm.input_rows(), d)).astype(np.float32)
+            dH0s.append(torch.from_numpy(dH0).cuda())
+            rows_r.append(gid[pos] - cfg.node_off[t])
+            grads_r.append(dH0[pos].astype(np.float64))
+        for r, sm in enumerate(sms):
+            call("gsb_sparse_emb_push", sm.h, C.c_void_p(sm.arena.data_ptr()), t, W, bnd, ptrs(G), ptrs(bits),
+                 C.c_void_p(dH0s[r].data_ptr()), d, 1.0 / W, None)
+        for w in range(W):
+            call("gsb_sparse_adagrad_apply", C.c_void_p(E[w].data_ptr()), C.c_void_p(S[w].data_ptr()),
+                 C.c_void_p(G[w].data_ptr()), C.c_void_p(bits[w].data_ptr()), int(bounds[w + 1] - bounds[w]), d,
+                 LR, EPS, None)
+        oracle.sparse_adagrad_dist(E64, S64, rows_r, grads_r, LR, EPS)
+        got_E = torch.cat(E).cpu().numpy()
+        got_S = torch.cat(S).cpu().numpy()
+        close(got_S, S64, what=f"step {step} Adagrad state")
+        close(got_E, E64, what=f"step {step} table")
+        assert all(int(b.abs().sum()) == 0 for b in bits) and all(float(g.abs().sum()) == 0 for g in G)
