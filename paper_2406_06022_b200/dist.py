@@ -144,3 +144,87 @@ class PeerFeatures:
         store.feat_dim = dim
         store.feat_dtype = self.shards[0].dtype
         self.store = store
+
+
+class PeerEmbedding:
+    """A learnable table (§8(f) f1) partitioned over the ranks of one box (R-sparsedist): rank
+    w holds rows [bounds[w], bounds[w+1]) of the table, its Adagrad state, a gradient
+    accumulator and a touched bitmap; the table, accumulator and bitmap shards of every rank
+    are mapped into every process with CUDA IPC.  Forward loads each input row from its owner
+    (gsb_sparse_emb_fwd_peers); the update pushes 1/world of every touched dH0 row into the
+    owner's accumulator (gsb_sparse_emb_push), then -- after a barrier -- every owner takes one
+    Adagrad step per touched row (gsb_sparse_adagrad_apply); a second barrier orders the
+    update before the next forward.  The barriers are 1-element NCCL all-reduces on the
+    compute stream (device-side ordering, no host sync)."""
+
+    def __init__(self, E_full, world: int, rank: int, group=None):
+        import ctypes as C
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        from ._lib import call
+        n, d = int(E_full.shape[0]), int(E_full.shape[1])
+        self.world, self.rank, self.group, self.d = world, rank, group, d
+        self.bounds = np.array([n * w // world for w in range(world + 1)], np.int64)
+        lo, hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
+        dev = torch.device("cuda", torch.cuda.current_device())
+        rows = max(hi - lo, 1)
+        self.E = torch.zeros((rows, d), dtype=torch.float32, device=dev)
+        self.E[: hi - lo].copy_(E_full[lo:hi])
+        self.state = torch.zeros_like(self.E)
+        self.G = torch.zeros_like(self.E)
+        self.bits = torch.zeros((rows + 31) // 32, dtype=torch.int32, device=dev)
+        self.n_rows = hi - lo
+        self.tok = torch.zeros(1, dtype=torch.float32, device=dev)
+        mine = []
+        for t in (self.E, self.G, self.bits):
+            h = (C.c_char * 64)()
+            off = C.c_int64()
+            call("gsb_ipc_handle", C.c_void_p(t.data_ptr()), h, C.byref(off))
+            mine.append((bytes(h), int(off.value)))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self.ptrs = []
+        self.mapped = []
+        for k, own in enumerate((self.E, self.G, self.bits)):
+            arr = (C.c_void_p * world)()
+            for w in range(world):
+                if w == rank:
+                    arr[w] = own.data_ptr()
+                else:
+                    hb, off = allh[w][k]
+                    p = C.c_void_p()
+                    call("gsb_ipc_open", (C.c_char * 64).from_buffer_copy(hb), off, C.byref(p))
+                    arr[w] = p.value
+                    self.mapped.append(p.value - off)
+            self.ptrs.append(arr)
+        self._bnd = self.bounds.ctypes.data_as(C.c_void_p)
+
+    def barrier(self):
+        import torch.distributed as dist
+        dist.all_reduce(self.tok, group=self.group)
+
+    def fwd(self, sampler, ntype: int, H0, stream):
+        import ctypes as C
+        from ._lib import call
+        call("gsb_sparse_emb_fwd_peers", sampler.h, C.c_void_p(sampler.arena.data_ptr()), ntype, self.world,
+             self._bnd, self.ptrs[0], self.d, C.c_void_p(H0.data_ptr()), stream)
+
+    def update(self, sampler, ntype: int, dH0, lr: float, eps: float, stream):
+        import ctypes as C
+        from ._lib import call
+        call("gsb_sparse_emb_push", sampler.h, C.c_void_p(sampler.arena.data_ptr()), ntype, self.world, self._bnd,
+             self.ptrs[1], self.ptrs[2], C.c_void_p(dH0.data_ptr()), self.d, 1.0 / self.world, stream)
+        self.barrier()
+        call("gsb_sparse_adagrad_apply", C.c_void_p(self.E.data_ptr()), C.c_void_p(self.state.data_ptr()),
+             C.c_void_p(self.G.data_ptr()), C.c_void_p(self.bits.data_ptr()), self.n_rows, self.d, lr, eps, stream)
+        self.barrier()
+
+    def gather_full(self):
+        """The whole table (all shards) on every rank, for checks: NCCL all-gather."""
+        import torch
+        import torch.distributed as dist
+        parts = [torch.zeros((max(int(self.bounds[w + 1] - self.bounds[w]), 1), self.d), device=self.E.device)
+                 for w in range(self.world)]
+        dist.all_gather(parts, self.E, group=self.group)
+        return torch.cat([p[: int(self.bounds[w + 1] - self.bounds[w])] for w, p in enumerate(parts)])

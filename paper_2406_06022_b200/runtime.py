@@ -33,6 +33,13 @@ def _require_cuda():
         raise _lib.GsbError("libgsb needs a CUDA device (there is no CPU fallback)")
 
 
+class _PeerTable:
+    """Marker for a learnable table held by a dist.PeerEmbedding (partitioned over ranks)."""
+
+    def __init__(self, pe):
+        self.pe = pe
+
+
 class GraphStore:
     """Per-etype CSC + per-ntype feature tables resident in HBM."""
 
@@ -357,7 +364,10 @@ class _TrainerBase:
             call("gsb_encoder_fwd", sm.h, _ptr(sm.arena), self._win, self.d_in[0], _ptr(self.H0), _ptr(self.enc_ws),
                  self.enc_ws.numel(), s)
             for t, (E, _) in self.emb.items():     # f1: learnable tables replace the frozen rows
-                call("gsb_sparse_emb_fwd", sm.h, _ptr(sm.arena), t, _ptr(E), self.d_in[0], _ptr(self.H0), s)
+                if isinstance(E, _PeerTable):
+                    E.pe.fwd(sm, t, self.H0, s)
+                else:
+                    call("gsb_sparse_emb_fwd", sm.h, _ptr(sm.arena), t, _ptr(E), self.d_in[0], _ptr(self.H0), s)
             h = self.H0
         elif self.exchange is not None:   # partitioned features: NCCL all-to-all fetch (C4/C5)
             gids, n = sm.input_gids()
@@ -397,21 +407,29 @@ class _TrainerBase:
             call("gsb_encoder_bwd", sm.h, _ptr(sm.arena), self._win, _ptr(self.dH0), self.d_in[0], self._dwin,
                  _ptr(self.enc_ws), self.enc_ws.numel(), s)
 
-    def set_embedding(self, ntype: int, E: torch.Tensor, lr: float = 0.01, eps: float = 1e-10):
+    def set_embedding(self, ntype: int, E: torch.Tensor, lr: float = 0.01, eps: float = 1e-10, peers=None):
         """Make ntype's input rows a learnable table (§8(f) f1): E fp32 [N_t][d_in0] (copied),
         trained by sparse Adagrad on the rows each mini-batch touches (gsb_sparse_adagrad).
-        Needs the input-encoder path (H0) and a non-projected ntype; one GPU holds the table."""
+        Needs the input-encoder path (H0) and a non-projected ntype.  peers: a
+        dist.PeerEmbedding holding the table partitioned over the ranks (R-sparsedist);
+        otherwise this GPU holds all of it."""
         if not self.enc_types or ntype in self.enc_types:
             raise _lib.GsbError("learnable embeddings need the encoder path and a non-projected ntype")
-        E = E.to(self.device, torch.float32).contiguous().clone()
         if E.shape != (int(self.store.counts[ntype]), self.d_in[0]):
             raise _lib.GsbError(f"embedding table shape {tuple(E.shape)}")
-        self.emb[ntype] = (E, torch.zeros_like(E))
+        if peers is not None:
+            self.emb[ntype] = (_PeerTable(peers), None)
+        else:
+            E = E.to(self.device, torch.float32).contiguous().clone()
+            self.emb[ntype] = (E, torch.zeros_like(E))
         self.emb_lr, self.emb_eps = lr, eps
 
     def _sparse_update(self, stream=None):
         sm = self.sampler
         for t, (E, st) in self.emb.items():
+            if isinstance(E, _PeerTable):
+                E.pe.update(sm, t, self.dH0, self.emb_lr, self.emb_eps, _stream(stream))
+                continue
             call("gsb_sparse_adagrad", sm.h, _ptr(sm.arena), t, _ptr(E), _ptr(st), _ptr(self.dH0), self.d_in[0],
                  self.emb_lr, self.emb_eps, _stream(stream))
 

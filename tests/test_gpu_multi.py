@@ -134,3 +134,78 @@ def test_two_gpu_partitioned_features(feat_dtype):
     expW1 = exp[o:o + shapes["W1"]].reshape(out["peer_grad0"].shape)
     close(out["peer_grad0"], expW1, what="peer all-reduced grad W1")
     np.testing.assert_array_equal(out["peer_W1_0"], out["peer_W1_1"])
+
+
+def _emb_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device(f"cuda:{rank}"))
+    import synth
+    from paper_2406_06022_b200 import build
+    build.build()
+    from paper_2406_06022_b200.dist import PeerEmbedding, rank_step
+    from paper_2406_06022_b200.runtime import RGCNTrainer
+    from tests._pair import gpu_store
+    cfg = synth.scaled(synth.tiny_enc(), 0.5, "tiny_enc_half")
+    dev = f"cuda:{rank}"
+    st = gpu_store(cfg, device=dev)
+    tr = RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
+                     synth.param_order(cfg), torch.from_numpy(synth.labels(cfg)),
+                     int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
+    emb_t = [t for t in range(cfg.num_ntypes) if not cfg.project[t]]
+    pes = {}
+    for t in emb_t:
+        E = np.random.default_rng(100 + t).normal(scale=0.3, size=(cfg.counts[t], cfg.feat_dim)).astype(np.float32)
+        pes[t] = PeerEmbedding(torch.from_numpy(E).to(dev), world, rank)
+        tr.set_embedding(t, torch.from_numpy(E), lr=0.01, eps=1e-10, peers=pes[t])
+    step = rank_step(0, rank, world)
+    tr.forward_backward(torch.from_numpy(synth.nc_seeds(cfg, step)).to(dev), step)
+    torch.cuda.synchronize()
+    gid = tr.sampler.block(0).src_gid.cpu().numpy()
+    out["gid%d" % rank] = gid
+    out["H0_%d" % rank] = tr.H0[: len(gid)].cpu().numpy().copy()
+    out["dH0_%d" % rank] = tr.dH0[: len(gid)].cpu().numpy().copy()
+    tr._sparse_update()
+    for t in emb_t:
+        out["E%d_%d" % (t, rank)] = pes[t].gather_full().cpu().numpy()
+        out["bits_clear%d_%d" % (t, rank)] = int(pes[t].bits.abs().sum().item()) == 0
+    torch.cuda.synchronize()
+    dist.barrier()
+    del tr, pes
+    dist.destroy_process_group()
+
+
+def test_two_gpu_partitioned_embeddings():
+    """Learnable tables partitioned over 2 GPUs (§8(f) f1 with §8(e); R-sparsedist): each rank's
+    H0 rows are the table's rows read from their owners over NVLink, and after one sparse update
+    (push over NVLink, barrier, owner Adagrad) every rank sees the table the oracle's
+    sparse_adagrad_dist gives from the two ranks' dH0 rows."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
+    import torch.multiprocessing as mp
+    import oracle
+    import synth
+    from tests._pair import close
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_emb_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    cfg = synth.scaled(synth.tiny_enc(), 0.5, "tiny_enc_half")
+    for t in [t for t in range(cfg.num_ntypes) if not cfg.project[t]]:
+        E0 = np.random.default_rng(100 + t).normal(scale=0.3, size=(cfg.counts[t], cfg.feat_dim))
+        E0 = E0.astype(np.float32).astype(np.float64)
+        rows_r, grads_r = [], []
+        for r in range(2):
+            gid = out["gid%d" % r]
+            pos = np.nonzero((gid >= cfg.node_off[t]) & (gid < cfg.node_off[t + 1]))[0]
+            assert len(pos) > 0
+            assert np.array_equal(out["H0_%d" % r][pos], E0[gid[pos] - cfg.node_off[t]].astype(np.float32))
+            rows_r.append(gid[pos] - cfg.node_off[t])
+            grads_r.append(out["dH0_%d" % r][pos].astype(np.float64))
+        E, S = E0.copy(), np.zeros_like(E0)
+        oracle.sparse_adagrad_dist(E, S, rows_r, grads_r, 0.01, 1e-10)
+        for r in range(2):
+            assert out["bits_clear%d_%d" % (t, r)]
+            close(out["E%d_%d" % (t, r)], E, what=f"Emb{t} after the partitioned update (rank {r})")
