@@ -291,7 +291,14 @@ def build_gsb(cfg, device, partition=None, mode="peer"):
     if LP_OPTS["learnable_emb"] and getattr(tr, "enc_types", None):
         for t in range(cfg.num_ntypes):
             if not cfg.project[t]:     # init = the frozen table, widened to fp32
-                tr.set_embedding(t, synth.feature_table(cfg, t, backend="torch", device=device).float())
+                E = synth.feature_table(cfg, t, backend="torch", device=device).float()
+                pe = None
+                if partition is not None and partition[0] > 1:   # N > 1: partitioned over the ranks
+                    from paper_2406_06022_b200.dist import PeerEmbedding
+                    pe = PeerEmbedding(E, partition[0], partition[1])
+                    tr._peer_emb = getattr(tr, "_peer_emb", []) + [pe]
+                tr.set_embedding(t, E, peers=pe)
+                del E
     tr.exchange = ex
     return st, tr
 

@@ -52,7 +52,7 @@ __global__ void emb_adagrad_kernel(const HopMeta* __restrict__ m, const int64_t*
 // w owns local rows [lo[w], lo[w+1]) of the table and its Adagrad state, plus a gradient
 // accumulator G_w (zero between steps) and a touched bitmap; peers' shards are IPC-mapped.
 //   fwd:   H0[i] = E_{owner}[x - lo[owner]]                          (NVLink loads)
-//   push:  G_{owner}[x - lo] += scale * dH0[i]; set bit x - lo        (NVLink red.add / atomicOr)
+//   push:  G_{owner}[x - lo] += scale * dH0[i]; set bit x - lo        (NVLink red.add.v4 / atomicOr)
 //   apply: owner, every set bit: Adagrad with G row, then zero G row and the bit
 // push and apply are separated by a cross-rank barrier (caller), as are apply and the next fwd.
 // ------------------------------------------------------------------------------------
@@ -97,11 +97,7 @@ __global__ void emb_push_kernel(const HopMeta* __restrict__ m, const int64_t* __
         const int w = emb_owner(P, x);
         const int64_t l = x - P.lo[w];
         const float4 g = __ldg(reinterpret_cast<const float4*>(dH0 + row * d) + c);
-        float* o = P.G[w] + l * d + 4 * c;
-        atomicAdd(o, scale * g.x);
-        atomicAdd(o + 1, scale * g.y);
-        atomicAdd(o + 2, scale * g.z);
-        atomicAdd(o + 3, scale * g.w);
+        red_add_f4(P.G[w] + l * d + 4 * c, make_float4(scale * g.x, scale * g.y, scale * g.z, scale * g.w));
         if (c == 0) atomicOr(P.bits[w] + (l >> 5), 1u << (l & 31));
     }
 }

@@ -210,14 +210,25 @@ class PeerEmbedding:
         call("gsb_sparse_emb_fwd_peers", sampler.h, C.c_void_p(sampler.arena.data_ptr()), ntype, self.world,
              self._bnd, self.ptrs[0], self.d, C.c_void_p(H0.data_ptr()), stream)
 
-    def update(self, sampler, ntype: int, dH0, lr: float, eps: float, stream):
+    def push(self, sampler, ntype: int, dH0, stream):
         import ctypes as C
         from ._lib import call
         call("gsb_sparse_emb_push", sampler.h, C.c_void_p(sampler.arena.data_ptr()), ntype, self.world, self._bnd,
              self.ptrs[1], self.ptrs[2], C.c_void_p(dH0.data_ptr()), self.d, 1.0 / self.world, stream)
-        self.barrier()
+
+    def apply(self, lr: float, eps: float, stream):
+        import ctypes as C
+        from ._lib import call
         call("gsb_sparse_adagrad_apply", C.c_void_p(self.E.data_ptr()), C.c_void_p(self.state.data_ptr()),
              C.c_void_p(self.G.data_ptr()), C.c_void_p(self.bits.data_ptr()), self.n_rows, self.d, lr, eps, stream)
+
+    def update(self, sampler, ntype: int, dH0, lr: float, eps: float, stream, pushed: bool = False):
+        """push -> barrier -> apply -> barrier.  pushed: the push was issued before a collective
+        that already separates it from the apply (the dense-gradient all-reduce)."""
+        if not pushed:
+            self.push(sampler, ntype, dH0, stream)
+            self.barrier()
+        self.apply(lr, eps, stream)
         self.barrier()
 
     def gather_full(self):

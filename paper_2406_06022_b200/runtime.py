@@ -424,11 +424,21 @@ class _TrainerBase:
             self.emb[ntype] = (E, torch.zeros_like(E))
         self.emb_lr, self.emb_eps = lr, eps
 
+    def _peer_push(self, stream=None):
+        """N > 1: push the partitioned tables' gradients before the dense all-reduce, which
+        then doubles as the barrier between every rank's push and the owners' apply."""
+        for t, (E, _) in self.emb.items():
+            if isinstance(E, _PeerTable):
+                E.pe.push(self.sampler, t, self.dH0, _stream(stream))
+                self._pushed = True
+
     def _sparse_update(self, stream=None):
         sm = self.sampler
+        pushed = getattr(self, "_pushed", False)
+        self._pushed = False
         for t, (E, st) in self.emb.items():
             if isinstance(E, _PeerTable):
-                E.pe.update(sm, t, self.dH0, self.emb_lr, self.emb_eps, _stream(stream))
+                E.pe.update(sm, t, self.dH0, self.emb_lr, self.emb_eps, _stream(stream), pushed=pushed)
                 continue
             call("gsb_sparse_adagrad", sm.h, _ptr(sm.arena), t, _ptr(E), _ptr(st), _ptr(self.dH0), self.d_in[0],
                  self.emb_lr, self.emb_eps, _stream(stream))
@@ -476,6 +486,7 @@ class _TrainerBase:
     def replay(self):
         self.graph.replay()
         if self.graph_allreduce is not None:
+            self._peer_push()
             self.graph_allreduce(self.grad)
             self.optimizer_step(t_dev=True)
         self.t += 1
@@ -576,10 +587,18 @@ class _TrainerBase:
             self.pipe_graphs["compute"][b].replay()
         else:
             self._compute_ops()
-        self.ev_c.record(main)
         if self.pipe_allreduce is not None:
+            # the sparse table update (N > 1, after the all-reduce) still reads buffer b's block:
+            # the side stream may overwrite b (batch k+2) only after it
+            if not self.emb:
+                self.ev_c.record(main)
+            self._peer_push()
             self.pipe_allreduce(self.grad)
             self.optimizer_step(t_dev=True)
+            if self.emb:
+                self.ev_c.record(main)
+        else:
+            self.ev_c.record(main)
         self.t += 1
         self.pipe_k += 1
 
