@@ -328,3 +328,36 @@ def test_pipelined_steps_match_oracle(torch_cuda, use_graph, fuse):
         check_grads(tr, res, cfg, step)
         for k in synth.param_order(cfg):
             oracle.adam(params[k], res.grads[k], opt[k]["m"], opt[k]["v"], cfg.lr, step + 1)
+
+
+@pytest.mark.parametrize("n,d,C", [(1024, 128, 349), (37, 128, 8), (300, 64, 153), (65, 32, 512), (129, 96, 33)])
+def test_nc_loss_parity(torch_cuda, n, d, C):
+    """gsb_nc_loss (tcgen05 logits / dh / dWc with split-K, softmax CE with the fused batch
+    mean) against oracle.nc_loss at ragged shapes: loss, dh, dWc, dbc within 1e-5 (R-tol)."""
+    import ctypes as C_
+    import torch
+    from paper_2406_06022_b200._lib import call
+    rng = np.random.default_rng(n + d + C)
+    h = rng.normal(size=(n, d)).astype(np.float32)
+    Wc = (rng.normal(size=(d, C)) / np.sqrt(d)).astype(np.float32)
+    bc = rng.normal(size=C).astype(np.float32) * 0.1
+    y = rng.integers(0, C, size=n).astype(np.int32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    ht, Wt, bt, yt = t(h), t(Wc), t(bc), t(y)
+    gid = torch.arange(n, dtype=torch.int64, device="cuda")
+    ldl = (C + 3) // 4 * 4
+    logits = torch.zeros((n, ldl), dtype=torch.float32, device="cuda")
+    rl = torch.zeros(n + 1024, dtype=torch.float32, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float32, device="cuda")
+    dh = torch.zeros((n, d), dtype=torch.float32, device="cuda")
+    dWc = torch.zeros((d, C), dtype=torch.float32, device="cuda")
+    dbc = torch.zeros(C, dtype=torch.float32, device="cuda")
+    P = lambda x: C_.c_void_p(x.data_ptr())
+    for _ in range(2):      # the second call reuses the ticket word the first one reset
+        call("gsb_nc_loss", P(ht), n, d, P(Wt), P(bt), C, P(yt), P(gid), 0, P(logits), P(rl), P(loss), P(dh), P(dWc),
+             P(dbc), None)
+    ol, _, odh, odW, odb = oracle.nc_loss(h, Wc, bc, y)
+    close(loss.cpu().numpy()[0], ol, what="loss")
+    close(dh.cpu().numpy(), odh, what="dh")
+    close(dWc.cpu().numpy(), odW, what="dWc")
+    close(dbc.cpu().numpy(), odb, what="dbc")
