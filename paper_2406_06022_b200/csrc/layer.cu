@@ -25,7 +25,13 @@ __device__ __forceinline__ const uint4* src_row(const GraphDev& g, const char* h
 
 // FEAT: source rows come from the feature tables via e_src_gid / dst_gid (no x0 buffer)
 template <bool FEAT, bool BF16, int LPE>
-__global__ void __launch_bounds__(256, 4) agg_kernel(GraphDev g, const HopMeta* __restrict__ m,
+#ifndef GSB_AGG_MINB
+#define GSB_AGG_MINB 5
+#endif
+#ifndef GSB_AGG_BPS
+#define GSB_AGG_BPS 5
+#endif
+__global__ void __launch_bounds__(256, GSB_AGG_MINB) agg_kernel(GraphDev g, const HopMeta* __restrict__ m,
                                                   const int64_t* __restrict__ seg_ptr,
                                                   const int32_t* __restrict__ e_src,
                                                   const int64_t* __restrict__ e_src_gid,
@@ -243,7 +249,7 @@ static gsb_status launch_heavy(cudaStream_t s, const GraphDev& g, const HopBufs&
 static gsb_status launch_agg(const char* name, bool feat, int dtype, cudaStream_t s, const GraphDev& g,
                              const HopBufs& hb, const void* h, int d, float* acat, int64_t lda, const int32_t* rowmap,
                              int fanout) {
-    const int grid = grid_for(hb.cap_dst * 32, 256, kNumSMs * 8);
+    const int grid = grid_for(hb.cap_dst * 32, 256, kNumSMs * GSB_AGG_BPS);
     const int rb = d * dtype_size(dtype);
     const char* hc = static_cast<const char*>(h);
     const bool heavy = fanout < 0 || fanout > kSegCap;

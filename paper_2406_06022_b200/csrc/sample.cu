@@ -380,6 +380,9 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
 // piece's first and last edge qualify.  Segments longer than kFillCap are never Floyd draws
 // (those hold c <= fanout <= 32 edges), so every such edge is the copy rule's.
 constexpr int64_t kFillCap = 256;
+#ifndef GSB_FILL_BPS
+#define GSB_FILL_BPS 8
+#endif
 
 __global__ void __launch_bounds__(256) fill_tail_kernel(GraphDev g, const HopMeta* __restrict__ m,
                                                         const int64_t* __restrict__ dst_gid,
@@ -758,7 +761,7 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
         count_launch(2);
         {
             const int G = (f >= 1 && f <= 8) ? 8 : ((f >= 1 && f <= 16) ? 16 : 32);
-            const int grid = grid_for(nseg * G, 256, kNumSMs * 8);
+            const int grid = grid_for(nseg * G, 256, kNumSMs * GSB_FILL_BPS);
             const bool tail = f < 0 || f > kFillCap;
             const int64_t cap = tail ? kFillCap : INT64_MAX;
             if (G == 8)
