@@ -3,11 +3,11 @@
 //
 // Per hop h (frontier D_h, type-grouped):
 //   count   : thread per (dst j, slot s) -> c = min(f, deg'), marks map[gid(j)] = j
-//   scan    : seg_ptr = exclusive_scan(c)                     (CUB, decoupled look-back)
+//   scan    : seg_ptr = exclusive_scan(c)                     (count's block totals + block scans)
 //   fill    : warp per segment; Philox draws on lanes, Floyd resolved with shfl/ballot,
 //             bitonic sort of the chosen ranks, coalesced writes; marks new sources in a
 //             bitmap over the global id space
-//   rank    : popcount prefix over the bitmap                 (CUB)
+//   rank    : popcount prefix over the bitmap                 (block totals, then block scans)
 //   meta    : per-type counts of new sources -> src row offsets (device HopMeta)
 //   relabel : edge src gid -> src row (dst prefix via map, new via bitmap rank)
 //   next    : writes D_{h+1} (dst prefix ++ ascending new) and clears map/bitmap
@@ -239,44 +239,134 @@ __global__ void seed_fin_kernel(int T, int64_t n_cap, const int64_t* __restrict_
 }
 
 // ------------------------------------------------------------------------------------
-// count: thread per (dst j, slot s)
+// count: thread per (dst j, slot s), then seg_ptr = exclusive_scan(cnt) in one more launch.
+// Count block b owns the contiguous chunk [b*chunk, (b+1)*chunk) of the nseg+1 entries (thread
+// per entry, as many blocks as the latency-bound lookups want) and writes its total btot[b]; scan
+// block b owns kScanPerBlock count chunks and adds the totals of the earlier ones (replaces CUB's
+// init + look-back scan, two launches).
 // ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) count_kernel(GraphDev g, const HopMeta* __restrict__ m,
-                                                    const int64_t* __restrict__ dst_gid, int64_t cap_dst, int fanout,
-                                                    Excl ex, int32_t* __restrict__ map, int64_t* __restrict__ cnt,
-                                                    int* __restrict__ err) {
+constexpr int kCntThreads = 256, kCntPer = 8, kCntTile = kCntThreads * kCntPer, kCntMaxBlocks = kNumSMs * 16;
+constexpr int kScanPerBlock = kCntPer;   // count chunks (multiples of kCntThreads entries) per scan block
+
+__device__ __forceinline__ int64_t count_one(const GraphDev& g, int64_t i, int64_t n, int S,
+                                             const int64_t* __restrict__ dst_gid, int fanout, const Excl& ex,
+                                             int32_t* __restrict__ map, int* __restrict__ err) {
+    const int64_t j = i / S;
+    const int s = (int)(i - j * S);
+    if (j >= n) return 0;
+    const int64_t v = dst_gid[j];
+    const int t = type_of(g, v);
+    if (s == 0) {
+        int32_t old = atomicExch(map + v, (int32_t)j);
+        if (old != -1) atomicExch(err, ERR_DUPLICATE);
+    }
+    if (s >= g.n_slots[t]) return 0;
+    const int r = g.slot_etype[t][s];
+    const int64_t vl = v - g.node_off[t];
+    const int64_t a = g.indptr[r][vl];
+    int64_t deg = g.indptr[r][vl + 1] - a;
+    int64_t k0, k1;
+    excl_range(ex, r, v, k0, k1);
+    if (k1 > k0) deg -= excl_count(ex, k0, k1, g.indices[r] + a, deg, g.node_off[g.src_t[r]]);
+    return (fanout < 0 || deg <= fanout) ? deg : fanout;
+}
+
+// block-wide int64 sum over kCntThreads threads (valid in every thread)
+__device__ __forceinline__ int64_t cnt_block_sum(int64_t v, int64_t* red) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int64_t s = 0;
+#pragma unroll
+    for (int w = 0; w < kCntThreads / 32; ++w) s += red[w];
+    __syncthreads();
+    return s;
+}
+
+__global__ void __launch_bounds__(kCntThreads) count_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                            const int64_t* __restrict__ dst_gid, int64_t cap_dst,
+                                                            int fanout, Excl ex, int32_t* __restrict__ map,
+                                                            int64_t* __restrict__ cnt, int64_t chunk,
+                                                            int64_t* __restrict__ btot, int* __restrict__ err) {
     GSB_PDL_ENTRY();
+    __shared__ int64_t red[kCntThreads / 32];
     const int S = g.S;
     const int64_t n = (*(volatile int*)err) ? 0 : m->n_dst;
     const int64_t total = cap_dst * S;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= total; i += stride) {
-        if (i == total) {
-            cnt[i] = 0;
-            continue;
-        }
-        int64_t j = i / S;
-        int s = (int)(i - j * S);
-        int64_t c = 0;
-        if (j < n) {
-            int64_t v = dst_gid[j];
-            int t = type_of(g, v);
-            if (s == 0) {
-                int32_t old = atomicExch(map + v, (int32_t)j);
-                if (old != -1) atomicExch(err, ERR_DUPLICATE);
-            }
-            if (s < g.n_slots[t]) {
-                int r = g.slot_etype[t][s];
-                int64_t vl = v - g.node_off[t];
-                const int64_t a = g.indptr[r][vl];
-                int64_t deg = g.indptr[r][vl + 1] - a;
-                int64_t k0, k1;
-                excl_range(ex, r, v, k0, k1);
-                if (k1 > k0) deg -= excl_count(ex, k0, k1, g.indices[r] + a, deg, g.node_off[g.src_t[r]]);
-                c = (fanout < 0 || deg <= fanout) ? deg : fanout;
-            }
-        }
+    const int64_t i0 = blockIdx.x * chunk, i1 = min(i0 + chunk, total + 1);
+    int64_t sum = 0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += kCntThreads) {
+        const int64_t c = (i == total) ? 0 : count_one(g, i, n, S, dst_gid, fanout, ex, map, err);
         cnt[i] = c;
+        sum += c;
+    }
+    sum = cnt_block_sum(sum, red);
+    if (threadIdx.x == 0) btot[blockIdx.x] = sum;
+}
+
+__global__ void __launch_bounds__(kCntThreads) count_scan_kernel(const int64_t* __restrict__ cnt, int64_t n_ent,
+                                                                 int64_t chunk, const int64_t* __restrict__ btot,
+                                                                 int nb_count, int64_t* __restrict__ seg_ptr) {
+    GSB_PDL_ENTRY();
+    __shared__ int64_t red[kCntThreads / 32];
+    __shared__ int64_t wsum[kCntThreads / 32];
+    int64_t off = 0;
+    const int nprev = min((int)blockIdx.x * kScanPerBlock, nb_count);
+    for (int b = threadIdx.x; b < nprev; b += kCntThreads) off += btot[b];
+    off = cnt_block_sum(off, red);
+    const int64_t i0 = blockIdx.x * chunk, i1 = min(i0 + chunk, n_ent);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t t0 = i0; t0 < i1; t0 += kCntTile) {
+        const int64_t base = t0 + (int64_t)threadIdx.x * kCntPer;
+        int64_t c[kCntPer];
+        if (base + kCntPer <= i1) {
+            const longlong2* p = reinterpret_cast<const longlong2*>(cnt + base);
+#pragma unroll
+            for (int q = 0; q < kCntPer / 2; ++q) {
+                const longlong2 x = p[q];
+                c[2 * q] = x.x;
+                c[2 * q + 1] = x.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kCntPer; ++k) c[k] = (base + k < i1) ? cnt[base + k] : 0;
+        }
+        int64_t v = 0;
+#pragma unroll
+        for (int k = 0; k < kCntPer; ++k) v += c[k];
+        int64_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[wid] = inc;
+        __syncthreads();
+        int64_t before = 0, tile = 0;
+#pragma unroll
+        for (int w = 0; w < kCntThreads / 32; ++w) {
+            before += (w < wid) ? wsum[w] : 0;
+            tile += wsum[w];
+        }
+        __syncthreads();
+        int64_t r = off + before + inc - v;
+        if (base + kCntPer <= i1) {
+            longlong2* q = reinterpret_cast<longlong2*>(seg_ptr + base);
+#pragma unroll
+            for (int k = 0; k < kCntPer / 2; ++k) {
+                const int64_t r0 = r, r1 = r0 + c[2 * k];
+                r = r1 + c[2 * k + 1];
+                q[k] = make_longlong2(r0, r1);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kCntPer; ++k) {
+                if (base + k < i1) seg_ptr[base + k] = r;
+                r += c[k];
+            }
+        }
+        off += tile;
     }
 }
 
@@ -437,10 +527,99 @@ __global__ void __launch_bounds__(256) fill_tail_kernel(GraphDev g, const HopMet
 // ------------------------------------------------------------------------------------
 // rank / meta / relabel / next frontier
 // ------------------------------------------------------------------------------------
-__global__ void popc_kernel(const uint32_t* __restrict__ bitmap, int64_t n_words, int32_t* __restrict__ wrank) {
+// Word ranks of the visited bitmap in two launches (replaces popc + CUB's init + scan, three
+// launches): wrank[w] = sum_{v < w} popc(bitmap[v]) for w in [0, n_words], words >= n_words
+// count 0.  Block b owns the words [b*chunk, (b+1)*chunk) (chunk = whole tiles of
+// kRankTile words, kRankPerThread consecutive words per thread, at most kRankMaxBlocks
+// blocks); rank_sum_kernel writes the block's popcount total btot[b], rank_scan_kernel adds
+// the totals of the earlier blocks.
+constexpr int kRankThreads = 256, kRankPerThread = 4, kRankTile = kRankThreads * kRankPerThread;
+constexpr int kRankMaxBlocks = kNumSMs * 4;
+
+__device__ __forceinline__ void rank_load(const uint32_t* __restrict__ bitmap, int64_t n_words, int64_t base,
+                                          uint32_t (&c)[kRankPerThread]) {
+    if (base + kRankPerThread <= n_words) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(bitmap + base));
+        c[0] = __popc(v.x); c[1] = __popc(v.y); c[2] = __popc(v.z); c[3] = __popc(v.w);
+    } else {
+#pragma unroll
+        for (int i = 0; i < kRankPerThread; ++i) c[i] = (base + i < n_words) ? __popc(bitmap[base + i]) : 0;
+    }
+}
+
+// block-wide sum over kRankThreads threads (result valid in every thread)
+__device__ __forceinline__ int rank_block_sum(int v, int* red) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int s = 0;
+#pragma unroll
+    for (int w = 0; w < kRankThreads / 32; ++w) s += red[w];
+    __syncthreads();
+    return s;
+}
+
+__global__ void __launch_bounds__(kRankThreads) rank_sum_kernel(const uint32_t* __restrict__ bitmap, int64_t n_words,
+                                                                int64_t chunk, int32_t* __restrict__ btot) {
     GSB_PDL_ENTRY();
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= n_words; w += (int64_t)gridDim.x * blockDim.x)
-        wrank[w] = (w < n_words) ? __popc(bitmap[w]) : 0;
+    __shared__ int red[kRankThreads / 32];
+    const int64_t w0 = blockIdx.x * chunk, w1 = min(w0 + chunk, n_words + 1);
+    int v = 0;
+    for (int64_t base = w0 + (int64_t)threadIdx.x * kRankPerThread; base < w1; base += kRankTile) {
+        uint32_t c[kRankPerThread];
+        rank_load(bitmap, n_words, base, c);
+#pragma unroll
+        for (int i = 0; i < kRankPerThread; ++i) v += (int)c[i];
+    }
+    v = rank_block_sum(v, red);
+    if (threadIdx.x == 0) btot[blockIdx.x] = v;
+}
+
+__global__ void __launch_bounds__(kRankThreads) rank_scan_kernel(const uint32_t* __restrict__ bitmap, int64_t n_words,
+                                                                 int64_t chunk, const int32_t* __restrict__ btot,
+                                                                 int32_t* __restrict__ wrank) {
+    GSB_PDL_ENTRY();
+    __shared__ int red[kRankThreads / 32];
+    __shared__ int wsum[kRankThreads / 32];
+    int off = 0;   // words of earlier blocks
+    for (int b = threadIdx.x; b < (int)blockIdx.x; b += kRankThreads) off += btot[b];
+    off = rank_block_sum(off, red);
+    const int64_t w0 = blockIdx.x * chunk, w1 = min(w0 + chunk, n_words + 1);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t t0 = w0; t0 < w1; t0 += kRankTile) {
+        const int64_t base = t0 + (int64_t)threadIdx.x * kRankPerThread;
+        uint32_t c[kRankPerThread];
+        rank_load(bitmap, n_words, base, c);
+        const int v = (int)(c[0] + c[1] + c[2] + c[3]);
+        // exclusive scan of v over the block: warp inclusive scan, then warp totals
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[wid] = inc;
+        __syncthreads();
+        int before = 0, tile = 0;
+#pragma unroll
+        for (int w = 0; w < kRankThreads / 32; ++w) {
+            before += (w < wid) ? wsum[w] : 0;
+            tile += wsum[w];
+        }
+        __syncthreads();
+        int r0 = off + before + inc - v;
+        const int r1 = r0 + (int)c[0], r2 = r1 + (int)c[1], r3 = r2 + (int)c[2];
+        if (base + kRankPerThread <= w1) {
+            *reinterpret_cast<int4*>(wrank + base) = make_int4(r0, r1, r2, r3);
+        } else {
+            const int r[4] = {r0, r1, r2, r3};
+#pragma unroll
+            for (int i = 0; i < kRankPerThread; ++i)
+                if (base + i < w1) wrank[base + i] = r[i];
+        }
+        off += tile;
+    }
 }
 
 __device__ __forceinline__ int64_t bit_rank(const uint32_t* bitmap, const int32_t* wrank, int64_t x) {
@@ -622,8 +801,6 @@ gsb_status gsb_blocks_create(gsb_graph_t gh, int32_t L, const int32_t* fanouts, 
     for (int h = 1; h <= L; ++h) maxseg = std::max<int64_t>(maxseg, B->cap_dst[h] * S + 1);
     cub::DeviceScan::ExclusiveSum(nullptr, t, (int64_t*)nullptr, (int64_t*)nullptr, (int64_t)maxseg);
     cb = std::max(cb, t);
-    cub::DeviceScan::ExclusiveSum(nullptr, t, (int32_t*)nullptr, (int32_t*)nullptr, (int64_t)(B->n_words + 1));
-    cb = std::max(cb, t);
     if (max_excl > 0) {
         cub::DeviceRadixSort::SortKeys(nullptr, t, (const uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)(2 * max_excl), 0, 64);
         cb = std::max(cb, t);
@@ -643,7 +820,7 @@ gsb_status gsb_blocks_create(gsb_graph_t gh, int32_t L, const int32_t* fanouts, 
     B->off_seed = take(sizeof(int64_t) * max_seeds);
     for (int h = 1; h <= L; ++h) {
         int64_t nseg = B->cap_dst[h] * S + 1;
-        B->off_cnt[h] = take(sizeof(int64_t) * nseg);
+        B->off_cnt[h] = take(sizeof(int64_t) * (nseg + kCntMaxBlocks));   // counts, then count_kernel's block totals
         B->off_seg[h] = take(sizeof(int64_t) * nseg);
         B->off_esrcgid[h] = take(sizeof(int64_t) * B->cap_edges[h]);
         B->off_eeid[h] = take(sizeof(int64_t) * B->cap_edges[h]);
@@ -652,7 +829,8 @@ gsb_status gsb_blocks_create(gsb_graph_t gh, int32_t L, const int32_t* fanouts, 
     }
     B->off_map = take(sizeof(int32_t) * G->total_nodes);
     B->off_bitmap = take(sizeof(uint32_t) * B->n_words);
-    B->off_wrank = take(sizeof(int32_t) * (B->n_words + 1));
+    // word ranks [n_words + 1], then the per-block totals of the rank kernels
+    B->off_wrank = take(sizeof(int32_t) * (B->n_words + 1 + kRankMaxBlocks));
     B->off_excl = take(sizeof(uint64_t) * (8 * (max_excl > 0 ? max_excl : 1) + 2));
     B->off_cub = take(cb);
     B->total_bytes = off;
@@ -754,11 +932,19 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
         HopBufs hb = B->hop(h, arena);
         const int f = B->fanout[B->L - h];
         const int64_t nseg = hb.cap_dst * S;
-        GSB_LAUNCH("sample_count", count_kernel, grid_for(nseg + 1, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
-                   hb.dst_gid, hb.cap_dst, f, ex, map, hb.cnt, err);
-        size_t cb = B->cub_bytes;
-        GSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, hb.cnt, hb.seg_ptr, (int64_t)(nseg + 1), s));
-        count_launch(2);
+        {
+            // count chunks: whole multiples of kCntThreads entries, at most kCntMaxBlocks of them;
+            // scan chunks: kScanPerBlock count chunks (whole kCntTile tiles, 16-B aligned)
+            const int64_t chunk = ceil_div(ceil_div(nseg + 1, kCntThreads), kCntMaxBlocks) * kCntThreads;
+            const int nb = (int)ceil_div(nseg + 1, chunk);
+            const int64_t schunk = chunk * kScanPerBlock;
+            const int nbs = (int)ceil_div(nseg + 1, schunk);
+            int64_t* btot = hb.cnt + nseg + 1;
+            GSB_LAUNCH("sample_count", count_kernel, nb, kCntThreads, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst, f, ex,
+                       map, hb.cnt, chunk, btot, err);
+            GSB_LAUNCH("sample_scan", count_scan_kernel, nbs, kCntThreads, 0, s, hb.cnt, nseg + 1, schunk, btot, nb,
+                       hb.seg_ptr);
+        }
         {
             const int G = (f >= 1 && f <= 8) ? 8 : ((f >= 1 && f <= 16) ? 16 : 32);
             const int grid = grid_for(nseg * G, 256, kNumSMs * GSB_FILL_BPS);
@@ -780,11 +966,14 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
                 GSB_LAUNCH("sample_fill_tail", fill_tail_kernel, kNumSMs * 8, 256, 0, s, g, hb.meta, hb.dst_gid,
                            hb.seg_ptr, ex, map, bitmap, hb.e_src_gid, hb.e_eid, err);
         }
-        GSB_LAUNCH("bitmap_popc", popc_kernel, grid_for(B->n_words + 1, 256, kNumSMs * 8), 256, 0, s, bitmap,
-                   B->n_words, wrank);
-        cb = B->cub_bytes;
-        GSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, wrank, wrank, (int64_t)(B->n_words + 1), s));
-        count_launch(2);
+        {
+            const int64_t chunk = ceil_div(ceil_div(B->n_words + 1, kRankTile), kRankMaxBlocks) * kRankTile;
+            const int nb = (int)ceil_div(B->n_words + 1, chunk);
+            int32_t* btot = wrank + B->n_words + 1;
+            GSB_LAUNCH("bitmap_rank_sum", rank_sum_kernel, nb, kRankThreads, 0, s, bitmap, B->n_words, chunk, btot);
+            GSB_LAUNCH("bitmap_rank_scan", rank_scan_kernel, nb, kRankThreads, 0, s, bitmap, B->n_words, chunk, btot,
+                       wrank);
+        }
         HopMeta* next = (h < B->L) ? at<HopMeta>(arena, B->off_meta[h + 1]) : nullptr;
         GSB_LAUNCH("hop_meta", hop_meta_kernel, 1, 32, 0, s, g, hb.meta, next, hb.seg_ptr, nseg, bitmap, wrank,
                    hb.cap_src, err);
