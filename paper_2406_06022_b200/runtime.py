@@ -5,6 +5,7 @@ allocates buffers and passes pointers.
 """
 from __future__ import annotations
 
+import os
 import ctypes as C
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence
@@ -504,7 +505,12 @@ class _TrainerBase:
         cur = {k: getattr(self, k) for k in self._BUFFERED}
         nxt = {k: (v.twin() if isinstance(v, MiniBatchSampler) else torch.zeros_like(v)) for k, v in cur.items()}
         self._bufs = [cur, nxt]
-        self.side = torch.cuda.Stream(device=self.device)
+        # Stream priorities (A/B knob, profiles/round1e_stream_priority.md): GSB_PRIO=1 replays the
+        # compute phase on a high-priority stream, 2 gives the sample side stream the high
+        # priority, 0 (default) keeps both at the default priority.
+        prio = os.environ.get("GSB_PRIO", "0")
+        self.side = torch.cuda.Stream(device=self.device, priority=-1 if prio == "2" else 0)
+        self.hi = torch.cuda.Stream(device=self.device, priority=-1) if prio == "1" else None
         self.ev_s = [torch.cuda.Event(), torch.cuda.Event()]
         self.ev_c = torch.cuda.Event()
 
@@ -581,12 +587,18 @@ class _TrainerBase:
                 self._use(nb)
                 self._sample_ops()
             self.ev_s[nb].record(self.side)
-        main.wait_event(self.ev_s[b])
+        cs = main if self.hi is None else self.hi
+        if cs is not main:
+            cs.wait_stream(main)
+        cs.wait_event(self.ev_s[b])
         self._use(b)
-        if self.pipe_graphs is not None:
-            self.pipe_graphs["compute"][b].replay()
-        else:
-            self._compute_ops()
+        with torch.cuda.stream(cs):
+            if self.pipe_graphs is not None:
+                self.pipe_graphs["compute"][b].replay()
+            else:
+                self._compute_ops()
+        if cs is not main:
+            main.wait_stream(cs)
         if self.pipe_allreduce is not None:
             # the sparse table update (N > 1, after the all-reduce) still reads buffer b's block:
             # the side stream may overwrite b (batch k+2) only after it
