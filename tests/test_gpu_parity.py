@@ -151,6 +151,31 @@ def test_sample_large_seed_set(torch_cuda):
     assert sm.poll_error() == 1
 
 
+def test_sample_multi_tile_scans(torch_cuda):
+    """The sampling scans at sizes where a block owns several tiles (sample.cu count_kernel /
+    count_scan_kernel: more than 2368 x 256 segment entries; rank_sum / rank_scan: more than
+    592 x 1024 bitmap words, i.e. > 19.4M nodes): a 24M-node graph with a small edge set and
+    20k seeds, blocks bit-exact against the oracle, ragged last chunks included."""
+    from paper_2406_06022_b200.runtime import GraphStore, MiniBatchSampler
+    cfg = synth.Config(
+        name="wide", ntypes=["A", "B"], counts=[24_000_003, 40_001],
+        etypes=[synth.EType("r0", 0, 1, 300_000), synth.EType("r1", 1, 0, 300_000),
+                synth.EType("r2", 1, 1, 200_000)],
+        feat_dim=4, fanouts=[12, 15], batch=20_000, hidden=8, num_classes=2,
+        target_ntype=1, gen_seed=2406060220 + 77)
+    st = GraphStore(cfg.counts, cfg.etype_src(), cfg.etype_dst(), "cuda")
+    for r in range(cfg.num_etypes):
+        s_, d_ = synth.etype_coo(cfg, r, backend="torch", device="cuda")
+        st.load_etype(r, s_, d_)
+    og = oracle_graph(cfg)
+    rng = np.random.default_rng(5)
+    seeds = np.sort(rng.choice(cfg.counts[1], 20_000, replace=False)).astype(np.int64) + int(cfg.node_off[1])
+    sm = MiniBatchSampler(st, cfg.fanouts, max_seeds=len(seeds))
+    sm.sample(torch_cuda.from_numpy(seeds).cuda(), 9, 1)
+    assert sm.poll_error() == 0
+    _compare_blocks(cfg, st, sm, oracle.sample_blocks(og, seeds, cfg.fanouts, 9, 1))
+
+
 def test_sample_deterministic(pair, torch_cuda):
     from paper_2406_06022_b200.runtime import MiniBatchSampler
     cfg, st, og = pair
