@@ -303,6 +303,20 @@ def build_gsb(cfg, device, partition=None, mode="peer"):
     return st, tr
 
 
+def poll_all(tr):
+    """Poll the device error words of every sampler (both pipeline buffers).  Each word is
+    sticky (OR of every sample since the last poll), so one poll after a timed loop covers
+    all of its steps."""
+    samplers = [tr.sampler]
+    for b in (tr._bufs or []):
+        if b["sampler"] not in samplers:
+            samplers.append(b["sampler"])
+    for sm in samplers:
+        code = sm.poll_error()
+        if code != 0:
+            raise RuntimeError(f"device-side sampling error {code} latched")
+
+
 _GRAPH_LAUNCHES = {}
 
 
@@ -378,20 +392,18 @@ def run_gsb(args, cfg):
     def step(i):
         fb(i)
         if dist is not None:
-            dist.all_reduce(tr.grad)          # C6: NCCL all-reduce of the flat dense grads
-            tr.grad.mul_(1.0 / ws)
+            allreduce(tr.grad)                # C6: NCCL all-reduce (ncclAvg) of the flat dense grads
         tr.optimizer_step()
 
     def allreduce(g):
-        dist.all_reduce(g)
-        g.mul_(1.0 / ws)
+        from paper_2406_06022_b200.dist import allreduce_mean
+        allreduce_mean(g)
 
     W = max(args.warmup, 3)
     for i in range(W - 2):
         step(i)
     torch.cuda.synchronize()
-    if tr.sampler.poll_error() != 0:
-        raise RuntimeError("device-side sampling error latched")
+    poll_all(tr)
     # ---- CUDA graphs.  Pipelined (default): per-buffer graphs of the sample phase (side
     # stream, batch i+1) and of the compute phase (+ Adam) of batch i; otherwise ONE graph of
     # the whole step.  Replays advance the RNG step word and Adam's t on the device; inputs
@@ -421,8 +433,7 @@ def run_gsb(args, cfg):
     for i in range(W - 2, W):
         run(i)
     torch.cuda.synchronize()
-    if tr.sampler.poll_error() != 0:
-        raise RuntimeError("device-side sampling error latched")
+    poll_all(tr)
     # ---- timed region
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _lib.lib().gsb_launch_count()
@@ -441,6 +452,7 @@ def run_gsb(args, cfg):
         e1.record()
         host_enqueue_ms = (time.perf_counter() - th0) * 1e3
         torch.cuda.synchronize()
+    poll_all(tr)     # sticky latch: any sampling error in any timed step fails the run
     if dist is not None:
         dist.barrier()
     launches = _lib.lib().gsb_launch_count() - launches0
@@ -542,8 +554,7 @@ def run_gsb(args, cfg):
             else:
                 tr.forward_backward(tr.seeds_dev[:hb.numel()], base + i)
             if dist is not None:
-                dist.all_reduce(tr.grad)
-                tr.grad.mul_(1.0 / ws)
+                allreduce(tr.grad)
             tr.optimizer_step()
         loss_host[i:i + 1].copy_(tr.loss, non_blocking=True)
         loss_ev[i].record()
@@ -555,6 +566,7 @@ def run_gsb(args, cfg):
     torch.cuda.synchronize()
     losses_read.append(float(loss_host[args.steps - 1]))
     e2e_s = time.perf_counter() - t0
+    poll_all(tr)
     if dist is not None:
         t = torch.tensor([e2e_s], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

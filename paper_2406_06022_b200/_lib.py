@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO = os.environ.get("GSB_SO") or os.path.join(HERE, "libgsb.so")   # GSB_SO: A/B experiments only
+SO = os.path.join(HERE, "libgsb.so")
 
 P = C.c_void_p
 i32, i64, u32, u64, f32, sz = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_float, C.c_size_t

@@ -13,11 +13,32 @@
 // (global -> split -> st.shared, double-buffered), thread 0 issues the MMAs, all 8 warps
 // drain the 128x128 fp32 accumulator from TMEM.  Persistent over tiles.
 #pragma once
-#include "gemm_simt.cuh"   // RowGroups
 #include "gsb_internal.cuh"
 #include "umma.cuh"
 
 namespace gsb {
+
+// Row groups of a grouped GEMM: group t = the dst rows of ntype t (K-slots = its
+// in-relations + self), or one plain group of M rows.
+struct RowGroups {
+    const HopMeta* meta;   // rows of group t = [meta->dst_off[t], meta->dst_off[t+1]) ; or
+    int64_t M;             // meta == nullptr: one group [0, M)
+    int32_t G;             // number of groups
+    int32_t ks[kMaxT];     // K-slots of group t (in-relations + self)
+    int32_t slot_w[kMaxT][kMaxS + 1];
+};
+
+__device__ __forceinline__ void group_rows(const RowGroups& rg, int t, int64_t& r0, int64_t& r1) {
+    if (rg.meta) {
+        r0 = rg.meta->dst_off[t];
+        r1 = rg.meta->dst_off[t + 1];
+    } else {
+        r0 = 0;
+        r1 = rg.M;
+    }
+}
+
+constexpr int BK = 32;     // layer widths (d_in) are multiples of one 32-column tf32 panel
 
 using umma::cp16;
 using umma::cp4;
@@ -119,10 +140,21 @@ struct UCursor {
     int64_t row0, rlim;
 };
 
+// K panels of one (NN / NT) tile of group t, and the split count used for that group: never
+// more splits than panels, so every split owns a non-empty panel range [p0, p1).
+template <int MODE>
+__device__ __forceinline__ int panels_of_group(const UProb& P, int t) {
+    return MODE == UMMA_NN ? P.rg.ks[t] * (P.d_in / 32) : (P.N + 31) / 32;
+}
+template <int MODE>
+__device__ __forceinline__ int ksplit_of_group(const UProb& P, int t) {
+    return max(1, min(P.ksplit, panels_of_group<MODE>(P, t)));
+}
+
 template <int MODE>
 __device__ __forceinline__ int64_t tiles_of_group(const UProb& P, int t, int64_t r0, int64_t r1, int nct, int kct) {
-    if (MODE == UMMA_NN) return ((r1 - r0 + 127) / 128) * nct * P.ksplit;
-    if (MODE == UMMA_NT) return ((r1 - r0 + 127) / 128) * kct * P.rg.ks[t] * P.ksplit;
+    if (MODE == UMMA_NN) return ((r1 - r0 + 127) / 128) * nct * ksplit_of_group<MODE>(P, t);
+    if (MODE == UMMA_NT) return ((r1 - r0 + 127) / 128) * kct * P.rg.ks[t] * ksplit_of_group<MODE>(P, t);
     return ((r1 - r0 + P.rows_per_chunk - 1) / P.rows_per_chunk) * P.rg.ks[t] * kct * nct;
 }
 
@@ -140,9 +172,10 @@ __device__ __forceinline__ void decode_tile(const UProb& P, int64_t tile, int nc
     c.t = t;
     c.s = 0; c.c0 = 0; c.n0 = 0;
     c.split = 0;
+    const int kse = (MODE != UMMA_TN) ? ksplit_of_group<MODE>(P, t) : 1;
     if (MODE != UMMA_TN) {
-        c.split = (int)(rem % P.ksplit);
-        rem /= P.ksplit;
+        c.split = (int)(rem % kse);
+        rem /= kse;
     }
     if (MODE == UMMA_NN) {
         c.row0 = r0 + (rem / nct) * 128;
@@ -169,10 +202,10 @@ __device__ __forceinline__ void decode_tile(const UProb& P, int64_t tile, int nc
         c.KP = (int)((c.rlim - c.row0 + 31) / 32);
     }
     c.p0 = 0;
-    if (MODE != UMMA_TN && P.ksplit > 1) {
-        const int per = (c.KP + P.ksplit - 1) / P.ksplit;
-        c.p0 = min(c.KP, c.split * per);
-        c.KP = min(c.KP, c.p0 + per);
+    if (kse > 1) {   // split k owns panels [k*KP/kse, (k+1)*KP/kse): non-empty since kse <= KP
+        const int kp = c.KP;
+        c.p0 = (c.split * kp) / kse;
+        c.KP = ((c.split + 1) * kp) / kse;
     }
     c.p = c.p0;
 }

@@ -1,6 +1,5 @@
 // layer.cu -- RGCN layer forward / backward and the NC decoder + softmax-CE loss.
 // Contract: include/gsb.h "RGCN layer" and "Node-classification decoder".
-#include "gemm_simt.cuh"
 #include "gemm_umma.cuh"
 #include "gsb_internal.cuh"
 
@@ -422,6 +421,17 @@ __global__ void __launch_bounds__(256) relu_bwd_kernel(const HopMeta* __restrict
     }
 }
 
+// zero the first n_dst (device count) rows of a [rows][w] fp32 output before split-K
+// partials are red.added into it: a capacity-sized memset would write past a caller buffer
+// that holds only the live rows (e.g. one chunk of a full-graph table)
+__global__ void __launch_bounds__(256) zero_rows_kernel(const HopMeta* __restrict__ m, float* __restrict__ p,
+                                                        int64_t w) {
+    GSB_PDL_ENTRY();
+    const int64_t n = m->n_dst * w;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = 0.f;
+}
+
 static const char* lname(const char* base, int layer) {
     static const char* names[][4] = {
         {"rgcn_agg_l0", "rgcn_agg_l1", "rgcn_agg_l2", "rgcn_agg_l3"},
@@ -462,12 +472,6 @@ static RowGroups single_group(int64_t M) {
     return rg;
 }
 
-#ifdef GSB_SIMT_GEMM
-static int gemm_grid(int64_t rows_cap, int ncols_tiles, int groups) {
-    int64_t tiles = (ceil_div(rows_cap, BM) + groups) * ncols_tiles;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs * 4));
-}
-#endif
 
 }  // namespace gsb
 
@@ -527,19 +531,15 @@ gsb_status gsb_rgcn_layer_gemm(gsb_blocks_t b, const void* arena, int32_t layer,
     const GraphDev& g = B->g->dev;
     const int64_t lda = (int64_t)(g.S + 1) * d_in;
     RowGroups rg = layer_groups(B, arena, layer);
-#ifdef GSB_SIMT_GEMM
-    GSB_LAUNCH(lname("rgcn_gemm_fwd", layer), gemm_nn_kernel, gemm_grid(hb.cap_dst, (d_out + BN - 1) / BN, g.T), NT, 0, s, rg,
-               acat, lda, W, d_in, d_out, (int64_t)d_out, (int64_t)d_in * d_out, bias, relu, h_dst, (int64_t)d_out);
-    return GSB_OK;
-#else
     UProb P{};
     P.rg = rg; P.A = acat; P.lda = lda; P.B = W; P.ldb = d_out; P.bslot = (int64_t)d_in * d_out;
     P.relu = relu; P.d_in = d_in; P.N = d_out; P.C = h_dst; P.ldc = d_out; P.bias = bias;
     const int64_t tiles = (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_out, 128);
     P.ksplit = choose_ksplit(tiles, (g.S + 1) * (d_in / 32), !relu);
-    if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(h_dst, 0, sizeof(float) * (size_t)hb.cap_dst * d_out, s));
+    if (P.ksplit > 1)
+        GSB_LAUNCH("zero_rows", zero_rows_kernel, grid_for(hb.cap_dst * d_out, 256, kNumSMs * 4), 256, 0, s, hb.meta,
+                   h_dst, (int64_t)d_out);
     return launch_umma<UMMA_NN>(lname("rgcn_gemm_fwd", layer), P, tiles, s);
-#endif
 }
 
 gsb_status gsb_rgcn_layer_fwd_ex(gsb_blocks_t b, const void* arena, int32_t layer, const void* h_src, int32_t h_dtype,
@@ -566,7 +566,6 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     HopBufs hb = B->hop(h, const_cast<void*>(arena));
     const int64_t lda = (int64_t)(g.S + 1) * d_in;
     RowGroups rg = layer_groups(B, arena, layer);
-#ifndef GSB_SIMT_GEMM
     if (relu) {   // dZ once, in place; the GEMMs below then read dZ directly
         GSB_LAUNCH(lname("relu_bwd", layer), relu_bwd_kernel, grid_for(hb.cap_dst * d_out / 4, 256, kNumSMs * 8), 256, 0, s,
                    hb.meta, dh_dst, h_dst, d_out);
@@ -574,18 +573,8 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     // the weight gradient runs on the side stream, overlapping dA + scatter (joined below)
     cudaStream_t s_main = s;
     if (dh_src) s = fork_begin(s_main);
-#endif
     GSB_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)(g.R + 1) * d_in * d_out, s));
     GSB_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)d_out, s));
-#ifdef GSB_SIMT_GEMM
-    const int rpc = 256;
-    {
-        int64_t items = (ceil_div(hb.cap_dst, rpc) + g.T) * (g.S + 1) * ceil_div(d_in, BM) * ceil_div(d_out, BN);
-        int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, kNumSMs * 4));
-        GSB_LAUNCH(lname("rgcn_gemm_dW", layer), gemm_tn_kernel, grid, NT, 0, s, rg, acat, lda, dh_dst, h_dst, relu,
-                   (int64_t)d_out, d_in, d_out, rpc, dW, (int64_t)d_out, (int64_t)d_in * d_out, db);
-    }
-#else
     {
         // row chunks sized so the (type, slot, chunk) items cover ~2 waves of SMs
         const int64_t rows = hb.cap_dst;
@@ -601,13 +590,7 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     }
     cudaStream_t s_side = s;
     s = s_main;
-#endif
     if (dh_src) {
-#ifdef GSB_SIMT_GEMM
-        GSB_LAUNCH(lname("rgcn_gemm_dA", layer), gemm_nt_kernel, gemm_grid(hb.cap_dst, (int)ceil_div(d_in, BN) * (g.S + 1), g.T),
-                   NT, 0, s, rg, dh_dst, h_dst, relu, (int64_t)d_out, W, d_in, d_out, (int64_t)d_out,
-                   (int64_t)d_in * d_out, dacat_ws, lda);
-#else
         UProb P{};
         P.rg = rg; P.A = dh_dst; P.lda = d_out; P.B = W; P.ldb = d_out;
         P.bslot = (int64_t)d_in * d_out; P.d_in = d_in; P.N = d_out; P.C = dacat_ws; P.ldc = lda;
@@ -616,16 +599,11 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(dacat_ws, 0, sizeof(float) * (size_t)hb.cap_dst * lda, s));
         gsb_status st = launch_umma<UMMA_NT>(lname("rgcn_gemm_dA", layer), P, tiles, s);
         if (st != GSB_OK) return st;
-#endif
         GSB_CUDA(cudaMemsetAsync(dh_src, 0, sizeof(float) * (size_t)hb.cap_src * d_in, s));
         GSB_LAUNCH(lname("rgcn_scatter", layer), scatter_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
                    hb.meta, hb.seg_ptr, hb.e_src, dacat_ws, lda, d_in, dh_src);
     }
-#ifndef GSB_SIMT_GEMM
     return fork_end(s_main, s_side);
-#else
-    return GSB_OK;
-#endif
 }
 
 gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int32_t N,
@@ -658,10 +636,6 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
     cudaStream_t s = (cudaStream_t)stream;
     RowGroups rg = single_group(n);
     const int64_t ldl = (C + 3) / 4 * 4;   // padded logits row (16-B aligned rows)
-#ifdef GSB_SIMT_GEMM
-    GSB_LAUNCH("nc_logits", gemm_nn_kernel, gemm_grid(n, (C + BN - 1) / BN, 1), NT, 0, s, rg, h, (int64_t)d, Wc, d,
-               C, (int64_t)C, (int64_t)0, bc, 0, logits_ws, ldl);
-#else
     {
         UProb P{};
         P.rg = rg; P.A = h; P.lda = d; P.B = Wc; P.ldb = C; P.bslot = 0; P.d_in = d; P.N = C; P.C = logits_ws;
@@ -672,7 +646,6 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         gsb_status st = launch_umma<UMMA_NN>("nc_logits", P, tiles, s);
         if (st != GSB_OK) return st;
     }
-#endif
     {
         // fused batch mean: partials and the ticket word live in row_loss_ws after the n row
         // losses (caller-owned scratch of n + 640 floats, zero-filled before first use)
@@ -688,27 +661,15 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         GSB_CHECK_ARG(dWc && dbc, "dWc and dbc go together");
         GSB_CUDA(cudaMemsetAsync(dWc, 0, sizeof(float) * (size_t)d * C, s));
         GSB_CUDA(cudaMemsetAsync(dbc, 0, sizeof(float) * (size_t)C, s));
-#ifdef GSB_SIMT_GEMM
-        const int rpc = 128;
-        int64_t items = ceil_div(n, rpc) * ceil_div(d, BM) * ceil_div(C, BN);
-        GSB_LAUNCH("nc_gemm_dWc", gemm_tn_kernel, (int)std::min<int64_t>(items, kNumSMs * 4), NT, 0, s, rg, h,
-                   (int64_t)d, logits_ws, (const float*)nullptr, 0, ldl, d, C, rpc, dWc, (int64_t)C,
-                   (int64_t)0, dbc);
-#else
         UProb P{};
         P.rg = rg; P.A = h; P.lda = d; P.B = logits_ws; P.ldb = ldl; P.d_in = d; P.N = C; P.C = dWc; P.ldc = C;
         P.bslot = 0; P.db = dbc; P.rows_per_chunk = 64;
         gsb_status st = launch_umma<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, 64) * ceil_div(d, 128) * ceil_div(C, 128), s);
         if (st != GSB_OK) return st;
-#endif
     }
     cudaStream_t s_side = s;
     s = s_main;
     if (dh) {
-#ifdef GSB_SIMT_GEMM
-        GSB_LAUNCH("nc_gemm_dh", gemm_nt_kernel, gemm_grid(n, (int)ceil_div(d, BN), 1), NT, 0, s, rg, logits_ws,
-                   (const float*)nullptr, 0, ldl, Wc, d, C, (int64_t)C, (int64_t)0, dh, (int64_t)d);
-#else
         UProb P{};
         P.rg = rg; P.A = logits_ws; P.lda = ldl; P.B = Wc; P.ldb = C; P.bslot = 0; P.d_in = d; P.N = C; P.C = dh;
         P.ldc = d;
@@ -717,7 +678,6 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(dh, 0, sizeof(float) * (size_t)n * d, s));
         gsb_status st = launch_umma<UMMA_NT>("nc_gemm_dh", P, tiles, s);
         if (st != GSB_OK) return st;
-#endif
     }
     return fork_end(s_main, s_side);
 }

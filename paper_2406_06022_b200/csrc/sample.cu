@@ -34,6 +34,15 @@ struct Excl {
     const int64_t* cum;   // [n+1] exclusive prefix of the range lengths (duplicates: length 0)
 };
 
+// start of a sample: fold the previous sample's latch into the sticky word, clear the latch
+__global__ void err_roll_kernel(int* __restrict__ err) {
+    GSB_PDL_ENTRY();
+    if (threadIdx.x == 0) {
+        err[1] |= err[0];
+        err[0] = 0;
+    }
+}
+
 // Position range of every sorted exclusion key inside its destination's CSC segment
 // (one binary search pair per key, once per batch).  Duplicate keys get an empty range at the
 // previous key's end so that (lo - cum) stays non-decreasing within a segment.
@@ -740,7 +749,7 @@ __global__ void init_arena_kernel(int32_t* __restrict__ map, int64_t n, uint32_t
         if (i < n) map[i] = -1;
         if (i < n_words) bitmap[i] = 0;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *err = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) err[0] = err[1] = 0;
 }
 
 HopBufs Blocks::hop(int h, void* arena) const {
@@ -917,7 +926,9 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
         ex.cum = ecum;
     }
 
-    GSB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
+    // err[0] = this sample's latch; err[1] = sticky OR of every earlier sample's latch since the
+    // last poll, so an error in any step of a timed loop is still reported afterwards
+    GSB_LAUNCH("err_roll", err_roll_kernel, 1, 32, 0, s, err);
     if (n_seeds <= 8192) {
         GSB_LAUNCH("seed_meta", seed_meta_kernel, 1, 1024, 0, s, g, seeds, n_seeds, a->n_seeds_dev,
                    at<int64_t>(arena, B->off_seed), at<HopMeta>(arena, B->off_meta[1]), err);
@@ -1024,9 +1035,12 @@ gsb_status gsb_blocks_poll_error(gsb_blocks_t b, void* arena, int32_t* code, voi
     Blocks* B = reinterpret_cast<Blocks*>(b);
     GSB_CHECK_ARG(B && arena && code, "null argument");
     cudaStream_t s = (cudaStream_t)stream;
-    int h = 0;
-    GSB_CUDA(cudaMemcpyAsync(&h, at<int>(arena, B->off_err), sizeof(int), cudaMemcpyDeviceToHost, s));
+    int hw[2] = {0, 0};
+    int* err = at<int>(arena, B->off_err);
+    GSB_CUDA(cudaMemcpyAsync(hw, err, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    GSB_CUDA(cudaMemsetAsync(err + 1, 0, sizeof(int), s));      // the sticky word restarts
     GSB_CUDA(cudaStreamSynchronize(s));
+    const int h = hw[0] ? hw[0] : hw[1];
     *code = h;
     if (h != 0) {
         set_error("device-side error %d latched during sampling", h);

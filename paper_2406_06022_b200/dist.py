@@ -11,8 +11,13 @@ import torch
 
 
 def allreduce_mean(t: torch.Tensor, group=None, world: Optional[int] = None) -> torch.Tensor:
-    """In place: t <- mean over ranks of t (NCCL sum, then scale by 1/world)."""
+    """In place: t <- mean over ranks of t.  NCCL: one ncclAvg all-reduce (the 1/world scale
+    happens inside the collective, no extra kernel); gloo (CPU tests) has no AVG: sum, then
+    scale by 1/world."""
     import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.AVG, group=group)
+        return t
     ws = world if world is not None else dist.get_world_size(group)
     dist.all_reduce(t, group=group)
     if ws > 1:

@@ -386,3 +386,25 @@ def test_nc_loss_parity(torch_cuda, n, d, C):
     close(dh.cpu().numpy(), odh, what="dh")
     close(dWc.cpu().numpy(), odW, what="dWc")
     close(dbc.cpu().numpy(), odb, what="dbc")
+
+
+@pytest.mark.parametrize("name,batch", [("mag_small", 2600), ("mag_small", 3000), ("mag_small", 3200),
+                                        ("tiny", 700), ("tiny", 1500)])
+def test_nc_step_splitk_batches(torch_cuda, name, batch):
+    """Regression: batch sizes whose top-layer GEMM splits K across CTAs
+    (few output tiles) with a split count that does not divide the K panels, and ntypes with
+    fewer slots than the widest one.  Activations, loss and gradients within rtol."""
+    import torch
+    cfg = CASES[name]()
+    cfg.batch = batch
+    st, og = gpu_store(cfg), oracle_graph(cfg)
+    tr = _gpu_trainer(cfg, st)
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    seeds = synth.nc_seeds(cfg, 1)
+    tr.forward_backward(torch_cuda.from_numpy(seeds).cuda(), 1)
+    res = oracle.nc_step(og, params, seeds, synth.labels(cfg), 1, cfg.rng_seed)
+    for l in range(len(cfg.fanouts)):
+        nd = len(res.blocks[l].dst_gid)
+        close(tr.hout[l][:nd].cpu().numpy(), res.hs[l], what=f"batch {batch} h{l}")
+    close(tr.loss.cpu().numpy()[0], res.loss, what="loss")
+    check_grads(tr, res, cfg, 1)
