@@ -275,6 +275,9 @@ gsb_status gsb_encoder_bwd(gsb_blocks_t b, const void* arena, const float* const
  *   mode 2 (TN): C[K][N] += A[M][K]^T B[M][N]      (C accumulated; zero it first) */
 gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int32_t N,
                     int32_t K, float* C, int64_t ldc, void* stream);
+/* Tools: copies n (<= 256) globaltimer stamps recorded by CTA 0 of the last GEMM launched with
+ * GSB_GEMM_DBG & 1024 ([role][64]: producer, MMA, splitters, epilogue; slot 63 = start). */
+gsb_status gsb_gemm_trace(uint64_t* out, int32_t n);
 
 /* ======================================================================================
  * Node-classification decoder + softmax cross-entropy (P:L477 ClassifyLossFunc, P:L489;

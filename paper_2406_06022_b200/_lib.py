@@ -72,6 +72,7 @@ SIGS = {
     "gsb_encoder_bwd": [P, P, P, P, i32, P, P, sz, P],
     "gsb_graph_set_feature_peers": [P, i32, i32, P, P, i32, i32],
     "gsb_gemm": [i32, P, i64, P, i64, i64, i32, i32, P, i64, P],
+    "gsb_gemm_trace": [P, i32],
     "gsb_nc_loss": [P, i64, i32, P, P, i32, P, P, i64, P, P, P, P, P, P, P],
     "gsb_adam_step": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P],
     "gsb_counter_add": [P, i32, P],

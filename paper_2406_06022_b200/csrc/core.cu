@@ -7,6 +7,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "gemm_tma.cuh"
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -280,6 +281,43 @@ gsb_status fork_end(cudaStream_t s, cudaStream_t side) {
     GSB_CUDA(cudaStreamWaitEvent(s, f.ev_join, 0));
     return GSB_OK;
 }
+
+// ------------------------------------------------------------------------------------
+// TMA tensor maps (gemm_tma.cuh): cuTensorMapEncodeTiled through the runtime's driver entry
+// point (no libcuda link dependency)
+// ------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+bool encode_tmap_f32(CUtensorMap* m, const float* base, int64_t width, int64_t rows, int64_t ld, int box_w,
+                     int box_h, bool swz128) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || width < 1 || rows < 1) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 }  // namespace gsb
 
 extern "C" {

@@ -1,6 +1,6 @@
 // layer.cu -- RGCN layer forward / backward and the NC decoder + softmax-CE loss.
 // Contract: include/gsb.h "RGCN layer" and "Node-classification decoder".
-#include "gemm_umma.cuh"
+#include "gemm_tma.cuh"
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -539,7 +539,8 @@ gsb_status gsb_rgcn_layer_gemm(gsb_blocks_t b, const void* arena, int32_t layer,
     if (P.ksplit > 1)
         GSB_LAUNCH("zero_rows", zero_rows_kernel, grid_for(hb.cap_dst * d_out, 256, kNumSMs * 4), 256, 0, s, hb.meta,
                    h_dst, (int64_t)d_out);
-    return launch_umma<UMMA_NN>(lname("rgcn_gemm_fwd", layer), P, tiles, s);
+    return launch_gemm<UMMA_NN>(lname("rgcn_gemm_fwd", layer), P, tiles, hb.cap_dst, lda, (int64_t)(g.R + 1) * d_in,
+                                d_out, s);
 }
 
 gsb_status gsb_rgcn_layer_fwd_ex(gsb_blocks_t b, const void* arena, int32_t layer, const void* h_src, int32_t h_dtype,
@@ -585,7 +586,8 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         P.d_in = d_in; P.N = d_out; P.C = dW; P.ldc = d_out; P.bslot = (int64_t)d_in * d_out; P.db = db;
         P.rows_per_chunk = rpc;
         int64_t items = (ceil_div(rows, rpc) + g.T) * (g.S + 1) * ceil_div(d_in, 128) * ceil_div(d_out, 128);
-        gsb_status st = launch_umma<UMMA_TN>(lname("rgcn_gemm_dW", layer), P, items, s);
+        gsb_status st = launch_gemm<UMMA_TN>(lname("rgcn_gemm_dW", layer), P, items, hb.cap_dst, lda, hb.cap_dst,
+                                             d_out, s);
         if (st != GSB_OK) return st;
     }
     cudaStream_t s_side = s;
@@ -597,13 +599,20 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         const int64_t tiles = (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_in, 128) * (g.S + 1);
         P.ksplit = choose_ksplit(tiles, (d_out + 31) / 32, true);
         if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(dacat_ws, 0, sizeof(float) * (size_t)hb.cap_dst * lda, s));
-        gsb_status st = launch_umma<UMMA_NT>(lname("rgcn_gemm_dA", layer), P, tiles, s);
+        gsb_status st = launch_gemm<UMMA_NT>(lname("rgcn_gemm_dA", layer), P, tiles, hb.cap_dst, d_out,
+                                             (int64_t)(g.R + 1) * d_in, d_out, s);
         if (st != GSB_OK) return st;
         GSB_CUDA(cudaMemsetAsync(dh_src, 0, sizeof(float) * (size_t)hb.cap_src * d_in, s));
         GSB_LAUNCH(lname("rgcn_scatter", layer), scatter_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
                    hb.meta, hb.seg_ptr, hb.e_src, dacat_ws, lda, d_in, dh_src);
     }
     return fork_end(s_main, s_side);
+}
+
+gsb_status gsb_gemm_trace(uint64_t* out, int32_t n) {
+    GSB_CHECK_ARG(out && n > 0 && n <= 4 * TG_TRACE, "bad argument");
+    GSB_CUDA(cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(uint64_t) * n));
+    return GSB_OK;
 }
 
 gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int32_t N,
@@ -616,13 +625,14 @@ gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, i
     if (mode == 0) {            // C[M][N] = A[M][K] B[K][N]
         GSB_CHECK_ARG(K % 32 == 0, "NN needs K %% 32 == 0");
         P.d_in = K; P.N = N;
-        return launch_umma<UMMA_NN>("gemm_nn", P, ceil_div(M, 128) * ceil_div(N, 128), s);
+        return launch_gemm<UMMA_NN>("gemm_nn", P, ceil_div(M, 128) * ceil_div(N, 128), M, K, K, N, s);
     } else if (mode == 1) {     // C[M][K] = A[M][N] B[K][N]^T
         P.d_in = K; P.N = N;
-        return launch_umma<UMMA_NT>("gemm_nt", P, ceil_div(M, 128) * ceil_div(K, 128), s);
+        return launch_gemm<UMMA_NT>("gemm_nt", P, ceil_div(M, 128) * ceil_div(K, 128), M, N, K, N, s);
     } else if (mode == 2) {     // C[K][N] += A[M][K]^T B[M][N]
         P.d_in = K; P.N = N; P.rows_per_chunk = 128;
-        return launch_umma<UMMA_TN>("gemm_tn", P, ceil_div(M, 128) * ceil_div(K, 128) * ceil_div(N, 128), s);
+        return launch_gemm<UMMA_TN>("gemm_tn", P, ceil_div(M, 128) * ceil_div(K, 128) * ceil_div(N, 128), M, K, M,
+                                    N, s);
     }
     set_error("mode %d not in {0,1,2}", mode);
     return GSB_EINVAL;
@@ -643,7 +653,7 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         const int64_t tiles = ceil_div(n, 128) * ceil_div(C, 128);
         P.ksplit = choose_ksplit(tiles, d / 32, true);
         if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(logits_ws, 0, sizeof(float) * (size_t)n * ldl, s));
-        gsb_status st = launch_umma<UMMA_NN>("nc_logits", P, tiles, s);
+        gsb_status st = launch_gemm<UMMA_NN>("nc_logits", P, tiles, n, d, d, C, s);
         if (st != GSB_OK) return st;
     }
     {
@@ -664,7 +674,8 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         UProb P{};
         P.rg = rg; P.A = h; P.lda = d; P.B = logits_ws; P.ldb = ldl; P.d_in = d; P.N = C; P.C = dWc; P.ldc = C;
         P.bslot = 0; P.db = dbc; P.rows_per_chunk = 64;
-        gsb_status st = launch_umma<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, 64) * ceil_div(d, 128) * ceil_div(C, 128), s);
+        gsb_status st = launch_gemm<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, 64) * ceil_div(d, 128) * ceil_div(C, 128),
+                                             n, d, n, C, s);
         if (st != GSB_OK) return st;
     }
     cudaStream_t s_side = s;
@@ -676,7 +687,7 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         const int64_t tiles = ceil_div(n, 128) * ceil_div(d, 128);
         P.ksplit = choose_ksplit(tiles, (C + 31) / 32, true);
         if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(dh, 0, sizeof(float) * (size_t)n * d, s));
-        gsb_status st = launch_umma<UMMA_NT>("nc_gemm_dh", P, tiles, s);
+        gsb_status st = launch_gemm<UMMA_NT>("nc_gemm_dh", P, tiles, n, C, d, C, s);
         if (st != GSB_OK) return st;
     }
     return fork_end(s_main, s_side);
