@@ -118,6 +118,143 @@ __global__ void __launch_bounds__(256, GSB_AGG_MINB) agg_kernel(GraphDev g, cons
     }
 }
 
+// ------------------------------------------------------------------------------------
+// aggregation, segment-parallel (default): a group of LPE lanes owns one (dst row j, slot s)
+// unit -- a relation's segment (its mean) or the self slot (the dst's own row) -- and each
+// lane owns 32 bytes of the row (LPE = row bytes / 32: 8 lanes for 128-d bf16 or 64-d fp32,
+// 16 for 128-d fp32).  Every lane walks the segment's edges itself, U source rows in flight
+// (256-bit loads, LDG.E.ENL2.256), and sums in registers: no cross-lane reduction, no
+// shuffles, and empty slots cost one store.  A warp's 32/LPE groups take consecutive units.
+// ------------------------------------------------------------------------------------
+template <bool W256 = true>
+__device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
+    if (!W256) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(p)), b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
+        r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+        return;
+    }
+    asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+}
+template <bool BF16>
+__device__ __forceinline__ void acc256(float* acc, const uint32_t (&r)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (BF16) {
+            acc[2 * i] += bf16_lo(r[i]);
+            acc[2 * i + 1] += bf16_hi(r[i]);
+        } else {
+            acc[i] += __uint_as_float(r[i]);
+        }
+    }
+}
+
+template <bool FEAT, bool BF16, int LPE, int U, bool W256 = true>
+__global__ void __launch_bounds__(256) agg_seg_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                      const int64_t* __restrict__ seg_ptr,
+                                                      const int32_t* __restrict__ e_src,
+                                                      const int64_t* __restrict__ e_src_gid,
+                                                      const int64_t* __restrict__ dst_gid, const char* __restrict__ h,
+                                                      int row_bytes, int d, float* __restrict__ acat, int64_t lda,
+                                                      const int32_t* __restrict__ rowmap, int64_t seg_cap) {
+    GSB_PDL_ENTRY();
+    constexpr int V = BF16 ? 16 : 8;            // floats per lane (32 bytes of the row)
+    __shared__ int64_t s_dst_off[kMaxT + 1], s_src_off[kMaxT + 1];
+    if (threadIdx.x <= (unsigned)g.T) {
+        s_dst_off[threadIdx.x] = m->dst_off[threadIdx.x];
+        s_src_off[threadIdx.x] = m->src_off[threadIdx.x];
+    }
+    const int64_t n = m->n_dst;
+    __syncthreads();
+    const int sub = threadIdx.x % LPE;
+    const int S = g.S;
+    const uint32_t S1 = (uint32_t)S + 1;
+    const uint32_t units = (uint32_t)(n * S1);
+    const uint32_t groups = gridDim.x * (blockDim.x / LPE);
+    for (uint32_t u = blockIdx.x * (blockDim.x / LPE) + threadIdx.x / LPE; u < units; u += groups) {
+        const uint32_t j = u / S1;
+        const int s = (int)(u - j * S1);
+        int t = 0;
+        for (int k = 1; k < g.T; ++k) t += ((int64_t)j >= s_dst_off[k]) ? 1 : 0;
+        const int St = g.n_slots[t];
+        if (s > St) continue;
+        float acc[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = 0.f;
+        if (s == St) {          // self slot: the dst's own row
+            const char* row = FEAT ? reinterpret_cast<const char*>(feat_row(g, dst_gid[j]))
+                                   : reinterpret_cast<const char*>(
+                                         src_row<false>(g, h, row_bytes, s_src_off[t] + ((int64_t)j - s_dst_off[t]), rowmap));
+            uint32_t r[8];
+            ldg256<W256>(row + sub * 32, r);
+            acc256<BF16>(acc, r);
+        } else {
+            const int64_t e0 = seg_ptr[(int64_t)j * S + s], e1 = seg_ptr[(int64_t)j * S + s + 1];
+            // a segment longer than seg_cap (fanout ALL hubs) leaves its tail to heavy_kernel
+            const int64_t ec = (e1 - e0 > seg_cap) ? e0 + seg_cap : e1;
+            for (int64_t e = e0; e < ec; e += U) {
+                const char* p[U];
+#pragma unroll
+                for (int k = 0; k < U; ++k)
+                    p[k] = (e + k < ec) ? reinterpret_cast<const char*>(src_row<FEAT>(
+                                              g, h, row_bytes, FEAT ? e_src_gid[e + k] : (int64_t)e_src[e + k], rowmap))
+                                        : nullptr;
+                uint32_t r[U][8];
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    if (p[k]) {
+                        ldg256<W256>(p[k] + sub * 32, r[k]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) r[k][i] = 0u;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < U; ++k) acc256<BF16>(acc, r[k]);
+            }
+            const float inv = (e1 > e0) ? 1.f / (float)(e1 - e0) : 0.f;
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] *= inv;
+        }
+        float4* o4 = reinterpret_cast<float4*>(acat + (int64_t)j * lda + (int64_t)s * d + (int64_t)sub * V);
+#pragma unroll
+        for (int v = 0; v < V; v += 4) o4[v / 4] = make_float4(acc[v], acc[v + 1], acc[v + 2], acc[v + 3]);
+    }
+}
+
+template <bool FEAT, bool BF16>
+static gsb_status launch_agg_seg(const char* name, cudaStream_t s, const GraphDev& g, const HopBufs& hb, const char* h,
+                                 int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap,
+                                 int64_t seg_cap) {
+    const int lpe = row_bytes / 32;
+    const int64_t units = hb.cap_dst * (g.S + 1);
+    // one wave of resident blocks (A/B knobs: GSB_AGG_BPS blocks per SM, GSB_AGG_U rows in flight)
+    static const int bps = getenv("GSB_AGG_BPS") ? atoi(getenv("GSB_AGG_BPS")) : 4;
+    static const int uu = getenv("GSB_AGG_U") ? atoi(getenv("GSB_AGG_U")) : 8;
+    const int grid = grid_for(units * lpe, 256, kNumSMs * bps);
+#define GSB_AGG_SEG(L, UU)                                                                                       \
+    GSB_LAUNCH(name, (agg_seg_kernel<FEAT, BF16, L, UU>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,     \
+               hb.e_src_gid, hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap)
+    static const bool w128 = getenv("GSB_AGG_W") && atoi(getenv("GSB_AGG_W")) == 128;
+    if (w128 && lpe == 8 && uu == 8) {
+        GSB_LAUNCH(name, (agg_seg_kernel<FEAT, BF16, 8, 8, false>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,
+                   hb.e_src_gid, hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
+    } else if (uu == 4) {
+        if (lpe == 4) GSB_AGG_SEG(4, 4);
+        else if (lpe == 8) GSB_AGG_SEG(8, 4);
+        else if (lpe == 16) GSB_AGG_SEG(16, 4);
+        else GSB_AGG_SEG(32, 4);
+    } else {
+        if (lpe == 4) GSB_AGG_SEG(4, 8);
+        else if (lpe == 8) GSB_AGG_SEG(8, 8);
+        else if (lpe == 16) GSB_AGG_SEG(16, 8);
+        else GSB_AGG_SEG(32, 8);
+    }
+#undef GSB_AGG_SEG
+    return GSB_OK;
+}
+
 template <bool FEAT, bool BF16>
 static gsb_status launch_agg_lpe(const char* name, int grid, cudaStream_t s, const GraphDev& g, const HopBufs& hb,
                                  const char* h, int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap,
@@ -254,7 +391,22 @@ static gsb_status launch_agg(const char* name, bool feat, int dtype, cudaStream_
     const bool heavy = fanout < 0 || fanout > kSegCap;
     const int64_t cap = heavy ? kSegCap : INT64_MAX;
     gsb_status st;
-    if (feat)
+    // segment-parallel kernel for hidden-layer inputs (layer >= 1: 10.0 vs 15.1 us under ncu on the
+    // mag step); the layer-0 feature gather keeps the warp-per-row kernel, whose per-warp
+    // address resolution beats the per-lane one there (profiles/round2_agg_ab.md).  GSB_AGG=warp /
+    // seg forces either (A/B).  32-byte lanes: rows of 4..32 such chunks, 32-B aligned.
+    static const int agg_mode = !getenv("GSB_AGG") ? 0 : (strcmp(getenv("GSB_AGG"), "warp") == 0 ? 1 : 2);
+    const bool want_seg = agg_mode == 2 || (agg_mode == 0 && !feat);
+    const bool use_seg = want_seg && rb % 32 == 0 && rb / 32 >= 4 && rb / 32 <= 32 && d % 4 == 0 &&
+                         (feat || (reinterpret_cast<uintptr_t>(h) & 31) == 0);
+    if (use_seg) {
+        if (feat)
+            st = dtype == GSB_BF16 ? launch_agg_seg<true, true>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
+                                   : launch_agg_seg<true, false>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
+        else
+            st = dtype == GSB_BF16 ? launch_agg_seg<false, true>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
+                                   : launch_agg_seg<false, false>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
+    } else if (feat)
         st = dtype == GSB_BF16 ? launch_agg_lpe<true, true>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
                                : launch_agg_lpe<true, false>(name, grid, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
     else
