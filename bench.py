@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--peer-gather", default="unique", choices=["unique", "fused"],
                     help="peer mode: gather the unique input rows over NVLink first (unique) or read them per "
                          "edge inside the fused aggregation (fused)")
+    ap.add_argument("--topology", default="partitioned", choices=["partitioned", "replicate"],
+                    help="N>1 graph store: CSC partitioned by dst node ID, remote segments read over NVLink by "
+                         "the sampling kernels (partitioned, default; §8(e)), or the whole CSC on every rank")
     ap.add_argument("--features", default="peer", choices=["peer", "alltoall", "replicate"],
                     help="N>1 feature store: partitioned by node ID and read over NVLink inside the kernels "
                          "(peer, default), partitioned + NCCL all-to-all fetch (alltoall), or replicated")
@@ -238,9 +241,11 @@ def roofline_of(name, prof, sizes, cfg, pk, profile_steps):
 
 
 # ------------------------------------------------------------------------------ gsb arm
-def build_gsb(cfg, device, partition=None, mode="peer"):
+def build_gsb(cfg, device, partition=None, mode="peer", topology="replicate"):
     """partition = (world, rank) -> features partitioned by node ID: mode "peer" maps every
-    rank's shard over NVLink (PeerFeatures), "alltoall" fetches rows with NCCL (FeatureExchange)."""
+    rank's shard over NVLink (PeerFeatures), "alltoall" fetches rows with NCCL (FeatureExchange).
+    topology "partitioned" (with a partition): every rank builds only the CSC of the dst nodes
+    it owns and maps the others' shards over NVLink (PeerCSC)."""
     import torch
     from paper_2406_06022_b200.runtime import GraphStore, LPTrainer, RGCNTrainer
     st = GraphStore(cfg.counts, cfg.etype_src(), cfg.etype_dst(), device)
@@ -250,10 +255,22 @@ def build_gsb(cfg, device, partition=None, mode="peer"):
         keep = {cfg.lp_etype: k}
         if cfg.lp_rev_etype >= 0:
             keep[cfg.lp_rev_etype] = k
+    part_topo = partition is not None and topology == "partitioned"
+    if part_topo:
+        from paper_2406_06022_b200.dist import balanced_bounds
+        pb = balanced_bounds(cfg.counts, partition[0])
     for r in range(cfg.num_etypes):
         s, d = synth.etype_coo(cfg, r, backend="torch", device=device)
-        st.load_etype(r, s, d, None if keep is None else keep.get(r))
+        if part_topo:
+            t = int(cfg.etypes[r].dst)
+            st.load_etype_range(r, s, d, int(pb[t][partition[1]]), int(pb[t][partition[1] + 1]),
+                                None if keep is None else keep.get(r))
+        else:
+            st.load_etype(r, s, d, None if keep is None else keep.get(r))
         del s, d
+    if part_topo:
+        from paper_2406_06022_b200.dist import PeerCSC
+        st._peer_csc = PeerCSC(st, partition[0], partition[1], pb)
     ex = None
     if partition is None:
         for t in range(cfg.num_ntypes):
@@ -358,7 +375,7 @@ def run_gsb(args, cfg):
     from paper_2406_06022_b200 import _lib
     t0 = time.time()
     partitioned = dist is not None and args.features != "replicate"
-    st, tr = build_gsb(cfg, device, (ws, rank) if partitioned else None, args.features)
+    st, tr = build_gsb(cfg, device, (ws, rank) if partitioned else None, args.features, args.topology)
     if partitioned and args.features == "peer" and args.peer_gather == "unique":
         tr.fuse_gather = False   # unique rows over NVLink once (peer loads bypass L2), then local aggregation
     setup_s = time.time() - t0
@@ -590,11 +607,13 @@ def run_gsb(args, cfg):
     kernels = {k: {"us_per_step": v["total_ms"] * 1e3 / args.profile_steps,
                    "share": v["total_ms"] / args.profile_steps / step_ms_prof} for k, v in
                sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])}
+    topo = ("CSC partitioned by dst node ID, remote segments read over NVLink by the sampling kernels"
+            if args.topology == "partitioned" and args.features != "replicate" else "topology replicated")
     par = ("single" if ws == 1 else {
         "peer": f"dp{ws}: features partitioned by node ID, read over NVLink (CUDA IPC) by libgsb kernels "
-                f"({args.peer_gather} gather); topology replicated; NCCL grad all-reduce after the CUDA graph",
-        "alltoall": f"dp{ws}: features partitioned by node ID, NCCL all-to-all fetch; topology replicated; "
-                    f"NCCL grad all-reduce",
+                f"({args.peer_gather} gather); {topo}; NCCL mean all-reduce of the grads after the CUDA graph",
+        "alltoall": f"dp{ws}: features partitioned by node ID, NCCL all-to-all fetch; {topo}; "
+                    f"NCCL mean all-reduce of the grads",
         "replicate": f"dp{ws}: graph + features replicated, NCCL grad all-reduce"}[args.features])
     unit = UNIT if cfg.task == "nc" else "pos_edges/s"
     metric = METRIC if cfg.task == "nc" else "RGCN LP train positive edges/sec on B200"

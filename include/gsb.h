@@ -99,6 +99,17 @@ gsb_status gsb_csc_build(gsb_graph_t g, int32_t etype, const int32_t* src, const
                          const uint8_t* keep, int64_t n_edges, int64_t* indptr, int32_t* indices,
                          int64_t* n_kept, void* ws, size_t ws_bytes, void* stream);
 
+/* Partitioned build (§8(e): the graph partitioned by node ID, edges owned by their dst's
+ * owner): as gsb_csc_build over the kept edges whose dst local id lies in
+ * [dst_lo, dst_hi) only, with dst ids shifted by -dst_lo (indptr: device int64
+ * [dst_hi - dst_lo + 1]).  *n_before (host) receives the kept edges with dst < dst_lo: the
+ * global CSC position of this range's first edge, registered as the etype's eid_base (edge ids
+ * stay those of the whole graph, R-eid).  gsb_csc_build = the range [0, count). */
+gsb_status gsb_csc_build_range(gsb_graph_t g, int32_t etype, const int32_t* src, const int32_t* dst,
+                               const uint8_t* keep, int64_t n_edges, int64_t dst_lo, int64_t dst_hi, int64_t* indptr,
+                               int32_t* indices, int64_t* n_kept, int64_t* n_before, void* ws, size_t ws_bytes,
+                               void* stream);
+
 /* Register a prebuilt CSC (device pointers) for `etype`; eid_base is added to CSC
  * positions to form edge ids (multi-GPU partitions). */
 gsb_status gsb_graph_set_csc(gsb_graph_t g, int32_t etype, const int64_t* indptr, const int32_t* indices,
@@ -468,6 +479,19 @@ gsb_status gsb_ipc_close(void* base_ptr);
 /* Register ntype t's partitioned table: bounds host int64 [world+1] (local-id ranges, bounds[0]
  * = 0, bounds[world] = count), ptrs host [world] device pointers (own shard + IPC-mapped peer
  * shards), row-major [bounds[w+1]-bounds[w]][dim] of dtype (GSB_F32 / GSB_BF16).  world <= 8. */
+/* Partitioned topology read over NVLink (§8(e); P:L86 sampling "on a distributed graph"):
+ * rank w of `world` holds the CSC of the dst nodes it owns -- local ids [bounds[t][w],
+ * bounds[t][w+1]) of every ntype t (bounds: host int64 [T][world+1]) -- built with
+ * gsb_csc_build_range; indptr_w[w] / indices_w[w] are rank w's arrays of `etype` (this
+ * process's own, or IPC-mapped peers' from gsb_ipc_open) and eid_base_w[w] their n_before.
+ * After registration the sampler reads each dst's segment from its owner's HBM (keyed draws:
+ * blocks identical to a whole-graph sampler, bit-exact).  table_dev: caller-owned device
+ * memory of gsb_csc_peers_bytes() bytes, the same for every etype of g.  Syncs stream. */
+gsb_status gsb_csc_peers_bytes(size_t* bytes);
+gsb_status gsb_graph_set_csc_peers(gsb_graph_t g, void* table_dev, int32_t etype, int32_t world,
+                                   const int64_t* bounds, const int64_t* const* indptr_w,
+                                   const int32_t* const* indices_w, const int64_t* eid_base_w, void* stream);
+
 gsb_status gsb_graph_set_feature_peers(gsb_graph_t g, int32_t ntype, int32_t world, const int64_t* bounds,
                                        const void* const* ptrs, int32_t dim, int32_t dtype);
 

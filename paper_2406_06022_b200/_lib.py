@@ -38,6 +38,9 @@ SIGS = {
     "gsb_csc_build_bytes": [P, i32, i64, C.POINTER(sz)],
     "gsb_csc_build": [P, i32, P, P, P, i64, P, P, C.POINTER(i64), P, sz, P],
     "gsb_graph_set_csc": [P, i32, P, P, i64, i64],
+    "gsb_csc_build_range": [P, i32, P, P, P, i64, i64, i64, P, P, C.POINTER(i64), C.POINTER(i64), P, sz, P],
+    "gsb_csc_peers_bytes": [C.POINTER(sz)],
+    "gsb_graph_set_csc_peers": [P, P, i32, i32, P, P, P, P, P],
     "gsb_graph_set_features": [P, i32, P, i32, i32],
     "gsb_gather": [P, P, i64, P, P],
     "gsb_blocks_create": [P, i32, P, i64, i64, C.POINTER(P)],

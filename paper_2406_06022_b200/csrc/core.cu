@@ -72,20 +72,30 @@ void prof_end(cudaStream_t s) {
 // ------------------------------------------------------------------------------------
 // CSC build kernels
 // ------------------------------------------------------------------------------------
+// keys (dst - dst_lo, src) of the kept edges whose dst lies in [dst_lo, dst_hi) (the whole
+// range for a plain build); n_kept[1] counts the kept edges with dst < dst_lo (the global CSC
+// position of a partition's first edge)
 __global__ void csc_keys_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
-                                const uint8_t* __restrict__ keep, int64_t n, uint64_t* __restrict__ keys,
-                                unsigned long long* __restrict__ n_kept) {
+                                const uint8_t* __restrict__ keep, int64_t n, int64_t dst_lo, int64_t dst_hi,
+                                uint64_t* __restrict__ keys, unsigned long long* __restrict__ n_kept) {
     GSB_PDL_ENTRY();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    unsigned long long local = 0;
+    unsigned long long local = 0, before = 0;
     for (; i < n; i += stride) {
-        bool k = keep ? (keep[i] != 0) : true;
-        keys[i] = k ? (((uint64_t)(uint32_t)dst[i] << 32) | (uint32_t)src[i]) : ~0ull;
-        local += k ? 1 : 0;
+        const bool k = keep ? (keep[i] != 0) : true;
+        const int64_t d = dst[i];
+        const bool in = k && d >= dst_lo && d < dst_hi;
+        keys[i] = in ? (((uint64_t)(d - dst_lo) << 32) | (uint32_t)src[i]) : ~0ull;
+        local += in ? 1 : 0;
+        before += (k && d < dst_lo) ? 1 : 0;
     }
-    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        local += __shfl_xor_sync(0xffffffffu, local, o);
+        before += __shfl_xor_sync(0xffffffffu, before, o);
+    }
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_kept, local);
+    if ((threadIdx.x & 31) == 0 && before) atomicAdd(n_kept + 1, before);
 }
 
 __global__ void csc_finish_kernel(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ n_kept_p,
@@ -413,7 +423,9 @@ gsb_status gsb_graph_create(int32_t T, const int64_t* counts, int32_t R, const i
 }
 
 gsb_status gsb_graph_destroy(gsb_graph_t g) {
-    delete reinterpret_cast<Graph*>(g);
+    Graph* G = reinterpret_cast<Graph*>(g);
+    if (G) delete G->cpeers_host;
+    delete G;
     return GSB_OK;
 }
 
@@ -433,7 +445,7 @@ static size_t csc_cub_bytes(int64_t n) {
 gsb_status gsb_csc_build_bytes(gsb_graph_t g, int32_t etype, int64_t n_edges, size_t* bytes) {
     Graph* G = reinterpret_cast<Graph*>(g);
     GSB_CHECK_ARG(G && bytes && etype >= 0 && etype < G->dev.R && n_edges >= 0, "bad argument");
-    *bytes = align_up(sizeof(unsigned long long)) + 2 * align_up(sizeof(uint64_t) * (size_t)(n_edges + 1)) +
+    *bytes = align_up(2 * sizeof(unsigned long long)) + 2 * align_up(sizeof(uint64_t) * (size_t)(n_edges + 1)) +
              align_up(csc_cub_bytes(n_edges));
     return GSB_OK;
 }
@@ -443,8 +455,20 @@ gsb_status gsb_csc_build(gsb_graph_t g, int32_t etype, const int32_t* src, const
                          size_t ws_bytes, void* stream) {
     Graph* G = reinterpret_cast<Graph*>(g);
     GSB_CHECK_ARG(G && etype >= 0 && etype < G->dev.R, "bad graph/etype");
+    int64_t before = 0;
+    return gsb_csc_build_range(g, etype, src, dst, keep, n_edges, 0, G->counts[G->dev.dst_t[etype]], indptr, indices,
+                               n_kept, &before, ws, ws_bytes, stream);
+}
+
+gsb_status gsb_csc_build_range(gsb_graph_t g, int32_t etype, const int32_t* src, const int32_t* dst,
+                               const uint8_t* keep, int64_t n_edges, int64_t dst_lo, int64_t dst_hi, int64_t* indptr,
+                               int32_t* indices, int64_t* n_kept, int64_t* n_before, void* ws, size_t ws_bytes,
+                               void* stream) {
+    Graph* G = reinterpret_cast<Graph*>(g);
+    GSB_CHECK_ARG(G && etype >= 0 && etype < G->dev.R, "bad graph/etype");
     GSB_CHECK_ARG(n_edges == 0 || (src && dst), "null COO");
-    GSB_CHECK_ARG(indptr && indices && n_kept && ws, "null output/workspace");
+    GSB_CHECK_ARG(indptr && indices && n_kept && n_before && ws, "null output/workspace");
+    GSB_CHECK_ARG(dst_lo >= 0 && dst_lo <= dst_hi && dst_hi <= G->counts[G->dev.dst_t[etype]], "bad dst range");
     size_t need = 0;
     gsb_csc_build_bytes(g, etype, n_edges, &need);
     if (ws_bytes < need) {
@@ -454,17 +478,17 @@ gsb_status gsb_csc_build(gsb_graph_t g, int32_t etype, const int32_t* src, const
     cudaStream_t s = (cudaStream_t)stream;
     char* p = (char*)ws;
     unsigned long long* d_cnt = (unsigned long long*)p;
-    p += align_up(sizeof(unsigned long long));
+    p += align_up(2 * sizeof(unsigned long long));
     uint64_t* k_in = (uint64_t*)p;
     p += align_up(sizeof(uint64_t) * (size_t)(n_edges + 1));
     uint64_t* k_out = (uint64_t*)p;
     p += align_up(sizeof(uint64_t) * (size_t)(n_edges + 1));
     size_t cub_b = csc_cub_bytes(n_edges);
-    const int64_t n_dst = G->counts[G->dev.dst_t[etype]];
-    GSB_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s));
+    const int64_t n_dst = dst_hi - dst_lo;
+    GSB_CUDA(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(unsigned long long), s));
     if (n_edges > 0) {
         GSB_LAUNCH("csc_keys", csc_keys_kernel, grid_for(n_edges, 256, kNumSMs * 32), 256, 0, s, src, dst, keep,
-                   n_edges, k_in, d_cnt);
+                   n_edges, dst_lo, dst_hi, k_in, d_cnt);
         int end_bit = 32;
         while (end_bit < 64 && ((int64_t)1 << (end_bit - 32)) <= n_dst) ++end_bit;
         GSB_CUDA(cub::DeviceRadixSort::SortKeys(p, cub_b, k_in, k_out, (int64_t)n_edges, 0, end_bit, s));
@@ -472,14 +496,15 @@ gsb_status gsb_csc_build(gsb_graph_t g, int32_t etype, const int32_t* src, const
     }
     GSB_LAUNCH("csc_finish", csc_finish_kernel, grid_for(n_edges > n_dst ? n_edges : n_dst + 1, 256, kNumSMs * 32),
                256, 0, s, k_out, d_cnt, n_dst, indptr, indices);
-    unsigned long long h = 0;
-    GSB_CUDA(cudaMemcpyAsync(&h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+    unsigned long long h[2] = {0, 0};
+    GSB_CUDA(cudaMemcpyAsync(h, d_cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
     GSB_CUDA(cudaStreamSynchronize(s));
-    *n_kept = (int64_t)h;
+    *n_kept = (int64_t)h[0];
+    *n_before = (int64_t)h[1];
     G->dev.indptr[etype] = indptr;
     G->dev.indices[etype] = indices;
-    G->dev.eid_base[etype] = 0;
-    G->n_edges[etype] = (int64_t)h;
+    G->dev.eid_base[etype] = (int64_t)h[1];
+    G->n_edges[etype] = (int64_t)h[0];
     return GSB_OK;
 }
 

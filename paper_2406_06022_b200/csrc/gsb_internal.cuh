@@ -120,7 +120,50 @@ struct GraphDev {
     int32_t nparts;
     int64_t plo[kMaxT][kMaxPeers + 1];
     const char* peer[kMaxT][kMaxPeers];
+    // node-ID partitioned topology (peer.cu, §8(e)): device table of every rank's CSC shard,
+    // or null when this process holds the whole CSC (indptr / indices above)
+    const struct CscPeers* cpeers;
 };
+
+// Partitioned CSC: rank w holds the in-edges of the dst nodes it owns, local ids
+// [lo[t][w], lo[t][w+1]) of every ntype t, as a CSC over that range (positions local to its
+// own indices array) whose first edge has global CSC position eid_base[r][w].  Segments of
+// other ranks' dst nodes are read from the owner's HBM over NVLink (CUDA IPC pointers).
+// Lives in caller-owned device memory (gsb_csc_peers_bytes).
+struct CscPeers {
+    int32_t world;
+    int64_t lo[kMaxT][kMaxPeers + 1];
+    const int64_t* indptr[kMaxR][kMaxPeers];
+    const int32_t* indices[kMaxR][kMaxPeers];
+    int64_t eid_base[kMaxR][kMaxPeers];
+};
+
+// In-edge segment of dst local id vl (ntype t) in etype r: indices seg[0..deg), edge ids
+// eid0 + position.  Whole CSC, or the owner's shard of a partitioned one.
+struct CscSeg {
+    const int32_t* seg;
+    int64_t deg, eid0;
+};
+__device__ __forceinline__ CscSeg csc_seg(const GraphDev& g, int r, int t, int64_t vl) {
+    CscSeg c;
+    if (g.cpeers) {
+        const CscPeers& P = *g.cpeers;
+        int w = 0;
+#pragma unroll 1
+        for (int k = 1; k < P.world; ++k) w += (vl >= P.lo[t][k]) ? 1 : 0;
+        const int64_t* ip = P.indptr[r][w] + (vl - P.lo[t][w]);
+        const int64_t a = ip[0];
+        c.deg = ip[1] - a;
+        c.seg = P.indices[r][w] + a;
+        c.eid0 = P.eid_base[r][w] + a;
+    } else {
+        const int64_t a = g.indptr[r][vl];
+        c.deg = g.indptr[r][vl + 1] - a;
+        c.seg = g.indices[r] + a;
+        c.eid0 = g.eid_base[r] + a;
+    }
+    return c;
+}
 
 __host__ __device__ inline int type_of(const GraphDev& g, int64_t gid) {
     int t = 0;
@@ -177,6 +220,7 @@ struct HopBufs {
 
 struct Graph {
     GraphDev dev;
+    CscPeers* cpeers_host = nullptr;   // host mirror of the partitioned-CSC table (peer.cu)
     bool dtype_set = false;
     int64_t counts[kMaxT];
     int64_t n_edges[kMaxR];

@@ -81,4 +81,43 @@ gsb_status gsb_graph_set_feature_peers(gsb_graph_t g, int32_t ntype, int32_t wor
     return GSB_OK;
 }
 
+gsb_status gsb_csc_peers_bytes(size_t* bytes) {
+    GSB_CHECK_ARG(bytes, "null argument");
+    *bytes = sizeof(CscPeers);
+    return GSB_OK;
+}
+
+gsb_status gsb_graph_set_csc_peers(gsb_graph_t g, void* table_dev, int32_t etype, int32_t world,
+                                   const int64_t* bounds, const int64_t* const* indptr_w,
+                                   const int32_t* const* indices_w, const int64_t* eid_base_w, void* stream) {
+    Graph* G = reinterpret_cast<Graph*>(g);
+    GSB_CHECK_ARG(G && table_dev && bounds && indptr_w && indices_w && eid_base_w, "null argument");
+    GSB_CHECK_ARG(etype >= 0 && etype < G->dev.R, "etype %d out of range", etype);
+    GSB_CHECK_ARG(world >= 1 && world <= kMaxPeers, "world %d out of [1, %d]", world, kMaxPeers);
+    GSB_CHECK_ARG(((uintptr_t)table_dev & 15) == 0, "table must be 16-byte aligned");
+    if (!G->cpeers_host) {
+        G->cpeers_host = new CscPeers();
+        memset(G->cpeers_host, 0, sizeof(CscPeers));
+    }
+    CscPeers& P = *G->cpeers_host;
+    GSB_CHECK_ARG(P.world == 0 || P.world == world, "world changed between etypes");
+    P.world = world;
+    for (int t = 0; t < G->dev.T; ++t) {
+        GSB_CHECK_ARG(bounds[t * (world + 1)] == 0 && bounds[t * (world + 1) + world] == G->counts[t],
+                      "bounds of ntype %d must span [0, count)", t);
+        for (int w = 0; w <= world; ++w) P.lo[t][w] = bounds[t * (world + 1) + w];
+    }
+    for (int w = 0; w < world; ++w) {
+        GSB_CHECK_ARG(indptr_w[w], "null indptr of rank %d", w);
+        P.indptr[etype][w] = indptr_w[w];
+        P.indices[etype][w] = indices_w[w];
+        P.eid_base[etype][w] = eid_base_w[w];
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    GSB_CUDA(cudaMemcpyAsync(table_dev, &P, sizeof(CscPeers), cudaMemcpyHostToDevice, s));
+    GSB_CUDA(cudaStreamSynchronize(s));
+    G->dev.cpeers = static_cast<const CscPeers*>(table_dev);
+    return GSB_OK;
+}
+
 }  // extern "C"

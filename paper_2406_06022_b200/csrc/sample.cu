@@ -62,10 +62,10 @@ __global__ void excl_ranges_kernel(GraphDev g, const uint64_t* __restrict__ keys
             const int64_t u = (int64_t)(key & 0x7FFFFFFFull);
             const int t = type_of(g, v);
             const int64_t vl = v - g.node_off[t];
-            const int64_t a = g.indptr[r][vl];
-            const int64_t deg = g.indptr[r][vl + 1] - a;
+            const CscSeg cs = csc_seg(g, r, t, vl);
+            const int64_t deg = cs.deg;
             const int32_t ul = (int32_t)(u - g.node_off[g.src_t[r]]);
-            const int32_t* seg = g.indices[r] + a;
+            const int32_t* seg = cs.seg;
             int64_t l = 0, h = deg;
             while (l < h) { int64_t m = (l + h) >> 1; if (seg[m] < ul) l = m + 1; else h = m; }
             lo = l;
@@ -272,11 +272,11 @@ __device__ __forceinline__ int64_t count_one(const GraphDev& g, int64_t i, int64
     if (s >= g.n_slots[t]) return 0;
     const int r = g.slot_etype[t][s];
     const int64_t vl = v - g.node_off[t];
-    const int64_t a = g.indptr[r][vl];
-    int64_t deg = g.indptr[r][vl + 1] - a;
+    const CscSeg cs = csc_seg(g, r, t, vl);
+    int64_t deg = cs.deg;
     int64_t k0, k1;
     excl_range(ex, r, v, k0, k1);
-    if (k1 > k0) deg -= excl_count(ex, k0, k1, g.indices[r] + a, deg, g.node_off[g.src_t[r]]);
+    if (k1 > k0) deg -= excl_count(ex, k0, k1, cs.seg, deg, g.node_off[g.src_t[r]]);
     return (fanout < 0 || deg <= fanout) ? deg : fanout;
 }
 
@@ -409,9 +409,9 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
         const int t = type_of(g, v);
         const int r = g.slot_etype[t][s];
         const int64_t vl = v - g.node_off[t];
-        const int64_t a = g.indptr[r][vl];
-        const int64_t deg = g.indptr[r][vl + 1] - a;
-        const int32_t* seg = g.indices[r] + a;
+        const CscSeg cs = csc_seg(g, r, t, vl);
+        const int64_t deg = cs.deg;
+        const int32_t* seg = cs.seg;
         const int64_t src_off = g.node_off[g.src_t[r]];
         int64_t k0, k1;
         excl_range(ex, r, v, k0, k1);
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
                 int64_t p = has_ex ? excl_map(ex, k0, k1, seg, deg, src_off, q) : q;
                 int64_t u = src_off + seg[p];
                 e_src_gid[base + q] = u;
-                e_eid[base + q] = g.eid_base[r] + a + p;
+                e_eid[base + q] = cs.eid0 + p;
                 if (map[u] < 0) {
                     uint32_t bit = 1u << (u & 31);
                     if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
             int64_t p = has_ex ? excl_map(ex, k0, k1, seg, deg, src_off, sel) : sel;
             int64_t u = src_off + seg[p];
             e_src_gid[base + gl] = u;
-            e_eid[base + gl] = g.eid_base[r] + a + p;
+            e_eid[base + gl] = cs.eid0 + p;
             if (map[u] < 0) {
                 uint32_t bit = 1u << (u & 31);
                 if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);
@@ -510,9 +510,9 @@ __global__ void __launch_bounds__(256) fill_tail_kernel(GraphDev g, const HopMet
                 const int t = type_of(g, v);
                 const int r = g.slot_etype[t][s];
                 const int64_t vl = v - g.node_off[t];
-                const int64_t a = g.indptr[r][vl];
-                const int64_t deg = g.indptr[r][vl + 1] - a;
-                const int32_t* seg = g.indices[r] + a;
+                const CscSeg cs = csc_seg(g, r, t, vl);
+                const int64_t deg = cs.deg;
+                const int32_t* seg = cs.seg;
                 const int64_t src_off = g.node_off[g.src_t[r]];
                 int64_t k0, k1;
                 excl_range(ex, r, v, k0, k1);
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(256) fill_tail_kernel(GraphDev g, const HopMet
                     const int64_t p = has_ex ? excl_map(ex, k0, k1, seg, deg, src_off, q) : q;
                     const int64_t u = src_off + seg[p];
                     e_src_gid[base + q] = u;
-                    e_eid[base + q] = g.eid_base[r] + a + p;
+                    e_eid[base + q] = cs.eid0 + p;
                     if (map[u] < 0) {
                         const uint32_t bit = 1u << (u & 31);
                         if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);

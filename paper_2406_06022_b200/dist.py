@@ -151,6 +151,58 @@ class PeerFeatures:
         self.store = store
 
 
+class PeerCSC:
+    """Node-ID partitioned topology read over NVLink (§8(e); "a
+    worker reads only its own partition's storage"): rank w built (GraphStore.load_etype_range)
+    the CSC of every etype over the dst nodes it owns; the shards of all ranks are mapped into
+    every process with CUDA IPC and registered (gsb_graph_set_csc_peers), so the sampling
+    kernels read each dst's in-edge segment from its owner's HBM.  Keyed draws make the blocks
+    identical to the whole-graph sampler's (bit-exact), with no collective on the data path."""
+
+    def __init__(self, store, world: int, rank: int, bounds, group=None):
+        import ctypes as C
+        import numpy as np
+        import torch.distributed as dist
+        from ._lib import call
+        self.bounds = np.ascontiguousarray(bounds, dtype=np.int64)        # [T][world+1]
+        mine = []
+        for r in range(store.R):
+            hs = []
+            for t in (store.indptr[r], store.indices[r]):
+                h = (C.c_char * 64)()
+                off = C.c_int64()
+                call("gsb_ipc_handle", C.c_void_p(t.data_ptr()), h, C.byref(off))
+                hs.append((bytes(h), int(off.value)))
+            mine.append((hs, int(store.eid_base[r])))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        nb = C.c_size_t()
+        call("gsb_csc_peers_bytes", C.byref(nb))
+        dev = store.device
+        self.table = torch.zeros(int(nb.value), dtype=torch.uint8, device=dev)
+        self.mapped = []
+        s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for r in range(store.R):
+            ip = (C.c_void_p * world)()
+            ix = (C.c_void_p * world)()
+            eb = (C.c_int64 * world)()
+            for w in range(world):
+                (hip, hix), base = allh[w][r]
+                eb[w] = base
+                if w == rank:
+                    ip[w] = store.indptr[r].data_ptr()
+                    ix[w] = store.indices[r].data_ptr()
+                    continue
+                for arr, (hb, off) in ((ip, hip), (ix, hix)):
+                    p = C.c_void_p()
+                    call("gsb_ipc_open", (C.c_char * 64).from_buffer_copy(hb), off, C.byref(p))
+                    arr[w] = p.value
+                    self.mapped.append(p.value - off)
+            call("gsb_graph_set_csc_peers", store.h, C.c_void_p(self.table.data_ptr()), r, world,
+                 self.bounds.ctypes.data_as(C.c_void_p), ip, ix, eb, s)
+        store._csc_peers = self
+
+
 class PeerEmbedding:
     """A learnable table (§8(f) f1) partitioned over the ranks of one box (R-sparsedist): rank
     w holds rows [bounds[w], bounds[w+1]) of the table, its Adagrad state, a gradient

@@ -103,6 +103,35 @@ class GraphStore:
         self.indices[r] = indices
         self.n_edges[r] = int(kept.value)
 
+    def load_etype_range(self, r: int, src: torch.Tensor, dst: torch.Tensor, lo: int, hi: int,
+                         keep: Optional[torch.Tensor] = None):
+        """gsb_csc_build_range: this rank's shard of etype r's CSC -- the in-edges of the dst
+        local ids [lo, hi) it owns (§8(e), node-ID partition); eid_base = global position of
+        the shard's first edge."""
+        s = torch.as_tensor(src, dtype=torch.int32).to(self.device).contiguous()
+        d = torch.as_tensor(dst, dtype=torch.int32).to(self.device).contiguous()
+        k = None if keep is None else torch.as_tensor(keep, dtype=torch.uint8).to(self.device).contiguous()
+        n = s.numel()
+        ws_b = C.c_size_t()
+        call("gsb_csc_build_bytes", self.h, r, n, C.byref(ws_b))
+        ws = torch.empty(max(int(ws_b.value), 1), dtype=torch.uint8, device=self.device)
+        indptr = torch.empty(hi - lo + 1, dtype=torch.int64, device=self.device)
+        # capacity: every edge could fall in range; trimmed to the kept count below
+        indices = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        kept, before = C.c_int64(), C.c_int64()
+        call("gsb_csc_build_range", self.h, r, _ptr(s), _ptr(d), _ptr(k), n, lo, hi, _ptr(indptr), _ptr(indices),
+             C.byref(kept), C.byref(before), _ptr(ws), ws.numel(), _stream())
+        del ws
+        indices = indices[:max(int(kept.value), 1)].clone()
+        call("gsb_graph_set_csc", self.h, r, _ptr(indptr), _ptr(indices), int(kept.value), int(before.value))
+        self.indptr[r] = indptr
+        self.indices[r] = indices
+        self.n_edges[r] = int(kept.value)
+        self.eid_base = getattr(self, "eid_base", [0] * self.R)
+        self.eid_base[r] = int(before.value)
+        self.part_range = getattr(self, "part_range", {})
+        self.part_range[r] = (lo, hi)
+
     def set_features(self, t: int, feat: torch.Tensor):
         """Register ntype t's feature table (fp32 or bf16 rows; one format for all ntypes)."""
         dt = feat.dtype if feat.dtype in DTYPE_CODE else torch.float32
