@@ -36,8 +36,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="gsb", choices=["gsb", "reference"])
-    ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b", "amazon_lp", "tiny_lp", "mag240m",
-                                                        "mag240m_1_16"])
+    ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b", "gcn_1b", "amazon_lp", "tiny_lp",
+                                                        "mag240m", "mag240m_1_16"])
     ap.add_argument("--feat-dtype", default="auto", choices=["auto", "f32", "bf16"],
                     help="feature storage type; compute stays fp32 (auto: bf16 for the large configs, as "
                          "SURVEY §8(d) plans, fp32 for tiny)")
@@ -172,10 +172,15 @@ def peaks():
 
 
 def kernel_work(name: str, sz: dict, cfg: synth.Config):
-    """Algorithmic bytes (HBM-bound kernels) or flops (GEMMs) of ONE launch of `name` for a
-    step with block sizes sz (DESIGN.md §6 per-unit figures x units of the launch)."""
+    """Algorithmic bytes (HBM-bound kernels) or flops (GEMMs) of `name` over ONE STEP with block
+    sizes sz: SURVEY §8(d)'s per-unit figures x the units of the step.
+      gather / aggregation: per sampled edge one d-wide source row + a 4-B index; per dst row its
+        self row; per non-empty (dst, relation) segment one fp32 mean row written (the copy of
+        the self row into the GEMM operand is not counted);
+      sampling fill: per (dst, relation) 16 B of indptr; per sampled edge 4 B index read + 16 B
+        (src gid, eid) written;
+      GEMMs: 2 M N K flop (the 3xTF32 split is not counted)."""
     d0, hd, C = cfg.feat_dim, cfg.hidden, cfg.num_classes
-    L = len(cfg.fanouts)
     lay = None
     if name[-3:-1] == "_l" and name[-1].isdigit():
         lay = int(name[-1])
@@ -183,16 +188,15 @@ def kernel_work(name: str, sz: dict, cfg: synth.Config):
     fe = 2 if cfg.feat_dtype == "bf16" else 4      # feature element bytes (layer-0 inputs)
     if name == "gather":
         n = sz["n_src"][0]
-        return "bytes", n * d0 * fe * 2 + n * 8
+        return "bytes", n * d0 * fe * 2 + n * 4
     if name == "rgcn_agg" and lay is not None:
         d = d0 if lay == 0 else hd
         es = fe if lay == 0 else 4
-        # per sampled edge: one d-wide source row + its index; per dst row: self row + fp32 Acat row
-        idx = 12 if lay == 0 else 4
-        return "bytes", sz["n_edges"][lay] * (d * es + idx) + sz["n_dst"][lay] * d * es + sz["acat_cols"][lay] * 4
-    if name in ("rgcn_gemm_fwd", "rgcn_gemm_dW") and lay is not None:
-        return "flops", 2 * sz["acat_cols"][lay] * hd
-    if name == "rgcn_gemm_dA" and lay is not None:
+        return "bytes", (sz["n_edges"][lay] * (d * es + 4) + sz["n_dst"][lay] * d * es +
+                         sz["nonempty_segs"][lay] * d * 4)
+    if name == "sample_fill":
+        return "bytes", sum(16 * sz["dst_rel"][l] + 20 * sz["n_edges"][l] for l in range(len(cfg.fanouts)))
+    if name in ("rgcn_gemm_fwd", "rgcn_gemm_dW", "rgcn_gemm_dA") and lay is not None:
         return "flops", 2 * sz["acat_cols"][lay] * hd
     if name in ("enc_gemm_fwd", "enc_gemm_dW") and cfg.has_encoder:
         # a6: HBM bytes of the gathered bf16 rows of projected ntypes (+ the fp32 H0 rows written
@@ -205,14 +209,27 @@ def kernel_work(name: str, sz: dict, cfg: synth.Config):
     return None, None
 
 
+def traffic_of(cfg, name):
+    """DRAM bytes per launch of `name` from the ncu --set full capture recorded in
+    profiles/roofline_traffic.json for this config (dram__bytes_read.sum + write.sum)."""
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+        e = tj.get(f"{cfg.name}:{name}")
+        return (e["bytes"], e["capture"]) if e else (None, None)
+    except Exception:
+        return None, None
+
+
 def roofline_of(name, prof, sizes, cfg, pk, profile_steps):
-    """Roofline entry of kernel `name`: algorithmic work per launch (kernel_work) / its mean
-    CUDA-event launch time, against the measured peak; DRAM traffic from the ncu capture
-    recorded in profiles/roofline_traffic.json for this config (null if none)."""
+    """Roofline entry of kernel `name`: algorithmic work per launch (kernel_work per step /
+    launches per step) / its mean CUDA-event launch time, against the measured peak; DRAM
+    traffic per launch from the ncu capture (profiles/roofline_traffic.json) and the DRAM
+    fraction it implies at the same launch time."""
     kind, _ = kernel_work(name, sizes[0], cfg)
     if kind is None or name not in prof:
         return None
-    per_launch_work = float(np.mean([kernel_work(name, s, cfg)[1] for s in sizes]))
+    lps = prof[name]["launches"] / profile_steps
+    per_launch_work = float(np.mean([kernel_work(name, s, cfg)[1] for s in sizes])) / lps
     avg_ms = prof[name]["total_ms"] / prof[name]["launches"]
     if kind == "bytes":
         ach = per_launch_work / (avg_ms / 1e3) / 1e9
@@ -226,16 +243,13 @@ def roofline_of(name, prof, sizes, cfg, pk, profile_steps):
         roof = {"kernel": name, "bound": "tensor", "achieved": ach, "peak": tf32, "unit": "TFLOP/s",
                 "frac": ach / tf32, "traffic": None,
                 "peak_src": "dense TF32 = measured bf16 burst (MEASURED_PEAKS.json) x 0.5 (nominal ratio)"}
-    try:
-        tj = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
-        key = f"{cfg.name}:{name}"
-        if key in tj:
-            roof["traffic"] = tj[key]["bytes"]
-            roof["traffic_src"] = tj[key]["capture"]
-    except Exception:
-        pass
+    tb, tsrc = traffic_of(cfg, name)
+    if tb is not None:
+        roof["traffic"] = tb
+        roof["traffic_src"] = tsrc
+        roof["dram_frac"] = tb / (avg_ms / 1e3) / 1e9 / pk["hbm_gbs"]
     roof["avg_launch_us"] = avg_ms * 1e3
-    roof["launches_per_step"] = prof[name]["launches"] / profile_steps
+    roof["launches_per_step"] = lps
     roof["algorithmic_per_launch"] = per_launch_work
     return roof
 
@@ -349,7 +363,8 @@ def launches_per_step_graph(tr, cfg):
 def block_sizes(tr, cfg):
     L = len(cfg.fanouts)
     sm = tr.sampler
-    out = {"n_dst": [], "n_src": [], "n_edges": [], "acat_cols": [], "src_type_cnt0": None}
+    out = {"n_dst": [], "n_src": [], "n_edges": [], "acat_cols": [], "src_type_cnt0": None, "nonempty_segs": [],
+           "dst_rel": [], "src_gid0": None}
     slots = tr.store.slot_etypes()
     for l in range(L):
         b = sm.block(l)
@@ -358,6 +373,10 @@ def block_sizes(tr, cfg):
         out["n_src"].append(int(b.src_gid.numel()))
         out["n_edges"].append(int(b.e_src.numel()))
         out["acat_cols"].append(int(sum(int(b.dst_type_cnt[t]) * (len(slots[t]) + 1) * d for t in range(len(slots)))))
+        out["nonempty_segs"].append(int((b.seg_ptr[1:] > b.seg_ptr[:-1]).sum().item()))
+        out["dst_rel"].append(int(sum(int(b.dst_type_cnt[t]) * len(slots[t]) for t in range(len(slots)))))
+        if l == 0:
+            out["src_gid0"] = b.src_gid.cpu().numpy()
         if l == 0:
             out["src_type_cnt0"] = [int(x) for x in b.src_type_cnt]
     return out
@@ -603,6 +622,35 @@ def run_gsb(args, cfg):
     dom = next((k for k in ranked if kernel_work(k, sizes[0], cfg)[0] is not None), ranked[0])
     roof = roofline_of(dom, prof, sizes, cfg, pk, args.profile_steps)
     roof_agg = roofline_of("rgcn_agg_l0", prof, sizes, cfg, pk, args.profile_steps) if "rgcn_agg_l0" in prof else None
+    roof_more = {}
+    for k in ranked:
+        if k == dom or k == "rgcn_agg_l0":
+            continue
+        e = roofline_of(k, prof, sizes, cfg, pk, args.profile_steps)
+        if e is not None:
+            roof_more[k] = {x: e[x] for x in ("bound", "achieved", "peak", "unit", "frac", "avg_launch_us",
+                                               "launches_per_step", "traffic", "dram_frac") if x in e}
+    nvlink = None
+    if ws > 1 and args.features == "peer":
+        # unique input rows owned by other ranks, fetched over NVLink (peer loads) per step; the
+        # remote CSC segments the sampler reads are small next to them (16 B indptr + f x 4 B)
+        from paper_2406_06022_b200.dist import balanced_bounds
+        bnd = balanced_bounds(cfg.counts, ws)
+        rem = []
+        for sz in sizes:
+            g0 = sz["src_gid0"]
+            t = np.searchsorted(cfg.node_off, g0, side="right") - 1
+            loc = g0 - cfg.node_off[t]
+            own = (loc >= bnd[t, rank]) & (loc < bnd[t, rank + 1])
+            rem.append(int((~own).sum()))
+        rbytes = float(np.mean(rem)) * cfg.feat_dim * (2 if cfg.feat_dtype == "bf16" else 4)
+        k = "gather" if "gather" in prof else "rgcn_agg_l0"
+        kus = prof[k]["total_ms"] / args.profile_steps * 1e3 if k in prof else None
+        nvlink = {"kernel": k, "remote_rows_per_step": float(np.mean(rem)), "bytes_per_step": rbytes,
+                  "achieved": rbytes / (kus / 1e6) / 1e9 if kus else None, "peak": 900.0, "unit": "GB/s",
+                  "frac": (rbytes / (kus / 1e6) / 1e9 / 900.0) if kus else None,
+                  "peak_src": "NVLink 5 per-direction bandwidth per GPU (B200_PROFILING.md)",
+                  "note": "bytes the kernel pulls from peer HBM / its CUDA-event time in the profiled steps"}
     step_ms_prof = sum(v["total_ms"] for v in prof.values()) / args.profile_steps
     kernels = {k: {"us_per_step": v["total_ms"] * 1e3 / args.profile_steps,
                    "share": v["total_ms"] / args.profile_steps / step_ms_prof} for k, v in
@@ -627,6 +675,8 @@ def run_gsb(args, cfg):
         "sampled_edges_per_s": edges_per_step * ws / (ms_per_step / 1e3),
         "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches), "roofline": roof,
         "roofline_gather_aggregation": roof_agg,
+        "roofline_kernels": roof_more,
+        "nvlink": nvlink,
         "kernels": kernels, "setup_s": setup_s,
         "phase_ms_alone": phase_ms,
         "host_enqueue_ms_per_step": host_enqueue_ms / args.steps,
@@ -639,9 +689,21 @@ def run_gsb(args, cfg):
 
 
 # ------------------------------------------------------------------------------ oracle
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def oracle_rate(cfg, seconds: float, sub_batch: int, max_steps: int = 10 ** 9, min_steps: int = 1):
-    """Time the oracle (as it stands, single-threaded) on bounded samples of the workload:
-    train steps on sub-batches of `sub_batch` seeds until `seconds` of CPU work."""
+    """Time the oracle (as it stands) on bounded samples of the workload: train steps on
+    sub-batches of `sub_batch` seeds, first single-threaded, then on all host cores
+    (oracle_set_threads: the layer loops over OpenMP threads, bit-identical results), each
+    for about seconds/2 of CPU work.  value = the all-core rate."""
     import oracle
     t0 = time.time()
     og = oracle.Graph(cfg)
@@ -653,18 +715,30 @@ def oracle_rate(cfg, seconds: float, sub_batch: int, max_steps: int = 10 ** 9, m
     opt = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}
     labels = synth.labels(cfg)
     train = synth.train_nodes(cfg)
-    n_seeds, steps, el = 0, 0, 0.0
-    while (el < seconds or steps < min_steps) and steps < max_steps:
-        seeds = synth.nc_seeds(cfg, steps, train)[:sub_batch]
-        t1 = time.perf_counter()
-        oracle.train_step(og, params, opt, steps + 1, (seeds, labels), steps, cfg.rng_seed, cfg.lr)
-        el += time.perf_counter() - t1
-        n_seeds += len(seeds)
-        steps += 1
-    return {"value": n_seeds / el, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{steps} oracle train steps of {sub_batch} seeds each ({cfg.name} graph, fanouts "
-                      f"{cfg.fanouts}), {el:.1f} s of single-threaded CPU work; oracle CSC build "
-                      f"{setup:.1f} s excluded", "steps": steps, "seconds": el}
+    nproc = os.cpu_count() or 1
+    rates = {}
+    step_i = 0
+    for threads in (1, nproc):
+        oracle.set_threads(threads)
+        n_seeds, steps, el = 0, 0, 0.0
+        while (el < seconds / 2 or steps < min_steps) and steps < max_steps:
+            seeds = synth.nc_seeds(cfg, step_i, train)[:sub_batch]
+            t1 = time.perf_counter()
+            oracle.train_step(og, params, opt, step_i + 1, (seeds, labels), step_i, cfg.rng_seed, cfg.lr)
+            el += time.perf_counter() - t1
+            n_seeds += len(seeds)
+            steps += 1
+            step_i += 1
+        rates[threads] = (n_seeds / el, steps, el)
+    oracle.set_threads(1)
+    v1, s1, e1 = rates[1]
+    vn, sn, en = rates[nproc]
+    return {"value": vn, "unit": UNIT, "cores": nproc, "kind": "oracle",
+            "sample": f"oracle train steps of {sub_batch} seeds each ({cfg.name} graph, fanouts {cfg.fanouts}): "
+                      f"{sn} steps in {en:.1f} s on {nproc} threads (OpenMP over dst rows, bit-identical), "
+                      f"{s1} steps in {e1:.1f} s on 1 thread; oracle CSC build {setup:.1f} s excluded",
+            "value_1thread": v1, "nproc": nproc, "cpu_model": cpu_model(), "steps": sn + s1,
+            "seconds": en + e1}
 
 
 def run_reference(args, cfg):
@@ -673,6 +747,8 @@ def run_reference(args, cfg):
         return None
     sub = max(8, cfg.batch // 16)
     import oracle
+    nproc = os.cpu_count() or 1
+    oracle.set_threads(nproc)          # the oracle as it stands, on all host cores (bit-identical)
     t0 = time.time()
     og = oracle.Graph(cfg)
     if not cfg.has_encoder:   # encoder configs read rows from the generator's closed form
@@ -699,9 +775,10 @@ def run_reference(args, cfg):
             "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded hash generator, synth/)", "impl": "reference",
             "config": cfg_json(cfg, ws, {"reference_sub_batch": sub}),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"each step = one oracle train step on {sub} of the batch's seeds; "
-                                       f"oracle CSC build {setup:.1f} s excluded"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nproc, "kind": "oracle",
+                             "sample": f"each step = one oracle train step on {sub} of the batch's seeds, "
+                                       f"{nproc} OpenMP threads; oracle CSC build {setup:.1f} s excluded",
+                             "cpu_model": cpu_model(), "nproc": nproc},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
 

@@ -26,9 +26,10 @@ _SRC = os.path.join(_HERE, "oracle.c")
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.c with gcc (plain -O2, single-threaded)."""
+    """Compile oracle.c with gcc (plain -O2; OpenMP only for oracle_set_threads > 1)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-o", _SO, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-fopenmp", "-shared", "-fPIC", "-o", _SO, _SRC,
+                               "-lm"])
     return _SO
 
 
@@ -65,6 +66,8 @@ def lib():
             "oracle_adam": (None, [i64, P, P, P, P, dbl, dbl, dbl, dbl, i32]),
             "oracle_sparse_adagrad": (None, [i64, i32, P, P, P, P, dbl, dbl]),
             "oracle_sgd": (None, [i64, P, P, dbl]),
+            "oracle_set_threads": (None, [i32]),
+            "oracle_max_threads": (i32, []),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -72,6 +75,15 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """Threads of the layer loops (bit-identical results for any n; see oracle.c header)."""
+    lib().oracle_set_threads(int(n))
+
+
+def max_threads() -> int:
+    return int(lib().oracle_max_threads())
 
 
 def _p(a: Optional[np.ndarray]):

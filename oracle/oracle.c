@@ -17,14 +17,34 @@
  *
  * Parity pins: see tests/test_oracle_*.py.  Functions without a pin: none (the
  * end-to-end loss trajectory on large configs is "parity unpinned").
+ *
+ * Threads: single-threaded by default.  oracle_set_threads(n) runs the layer's per-dst-row
+ * loops (segment means, forward rows) and the weight gradient's per-(relation, input column)
+ * rows on n OpenMP threads; every output element is still summed by one thread in the same
+ * order as the serial loops, so the results are bit-identical for any n (used to time the
+ * oracle on all host cores, bench.py cpu_baseline).
  */
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
 #define OR_MAXT 16
 #define OR_MAXR 64
+
+static int g_threads = 1;
+void oracle_set_threads(int32_t n) { g_threads = n < 1 ? 1 : n; }
+int32_t oracle_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_num_procs();
+#else
+    return 1;
+#endif
+}
 
 /* ======================================================================================
  * 1. Philox4x32-10 (Salmon et al., SC'11).  The paper is silent on the RNG (R-rng);
@@ -367,18 +387,26 @@ static void rel_counts(int64_t n_dst, int32_t R, const int64_t* e_dst, const int
 static void rel_means(int64_t n_dst, int32_t R, int32_t d_in, const int64_t* e_dst, const int32_t* e_et,
                       const int32_t* e_src, int64_t E, const int64_t* c, const double* h_src, double* A) {
     memset(A, 0, sizeof(double) * (size_t)(n_dst * R * d_in));
-    for (int64_t e = 0; e < E; ++e) {
-        double* a = A + ((size_t)e_dst[e] * R + e_et[e]) * d_in;
-        const double* h = h_src + (size_t)e_src[e] * d_in;
-        for (int32_t k = 0; k < d_in; ++k) a[k] += h[k];
-    }
-    for (int64_t v = 0; v < n_dst; ++v)
+    /* edges come dst-row-major (j-major sampler order): the edges of row v are [off[v],
+     * off[v+1]); each row's sums run in edge order whether the rows run serially or not */
+    int64_t* off = (int64_t*)calloc((size_t)n_dst + 1, sizeof(int64_t));
+    for (int64_t e = 0; e < E; ++e) off[e_dst[e] + 1] += 1;
+    for (int64_t v = 0; v < n_dst; ++v) off[v + 1] += off[v];
+    #pragma omp parallel for schedule(static) num_threads(g_threads)
+    for (int64_t v = 0; v < n_dst; ++v) {
+        for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+            double* a = A + ((size_t)v * R + e_et[e]) * d_in;
+            const double* h = h_src + (size_t)e_src[e] * d_in;
+            for (int32_t k = 0; k < d_in; ++k) a[k] += h[k];
+        }
         for (int32_t r = 0; r < R; ++r) {
             int64_t cc = c[v * R + r];
             if (cc == 0) continue;
             double* a = A + ((size_t)v * R + r) * d_in;
             for (int32_t k = 0; k < d_in; ++k) a[k] = a[k] / (double)cc;
         }
+    }
+    free(off);
 }
 
 /* Exposed for tests: the per-relation means A[v][r][:] and counts c[v][r] (section 6). */
@@ -396,6 +424,7 @@ void oracle_rgcn_fwd(int64_t n_dst, int32_t R, int32_t d_in, int32_t d_out,
     double* A = (double*)malloc(sizeof(double) * (size_t)(n_dst * R * d_in + 1));
     rel_counts(n_dst, R, e_dst, e_et, E, c);
     rel_means(n_dst, R, d_in, e_dst, e_et, e_src, E, c, h_src, A);
+    #pragma omp parallel for schedule(static) num_threads(g_threads)
     for (int64_t v = 0; v < n_dst; ++v) {
         double* zv = z + (size_t)v * d_out;
         for (int32_t n = 0; n < d_out; ++n) zv[n] = b[n];
@@ -433,16 +462,27 @@ void oracle_rgcn_bwd(int64_t n_dst, int64_t n_src, int32_t R, int32_t d_in, int3
     memset(dW, 0, sizeof(double) * (size_t)(R + 1) * d_in * d_out);
     memset(db, 0, sizeof(double) * (size_t)d_out);
     if (dh_src) memset(dh_src, 0, sizeof(double) * (size_t)(n_src * d_in));
+    /* dW_r[k][:] = sum over v (in row order) of a_v[k] * dZ_v: rows k of one relation in
+     * blocks of 16 per thread, every element summed over v in ascending order */
+    const int32_t nkb = (d_in + 15) / 16;
+    #pragma omp parallel for schedule(static) num_threads(g_threads)
+    for (int64_t rb = 0; rb < (int64_t)(R + 1) * nkb; ++rb) {
+        const int32_t r = (int32_t)(rb / nkb), k0 = (int32_t)(rb % nkb) * 16;
+        const int32_t k1 = k0 + 16 < d_in ? k0 + 16 : d_in;
+        double* dWr = dW + (size_t)r * d_in * d_out;
+        for (int64_t v = 0; v < n_dst; ++v) {
+            if (r < R && c[v * R + r] == 0) continue;
+            const double* a = (r < R) ? A + ((size_t)v * R + r) * d_in : h_src + (size_t)self_row[v] * d_in;
+            const double* g = dZ + (size_t)v * d_out;
+            for (int32_t k = k0; k < k1; ++k) {
+                const double ak = a[k];
+                for (int32_t n = 0; n < d_out; ++n) dWr[(size_t)k * d_out + n] += ak * g[n];
+            }
+        }
+    }
     for (int64_t v = 0; v < n_dst; ++v) {
         const double* g = dZ + (size_t)v * d_out;
         for (int32_t n = 0; n < d_out; ++n) db[n] += g[n];
-        for (int32_t r = 0; r <= R; ++r) {
-            if (r < R && c[v * R + r] == 0) continue;
-            const double* a = (r < R) ? A + ((size_t)v * R + r) * d_in : h_src + (size_t)self_row[v] * d_in;
-            double* dWr = dW + (size_t)r * d_in * d_out;
-            for (int32_t k = 0; k < d_in; ++k)
-                for (int32_t n = 0; n < d_out; ++n) dWr[(size_t)k * d_out + n] += a[k] * g[n];
-        }
         if (dh_src) {
             /* self term */
             const double* Ws = W + (size_t)R * d_in * d_out;

@@ -211,6 +211,18 @@ def synth_1b(scale: float = 1.0) -> Config:
         gen_seed=2406060220 + 5)
 
 
+def gcn_1b(scale: float = 1.0) -> Config:
+    """Table 3: homogeneous synthetic graph with 1B edges, average degree 100
+    (10M nodes), 64-d features, a GCN for node classification with 80 % training nodes (8M, as
+    the table's caption states).  GCN = the RGCN layer with one relation (R-gcn): mean over the
+    sampled in-neighbours + self loop.  Fanouts / batch / classes as configs[4]."""
+    n = int(10_000_000 * scale)
+    return Config(
+        name="gcn_1b" if scale == 1.0 else f"gcn_1b_x{scale:g}", ntypes=["node"], counts=[n],
+        etypes=[EType("edge", 0, 0, int(1_000_000_000 * scale))], feat_dim=64, fanouts=[10, 10], batch=1024,
+        hidden=128, num_classes=16, target_ntype=0, gen_seed=2406060220 + 6)
+
+
 def mag240m(scale: float = 1.0) -> Config:
     """configs[3]: MAG240M-shaped (OGB-LSC counts [EXT], SURVEY §8(d) cfg 4): paper 768-d bf16
     features with a trainable input projection 768 -> 128 (a6); author / institution are
@@ -250,7 +262,7 @@ def with_dtype(cfg: Config, feat_dtype: str) -> Config:
 
 CONFIGS = {"tiny": tiny, "mag": mag, "amazon_lp": amazon_lp, "tiny_lp": tiny_lp,
            "synth_1b": synth_1b, "mag240m": mag240m, "mag240m_1_16": lambda: mag240m(1.0 / 16),
-           "tiny_enc": tiny_enc}
+           "tiny_enc": tiny_enc, "gcn_1b": gcn_1b}
 
 
 def get(name: str) -> Config:

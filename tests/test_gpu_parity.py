@@ -408,3 +408,25 @@ def test_nc_step_splitk_batches(torch_cuda, name, batch):
         close(tr.hout[l][:nd].cpu().numpy(), res.hs[l], what=f"batch {batch} h{l}")
     close(tr.loss.cpu().numpy()[0], res.loss, what="loss")
     check_grads(tr, res, cfg, 1)
+
+
+def test_gcn_homogeneous_step_parity(torch_cuda):
+    """Table 3's workload (§8(f) f4): a homogeneous graph (one ntype, one relation,
+    average degree 100, 64-d features) and a GCN (the RGCN layer with R = 1, R-gcn), at 1/1000
+    of the 1B-edge size: blocks bit-exact, activations / loss / gradients within rtol."""
+    import torch
+    cfg = synth.gcn_1b(0.001)
+    assert cfg.num_ntypes == 1 and cfg.num_etypes == 1
+    st, og = gpu_store(cfg), oracle_graph(cfg)
+    tr = _gpu_trainer(cfg, st)
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    for step in (0, 1):
+        seeds = synth.nc_seeds(cfg, step)
+        tr.forward_backward(torch_cuda.from_numpy(seeds).cuda(), step)
+        res = oracle.nc_step(og, params, seeds, synth.labels(cfg), step, cfg.rng_seed)
+        _compare_blocks(cfg, st, tr.sampler, res.blocks)
+        for l in range(len(cfg.fanouts)):
+            nd = len(res.blocks[l].dst_gid)
+            close(tr.hout[l][:nd].cpu().numpy(), res.hs[l], what=f"gcn step {step} h{l}")
+        close(tr.loss.cpu().numpy()[0], res.loss, what="gcn loss")
+        check_grads(tr, res, cfg, step)

@@ -329,3 +329,23 @@ def test_encoder_frozen_rows_are_table_rows():
     X = synth.feature_rows(cfg, 0, [11]).astype(np.float64)
     assert X.shape == (1, cfg.dim_of(0))
     np.testing.assert_allclose(H0[2], (X @ params["Win0"])[0], rtol=1e-12, atol=1e-12)
+
+
+def test_oracle_threads_bit_identical():
+    """oracle_set_threads(n) parallelises the layer loops over dst rows / weight-gradient rows
+    without changing any summation order: a whole NC step is bit-identical for 1 and 4
+    threads (the all-core cpu_baseline times the same computation)."""
+    cfg = synth.scaled(synth.mag(), 0.005, "mag_tiny")
+    g = oracle.Graph(cfg)
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    seeds = synth.nc_seeds(cfg, 2)
+    res = []
+    for n in (1, 4):
+        oracle.set_threads(n)
+        res.append(oracle.nc_step(g, params, seeds, synth.labels(cfg), 2, cfg.rng_seed))
+    oracle.set_threads(1)
+    assert res[0].loss == res[1].loss
+    for k in res[0].grads:
+        assert np.array_equal(res[0].grads[k], res[1].grads[k]), k
+    for a, b in zip(res[0].hs, res[1].hs):
+        assert np.array_equal(a, b)
