@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--topology", default="partitioned", choices=["partitioned", "replicate"],
                     help="N>1 graph store: CSC partitioned by dst node ID, remote segments read over NVLink by "
                          "the sampling kernels (partitioned, default; §8(e)), or the whole CSC on every rank")
+    ap.add_argument("--sampling", default="peer", choices=["peer", "nccl"],
+                    help="partitioned topology: read remote CSC segments over NVLink inside the sampling kernels "
+                         "(peer), or send the frontier to its owners and the sampled edges back with NCCL "
+                         "all-to-alls (nccl: §8(e) C2/C3, owner-side sampling; implies --features alltoall, eager steps)")
     ap.add_argument("--features", default="peer", choices=["peer", "alltoall", "replicate"],
                     help="N>1 feature store: partitioned by node ID and read over NVLink inside the kernels "
                          "(peer, default), partitioned + NCCL all-to-all fetch (alltoall), or replicated")
@@ -255,7 +259,7 @@ def roofline_of(name, prof, sizes, cfg, pk, profile_steps):
 
 
 # ------------------------------------------------------------------------------ gsb arm
-def build_gsb(cfg, device, partition=None, mode="peer", topology="replicate"):
+def build_gsb(cfg, device, partition=None, mode="peer", topology="replicate", sampling="peer"):
     """partition = (world, rank) -> features partitioned by node ID: mode "peer" maps every
     rank's shard over NVLink (PeerFeatures), "alltoall" fetches rows with NCCL (FeatureExchange).
     topology "partitioned" (with a partition): every rank builds only the CSC of the dst nodes
@@ -284,7 +288,7 @@ def build_gsb(cfg, device, partition=None, mode="peer", topology="replicate"):
         del s, d
     if part_topo:
         from paper_2406_06022_b200.dist import PeerCSC
-        st._peer_csc = PeerCSC(st, partition[0], partition[1], pb)
+        st._peer_csc = PeerCSC(st, partition[0], partition[1], pb, map_peers=(sampling == "peer"))
     ex = None
     if partition is None:
         for t in range(cfg.num_ntypes):
@@ -331,6 +335,9 @@ def build_gsb(cfg, device, partition=None, mode="peer", topology="replicate"):
                 tr.set_embedding(t, E, peers=pe)
                 del E
     tr.exchange = ex
+    if part_topo and sampling == "nccl":
+        from paper_2406_06022_b200.dist import SampleExchange
+        tr._sx = SampleExchange(tr.sampler, partition[0], partition[1], first_hop=1)
     return st, tr
 
 
@@ -393,8 +400,11 @@ def run_gsb(args, cfg):
         dist.init_process_group("nccl", device_id=torch.device(device))
     from paper_2406_06022_b200 import _lib
     t0 = time.time()
+    if args.sampling == "nccl":
+        args.features = "alltoall"
     partitioned = dist is not None and args.features != "replicate"
-    st, tr = build_gsb(cfg, device, (ws, rank) if partitioned else None, args.features, args.topology)
+    st, tr = build_gsb(cfg, device, (ws, rank) if partitioned else None, args.features, args.topology,
+                       args.sampling)
     if partitioned and args.features == "peer" and args.peer_gather == "unique":
         tr.fuse_gather = False   # unique rows over NVLink once (peer loads bypass L2), then local aggregation
     setup_s = time.time() - t0
@@ -475,6 +485,8 @@ def run_gsb(args, cfg):
     launches0 = _lib.lib().gsb_launch_count()
     if tr.exchange is not None:
         tr.exchange.bytes_sent = 0
+    if getattr(tr, "_sx", None) is not None:
+        tr._sx.bytes_sent = 0
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -493,6 +505,8 @@ def run_gsb(args, cfg):
         dist.barrier()
     launches = _lib.lib().gsb_launch_count() - launches0
     nv_bytes = tr.exchange.bytes_sent / args.steps if tr.exchange is not None else 0
+    if getattr(tr, "_sx", None) is not None:
+        nv_bytes += tr._sx.bytes_sent / args.steps      # C2/C3 frontier exchange
     if use_graph:   # kernels inside a replayed graph are not re-counted by the library
         launches = launches_per_step_graph(tr, cfg) * args.steps
     ms = e0.elapsed_time(e1)
@@ -657,6 +671,9 @@ def run_gsb(args, cfg):
                sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])}
     topo = ("CSC partitioned by dst node ID, remote segments read over NVLink by the sampling kernels"
             if args.topology == "partitioned" and args.features != "replicate" else "topology replicated")
+    if args.sampling == "nccl" and args.topology == "partitioned":
+        topo = ("CSC partitioned by dst node ID, frontier sent to the owners and sampled edges returned by NCCL "
+                "all-to-alls (C2/C3, owner-side keyed sampling)")
     par = ("single" if ws == 1 else {
         "peer": f"dp{ws}: features partitioned by node ID, read over NVLink (CUDA IPC) by libgsb kernels "
                 f"({args.peer_gather} gather); {topo}; NCCL mean all-reduce of the grads after the CUDA graph",

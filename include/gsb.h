@@ -43,6 +43,7 @@ typedef int32_t gsb_status;
 #define GSB_EWORKSPACE 2  /* caller-provided buffer too small                         */
 #define GSB_ECUDA 3       /* a CUDA runtime call or kernel launch failed              */
 #define GSB_EDEVICE 4     /* a latched device-side error (see gsb_blocks_poll_error)  */
+#define GSB_ECALLBACK 5   /* a host callback (gsb_exchange_fn) reported failure         */
 
 /* feature element types */
 #define GSB_F32 0
@@ -147,9 +148,43 @@ typedef struct gsb_blocks* gsb_blocks_t;
 
 /* fanouts: host [num_layers], f[l] for layer l, each -1 or 1..GSB_MAX_FANOUT.
  * max_seeds: capacity of the seed frontier; max_excl: capacity of LP exclusion pairs. */
+/* Host callback of the NCCL frontier exchange (gsb_blocks_set_exchange).  phase 0: the library
+ * has bucketed this hop's frontier by owner (send_cnt, req_send); the callback runs the
+ * all-to-alls of the counts and of the request ids into req_recv (grouped by source rank) on
+ * `stream` and stores the received counts per rank in counts[0..world).  phase 1: the library
+ * has sampled the received requests (srv_cnt per (request, slot), srv_gid / srv_eid edges,
+ * srv_wcnt edges per requesting rank); the callback returns them with all-to-alls into
+ * resp_cnt (this rank's requests, in req_send order) and resp_gid / resp_eid.  Returns 0 on
+ * success. */
+typedef int32_t (*gsb_exchange_fn)(void* user, int32_t phase, int32_t hop, void* stream, int64_t* counts);
+
+/* Caller-owned device buffers of the exchange (sizes from gsb_exchange_sizes):
+ * int64 req_send[cap_dst], int32 req_perm[cap_dst], int64 send_cnt[world], cursor[world],
+ * int64 req_recv[cap_recv], int64 xoff[world+1], srv_meta[meta_bytes],
+ * int64 srv_cnt[srv_cnt_len], srv_seg[cap_recv*S+1], srv_gid / srv_eid[cap_srv_e],
+ * int64 srv_wcnt[world], resp_cnt / resp_seg[cap_dst*S+1], resp_gid / resp_eid[cap_resp_e]. */
+typedef struct {
+    int64_t* req_send; int32_t* req_perm; int64_t* send_cnt; int64_t* cursor;
+    int64_t* req_recv; int64_t cap_recv; int64_t* xoff; void* srv_meta;
+    int64_t* srv_cnt; int64_t* srv_seg; int64_t* srv_gid; int64_t* srv_eid; int64_t cap_srv_e; int64_t* srv_wcnt;
+    int64_t* resp_cnt; int64_t* resp_seg; int64_t* resp_gid; int64_t* resp_eid; int64_t cap_resp_e;
+} gsb_exchange_bufs;
+
 gsb_status gsb_blocks_create(gsb_graph_t g, int32_t num_layers, const int32_t* fanouts, int64_t max_seeds,
                              int64_t max_excl, gsb_blocks_t* out);
 gsb_status gsb_blocks_destroy(gsb_blocks_t b);
+/* NCCL frontier exchange (§8(e) C2/C3; P:L86 sampling on a distributed graph, P:L172 remote
+ * partition access): with first_hop > 0, hops >= first_hop of gsb_sample send every frontier
+ * node to its owner (bounds of gsb_graph_set_csc_peers: this rank's own CSC shard is the only
+ * one it reads), the owners sample the requests with the keyed RNG (requester's step word:
+ * this rank's + requester - rank) and reply with the counts and edges; the blocks are those of
+ * a whole-graph sampler, bit-exact.  fn runs the all-to-alls (see gsb_exchange_fn);
+ * gsb_sample then synchronizes the host twice per exchanged hop.  first_hop 0 turns it off. */
+gsb_status gsb_blocks_set_exchange(gsb_blocks_t b, int32_t world, int32_t rank, int32_t first_hop,
+                                   const gsb_exchange_bufs* bufs, gsb_exchange_fn fn, void* user);
+gsb_status gsb_exchange_sizes(gsb_blocks_t b, int32_t world, int64_t* cap_dst, int64_t* cap_recv,
+                              int64_t* cap_srv_e, int64_t* cap_resp_e, int64_t* srv_cnt_len, int64_t* meta_bytes);
+
 /* Device arena bytes for all blocks of one mini-batch (upper bounds). */
 gsb_status gsb_blocks_arena_bytes(gsb_blocks_t b, size_t* bytes);
 /* One-time arena initialisation (node maps to "absent").  Must precede the first sample. */
@@ -486,11 +521,13 @@ gsb_status gsb_ipc_close(void* base_ptr);
  * process's own, or IPC-mapped peers' from gsb_ipc_open) and eid_base_w[w] their n_before.
  * After registration the sampler reads each dst's segment from its owner's HBM (keyed draws:
  * blocks identical to a whole-graph sampler, bit-exact).  table_dev: caller-owned device
- * memory of gsb_csc_peers_bytes() bytes, the same for every etype of g.  Syncs stream. */
+ * memory of gsb_csc_peers_bytes() bytes, the same for every etype of g.  n_edges_total: the
+ * etype's edge count over all shards (sizes the sampler's capacities).  Syncs stream. */
 gsb_status gsb_csc_peers_bytes(size_t* bytes);
 gsb_status gsb_graph_set_csc_peers(gsb_graph_t g, void* table_dev, int32_t etype, int32_t world,
                                    const int64_t* bounds, const int64_t* const* indptr_w,
-                                   const int32_t* const* indices_w, const int64_t* eid_base_w, void* stream);
+                                   const int32_t* const* indices_w, const int64_t* eid_base_w, int64_t n_edges_total,
+                                   void* stream);
 
 gsb_status gsb_graph_set_feature_peers(gsb_graph_t g, int32_t ntype, int32_t world, const int64_t* bounds,
                                        const void* const* ptrs, int32_t dim, int32_t dtype);

@@ -26,6 +26,16 @@ class gsb_sample_args(C.Structure):
                 ("excl_rev_etype", i32)]
 
 
+class gsb_exchange_bufs(C.Structure):
+    _fields_ = [("req_send", P), ("req_perm", P), ("send_cnt", P), ("cursor", P), ("req_recv", P), ("cap_recv", i64),
+                ("xoff", P), ("srv_meta", P), ("srv_cnt", P), ("srv_seg", P), ("srv_gid", P), ("srv_eid", P),
+                ("cap_srv_e", i64), ("srv_wcnt", P), ("resp_cnt", P), ("resp_seg", P), ("resp_gid", P),
+                ("resp_eid", P), ("cap_resp_e", i64)]
+
+
+# gsb_exchange_fn(user, phase, hop, stream, counts)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_int64))
+
 # name -> argtypes (all return gsb_status = int32 unless listed in _RET)
 SIGS = {
     "gsb_last_error": [],
@@ -40,7 +50,7 @@ SIGS = {
     "gsb_graph_set_csc": [P, i32, P, P, i64, i64],
     "gsb_csc_build_range": [P, i32, P, P, P, i64, i64, i64, P, P, C.POINTER(i64), C.POINTER(i64), P, sz, P],
     "gsb_csc_peers_bytes": [C.POINTER(sz)],
-    "gsb_graph_set_csc_peers": [P, P, i32, i32, P, P, P, P, P],
+    "gsb_graph_set_csc_peers": [P, P, i32, i32, P, P, P, P, i64, P],
     "gsb_graph_set_features": [P, i32, P, i32, i32],
     "gsb_gather": [P, P, i64, P, P],
     "gsb_blocks_create": [P, i32, P, i64, i64, C.POINTER(P)],
@@ -76,6 +86,9 @@ SIGS = {
     "gsb_graph_set_feature_peers": [P, i32, i32, P, P, i32, i32],
     "gsb_gemm": [i32, P, i64, P, i64, i64, i32, i32, P, i64, P],
     "gsb_gemm_trace": [P, i32],
+    "gsb_blocks_set_exchange": [P, i32, i32, i32, C.POINTER(gsb_exchange_bufs), EXCHANGE_FN, P],
+    "gsb_exchange_sizes": [P, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64),
+                           C.POINTER(i64)],
     "gsb_nc_loss": [P, i64, i32, P, P, i32, P, P, i64, P, P, P, P, P, P, P],
     "gsb_adam_step": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P],
     "gsb_counter_add": [P, i32, P],

@@ -57,8 +57,18 @@ static cudaEvent_t get_event() {
 // Every launch sits in an NVTX range named after the kernel's role (rgcn_agg_l0,
 // sample_fill, ...): ncu --nvtx --print-nvtx-rename kernel reports launches by these names.
 // Without an attached tool the NVTX calls are no-ops.
+// GSB_DEBUG_SYNC=1 (tools): synchronize after every eager launch and report the failing
+// kernel by name (device faults otherwise surface at a later, unrelated call)
+static thread_local const char* t_last_launch = nullptr;
+static bool debug_sync() {
+    static int on = -1;
+    if (on < 0) on = getenv("GSB_DEBUG_SYNC") ? 1 : 0;
+    return on == 1;
+}
+
 void prof_begin(const char* name, cudaStream_t s) {
     nvtxRangePushA(name);
+    t_last_launch = name;
     if (!g_prof_on) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_pending_name = name;
@@ -68,6 +78,15 @@ void prof_begin(const char* name, cudaStream_t s) {
 
 void prof_end(cudaStream_t s) {
     nvtxRangePop();
+    if (debug_sync()) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cs);
+        if (cs == cudaStreamCaptureStatusNone) {
+            const cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess)
+                fprintf(stderr, "[gsb] kernel %s failed: %s\n", t_last_launch ? t_last_launch : "?", cudaGetErrorString(e));
+        }
+    }
     if (!g_prof_on || !g_pending_name) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEvent_t b = get_event();

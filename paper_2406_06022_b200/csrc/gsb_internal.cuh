@@ -227,8 +227,36 @@ struct Graph {
     int64_t total_nodes;
 };
 
+// NCCL exchange of the sampling frontier (§8(e) C2/C3; gsb_blocks_set_exchange): caller-owned
+// device buffers; all zero = off.
+struct Xchg {
+    int32_t world, rank, first_hop;                 // first_hop 0: exchange off
+    int64_t* req_send;   // [cap_dst] frontier gids grouped by owner
+    int32_t* req_perm;   // [cap_dst] position of frontier row j in req_send
+    int64_t* send_cnt;   // [world] requests per owner (device; read by the callback)
+    int64_t* cursor;     // [world]
+    int64_t* req_recv;   // [cap_recv] requests received, grouped by requesting rank
+    int64_t cap_recv;
+    int64_t* xoff;       // [world+1] prefix of the received request counts (device)
+    HopMeta* srv_meta;   // n_dst = received requests
+    int64_t* srv_cnt;    // [cap_recv*S + 1 + kCntMaxBlocks] per (request, slot) counts
+    int64_t* srv_seg;    // [cap_recv*S + 1]
+    int64_t* srv_gid;    // [cap_srv_e] sampled edges of the served requests
+    int64_t* srv_eid;
+    int64_t cap_srv_e;
+    int64_t* srv_wcnt;   // [world] edges to return to each requesting rank (device)
+    int64_t* resp_cnt;   // [cap_dst*S + 1] counts of this rank's requests, in req_send order
+    int64_t* resp_seg;   // [cap_dst*S + 1]
+    int64_t* resp_gid;   // [cap_resp_e] returned edges, grouped by owner in req_send order
+    int64_t* resp_eid;
+    int64_t cap_resp_e;
+    gsb_exchange_fn fn;
+    void* user;
+};
+
 struct Blocks {
     Graph* g;
+    Xchg x;
     int32_t L;
     int32_t fanout[kMaxL];     // f[l] for layer l
     int64_t max_seeds, max_excl;

@@ -89,7 +89,8 @@ gsb_status gsb_csc_peers_bytes(size_t* bytes) {
 
 gsb_status gsb_graph_set_csc_peers(gsb_graph_t g, void* table_dev, int32_t etype, int32_t world,
                                    const int64_t* bounds, const int64_t* const* indptr_w,
-                                   const int32_t* const* indices_w, const int64_t* eid_base_w, void* stream) {
+                                   const int32_t* const* indices_w, const int64_t* eid_base_w, int64_t n_edges_total,
+                                   void* stream) {
     Graph* G = reinterpret_cast<Graph*>(g);
     GSB_CHECK_ARG(G && table_dev && bounds && indptr_w && indices_w && eid_base_w, "null argument");
     GSB_CHECK_ARG(etype >= 0 && etype < G->dev.R, "etype %d out of range", etype);
@@ -113,6 +114,9 @@ gsb_status gsb_graph_set_csc_peers(gsb_graph_t g, void* table_dev, int32_t etype
         P.indices[etype][w] = indices_w[w];
         P.eid_base[etype][w] = eid_base_w[w];
     }
+    GSB_CHECK_ARG(n_edges_total >= 0, "bad n_edges_total");
+    // capacities (fanout ALL, full-graph sweeps) are sized by the whole graph's edge count
+    G->n_edges[etype] = n_edges_total;
     cudaStream_t s = (cudaStream_t)stream;
     GSB_CUDA(cudaMemcpyAsync(table_dev, &P, sizeof(CscPeers), cudaMemcpyHostToDevice, s));
     GSB_CUDA(cudaStreamSynchronize(s));

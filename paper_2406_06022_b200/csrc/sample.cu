@@ -265,7 +265,7 @@ __device__ __forceinline__ int64_t count_one(const GraphDev& g, int64_t i, int64
     if (j >= n) return 0;
     const int64_t v = dst_gid[j];
     const int t = type_of(g, v);
-    if (s == 0) {
+    if (s == 0 && map) {      // map == null: serving another rank's requests (no relabel here)
         int32_t old = atomicExch(map + v, (int32_t)j);
         if (old != -1) atomicExch(err, ERR_DUPLICATE);
     }
@@ -389,14 +389,15 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
                                                    uint64_t seed, uint32_t step_host, const uint32_t* step_dev, int hop,
                                                    const int32_t* __restrict__ map, uint32_t* __restrict__ bitmap,
                                                    int64_t* __restrict__ e_src_gid, int64_t* __restrict__ e_eid,
-                                                   const int* __restrict__ err, int64_t cap) {
+                                                   const int* __restrict__ err, int64_t cap,
+                                                   const int64_t* __restrict__ xoff, int xworld, int xrank) {
     GSB_PDL_ENTRY();
     const int S = g.S;
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);                       // lane inside the group
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const int64_t n = (*(volatile const int*)err) ? 0 : m->n_dst;
-    const uint32_t step = step_dev ? *step_dev : step_host;
+    const uint32_t step0 = step_dev ? *step_dev : step_host;
     const int64_t nseg = n * S;
     const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / G;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; i < nseg; i += groups) {
@@ -405,6 +406,14 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
         if (c == 0) continue;
         const int64_t j = i / S;
         const int s = (int)(i - j * S);
+        // serving requests (xoff): row j came from rank w, whose step word is this rank's
+        // shifted by w - xrank (ranks step in lockstep, word = step * world + rank)
+        uint32_t step = step0;
+        if (xoff) {
+            int w = 0;
+            for (int k = 1; k < xworld; ++k) w += (j >= xoff[k]) ? 1 : 0;
+            step = step0 + (uint32_t)(w - xrank);
+        }
         const int64_t v = dst_gid[j];
         const int t = type_of(g, v);
         const int r = g.slot_etype[t][s];
@@ -425,7 +434,7 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
                 int64_t u = src_off + seg[p];
                 e_src_gid[base + q] = u;
                 e_eid[base + q] = cs.eid0 + p;
-                if (map[u] < 0) {
+                if (map && map[u] < 0) {
                     uint32_t bit = 1u << (u & 31);
                     if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);
                 }
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
             int64_t u = src_off + seg[p];
             e_src_gid[base + gl] = u;
             e_eid[base + gl] = cs.eid0 + p;
-            if (map[u] < 0) {
+            if (map && map[u] < 0) {
                 uint32_t bit = 1u << (u & 31);
                 if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);
             }
@@ -529,6 +538,145 @@ __global__ void __launch_bounds__(256) fill_tail_kernel(GraphDev g, const HopMet
                 }
             }
             if (i == ib) break;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// NCCL frontier exchange (§8(e) C2/C3, gsb_blocks_set_exchange): requester side buckets the
+// hop's frontier by owner (K11); the owner runs count / scan / fill on the requests it
+// received (keyed draws with the requester's step word: the same blocks as a whole-graph
+// sampler); the requester unpacks the returned counts and edges into frontier order.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int x_owner(const GraphDev& g, int64_t v) {
+    const CscPeers& P = *g.cpeers;
+    const int t = type_of(g, v);
+    const int64_t vl = v - g.node_off[t];
+    int w = 0;
+    for (int k = 1; k < P.world; ++k) w += (vl >= P.lo[t][k]) ? 1 : 0;
+    return w;
+}
+
+// per-owner request counts, one shared atomic per (warp, owner)
+__global__ void x_owner_count_kernel(GraphDev g, const HopMeta* __restrict__ m, const int64_t* __restrict__ dst_gid,
+                                     int world, unsigned long long* __restrict__ cnt) {
+    GSB_PDL_ENTRY();
+    __shared__ unsigned long long sc[kMaxPeers];
+    if (threadIdx.x < kMaxPeers) sc[threadIdx.x] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t n = m->n_dst;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = b + threadIdx.x;
+        const int w = i < n ? x_owner(g, dst_gid[i]) : -1;
+        for (int o = 0; o < world; ++o) {
+            const unsigned bal = __ballot_sync(0xffffffffu, w == o);
+            if (lane == 0 && bal) atomicAdd(&sc[o], (unsigned long long)__popc(bal));
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < world && sc[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], sc[threadIdx.x]);
+}
+
+__global__ void x_scatter_kernel(GraphDev g, const HopMeta* __restrict__ m, const int64_t* __restrict__ dst_gid,
+                                 int world, const unsigned long long* __restrict__ cnt,
+                                 unsigned long long* __restrict__ cursor, int64_t* __restrict__ req_send,
+                                 int32_t* __restrict__ perm) {
+    GSB_PDL_ENTRY();
+    __shared__ unsigned long long base[kMaxPeers];
+    if (threadIdx.x == 0) {
+        unsigned long long a = 0;
+        for (int w = 0; w < world; ++w) {
+            base[w] = a;
+            a += cnt[w];
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t n = m->n_dst;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = b + threadIdx.x;
+        int64_t v = 0;
+        int w = -1;
+        if (i < n) {
+            v = dst_gid[i];
+            w = x_owner(g, v);
+        }
+        for (int o = 0; o < world; ++o) {
+            const unsigned bal = __ballot_sync(0xffffffffu, w == o);
+            if (!bal) continue;
+            const int leader = __ffs(bal) - 1;
+            unsigned long long start = 0;
+            if (lane == leader) start = atomicAdd(&cursor[o], (unsigned long long)__popc(bal));
+            start = __shfl_sync(0xffffffffu, start, leader);
+            if (w == o) {
+                const int64_t pos = (int64_t)(base[o] + start + __popc(bal & lt));
+                req_send[pos] = v;
+                perm[i] = (int32_t)pos;
+            }
+        }
+    }
+}
+
+// edges to return to each requesting rank: its requests are rows [xoff[w], xoff[w+1])
+__global__ void x_wcnt_kernel(const int64_t* __restrict__ srv_seg, const int64_t* __restrict__ xoff, int world, int S,
+                              int64_t* __restrict__ wcnt) {
+    GSB_PDL_ENTRY();
+    const int w = threadIdx.x;
+    if (w < world) wcnt[w] = srv_seg[xoff[w + 1] * S] - srv_seg[xoff[w] * S];
+}
+
+// requester: per (frontier row, slot) counts from the owners' replies; dst map for relabel;
+// entries past the live rows are zero (the scan runs over the capacity)
+__global__ void x_unpack_count_kernel(const HopMeta* __restrict__ m, const int64_t* __restrict__ dst_gid,
+                                      const int32_t* __restrict__ perm, const int64_t* __restrict__ resp_cnt, int S,
+                                      int64_t cap_entries, int32_t* __restrict__ map, int64_t* __restrict__ cnt,
+                                      int* __restrict__ err) {
+    GSB_PDL_ENTRY();
+    const int64_t n = (*(volatile const int*)err) ? 0 : m->n_dst;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= cap_entries;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = i / S;
+        const int s = (int)(i - j * S);
+        if (j >= n) {
+            cnt[i] = 0;
+            continue;
+        }
+        cnt[i] = resp_cnt[(int64_t)perm[j] * S + s];
+        if (s == 0) {
+            const int32_t old = atomicExch(map + dst_gid[j], (int32_t)j);
+            if (old != -1) atomicExch(err, ERR_DUPLICATE);
+        }
+    }
+}
+
+// requester: copy every segment's returned edges into frontier order, mark new sources
+__global__ void x_unpack_fill_kernel(const HopMeta* __restrict__ m, const int32_t* __restrict__ perm, int S,
+                                     const int64_t* __restrict__ seg_ptr, const int64_t* __restrict__ resp_seg,
+                                     const int64_t* __restrict__ resp_gid, const int64_t* __restrict__ resp_eid,
+                                     const int32_t* __restrict__ map, uint32_t* __restrict__ bitmap,
+                                     int64_t* __restrict__ e_src_gid, int64_t* __restrict__ e_eid,
+                                     const int* __restrict__ err) {
+    GSB_PDL_ENTRY();
+    const int64_t n = (*(volatile const int*)err) ? 0 : m->n_dst;
+    const int64_t nseg = n * S;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < nseg; i += warps) {
+        const int64_t d0 = seg_ptr[i], c = seg_ptr[i + 1] - d0;
+        if (c == 0) continue;
+        const int64_t j = i / S;
+        const int s = (int)(i - j * S);
+        const int64_t r0 = resp_seg[(int64_t)perm[j] * S + s];
+        for (int64_t q = lane; q < c; q += 32) {
+            const int64_t u = resp_gid[r0 + q];
+            e_src_gid[d0 + q] = u;
+            e_eid[d0 + q] = resp_eid[r0 + q];
+            if (map[u] < 0) {
+                const uint32_t bit = 1u << (u & 31);
+                if (!(bitmap[u >> 5] & bit)) atomicOr(bitmap + (u >> 5), bit);
+            }
         }
     }
 }
@@ -768,6 +916,88 @@ HopBufs Blocks::hop(int h, void* arena) const {
     return b;
 }
 
+// One hop of the NCCL exchange mode (see the kernels above): bucket -> callback phase 0
+// (request all-to-all) -> owner-side count / scan / fill of the received requests -> callback
+// phase 1 (reply all-to-alls) -> unpack into this rank's hop buffers.  Host-synchronous at
+// the two callbacks (the exchange sizes are read on the host); not CUDA-graph capturable.
+static gsb_status exchange_hop(Blocks* B, const gsb_sample_args* a, const HopBufs& hb, int h, int f, int S,
+                               uint64_t rng_seed, int32_t* map, uint32_t* bitmap, int* err, void* cub_tmp,
+                               cudaStream_t s) {
+    const GraphDev& g = B->g->dev;
+    Xchg& x = B->x;
+    GSB_CHECK_ARG(f >= 1 && f <= GSB_MAX_FANOUT, "exchange mode needs a fanout in [1, %d]", GSB_MAX_FANOUT);
+    GSB_CHECK_ARG(g.cpeers, "exchange mode needs the partition bounds (gsb_graph_set_csc_peers)");
+    const Excl ex0{nullptr, 0, -1, -2, nullptr, nullptr};
+    // (1) bucket the frontier by owner
+    GSB_CUDA(cudaMemsetAsync(x.send_cnt, 0, sizeof(int64_t) * x.world, s));
+    GSB_CUDA(cudaMemsetAsync(x.cursor, 0, sizeof(int64_t) * x.world, s));
+    const int gb = grid_for(hb.cap_dst, 256, kNumSMs * 4);
+    GSB_LAUNCH("x_bucket", x_owner_count_kernel, gb, 256, 0, s, g, hb.meta, hb.dst_gid, x.world,
+               reinterpret_cast<unsigned long long*>(x.send_cnt));
+    GSB_LAUNCH("x_scatter", x_scatter_kernel, gb, 256, 0, s, g, hb.meta, hb.dst_gid, x.world,
+               reinterpret_cast<const unsigned long long*>(x.send_cnt), reinterpret_cast<unsigned long long*>(x.cursor),
+               x.req_send, x.req_perm);
+    // (2) C2: requests to their owners
+    int64_t cnt[kMaxPeers + 1] = {0};
+    if (x.fn(x.user, 0, h, (void*)s, cnt) != 0) {
+        set_error("exchange callback failed (phase 0, hop %d)", h);
+        return GSB_ECALLBACK;
+    }
+    int64_t off[kMaxPeers + 1];
+    off[0] = 0;
+    for (int w = 0; w < x.world; ++w) off[w + 1] = off[w] + cnt[w];
+    const int64_t n_recv = off[x.world];
+    GSB_CHECK_ARG(n_recv <= x.cap_recv, "received %lld requests > capacity %lld", (long long)n_recv,
+                  (long long)x.cap_recv);
+    HopMeta hm;
+    memset(&hm, 0, sizeof(hm));
+    hm.n_dst = n_recv;
+    GSB_CUDA(cudaMemcpyAsync(x.srv_meta, &hm, sizeof(HopMeta), cudaMemcpyHostToDevice, s));
+    GSB_CUDA(cudaMemcpyAsync(x.xoff, off, sizeof(int64_t) * (x.world + 1), cudaMemcpyHostToDevice, s));
+    // (3) serve: count / scan / fill over the received requests (no relabel state touched)
+    const int64_t sseg = n_recv * S;
+    {
+        const int64_t chunk = ceil_div(ceil_div(sseg + 1, kCntThreads), kCntMaxBlocks) * kCntThreads;
+        const int nb = (int)ceil_div(sseg + 1, chunk);
+        const int nbs = (int)ceil_div(sseg + 1, chunk * kScanPerBlock);
+        int64_t* btot = x.srv_cnt + sseg + 1;
+        GSB_LAUNCH("x_serve_count", count_kernel, nb, kCntThreads, 0, s, g, x.srv_meta, x.req_recv, n_recv, f, ex0,
+                   (int32_t*)nullptr, x.srv_cnt, chunk, btot, err);
+        GSB_LAUNCH("x_serve_scan", count_scan_kernel, nbs, kCntThreads, 0, s, x.srv_cnt, sseg + 1,
+                   chunk * kScanPerBlock, btot, nb, x.srv_seg);
+        const int G = f <= 8 ? 8 : (f <= 16 ? 16 : 32);
+        const int grid = grid_for(std::max<int64_t>(sseg, 1) * G, 256, kNumSMs * GSB_FILL_BPS);
+#define GSB_XFILL(GG)                                                                                            \
+    GSB_LAUNCH("x_serve_fill", fill_kernel<GG>, grid, 256, 0, s, g, x.srv_meta, x.req_recv, n_recv, x.srv_seg, f,   \
+               ex0, rng_seed, a->step, a->step_dev, h, (const int32_t*)nullptr, (uint32_t*)nullptr, x.srv_gid,     \
+               x.srv_eid, err, INT64_MAX, (const int64_t*)x.xoff, x.world, x.rank)
+        if (G == 8) GSB_XFILL(8);
+        else if (G == 16) GSB_XFILL(16);
+        else GSB_XFILL(32);
+#undef GSB_XFILL
+        GSB_LAUNCH("x_wcnt", x_wcnt_kernel, 1, 32, 0, s, x.srv_seg, x.xoff, x.world, S, x.srv_wcnt);
+    }
+    // (4) C3: replies back to the requesters
+    GSB_CUDA(cudaMemsetAsync(x.resp_cnt, 0, sizeof(int64_t) * (size_t)(hb.cap_dst * S + 1), s));
+    if (x.fn(x.user, 1, h, (void*)s, cnt) != 0) {
+        set_error("exchange callback failed (phase 1, hop %d)", h);
+        return GSB_ECALLBACK;
+    }
+    // (5) unpack into frontier order: counts -> seg_ptr; reply offsets; edges
+    const int64_t nseg = hb.cap_dst * S;
+    GSB_LAUNCH("x_unpack_count", x_unpack_count_kernel, grid_for(nseg + 1, 256, kNumSMs * 8), 256, 0, s, hb.meta,
+               hb.dst_gid, x.req_perm, x.resp_cnt, S, nseg, map, hb.cnt, err);
+    size_t cb = B->cub_bytes;
+    GSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, hb.cnt, hb.seg_ptr, (int64_t)(nseg + 1), s));
+    cb = B->cub_bytes;
+    GSB_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, cb, x.resp_cnt, x.resp_seg, (int64_t)(nseg + 1), s));
+    count_launch(4);
+    GSB_LAUNCH("x_unpack_fill", x_unpack_fill_kernel, grid_for(nseg * 32, 256, kNumSMs * 8), 256, 0, s, hb.meta,
+               x.req_perm, S, hb.seg_ptr, x.resp_seg, x.resp_gid, x.resp_eid, map, bitmap, hb.e_src_gid, hb.e_eid,
+               err);
+    return GSB_OK;
+}
+
 }  // namespace gsb
 
 using namespace gsb;
@@ -943,6 +1173,10 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
         HopBufs hb = B->hop(h, arena);
         const int f = B->fanout[B->L - h];
         const int64_t nseg = hb.cap_dst * S;
+        if (B->x.first_hop > 0 && h >= B->x.first_hop) {
+            gsb_status st = exchange_hop(B, a, hb, h, f, S, rng_seed, map, bitmap, err, cub_tmp, s);
+            if (st != GSB_OK) return st;
+        } else {
         {
             // count chunks: whole multiples of kCntThreads entries, at most kCntMaxBlocks of them;
             // scan chunks: kScanPerBlock count chunks (whole kCntTile tiles, 16-B aligned)
@@ -964,18 +1198,19 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
             if (G == 8)
                 GSB_LAUNCH("sample_fill", fill_kernel<8>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
                            hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
-                           err, cap);
+                           err, cap, (const int64_t*)nullptr, 1, 0);
             else if (G == 16)
                 GSB_LAUNCH("sample_fill", fill_kernel<16>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
                            hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
-                           err, cap);
+                           err, cap, (const int64_t*)nullptr, 1, 0);
             else
                 GSB_LAUNCH("sample_fill", fill_kernel<32>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
                            hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
-                           err, cap);
+                           err, cap, (const int64_t*)nullptr, 1, 0);
             if (tail)
                 GSB_LAUNCH("sample_fill_tail", fill_tail_kernel, kNumSMs * 8, 256, 0, s, g, hb.meta, hb.dst_gid,
                            hb.seg_ptr, ex, map, bitmap, hb.e_src_gid, hb.e_eid, err);
+        }
         }
         {
             const int64_t chunk = ceil_div(ceil_div(B->n_words + 1, kRankTile), kRankMaxBlocks) * kRankTile;
@@ -1028,6 +1263,62 @@ gsb_status gsb_block_view_get(gsb_blocks_t b, const void* arena, int32_t layer, 
     out->e_eid = hb.e_eid;
     out->e_src = hb.e_src;
     out->num_slots = B->g->dev.S > 0 ? B->g->dev.S : 1;
+    return GSB_OK;
+}
+
+gsb_status gsb_blocks_set_exchange(gsb_blocks_t b, int32_t world, int32_t rank, int32_t first_hop,
+                                   const gsb_exchange_bufs* bufs, gsb_exchange_fn fn, void* user) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && (first_hop == 0 || (bufs && fn)), "null argument");
+    GSB_CHECK_ARG(world >= 1 && world <= kMaxPeers && rank >= 0 && rank < world, "bad world / rank");
+    GSB_CHECK_ARG(first_hop >= 0 && first_hop <= B->L, "first_hop %d out of [0, %d]", first_hop, B->L);
+    memset(&B->x, 0, sizeof(Xchg));
+    if (first_hop == 0) return GSB_OK;
+    B->x.world = world;
+    B->x.rank = rank;
+    B->x.first_hop = first_hop;
+    B->x.req_send = bufs->req_send;
+    B->x.req_perm = bufs->req_perm;
+    B->x.send_cnt = bufs->send_cnt;
+    B->x.cursor = bufs->cursor;
+    B->x.req_recv = bufs->req_recv;
+    B->x.cap_recv = bufs->cap_recv;
+    B->x.xoff = bufs->xoff;
+    B->x.srv_meta = reinterpret_cast<HopMeta*>(bufs->srv_meta);
+    B->x.srv_cnt = bufs->srv_cnt;
+    B->x.srv_seg = bufs->srv_seg;
+    B->x.srv_gid = bufs->srv_gid;
+    B->x.srv_eid = bufs->srv_eid;
+    B->x.cap_srv_e = bufs->cap_srv_e;
+    B->x.srv_wcnt = bufs->srv_wcnt;
+    B->x.resp_cnt = bufs->resp_cnt;
+    B->x.resp_seg = bufs->resp_seg;
+    B->x.resp_gid = bufs->resp_gid;
+    B->x.resp_eid = bufs->resp_eid;
+    B->x.cap_resp_e = bufs->cap_resp_e;
+    B->x.fn = fn;
+    B->x.user = user;
+    return GSB_OK;
+}
+
+gsb_status gsb_exchange_sizes(gsb_blocks_t b, int32_t world, int64_t* cap_dst, int64_t* cap_recv,
+                              int64_t* cap_srv_e, int64_t* cap_resp_e, int64_t* srv_cnt_len, int64_t* meta_bytes) {
+    Blocks* B = reinterpret_cast<Blocks*>(b);
+    GSB_CHECK_ARG(B && cap_dst && cap_recv && cap_srv_e && cap_resp_e && srv_cnt_len && meta_bytes, "null argument");
+    GSB_CHECK_ARG(world >= 1 && world <= kMaxPeers, "bad world");
+    const int S = B->g->dev.S > 0 ? B->g->dev.S : 1;
+    int64_t cd = 0, ce = 0, fmax = 1;
+    for (int h = 1; h <= B->L; ++h) {
+        cd = std::max(cd, B->cap_dst[h]);
+        ce = std::max(ce, B->cap_edges[h]);
+        fmax = std::max<int64_t>(fmax, B->fanout[B->L - h]);
+    }
+    *cap_dst = cd;
+    *cap_recv = cd * world;                 // every rank may ask this one for its whole frontier
+    *cap_srv_e = cd * world * S * fmax;
+    *cap_resp_e = ce;
+    *srv_cnt_len = cd * world * S + 1 + kCntMaxBlocks;
+    *meta_bytes = sizeof(HopMeta);
     return GSB_OK;
 }
 

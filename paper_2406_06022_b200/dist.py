@@ -159,12 +159,34 @@ class PeerCSC:
     kernels read each dst's in-edge segment from its owner's HBM.  Keyed draws make the blocks
     identical to the whole-graph sampler's (bit-exact), with no collective on the data path."""
 
-    def __init__(self, store, world: int, rank: int, bounds, group=None):
+    def __init__(self, store, world: int, rank: int, bounds, group=None, map_peers: bool = True):
+        """map_peers=False: register the partition bounds and this rank's own shard only (the
+        NCCL exchange mode, SampleExchange, never reads another rank's CSC)."""
         import ctypes as C
         import numpy as np
         import torch.distributed as dist
         from ._lib import call
         self.bounds = np.ascontiguousarray(bounds, dtype=np.int64)        # [T][world+1]
+        if not map_peers:
+            nb = C.c_size_t()
+            call("gsb_csc_peers_bytes", C.byref(nb))
+            self.table = torch.zeros(int(nb.value), dtype=torch.uint8, device=store.device)
+            self.mapped = []
+            s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+            for r in range(store.R):
+                ip = (C.c_void_p * world)()
+                ix = (C.c_void_p * world)()
+                eb = (C.c_int64 * world)()
+                for w in range(world):      # other ranks' entries: never dereferenced
+                    ip[w] = store.indptr[r].data_ptr()
+                    ix[w] = store.indices[r].data_ptr()
+                    eb[w] = int(store.eid_base[r])
+                tot = torch.tensor([store.n_edges[r]], dtype=torch.int64, device=store.device)
+                dist.all_reduce(tot, group=group)
+                call("gsb_graph_set_csc_peers", store.h, C.c_void_p(self.table.data_ptr()), r, world,
+                     self.bounds.ctypes.data_as(C.c_void_p), ip, ix, eb, int(tot.item()), s)
+            store._csc_peers = self
+            return
         mine = []
         for r in range(store.R):
             hs = []
@@ -173,7 +195,7 @@ class PeerCSC:
                 off = C.c_int64()
                 call("gsb_ipc_handle", C.c_void_p(t.data_ptr()), h, C.byref(off))
                 hs.append((bytes(h), int(off.value)))
-            mine.append((hs, int(store.eid_base[r])))
+            mine.append((hs, int(store.eid_base[r]), int(store.n_edges[r])))
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         nb = C.c_size_t()
@@ -187,7 +209,7 @@ class PeerCSC:
             ix = (C.c_void_p * world)()
             eb = (C.c_int64 * world)()
             for w in range(world):
-                (hip, hix), base = allh[w][r]
+                (hip, hix), base, _ = allh[w][r]
                 eb[w] = base
                 if w == rank:
                     ip[w] = store.indptr[r].data_ptr()
@@ -199,8 +221,88 @@ class PeerCSC:
                     arr[w] = p.value
                     self.mapped.append(p.value - off)
             call("gsb_graph_set_csc_peers", store.h, C.c_void_p(self.table.data_ptr()), r, world,
-                 self.bounds.ctypes.data_as(C.c_void_p), ip, ix, eb, s)
+                 self.bounds.ctypes.data_as(C.c_void_p), ip, ix, eb, sum(allh[w][r][2] for w in range(world)), s)
         store._csc_peers = self
+
+
+class SampleExchange:
+    """NCCL frontier exchange of the partitioned graph (§8(e) C2/C3 as north_star states it;
+    P:L86): every rank holds only the CSC of the dst nodes it owns
+    (GraphStore.load_etype_range + partition bounds registered through PeerCSC(..., map=False))
+    and never reads another rank's storage.  For every hop >= first_hop, gsb_sample
+    buckets the frontier by owner, this object's callback all-to-alls the requests (C2), the
+    owners sample them with the keyed RNG, and the callback all-to-alls the per-(request, slot)
+    counts and the sampled (src gid, eid) edges back (C3); gsb_sample unpacks them into frontier
+    order.  Exact-size all-to-alls: the sizes are read on the host (two syncs per hop), so the
+    sample phase runs eagerly (no CUDA graph) in this mode.  Buffers are torch tensors sized by
+    gsb_exchange_sizes (worst-case capacities, no device allocation in the library)."""
+
+    def __init__(self, sampler, world: int, rank: int, first_hop: int = 1, group=None):
+        import ctypes as C
+        from . import _lib
+        from ._lib import call
+        self.world, self.rank, self.group = world, rank, group
+        self.S = max(len(x) for x in sampler.store.slot_etypes())
+        vals = [C.c_int64() for _ in range(6)]
+        call("gsb_exchange_sizes", sampler.h, world, *[C.byref(v) for v in vals])
+        cap_dst, cap_recv, cap_srv_e, cap_resp_e, srv_cnt_len, meta_b = [int(v.value) for v in vals]
+        dev = sampler.arena.device
+        I64 = lambda n: torch.zeros(max(int(n), 1), dtype=torch.int64, device=dev)
+        S = self.S
+        self.req_send, self.req_perm = I64(cap_dst), torch.zeros(cap_dst, dtype=torch.int32, device=dev)
+        self.send_cnt, self.cursor = I64(world), I64(world)
+        self.req_recv, self.xoff = I64(cap_recv), I64(world + 1)
+        self.srv_meta = torch.zeros(meta_b, dtype=torch.uint8, device=dev)
+        self.srv_cnt, self.srv_seg = I64(srv_cnt_len), I64(cap_recv * S + 1)
+        self.srv_gid, self.srv_eid, self.srv_wcnt = I64(cap_srv_e), I64(cap_srv_e), I64(world)
+        self.resp_cnt, self.resp_seg = I64(cap_dst * S + 1), I64(cap_dst * S + 1)
+        self.resp_gid, self.resp_eid = I64(cap_resp_e), I64(cap_resp_e)
+        P = lambda t: C.c_void_p(t.data_ptr())
+        b = _lib.gsb_exchange_bufs(P(self.req_send), P(self.req_perm), P(self.send_cnt), P(self.cursor),
+                                   P(self.req_recv), cap_recv, P(self.xoff), P(self.srv_meta), P(self.srv_cnt),
+                                   P(self.srv_seg), P(self.srv_gid), P(self.srv_eid), cap_srv_e, P(self.srv_wcnt),
+                                   P(self.resp_cnt), P(self.resp_seg), P(self.resp_gid), P(self.resp_eid), cap_resp_e)
+        self._bufs = b
+        self._fn = _lib.EXCHANGE_FN(self._callback)     # kept alive with self
+        self.bytes_sent = 0
+        call("gsb_blocks_set_exchange", sampler.h, world, rank, first_hop, C.byref(b), self._fn, None)
+        self.sampler = sampler
+
+    def _a2a(self, out, inp, out_splits, in_splits):
+        import torch.distributed as dist
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+
+    def _callback(self, user, phase, hop, stream, counts):
+        try:
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                w = self.world
+                if phase == 0:
+                    recv = torch.empty_like(self.send_cnt)
+                    self._a2a(recv, self.send_cnt, None, None)                       # C1: counts
+                    both = torch.cat([self.send_cnt, recv]).tolist()                 # host sync
+                    self.sc, self.rc = both[:w], both[w:]
+                    ns, nr = sum(self.sc), sum(self.rc)
+                    self._a2a(self.req_recv[:nr], self.req_send[:ns], self.rc, self.sc)   # C2: request ids
+                    for k in range(w):
+                        counts[k] = self.rc[k]
+                    self.bytes_sent += (ns - self.sc[self.rank]) * 8
+                    return 0
+                S = self.S
+                ew = self.srv_wcnt.tolist()                                          # host sync
+                er_t = torch.empty_like(self.srv_wcnt)
+                self._a2a(er_t, self.srv_wcnt, None, None)
+                er = er_t.tolist()
+                ns, nr = sum(self.sc), sum(self.rc)
+                self._a2a(self.resp_cnt[:ns * S], self.srv_cnt[:nr * S], [x * S for x in self.sc],
+                          [x * S for x in self.rc])                                  # C3: counts
+                self._a2a(self.resp_gid[:sum(er)], self.srv_gid[:sum(ew)], er, ew)   # C3: edges
+                self._a2a(self.resp_eid[:sum(er)], self.srv_eid[:sum(ew)], er, ew)
+                self.bytes_sent += (nr - self.rc[self.rank]) * S * 8 + (sum(ew) - ew[self.rank]) * 16
+                return 0
+        except Exception as e:   # reported through the library's status
+            import sys
+            print(f"[gsb] exchange callback failed: {e!r}", file=sys.stderr)
+            return 1
 
 
 class PeerEmbedding:

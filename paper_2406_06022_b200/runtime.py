@@ -570,12 +570,15 @@ class _TrainerBase:
             raise GsbError("pipeline needs device-resident sizes (no all-to-all exchange mode)")
         self.enable_prefetch()
         self.pipe_ws, self.pipe_allreduce = ws, allreduce
+        sample_graph = getattr(self, "sample_graph", True)   # False: NCCL frontier exchange (host-synced)
         if use_graph and self.pipe_graphs is None:
             torch.cuda.synchronize()
             launches0 = lib().gsb_launch_count()
             cap = torch.cuda.Stream(device=self.device)
             graphs = {"sample": [], "compute": []}
-            for kind, fn in (("sample", self._sample_ops), ("compute", self._compute_ops)):
+            kinds = (("sample", self._sample_ops), ("compute", self._compute_ops)) if sample_graph else \
+                (("compute", self._compute_ops),)
+            for kind, fn in kinds:
                 for b in (0, 1):
                     g = torch.cuda.CUDAGraph()
                     cap.wait_stream(torch.cuda.current_stream())
@@ -588,7 +591,7 @@ class _TrainerBase:
             torch.cuda.synchronize()
             # kernels per step = one sample graph + one compute graph
             self.graph_launches = (lib().gsb_launch_count() - launches0) // 2
-            self.pipe_graphs = graphs
+            self.pipe_graphs = graphs if sample_graph else dict(graphs, sample=None)
         elif not use_graph:
             self.pipe_graphs = None
         self.pipe_k = 0
@@ -607,27 +610,42 @@ class _TrainerBase:
         b = self.pipe_k & 1
         nb = b ^ 1
         main = torch.cuda.current_stream()
-        self.side.wait_event(self.ev_c)          # buffer nb is free once batch k-1 computed
-        with torch.cuda.stream(self.side):
-            self._load_inputs(self._bufs[nb], *next_inputs)
-            if self.pipe_graphs is not None:
-                self.pipe_graphs["sample"][nb].replay()
-            else:
-                self._use(nb)
-                self._sample_ops()
-            self.ev_s[nb].record(self.side)
+
+        def sample_next():
+            self.side.wait_event(self.ev_c)          # buffer nb is free once batch k-1 computed
+            with torch.cuda.stream(self.side):
+                self._load_inputs(self._bufs[nb], *next_inputs)
+                if self.pipe_graphs is not None and self.pipe_graphs["sample"] is not None:
+                    self.pipe_graphs["sample"][nb].replay()
+                else:
+                    self._use(nb)
+                    self._sample_ops()
+                self.ev_s[nb].record(self.side)
+
         cs = main if self.hi is None else self.hi
-        if cs is not main:
-            cs.wait_stream(main)
-        cs.wait_event(self.ev_s[b])
-        self._use(b)
-        with torch.cuda.stream(cs):
-            if self.pipe_graphs is not None:
-                self.pipe_graphs["compute"][b].replay()
-            else:
-                self._compute_ops()
-        if cs is not main:
-            main.wait_stream(cs)
+
+        def compute():
+            if cs is not main:
+                cs.wait_stream(main)
+            cs.wait_event(self.ev_s[b])
+            self._use(b)
+            with torch.cuda.stream(cs):
+                if self.pipe_graphs is not None:
+                    self.pipe_graphs["compute"][b].replay()
+                else:
+                    self._compute_ops()
+            if cs is not main:
+                main.wait_stream(cs)
+
+        if getattr(self, "sample_graph", True):
+            sample_next()
+            compute()
+        else:
+            # host-synced sampling (NCCL exchange): enqueue the compute graph first, so the host
+            # waits inside the exchange while batch k computes on the device
+            compute()
+            sample_next()
+            self._use(b)
         if self.pipe_allreduce is not None:
             # the sparse table update (N > 1, after the all-reduce) still reads buffer b's block:
             # the side stream may overwrite b (batch k+2) only after it

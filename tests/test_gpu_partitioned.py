@@ -31,7 +31,7 @@ def _cfg(name):
     return synth.scaled(synth.synth_1b(), 0.01, "synth_small")
 
 
-def _worker(rank, world, port, out, name):
+def _worker(rank, world, port, out, name, mode):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -40,7 +40,8 @@ def _worker(rank, world, port, out, name):
     import synth
     from paper_2406_06022_b200 import build
     build.build()
-    from paper_2406_06022_b200.dist import PeerCSC, PeerFeatures, allreduce_mean, balanced_bounds, rank_step
+    from paper_2406_06022_b200.dist import (FeatureExchange, PeerCSC, PeerFeatures, SampleExchange, allreduce_mean,
+                                            balanced_bounds, rank_step)
     from paper_2406_06022_b200.runtime import GraphStore, RGCNTrainer
     cfg = _cfg(name)
     dev = f"cuda:{rank}"
@@ -52,14 +53,22 @@ def _worker(rank, world, port, out, name):
         st.load_etype_range(r, s_, d_, int(bounds[t][rank]), int(bounds[t][rank + 1]))
         del s_, d_
     out["local_edges%d" % rank] = sum(st.n_edges)
-    csc = PeerCSC(st, world, rank, bounds)
+    csc = PeerCSC(st, world, rank, bounds, map_peers=(mode == "peer"))
     shards = [synth.feature_table(cfg, t, "torch", dev, lo=int(bounds[t][rank]), hi=int(bounds[t][rank + 1]))
               for t in range(cfg.num_ntypes)]
-    pf = PeerFeatures(st, cfg.counts, world, rank, shards, cfg.feat_dim)
+    if mode == "peer":
+        pf = PeerFeatures(st, cfg.counts, world, rank, shards, cfg.feat_dim)
+    else:                         # NCCL all-to-all of features (C4/C5)
+        pf = FeatureExchange(cfg.counts, world, rank, shards, cfg.feat_dim)
+        st.feat_dim = cfg.feat_dim
+        st.feat_dtype = shards[0].dtype
     tr = RGCNTrainer(st, cfg.fanouts, cfg.batch, cfg.hidden, cfg.num_classes, synth.init_params(cfg),
                      synth.param_order(cfg), torch.from_numpy(synth.labels(cfg)),
                      int(cfg.node_off[cfg.target_ntype]), lr=cfg.lr, rng_seed=cfg.rng_seed)
     tr.fuse_gather = False        # unique input rows fetched over NVLink in the sample phase
+    if mode == "nccl":            # frontier exchange C2/C3 at every hop; features C4/C5
+        sx = SampleExchange(tr.sampler, world, rank, first_hop=1)
+        tr.exchange = pf
     # eager step 0 (seeds of global batch rank_step(0, rank)), blocks + grads
     step = rank_step(0, rank, world)
     tr.forward_backward(torch.from_numpy(synth.nc_seeds(cfg, step)).to(dev), step)
@@ -72,6 +81,12 @@ def _worker(rank, world, port, out, name):
                                  b.e_src_gid.cpu().numpy(), b.e_eid.cpu().numpy())
     out["grad%d" % rank] = tr.grad.cpu().numpy().copy()
     out["loss%d" % rank] = float(tr.loss.item())
+    if mode == "nccl":
+        out["xbytes%d" % rank] = sx.bytes_sent
+        dist.barrier()
+        del sx, pf, csc
+        dist.destroy_process_group()
+        return
     # the bench configuration: pipelined per-buffer CUDA graphs + NCCL mean after each compute graph
     ar = lambda g: allreduce_mean(g)
     seeds = [torch.from_numpy(synth.nc_seeds(cfg, rank_step(i, rank, world))).to(dev) for i in range(1, 4)]
@@ -88,8 +103,12 @@ def _worker(rank, world, port, out, name):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["mag_small_bf16", "synth_small"])
-def test_partitioned_topology_multi_gpu(name):
+@pytest.mark.parametrize("name,mode", [("mag_small_bf16", "peer"), ("synth_small", "peer"),
+                                       ("mag_small_bf16", "nccl"), ("synth_small", "nccl")])
+def test_partitioned_topology_multi_gpu(name, mode):
+    """mode peer: shards mapped over NVLink, read by the kernels; mode nccl: no rank reads
+    another's storage -- frontier requests / sampled edges (C2/C3) and feature rows (C4/C5) go
+    through NCCL all-to-alls, the owners sample their requests."""
     import torch
     world = min(torch.cuda.device_count(), 4)
     if world < 2:
@@ -101,7 +120,7 @@ def test_partitioned_topology_multi_gpu(name):
     from tests._pair import close, close_slack, relu_tie_slack
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), out, name), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, name, mode), nprocs=world, join=True)
     cfg = _cfg(name)
     og = oracle.Graph(cfg)
     # every rank stored only its own dst ranges: the shards partition the edges
@@ -121,6 +140,9 @@ def test_partitioned_topology_multi_gpu(name):
         sW, sb, _ = relu_tie_slack(res, cfg.num_etypes, 0)
         slW.append(sW)
         slb.append(sb)
+        if mode == "nccl":
+            assert out["xbytes%d" % r] > 0
+            continue
         # pipelined step (global batch rank_step(1, r)) under the partitioned graph
         step1 = rank_step(1, r, world)
         ob1 = oracle.sample_blocks(og, synth.nc_seeds(cfg, step1), cfg.fanouts, cfg.rng_seed, step1)
