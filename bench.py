@@ -409,6 +409,7 @@ def run_gsb(args, cfg):
         tr.fuse_gather = False   # unique rows over NVLink once (peer loads bypass L2), then local aggregation
     setup_s = time.time() - t0
     n_batches = args.warmup + args.steps + args.profile_steps + 8
+    local_seeds = ws > 1 and partitioned and args.topology == "partitioned"
     if cfg.task == "lp":
         lpb = synth.LPBatcher(cfg)
         uv = [lpb.batch((i * ws + rank) % 100000) for i in range(n_batches)]
@@ -417,11 +418,24 @@ def run_gsb(args, cfg):
         host_batches = [np.stack([x[0], x[1]]) for x in uv[:args.steps + 1]]
     else:
         train = synth.train_nodes(cfg)
-        per_epoch = max(1, len(train) // cfg.batch)
+        if local_seeds:
+            # partitioned graph: every rank iterates over the training nodes it owns (DistDGL-style
+            # locality, SURVEY §8(e) "NC: each GPU takes seeds from its own training nodes"), so
+            # the seeds' own segments and rows are local; batch b of rank r = slice b of its epoch
+            # permutation, RNG step word b * ws + r (globally unique)
+            from paper_2406_06022_b200.dist import balanced_bounds
+            bt = balanced_bounds(cfg.counts, ws)[cfg.target_ntype]
+            loc = train - cfg.node_off[cfg.target_ntype]
+            train = train[(loc >= bt[rank]) & (loc < bt[rank + 1])]
+            per_epoch = max(1, len(train) // cfg.batch)
+            bidx = lambda i: i % (per_epoch * 4)
+        else:
+            per_epoch = max(1, len(train) // cfg.batch)
+            bidx = lambda i: (i * ws + rank) % (per_epoch * 4)
         # seed batches (a1): device-resident epoch permutation slices; rank r takes batch step*ws + r
-        seeds_all = torch.from_numpy(np.stack([synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train)
+        seeds_all = torch.from_numpy(np.stack([synth.nc_seeds(cfg, bidx(i), train)
                                                for i in range(n_batches)])).to(device)
-        host_batches = [synth.nc_seeds(cfg, (i * ws + rank) % (per_epoch * 4), train) for i in range(args.steps + 1)]
+        host_batches = [synth.nc_seeds(cfg, bidx(i), train) for i in range(args.steps + 1)]
 
     def fb(i):
         if cfg.task == "lp":
@@ -687,6 +701,8 @@ def run_gsb(args, cfg):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if cfg.feat_dtype == "f32" else "f32 (bf16 feature storage)", "data": "synthetic (seeded hash generator, synth/)",
         "config": cfg_json(cfg, ws, {"parallelism": par, "cuda_graph": use_graph,
+                                     "seeds": ("each rank's batches are slices of its own training nodes (owner-local)"
+                                               if cfg.task == "nc" and local_seeds else "global epoch permutation"),
                                      "pipeline": "sample i+1 on a side stream during compute i" if pipelined
                                      else "off"}),
         "sampled_edges_per_s": edges_per_step * ws / (ms_per_step / 1e3),

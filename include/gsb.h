@@ -321,6 +321,18 @@ gsb_status gsb_encoder_bwd(gsb_blocks_t b, const void* arena, const float* const
  *   mode 2 (TN): C[K][N] += A[M][K]^T B[M][N]      (C accumulated; zero it first) */
 gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, int64_t ldb, int64_t M, int32_t N,
                     int32_t K, float* C, int64_t ldc, void* stream);
+/* Weight images (3xTF32 operand splits of weights, weights.cu): register W [slots][K][N]
+ * (device fp32) with a caller-owned buffer of gsb_weight_images_bytes() bytes; refresh
+ * recomputes the images of the given registered weights (call it after every update of W,
+ * before the GEMMs that read it, in stream order -- inside a captured step is fine).  While a
+ * weight is registered, the layer / decoder GEMMs whose B operand is that W read its images
+ * through TMA instead of splitting W in every CTA.  Unregister before freeing W or the buffer. */
+gsb_status gsb_weight_images_bytes(int32_t slots, int32_t K, int32_t N, size_t* bytes);
+gsb_status gsb_weight_images_register(const float* W, int32_t slots, int32_t K, int32_t N, void* img,
+                                      size_t img_bytes, void* stream);
+gsb_status gsb_weight_images_unregister(const float* W);
+gsb_status gsb_weight_images_refresh(const float* const* Ws, int32_t n, void* stream);
+
 /* Tools: copies n (<= 256) globaltimer stamps recorded by CTA 0 of the last GEMM launched with
  * GSB_GEMM_DBG & 1024 ([role][64]: producer, MMA, splitters, epilogue; slot 63 = start). */
 gsb_status gsb_gemm_trace(uint64_t* out, int32_t n);

@@ -86,6 +86,10 @@ SIGS = {
     "gsb_graph_set_feature_peers": [P, i32, i32, P, P, i32, i32],
     "gsb_gemm": [i32, P, i64, P, i64, i64, i32, i32, P, i64, P],
     "gsb_gemm_trace": [P, i32],
+    "gsb_weight_images_bytes": [i32, i32, i32, C.POINTER(sz)],
+    "gsb_weight_images_register": [P, i32, i32, i32, P, sz, P],
+    "gsb_weight_images_unregister": [P],
+    "gsb_weight_images_refresh": [P, i32, P],
     "gsb_blocks_set_exchange": [P, i32, i32, i32, C.POINTER(gsb_exchange_bufs), EXCHANGE_FN, P],
     "gsb_exchange_sizes": [P, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64),
                            C.POINTER(i64)],

@@ -149,8 +149,13 @@ __device__ __forceinline__ void panel_coords(const UProb& P, const UCursor& c, i
         const int kk = (c.p - sp * per) * 32;
         a0 = sp * P.d_in + kk;
         a1 = (int32_t)c.row0;
-        b0 = c.n0;
-        b1 = P.rg.slot_w[c.t][sp] * P.brow + kk;
+        if (P.bimg) {               // weight image W^T [(slots) N][K]: K-major, brow = N
+            b0 = kk;
+            b1 = P.rg.slot_w[c.t][sp] * P.brow + c.n0;
+        } else {
+            b0 = c.n0;
+            b1 = P.rg.slot_w[c.t][sp] * P.brow + kk;
+        }
     } else if (MODE == UMMA_NT) {   // A = dZ [rows][N] K-major ; B = W [(slots) d_in][N] K-major
         a0 = c.p * 32;
         a1 = (int32_t)c.row0;
@@ -178,7 +183,8 @@ __device__ __forceinline__ int64_t total_tiles(const UProb& P, int nct, int kct)
 
 template <int MODE>
 __global__ void __launch_bounds__(TG_THREADS, 1) tma_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
-                                                                  const __grid_constant__ CUtensorMap mapB, UProb P) {
+                                                                  const __grid_constant__ CUtensorMap mapB,
+                                                                  const __grid_constant__ CUtensorMap mapB2, UProb P) {
     GSB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1) tma_gemm_kernel(const __grid_co
             umma::mbar_init(&raw_empty[s], TG_SPLIT_WARPS);
         }
         for (int s = 0; s < TG_MMA; ++s) {
-            umma::mbar_init(&mma_full[s], TG_SPLIT_WARPS);
+            umma::mbar_init(&mma_full[s], TG_SPLIT_WARPS + (P.bimg ? 1 : 0));
             umma::mbar_init(&mma_empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -206,6 +212,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1) tma_gemm_kernel(const __grid_co
         umma::fence_barrier_init();
         tma::prefetch_map(&mapA);
         tma::prefetch_map(&mapB);
+        if (P.bimg) tma::prefetch_map(&mapB2);
     }
     if (tid < 128) dbred[tid] = 0.f;
     if (warp == 1) umma::tmem_alloc<256>(&tmem_sh);
@@ -218,7 +225,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1) tma_gemm_kernel(const __grid_co
     const int kct = (P.d_in + 127) / 128;
     const int64_t total = (P.dbg & 64) ? 0 : total_tiles<MODE>(P, nct, kct);
     constexpr bool A_MN = (MODE == UMMA_TN);
-    constexpr bool B_MN = (MODE != UMMA_NT);
+    const bool B_MN = (MODE == UMMA_TN) || (MODE == UMMA_NN && !P.bimg);
 
     UCursor c;
     c.tile = blockIdx.x;
@@ -244,6 +251,9 @@ __global__ void __launch_bounds__(TG_THREADS, 1) tma_gemm_kernel(const __grid_co
                 const uint32_t dst = umma::smem_u32(raw_ring + rs * TG_RAW_STAGE);
                 if (P.dbg & 4) {
                     tma::mbar_arrive(&raw_full[rs]);
+                } else if (P.bimg) {            // A only: B goes straight into the MMA ring (lane 1)
+                    tma::mbar_expect_tx(&raw_full[rs], UM_PANEL);
+                    tma::load_2d(dst, &mapA, a0, a1, &raw_full[rs]);
                 } else {
                     tma::mbar_expect_tx(&raw_full[rs], TG_RAW_STAGE);
                     tma::load_2d(dst, &mapA, a0, a1, &raw_full[rs]);
@@ -253,11 +263,27 @@ __global__ void __launch_bounds__(TG_THREADS, 1) tma_gemm_kernel(const __grid_co
                 if (++rs == TG_RAW) { rs = 0; rph ^= 1u; }
                 advance(c);
             }
+        } else if (lane == 1 && P.bimg) {
+            // pre-split weights: the hi / lo panels are TMA'd into the MMA stage once the MMAs of
+            // the panel two back have drained it; the splitters only split A
+            int ms = 0;
+            uint32_t mph = 0;
+            while (c.tile < total) {
+                tma::mbar_wait_k(&mma_empty[ms], mph ^ 1u, false);
+                int32_t a0, a1, b0, b1;
+                panel_coords<MODE>(P, c, a0, a1, b0, b1);
+                const uint32_t mm = umma::smem_u32(mma_ring + ms * TG_MMA_STAGE);
+                tma::mbar_expect_tx(&mma_full[ms], 2 * UM_PANEL);
+                tma::load_2d(mm + 2 * UM_PANEL, &mapB, b0, b1, &mma_full[ms]);
+                tma::load_2d(mm + 3 * UM_PANEL, &mapB2, b0, b1, &mma_full[ms]);
+                if (++ms == TG_MMA) { ms = 0; mph ^= 1u; }
+                advance(c);
+            }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA issuer
         if (lane == 0) {
-            constexpr uint32_t IDESC = umma::idesc_tf32(128, A_MN, B_MN);
+            const uint32_t IDESC = umma::idesc_tf32(128, A_MN, B_MN);
             int ms = 0, as = 0, pi = 0;
             uint32_t mph = 0, aph = 0;
             while (c.tile < total) {
@@ -323,7 +349,8 @@ __global__ void __launch_bounds__(TG_THREADS, 1) tma_gemm_kernel(const __grid_co
                 cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w;
             } else {
                 split_panel_tma<false>(raw, mm, mm + UM_PANEL, offK, offK, kr, 32);
-                if (MODE == UMMA_NN)
+                if (P.bimg) {
+                } else if (MODE == UMMA_NN)
                     split_panel_tma<false>(raw + UM_PANEL, mm + 2 * UM_PANEL, mm + 3 * UM_PANEL, offK, offM, kr, 32);
                 else
                     split_panel_tma<false>(raw + UM_PANEL, mm + 2 * UM_PANEL, mm + 3 * UM_PANEL, offK, offK, kr, 32);
@@ -464,6 +491,18 @@ __global__ void __launch_bounds__(TG_THREADS, 1) tma_gemm_kernel(const __grid_co
 bool encode_tmap_f32(CUtensorMap* m, const float* base, int64_t width, int64_t rows, int64_t ld, int box_w,
                      int box_h, bool swz128);
 
+// Weight images (gsb_weight_images_register / _refresh, weights.cu): tf32 hi / lo splits of a
+// weight tensor W [slots][K][N] kept in caller memory and refreshed once per step, so the NN
+// and NT GEMMs TMA the B operand straight into the MMA ring (no per-CTA split of the same W).
+//   nn_hi / nn_lo : W^T  [slots][N][K]   (NN B operand, K-major)
+//   nt_hi / nt_lo : W    [slots][K][ldn] (NT B operand, K-major; columns >= N zero)
+struct WeightImage {
+    const float* W;
+    int32_t slots, K, N, ldn;
+    float *nn_hi, *nn_lo, *nt_hi, *nt_lo;
+};
+const WeightImage* find_weight_image(const float* W);
+
 // TMA pipeline when every operand satisfies TMA's alignment rules (16-B aligned bases, row
 // strides multiple of 16 B), else the cp.async kernel.  a_rows / b_rows: row extents of the
 // A and B matrices (A: [a_rows][lda], B: [b_rows][ldb]); a_w / b_w: their widths.
@@ -474,6 +513,7 @@ inline gsb_status launch_gemm(const char* name, UProb P, int64_t tiles_upper, in
     static const int dbg_knobs = getenv("GSB_GEMM_DBG") ? atoi(getenv("GSB_GEMM_DBG")) : 0;
     P.dbg = dbg_knobs;
     P.brow = (int)(P.bslot / std::max<int64_t>(P.ldb, 1));
+    P.bimg = 0;
     static int use_tma = -1;
     if (use_tma < 0) {
         const char* e = getenv("GSB_GEMM");
@@ -488,6 +528,36 @@ inline gsb_status launch_gemm(const char* name, UProb P, int64_t tiles_upper, in
         fprintf(stderr, "[gsb] %s: tma=%d aligned=%d (A %p lda %lld, B %p ldb %lld, bslot %lld)\n", name, use_tma,
                 (int)aligned, (const void*)P.A, (long long)P.lda, (const void*)P.B, (long long)P.ldb,
                 (long long)P.bslot);
+    static const bool no_img = getenv("GSB_NO_WIMG") != nullptr;    // A/B knob
+    const WeightImage* wi = (MODE != UMMA_TN && !no_img) ? find_weight_image(P.B) : nullptr;
+    const bool a_ok = ((reinterpret_cast<uintptr_t>(P.A) & 15) == 0) && ((P.lda & 3) == 0) && a_rows >= 1;
+    if (use_tma && wi && a_ok) {
+        CUtensorMap ma, mb, mb2;
+        const bool kA = true;
+        bool ok = encode_tmap_f32(&ma, P.A, a_w, a_rows, P.lda, kA ? 32 : 128, kA ? 128 : 32, kA);
+        UProb Q = P;
+        Q.bimg = 1;
+        if (MODE == UMMA_NN) {   // W^T [slots*N][K]
+            ok = ok && encode_tmap_f32(&mb, wi->nn_hi, wi->K, (int64_t)wi->slots * wi->N, wi->K, 32, 128, true) &&
+                 encode_tmap_f32(&mb2, wi->nn_lo, wi->K, (int64_t)wi->slots * wi->N, wi->K, 32, 128, true);
+            Q.brow = wi->N;
+        } else {                 // W [slots*K][ldn]
+            ok = ok && encode_tmap_f32(&mb, wi->nt_hi, wi->N, (int64_t)wi->slots * wi->K, wi->ldn, 32, 128, true) &&
+                 encode_tmap_f32(&mb2, wi->nt_lo, wi->N, (int64_t)wi->slots * wi->K, wi->ldn, 32, 128, true);
+            Q.brow = wi->K;
+        }
+        if (ok) {
+            static bool attr_set2 = false;
+            if (!attr_set2) {
+                GSB_CUDA(cudaFuncSetAttribute(tma_gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              TG_SMEM));
+                attr_set2 = true;
+            }
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_upper * Q.ksplit, kNumSMs));
+            GSB_LAUNCH(name, tma_gemm_kernel<MODE>, grid, TG_THREADS, TG_SMEM, s, ma, mb, mb2, Q);
+            return GSB_OK;
+        }
+    }
     if (use_tma && aligned) {
         CUtensorMap ma, mb;
         const bool kA = (MODE != UMMA_TN), kB = (MODE == UMMA_NT);
@@ -501,7 +571,7 @@ inline gsb_status launch_gemm(const char* name, UProb P, int64_t tiles_upper, in
                 attr_set = true;
             }
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_upper * P.ksplit, kNumSMs));
-            GSB_LAUNCH(name, tma_gemm_kernel<MODE>, grid, TG_THREADS, TG_SMEM, s, ma, mb, P);
+            GSB_LAUNCH(name, tma_gemm_kernel<MODE>, grid, TG_THREADS, TG_SMEM, s, ma, mb, mb, P);
             return GSB_OK;
         }
         if (dbg) fprintf(stderr, "[gsb] %s: tensor map encoding failed\n", name);

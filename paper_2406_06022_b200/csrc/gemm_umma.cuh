@@ -66,6 +66,7 @@ struct UProb {
     int ksplit;            // NN/NT: K-panel splits per tile (>1: partials red.add into a zeroed C; no relu)
     int dbg;               // gemm_tma.cuh A/B knobs (GSB_GEMM_DBG): 1 no split, 2 no MMA, 4 no TMA
     int brow;              // gemm_tma.cuh: rows of B per weight slot (bslot / ldb)
+    int bimg;              // gemm_tma.cuh: B comes pre-split (weight images, mapB = hi, mapB2 = lo)
 };
 
 #ifndef GSB_UM_THREADS

@@ -1,0 +1,126 @@
+// weights.cu -- tf32 hi / lo images of the layer and decoder weights for the TMA GEMMs
+// (gemm_tma.cuh).  3xTF32 needs every fp32 operand split into hi = rna_tf32(x) and
+// lo = rna_tf32(x - hi); a weight is the B operand of every CTA of a GEMM, so instead of each
+// CTA splitting the same W in shared memory, W is split once per step into caller-owned images
+// in the two layouts the NN (W^T) and NT (W) GEMMs read K-major, and the GEMMs TMA them
+// straight into the MMA stage.  Contract: include/gsb.h "Weight images".
+#include <mutex>
+
+#include "gemm_tma.cuh"
+#include "gsb_internal.cuh"
+
+namespace gsb {
+
+static std::mutex g_wi_mu;
+static std::vector<WeightImage> g_wi;
+
+const WeightImage* find_weight_image(const float* W) {
+    std::lock_guard<std::mutex> lk(g_wi_mu);
+    for (const WeightImage& w : g_wi)
+        if (w.W == W) return &w;
+    return nullptr;
+}
+
+static size_t wi_floats(int slots, int K, int N, int ldn) {
+    const size_t nn = (size_t)slots * N * K, nt = (size_t)slots * K * ldn;
+    return 2 * ((nn + 3) / 4 * 4) + 2 * ((nt + 3) / 4 * 4);
+}
+
+constexpr int kMaxImages = 8;
+struct WiBatch {
+    int n;
+    WeightImage w[kMaxImages];
+};
+
+// one thread per weight element of every registered image: split, write W^T and W layouts
+__global__ void __launch_bounds__(256) weight_split_kernel(WiBatch b) {
+    GSB_PDL_ENTRY();
+    for (int q = 0; q < b.n; ++q) {
+        const WeightImage& w = b.w[q];
+        const int64_t total = (int64_t)w.slots * w.K * w.N;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t s = i / ((int64_t)w.K * w.N);
+            const int64_t r = i - s * w.K * w.N;
+            const int k = (int)(r / w.N), n = (int)(r - (int64_t)k * w.N);
+            uint32_t hi, lo;
+            umma::split_tf32(w.W[i], hi, lo);
+            const int64_t tn = (s * w.N + n) * w.K + k;            // W^T [s][n][k]
+            const int64_t tk = (s * w.K + k) * w.ldn + n;          // W   [s][k][n] (ldn)
+            w.nn_hi[tn] = __uint_as_float(hi);
+            w.nn_lo[tn] = __uint_as_float(lo);
+            w.nt_hi[tk] = __uint_as_float(hi);
+            w.nt_lo[tk] = __uint_as_float(lo);
+        }
+    }
+}
+
+}  // namespace gsb
+
+using namespace gsb;
+
+extern "C" {
+
+gsb_status gsb_weight_images_bytes(int32_t slots, int32_t K, int32_t N, size_t* bytes) {
+    GSB_CHECK_ARG(bytes && slots >= 1 && K >= 1 && N >= 1, "bad argument");
+    *bytes = sizeof(float) * wi_floats(slots, K, N, (N + 3) / 4 * 4);
+    return GSB_OK;
+}
+
+gsb_status gsb_weight_images_register(const float* W, int32_t slots, int32_t K, int32_t N, void* img,
+                                      size_t img_bytes, void* stream) {
+    GSB_CHECK_ARG(W && img && slots >= 1 && K >= 1 && N >= 1, "bad argument");
+    GSB_CHECK_ARG(((uintptr_t)img & 15) == 0, "image buffer must be 16-byte aligned");
+    const int ldn = (N + 3) / 4 * 4;
+    GSB_CHECK_ARG(img_bytes >= sizeof(float) * wi_floats(slots, K, N, ldn), "image buffer too small");
+    WeightImage w;
+    w.W = W;
+    w.slots = slots;
+    w.K = K;
+    w.N = N;
+    w.ldn = ldn;
+    float* p = static_cast<float*>(img);
+    const size_t nn = ((size_t)slots * N * K + 3) / 4 * 4, nt = ((size_t)slots * K * ldn + 3) / 4 * 4;
+    w.nn_hi = p;
+    w.nn_lo = p + nn;
+    w.nt_hi = p + 2 * nn;
+    w.nt_lo = p + 2 * nn + nt;
+    // padding columns of the W layout stay zero (the NT GEMM reduces over them)
+    GSB_CUDA(cudaMemsetAsync(img, 0, img_bytes, (cudaStream_t)stream));
+    std::lock_guard<std::mutex> lk(g_wi_mu);
+    for (WeightImage& x : g_wi)
+        if (x.W == W) {
+            x = w;
+            return GSB_OK;
+        }
+    GSB_CHECK_ARG(g_wi.size() < 64, "too many weight images");
+    g_wi.push_back(w);
+    return GSB_OK;
+}
+
+gsb_status gsb_weight_images_unregister(const float* W) {
+    std::lock_guard<std::mutex> lk(g_wi_mu);
+    for (size_t i = 0; i < g_wi.size(); ++i)
+        if (g_wi[i].W == W) {
+            g_wi.erase(g_wi.begin() + (long)i);
+            break;
+        }
+    return GSB_OK;
+}
+
+gsb_status gsb_weight_images_refresh(const float* const* Ws, int32_t n, void* stream) {
+    GSB_CHECK_ARG(Ws && n >= 1 && n <= kMaxImages, "1..%d weights per refresh", kMaxImages);
+    WiBatch b;
+    b.n = n;
+    int64_t total = 0;
+    for (int q = 0; q < n; ++q) {
+        const WeightImage* w = find_weight_image(Ws[q]);
+        GSB_CHECK_ARG(w, "weight %d has no registered image", q);
+        b.w[q] = *w;
+        total = std::max<int64_t>(total, (int64_t)w->slots * w->K * w->N);
+    }
+    GSB_LAUNCH("weight_split", weight_split_kernel, grid_for(total, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream, b);
+    return GSB_OK;
+}
+
+}  // extern "C"

@@ -274,7 +274,8 @@ class SampleExchange:
 
     def _callback(self, user, phase, hop, stream, counts):
         try:
-            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+            st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+            with torch.cuda.stream(st):
                 w = self.world
                 if phase == 0:
                     recv = torch.empty_like(self.send_cnt)

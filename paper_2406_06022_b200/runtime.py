@@ -354,6 +354,38 @@ class _TrainerBase:
         self._bufs = None         # double-buffered per-batch state (enable_prefetch)
         self.pipe_graphs = None
         self.pipe_k = 0
+        self._wimg_names = []
+        # opt-in (GSB_WIMG=1): measured neutral on the GEMMs and +11.7 us for the refresh on the
+        # mag step (profiles/round2_weight_images.md)
+        if os.environ.get("GSB_WIMG") == "1":
+            self._register_weight_images()
+
+    def _register_weight_images(self):
+        """tf32 hi/lo images of the layer weights and the NC decoder (gsb_weight_images_*): the
+        GEMMs then TMA the split B operand instead of splitting W in every CTA; refreshed at the
+        start of every compute phase (after the previous step's Adam)."""
+        self._wimg_names = [f"W{l}" for l in range(self.L)] + (["Wc"] if "Wc" in self.names else [])
+        self._wimg_bufs = []
+        for name in self._wimg_names:
+            shp = self.shapes[name]
+            slots, K, N = (int(shp[0]), int(shp[1]), int(shp[2])) if len(shp) == 3 else (1, int(shp[0]), int(shp[1]))
+            nb = C.c_size_t()
+            call("gsb_weight_images_bytes", slots, K, N, C.byref(nb))
+            buf = torch.empty(int(nb.value), dtype=torch.uint8, device=self.device)
+            call("gsb_weight_images_register", self._pp(name), slots, K, N, _ptr(buf), buf.numel(), _stream())
+            self._wimg_bufs.append(buf)
+        self._wimg_ptrs = (C.c_void_p * len(self._wimg_names))(*[self._pp(n).value for n in self._wimg_names])
+
+    def _refresh_weight_images(self, s):
+        if self._wimg_names:
+            call("gsb_weight_images_refresh", self._wimg_ptrs, len(self._wimg_names), s)
+
+    def __del__(self):
+        try:
+            for name in getattr(self, "_wimg_names", []):
+                lib().gsb_weight_images_unregister(self._pp(name))
+        except Exception:
+            pass
 
     # parameter views -------------------------------------------------------------------
     def pview(self, name: str, which: str = "p") -> torch.Tensor:
@@ -698,6 +730,7 @@ class RGCNTrainer(_TrainerBase):
 
     def _compute_phase(self, stream=None, seeds=None):
         s = _stream(stream)
+        self._refresh_weight_images(s)
         seeds = self.seeds_dev if seeds is None else seeds
         n = seeds.numel()
         h = self._encode(s)
@@ -826,6 +859,7 @@ class LPTrainer(_TrainerBase):
 
     def _compute_phase(self, stream=None, seeds=None):
         s = _stream(stream)
+        self._refresh_weight_images(s)
         h = self._encode(s)
         top = self.L - 1
         dm = self.score == "distmult"
