@@ -195,6 +195,155 @@ __global__ void __launch_bounds__(256) lp_score_kernel(const float* __restrict__
         for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(drel + c, s_drel[c]);
 }
 
+// ------------------------------------------------------------------------------------
+// Joint negatives (group == K <= 32): one CTA per group of K positives that share K
+// negatives.  The negatives' rows are staged in shared memory once per group (instead of once
+// per positive), lane j of a positive's warp scores negative j against the staged u*r row, and
+// the negatives' gradients dH[neg_j] += sum_i ds_ij (u_i * r) are reduced over the group in
+// shared memory and added once per group (instead of one red.add per positive and negative).
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) lp_group_kernel(const float* __restrict__ H, int d,
+                                                       const int32_t* __restrict__ iu, const int32_t* __restrict__ iv,
+                                                       const int32_t* __restrict__ ineg, int64_t B, int K,
+                                                       const float* __restrict__ rel, int kind,
+                                                       const float* __restrict__ wpos, float* __restrict__ scores,
+                                                       float* __restrict__ row_loss, float* __restrict__ dH,
+                                                       float* __restrict__ drel) {
+    GSB_PDL_ENTRY();
+    extern __shared__ float sm[];
+    const int d4 = d >> 2, ldn = d + 4;
+    float* s_neg = sm;                      // [K][ldn] negative rows
+    float* s_ur = s_neg + K * ldn;          // [K][ldn] u*r of the group's positives
+    float* s_ds = s_ur + K * ldn;           // [K][32]  dloss / dscore(positive p, negative j)
+    float* s_drel = s_ds + K * 32;          // [d]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (int c = tid; c < d; c += blockDim.x) s_drel[c] = 0.f;
+    float4 r[kMaxC4], dr[kMaxC4];
+#pragma unroll
+    for (int q = 0; q < kMaxC4; ++q) {
+        const int c = lane + 32 * q;
+        r[q] = (c >= d4) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                         : (rel ? __ldg(reinterpret_cast<const float4*>(rel) + c) : make_float4(1.f, 1.f, 1.f, 1.f));
+        dr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float invB = 1.f / (float)B;
+    const int64_t G = (B + K - 1) / K;
+    for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
+        const int64_t i0 = g * K;
+        const int np = (int)min((int64_t)K, B - i0);
+        __syncthreads();       // the previous group's readers of s_neg / s_ur / s_ds are done
+        for (int x = tid; x < K * d4; x += blockDim.x) {
+            const int j = x / d4, c = x - j * d4;
+            *reinterpret_cast<float4*>(s_neg + j * ldn + 4 * c) =
+                __ldg(reinterpret_cast<const float4*>(H + (int64_t)ineg[i0 + j] * d) + c);
+        }
+        __syncthreads();
+        for (int p = warp; p < np; p += nwarps) {
+            const int64_t i = i0 + p;
+            const float* hu = H + (int64_t)iu[i] * d;
+            const float* hv = H + (int64_t)iv[i] * d;
+            float4 u[kMaxC4], ur[kMaxC4], v[kMaxC4];
+            float s0 = 0.f;
+#pragma unroll
+            for (int q = 0; q < kMaxC4; ++q) {
+                const int c = lane + 32 * q;
+                u[q] = v[q] = ur[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (c < d4) {
+                    u[q] = reinterpret_cast<const float4*>(hu)[c];
+                    v[q] = reinterpret_cast<const float4*>(hv)[c];
+                    ur[q] = make_float4(u[q].x * r[q].x, u[q].y * r[q].y, u[q].z * r[q].z, u[q].w * r[q].w);
+                    s0 += ur[q].x * v[q].x + ur[q].y * v[q].y + ur[q].z * v[q].z + ur[q].w * v[q].w;
+                    *reinterpret_cast<float4*>(s_ur + p * ldn + 4 * c) = ur[q];
+                }
+            }
+            s0 = warp_sum(s0);
+            __syncwarp();
+            // lane j: score of negative j (rows padded to ldn: lanes hit distinct banks)
+            float sj = 0.f;
+            if (lane < K) {
+                const float4* a = reinterpret_cast<const float4*>(s_ur + p * ldn);
+                const float4* b = reinterpret_cast<const float4*>(s_neg + lane * ldn);
+                for (int c = 0; c < d4; ++c) {
+                    const float4 x = a[c], y = b[c];
+                    sj += x.x * y.x + x.y * y.y + x.z * y.z + x.w * y.w;
+                }
+            }
+            float* sc = scores + i * (K + 1);
+            if (lane == 0) sc[0] = s0;
+            if (lane < K) sc[1 + lane] = sj;
+            float mx = (lane < K) ? fmaxf(sj, s0) : s0;
+            for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const float se = expf(s0 - mx) + warp_sum(lane < K ? expf(sj - mx) : 0.f);
+            const float lse = mx + logf(se);
+            const float wi = (kind == 2) ? wpos[i] : 1.f;
+            const float lsum = wi * softplus(-s0) + warp_sum(lane < K ? softplus(sj) : 0.f);
+            if (lane == 0) row_loss[i] = (kind == 0) ? (lse - s0) : lsum / (float)(K + 1);
+            const float ds0 =
+                (kind == 0) ? (expf(s0 - lse) - 1.f) * invB : wi * (sigm(s0) - 1.f) / (float)(K + 1) * invB;
+            const float dsj = (lane < K) ? ((kind == 0) ? expf(sj - lse) * invB : sigm(sj) / (float)(K + 1) * invB) : 0.f;
+            s_ds[p * 32 + lane] = dsj;
+            float4 du[kMaxC4];
+#pragma unroll
+            for (int q = 0; q < kMaxC4; ++q) {
+                du[q] = make_float4(ds0 * r[q].x * v[q].x, ds0 * r[q].y * v[q].y, ds0 * r[q].z * v[q].z,
+                                    ds0 * r[q].w * v[q].w);
+                dr[q].x += ds0 * u[q].x * v[q].x; dr[q].y += ds0 * u[q].y * v[q].y;
+                dr[q].z += ds0 * u[q].z * v[q].z; dr[q].w += ds0 * u[q].w * v[q].w;
+            }
+            for (int j = 0; j < K; ++j) {
+                const float ds = __shfl_sync(0xffffffffu, dsj, j);
+#pragma unroll
+                for (int q = 0; q < kMaxC4; ++q) {
+                    const int c = lane + 32 * q;
+                    if (c < d4) {
+                        const float4 n = *reinterpret_cast<const float4*>(s_neg + j * ldn + 4 * c);
+                        du[q].x += ds * r[q].x * n.x; du[q].y += ds * r[q].y * n.y;
+                        du[q].z += ds * r[q].z * n.z; du[q].w += ds * r[q].w * n.w;
+                        dr[q].x += ds * u[q].x * n.x; dr[q].y += ds * u[q].y * n.y;
+                        dr[q].z += ds * u[q].z * n.z; dr[q].w += ds * u[q].w * n.w;
+                    }
+                }
+            }
+            float* duo = dH + (int64_t)iu[i] * d;
+            float* dvo = dH + (int64_t)iv[i] * d;
+#pragma unroll
+            for (int q = 0; q < kMaxC4; ++q) {
+                const int c = lane + 32 * q;
+                if (c < d4) {
+                    red_add_f4(duo + 4 * c, du[q]);
+                    red_add_f4(dvo + 4 * c, make_float4(ds0 * ur[q].x, ds0 * ur[q].y, ds0 * ur[q].z, ds0 * ur[q].w));
+                }
+            }
+        }
+        __syncthreads();
+        // negatives: dH[neg_j] += sum over the group's positives p of ds[p][j] * (u_p * r)
+        for (int x = tid; x < K * d4; x += blockDim.x) {
+            const int j = x / d4, c = x - j * d4;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int p = 0; p < np; ++p) {
+                const float w = s_ds[p * 32 + j];
+                const float4 y = *reinterpret_cast<const float4*>(s_ur + p * ldn + 4 * c);
+                acc.x += w * y.x; acc.y += w * y.y; acc.z += w * y.z; acc.w += w * y.w;
+            }
+            red_add_f4(dH + (int64_t)ineg[i0 + j] * d + 4 * c, acc);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kMaxC4; ++q) {
+        const int c = lane + 32 * q;
+        if (c < d4) {
+            atomicAdd(&s_drel[4 * c + 0], dr[q].x);
+            atomicAdd(&s_drel[4 * c + 1], dr[q].y);
+            atomicAdd(&s_drel[4 * c + 2], dr[q].z);
+            atomicAdd(&s_drel[4 * c + 3], dr[q].w);
+        }
+    }
+    __syncthreads();
+    if (rel)
+        for (int c = tid; c < d; c += blockDim.x) atomicAdd(drel + c, s_drel[c]);
+}
+
 __global__ void __launch_bounds__(1024) lp_mean_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
     GSB_PDL_ENTRY();
     __shared__ float sm[32];
@@ -448,6 +597,17 @@ gsb_status gsb_lp_score_ex(const float* H, int64_t n_rows_cap, int32_t d, const 
         if (st != GSB_OK) return st;
         GSB_LAUNCH("lp_ib_finish", ib_finish_kernel, grid_for(n4, 256, kNumSMs * 4), 256, sizeof(float) * d, s, U, M,
                    dV, iu, iv, B, d, rel, dH, drel);
+    } else if (neg_mode == 0 && group == K && K <= 32 && !getenv("GSB_LP_WARP")) {
+        // joint negatives: one CTA per group (GSB_LP_WARP=1: the warp-per-positive kernel, A/B)
+        const size_t smem = sizeof(float) * (size_t)(2 * K * (d + 4) + K * 32 + d);
+        static size_t smem_set = 0;
+        if (smem > 48 * 1024 && smem > smem_set) {
+            GSB_CUDA(cudaFuncSetAttribute(lp_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            smem_set = smem;
+        }
+        const int64_t G = (B + K - 1) / K;
+        GSB_LAUNCH("lp_score", lp_group_kernel, (int)std::min<int64_t>(G, kNumSMs * 8), 256, smem, s, H, d, iu, iv,
+                   ineg, B, K, rel, loss_kind, w, scores, row_loss_ws, dH, drel);
     } else {
         GSB_LAUNCH("lp_score", lp_score_kernel, grid_for(B * 32, 256, kNumSMs * 4), 256, sizeof(float) * d, s, H, d,
                    iu, iv, ineg, B, K, neg_mode == 0 ? group : 1, neg_mode, rel, loss_kind, w, scores, row_loss_ws,

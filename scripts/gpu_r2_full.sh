@@ -9,9 +9,11 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}
 . scripts/summ.sh
 timeout 900 python bench.py > gpurun_out/${T}_bench.log 2>&1; echo bench rc $?; summ gpurun_out/${T}_bench.log
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/${T}_ref.log 2>&1; echo ref rc $?; tail -c 300 gpurun_out/${T}_ref.log; echo
-for c in synth_1b gcn_1b; do
-  timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/${T}_bench_$c.log 2>&1; echo bench $c rc $?; summ gpurun_out/${T}_bench_$c.log | head -2
+for c in synth_1b gcn_1b amazon_lp mag240m_1_16; do
+  timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/${T}_bench_$c.log 2>&1; echo bench $c rc $?; summ gpurun_out/${T}_bench_$c.log | head -2
 done
+timeout 600 python bench.py --feat-dtype f32 --no-cpu-baseline > gpurun_out/${T}_bench_mag_f32.log 2>&1; echo bench mag f32 rc $?; summ gpurun_out/${T}_bench_mag_f32.log | head -2
+GSB_LP_WARP=1 timeout 600 python bench.py --config amazon_lp --no-cpu-baseline > gpurun_out/${T}_bench_amazon_lp_warp.log 2>&1; echo bench lp warp rc $?; summ gpurun_out/${T}_bench_amazon_lp_warp.log | head -2
 CMD="python bench.py --no-cpu-baseline --steps 3 --warmup 3 --profile-steps 2 --no-graph --pipeline off"
 timeout 900 ncu --nvtx --print-nvtx-rename kernel --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   --print-units base --clock-control none --csv --log-file gpurun_out/${T}_traffic.csv $CMD > gpurun_out/${T}_ncu_traffic.log 2>&1; echo traffic rc $?
