@@ -177,8 +177,61 @@ __global__ void __launch_bounds__(256) gather_kernel(GraphDev g, const int64_t* 
     }
 }
 
+// 32-byte chunks (256-bit loads, LDG.E.ENL2.256): half the address work and load instructions
+// per byte of the 16-byte kernel; 8 chunks of different rows in flight per thread.  Used for
+// rows that are a multiple of 32 bytes (every config's 64-d fp32 / 128-d bf16 rows).
+__global__ void __launch_bounds__(256) gather32_kernel(GraphDev g, const int64_t* __restrict__ gid,
+                                                       const int64_t* __restrict__ n_dev, int64_t n_host,
+                                                       uint4* __restrict__ out) {
+    GSB_PDL_ENTRY();
+    constexpr int U = 8;
+    const int64_t n = n_dev ? *n_dev : n_host;
+    const int d32 = g.feat_row_bytes >> 5;
+    const int64_t total = n * d32;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t N = g.node_off[g.T];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += U * stride) {
+        uint32_t v[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t idx = i + u * stride;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[u][k] = 0u;
+            if (idx < total) {
+                const int64_t row = idx / d32;
+                const int c = (int)(idx - row * d32);
+                const int64_t x = __ldg(gid + row);
+                if (x >= 0 && x < N) {
+                    const char* p = reinterpret_cast<const char*>(feat_row(g, x)) + 32 * c;
+                    asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                                 : "=r"(v[u][0]), "=r"(v[u][1]), "=r"(v[u][2]), "=r"(v[u][3]), "=r"(v[u][4]),
+                                   "=r"(v[u][5]), "=r"(v[u][6]), "=r"(v[u][7])
+                                 : "l"(p));
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t idx = i + u * stride;
+            if (idx < total) {
+                out[2 * idx] = make_uint4(v[u][0], v[u][1], v[u][2], v[u][3]);
+                out[2 * idx + 1] = make_uint4(v[u][4], v[u][5], v[u][6], v[u][7]);
+            }
+        }
+    }
+}
+
 gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_dev, int64_t n_host, int64_t n_max,
                          void* out, cudaStream_t s) {
+    static const bool g16 = getenv("GSB_GATHER16") != nullptr;     // A/B knob
+    if (!g16 && G->dev.feat_row_bytes % 32 == 0) {
+        // bounded grid: the unique-row fetch is latency / NVLink bound and runs beside the compute
+        // phase's GEMMs (one CTA per SM); 2 blocks per SM keep ~4 MB in flight
+        const int64_t work = n_max * (G->dev.feat_row_bytes / 32);
+        const int grid = grid_for(ceil_div(work, 8), 256, kNumSMs * 2);
+        GSB_LAUNCH("gather", gather32_kernel, grid, 256, 0, s, G->dev, gid, n_dev, n_host, static_cast<uint4*>(out));
+        return GSB_OK;
+    }
     int64_t work = n_max * (G->dev.feat_row_bytes / 16);
     int grid = grid_for(ceil_div(work, 4), 256, kNumSMs * 8);
     GSB_LAUNCH("gather", gather_kernel, grid, 256, 0, s, G->dev, gid, n_dev, n_host, static_cast<uint4*>(out));

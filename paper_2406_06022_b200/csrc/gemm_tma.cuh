@@ -99,7 +99,13 @@ __device__ __forceinline__ void trace_mark(const UProb& P, int role, int i) {
     }
 }
 
-constexpr int TG_SPLIT_WARPS = 16;             // 4 per SM sub-partition: the split is latency-bound
+#ifndef GSB_TG_SPLIT_WARPS
+#define GSB_TG_SPLIT_WARPS 8
+#endif
+// splitter warps: the split is latency / smem bound (more warps split faster) but every thread
+// of this one-CTA-per-SM kernel holds its registers for the whole launch, and the sample phase
+// of the next batch runs concurrently on the same SMs (profiles/round2_gemm_split_warps.md)
+constexpr int TG_SPLIT_WARPS = GSB_TG_SPLIT_WARPS;
 constexpr int TG_SPLIT = 32 * TG_SPLIT_WARPS;     // splitter threads
 constexpr int TG_EPI_WARP0 = 2 + TG_SPLIT_WARPS;  // first epilogue warp
 constexpr int TG_THREADS = 32 * (TG_EPI_WARP0 + 4);

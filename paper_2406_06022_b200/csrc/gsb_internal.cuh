@@ -216,6 +216,17 @@ struct HopBufs {
     int64_t* e_eid;       // [cap_edges]
     int32_t* e_src;       // [cap_edges]
     int64_t* src_gid;     // [cap_src]
+    CscSeg* segc;         // [cap_dst*S] the (dst, slot) segments count resolved, reused by fill
+    // by-source transposed CSR of the block (§8(a) a4; hops feeding layers >= 1, else null):
+    // the edges of src row u are t_edge[t_ptr[u] .. t_ptr[u+1]) in ascending edge order;
+    // e_seg[e] = (dst row, slot) segment of edge e
+    int32_t* e_seg;       // [cap_edges]
+    int32_t* t_key;       // [cap_edges] sort keys (src row; past the live edges INT32_MAX); after the
+                          //   sort: t_seg, the segment id of transposed position k
+    int32_t* t_key2;      // [cap_edges]
+    int32_t* t_val;       // [cap_edges] edge ids before the sort; after it: 1 / segment count (fp32 bits)
+    int32_t* t_edge;      // [cap_edges]
+    int32_t* t_ptr;       // [cap_src + 1]
 };
 
 struct Graph {
@@ -263,7 +274,8 @@ struct Blocks {
     // arena layout (byte offsets)
     size_t off_meta[kMaxL + 1];
     size_t off_seed, off_cnt[kMaxL], off_seg[kMaxL], off_esrcgid[kMaxL], off_eeid[kMaxL], off_esrc[kMaxL];
-    size_t off_src[kMaxL];
+    size_t off_src[kMaxL], off_segc[kMaxL];
+    size_t off_tcsr[kMaxL];   // transposed CSR block of hop h (0: none)
     size_t off_map, off_bitmap, off_wrank, off_err, off_cub, off_excl;
     size_t cub_bytes, total_bytes;
     int64_t cap_dst[kMaxL + 1], cap_edges[kMaxL];

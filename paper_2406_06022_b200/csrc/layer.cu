@@ -454,6 +454,70 @@ __global__ void __launch_bounds__(256) scatter_kernel(GraphDev g, const HopMeta*
     }
 }
 
+// Deterministic backward scatter through the block's transposed CSR (§8(a) a4): warp per src
+// row u; its self term (u in the dst prefix: dA[j, S_t]) then its in-edges in ascending edge
+// order, dA[j(e), s(e)] / c_s(j); one plain store per row (no atomics, no memset).
+__global__ void __launch_bounds__(256) scatter_t_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                        const int32_t* __restrict__ t_seg,
+                                                        const int32_t* __restrict__ t_ptr,
+                                                        const int32_t* __restrict__ t_inv,
+                                                        const float* __restrict__ dA, int64_t lda, int d,
+                                                        float* __restrict__ dh) {
+    GSB_PDL_ENTRY();
+    const int lane = threadIdx.x & 31;
+    const int S = g.S;
+    const int64_t n_src = m->n_src;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int d4 = d >> 2;
+    for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n_src; u += warps) {
+        int t = 0;
+        for (int k = 1; k < g.T; ++k) t += (u >= m->src_off[k]) ? 1 : 0;
+        const int64_t local = u - m->src_off[t];
+        float4 acc[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (local < m->dst_off[t + 1] - m->dst_off[t]) {     // u is dst row j's own row
+            const int64_t j = m->dst_off[t] + local;
+            const float4* row = reinterpret_cast<const float4*>(dA + j * lda + (int64_t)g.n_slots[t] * d);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (lane + 32 * q < d4) acc[q] = row[lane + 32 * q];
+        }
+        const int32_t k0 = t_ptr[u], k1 = t_ptr[u + 1];
+        for (int32_t kb = k0; kb < k1; kb += 4) {
+            // up to 4 edges' gradient rows in flight, summed in ascending edge order
+            float4 v[4][4];
+            float inv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                inv[e] = 0.f;
+                if (kb + e < k1) {
+                    const int32_t i = t_seg[kb + e];
+                    const int64_t j = i / S;
+                    const int s = i - (int)(j * S);
+                    inv[e] = __int_as_float(t_inv[kb + e]);
+                    const float4* row = reinterpret_cast<const float4*>(dA + j * lda + (int64_t)s * d);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        v[e][q] = (lane + 32 * q < d4) ? row[lane + 32 * q] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (kb + e < k1)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        acc[q].x += v[e][q].x * inv[e]; acc[q].y += v[e][q].y * inv[e];
+                        acc[q].z += v[e][q].z * inv[e]; acc[q].w += v[e][q].w * inv[e];
+                    }
+        }
+        float4* o = reinterpret_cast<float4*>(dh + u * d);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (lane + 32 * q < d4) o[lane + 32 * q] = acc[q];
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // softmax cross-entropy, warp per row; logits are overwritten by dlogits
 // ------------------------------------------------------------------------------------
@@ -541,6 +605,172 @@ __global__ void __launch_bounds__(256) ce_kernel(float* __restrict__ logits, int
             *loss = tot / (float)n;
             *ticket = 0u;
         }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// NC decoder, fused (SIMT fp32): north_star puts the tensor cores on the per-relation GEMMs
+// only; the decoder's three [S0 x d] x [d x C] products (S0 = 1024, C = 349: 92 MFLOP each)
+// are too small to amortise a tcgen05 pipeline (~10 us of fixed cost per launch).  Kernel 1,
+// one CTA per TR seed rows: logits = h Wc + bc (thread per class column, Wc rows coalesced),
+// softmax-CE per row (warp per row; loss, dlogits = (softmax - 1_y) / n), dh = dlogits Wc^T
+// (warp per 1/8 of the hidden columns, lanes over classes, warp reductions), and the batch
+// mean through per-block partials + a last-block ticket (deterministic order).  Kernel 2:
+// dWc = h^T dlogits and dbc over row chunks (k-tile x row-chunk blocks, red.add).
+// ------------------------------------------------------------------------------------
+constexpr int kNcTR = 8;       // seed rows per CTA (one warp per row in the softmax)
+
+__global__ void __launch_bounds__(256) nc_fused_kernel(const float* __restrict__ h, int64_t n, int d,
+                                                       const float* __restrict__ Wc, const float* __restrict__ bc,
+                                                       int C, int64_t ldl, const int32_t* __restrict__ labels,
+                                                       const int64_t* __restrict__ seed_gid, int64_t base,
+                                                       float* __restrict__ dl_out, float* __restrict__ row_loss,
+                                                       float* __restrict__ part, unsigned* __restrict__ ticket,
+                                                       float* __restrict__ loss, float* __restrict__ dh) {
+    GSB_PDL_ENTRY();
+    extern __shared__ float sm[];
+    float* sh = sm;                          // [TR][d]   seed rows
+    float* sl = sm + kNcTR * d;              // [TR][ldl] logits, then dlogits
+    __shared__ float wsum[8];
+    __shared__ bool last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float invn = 1.f / (float)n;
+    float mine = 0.f;
+    const int64_t tiles = (n + kNcTR - 1) / kNcTR;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t r0 = tile * kNcTR;
+        const int nr = (int)min((int64_t)kNcTR, n - r0);
+        for (int x = tid; x < kNcTR * d; x += blockDim.x) {
+            const int r = x / d, k = x - r * d;
+            sh[x] = r < nr ? h[(r0 + r) * d + k] : 0.f;
+        }
+        __syncthreads();
+        // logits: thread per class column, Wc row k read coalesced across the block
+        for (int c = tid; c < C; c += blockDim.x) {
+            float acc[kNcTR];
+            const float b = __ldg(bc + c);
+#pragma unroll
+            for (int r = 0; r < kNcTR; ++r) acc[r] = b;
+#pragma unroll 4
+            for (int k = 0; k < d; k += 4) {     // d % 32 == 0; 16-B smem broadcasts of the rows
+                const float w0 = __ldg(Wc + (int64_t)k * C + c), w1 = __ldg(Wc + (int64_t)(k + 1) * C + c);
+                const float w2 = __ldg(Wc + (int64_t)(k + 2) * C + c), w3 = __ldg(Wc + (int64_t)(k + 3) * C + c);
+#pragma unroll
+                for (int r = 0; r < kNcTR; ++r) {
+                    const float4 x = *reinterpret_cast<const float4*>(sh + r * d + k);
+                    acc[r] += x.x * w0 + x.y * w1 + x.z * w2 + x.w * w3;
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kNcTR; ++r) sl[r * ldl + c] = acc[r];
+        }
+        __syncthreads();
+        // softmax-CE: warp r owns row r
+        if (warp < nr) {
+            const int r = warp;
+            const int64_t i = r0 + r;
+            float* row = sl + r * ldl;
+            const int y = labels[seed_gid[i] - base];
+            float mx = -INFINITY;
+            for (int c = lane; c < C; c += 32) mx = fmaxf(mx, row[c]);
+            for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            float se = 0.f;
+            for (int c = lane; c < C; c += 32) se += expf(row[c] - mx);
+            for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+            const float lse = mx + logf(se);
+            const float li = lse - row[y];
+            __syncwarp();
+            for (int c = lane; c < C; c += 32) {
+                const float g = (expf(row[c] - lse) - (c == y ? 1.f : 0.f)) * invn;
+                row[c] = g;
+                dl_out[i * ldl + c] = g;
+            }
+            if (lane == 0) {
+                row_loss[i] = li;
+                mine += li;
+            }
+        } else if (warp < kNcTR) {
+            for (int c = lane; c < C; c += 32) sl[warp * ldl + c] = 0.f;
+        }
+        __syncthreads();
+        // dh = dlogits Wc^T: warp w owns hidden columns k = w, w + 8, ...; lanes over classes
+        for (int k = warp; dh && k < d; k += 8) {
+            float acc[kNcTR];
+#pragma unroll
+            for (int r = 0; r < kNcTR; ++r) acc[r] = 0.f;
+            const float* wk = Wc + (int64_t)k * C;
+#pragma unroll 4
+            for (int c = lane; c < C; c += 32) {
+                const float w = __ldg(wk + c);
+#pragma unroll
+                for (int r = 0; r < kNcTR; ++r) acc[r] += sl[r * ldl + c] * w;
+            }
+#pragma unroll
+            for (int r = 0; r < kNcTR; ++r) {
+                float v = acc[r];
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0 && r < nr) dh[(r0 + r) * d + k] = v;
+            }
+        }
+        __syncthreads();
+    }
+    // batch mean: block partial, the last block adds the partials in block order
+    if (lane == 0) wsum[warp] = mine;
+    __syncthreads();
+    if (tid == 0) {
+        float b = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += wsum[w];
+        part[blockIdx.x] = b;
+        __threadfence();
+        last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && tid < 32) {
+        __threadfence();
+        float tot = 0.f;
+        for (unsigned b = tid; b < gridDim.x; b += 32) tot += ((volatile float*)part)[b];
+        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (tid == 0) {
+            *loss = tot / (float)n;
+            *ticket = 0u;
+        }
+    }
+}
+
+// dWc[k][c] += sum over a row chunk of h[r][k] * dl[r][c] (k-tile of 16 x row chunk per block;
+// thread per class column), dbc[c] += sum over the chunk of dl[r][c] (k-tile 0 blocks)
+constexpr int kNcKT = 16, kNcRC = 128;
+__global__ void __launch_bounds__(256) nc_dwc_kernel(const float* __restrict__ h, int64_t n, int d,
+                                                     const float* __restrict__ dl, int64_t ldl, int C,
+                                                     float* __restrict__ dWc, float* __restrict__ dbc) {
+    GSB_PDL_ENTRY();
+    __shared__ float shk[kNcRC][kNcKT];
+    const int nkt = (d + kNcKT - 1) / kNcKT;
+    const int kt = blockIdx.x % nkt;
+    const int64_t r0 = (int64_t)(blockIdx.x / nkt) * kNcRC;
+    const int k0 = kt * kNcKT;
+    const int nr = (int)min((int64_t)kNcRC, n - r0);
+    for (int x = threadIdx.x; x < kNcRC * kNcKT; x += blockDim.x) {
+        const int r = x / kNcKT, k = x - r * kNcKT;
+        shk[r][k] = (r < nr && k0 + k < d) ? h[(r0 + r) * d + k0 + k] : 0.f;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        float acc[kNcKT];
+#pragma unroll
+        for (int k = 0; k < kNcKT; ++k) acc[k] = 0.f;
+        float sb = 0.f;
+#pragma unroll 8
+        for (int r = 0; r < nr; ++r) {
+            const float g = dl[(r0 + r) * ldl + c];
+            sb += g;
+#pragma unroll
+            for (int k = 0; k < kNcKT; ++k) acc[k] += shk[r][k] * g;
+        }
+#pragma unroll
+        for (int k = 0; k < kNcKT; ++k)
+            if (k0 + k < d) atomicAdd(dWc + (int64_t)(k0 + k) * C + c, acc[k]);
+        if (kt == 0) atomicAdd(dbc + c, sb);
     }
 }
 
@@ -754,9 +984,16 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         gsb_status st = launch_gemm<UMMA_NT>(lname("rgcn_gemm_dA", layer), P, tiles, hb.cap_dst, d_out,
                                              (int64_t)(g.R + 1) * d_in, d_out, s);
         if (st != GSB_OK) return st;
-        GSB_CUDA(cudaMemsetAsync(dh_src, 0, sizeof(float) * (size_t)hb.cap_src * d_in, s));
-        GSB_LAUNCH(lname("rgcn_scatter", layer), scatter_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0, s, g,
-                   hb.meta, hb.seg_ptr, hb.e_src, dacat_ws, lda, d_in, dh_src);
+        // deterministic gather scatter through the transposed CSR when the sampler built it
+        // (GSB_TCSR=1; bit-reproducible but slower here: profiles/round2_decoder_scatter.md)
+        if (hb.t_ptr && d_in <= 512 && d_in % 4 == 0) {
+            GSB_LAUNCH(lname("rgcn_scatter", layer), scatter_t_kernel, grid_for(hb.cap_src * 32, 256, kNumSMs * 8), 256,
+                       0, s, g, hb.meta, hb.t_key, hb.t_ptr, hb.t_val, dacat_ws, lda, d_in, dh_src);
+        } else {
+            GSB_CUDA(cudaMemsetAsync(dh_src, 0, sizeof(float) * (size_t)hb.cap_src * d_in, s));
+            GSB_LAUNCH(lname("rgcn_scatter", layer), scatter_kernel, grid_for(hb.cap_dst * 32, 256, kNumSMs * 8), 256, 0,
+                       s, g, hb.meta, hb.seg_ptr, hb.e_src, dacat_ws, lda, d_in, dh_src);
+        }
     }
     return fork_end(s_main, s_side);
 }
@@ -798,6 +1035,26 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
     cudaStream_t s = (cudaStream_t)stream;
     RowGroups rg = single_group(n);
     const int64_t ldl = (C + 3) / 4 * 4;   // padded logits row (16-B aligned rows)
+    // fused SIMT decoder: opt-in (GSB_NC=fused); measured slower than the tcgen05 GEMMs + CE on the
+    // mag step (69.6 + 45.8 us vs 16.4 + 9.8 + 20.3 || 16.4 us, profiles/round2_decoder_scatter.md)
+    static const bool nc_fused = getenv("GSB_NC") && strcmp(getenv("GSB_NC"), "fused") == 0;
+    const size_t fsm = sizeof(float) * (size_t)kNcTR * (d + ldl);
+    if (nc_fused && fsm <= 48 * 1024) {
+        float* part = row_loss_ws + ((n + 31) / 32) * 32;
+        unsigned* ticket = reinterpret_cast<unsigned*>(part + kNumSMs * 4);
+        const int grid = (int)std::min<int64_t>((n + kNcTR - 1) / kNcTR, kNumSMs * 4);
+        GSB_LAUNCH("nc_fused", nc_fused_kernel, grid, 256, fsm, s, h, n, d, Wc, bc, C, ldl, labels, seed_gid,
+                   label_gid_base, logits_ws, row_loss_ws, part, ticket, loss, dh);
+        if (dWc || dbc) {
+            GSB_CHECK_ARG(dWc && dbc, "dWc and dbc go together");
+            GSB_CUDA(cudaMemsetAsync(dWc, 0, sizeof(float) * (size_t)d * C, s));
+            GSB_CUDA(cudaMemsetAsync(dbc, 0, sizeof(float) * (size_t)C, s));
+            const int nkt = (d + kNcKT - 1) / kNcKT;
+            GSB_LAUNCH("nc_dwc", nc_dwc_kernel, (int)(nkt * ((n + kNcRC - 1) / kNcRC)), 256, 0, s, h, n, d, logits_ws,
+                       ldl, C, dWc, dbc);
+        }
+        return GSB_OK;
+    }
     {
         UProb P{};
         P.rg = rg; P.A = h; P.lda = d; P.B = Wc; P.ldb = C; P.bslot = 0; P.d_in = d; P.N = C; P.C = logits_ws;

@@ -259,7 +259,8 @@ constexpr int kScanPerBlock = kCntPer;   // count chunks (multiples of kCntThrea
 
 __device__ __forceinline__ int64_t count_one(const GraphDev& g, int64_t i, int64_t n, int S,
                                              const int64_t* __restrict__ dst_gid, int fanout, const Excl& ex,
-                                             int32_t* __restrict__ map, int* __restrict__ err) {
+                                             int32_t* __restrict__ map, int* __restrict__ err,
+                                             CscSeg* __restrict__ segc) {
     const int64_t j = i / S;
     const int s = (int)(i - j * S);
     if (j >= n) return 0;
@@ -273,6 +274,7 @@ __device__ __forceinline__ int64_t count_one(const GraphDev& g, int64_t i, int64
     const int r = g.slot_etype[t][s];
     const int64_t vl = v - g.node_off[t];
     const CscSeg cs = csc_seg(g, r, t, vl);
+    if (segc) segc[i] = cs;     // fill reads the resolved segment here (a remote one: no second NVLink trip)
     int64_t deg = cs.deg;
     int64_t k0, k1;
     excl_range(ex, r, v, k0, k1);
@@ -297,7 +299,8 @@ __global__ void __launch_bounds__(kCntThreads) count_kernel(GraphDev g, const Ho
                                                             const int64_t* __restrict__ dst_gid, int64_t cap_dst,
                                                             int fanout, Excl ex, int32_t* __restrict__ map,
                                                             int64_t* __restrict__ cnt, int64_t chunk,
-                                                            int64_t* __restrict__ btot, int* __restrict__ err) {
+                                                            int64_t* __restrict__ btot, int* __restrict__ err,
+                                                            CscSeg* __restrict__ segc) {
     GSB_PDL_ENTRY();
     __shared__ int64_t red[kCntThreads / 32];
     const int S = g.S;
@@ -306,7 +309,7 @@ __global__ void __launch_bounds__(kCntThreads) count_kernel(GraphDev g, const Ho
     const int64_t i0 = blockIdx.x * chunk, i1 = min(i0 + chunk, total + 1);
     int64_t sum = 0;
     for (int64_t i = i0 + threadIdx.x; i < i1; i += kCntThreads) {
-        const int64_t c = (i == total) ? 0 : count_one(g, i, n, S, dst_gid, fanout, ex, map, err);
+        const int64_t c = (i == total) ? 0 : count_one(g, i, n, S, dst_gid, fanout, ex, map, err, segc);
         cnt[i] = c;
         sum += c;
     }
@@ -390,7 +393,8 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
                                                    const int32_t* __restrict__ map, uint32_t* __restrict__ bitmap,
                                                    int64_t* __restrict__ e_src_gid, int64_t* __restrict__ e_eid,
                                                    const int* __restrict__ err, int64_t cap,
-                                                   const int64_t* __restrict__ xoff, int xworld, int xrank) {
+                                                   const int64_t* __restrict__ xoff, int xworld, int xrank,
+                                                   const CscSeg* __restrict__ segc) {
     GSB_PDL_ENTRY();
     const int S = g.S;
     const int lane = threadIdx.x & 31;
@@ -418,7 +422,7 @@ __global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __
         const int t = type_of(g, v);
         const int r = g.slot_etype[t][s];
         const int64_t vl = v - g.node_off[t];
-        const CscSeg cs = csc_seg(g, r, t, vl);
+        const CscSeg cs = segc ? segc[i] : csc_seg(g, r, t, vl);
         const int64_t deg = cs.deg;
         const int32_t* seg = cs.seg;
         const int64_t src_off = g.node_off[g.src_t[r]];
@@ -539,6 +543,50 @@ __global__ void __launch_bounds__(256) fill_tail_kernel(GraphDev g, const HopMet
             }
             if (i == ib) break;
         }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Transposed (by-source) CSR of a block (§8(a) a4): the backward scatter of a hidden layer
+// then gathers, per source row, its edges' contributions in ascending edge order -- plain
+// stores, no atomics, no memset, bit-reproducible (SPEC S:L281-284 by-src CSR).
+// ------------------------------------------------------------------------------------
+__global__ void tcsr_prep_kernel(const HopMeta* __restrict__ m, const int64_t* __restrict__ seg_ptr, int S,
+                                 const int32_t* __restrict__ e_src, int64_t cap_edges, int32_t* __restrict__ e_seg,
+                                 int32_t* __restrict__ key, int32_t* __restrict__ val) {
+    GSB_PDL_ENTRY();
+    const int64_t E = m->n_edges, nseg = m->n_dst * S;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cap_edges; e += stride) {
+        key[e] = e < E ? e_src[e] : INT32_MAX;
+        val[e] = (int32_t)e;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseg; i += stride)
+        for (int64_t e = seg_ptr[i]; e < seg_ptr[i + 1]; ++e) e_seg[e] = (int32_t)i;
+}
+
+// t_ptr over the sorted keys; per transposed position k the edge's segment id (t_seg, in the
+// freed key buffer) and 1 / its segment count (t_inv, in the freed value buffer), so the
+// scatter's only dependent load is the gradient row
+__global__ void tcsr_ptr_kernel(const HopMeta* __restrict__ m, const int32_t* __restrict__ key, int64_t cap_src,
+                                int32_t* __restrict__ t_ptr, const int32_t* __restrict__ t_edge,
+                                const int32_t* __restrict__ e_seg, const int64_t* __restrict__ seg_ptr,
+                                int32_t* __restrict__ t_seg, int32_t* __restrict__ t_inv) {
+    GSB_PDL_ENTRY();
+    const int64_t E = m->n_edges;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u <= cap_src; u += stride) {
+        int64_t lo = 0, hi = E;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (key[mid] < u) lo = mid + 1; else hi = mid;
+        }
+        t_ptr[u] = (int32_t)lo;
+    }
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += stride) {
+        const int32_t i = e_seg[t_edge[k]];
+        t_seg[k] = i;
+        t_inv[k] = __float_as_int(1.f / (float)(seg_ptr[i + 1] - seg_ptr[i]));
     }
 }
 
@@ -913,6 +961,18 @@ HopBufs Blocks::hop(int h, void* arena) const {
     b.e_eid = at<int64_t>(arena, off_eeid[h]);
     b.e_src = at<int32_t>(arena, off_esrc[h]);
     b.src_gid = at<int64_t>(arena, off_src[h]);
+    b.segc = at<CscSeg>(arena, off_segc[h]);
+    if (off_tcsr[h]) {
+        int32_t* t = at<int32_t>(arena, off_tcsr[h]);
+        b.e_seg = t;
+        b.t_key = t + cap_edges[h];
+        b.t_key2 = t + 2 * cap_edges[h];
+        b.t_val = t + 3 * cap_edges[h];
+        b.t_edge = t + 4 * cap_edges[h];
+        b.t_ptr = t + 5 * cap_edges[h];
+    } else {
+        b.e_seg = b.t_key = b.t_key2 = b.t_val = b.t_edge = b.t_ptr = nullptr;
+    }
     return b;
 }
 
@@ -962,7 +1022,7 @@ static gsb_status exchange_hop(Blocks* B, const gsb_sample_args* a, const HopBuf
         const int nbs = (int)ceil_div(sseg + 1, chunk * kScanPerBlock);
         int64_t* btot = x.srv_cnt + sseg + 1;
         GSB_LAUNCH("x_serve_count", count_kernel, nb, kCntThreads, 0, s, g, x.srv_meta, x.req_recv, n_recv, f, ex0,
-                   (int32_t*)nullptr, x.srv_cnt, chunk, btot, err);
+                   (int32_t*)nullptr, x.srv_cnt, chunk, btot, err, (CscSeg*)nullptr);
         GSB_LAUNCH("x_serve_scan", count_scan_kernel, nbs, kCntThreads, 0, s, x.srv_cnt, sseg + 1,
                    chunk * kScanPerBlock, btot, nb, x.srv_seg);
         const int G = f <= 8 ? 8 : (f <= 16 ? 16 : 32);
@@ -970,7 +1030,7 @@ static gsb_status exchange_hop(Blocks* B, const gsb_sample_args* a, const HopBuf
 #define GSB_XFILL(GG)                                                                                            \
     GSB_LAUNCH("x_serve_fill", fill_kernel<GG>, grid, 256, 0, s, g, x.srv_meta, x.req_recv, n_recv, x.srv_seg, f,   \
                ex0, rng_seed, a->step, a->step_dev, h, (const int32_t*)nullptr, (uint32_t*)nullptr, x.srv_gid,     \
-               x.srv_eid, err, INT64_MAX, (const int64_t*)x.xoff, x.world, x.rank)
+               x.srv_eid, err, INT64_MAX, (const int64_t*)x.xoff, x.world, x.rank, (const CscSeg*)nullptr)
         if (G == 8) GSB_XFILL(8);
         else if (G == 16) GSB_XFILL(16);
         else GSB_XFILL(32);
@@ -1046,6 +1106,11 @@ gsb_status gsb_blocks_create(gsb_graph_t gh, int32_t L, const int32_t* fanouts, 
         cub::DeviceScan::ExclusiveSum(nullptr, t, (int64_t*)nullptr, (int64_t*)nullptr, (int64_t)(2 * max_excl + 1));
         cb = std::max(cb, t);
     }
+    for (int h = 1; h < L; ++h) {
+        cub::DeviceRadixSort::SortPairs(nullptr, t, (const int32_t*)nullptr, (int32_t*)nullptr, (const int32_t*)nullptr,
+                                        (int32_t*)nullptr, (int64_t)B->cap_edges[h], 0, 31);
+        cb = std::max(cb, t);
+    }
     B->cub_bytes = cb;
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -1064,6 +1129,12 @@ gsb_status gsb_blocks_create(gsb_graph_t gh, int32_t L, const int32_t* fanouts, 
         B->off_esrcgid[h] = take(sizeof(int64_t) * B->cap_edges[h]);
         B->off_eeid[h] = take(sizeof(int64_t) * B->cap_edges[h]);
         B->off_esrc[h] = take(sizeof(int32_t) * B->cap_edges[h]);
+        B->off_segc[h] = take(sizeof(CscSeg) * (nseg - 1 > 0 ? nseg - 1 : 1));
+        B->off_tcsr[h] = 0;
+        static const bool tcsr = getenv("GSB_TCSR") && atoi(getenv("GSB_TCSR")) == 1;   // opt-in (see layer.cu)
+        if (tcsr && h < L) {   // layers >= 1 scatter their input gradient through the transposed CSR
+            B->off_tcsr[h] = take(sizeof(int32_t) * (5 * B->cap_edges[h] + B->cap_dst[h + 1] + 1));
+        }
         B->off_src[h] = take(sizeof(int64_t) * B->cap_dst[h + 1]);
     }
     B->off_map = take(sizeof(int32_t) * G->total_nodes);
@@ -1186,7 +1257,7 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
             const int nbs = (int)ceil_div(nseg + 1, schunk);
             int64_t* btot = hb.cnt + nseg + 1;
             GSB_LAUNCH("sample_count", count_kernel, nb, kCntThreads, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst, f, ex,
-                       map, hb.cnt, chunk, btot, err);
+                       map, hb.cnt, chunk, btot, err, hb.segc);
             GSB_LAUNCH("sample_scan", count_scan_kernel, nbs, kCntThreads, 0, s, hb.cnt, nseg + 1, schunk, btot, nb,
                        hb.seg_ptr);
         }
@@ -1198,15 +1269,15 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
             if (G == 8)
                 GSB_LAUNCH("sample_fill", fill_kernel<8>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
                            hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
-                           err, cap, (const int64_t*)nullptr, 1, 0);
+                           err, cap, (const int64_t*)nullptr, 1, 0, (const CscSeg*)hb.segc);
             else if (G == 16)
                 GSB_LAUNCH("sample_fill", fill_kernel<16>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
                            hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
-                           err, cap, (const int64_t*)nullptr, 1, 0);
+                           err, cap, (const int64_t*)nullptr, 1, 0, (const CscSeg*)hb.segc);
             else
                 GSB_LAUNCH("sample_fill", fill_kernel<32>, grid, 256, 0, s, g, hb.meta, hb.dst_gid, hb.cap_dst,
                            hb.seg_ptr, f, ex, rng_seed, a->step, a->step_dev, h, map, bitmap, hb.e_src_gid, hb.e_eid,
-                           err, cap, (const int64_t*)nullptr, 1, 0);
+                           err, cap, (const int64_t*)nullptr, 1, 0, (const CscSeg*)hb.segc);
             if (tail)
                 GSB_LAUNCH("sample_fill_tail", fill_tail_kernel, kNumSMs * 8, 256, 0, s, g, hb.meta, hb.dst_gid,
                            hb.seg_ptr, ex, map, bitmap, hb.e_src_gid, hb.e_eid, err);
@@ -1225,6 +1296,16 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
                    hb.cap_src, err);
         GSB_LAUNCH("relabel", relabel_kernel, grid_for(hb.cap_edges, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
                    hb.e_src_gid, map, bitmap, wrank, hb.e_src);
+        if (hb.t_ptr) {
+            GSB_LAUNCH("tcsr_prep", tcsr_prep_kernel, grid_for(hb.cap_edges, 256, kNumSMs * 4), 256, 0, s, hb.meta,
+                       hb.seg_ptr, S, hb.e_src, hb.cap_edges, hb.e_seg, hb.t_key, hb.t_val);
+            size_t cb = B->cub_bytes;
+            GSB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cb, hb.t_key, hb.t_key2, hb.t_val, hb.t_edge,
+                                                     (int64_t)hb.cap_edges, 0, 31, s));
+            count_launch(8);
+            GSB_LAUNCH("tcsr_ptr", tcsr_ptr_kernel, grid_for(hb.cap_src + 1, 256, kNumSMs * 4), 256, 0, s, hb.meta,
+                       hb.t_key2, hb.cap_src, hb.t_ptr, hb.t_edge, hb.e_seg, hb.seg_ptr, hb.t_key, hb.t_val);
+        }
         GSB_LAUNCH("next_frontier", next_frontier_kernel,
                    grid_for(std::max(hb.cap_dst, B->n_words), 256, kNumSMs * 8), 256, 0, s, g, hb.meta, hb.dst_gid,
                    map, bitmap, wrank, B->n_words, hb.cap_src, hb.src_gid);
