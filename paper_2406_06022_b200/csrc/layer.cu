@@ -1037,7 +1037,7 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
     const int64_t ldl = (C + 3) / 4 * 4;   // padded logits row (16-B aligned rows)
     // fused SIMT decoder: opt-in (GSB_NC=fused); measured slower than the tcgen05 GEMMs + CE on the
     // mag step (69.6 + 45.8 us vs 16.4 + 9.8 + 20.3 || 16.4 us, profiles/round2_decoder_scatter.md)
-    static const bool nc_fused = getenv("GSB_NC") && strcmp(getenv("GSB_NC"), "fused") == 0;
+    const bool nc_fused = getenv("GSB_NC") && strcmp(getenv("GSB_NC"), "fused") == 0;
     const size_t fsm = sizeof(float) * (size_t)kNcTR * (d + ldl);
     if (nc_fused && fsm <= 48 * 1024) {
         float* part = row_loss_ws + ((n + 31) / 32) * 32;

@@ -1131,7 +1131,7 @@ gsb_status gsb_blocks_create(gsb_graph_t gh, int32_t L, const int32_t* fanouts, 
         B->off_esrc[h] = take(sizeof(int32_t) * B->cap_edges[h]);
         B->off_segc[h] = take(sizeof(CscSeg) * (nseg - 1 > 0 ? nseg - 1 : 1));
         B->off_tcsr[h] = 0;
-        static const bool tcsr = getenv("GSB_TCSR") && atoi(getenv("GSB_TCSR")) == 1;   // opt-in (see layer.cu)
+        const bool tcsr = getenv("GSB_TCSR") && atoi(getenv("GSB_TCSR")) == 1;   // opt-in (see layer.cu)
         if (tcsr && h < L) {   // layers >= 1 scatter their input gradient through the transposed CSR
             B->off_tcsr[h] = take(sizeof(int32_t) * (5 * B->cap_edges[h] + B->cap_dst[h + 1] + 1));
         }

@@ -430,3 +430,29 @@ def test_gcn_homogeneous_step_parity(torch_cuda):
             close(tr.hout[l][:nd].cpu().numpy(), res.hs[l], what=f"gcn step {step} h{l}")
         close(tr.loss.cpu().numpy()[0], res.loss, what="gcn loss")
         check_grads(tr, res, cfg, step)
+
+
+@pytest.mark.parametrize("knob", ["GSB_TCSR", "GSB_NC"])
+def test_optin_paths_parity(torch_cuda, knob, monkeypatch):
+    """The opt-in paths keep parity: GSB_TCSR=1 (by-source transposed CSR per block + the
+    deterministic gather scatter of the hidden layer's input gradient, §8(a) a4) and GSB_NC=fused
+    (the fused SIMT decoder: logits, softmax-CE, dh, dWc, dbc)."""
+    import torch
+    monkeypatch.setenv(knob, "1" if knob == "GSB_TCSR" else "fused")
+    cfg = CASES["mag_small"]()
+    st, og = gpu_store(cfg), oracle_graph(cfg)
+    tr = _gpu_trainer(cfg, st)
+    params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
+    for step in (0, 2):
+        seeds = synth.nc_seeds(cfg, step)
+        tr.forward_backward(torch_cuda.from_numpy(seeds).cuda(), step)
+        res = oracle.nc_step(og, params, seeds, synth.labels(cfg), step, cfg.rng_seed)
+        close(tr.loss.cpu().numpy()[0], res.loss, what=f"{knob} loss")
+        check_grads(tr, res, cfg, step)
+        if knob == "GSB_TCSR":    # the scatter's output: layer 1's input gradient, ReLU-masked in place
+            z = res.zs[0]            # by layer 0's backward; ambiguous units (|z| ~ 0) left out (R-relutie)
+            n0 = z.shape[0]
+            keep = np.abs(z) > 1e-5 * np.abs(z).max()
+            exp = np.where(z > 0, res.extra["dh"][0], 0.0)
+            got = tr.dh[0][:n0].cpu().numpy()
+            close(got[keep], exp[keep], what="dh0 via the transposed CSR")
