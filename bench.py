@@ -36,8 +36,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="gsb", choices=["gsb", "reference"])
-    ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b", "gcn_1b", "amazon_lp", "tiny_lp",
-                                                        "mag240m", "mag240m_1_16"])
+    ap.add_argument("--config", default="mag", choices=["mag", "tiny", "synth_1b", "synth_10b", "gcn_1b", "amazon_lp",
+                                                        "tiny_lp", "mag240m", "mag240m_1_16"])
     ap.add_argument("--feat-dtype", default="auto", choices=["auto", "f32", "bf16"],
                     help="feature storage type; compute stays fp32 (auto: bf16 for the large configs, as "
                          "SURVEY §8(d) plans, fp32 for tiny)")
@@ -278,14 +278,34 @@ def build_gsb(cfg, device, partition=None, mode="peer", topology="replicate", sa
         from paper_2406_06022_b200.dist import balanced_bounds
         pb = balanced_bounds(cfg.counts, partition[0])
     for r in range(cfg.num_etypes):
-        s, d = synth.etype_coo(cfg, r, backend="torch", device=device)
-        if part_topo:
+        if part_topo and keep is None:
+            # synthetic input generation in edge chunks, keeping this rank's dst range only (a
+            # rank never holds the whole COO: 2.16B edges for MAG240M, 10B for synth_10b); the
+            # global CSC position of the range's first edge = the edges with a smaller dst
+            t = int(cfg.etypes[r].dst)
+            lo, hi = int(pb[t][partition[1]]), int(pb[t][partition[1] + 1])
+            E = cfg.etypes[r if cfg.etypes[r].reverse_of is None else cfg.etypes[r].reverse_of].num_edges
+            ss, dd, before = [], [], 0
+            for a in range(0, E, 1 << 28):
+                s, d = synth.etype_coo(cfg, r, backend="torch", device=device, lo=a, hi=min(E, a + (1 << 28)))
+                m = (d >= lo) & (d < hi)
+                before += int((d < lo).sum().item())
+                ss.append(s[m])
+                dd.append(d[m])
+                del s, d, m
+            s, d = torch.cat(ss), torch.cat(dd)
+            del ss, dd
+            st.load_etype_range(r, s, d, lo, hi, eid_base=before)
+        elif part_topo:
+            s, d = synth.etype_coo(cfg, r, backend="torch", device=device)
             t = int(cfg.etypes[r].dst)
             st.load_etype_range(r, s, d, int(pb[t][partition[1]]), int(pb[t][partition[1] + 1]),
                                 None if keep is None else keep.get(r))
         else:
+            s, d = synth.etype_coo(cfg, r, backend="torch", device=device)
             st.load_etype(r, s, d, None if keep is None else keep.get(r))
         del s, d
+        torch.cuda.empty_cache()
     if part_topo:
         from paper_2406_06022_b200.dist import PeerCSC
         st._peer_csc = PeerCSC(st, partition[0], partition[1], pb, map_peers=(sampling == "peer"))
@@ -833,7 +853,8 @@ def main():
     if out is None:
         return
     line, st, tr = out
-    if not args.no_cpu_baseline and cfg.task == "nc":
+    # the oracle baseline: rank 0 at N=1 only, and only where the oracle can hold the graph
+    if not args.no_cpu_baseline and cfg.task == "nc" and dist_env()[0] == 1 and cfg.num_edges <= 200_000_000:
         del tr, st
         import torch
         torch.cuda.empty_cache()

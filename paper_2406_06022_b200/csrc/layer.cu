@@ -255,6 +255,148 @@ static gsb_status launch_agg_seg(const char* name, cudaStream_t s, const GraphDe
     return GSB_OK;
 }
 
+// ------------------------------------------------------------------------------------
+// aggregation, row-streaming (default for layer 0): warp per dst row, the whole warp on one
+// source row at a time (lane = row_bytes / 32 bytes of it: 8 B = 4 bf16 of a 128-d bf16 row),
+// U source rows in flight.  A row's edges of all its slots are contiguous, [seg_ptr[j*S],
+// seg_ptr[j*S + St]), so one coalesced key load per 32 edges and one stream of row loads
+// cover every slot; the slot boundary is warp-uniform, so a finished slot's mean is stored
+// (16 B per lane) without any cross-lane reduction, and empty slots cost one store.
+// ------------------------------------------------------------------------------------
+template <int BPL>
+struct LaneChunk;                       // BPL bytes of a row per lane
+template <>
+struct LaneChunk<4> { using T = uint32_t; };
+template <>
+struct LaneChunk<8> { using T = uint2; };
+template <>
+struct LaneChunk<16> { using T = uint4; };
+
+template <bool BF16, int BPL>
+__device__ __forceinline__ void lane_acc(float* acc, const typename LaneChunk<BPL>::T& x) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&x);
+#pragma unroll
+    for (int i = 0; i < BPL / 4; ++i) {
+        if (BF16) {
+            acc[2 * i] += bf16_lo(w[i]);
+            acc[2 * i + 1] += bf16_hi(w[i]);
+        } else {
+            acc[i] += __uint_as_float(w[i]);
+        }
+    }
+}
+
+template <bool FEAT, bool BF16, int BPL>
+__global__ void __launch_bounds__(256, 4) agg_row_kernel(GraphDev g, const HopMeta* __restrict__ m,
+                                                      const int64_t* __restrict__ seg_ptr,
+                                                      const int32_t* __restrict__ e_src,
+                                                      const int64_t* __restrict__ e_src_gid,
+                                                      const int64_t* __restrict__ dst_gid, const char* __restrict__ h,
+                                                      int row_bytes, int d, float* __restrict__ acat, int64_t lda,
+                                                      const int32_t* __restrict__ rowmap, int64_t seg_cap) {
+    GSB_PDL_ENTRY();
+    using CT = typename LaneChunk<BPL>::T;
+    constexpr int V = BF16 ? BPL / 2 : BPL / 4;      // floats per lane
+    constexpr int U = 8;                              // source rows in flight
+    __shared__ int64_t s_dst_off[kMaxT + 1], s_src_off[kMaxT + 1];
+    if (threadIdx.x <= (unsigned)g.T) {
+        s_dst_off[threadIdx.x] = m->dst_off[threadIdx.x];
+        s_src_off[threadIdx.x] = m->src_off[threadIdx.x];
+    }
+    const int64_t n = m->n_dst;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int S = g.S;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < n; j += warps) {
+        int t = 0;
+        for (int k = 1; k < g.T; ++k) t += (j >= s_dst_off[k]) ? 1 : 0;
+        const int St = g.n_slots[t];
+        float* out = acat + j * lda + lane * V;
+        const int64_t bl = (lane <= St) ? seg_ptr[j * S + lane] : 0;    // slot boundaries
+        const int64_t E0 = __shfl_sync(0xffffffffu, bl, 0), E1 = __shfl_sync(0xffffffffu, bl, St);
+        // the self row's chunk, loaded while the edges stream
+        const char* ps = reinterpret_cast<const char*>(
+            src_row<FEAT>(g, h, row_bytes, FEAT ? dst_gid[j] : s_src_off[t] + (j - s_dst_off[t]), rowmap));
+        const CT xs = *reinterpret_cast<const CT*>(ps + lane * BPL);
+        int slot = 0;
+        int64_t b0 = E0, b1 = __shfl_sync(0xffffffffu, bl, 1);   // current slot [b0, b1)
+        float acc[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = 0.f;
+        auto flush = [&]() {    // mean of slot `slot` (warp-uniform), then the next slot
+            const float inv = (b1 > b0) ? 1.f / (float)(b1 - b0) : 0.f;
+            float* o = out + (int64_t)slot * d;
+#pragma unroll
+            for (int v = 0; v < V; v += 4)
+                if (v + 3 < V) *reinterpret_cast<float4*>(o + v) = make_float4(acc[v] * inv, acc[v + 1] * inv,
+                                                                               acc[v + 2] * inv, acc[v + 3] * inv);
+                else
+                    for (int q = v; q < V; ++q) o[q] = acc[q] * inv;
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] = 0.f;
+            ++slot;
+            b0 = b1;
+            b1 = __shfl_sync(0xffffffffu, bl, min(slot + 1, St));
+        };
+        while (slot < St && b1 == b0) flush();            // leading empty slots
+        for (int64_t cb = E0; cb < E1; cb += 32) {
+            const int64_t ek = cb + lane;
+            const char* pk = (ek < E1) ? reinterpret_cast<const char*>(src_row<FEAT>(
+                                             g, h, row_bytes, FEAT ? e_src_gid[ek] : (int64_t)e_src[ek], rowmap))
+                                       : nullptr;
+            const int cnt = (int)min((int64_t)32, E1 - cb);
+            for (int k = 0; k < cnt; k += U) {
+                CT x[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint64_t pu = __shfl_sync(0xffffffffu, (uint64_t)pk, (k + u) & 31);
+                    if (k + u < cnt) x[u] = __ldg(reinterpret_cast<const CT*>(pu + lane * BPL));
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (k + u < cnt) {
+                        // a long segment is capped (fanout ALL hubs): heavy_kernel adds the tail
+                        if (cb + k + u - b0 < seg_cap) lane_acc<BF16, BPL>(acc, x[u]);
+                        if (cb + k + u + 1 == b1)
+                            do flush(); while (slot < St && b1 == b0);
+                    }
+                }
+            }
+        }
+        while (slot < St) flush();                          // trailing empty slots
+        float r[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) r[v] = 0.f;
+        lane_acc<BF16, BPL>(r, xs);
+        float* o = out + (int64_t)St * d;
+#pragma unroll
+        for (int v = 0; v < V; v += 4)
+            if (v + 3 < V) *reinterpret_cast<float4*>(o + v) = make_float4(r[v], r[v + 1], r[v + 2], r[v + 3]);
+            else
+                for (int q = v; q < V; ++q) o[q] = r[q];
+    }
+}
+
+template <bool FEAT, bool BF16>
+static gsb_status launch_agg_row(const char* name, cudaStream_t s, const GraphDev& g, const HopBufs& hb, const char* h,
+                                 int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap,
+                                 int64_t seg_cap) {
+    static const int bps = getenv("GSB_AGG_BPS") ? atoi(getenv("GSB_AGG_BPS")) : 4;   // one wave at 4 blocks / SM
+    const int grid = grid_for(hb.cap_dst * 32, 256, kNumSMs * bps);
+    const int bpl = row_bytes / 32;
+    if (bpl == 4)
+        GSB_LAUNCH(name, (agg_row_kernel<FEAT, BF16, 4>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,
+                   hb.e_src_gid, hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
+    else if (bpl == 8)
+        GSB_LAUNCH(name, (agg_row_kernel<FEAT, BF16, 8>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,
+                   hb.e_src_gid, hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
+    else
+        GSB_LAUNCH(name, (agg_row_kernel<FEAT, BF16, 16>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,
+                   hb.e_src_gid, hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
+    return GSB_OK;
+}
+
 template <bool FEAT, bool BF16>
 static gsb_status launch_agg_lpe(const char* name, int grid, cudaStream_t s, const GraphDev& g, const HopBufs& hb,
                                  const char* h, int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap,
@@ -395,11 +537,24 @@ static gsb_status launch_agg(const char* name, bool feat, int dtype, cudaStream_
     // mag step); the layer-0 feature gather keeps the warp-per-row kernel, whose per-warp
     // address resolution beats the per-lane one there (profiles/round2_agg_ab.md).  GSB_AGG=warp /
     // seg forces either (A/B).  32-byte lanes: rows of 4..32 such chunks, 32-B aligned.
-    static const int agg_mode = !getenv("GSB_AGG") ? 0 : (strcmp(getenv("GSB_AGG"), "warp") == 0 ? 1 : 2);
+    const char* am = getenv("GSB_AGG");
+    static const int agg_mode = !am ? 0 : (strcmp(am, "warp") == 0 ? 1 : (strcmp(am, "seg") == 0 ? 2 : 3));
     const bool want_seg = agg_mode == 2 || (agg_mode == 0 && !feat);
     const bool use_seg = want_seg && rb % 32 == 0 && rb / 32 >= 4 && rb / 32 <= 32 && d % 4 == 0 &&
                          (feat || (reinterpret_cast<uintptr_t>(h) & 31) == 0);
-    if (use_seg) {
+    // row-streaming kernel: opt-in (GSB_AGG=row); on the mag step's layer 0 it measured 44.0 us vs
+    // 35.9 for the warp kernel (profiles/round2_agg_ab.md)
+    const bool want_row = agg_mode == 3;
+    const bool use_row = want_row && !use_seg && (rb == 128 || rb == 256 || rb == 512) && d % 4 == 0 &&
+                         (feat || (reinterpret_cast<uintptr_t>(h) & 15) == 0);
+    if (use_row) {
+        if (feat)
+            st = dtype == GSB_BF16 ? launch_agg_row<true, true>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
+                                   : launch_agg_row<true, false>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
+        else
+            st = dtype == GSB_BF16 ? launch_agg_row<false, true>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
+                                   : launch_agg_row<false, false>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
+    } else if (use_seg) {
         if (feat)
             st = dtype == GSB_BF16 ? launch_agg_seg<true, true>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
                                    : launch_agg_seg<true, false>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);

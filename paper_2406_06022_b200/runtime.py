@@ -104,10 +104,11 @@ class GraphStore:
         self.n_edges[r] = int(kept.value)
 
     def load_etype_range(self, r: int, src: torch.Tensor, dst: torch.Tensor, lo: int, hi: int,
-                         keep: Optional[torch.Tensor] = None):
+                         keep: Optional[torch.Tensor] = None, eid_base: Optional[int] = None):
         """gsb_csc_build_range: this rank's shard of etype r's CSC -- the in-edges of the dst
         local ids [lo, hi) it owns (§8(e), node-ID partition); eid_base = global position of
-        the shard's first edge."""
+        the shard's first edge (counted by the build over the given COO, or given by the caller
+        when the COO passed is already restricted to the range)."""
         s = torch.as_tensor(src, dtype=torch.int32).to(self.device).contiguous()
         d = torch.as_tensor(dst, dtype=torch.int32).to(self.device).contiguous()
         k = None if keep is None else torch.as_tensor(keep, dtype=torch.uint8).to(self.device).contiguous()
@@ -123,6 +124,8 @@ class GraphStore:
              C.byref(kept), C.byref(before), _ptr(ws), ws.numel(), _stream())
         del ws
         indices = indices[:max(int(kept.value), 1)].clone()
+        if eid_base is not None:
+            before = C.c_int64(int(eid_base))
         call("gsb_graph_set_csc", self.h, r, _ptr(indptr), _ptr(indices), int(kept.value), int(before.value))
         self.indptr[r] = indptr
         self.indices[r] = indices

@@ -21,7 +21,7 @@ for r in rows[1:]:
         pass
 agg = collections.defaultdict(lambda: {"bytes": [], "us": []})
 for (_, name), m in per.items():
-    name = name.split("/")[-1].strip()
+    name = name.split("/")[0].strip() if "/" in name.split("(")[0] else name.strip()
     if "dram__bytes_read.sum" not in m:
         continue
     agg[name]["bytes"].append(m["dram__bytes_read.sum"] + m.get("dram__bytes_write.sum", 0.0))

@@ -262,7 +262,7 @@ def with_dtype(cfg: Config, feat_dtype: str) -> Config:
 
 CONFIGS = {"tiny": tiny, "mag": mag, "amazon_lp": amazon_lp, "tiny_lp": tiny_lp,
            "synth_1b": synth_1b, "mag240m": mag240m, "mag240m_1_16": lambda: mag240m(1.0 / 16),
-           "tiny_enc": tiny_enc, "gcn_1b": gcn_1b}
+           "tiny_enc": tiny_enc, "gcn_1b": gcn_1b, "synth_10b": lambda: synth_1b(10.0)}
 
 
 def get(name: str) -> Config:
