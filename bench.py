@@ -98,6 +98,9 @@ def cfg_json(cfg: synth.Config, n_gpus: int, extra=None) -> dict:
          "layers": len(cfg.fanouts), "optimizer": "adam",
          "parallelism": "single" if n_gpus == 1 else f"dp{n_gpus} (graph replicated, NCCL grad all-reduce)",
          "l2": "inputs larger than L2: feature table + CSC >> 126 MB, fresh random seed batch every step"}
+    if getattr(cfg, "feat_dims", None):
+        d["feat_dims"] = list(cfg.feat_dims)        # per ntype stored width (input encoder where projected)
+        d["projected"] = [bool(x) for x in cfg.project]
     if LP_OPTS["learnable_emb"] and any(getattr(cfg, "project", None) or []):
         d["featureless_inputs"] = "learnable tables, sparse Adagrad on touched rows"
     if extra:
