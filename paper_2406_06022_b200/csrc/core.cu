@@ -9,7 +9,7 @@
 
 #include <nvtx3/nvToolsExt.h>
 
-#include "gemm_tma.cuh"
+#include "gemm_tma3.cuh"
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -403,6 +403,24 @@ bool encode_tmap_f32(CUtensorMap* m, const float* base, int64_t width, int64_t r
     const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE,
                           swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool encode_tmap_nd(CUtensorMap* m, const float* base, int rank, const int64_t* dims, const int64_t* strides,
+                    const int* box, int swizzle) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || rank < 2 || rank > 3) return false;
+    cuuint64_t d[3], st[2];
+    cuuint32_t b[3], es[3] = {1, 1, 1};
+    for (int i = 0; i < rank; ++i) {
+        if (dims[i] < 1) return false;
+        d[i] = (cuuint64_t)dims[i];
+        b[i] = (cuuint32_t)box[i];
+    }
+    for (int i = 0; i < rank - 1; ++i) st[i] = (cuuint64_t)strides[i] * sizeof(float);
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<float*>(base), d, st, b, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, (CUtensorMapSwizzle)swizzle,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }

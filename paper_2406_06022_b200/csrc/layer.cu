@@ -1,6 +1,6 @@
 // layer.cu -- RGCN layer forward / backward and the NC decoder + softmax-CE loss.
 // Contract: include/gsb.h "RGCN layer" and "Node-classification decoder".
-#include "gemm_tma.cuh"
+#include "gemm_tma3.cuh"
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -1076,7 +1076,7 @@ gsb_status gsb_rgcn_layer_gemm(gsb_blocks_t b, const void* arena, int32_t layer,
     if (P.ksplit > 1)
         GSB_LAUNCH("zero_rows", zero_rows_kernel, grid_for(hb.cap_dst * d_out, 256, kNumSMs * 4), 256, 0, s, hb.meta,
                    h_dst, (int64_t)d_out);
-    return launch_gemm<UMMA_NN>(lname("rgcn_gemm_fwd", layer), P, tiles, hb.cap_dst, lda, (int64_t)(g.R + 1) * d_in,
+    return launch_gemm_v<UMMA_NN>(lname("rgcn_gemm_fwd", layer), P, tiles, hb.cap_dst, lda, (int64_t)(g.R + 1) * d_in,
                                 d_out, s);
 }
 
@@ -1123,7 +1123,7 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         P.d_in = d_in; P.N = d_out; P.C = dW; P.ldc = d_out; P.bslot = (int64_t)d_in * d_out; P.db = db;
         P.rows_per_chunk = rpc;
         int64_t items = (ceil_div(rows, rpc) + g.T) * (g.S + 1) * ceil_div(d_in, 128) * ceil_div(d_out, 128);
-        gsb_status st = launch_gemm<UMMA_TN>(lname("rgcn_gemm_dW", layer), P, items, hb.cap_dst, lda, hb.cap_dst,
+        gsb_status st = launch_gemm_v<UMMA_TN>(lname("rgcn_gemm_dW", layer), P, items, hb.cap_dst, lda, hb.cap_dst,
                                              d_out, s);
         if (st != GSB_OK) return st;
     }
@@ -1136,7 +1136,7 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
         const int64_t tiles = (ceil_div(hb.cap_dst, 128) + g.T) * ceil_div(d_in, 128) * (g.S + 1);
         P.ksplit = choose_ksplit(tiles, (d_out + 31) / 32, true);
         if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(dacat_ws, 0, sizeof(float) * (size_t)hb.cap_dst * lda, s));
-        gsb_status st = launch_gemm<UMMA_NT>(lname("rgcn_gemm_dA", layer), P, tiles, hb.cap_dst, d_out,
+        gsb_status st = launch_gemm_v<UMMA_NT>(lname("rgcn_gemm_dA", layer), P, tiles, hb.cap_dst, d_out,
                                              (int64_t)(g.R + 1) * d_in, d_out, s);
         if (st != GSB_OK) return st;
         // deterministic gather scatter through the transposed CSR when the sampler built it
@@ -1169,13 +1169,13 @@ gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, i
     if (mode == 0) {            // C[M][N] = A[M][K] B[K][N]
         GSB_CHECK_ARG(K % 32 == 0, "NN needs K %% 32 == 0");
         P.d_in = K; P.N = N;
-        return launch_gemm<UMMA_NN>("gemm_nn", P, ceil_div(M, 128) * ceil_div(N, 128), M, K, K, N, s);
+        return launch_gemm_v<UMMA_NN>("gemm_nn", P, ceil_div(M, 128) * ceil_div(N, 128), M, K, K, N, s);
     } else if (mode == 1) {     // C[M][K] = A[M][N] B[K][N]^T
         P.d_in = K; P.N = N;
-        return launch_gemm<UMMA_NT>("gemm_nt", P, ceil_div(M, 128) * ceil_div(K, 128), M, N, K, N, s);
+        return launch_gemm_v<UMMA_NT>("gemm_nt", P, ceil_div(M, 128) * ceil_div(K, 128), M, N, K, N, s);
     } else if (mode == 2) {     // C[K][N] += A[M][K]^T B[M][N]
         P.d_in = K; P.N = N; P.rows_per_chunk = 128;
-        return launch_gemm<UMMA_TN>("gemm_tn", P, ceil_div(M, 128) * ceil_div(K, 128) * ceil_div(N, 128), M, K, M,
+        return launch_gemm_v<UMMA_TN>("gemm_tn", P, ceil_div(M, 128) * ceil_div(K, 128) * ceil_div(N, 128), M, K, M,
                                     N, s);
     }
     set_error("mode %d not in {0,1,2}", mode);
@@ -1217,7 +1217,7 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         const int64_t tiles = ceil_div(n, 128) * ceil_div(C, 128);
         P.ksplit = choose_ksplit(tiles, d / 32, true);
         if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(logits_ws, 0, sizeof(float) * (size_t)n * ldl, s));
-        gsb_status st = launch_gemm<UMMA_NN>("nc_logits", P, tiles, n, d, d, C, s);
+        gsb_status st = launch_gemm_v<UMMA_NN>("nc_logits", P, tiles, n, d, d, C, s);
         if (st != GSB_OK) return st;
     }
     {
@@ -1238,7 +1238,7 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         UProb P{};
         P.rg = rg; P.A = h; P.lda = d; P.B = logits_ws; P.ldb = ldl; P.d_in = d; P.N = C; P.C = dWc; P.ldc = C;
         P.bslot = 0; P.db = dbc; P.rows_per_chunk = 64;
-        gsb_status st = launch_gemm<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, 64) * ceil_div(d, 128) * ceil_div(C, 128),
+        gsb_status st = launch_gemm_v<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, 64) * ceil_div(d, 128) * ceil_div(C, 128),
                                              n, d, n, C, s);
         if (st != GSB_OK) return st;
     }
@@ -1251,7 +1251,7 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         const int64_t tiles = ceil_div(n, 128) * ceil_div(d, 128);
         P.ksplit = choose_ksplit(tiles, (C + 31) / 32, true);
         if (P.ksplit > 1) GSB_CUDA(cudaMemsetAsync(dh, 0, sizeof(float) * (size_t)n * d, s));
-        gsb_status st = launch_gemm<UMMA_NT>("nc_gemm_dh", P, tiles, n, C, d, C, s);
+        gsb_status st = launch_gemm_v<UMMA_NT>("nc_gemm_dh", P, tiles, n, C, d, C, s);
         if (st != GSB_OK) return st;
     }
     return fork_end(s_main, s_side);

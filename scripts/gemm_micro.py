@@ -39,6 +39,14 @@ for (M, K, N) in [(16384, 512, 128), (1024, 512, 128)]:
         torch.cuda.current_stream().wait_stream(st)
         g.replay()
         torch.cuda.synchronize()
+        # correctness of one launch against fp64
+        for x in (out, o2, oW):
+            x.zero_()
+        fn()
+        torch.cuda.synchronize()
+        ref = {0: A.double() @ B.double(), 1: A2.double() @ B.double().T, 2: A.double().T @ A2.double()}[mode]
+        got = {0: out, 1: o2, 2: oW}[mode].double()
+        rel = ((got - ref).norm() / ref.norm()).item()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         g.replay()
@@ -47,4 +55,4 @@ for (M, K, N) in [(16384, 512, 128), (1024, 512, 128)]:
         us = e0.elapsed_time(e1) / 20 * 1e3
         fl = 2 * M * K * N
         print(f"{tag} mode={mode} M={M} K={K} N={N}: {us:8.1f} us  {fl / us / 1e6:7.1f} TFLOP/s  "
-              f"A bytes {M * K * 4 / us / 1e3:7.1f} GB/s", flush=True)
+              f"A bytes {M * K * 4 / us / 1e3:7.1f} GB/s  rel err {rel:.2e}", flush=True)
