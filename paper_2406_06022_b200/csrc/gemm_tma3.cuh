@@ -26,6 +26,7 @@
 #pragma once
 #include <cuda.h>
 
+#include "gemm_simt.cuh"
 #include "gemm_tma.cuh"
 
 namespace gsb {
@@ -514,6 +515,14 @@ inline gsb_status launch_gemm_v(const char* name, UProb P, int64_t tiles_upper, 
     if (ver < 0) {
         const char* e = getenv("GSB_GEMM");
         ver = (e && (strcmp(e, "tma2") == 0 || strcmp(e, "umma") == 0)) ? 2 : 3;
+    }
+    // SIMT small-problem path: opt-in (GSB_SIMT=1); its K chunks are load-latency bound and it
+    // measured slower than the tcgen05 kernel in the step (profiles/round2_gemm_tma3.md)
+    static const bool simt = getenv("GSB_SIMT") && strcmp(getenv("GSB_SIMT"), "1") == 0;
+    if (simt && ver == 3) {
+        bool launched = false;
+        const gsb_status st = launch_simt_gemm<MODE>(name, P, a_rows, s, &launched);
+        if (st != GSB_OK || launched) return st;
     }
     if (ver == 3) {
         UProb Q = P;

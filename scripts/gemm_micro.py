@@ -13,7 +13,8 @@ from paper_2406_06022_b200._lib import call  # noqa
 
 P = lambda x: C.c_void_p(x.data_ptr())
 tag = f"gemm={os.environ.get('GSB_GEMM', 'tma')} dbg={os.environ.get('GSB_GEMM_DBG', '0')}"
-for (M, K, N) in [(16384, 512, 128), (1024, 512, 128)]:
+SHAPES = [tuple(int(v) for v in x.split("x")) for x in os.environ.get("SHAPES", "16384x512x128,1024x512x128").split(",")]
+for (M, K, N) in SHAPES:
     A = torch.randn(M, K, device="cuda")
     B = torch.randn(K, N, device="cuda")
     out = torch.zeros(M, N, device="cuda")
