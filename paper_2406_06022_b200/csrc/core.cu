@@ -407,6 +407,20 @@ bool encode_tmap_f32(CUtensorMap* m, const float* base, int64_t width, int64_t r
     return r == CUDA_SUCCESS;
 }
 
+bool encode_tmap_bf16_2d(CUtensorMap* m, const void* base, int64_t width, int64_t rows, int64_t ld, int box_w,
+                         int box_h) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || width < 1 || rows < 1) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 bool encode_tmap_nd(CUtensorMap* m, const float* base, int rank, const int64_t* dims, const int64_t* strides,
                     const int* box, int swizzle) {
     EncodeTiledFn fn = encode_fn();

@@ -12,6 +12,9 @@
 // Contract: include/gsb.h "Input encoder".
 #include <cuda_bf16.h>
 
+#include <cuda.h>
+
+#include "gemm_tma.cuh"
 #include "gsb_internal.cuh"
 #include "umma.cuh"
 
@@ -40,6 +43,17 @@ struct EncDev {
 struct EncOut {
     float* dW[kMaxT];                      // backward: dW_t [dim_t][d_out] (accumulated)
 };
+
+// TMA maps of the B operand (use = 1): forward: W_t^T hi / lo per projected type, [d_out][dim_t]
+// bf16, box {64, 128} SWIZZLE_128B (= the K-major kmaj16 panel layout); backward: dH0 hi / lo
+// [rows][d_out] bf16 in [0], box {64, 64} SWIZZLE_128B, two boxes per 128-wide MN panel 8192 B
+// apart (MN-major: LBO 8192, SBO 1024, 16-row k-step 2048 B; scripts/probe_tf32.cu (e)).
+struct EncMaps {
+    CUtensorMap hi[kMaxT], lo[kMaxT];
+    int use;
+};
+bool encode_tmap_bf16_2d(CUtensorMap* m, const void* base, int64_t width, int64_t rows, int64_t ld, int box_w,
+                         int box_h);
 
 struct EnCursor {
     int64_t tile;      // >= total: exhausted
@@ -134,7 +148,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 template <bool BWD>
 __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, EncDev e, const HopMeta* __restrict__ m,
                                                                     const int64_t* __restrict__ src_gid,
-                                                                    float* __restrict__ H0, EncOut out) {
+                                                                    float* __restrict__ H0, EncOut out,
+                                                                    const __grid_constant__ EncMaps maps) {
     GSB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -144,7 +159,7 @@ __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, 
     if (warp == 0) umma::tmem_alloc<256>(&tmem_sh);
     if (tid == 0) {
         for (int s = 0; s < EN_STAGES; ++s) {
-            umma::mbar_init(&full[s], 128);
+            umma::mbar_init(&full[s], 128 + (maps.use ? 1 : 0));
             umma::mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -189,15 +204,22 @@ __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, 
                     const int st = (int)(it % EN_STAGES);
                     if (it >= EN_STAGES) umma::mbar_wait(&empty[st], (uint32_t)((it / EN_STAGES) - 1) & 1u);
                     const uint32_t sA = umma::smem_u32(smem + st * EN_STAGE), sBh = sA + EN_PANEL, sBl = sA + 2 * EN_PANEL;
+                    if (maps.use && p == 0) {      // W_t^T hi / lo panels: two TMA boxes
+                        tma::mbar_expect_tx(&full[st], 2 * EN_PANEL);
+                        tma::load_2d(sBh, &maps.hi[c.t], pn * 64, c.n0, &full[st]);
+                        tma::load_2d(sBl, &maps.lo[c.t], pn * 64, c.n0, &full[st]);
+                    }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int r = rg + 16 * i;
                         const uint32_t o = umma::kmaj16_chunk(r, ch);
                         cp16(sA + o, arow[i] ? arow[i] + pn * 128 + ch * 16 : reinterpret_cast<const char*>(whi),
                              arow[i] ? 16 : 0);
-                        const size_t off = (size_t)(c.n0 + r) * dim + pn * 64 + ch * 8;
-                        cp16(sBh + o, whi + off, 16);
-                        cp16(sBl + o, wlo + off, 16);
+                        if (!maps.use) {
+                            const size_t off = (size_t)(c.n0 + r) * dim + pn * 64 + ch * 8;
+                            cp16(sBh + o, whi + off, 16);
+                            cp16(sBl + o, wlo + off, 16);
+                        }
                     }
                     cp_arrive_noinc(&full[st]);
                 }
@@ -221,6 +243,14 @@ __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, 
                     const int st = (int)(it % EN_STAGES);
                     if (it >= EN_STAGES) umma::mbar_wait(&empty[st], (uint32_t)((it / EN_STAGES) - 1) & 1u);
                     const uint32_t sA = umma::smem_u32(smem + st * EN_STAGE), sBh = sA + EN_PANEL, sBl = sA + 2 * EN_PANEL;
+                    if (maps.use && p == 0) {      // dH0 hi / lo rows of this panel: 2 x 2 TMA boxes
+                        const int32_t r0 = (int32_t)(c.row0 + (int64_t)pn * 64);
+                        tma::mbar_expect_tx(&full[st], 2 * EN_PANEL);
+                        tma::load_2d(sBh, &maps.hi[0], c.n0, r0, &full[st]);
+                        tma::load_2d(sBh + 8192, &maps.hi[0], c.n0 + 64, r0, &full[st]);
+                        tma::load_2d(sBl, &maps.lo[0], c.n0, r0, &full[st]);
+                        tma::load_2d(sBl + 8192, &maps.lo[0], c.n0 + 64, r0, &full[st]);
+                    }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int kr = kb + 8 * i;
@@ -230,9 +260,11 @@ __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, 
                         const char* src = ok ? reinterpret_cast<const char*>(feat_row(g, gid[i])) + (size_t)(c.m0 + cc * 8) * 2
                                              : reinterpret_cast<const char*>(e.d_hi);
                         cp16(sA + o, src, ok ? 16 : 0);
-                        const size_t off = (size_t)(ok ? row : 0) * e.d_out + c.n0 + cc * 8;
-                        cp16(sBh + o, e.d_hi + off, ok ? 16 : 0);
-                        cp16(sBl + o, e.d_lo + off, ok ? 16 : 0);
+                        if (!maps.use) {
+                            const size_t off = (size_t)(ok ? row : 0) * e.d_out + c.n0 + cc * 8;
+                            cp16(sBh + o, e.d_hi + off, ok ? 16 : 0);
+                            cp16(sBl + o, e.d_lo + off, ok ? 16 : 0);
+                        }
                     }
                     cp_arrive_noinc(&full[st]);
                 }
@@ -261,8 +293,13 @@ __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, 
                     for (int ks = 0; ks < 4; ++ks) {
                         const uint32_t o = BWD ? ks * 4096u : ks * 32u;
                         const uint64_t da = BWD ? umma::desc_mnmajor16(a + o) : umma::desc_kmajor(a + o);
-                        const uint64_t dbh = BWD ? umma::desc_mnmajor16(bh + o) : umma::desc_kmajor(bh + o);
-                        const uint64_t dbl = BWD ? umma::desc_mnmajor16(bl + o) : umma::desc_kmajor(bl + o);
+                        // backward B from TMA boxes: MN atoms 8192 B apart, 8-row K groups 1024 B, k-step 2048 B
+                        const uint64_t dbh = !BWD ? umma::desc_kmajor(bh + o)
+                                             : maps.use ? umma::desc_encode(bh + ks * 2048u, 8192, 1024, 2)
+                                                        : umma::desc_mnmajor16(bh + o);
+                        const uint64_t dbl = !BWD ? umma::desc_kmajor(bl + o)
+                                             : maps.use ? umma::desc_encode(bl + ks * 2048u, 8192, 1024, 2)
+                                                        : umma::desc_mnmajor16(bl + o);
                         umma::mma_f16(d, da, dbh, IDESC, (pn > 0 || ks > 0) ? 1u : 0u);
                         umma::mma_f16(d, da, dbl, IDESC, 1u);
                     }
@@ -430,15 +467,31 @@ static gsb_status enc_check(const Blocks* B, const float* const* W, int d_out) {
     return GSB_OK;
 }
 
+// B operand by TMA unless GSB_ENC_TMA=0 or a map cannot be encoded (then every producer thread
+// copies its B chunks with cp.async as well)
 template <bool BWD>
 static gsb_status launch_enc(const char* name, const GraphDev& g, const EncDev& e, const HopMeta* m,
-                             const int64_t* src_gid, float* H0, const EncOut& out, cudaStream_t s) {
+                             const int64_t* src_gid, float* H0, const EncOut& out, int64_t cap_rows, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         GSB_CUDA(cudaFuncSetAttribute(enc_umma_kernel<BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, EN_SMEM));
         attr = true;
     }
-    GSB_LAUNCH(name, enc_umma_kernel<BWD>, kNumSMs, EN_WS_THREADS, EN_SMEM, s, g, e, m, src_gid, H0, out);
+    static const bool want = !(getenv("GSB_ENC_TMA") && strcmp(getenv("GSB_ENC_TMA"), "0") == 0);
+    EncMaps maps;
+    memset(&maps, 0, sizeof(maps));
+    bool ok = want;
+    if (ok && !BWD) {
+        for (int t = 0; t < e.T && ok; ++t)
+            if (e.proj[t])
+                ok = encode_tmap_bf16_2d(&maps.hi[t], e.wt_hi[t], e.dim[t], e.d_out, e.dim[t], 64, 128) &&
+                     encode_tmap_bf16_2d(&maps.lo[t], e.wt_lo[t], e.dim[t], e.d_out, e.dim[t], 64, 128);
+    } else if (ok) {
+        ok = encode_tmap_bf16_2d(&maps.hi[0], e.d_hi, e.d_out, cap_rows, e.d_out, 64, 64) &&
+             encode_tmap_bf16_2d(&maps.lo[0], e.d_lo, e.d_out, cap_rows, e.d_out, 64, 64);
+    }
+    maps.use = ok ? 1 : 0;
+    GSB_LAUNCH(name, enc_umma_kernel<BWD>, kNumSMs, EN_WS_THREADS, EN_SMEM, s, g, e, m, src_gid, H0, out, maps);
     return GSB_OK;
 }
 
@@ -487,7 +540,7 @@ gsb_status gsb_encoder_fwd(gsb_blocks_t b, const void* arena, const float* const
     }
     if (any_proj) {
         EncOut out{};
-        return launch_enc<false>("enc_gemm_fwd", g, e, hb.meta, hb.src_gid, H0, out, s);
+        return launch_enc<false>("enc_gemm_fwd", g, e, hb.meta, hb.src_gid, H0, out, B->cap_dst[B->L + 1], s);
     }
     return GSB_OK;
 }
@@ -516,7 +569,7 @@ gsb_status gsb_encoder_bwd(gsb_blocks_t b, const void* arena, const float* const
     if (!any) return GSB_OK;
     GSB_LAUNCH("enc_dsplit", enc_dsplit_kernel, grid_for(hb.cap_src * d_out / 4, 256, kNumSMs * 8), 256, 0, s, e,
                hb.meta, dH0, const_cast<__nv_bfloat16*>(e.d_hi), const_cast<__nv_bfloat16*>(e.d_lo));
-    return launch_enc<true>("enc_gemm_dW", g, e, hb.meta, hb.src_gid, nullptr, out, s);
+    return launch_enc<true>("enc_gemm_dW", g, e, hb.meta, hb.src_gid, nullptr, out, B->cap_dst[B->L + 1], s);
 }
 
 }  // extern "C"

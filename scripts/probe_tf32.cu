@@ -7,6 +7,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -I paper_2406_06022_b200/csrc
 //      scripts/probe_tf32.cu -o /tmp/probe_tf32 -lcuda
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -170,6 +171,57 @@ __global__ void probe_d(const __grid_constant__ CUtensorMap mA, const __grid_con
     if (warp == 0) umma::tmem_dealloc<128>(t);
 }
 
+// (e) bf16 MN-major B straight from TMA SWIZZLE_128B boxes {64 mn, 64 k} (2 boxes 8192 B apart):
+// D[128 m][128 n] = A[m][k] B[k][n], K = 64; A K-major bf16 (kmaj16 via STS); desc LBO / SBO given.
+__global__ void probe_e(const __grid_constant__ CUtensorMap mB, const __nv_bfloat16* A, uint32_t lbo, uint32_t sbo,
+                        float* D) {
+    __shared__ __align__(1024) uint8_t sm[2 * 16384];
+    __shared__ __align__(8) uint64_t bar, bar2;
+    __shared__ uint32_t tm;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 128 * 8; i += blockDim.x) {   // 16-B chunks: row r, chunk c (8 bf16)
+        const int r = i / 8, c = i % 8;
+        *reinterpret_cast<uint4*>(sm + umma::kmaj16_chunk(r, c)) = *reinterpret_cast<const uint4*>(A + r * 64 + c * 8);
+    }
+    if (tid == 0) {
+        umma::mbar_init(&bar, 1);
+        umma::mbar_init(&bar2, 1);
+        umma::fence_barrier_init();
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(umma::smem_u32(&bar)), "r"(16384)
+                     : "memory");
+        for (int j = 0; j < 2; ++j)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                    umma::smem_u32(sm + 16384 + j * 8192)),
+                "l"(reinterpret_cast<uint64_t>(&mB)), "r"(j * 64), "r"(0), "r"(umma::smem_u32(&bar))
+                : "memory");
+    }
+    if (warp == 0) umma::tmem_alloc<128>(&tm);
+    umma::fence_proxy_async_smem();
+    umma::tc_fence_before();
+    __syncthreads();
+    umma::tc_fence_after();
+    umma::mbar_wait(&bar, 0);
+    const uint32_t t = tm;
+    if (tid == 0) {
+        const uint32_t a0 = umma::smem_u32(sm), b0 = a0 + 16384;
+        for (int ks = 0; ks < 4; ++ks)
+            umma::mma_f16(t, umma::desc_kmajor(a0 + ks * 32), umma::desc_encode(b0 + ks * 2048, lbo, sbo, 2),
+                          umma::idesc_bf16(128, false, true), ks > 0);
+        umma::mma_commit(&bar2);
+    }
+    umma::mbar_wait(&bar2, 0);
+    umma::tc_fence_after();
+    for (int c = 0; c < 4; ++c) {
+        float v[32];
+        umma::tmem_ld32(t + ((uint32_t)(warp * 32) << 16) + c * 32, v);
+        for (int j = 0; j < 32; ++j) D[(warp * 32 + (tid & 31)) * 128 + c * 32 + j] = v[j];
+    }
+    umma::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) umma::tmem_dealloc<128>(t);
+}
+
 typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -300,6 +352,39 @@ int main() {
                 }
                 printf("(d) a_mn %d lbo %u sbo %u: max|D-exact| %.3g\n", a_mn, lbos[v], sbos[v], me);
             }
+    }
+    // ---- (e)
+    {
+        std::vector<__nv_bfloat16> Ab(128 * 64), Bt(64 * 128);   // A [m][k], Bt [k][n]
+        std::vector<float> Af(128 * 64), Bf(64 * 128);
+        for (int i = 0; i < 128 * 64; ++i) { Ab[i] = __float2bfloat16((float)rand() / RAND_MAX - 0.5f); Af[i] = __bfloat162float(Ab[i]); }
+        for (int i = 0; i < 64 * 128; ++i) { Bt[i] = __float2bfloat16((float)rand() / RAND_MAX - 0.5f); Bf[i] = __bfloat162float(Bt[i]); }
+        __nv_bfloat16 *dAb, *dBt;
+        CK(cudaMalloc(&dAb, 2 * 8192));
+        CK(cudaMalloc(&dBt, 2 * 8192));
+        CK(cudaMemcpy(dAb, Ab.data(), 2 * 8192, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dBt, Bt.data(), 2 * 8192, cudaMemcpyHostToDevice));
+        CUtensorMap mb;
+        const cuuint64_t dims[2] = {128, 64};
+        const cuuint64_t str[1] = {128 * 2};
+        const cuuint32_t box[2] = {64, 64}, es[2] = {1, 1};
+        CUresult r = enc(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dBt, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        printf("(e) encode %d\n", (int)r);
+        const uint32_t lbos[2] = {8192, 1024}, sbos[2] = {1024, 8192};
+        for (int v = 0; v < 2; ++v) {
+            probe_e<<<1, 128>>>(mb, dAb, lbos[v], sbos[v], dD);
+            CK(cudaDeviceSynchronize());
+            CK(cudaMemcpy(D.data(), dD, 4 * 16384, cudaMemcpyDeviceToHost));
+            double me = 0;
+            for (int i = 0; i < 16384; ++i) {
+                const int rr = i / 128, c = i % 128;
+                double ref = 0;
+                for (int k = 0; k < 64; ++k) ref += (double)Af[rr * 64 + k] * Bf[k * 128 + c];
+                me = fmax(me, fabs(D[i] - ref));
+            }
+            printf("(e) bf16 MN-major B lbo %u sbo %u: max|D-exact| %.3g\n", lbos[v], sbos[v], me);
+        }
     }
     return 0;
 }
