@@ -598,6 +598,11 @@ def run_gsb(args, cfg):
             tr.sampler.sample(seeds_all[i], tr.rng_seed, i * ws + rank)
         sizes.append(block_sizes(tr, cfg))
     buf = C.create_string_buffer(1 << 16)
+    if os.environ.get("GSB_TIMELINE"):   # tools: per-launch timeline of the profiled steps
+        tl = C.create_string_buffer(1 << 20)
+        _lib.call("gsb_profile_timeline", tl, len(tl))
+        with open(os.environ["GSB_TIMELINE"], "w") as f:
+            f.write(tl.value.decode())
     _lib.call("gsb_profile_dump", buf, len(buf))
     prof = {}
     for line in buf.value.decode().splitlines():

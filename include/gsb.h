@@ -70,6 +70,10 @@ int32_t gsb_version(void);
 int64_t gsb_launch_count(void);
 gsb_status gsb_profile_enable(int32_t on);
 gsb_status gsb_profile_dump(char* buf, size_t buflen);
+/* Tools: one line per launch profiled since the last dump, in enqueue order -- "name stream
+ * start_us dur_us" (stream = index in order of first use, start relative to the earliest
+ * launch); does not clear the records (gsb_profile_dump does). */
+gsb_status gsb_profile_timeline(char* buf, size_t buflen);
 
 /* ======================================================================================
  * Graph store ("distributed graph engine"; S:L225 load_partition, S:L240 edge

@@ -43,6 +43,7 @@ SIGS = {
     "gsb_launch_count": [],
     "gsb_profile_enable": [i32],
     "gsb_profile_dump": [C.c_char_p, sz],
+    "gsb_profile_timeline": [C.c_char_p, sz],
     "gsb_graph_create": [i32, P, i32, P, P, C.POINTER(P)],
     "gsb_graph_destroy": [P],
     "gsb_csc_build_bytes": [P, i32, i64, C.POINTER(sz)],

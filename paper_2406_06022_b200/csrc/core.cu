@@ -20,6 +20,7 @@ static bool g_prof_on = false;
 struct ProfRec {
     const char* name;
     cudaEvent_t a, b;
+    cudaStream_t s;
 };
 static std::vector<ProfRec> g_prof;
 static std::vector<cudaEvent_t> g_event_pool;
@@ -91,7 +92,7 @@ void prof_end(cudaStream_t s) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     cudaEvent_t b = get_event();
     cudaEventRecord(b, s);
-    g_prof.push_back({g_pending_name, g_pending_ev, b});
+    g_prof.push_back({g_pending_name, g_pending_ev, b, s});
     g_pending_name = nullptr;
 }
 
@@ -449,6 +450,41 @@ int64_t gsb_launch_count(void) { return g_launches.load(); }
 
 gsb_status gsb_profile_enable(int32_t on) {
     g_prof_on = on != 0;
+    return GSB_OK;
+}
+
+// one line per profiled launch, in enqueue order: name, stream index (order of first use),
+// start and duration in us relative to the earliest launch start (tools: step timelines)
+gsb_status gsb_profile_timeline(char* buf, size_t buflen) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    GSB_CUDA(cudaDeviceSynchronize());
+    std::string out;
+    if (!g_prof.empty()) {
+        std::vector<cudaStream_t> streams;
+        float t0 = 0.f;
+        for (auto& r : g_prof) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, g_prof[0].a, r.a);
+            t0 = std::min(t0, t);
+        }
+        char line[256];
+        for (auto& r : g_prof) {
+            float st = 0.f, du = 0.f;
+            cudaEventElapsedTime(&st, g_prof[0].a, r.a);
+            cudaEventElapsedTime(&du, r.a, r.b);
+            size_t k = 0;
+            for (; k < streams.size(); ++k)
+                if (streams[k] == r.s) break;
+            if (k == streams.size()) streams.push_back(r.s);
+            snprintf(line, sizeof(line), "%s %zu %.2f %.2f\n", r.name, k, (st - t0) * 1e3, du * 1e3);
+            out += line;
+        }
+    }
+    if (buf && buflen) {
+        size_t n = out.size() < buflen - 1 ? out.size() : buflen - 1;
+        memcpy(buf, out.data(), n);
+        buf[n] = 0;
+    }
     return GSB_OK;
 }
 

@@ -497,15 +497,14 @@ __global__ void __launch_bounds__(TG_THREADS, 1) tma_gemm_kernel(const __grid_co
 bool encode_tmap_f32(CUtensorMap* m, const float* base, int64_t width, int64_t rows, int64_t ld, int box_w,
                      int box_h, bool swz128);
 
-// Weight images (gsb_weight_images_register / _refresh, weights.cu): tf32 hi / lo splits of a
-// weight tensor W [slots][K][N] kept in caller memory and refreshed once per step, so the NN
-// and NT GEMMs TMA the B operand straight into the MMA ring (no per-CTA split of the same W).
-//   nn_hi / nn_lo : W^T  [slots][N][K]   (NN B operand, K-major)
-//   nt_hi / nt_lo : W    [slots][K][ldn] (NT B operand, K-major; columns >= N zero)
+// Weight images (gsb_weight_images_register / _refresh, weights.cu): the 3xTF32 split of a
+// weight tensor W [slots][K][N], hi = rna_tf32(W) and lo = rna_tf32(W - hi), both in W's own
+// layout with a 16-B aligned row stride ldn = ceil4(N), kept in caller memory and refreshed once
+// per step.  The TMA-everything GEMM (gemm_tma3.cuh) loads the NN / NT B operand from them.
 struct WeightImage {
     const float* W;
     int32_t slots, K, N, ldn;
-    float *nn_hi, *nn_lo, *nt_hi, *nt_lo;
+    float *hi, *lo;
 };
 const WeightImage* find_weight_image(const float* W);
 
@@ -534,36 +533,6 @@ inline gsb_status launch_gemm(const char* name, UProb P, int64_t tiles_upper, in
         fprintf(stderr, "[gsb] %s: tma=%d aligned=%d (A %p lda %lld, B %p ldb %lld, bslot %lld)\n", name, use_tma,
                 (int)aligned, (const void*)P.A, (long long)P.lda, (const void*)P.B, (long long)P.ldb,
                 (long long)P.bslot);
-    static const bool no_img = getenv("GSB_NO_WIMG") != nullptr;    // A/B knob
-    const WeightImage* wi = (MODE != UMMA_TN && !no_img) ? find_weight_image(P.B) : nullptr;
-    const bool a_ok = ((reinterpret_cast<uintptr_t>(P.A) & 15) == 0) && ((P.lda & 3) == 0) && a_rows >= 1;
-    if (use_tma && wi && a_ok) {
-        CUtensorMap ma, mb, mb2;
-        const bool kA = true;
-        bool ok = encode_tmap_f32(&ma, P.A, a_w, a_rows, P.lda, kA ? 32 : 128, kA ? 128 : 32, kA);
-        UProb Q = P;
-        Q.bimg = 1;
-        if (MODE == UMMA_NN) {   // W^T [slots*N][K]
-            ok = ok && encode_tmap_f32(&mb, wi->nn_hi, wi->K, (int64_t)wi->slots * wi->N, wi->K, 32, 128, true) &&
-                 encode_tmap_f32(&mb2, wi->nn_lo, wi->K, (int64_t)wi->slots * wi->N, wi->K, 32, 128, true);
-            Q.brow = wi->N;
-        } else {                 // W [slots*K][ldn]
-            ok = ok && encode_tmap_f32(&mb, wi->nt_hi, wi->N, (int64_t)wi->slots * wi->K, wi->ldn, 32, 128, true) &&
-                 encode_tmap_f32(&mb2, wi->nt_lo, wi->N, (int64_t)wi->slots * wi->K, wi->ldn, 32, 128, true);
-            Q.brow = wi->K;
-        }
-        if (ok) {
-            static bool attr_set2 = false;
-            if (!attr_set2) {
-                GSB_CUDA(cudaFuncSetAttribute(tma_gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              TG_SMEM));
-                attr_set2 = true;
-            }
-            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_upper * Q.ksplit, kNumSMs));
-            GSB_LAUNCH(name, tma_gemm_kernel<MODE>, grid, TG_THREADS, TG_SMEM, s, ma, mb, mb2, Q);
-            return GSB_OK;
-        }
-    }
     if (use_tma && aligned) {
         CUtensorMap ma, mb;
         const bool kA = (MODE != UMMA_TN), kB = (MODE == UMMA_NT);

@@ -77,8 +77,13 @@ constexpr int T3_STAGE = 4 * UM_PANEL;             // A raw(hi), A lo, B raw(hi)
 constexpr int T3_OUT = UM_PANEL;                   // one 128 x 32 fp32 epilogue staging tile
 constexpr int t3_smem(int stages) { return stages * T3_STAGE + 2 * T3_OUT + 1024; }
 
-// lo = x - trunc_tf32(x) (exact): the tf32 hi the tensor core reads from the raw value
-__device__ __forceinline__ float lo_of(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// lo = x - trunc_tf32(x) (exact in fp32; the tf32 hi the tensor core reads from the raw value),
+// rounded to tf32 to nearest here: the tensor core would truncate it, and truncation errors all
+// carry the sign of x (a bias that does not average out in long sums)
+__device__ __forceinline__ float lo_of(float x) {
+    const float r = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    return __uint_as_float(umma::rna_tf32_bits(__float_as_uint(r)));
+}
 
 // desc of an MN-major panel as TMA ATOM_32B lays it out (4 boxes {32 mn, 32 k} 4096 B apart)
 __device__ __forceinline__ uint64_t desc_mn_tma(uint32_t addr) { return umma::desc_encode(addr, 4096, 512, 1); }
@@ -106,9 +111,13 @@ __device__ __forceinline__ T3Off t3_offsets(int t) {
 }
 
 // lo of one operand panel; ZERO: K rows kk >= klim are zeroed in raw and lo (TN chunk ends);
-// CS: column sums of the (zeroed) values, per thread (TN bias gradient)
-template <bool MN, bool ZERO, bool CS>
-__device__ __forceinline__ void t3_split(uint32_t raw, uint32_t lo, const T3Off& o, int klim, float4& cs) {
+// CS: column sums of the (zeroed) values, per thread (TN bias gradient).
+// HI: also round the hi operand to nearest in place (hi = rna_tf32(x), lo = rna_tf32(x - hi))
+// for ONE of the two operands: with both his truncated the dropped lo_A lo_B term has the sign
+// of every product (both residuals carry the sign of their x) and accumulates like the result
+// itself; one round-to-nearest residual makes it zero-mean (the 3xTF32 accuracy of an rna split)
+template <bool MN, bool ZERO, bool CS, bool HI>
+__device__ __forceinline__ void t3_split(uint32_t raw, uint32_t lo, const T3Off& o, int klim, double4& cs) {
     float4 v[T3_PER];
 #pragma unroll
     for (int i = 0; i < T3_PER; ++i) v[i] = lds128(raw + (MN ? o.m[i] : o.k[i]));
@@ -119,9 +128,19 @@ __device__ __forceinline__ void t3_split(uint32_t raw, uint32_t lo, const T3Off&
             v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             sts128(raw + off, 0u, 0u, 0u, 0u);
         }
-        if (CS) { cs.x += v[i].x; cs.y += v[i].y; cs.z += v[i].z; cs.w += v[i].w; }
-        sts128(lo + off, __float_as_uint(lo_of(v[i].x)), __float_as_uint(lo_of(v[i].y)),
-               __float_as_uint(lo_of(v[i].z)), __float_as_uint(lo_of(v[i].w)));
+        if (CS) { cs.x += v[i].x; cs.y += v[i].y; cs.z += v[i].z; cs.w += v[i].w; }   // fp64: exact-ish sums
+        if (HI) {
+            uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
+            umma::split_tf32(v[i].x, h0, l0);
+            umma::split_tf32(v[i].y, h1, l1);
+            umma::split_tf32(v[i].z, h2, l2);
+            umma::split_tf32(v[i].w, h3, l3);
+            sts128(raw + off, h0, h1, h2, h3);
+            sts128(lo + off, l0, l1, l2, l3);
+        } else {
+            sts128(lo + off, __float_as_uint(lo_of(v[i].x)), __float_as_uint(lo_of(v[i].y)),
+                   __float_as_uint(lo_of(v[i].z)), __float_as_uint(lo_of(v[i].w)));
+        }
     }
 }
 
@@ -159,9 +178,12 @@ __device__ __forceinline__ void t3_epi_direct(const UProb& P, const UCursor& c, 
 
 // maps: A, B operands; C output (NN: 2-D [rows][N]; NT: 3-D {d_in, slots, rows}; TN: 3-D
 // {N, d_in, slots}), box 32 x 128 SWIZZLE_128B
+// P.bimg: the NN / NT B operand comes pre-split from weight images (mapB = hi, mapB2 = lo,
+// both rna; weights.cu), so the splitters only write A's lo
 template <int MODE, int T3_STAGES>
 __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                                                                    const __grid_constant__ CUtensorMap mapB,
+                                                                   const __grid_constant__ CUtensorMap mapB2,
                                                                    const __grid_constant__ CUtensorMap mapC, UProb P) {
     GSB_PDL_ENTRY();
     if (threadIdx.x == 0) trace_mark(P, 0, TG_TRACE - 2);
@@ -172,7 +194,7 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
     __shared__ __align__(8) uint64_t full[T3_STAGES], split_done[T3_STAGES], empty[T3_STAGES];
     __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_sh;
-    __shared__ float dbred[128];
+    __shared__ double dbred[128];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr bool A_MN = (MODE == UMMA_TN);
     constexpr bool B_MN = (MODE != UMMA_NT);
@@ -190,9 +212,10 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
         umma::fence_barrier_init();
         tma::prefetch_map(&mapA);
         tma::prefetch_map(&mapB);
+        if (P.bimg) tma::prefetch_map(&mapB2);
         tma::prefetch_map(&mapC);
     }
-    if (tid < 128) dbred[tid] = 0.f;
+    if (tid < 128) dbred[tid] = 0.0;
     if (warp == 1) umma::tmem_alloc<256>(&tmem_sh);
     umma::tc_fence_before();
     __syncthreads();
@@ -228,7 +251,7 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
                 if (P.dbg & 4) {
                     tma::mbar_arrive(&full[st]);    // A/B knob: no loads
                 } else if (MODE == UMMA_NN) {
-                    tma::mbar_expect_tx(&full[st], 2 * UM_PANEL);
+                    tma::mbar_expect_tx(&full[st], (P.bimg ? 3 : 2) * UM_PANEL);
                     const int per = P.d_in / 32;
                     const int sp = c.p / per;
                     const int kk = (c.p - sp * per) * 32;
@@ -236,10 +259,17 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
                     const int32_t wrow = P.rg.slot_w[c.t][sp] * P.brow + kk;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) tma::load_2d(b + j * 4096, &mapB, c.n0 + 32 * j, wrow, &full[st]);
+                    if (P.bimg) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            tma::load_2d(b + UM_PANEL + j * 4096, &mapB2, c.n0 + 32 * j, wrow, &full[st]);
+                    }
                 } else if (MODE == UMMA_NT) {
-                    tma::mbar_expect_tx(&full[st], 2 * UM_PANEL);
+                    tma::mbar_expect_tx(&full[st], (P.bimg ? 3 : 2) * UM_PANEL);
                     tma::load_2d(a, &mapA, c.p * 32, (int32_t)c.row0, &full[st]);
-                    tma::load_2d(b, &mapB, c.p * 32, P.rg.slot_w[c.t][c.s] * P.brow + c.c0, &full[st]);
+                    const int32_t wrow = P.rg.slot_w[c.t][c.s] * P.brow + c.c0;
+                    tma::load_2d(b, &mapB, c.p * 32, wrow, &full[st]);
+                    if (P.bimg) tma::load_2d(b + UM_PANEL, &mapB2, c.p * 32, wrow, &full[st]);
                 } else {
                     tma::mbar_expect_tx(&full[st], 2 * UM_PANEL);
                     const int32_t rb = (int32_t)(c.row0 + (int64_t)c.p * 32);
@@ -299,7 +329,7 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
         const T3Off o = t3_offsets(t);
         int st = 0, pi = 0;
         uint32_t ph = 0;
-        float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
+        double4 cs = make_double4(0.0, 0.0, 0.0, 0.0);
         while (c.tile < total) {
             tma::mbar_wait_k(&full[st], ph, P.dbg & 512);
             const uint32_t a = umma::smem_u32(ring + st * T3_STAGE), b = a + 2 * UM_PANEL;
@@ -307,18 +337,18 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
             } else if (MODE == UMMA_TN) {
                 const int klim = (int)min((int64_t)32, c.rlim - (c.row0 + (int64_t)c.p * 32));
                 if (klim < 32) {
-                    t3_split<true, true, false>(a, a + UM_PANEL, o, klim, cs);
-                    t3_split<true, true, true>(b, b + UM_PANEL, o, klim, cs);
+                    t3_split<true, true, false, false>(a, a + UM_PANEL, o, klim, cs);
+                    t3_split<true, true, true, true>(b, b + UM_PANEL, o, klim, cs);
                 } else {
-                    t3_split<true, false, false>(a, a + UM_PANEL, o, 32, cs);
-                    t3_split<true, false, true>(b, b + UM_PANEL, o, 32, cs);
+                    t3_split<true, false, false, false>(a, a + UM_PANEL, o, 32, cs);
+                    t3_split<true, false, true, true>(b, b + UM_PANEL, o, 32, cs);
                 }
             } else if (MODE == UMMA_NN) {
-                t3_split<false, false, false>(a, a + UM_PANEL, o, 32, cs);
-                t3_split<true, false, false>(b, b + UM_PANEL, o, 32, cs);
+                t3_split<false, false, false, false>(a, a + UM_PANEL, o, 32, cs);
+                if (!P.bimg) t3_split<true, false, false, true>(b, b + UM_PANEL, o, 32, cs);
             } else {
-                t3_split<false, false, false>(a, a + UM_PANEL, o, 32, cs);
-                t3_split<false, false, false>(b, b + UM_PANEL, o, 32, cs);
+                t3_split<false, false, false, false>(a, a + UM_PANEL, o, 32, cs);
+                if (!P.bimg) t3_split<false, false, false, true>(b, b + UM_PANEL, o, 32, cs);
             }
             umma::fence_proxy_async_smem();     // generic-proxy writes -> tensor-core reads
             __syncwarp();
@@ -337,11 +367,11 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
                     atomicAdd(&dbred[j + 2], cs.z);
                     atomicAdd(&dbred[j + 3], cs.w);
                     tma::named_sync(1, T3_SPLIT);
-                    if (t < 128 && c.n0 + t < P.N) atomicAdd(P.db + c.n0 + t, dbred[t]);
+                    if (t < 128 && c.n0 + t < P.N) atomicAdd(P.db + c.n0 + t, (float)dbred[t]);
                     tma::named_sync(1, T3_SPLIT);
-                    if (t < 128) dbred[t] = 0.f;
+                    if (t < 128) dbred[t] = 0.0;
                 }
-                cs = make_float4(0.f, 0.f, 0.f, 0.f);
+                cs = make_double4(0.0, 0.0, 0.0, 0.0);
             }
             advance(c);
         }
@@ -454,11 +484,11 @@ bool encode_tmap_nd(CUtensorMap* m, const float* base, int rank, const int64_t* 
 // encoded; the caller then falls back to the other kernels.  c_rows: rows of C (NN / NT);
 // c_slots: TN: weight slots of C (dW), NT: column slots per row of C (dacat).
 template <int MODE>
-inline gsb_status launch_gemm3(const char* name, const UProb& P, int64_t tiles_upper, int64_t a_rows, int64_t a_w,
+inline gsb_status launch_gemm3(const char* name, UProb P, int64_t tiles_upper, int64_t a_rows, int64_t a_w,
                                int64_t b_rows, int64_t b_w, int64_t c_rows, int64_t c_slots, cudaStream_t s,
-                               bool* launched) {
+                               bool* launched, const WeightImage* wi = nullptr) {
     *launched = false;
-    CUtensorMap ma, mb, mc;
+    CUtensorMap ma, mb, mb2, mc;
     const int SW128 = CU_TENSOR_MAP_SWIZZLE_128B, SW32 = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
     bool ok;
     if (MODE == UMMA_NN) {
@@ -466,15 +496,26 @@ inline gsb_status launch_gemm3(const char* name, const UProb& P, int64_t tiles_u
         const int64_t db[2] = {b_w, b_rows}, sb[1] = {P.ldb};
         const int64_t dc[2] = {P.N, c_rows}, sc[1] = {P.ldc};
         const int ba[2] = {32, 128}, bb[2] = {32, 32}, bc[2] = {32, 128};
-        ok = encode_tmap_nd(&ma, P.A, 2, da, sa, ba, SW128) && encode_tmap_nd(&mb, P.B, 2, db, sb, bb, SW32) &&
-             encode_tmap_nd(&mc, P.C, 2, dc, sc, bc, SW128);
+        ok = encode_tmap_nd(&ma, P.A, 2, da, sa, ba, SW128) && encode_tmap_nd(&mc, P.C, 2, dc, sc, bc, SW128);
+        if (wi) {
+            const int64_t di[2] = {wi->N, (int64_t)wi->slots * wi->K}, si[1] = {wi->ldn};
+            ok = ok && encode_tmap_nd(&mb, wi->hi, 2, di, si, bb, SW32) && encode_tmap_nd(&mb2, wi->lo, 2, di, si, bb, SW32);
+        } else {
+            ok = ok && encode_tmap_nd(&mb, P.B, 2, db, sb, bb, SW32);
+        }
     } else if (MODE == UMMA_NT) {
         const int64_t da[2] = {a_w, a_rows}, sa[1] = {P.lda};
         const int64_t db[2] = {b_w, b_rows}, sb[1] = {P.ldb};
         const int64_t dc[3] = {P.d_in, c_slots, c_rows}, sc[2] = {P.d_in, P.ldc};
         const int ba[2] = {32, 128}, bb[2] = {32, 128}, bc[3] = {32, 1, 128};
-        ok = encode_tmap_nd(&ma, P.A, 2, da, sa, ba, SW128) && encode_tmap_nd(&mb, P.B, 2, db, sb, bb, SW128) &&
-             encode_tmap_nd(&mc, P.C, 3, dc, sc, bc, SW128);
+        ok = encode_tmap_nd(&ma, P.A, 2, da, sa, ba, SW128) && encode_tmap_nd(&mc, P.C, 3, dc, sc, bc, SW128);
+        if (wi) {
+            const int64_t di[2] = {wi->N, (int64_t)wi->slots * wi->K}, si[1] = {wi->ldn};
+            ok = ok && encode_tmap_nd(&mb, wi->hi, 2, di, si, bb, SW128) &&
+                 encode_tmap_nd(&mb2, wi->lo, 2, di, si, bb, SW128);
+        } else {
+            ok = ok && encode_tmap_nd(&mb, P.B, 2, db, sb, bb, SW128);
+        }
     } else {
         const int64_t da[2] = {a_w, a_rows}, sa[1] = {P.lda};
         const int64_t db[2] = {b_w, b_rows}, sb[1] = {P.ldb};
@@ -485,6 +526,8 @@ inline gsb_status launch_gemm3(const char* name, const UProb& P, int64_t tiles_u
              encode_tmap_nd(&mc, P.C, 3, dc, sc, bc, SW128);
     }
     if (!ok) return GSB_OK;
+    P.bimg = wi ? 1 : 0;
+    if (!wi) mb2 = mb;
     // operand ring depth: 3 stages (225 KB, one CTA per SM) or 2 (161 KB: leaves room for
     // the concurrently running sample-phase kernels on the same SM); GSB_T3_STAGES
     static const int stages = (getenv("GSB_T3_STAGES") && atoi(getenv("GSB_T3_STAGES")) == 2) ? 2 : 3;
@@ -498,9 +541,9 @@ inline gsb_status launch_gemm3(const char* name, const UProb& P, int64_t tiles_u
     }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_upper * P.ksplit, kNumSMs));
     if (stages == 2)
-        GSB_LAUNCH(name, (tma3_gemm_kernel<MODE, 2>), grid, T3_THREADS, t3_smem(2), s, ma, mb, mc, P);
+        GSB_LAUNCH(name, (tma3_gemm_kernel<MODE, 2>), grid, T3_THREADS, t3_smem(2), s, ma, mb, mb2, mc, P);
     else
-        GSB_LAUNCH(name, (tma3_gemm_kernel<MODE, 3>), grid, T3_THREADS, t3_smem(3), s, ma, mb, mc, P);
+        GSB_LAUNCH(name, (tma3_gemm_kernel<MODE, 3>), grid, T3_THREADS, t3_smem(3), s, ma, mb, mb2, mc, P);
     *launched = true;
     return GSB_OK;
 }
@@ -543,10 +586,15 @@ inline gsb_status launch_gemm_v(const char* name, UProb P, int64_t tiles_upper, 
             ok = ok && Q.bslot % std::max<int64_t>(Q.ldb, 1) == 0;
             if (MODE == UMMA_NT) c_slots = (Q.ldc % Q.d_in == 0) ? Q.ldc / Q.d_in : 1;
         }
+        // registered weight image of the B operand (NN / NT): pre-split hi / lo, TMA'd directly
+        static const bool no_img = getenv("GSB_NO_WIMG") != nullptr;    // A/B knob
+        const WeightImage* wi = (MODE != UMMA_TN && !no_img) ? find_weight_image(Q.B) : nullptr;
+        if (wi && !(wi->N == Q.N && wi->K == Q.d_in && (int64_t)wi->K * wi->N == Q.bslot || (Q.bslot == 0 && wi->slots == 1 && wi->K == Q.d_in)))
+            wi = nullptr;
         if (ok) {
             bool launched = false;
             const gsb_status st = launch_gemm3<MODE>(name, Q, tiles_upper, a_rows, a_w, b_rows, b_w, a_rows, c_slots, s,
-                                                     &launched);
+                                                     &launched, wi);
             if (st != GSB_OK || launched) return st;
         }
     }

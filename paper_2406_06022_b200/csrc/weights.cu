@@ -1,9 +1,9 @@
-// weights.cu -- tf32 hi / lo images of the layer and decoder weights for the TMA GEMMs
-// (gemm_tma.cuh).  3xTF32 needs every fp32 operand split into hi = rna_tf32(x) and
-// lo = rna_tf32(x - hi); a weight is the B operand of every CTA of a GEMM, so instead of each
-// CTA splitting the same W in shared memory, W is split once per step into caller-owned images
-// in the two layouts the NN (W^T) and NT (W) GEMMs read K-major, and the GEMMs TMA them
-// straight into the MMA stage.  Contract: include/gsb.h "Weight images".
+// weights.cu -- tf32 hi / lo images of the layer weights for the TMA-everything GEMM
+// (gemm_tma3.cuh).  3xTF32 needs every fp32 operand split into hi and lo; a weight is the B
+// operand of every CTA of a GEMM, so instead of each CTA splitting the same W in shared memory,
+// W is split once per step (hi = rna_tf32(W), lo = rna_tf32(W - hi), in W's own layout) into
+// caller-owned images that the NN / NT GEMMs TMA straight into the MMA stage.
+// Contract: include/gsb.h "Weight images".
 #include <mutex>
 
 #include "gemm_tma.cuh"
@@ -22,8 +22,8 @@ const WeightImage* find_weight_image(const float* W) {
 }
 
 static size_t wi_floats(int slots, int K, int N, int ldn) {
-    const size_t nn = (size_t)slots * N * K, nt = (size_t)slots * K * ldn;
-    return 2 * ((nn + 3) / 4 * 4) + 2 * ((nt + 3) / 4 * 4);
+    (void)N;
+    return 2 * (size_t)slots * K * ldn;
 }
 
 constexpr int kMaxImages = 8;
@@ -32,7 +32,7 @@ struct WiBatch {
     WeightImage w[kMaxImages];
 };
 
-// one thread per weight element of every registered image: split, write W^T and W layouts
+// one thread per weight element of every registered image: split into hi / lo (W layout, ldn)
 __global__ void __launch_bounds__(256) weight_split_kernel(WiBatch b) {
     GSB_PDL_ENTRY();
     for (int q = 0; q < b.n; ++q) {
@@ -40,17 +40,13 @@ __global__ void __launch_bounds__(256) weight_split_kernel(WiBatch b) {
         const int64_t total = (int64_t)w.slots * w.K * w.N;
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
              i += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t s = i / ((int64_t)w.K * w.N);
-            const int64_t r = i - s * w.K * w.N;
-            const int k = (int)(r / w.N), n = (int)(r - (int64_t)k * w.N);
+            const int64_t r = i / w.N;                 // row (slot, k)
+            const int n = (int)(i - r * w.N);
             uint32_t hi, lo;
             umma::split_tf32(w.W[i], hi, lo);
-            const int64_t tn = (s * w.N + n) * w.K + k;            // W^T [s][n][k]
-            const int64_t tk = (s * w.K + k) * w.ldn + n;          // W   [s][k][n] (ldn)
-            w.nn_hi[tn] = __uint_as_float(hi);
-            w.nn_lo[tn] = __uint_as_float(lo);
-            w.nt_hi[tk] = __uint_as_float(hi);
-            w.nt_lo[tk] = __uint_as_float(lo);
+            const int64_t o = r * w.ldn + n;
+            w.hi[o] = __uint_as_float(hi);
+            w.lo[o] = __uint_as_float(lo);
         }
     }
 }
@@ -80,12 +76,9 @@ gsb_status gsb_weight_images_register(const float* W, int32_t slots, int32_t K, 
     w.N = N;
     w.ldn = ldn;
     float* p = static_cast<float*>(img);
-    const size_t nn = ((size_t)slots * N * K + 3) / 4 * 4, nt = ((size_t)slots * K * ldn + 3) / 4 * 4;
-    w.nn_hi = p;
-    w.nn_lo = p + nn;
-    w.nt_hi = p + 2 * nn;
-    w.nt_lo = p + 2 * nn + nt;
-    // padding columns of the W layout stay zero (the NT GEMM reduces over them)
+    w.hi = p;
+    w.lo = p + (size_t)slots * K * ldn;
+    // padding columns stay zero (the NT GEMM reduces over them)
     GSB_CUDA(cudaMemsetAsync(img, 0, img_bytes, (cudaStream_t)stream));
     std::lock_guard<std::mutex> lk(g_wi_mu);
     for (WeightImage& x : g_wi)

@@ -358,16 +358,18 @@ class _TrainerBase:
         self.pipe_graphs = None
         self.pipe_k = 0
         self._wimg_names = []
-        # opt-in (GSB_WIMG=1): measured neutral on the GEMMs and +11.7 us for the refresh on the
-        # mag step (profiles/round2_weight_images.md)
+        # pre-split layer weights for the TMA GEMMs: opt-in (GSB_WIMG=1); the per-step refresh
+        # launch costs more than the B split it saves (profiles/round2_gemm_tma3.md)
         if os.environ.get("GSB_WIMG") == "1":
             self._register_weight_images()
 
     def _register_weight_images(self):
-        """tf32 hi/lo images of the layer weights and the NC decoder (gsb_weight_images_*): the
-        GEMMs then TMA the split B operand instead of splitting W in every CTA; refreshed at the
-        start of every compute phase (after the previous step's Adam)."""
-        self._wimg_names = [f"W{l}" for l in range(self.L)] + (["Wc"] if "Wc" in self.names else [])
+        """tf32 hi/lo images of the layer weights (gsb_weight_images_*): the NN / NT GEMMs then
+        TMA the split B operand instead of splitting W in every CTA; refreshed at the start of
+        every compute phase (after the previous step's Adam).  The NC decoder weight is left
+        out: its class-count row stride is not TMA-addressable (the GEMMs take the cp.async
+        kernel there)."""
+        self._wimg_names = [f"W{l}" for l in range(self.L)]
         self._wimg_bufs = []
         for name in self._wimg_names:
             shp = self.shapes[name]
