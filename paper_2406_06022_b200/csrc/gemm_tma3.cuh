@@ -185,7 +185,6 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
                                                                    const __grid_constant__ CUtensorMap mapB,
                                                                    const __grid_constant__ CUtensorMap mapB2,
                                                                    const __grid_constant__ CUtensorMap mapC, UProb P) {
-    GSB_PDL_ENTRY();
     if (threadIdx.x == 0) trace_mark(P, 0, TG_TRACE - 2);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -221,6 +220,9 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
     __syncthreads();
     umma::tc_fence_after();
     const uint32_t tmem = tmem_sh;
+    // with PDL (GSB_PDL=1) the setup above overlaps the predecessor's tail; nothing it wrote
+    // (row-group sizes, operands) is read before this point
+    GSB_PDL_ENTRY();
 
     const int nct = (P.N + 127) / 128;
     const int kct = (P.d_in + 127) / 128;

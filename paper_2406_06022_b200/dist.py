@@ -289,10 +289,10 @@ class SampleExchange:
                     self.bytes_sent += (ns - self.sc[self.rank]) * 8
                     return 0
                 S = self.S
-                ew = self.srv_wcnt.tolist()                                          # host sync
                 er_t = torch.empty_like(self.srv_wcnt)
-                self._a2a(er_t, self.srv_wcnt, None, None)
-                er = er_t.tolist()
+                self._a2a(er_t, self.srv_wcnt, None, None)                          # edge counts
+                both = torch.cat([self.srv_wcnt, er_t]).tolist()                     # one host sync
+                ew, er = both[:w], both[w:]
                 ns, nr = sum(self.sc), sum(self.rc)
                 self._a2a(self.resp_cnt[:ns * S], self.srv_cnt[:nr * S], [x * S for x in self.sc],
                           [x * S for x in self.rc])                                  # C3: counts
