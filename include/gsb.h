@@ -336,6 +336,11 @@ gsb_status gsb_weight_images_register(const float* W, int32_t slots, int32_t K, 
                                       size_t img_bytes, void* stream);
 gsb_status gsb_weight_images_unregister(const float* W);
 gsb_status gsb_weight_images_refresh(const float* const* Ws, int32_t n, void* stream);
+/* Same, with caller-provided images in W's own layout (hi, lo: device fp32 [slots][K][N],
+ * N % 4 == 0, 16-B aligned) that the caller keeps current -- e.g. with gsb_adam_step_split
+ * over a flat parameter buffer whose hi / lo twins hold the images.  No memset, no copy. */
+gsb_status gsb_weight_images_register_split(const float* W, int32_t slots, int32_t K, int32_t N, float* hi,
+                                            float* lo);
 
 /* Tools: copies n (<= 256) globaltimer stamps recorded by CTA 0 of the last GEMM launched with
  * GSB_GEMM_DBG & 1024 ([role][64]: producer, MMA, splitters, epilogue; slot 63 = start). */
@@ -555,6 +560,12 @@ gsb_status gsb_graph_set_feature_peers(gsb_graph_t g, int32_t ntype, int32_t wor
 gsb_status gsb_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1,
                          float beta2, float eps, int32_t t, const int32_t* t_dev, void* stream);
 /* t_dev: optional device int32 overriding t (CUDA-graph replay). */
+/* Adam that also writes the 3xTF32 split of the updated parameters (hi = rna_tf32(p),
+ * lo = rna_tf32(p - hi); device fp32 [n], 16-B aligned): the weight images of
+ * gsb_weight_images_register_split stay current without a separate pass. */
+gsb_status gsb_adam_step_split(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1,
+                               float beta2, float eps, int32_t t, const int32_t* t_dev, float* hi, float* lo,
+                               void* stream);
 
 /* Add `delta` to a device int32/uint32 counter (graph-capturable step advance). */
 gsb_status gsb_counter_add(int32_t* counter, int32_t delta, void* stream);

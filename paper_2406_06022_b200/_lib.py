@@ -89,6 +89,7 @@ SIGS = {
     "gsb_gemm_trace": [P, i32],
     "gsb_weight_images_bytes": [i32, i32, i32, C.POINTER(sz)],
     "gsb_weight_images_register": [P, i32, i32, i32, P, sz, P],
+    "gsb_weight_images_register_split": [P, i32, i32, i32, P, P],
     "gsb_weight_images_unregister": [P],
     "gsb_weight_images_refresh": [P, i32, P],
     "gsb_blocks_set_exchange": [P, i32, i32, i32, C.POINTER(gsb_exchange_bufs), EXCHANGE_FN, P],
@@ -96,6 +97,7 @@ SIGS = {
                            C.POINTER(i64)],
     "gsb_nc_loss": [P, i64, i32, P, P, i32, P, P, i64, P, P, P, P, P, P, P],
     "gsb_adam_step": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P],
+    "gsb_adam_step_split": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P, P, P],
     "gsb_counter_add": [P, i32, P],
     "gsb_spin": [i64, P],
     "gsb_joint_negatives": [i64, i32, i64, i64, u64, u32, P, i64, P, P],

@@ -10,6 +10,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include "gemm_tma3.cuh"
+#include "umma.cuh"
 #include "gsb_internal.cuh"
 
 namespace gsb {
@@ -242,10 +243,19 @@ gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_de
 // ------------------------------------------------------------------------------------
 // Adam (bias-corrected), float4 vectorised
 // ------------------------------------------------------------------------------------
+// hi / lo (optional): the 3xTF32 split of the updated parameters (hi = rna_tf32(p), lo =
+// rna_tf32(p - hi)) for the GEMMs' weight images, written in the same pass
+__device__ __forceinline__ void adam_split(float x, float* hi, float* lo, int64_t i) {
+    uint32_t h, l;
+    umma::split_tf32(x, h, l);
+    hi[i] = __uint_as_float(h);
+    lo[i] = __uint_as_float(l);
+}
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const float* __restrict__ gr,
                                                    float* __restrict__ m, float* __restrict__ v, int64_t n, float lr,
                                                    float b1, float b2, float eps, float c1, float c2,
-                                                   const int32_t* __restrict__ t_dev) {
+                                                   const int32_t* __restrict__ t_dev, float* __restrict__ hi,
+                                                   float* __restrict__ lo) {
     GSB_PDL_ENTRY();
     __shared__ float sc[2];
     if (t_dev) {   // bias corrections from the device step counter (graph replay), once per block
@@ -275,6 +285,15 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
         reinterpret_cast<float4*>(m)[i] = mi;
         reinterpret_cast<float4*>(v)[i] = vi;
         reinterpret_cast<float4*>(p)[i] = pi;
+        if (hi) {
+            uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
+            umma::split_tf32(pi.x, h0, l0);
+            umma::split_tf32(pi.y, h1, l1);
+            umma::split_tf32(pi.z, h2, l2);
+            umma::split_tf32(pi.w, h3, l3);
+            reinterpret_cast<uint4*>(hi)[i] = make_uint4(h0, h1, h2, h3);
+            reinterpret_cast<uint4*>(lo)[i] = make_uint4(l0, l1, l2, l3);
+        }
     }
     for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
         const float g = gr[i];
@@ -283,6 +302,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
         m[i] = mi;
         v[i] = vi;
         p[i] -= a1 * mi / (sqrtf(vi * r2) + eps);
+        if (hi) adam_split(p[i], hi, lo, i);
     }
 }
 
@@ -695,7 +715,22 @@ gsb_status gsb_adam_step(float* p, const float* g, float* m, float* v, int64_t n
     GSB_CHECK_ARG(((uintptr_t)p & 15) == 0 && ((uintptr_t)g & 15) == 0 && ((uintptr_t)m & 15) == 0 &&
                       ((uintptr_t)v & 15) == 0, "adam buffers must be 16-byte aligned");
     GSB_LAUNCH("adam", adam_kernel, grid_for((n + 3) / 4, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream, p, g, m, v, n, lr,
-               b1, b2, eps, c1, c2, t_dev);
+               b1, b2, eps, c1, c2, t_dev, (float*)nullptr, (float*)nullptr);
+    return GSB_OK;
+}
+
+gsb_status gsb_adam_step_split(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                               float eps, int32_t t, const int32_t* t_dev, float* hi, float* lo, void* stream) {
+    GSB_CHECK_ARG(p && g && m && v && hi && lo && n >= 0 && (t >= 1 || t_dev), "bad argument");
+    if (t < 1) t = 1;
+    if (n == 0) return GSB_OK;
+    float c1 = 1.f - powf(b1, (float)t);
+    float c2 = 1.f - powf(b2, (float)t);
+    GSB_CHECK_ARG(((uintptr_t)p & 15) == 0 && ((uintptr_t)g & 15) == 0 && ((uintptr_t)m & 15) == 0 &&
+                      ((uintptr_t)v & 15) == 0 && ((uintptr_t)hi & 15) == 0 && ((uintptr_t)lo & 15) == 0,
+                  "adam buffers must be 16-byte aligned");
+    GSB_LAUNCH("adam", adam_kernel, grid_for((n + 3) / 4, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream, p, g, m, v, n, lr,
+               b1, b2, eps, c1, c2, t_dev, hi, lo);
     return GSB_OK;
 }
 

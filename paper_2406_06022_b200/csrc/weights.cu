@@ -91,6 +91,30 @@ gsb_status gsb_weight_images_register(const float* W, int32_t slots, int32_t K, 
     return GSB_OK;
 }
 
+gsb_status gsb_weight_images_register_split(const float* W, int32_t slots, int32_t K, int32_t N, float* hi,
+                                            float* lo) {
+    GSB_CHECK_ARG(W && hi && lo && slots >= 1 && K >= 1 && N >= 1, "bad argument");
+    GSB_CHECK_ARG(N % 4 == 0, "N %d must be a multiple of 4 (16-B rows)", N);
+    GSB_CHECK_ARG(((uintptr_t)hi & 15) == 0 && ((uintptr_t)lo & 15) == 0, "images must be 16-byte aligned");
+    WeightImage w;
+    w.W = W;
+    w.slots = slots;
+    w.K = K;
+    w.N = N;
+    w.ldn = N;
+    w.hi = hi;
+    w.lo = lo;
+    std::lock_guard<std::mutex> lk(g_wi_mu);
+    for (WeightImage& x : g_wi)
+        if (x.W == W) {
+            x = w;
+            return GSB_OK;
+        }
+    GSB_CHECK_ARG(g_wi.size() < 64, "too many weight images");
+    g_wi.push_back(w);
+    return GSB_OK;
+}
+
 gsb_status gsb_weight_images_unregister(const float* W) {
     std::lock_guard<std::mutex> lk(g_wi_mu);
     for (size_t i = 0; i < g_wi.size(); ++i)

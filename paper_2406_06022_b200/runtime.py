@@ -358,10 +358,14 @@ class _TrainerBase:
         self.pipe_graphs = None
         self.pipe_k = 0
         self._wimg_names = []
-        # pre-split layer weights for the TMA GEMMs: opt-in (GSB_WIMG=1); the per-step refresh
-        # launch costs more than the B split it saves (profiles/round2_gemm_tma3.md)
-        if os.environ.get("GSB_WIMG") == "1":
+        self.flat_hi = self.flat_lo = None
+        # pre-split layer weights for the TMA GEMMs (default; GSB_WIMG=0 off, =1 the separate
+        # per-step refresh launch instead of Adam's fused split, profiles/round2_gemm_tma3.md)
+        wimg = os.environ.get("GSB_WIMG", "adam")
+        if wimg == "1":
             self._register_weight_images()
+        elif wimg == "adam":
+            self._register_weight_images_adam()
 
     def _register_weight_images(self):
         """tf32 hi/lo images of the layer weights (gsb_weight_images_*): the NN / NT GEMMs then
@@ -381,9 +385,43 @@ class _TrainerBase:
             self._wimg_bufs.append(buf)
         self._wimg_ptrs = (C.c_void_p * len(self._wimg_names))(*[self._pp(n).value for n in self._wimg_names])
 
-    def _refresh_weight_images(self, s):
+    def _register_weight_images_adam(self):
+        """Weight images kept current by Adam itself (gsb_adam_step_split writes the hi / lo split
+        of every updated parameter into twins of the flat buffer): the layer weights' slices of
+        the twins are registered as their images; no per-step refresh launch.  Computed once
+        here; _params_changed() recomputes them after any write to `flat` outside Adam."""
+        names = [f"W{l}" for l in range(self.L)]
+        names = [n for n in names if len(self.shapes[n]) == 3 and int(self.shapes[n][2]) % 4 == 0]
+        if not names:
+            return
+        self.flat_hi = torch.zeros_like(self.flat)
+        self.flat_lo = torch.zeros_like(self.flat)
+        for name in names:
+            slots, K, N = (int(x) for x in self.shapes[name])
+            k = self.names.index(name)
+            off = int(self.offsets[k]) * 4
+            call("gsb_weight_images_register_split", self._pp(name), slots, K, N,
+                 C.c_void_p(self.flat_hi.data_ptr() + off), C.c_void_p(self.flat_lo.data_ptr() + off))
+        self._wimg_names = names
+        self._wimg_ptrs = (C.c_void_p * len(names))(*[self._pp(n).value for n in names])
+        self._wimg_adam = True
+        self._params_changed()
+
+    def _params_changed(self, s=None):
+        """Recompute the weight images after `flat` was written outside Adam (torch in-place
+        writes to `flat` or its pview()s are detected by the tensor's version counter)."""
         if self._wimg_names:
+            st = s if isinstance(s, C.c_void_p) else _stream(s)
+            call("gsb_weight_images_refresh", self._wimg_ptrs, len(self._wimg_names), st)
+            self._img_version = self.flat._version
+
+    def _refresh_weight_images(self, s):
+        if not self._wimg_names:
+            return
+        if not getattr(self, "_wimg_adam", False):
             call("gsb_weight_images_refresh", self._wimg_ptrs, len(self._wimg_names), s)
+        elif self.flat._version != getattr(self, "_img_version", -1):
+            self._params_changed(s)
 
     def __del__(self):
         try:
@@ -512,13 +550,16 @@ class _TrainerBase:
 
     def optimizer_step(self, stream=None, t_dev: bool = False):
         self._sparse_update(stream)
-        if t_dev:
+        t_ptr = C.c_void_p(self.counters.data_ptr() + 4) if t_dev else None
+        if not t_dev:
+            self.t += 1
+        t = 1 if t_dev else self.t
+        if self.flat_hi is not None:      # Adam also refreshes the GEMMs' weight images
+            call("gsb_adam_step_split", _ptr(self.flat), _ptr(self.grad), _ptr(self.m), _ptr(self.v), self.n_params,
+                 self.lr, 0.9, 0.999, 1e-8, t, t_ptr, _ptr(self.flat_hi), _ptr(self.flat_lo), _stream(stream))
+        else:
             call("gsb_adam_step", _ptr(self.flat), _ptr(self.grad), _ptr(self.m), _ptr(self.v), self.n_params,
-                 self.lr, 0.9, 0.999, 1e-8, 1, C.c_void_p(self.counters.data_ptr() + 4), _stream(stream))
-            return
-        self.t += 1
-        call("gsb_adam_step", _ptr(self.flat), _ptr(self.grad), _ptr(self.m), _ptr(self.v), self.n_params, self.lr,
-             0.9, 0.999, 1e-8, self.t, None, _stream(stream))
+                 self.lr, 0.9, 0.999, 1e-8, t, t_ptr, _stream(stream))
 
     # CUDA graph of one whole step ----------------------------------------------------------
     def capture(self, step0: int, ws: int = 1, allreduce=None):
@@ -531,6 +572,7 @@ class _TrainerBase:
         self.counters[0] = step0
         self.counters[1] = self.t
         self.graph_ws = ws
+        self._refresh_weight_images(_stream())   # images current before capture (none captured)
         torch.cuda.synchronize()
         launches0 = lib().gsb_launch_count()
         g = torch.cuda.CUDAGraph()
@@ -551,6 +593,7 @@ class _TrainerBase:
         return g
 
     def replay(self):
+        self._refresh_weight_images(_stream())   # only if flat was written since (version check)
         self.graph.replay()
         if self.graph_allreduce is not None:
             self._peer_push()
@@ -607,6 +650,7 @@ class _TrainerBase:
             raise GsbError("pipeline needs device-resident sizes (no all-to-all exchange mode)")
         self.enable_prefetch()
         self.pipe_ws, self.pipe_allreduce = ws, allreduce
+        self._refresh_weight_images(_stream())   # images current before capture (none captured)
         sample_graph = getattr(self, "sample_graph", True)   # False: NCCL frontier exchange (host-synced)
         if use_graph and self.pipe_graphs is None:
             torch.cuda.synchronize()
@@ -647,6 +691,7 @@ class _TrainerBase:
         b = self.pipe_k & 1
         nb = b ^ 1
         main = torch.cuda.current_stream()
+        self._refresh_weight_images(_stream())   # only if flat was written since (version check)
 
         def sample_next():
             self.side.wait_event(self.ev_c)          # buffer nb is free once batch k-1 computed
