@@ -562,10 +562,14 @@ gsb_status gsb_adam_step(float* p, const float* g, float* m, float* v, int64_t n
 /* t_dev: optional device int32 overriding t (CUDA-graph replay). */
 /* Adam that also writes the 3xTF32 split of the updated parameters (hi = rna_tf32(p),
  * lo = rna_tf32(p - hi); device fp32 [n], 16-B aligned): the weight images of
- * gsb_weight_images_register_split stay current without a separate pass. */
+ * gsb_weight_images_register_split stay current without a separate pass.  Optionally (pad_hi
+ * non-null) the split of one segment [pad_off, pad_off + pad_rows*pad_cols) is also written
+ * row by row with stride pad_ld into pad_hi / pad_lo (the padded image of a weight whose own
+ * row stride is not 16-B aligned, e.g. a 349-class decoder). */
 gsb_status gsb_adam_step_split(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1,
                                float beta2, float eps, int32_t t, const int32_t* t_dev, float* hi, float* lo,
-                               void* stream);
+                               int64_t pad_off, int32_t pad_rows, int32_t pad_cols, int32_t pad_ld, float* pad_hi,
+                               float* pad_lo, void* stream);
 
 /* Add `delta` to a device int32/uint32 counter (graph-capturable step advance). */
 gsb_status gsb_counter_add(int32_t* counter, int32_t delta, void* stream);

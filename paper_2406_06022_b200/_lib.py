@@ -97,7 +97,7 @@ SIGS = {
                            C.POINTER(i64)],
     "gsb_nc_loss": [P, i64, i32, P, P, i32, P, P, i64, P, P, P, P, P, P, P],
     "gsb_adam_step": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P],
-    "gsb_adam_step_split": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P, P, P],
+    "gsb_adam_step_split": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P, P, i64, i32, i32, i32, P, P, P],
     "gsb_counter_add": [P, i32, P],
     "gsb_spin": [i64, P],
     "gsb_joint_negatives": [i64, i32, i64, i64, u64, u32, P, i64, P, P],

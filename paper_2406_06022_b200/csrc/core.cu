@@ -251,11 +251,26 @@ __device__ __forceinline__ void adam_split(float x, float* hi, float* lo, int64_
     hi[i] = __uint_as_float(h);
     lo[i] = __uint_as_float(l);
 }
+// pad: one parameter segment [off, off + rows*cols) whose split is also written with a padded
+// row stride (ld) into pad_hi / pad_lo (a weight whose own row stride is not 16-B aligned)
+struct AdamPad {
+    int64_t off;
+    int32_t rows, cols, ld;
+    float *hi, *lo;
+};
+__device__ __forceinline__ void adam_pad(const AdamPad& pd, int64_t i, uint32_t h, uint32_t l) {
+    const int64_t q = i - pd.off;
+    if (q < 0 || q >= (int64_t)pd.rows * pd.cols) return;
+    const uint32_t r = (uint32_t)q / (uint32_t)pd.cols;
+    const int64_t o = (int64_t)r * pd.ld + ((uint32_t)q - r * (uint32_t)pd.cols);
+    pd.hi[o] = __uint_as_float(h);
+    pd.lo[o] = __uint_as_float(l);
+}
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const float* __restrict__ gr,
                                                    float* __restrict__ m, float* __restrict__ v, int64_t n, float lr,
                                                    float b1, float b2, float eps, float c1, float c2,
                                                    const int32_t* __restrict__ t_dev, float* __restrict__ hi,
-                                                   float* __restrict__ lo) {
+                                                   float* __restrict__ lo, AdamPad pd) {
     GSB_PDL_ENTRY();
     __shared__ float sc[2];
     if (t_dev) {   // bias corrections from the device step counter (graph replay), once per block
@@ -293,6 +308,12 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
             umma::split_tf32(pi.w, h3, l3);
             reinterpret_cast<uint4*>(hi)[i] = make_uint4(h0, h1, h2, h3);
             reinterpret_cast<uint4*>(lo)[i] = make_uint4(l0, l1, l2, l3);
+            if (pd.hi && 4 * i + 3 >= pd.off && 4 * i < pd.off + (int64_t)pd.rows * pd.cols) {
+                adam_pad(pd, 4 * i, h0, l0);
+                adam_pad(pd, 4 * i + 1, h1, l1);
+                adam_pad(pd, 4 * i + 2, h2, l2);
+                adam_pad(pd, 4 * i + 3, h3, l3);
+            }
         }
     }
     for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -302,7 +323,10 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
         m[i] = mi;
         v[i] = vi;
         p[i] -= a1 * mi / (sqrtf(vi * r2) + eps);
-        if (hi) adam_split(p[i], hi, lo, i);
+        if (hi) {
+            adam_split(p[i], hi, lo, i);
+            if (pd.hi) adam_pad(pd, i, __float_as_uint(hi[i]), __float_as_uint(lo[i]));
+        }
     }
 }
 
@@ -715,13 +739,18 @@ gsb_status gsb_adam_step(float* p, const float* g, float* m, float* v, int64_t n
     GSB_CHECK_ARG(((uintptr_t)p & 15) == 0 && ((uintptr_t)g & 15) == 0 && ((uintptr_t)m & 15) == 0 &&
                       ((uintptr_t)v & 15) == 0, "adam buffers must be 16-byte aligned");
     GSB_LAUNCH("adam", adam_kernel, grid_for((n + 3) / 4, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream, p, g, m, v, n, lr,
-               b1, b2, eps, c1, c2, t_dev, (float*)nullptr, (float*)nullptr);
+               b1, b2, eps, c1, c2, t_dev, (float*)nullptr, (float*)nullptr, AdamPad{0, 0, 0, 0, nullptr, nullptr});
     return GSB_OK;
 }
 
 gsb_status gsb_adam_step_split(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
-                               float eps, int32_t t, const int32_t* t_dev, float* hi, float* lo, void* stream) {
+                               float eps, int32_t t, const int32_t* t_dev, float* hi, float* lo, int64_t pad_off,
+                               int32_t pad_rows, int32_t pad_cols, int32_t pad_ld, float* pad_hi, float* pad_lo,
+                               void* stream) {
     GSB_CHECK_ARG(p && g && m && v && hi && lo && n >= 0 && (t >= 1 || t_dev), "bad argument");
+    GSB_CHECK_ARG(!pad_hi || (pad_lo && pad_off >= 0 && pad_rows >= 1 && pad_cols >= 1 && pad_ld >= pad_cols &&
+                              pad_off + (int64_t)pad_rows * pad_cols <= n),
+                  "bad padded segment");
     if (t < 1) t = 1;
     if (n == 0) return GSB_OK;
     float c1 = 1.f - powf(b1, (float)t);
@@ -730,7 +759,7 @@ gsb_status gsb_adam_step_split(float* p, const float* g, float* m, float* v, int
                       ((uintptr_t)v & 15) == 0 && ((uintptr_t)hi & 15) == 0 && ((uintptr_t)lo & 15) == 0,
                   "adam buffers must be 16-byte aligned");
     GSB_LAUNCH("adam", adam_kernel, grid_for((n + 3) / 4, 256, kNumSMs * 4), 256, 0, (cudaStream_t)stream, p, g, m, v, n, lr,
-               b1, b2, eps, c1, c2, t_dev, hi, lo);
+               b1, b2, eps, c1, c2, t_dev, hi, lo, AdamPad{pad_off, pad_rows, pad_cols, pad_ld, pad_hi, pad_lo});
     return GSB_OK;
 }
 

@@ -173,6 +173,16 @@ __device__ __forceinline__ void t3_epi_direct(const UProb& P, const UCursor& c, 
             if (P.ksplit > 1) atomicAdd(out + k, v[e]);
             else out[k] = v[e];
         }
+    } else {                  // TN with a C the TMA cannot address (e.g. a 349-column dWc)
+        const int k = c.c0 + r;
+        if (k >= P.d_in) return;
+        float* out = P.C + (int64_t)P.rg.slot_w[c.t][c.s] * P.bslot + (int64_t)k * P.ldc;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            const int n = c.n0 + col + e;
+            if (n >= P.N) break;
+            atomicAdd(out + n, v[e]);
+        }
     }
 }
 
@@ -391,7 +401,7 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
             const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(as * 128);
             const bool split = (MODE == UMMA_TN) || P.ksplit > 1;
             // a tile cut by its group end (next group's rows follow) cannot take a box store
-            const bool direct = (MODE != UMMA_TN) && (c.row0 + 128 > c.rlim);
+            const bool direct = P.cdirect || ((MODE != UMMA_TN) && (c.row0 + 128 > c.rlim));
 #pragma unroll 1
             for (int cc = 0; cc < 4; ++cc) {
                 const int col = cc * 32;
@@ -498,7 +508,8 @@ inline gsb_status launch_gemm3(const char* name, UProb P, int64_t tiles_upper, i
         const int64_t db[2] = {b_w, b_rows}, sb[1] = {P.ldb};
         const int64_t dc[2] = {P.N, c_rows}, sc[1] = {P.ldc};
         const int ba[2] = {32, 128}, bb[2] = {32, 32}, bc[2] = {32, 128};
-        ok = encode_tmap_nd(&ma, P.A, 2, da, sa, ba, SW128) && encode_tmap_nd(&mc, P.C, 2, dc, sc, bc, SW128);
+        ok = encode_tmap_nd(&ma, P.A, 2, da, sa, ba, SW128) &&
+             (P.cdirect || encode_tmap_nd(&mc, P.C, 2, dc, sc, bc, SW128));
         if (wi) {
             const int64_t di[2] = {wi->N, (int64_t)wi->slots * wi->K}, si[1] = {wi->ldn};
             ok = ok && encode_tmap_nd(&mb, wi->hi, 2, di, si, bb, SW32) && encode_tmap_nd(&mb2, wi->lo, 2, di, si, bb, SW32);
@@ -510,7 +521,8 @@ inline gsb_status launch_gemm3(const char* name, UProb P, int64_t tiles_upper, i
         const int64_t db[2] = {b_w, b_rows}, sb[1] = {P.ldb};
         const int64_t dc[3] = {P.d_in, c_slots, c_rows}, sc[2] = {P.d_in, P.ldc};
         const int ba[2] = {32, 128}, bb[2] = {32, 128}, bc[3] = {32, 1, 128};
-        ok = encode_tmap_nd(&ma, P.A, 2, da, sa, ba, SW128) && encode_tmap_nd(&mc, P.C, 3, dc, sc, bc, SW128);
+        ok = encode_tmap_nd(&ma, P.A, 2, da, sa, ba, SW128) &&
+             (P.cdirect || encode_tmap_nd(&mc, P.C, 3, dc, sc, bc, SW128));
         if (wi) {
             const int64_t di[2] = {wi->N, (int64_t)wi->slots * wi->K}, si[1] = {wi->ldn};
             ok = ok && encode_tmap_nd(&mb, wi->hi, 2, di, si, bb, SW128) &&
@@ -525,9 +537,10 @@ inline gsb_status launch_gemm3(const char* name, UProb P, int64_t tiles_upper, i
                       sc[2] = {P.ldc, P.bslot > 0 ? P.bslot : (int64_t)P.d_in * P.ldc};
         const int ba[2] = {32, 32}, bb[2] = {32, 32}, bc[3] = {32, 128, 1};
         ok = encode_tmap_nd(&ma, P.A, 2, da, sa, ba, SW32) && encode_tmap_nd(&mb, P.B, 2, db, sb, bb, SW32) &&
-             encode_tmap_nd(&mc, P.C, 3, dc, sc, bc, SW128);
+             (P.cdirect || encode_tmap_nd(&mc, P.C, 3, dc, sc, bc, SW128));
     }
     if (!ok) return GSB_OK;
+    if (P.cdirect) mc = ma;      // C not TMA-addressable: per-thread stores, map unused
     P.bimg = wi ? 1 : 0;
     if (!wi) mb2 = mb;
     // operand ring depth: 3 stages (225 KB, one CTA per SM) or 2 (161 KB: leaves room for
@@ -577,22 +590,26 @@ inline gsb_status launch_gemm_v(const char* name, UProb P, int64_t tiles_upper, 
         Q.brow = (int)(Q.bslot / std::max<int64_t>(Q.ldb, 1));
         Q.bimg = 0;
         auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-        bool ok = al(Q.A) && al(Q.B) && al(Q.C) && (Q.lda & 3) == 0 && (Q.ldb & 3) == 0 && (Q.ldc & 3) == 0 &&
-                  a_rows >= 1 && b_rows >= 1 && (Q.bslot & 3) == 0;
+        // registered weight image of the B operand (NN / NT): pre-split hi / lo, TMA'd directly
+        // (also when W itself is not TMA-addressable, e.g. the 349-column decoder weight)
+        static const bool no_img = getenv("GSB_NO_WIMG") != nullptr;    // A/B knob
+        const WeightImage* wi = (MODE != UMMA_TN && !no_img) ? find_weight_image(Q.B) : nullptr;
+        if (wi && !(wi->N == Q.N && wi->K == Q.d_in &&
+                    ((int64_t)wi->K * wi->N == Q.bslot || (Q.bslot == 0 && wi->slots == 1))))
+            wi = nullptr;
+        const bool b_ok = wi || (al(Q.B) && (Q.ldb & 3) == 0 &&
+                                 (MODE == UMMA_TN || Q.bslot % std::max<int64_t>(Q.ldb, 1) == 0));
+        // C: TMA store / reduce-add when addressable, else per-thread stores / atomics
+        Q.cdirect = !(al(Q.C) && (Q.ldc & 3) == 0 && (MODE != UMMA_TN || (Q.bslot & 3) == 0));
+        bool ok = al(Q.A) && (Q.lda & 3) == 0 && b_ok && a_rows >= 1 && b_rows >= 1;
         int64_t c_slots = 1;
         if (MODE == UMMA_TN) {
             ok = ok && Q.rows_per_chunk % 32 == 0;
             for (int t = 0; t < Q.rg.G; ++t)
                 for (int k = 0; k < Q.rg.ks[t]; ++k) c_slots = std::max<int64_t>(c_slots, Q.rg.slot_w[t][k] + 1);
-        } else {
-            ok = ok && Q.bslot % std::max<int64_t>(Q.ldb, 1) == 0;
-            if (MODE == UMMA_NT) c_slots = (Q.ldc % Q.d_in == 0) ? Q.ldc / Q.d_in : 1;
+        } else if (MODE == UMMA_NT) {
+            c_slots = (Q.ldc % Q.d_in == 0) ? Q.ldc / Q.d_in : 1;
         }
-        // registered weight image of the B operand (NN / NT): pre-split hi / lo, TMA'd directly
-        static const bool no_img = getenv("GSB_NO_WIMG") != nullptr;    // A/B knob
-        const WeightImage* wi = (MODE != UMMA_TN && !no_img) ? find_weight_image(Q.B) : nullptr;
-        if (wi && !(wi->N == Q.N && wi->K == Q.d_in && (int64_t)wi->K * wi->N == Q.bslot || (Q.bslot == 0 && wi->slots == 1 && wi->K == Q.d_in)))
-            wi = nullptr;
         if (ok) {
             bool launched = false;
             const gsb_status st = launch_gemm3<MODE>(name, Q, tiles_upper, a_rows, a_w, b_rows, b_w, a_rows, c_slots, s,

@@ -67,6 +67,7 @@ struct UProb {
     int dbg;               // gemm_tma.cuh A/B knobs (GSB_GEMM_DBG): 1 no split, 2 no MMA, 4 no TMA
     int brow;              // gemm_tma.cuh: rows of B per weight slot (bslot / ldb)
     int bimg;              // gemm_tma.cuh: B comes pre-split (weight images, mapB = hi, mapB2 = lo)
+    int cdirect;           // gemm_tma3.cuh: C is not TMA-addressable: per-thread stores / atomics
 };
 
 #ifndef GSB_UM_THREADS

@@ -1464,8 +1464,9 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
         GSB_CUDA(cudaMemsetAsync(dbc, 0, sizeof(float) * (size_t)C, s));
         UProb P{};
         P.rg = rg; P.A = h; P.lda = d; P.B = logits_ws; P.ldb = ldl; P.d_in = d; P.N = C; P.C = dWc; P.ldc = C;
-        P.bslot = 0; P.db = dbc; P.rows_per_chunk = 64;
-        gsb_status st = launch_gemm_v<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, 64) * ceil_div(d, 128) * ceil_div(C, 128),
+        static const int rpc = getenv("GSB_DWC_RPC") ? atoi(getenv("GSB_DWC_RPC")) : 64;   // A/B knob
+        P.bslot = 0; P.db = dbc; P.rows_per_chunk = rpc;
+        gsb_status st = launch_gemm_v<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, rpc) * ceil_div(d, 128) * ceil_div(C, 128),
                                              n, d, n, C, s);
         if (st != GSB_OK) return st;
     }

@@ -37,14 +37,13 @@ __global__ void __launch_bounds__(256) weight_split_kernel(WiBatch b) {
     GSB_PDL_ENTRY();
     for (int q = 0; q < b.n; ++q) {
         const WeightImage& w = b.w[q];
-        const int64_t total = (int64_t)w.slots * w.K * w.N;
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-             i += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t r = i / w.N;                 // row (slot, k)
-            const int n = (int)(i - r * w.N);
+        const uint32_t total = (uint32_t)w.slots * (uint32_t)w.K * (uint32_t)w.N;   // < 2^32 (checked)
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+            const uint32_t r = i / (uint32_t)w.N;       // row (slot, k)
+            const int n = (int)(i - r * (uint32_t)w.N);
             uint32_t hi, lo;
             umma::split_tf32(w.W[i], hi, lo);
-            const int64_t o = r * w.ldn + n;
+            const int64_t o = (int64_t)r * w.ldn + n;
             w.hi[o] = __uint_as_float(hi);
             w.lo[o] = __uint_as_float(lo);
         }
@@ -66,6 +65,7 @@ gsb_status gsb_weight_images_bytes(int32_t slots, int32_t K, int32_t N, size_t* 
 gsb_status gsb_weight_images_register(const float* W, int32_t slots, int32_t K, int32_t N, void* img,
                                       size_t img_bytes, void* stream) {
     GSB_CHECK_ARG(W && img && slots >= 1 && K >= 1 && N >= 1, "bad argument");
+    GSB_CHECK_ARG((int64_t)slots * K * N < ((int64_t)1 << 32), "weight too large for an image");
     GSB_CHECK_ARG(((uintptr_t)img & 15) == 0, "image buffer must be 16-byte aligned");
     const int ldn = (N + 3) / 4 * 4;
     GSB_CHECK_ARG(img_bytes >= sizeof(float) * wi_floats(slots, K, N, ldn), "image buffer too small");

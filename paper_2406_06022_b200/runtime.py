@@ -402,9 +402,23 @@ class _TrainerBase:
             off = int(self.offsets[k]) * 4
             call("gsb_weight_images_register_split", self._pp(name), slots, K, N,
                  C.c_void_p(self.flat_hi.data_ptr() + off), C.c_void_p(self.flat_lo.data_ptr() + off))
+        self._wimg_adam = True
+        # the NC decoder weight: its class-count rows are not 16-B aligned, so its image lives in
+        # its own padded buffer, written by the same Adam pass (gsb_adam_step_split's segment)
+        self._adam_pad = (0, 0, 0, 0, None, None)
+        if "Wc" in self.names:
+            K, N = (int(x) for x in self.shapes["Wc"])
+            nb = C.c_size_t()
+            call("gsb_weight_images_bytes", 1, K, N, C.byref(nb))
+            buf = torch.zeros(int(nb.value), dtype=torch.uint8, device=self.device)
+            call("gsb_weight_images_register", self._pp("Wc"), 1, K, N, _ptr(buf), buf.numel(), _stream())
+            ldn = (N + 3) // 4 * 4
+            self._wimg_pad_buf = buf
+            self._adam_pad = (int(self.offsets[self.names.index("Wc")]), K, N, ldn, C.c_void_p(buf.data_ptr()),
+                              C.c_void_p(buf.data_ptr() + K * ldn * 4))
+            names = names + ["Wc"]
         self._wimg_names = names
         self._wimg_ptrs = (C.c_void_p * len(names))(*[self._pp(n).value for n in names])
-        self._wimg_adam = True
         self._params_changed()
 
     def _params_changed(self, s=None):
@@ -416,6 +430,12 @@ class _TrainerBase:
             self._img_version = self.flat._version
 
     def _refresh_weight_images(self, s):
+        """Start of a compute phase: images refreshed when stale (with Adam's split: only after
+        writes to `flat` outside Adam)."""
+        self._sync_images(s)
+
+    def _sync_images(self, s):
+        """Weight images stale only after writes to `flat` outside Adam (or without Adam's split)."""
         if not self._wimg_names:
             return
         if not getattr(self, "_wimg_adam", False):
@@ -556,7 +576,8 @@ class _TrainerBase:
         t = 1 if t_dev else self.t
         if self.flat_hi is not None:      # Adam also refreshes the GEMMs' weight images
             call("gsb_adam_step_split", _ptr(self.flat), _ptr(self.grad), _ptr(self.m), _ptr(self.v), self.n_params,
-                 self.lr, 0.9, 0.999, 1e-8, t, t_ptr, _ptr(self.flat_hi), _ptr(self.flat_lo), _stream(stream))
+                 self.lr, 0.9, 0.999, 1e-8, t, t_ptr, _ptr(self.flat_hi), _ptr(self.flat_lo), *self._adam_pad,
+                 _stream(stream))
         else:
             call("gsb_adam_step", _ptr(self.flat), _ptr(self.grad), _ptr(self.m), _ptr(self.v), self.n_params,
                  self.lr, 0.9, 0.999, 1e-8, t, t_ptr, _stream(stream))
@@ -572,7 +593,7 @@ class _TrainerBase:
         self.counters[0] = step0
         self.counters[1] = self.t
         self.graph_ws = ws
-        self._refresh_weight_images(_stream())   # images current before capture (none captured)
+        self._sync_images(_stream())   # images current before capture (none captured)
         torch.cuda.synchronize()
         launches0 = lib().gsb_launch_count()
         g = torch.cuda.CUDAGraph()
@@ -593,7 +614,7 @@ class _TrainerBase:
         return g
 
     def replay(self):
-        self._refresh_weight_images(_stream())   # only if flat was written since (version check)
+        self._sync_images(_stream())   # only if flat was written since (version check)
         self.graph.replay()
         if self.graph_allreduce is not None:
             self._peer_push()
@@ -650,7 +671,7 @@ class _TrainerBase:
             raise GsbError("pipeline needs device-resident sizes (no all-to-all exchange mode)")
         self.enable_prefetch()
         self.pipe_ws, self.pipe_allreduce = ws, allreduce
-        self._refresh_weight_images(_stream())   # images current before capture (none captured)
+        self._sync_images(_stream())   # images current before capture (none captured)
         sample_graph = getattr(self, "sample_graph", True)   # False: NCCL frontier exchange (host-synced)
         if use_graph and self.pipe_graphs is None:
             torch.cuda.synchronize()
@@ -691,7 +712,7 @@ class _TrainerBase:
         b = self.pipe_k & 1
         nb = b ^ 1
         main = torch.cuda.current_stream()
-        self._refresh_weight_images(_stream())   # only if flat was written since (version check)
+        self._sync_images(_stream())   # only if flat was written since (version check)
 
         def sample_next():
             self.side.wait_event(self.ev_c)          # buffer nb is free once batch k-1 computed
