@@ -33,7 +33,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-o", SO + ".tmp", *sources()]
+    extra = os.environ.get("GSB_NVCC_EXTRA", "").split()   # tools: -D knobs for A/B builds
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-o", SO + ".tmp", *sources()]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
