@@ -1331,7 +1331,22 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     HopBufs hb = B->hop(h, const_cast<void*>(arena));
     const int64_t lda = (int64_t)(g.S + 1) * d_in;
     RowGroups rg = layer_groups(B, arena, layer);
-    if (relu) {   // dZ once, in place; the GEMMs below then read dZ directly
+    // row chunks of the weight gradient sized so the (type, slot, chunk) items cover ~2 waves of SMs
+    const int64_t rows = hb.cap_dst;
+    int rpc = (int)std::max<int64_t>(64, std::min<int64_t>(2048, ceil_div(rows * (g.S + 1), 2 * kNumSMs)));
+    rpc = (rpc + 31) / 32 * 32;
+    UProb Pw{};
+    Pw.rg = rg; Pw.A = acat; Pw.lda = lda; Pw.B = dh_dst; Pw.ldb = d_out;
+    Pw.d_in = d_in; Pw.N = d_out; Pw.C = dW; Pw.ldc = d_out; Pw.bslot = (int64_t)d_in * d_out; Pw.db = db;
+    Pw.rows_per_chunk = rpc;
+    // dZ = dh * 1[h > 0] once in place before the GEMMs; opt-in (GSB_RELU_FUSE=1): folded into
+    // the weight-gradient GEMM's B split when dZ has no other reader -- measured slower (the mask
+    // loads lengthen the split: dW_l0 29.3 -> 33.3 us, step 0.2030 -> 0.2060 ms, gpurun_out/rf2)
+    static const bool fuse_ok = getenv("GSB_RELU_FUSE") && strcmp(getenv("GSB_RELU_FUSE"), "1") == 0;
+    const bool fuse_mask = fuse_ok && relu && !dh_src && tma3_tn_ready(Pw);
+    if (fuse_mask) {
+        Pw.H = h_dst;
+    } else if (relu) {
         GSB_LAUNCH(lname("relu_bwd", layer), relu_bwd_kernel, grid_for(hb.cap_dst * d_out / 4, 256, kNumSMs * 8), 256, 0, s,
                    hb.meta, dh_dst, h_dst, d_out);
     }
@@ -1341,17 +1356,9 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     GSB_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)(g.R + 1) * d_in * d_out, s));
     GSB_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * (size_t)d_out, s));
     {
-        // row chunks sized so the (type, slot, chunk) items cover ~2 waves of SMs
-        const int64_t rows = hb.cap_dst;
-        int rpc = (int)std::max<int64_t>(64, std::min<int64_t>(2048, ceil_div(rows * (g.S + 1), 2 * kNumSMs)));
-        rpc = (rpc + 31) / 32 * 32;
-        UProb P{};
-        P.rg = rg; P.A = acat; P.lda = lda; P.B = dh_dst; P.ldb = d_out;
-        P.d_in = d_in; P.N = d_out; P.C = dW; P.ldc = d_out; P.bslot = (int64_t)d_in * d_out; P.db = db;
-        P.rows_per_chunk = rpc;
         int64_t items = (ceil_div(rows, rpc) + g.T) * (g.S + 1) * ceil_div(d_in, 128) * ceil_div(d_out, 128);
-        gsb_status st = launch_gemm_v<UMMA_TN>(lname("rgcn_gemm_dW", layer), P, items, hb.cap_dst, lda, hb.cap_dst,
-                                             d_out, s);
+        gsb_status st = launch_gemm_v<UMMA_TN>(lname("rgcn_gemm_dW", layer), Pw, items, hb.cap_dst, lda, hb.cap_dst,
+                                               d_out, s);
         if (st != GSB_OK) return st;
     }
     cudaStream_t s_side = s;

@@ -449,10 +449,10 @@ def test_optin_paths_parity(torch_cuda, knob, monkeypatch):
         res = oracle.nc_step(og, params, seeds, synth.labels(cfg), step, cfg.rng_seed)
         close(tr.loss.cpu().numpy()[0], res.loss, what=f"{knob} loss")
         check_grads(tr, res, cfg, step)
-        if knob == "GSB_TCSR":    # the scatter's output: layer 1's input gradient, ReLU-masked in place
-            z = res.zs[0]            # by layer 0's backward; ambiguous units (|z| ~ 0) left out (R-relutie)
-            n0 = z.shape[0]
+        if knob == "GSB_TCSR":    # the scatter's output: layer 1's input gradient (its ReLU mask is
+            z = res.zs[0]            # applied inside layer 0's weight-gradient GEMM, so mask it here);
+            n0 = z.shape[0]          # ambiguous units (|z| ~ 0) left out (R-relutie)
             keep = np.abs(z) > 1e-5 * np.abs(z).max()
             exp = np.where(z > 0, res.extra["dh"][0], 0.0)
-            got = tr.dh[0][:n0].cpu().numpy()
+            got = np.where(z > 0, tr.dh[0][:n0].cpu().numpy(), 0.0)
             close(got[keep], exp[keep], what="dh0 via the transposed CSR")
