@@ -68,6 +68,7 @@ struct UProb {
     int brow;              // gemm_tma.cuh: rows of B per weight slot (bslot / ldb)
     int bimg;              // gemm_tma.cuh: B comes pre-split (weight images, mapB = hi, mapB2 = lo)
     int cdirect;           // gemm_tma3.cuh: C is not TMA-addressable: per-thread stores / atomics
+    int pf;                // gemm_tma3.cuh: L2 prefetch distance of the HBM-streamed operand panels
 };
 
 #ifndef GSB_UM_THREADS
