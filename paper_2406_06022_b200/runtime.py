@@ -890,9 +890,10 @@ class LPTrainer(_TrainerBase):
         self.iv = torch.empty(B, dtype=torch.int32, device=dev)
         self.ineg = torch.empty(max(self.n_neg, 1), dtype=torch.int32, device=dev)
         self.pos_w = torch.ones(B, dtype=torch.float32, device=dev)    # Eq. 5 weights (loss_kind 2)
-        # the LP sample phase (negatives, seed set, exclusion-aware sampling) is already the
-        # longer of the two pipelined streams: keep the input aggregation in the compute phase
-        self.early_agg = False
+        # the input aggregation stays in the compute phase (GSB_LP_EARLY=1 moves it to the sample
+        # phase as for NC: the phases swap lengths but the overlapped step gets slower, 1.2753 ->
+        # 1.3053 ms on amazon_lp, gpurun_out/lp1: the two streams share the SMs either way)
+        self.early_agg = os.environ.get("GSB_LP_EARLY", "0") == "1"
         wb = C.c_size_t()
         call("gsb_lp_seeds_bytes", B, self.n_neg, C.byref(wb))
         self.seeds_ws = torch.empty(int(wb.value), dtype=torch.uint8, device=dev)
