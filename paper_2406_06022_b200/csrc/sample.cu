@@ -146,6 +146,12 @@ __global__ void __launch_bounds__(1024) seed_meta_kernel(GraphDev g, const int64
                                                          int* __restrict__ err) {
     GSB_PDL_ENTRY();
     __shared__ unsigned long long cnt[kMaxT];
+    // the error latch roll-over (err_roll_kernel) folded in: one block, done before any check
+    if (threadIdx.x == 0) {
+        err[1] |= err[0];
+        err[0] = 0;
+    }
+    __syncthreads();
     int64_t n = n_dev ? *n_dev : n_cap;
     if (n > n_cap) {
         if (threadIdx.x == 0) atomicExch(err, ERR_CAPACITY);
@@ -1229,11 +1235,11 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
 
     // err[0] = this sample's latch; err[1] = sticky OR of every earlier sample's latch since the
     // last poll, so an error in any step of a timed loop is still reported afterwards
-    GSB_LAUNCH("err_roll", err_roll_kernel, 1, 32, 0, s, err);
-    if (n_seeds <= 8192) {
+    if (n_seeds <= 8192) {      // seed_meta_kernel rolls the latch itself
         GSB_LAUNCH("seed_meta", seed_meta_kernel, 1, 1024, 0, s, g, seeds, n_seeds, a->n_seeds_dev,
                    at<int64_t>(arena, B->off_seed), at<HopMeta>(arena, B->off_meta[1]), err);
     } else {
+        GSB_LAUNCH("err_roll", err_roll_kernel, 1, 32, 0, s, err);
         HopMeta* m1 = at<HopMeta>(arena, B->off_meta[1]);
         GSB_CUDA(cudaMemsetAsync(m1, 0, sizeof(HopMeta), s));
         GSB_LAUNCH("seed_meta", seed_scan_kernel, grid_for(n_seeds, 256, kNumSMs * 8), 256, 0, s, g, seeds, n_seeds,
