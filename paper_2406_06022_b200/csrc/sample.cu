@@ -841,11 +841,11 @@ __device__ __forceinline__ int64_t bit_rank(const uint32_t* bitmap, const int32_
     return r;
 }
 
-__global__ void hop_meta_kernel(GraphDev g, HopMeta* __restrict__ m, HopMeta* __restrict__ next,
-                                const int64_t* __restrict__ seg_ptr, int64_t nseg_cap, const uint32_t* __restrict__ bitmap,
-                                const int32_t* __restrict__ wrank, int64_t cap_src, int* __restrict__ err) {
-    GSB_PDL_ENTRY();
-    __shared__ int64_t nn_s[kMaxT];
+// hop metadata from the finished word ranks, run by one warp (threads 0..31 of a block)
+__device__ __forceinline__ void hop_meta_body(const GraphDev& g, HopMeta* __restrict__ m, HopMeta* __restrict__ next,
+                                              const int64_t* __restrict__ seg_ptr, int64_t nseg_cap,
+                                              const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ wrank,
+                                              int64_t cap_src, int* __restrict__ err, int64_t* nn_s) {
     const int t = threadIdx.x;
     const bool bad = *(volatile int*)err != 0;
     if (!bad && t < kMaxT) {   // one thread per node type: new-source count via bitmap ranks
@@ -858,7 +858,7 @@ __global__ void hop_meta_kernel(GraphDev g, HopMeta* __restrict__ m, HopMeta* __
         }
         nn_s[t] = nn;
     }
-    __syncthreads();
+    __syncwarp();
     if (t != 0) return;
     if (bad) {   // latched: empty block and frontier (kernels downstream see 0 rows)
         m->n_edges = 0;
@@ -885,6 +885,103 @@ __global__ void hop_meta_kernel(GraphDev g, HopMeta* __restrict__ m, HopMeta* __
     if (next) {
         next->n_dst = m->n_src;
         for (int k = 0; k <= kMaxT; ++k) next->dst_off[k] = m->src_off[k];
+    }
+}
+
+__global__ void hop_meta_kernel(GraphDev g, HopMeta* __restrict__ m, HopMeta* __restrict__ next,
+                                const int64_t* __restrict__ seg_ptr, int64_t nseg_cap, const uint32_t* __restrict__ bitmap,
+                                const int32_t* __restrict__ wrank, int64_t cap_src, int* __restrict__ err) {
+    GSB_PDL_ENTRY();
+    __shared__ int64_t nn_s[kMaxT];
+    if (threadIdx.x < 32) hop_meta_body(g, m, next, seg_ptr, nseg_cap, bitmap, wrank, cap_src, err, nn_s);
+}
+
+// One launch for the word ranks and the hop metadata (rank_sum + rank_scan + hop_meta): every
+// block sums its chunk's bit counts, publishes the total in an epoch-tagged flag, adds the
+// totals of the blocks before it (decoupled look-back; blocks are scheduled in index order, so
+// a block only waits on blocks already resident or done), writes its words' exclusive ranks, and
+// the last block to finish (ticket) builds the hop metadata and advances the epoch.
+__global__ void __launch_bounds__(kRankThreads) rank_fused_kernel(
+    GraphDev g, const uint32_t* __restrict__ bitmap, int64_t n_words, int64_t chunk, int32_t* __restrict__ wrank,
+    unsigned long long* __restrict__ flags, HopMeta* __restrict__ m, HopMeta* __restrict__ next,
+    const int64_t* __restrict__ seg_ptr, int64_t nseg_cap, int64_t cap_src, int* __restrict__ err) {
+    GSB_PDL_ENTRY();
+    __shared__ int red[kRankThreads / 32];
+    __shared__ int wsum[kRankThreads / 32];
+    __shared__ int64_t nn_s[kMaxT];
+    __shared__ unsigned last;
+    unsigned* epoch_p = reinterpret_cast<unsigned*>(flags + kRankMaxBlocks);
+    unsigned* ticket_p = epoch_p + 1;
+    const unsigned long long tag = (unsigned long long)(*(volatile unsigned*)epoch_p + 1u) << 32;
+    const int64_t w0 = blockIdx.x * chunk, w1 = min(w0 + chunk, n_words + 1);
+    // (1) this block's total, published
+    int v = 0;
+    for (int64_t base = w0 + (int64_t)threadIdx.x * kRankPerThread; base < w1; base += kRankTile) {
+        uint32_t c[kRankPerThread];
+        rank_load(bitmap, n_words, base, c);
+#pragma unroll
+        for (int i = 0; i < kRankPerThread; ++i) v += (int)c[i];
+    }
+    v = rank_block_sum(v, red);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(flags + blockIdx.x, tag | (unsigned)v);
+    }
+    // (2) totals of the earlier blocks
+    int off = 0;
+    for (int b = threadIdx.x; b < (int)blockIdx.x; b += kRankThreads) {
+        unsigned long long f;
+        do {
+            f = *(volatile unsigned long long*)(flags + b);
+        } while ((f & 0xFFFFFFFF00000000ull) != tag);
+        off += (int)(unsigned)f;
+    }
+    off = rank_block_sum(off, red);
+    // (3) exclusive word ranks of the chunk
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t t0 = w0; t0 < w1; t0 += kRankTile) {
+        const int64_t base = t0 + (int64_t)threadIdx.x * kRankPerThread;
+        uint32_t c[kRankPerThread];
+        rank_load(bitmap, n_words, base, c);
+        const int vv = (int)(c[0] + c[1] + c[2] + c[3]);
+        int inc = vv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[wid] = inc;
+        __syncthreads();
+        int before = 0, tile = 0;
+#pragma unroll
+        for (int w = 0; w < kRankThreads / 32; ++w) {
+            before += (w < wid) ? wsum[w] : 0;
+            tile += wsum[w];
+        }
+        __syncthreads();
+        const int r0 = off + before + inc - vv;
+        const int r1 = r0 + (int)c[0], r2 = r1 + (int)c[1], r3 = r2 + (int)c[2];
+        if (base + kRankPerThread <= w1) {
+            *reinterpret_cast<int4*>(wrank + base) = make_int4(r0, r1, r2, r3);
+        } else {
+            const int r[4] = {r0, r1, r2, r3};
+#pragma unroll
+            for (int i = 0; i < kRankPerThread; ++i)
+                if (base + i < w1) wrank[base + i] = r[i];
+        }
+        off += tile;
+    }
+    // (4) the last block: hop metadata, next epoch
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(ticket_p, 1u) == gridDim.x - 1) ? 1u : 0u;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x < 32) hop_meta_body(g, m, next, seg_ptr, nseg_cap, bitmap, wrank, cap_src, err, nn_s);
+    if (threadIdx.x == 0) {
+        *ticket_p = 0;
+        *epoch_p = *epoch_p + 1u;
     }
 }
 
@@ -952,6 +1049,12 @@ __global__ void init_arena_kernel(int32_t* __restrict__ map, int64_t n, uint32_t
         if (i < n_words) bitmap[i] = 0;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) err[0] = err[1] = 0;
+}
+
+// the fused rank kernel's int64 block flags (+ epoch, ticket), 8-B aligned after the ranks
+static int64_t* rank_flags(const Blocks* B, void* arena) {
+    const uintptr_t p = reinterpret_cast<uintptr_t>(at<int32_t>(arena, B->off_wrank) + B->n_words + 1 + kRankMaxBlocks);
+    return reinterpret_cast<int64_t*>((p + 7) & ~uintptr_t(7));
 }
 
 HopBufs Blocks::hop(int h, void* arena) const {
@@ -1146,7 +1249,8 @@ gsb_status gsb_blocks_create(gsb_graph_t gh, int32_t L, const int32_t* fanouts, 
     B->off_map = take(sizeof(int32_t) * G->total_nodes);
     B->off_bitmap = take(sizeof(uint32_t) * B->n_words);
     // word ranks [n_words + 1], then the per-block totals of the rank kernels
-    B->off_wrank = take(sizeof(int32_t) * (B->n_words + 1 + kRankMaxBlocks));
+    // word ranks, per-block totals, then the fused rank kernel's int64 block flags + epoch + ticket
+    B->off_wrank = take(sizeof(int32_t) * (B->n_words + 1 + kRankMaxBlocks) + 8 + sizeof(int64_t) * kRankMaxBlocks + 16);
     B->off_excl = take(sizeof(uint64_t) * (8 * (max_excl > 0 ? max_excl : 1) + 2));
     B->off_cub = take(cb);
     B->total_bytes = off;
@@ -1178,6 +1282,7 @@ gsb_status gsb_blocks_init_arena(gsb_blocks_t b, void* arena, size_t arena_bytes
     GSB_LAUNCH("init_arena", init_arena_kernel, grid_for(std::max(N, B->n_words), 256, kNumSMs * 8), 256, 0, s,
                at<int32_t>(arena, B->off_map), N, at<uint32_t>(arena, B->off_bitmap), B->n_words,
                at<int>(arena, B->off_err));
+    GSB_CUDA(cudaMemsetAsync(rank_flags(B, arena), 0, sizeof(int64_t) * kRankMaxBlocks + 16, s));
     return GSB_OK;
 }
 
@@ -1289,17 +1394,25 @@ gsb_status gsb_sample(gsb_blocks_t b, const gsb_sample_args* a, void* arena, siz
                            hb.seg_ptr, ex, map, bitmap, hb.e_src_gid, hb.e_eid, err);
         }
         }
+        HopMeta* next = (h < B->L) ? at<HopMeta>(arena, B->off_meta[h + 1]) : nullptr;
         {
             const int64_t chunk = ceil_div(ceil_div(B->n_words + 1, kRankTile), kRankMaxBlocks) * kRankTile;
             const int nb = (int)ceil_div(B->n_words + 1, chunk);
-            int32_t* btot = wrank + B->n_words + 1;
-            GSB_LAUNCH("bitmap_rank_sum", rank_sum_kernel, nb, kRankThreads, 0, s, bitmap, B->n_words, chunk, btot);
-            GSB_LAUNCH("bitmap_rank_scan", rank_scan_kernel, nb, kRankThreads, 0, s, bitmap, B->n_words, chunk, btot,
-                       wrank);
+            // one launch (rank_fused_kernel) unless GSB_RANK_FUSED=0 (the three-kernel A/B path)
+            static const bool fused = !(getenv("GSB_RANK_FUSED") && strcmp(getenv("GSB_RANK_FUSED"), "0") == 0);
+            if (fused) {
+                GSB_LAUNCH("bitmap_rank", rank_fused_kernel, nb, kRankThreads, 0, s, g, bitmap, B->n_words, chunk, wrank,
+                           reinterpret_cast<unsigned long long*>(rank_flags(B, arena)), hb.meta, next, hb.seg_ptr, nseg,
+                           hb.cap_src, err);
+            } else {
+                int32_t* btot = wrank + B->n_words + 1;
+                GSB_LAUNCH("bitmap_rank_sum", rank_sum_kernel, nb, kRankThreads, 0, s, bitmap, B->n_words, chunk, btot);
+                GSB_LAUNCH("bitmap_rank_scan", rank_scan_kernel, nb, kRankThreads, 0, s, bitmap, B->n_words, chunk,
+                           btot, wrank);
+                GSB_LAUNCH("hop_meta", hop_meta_kernel, 1, 32, 0, s, g, hb.meta, next, hb.seg_ptr, nseg, bitmap, wrank,
+                           hb.cap_src, err);
+            }
         }
-        HopMeta* next = (h < B->L) ? at<HopMeta>(arena, B->off_meta[h + 1]) : nullptr;
-        GSB_LAUNCH("hop_meta", hop_meta_kernel, 1, 32, 0, s, g, hb.meta, next, hb.seg_ptr, nseg, bitmap, wrank,
-                   hb.cap_src, err);
         GSB_LAUNCH("relabel", relabel_kernel, grid_for(hb.cap_edges, 256, kNumSMs * 8), 256, 0, s, g, hb.meta,
                    hb.e_src_gid, map, bitmap, wrank, hb.e_src);
         if (hb.t_ptr) {
