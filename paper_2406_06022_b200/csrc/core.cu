@@ -230,7 +230,8 @@ gsb_status launch_gather(const Graph* G, const int64_t* gid, const int64_t* n_de
         // bounded grid: the unique-row fetch is latency / NVLink bound and runs beside the compute
         // phase's GEMMs (one CTA per SM); 2 blocks per SM keep ~4 MB in flight
         const int64_t work = n_max * (G->dev.feat_row_bytes / 32);
-        const int grid = grid_for(ceil_div(work, 8), 256, kNumSMs * 2);
+        static const int bps = getenv("GSB_GATHER_BPS") ? atoi(getenv("GSB_GATHER_BPS")) : 2;   // A/B knob
+        const int grid = grid_for(ceil_div(work, 8), 256, kNumSMs * bps);
         GSB_LAUNCH("gather", gather32_kernel, grid, 256, 0, s, G->dev, gid, n_dev, n_host, static_cast<uint4*>(out));
         return GSB_OK;
     }

@@ -341,7 +341,7 @@ class _TrainerBase:
         self.acat = [torch.empty(self.sampler.acat_floats(l, self.d_in[l]), dtype=torch.float32, device=dev)
                      for l in range(self.L)]
         self.acat0 = self.acat[0]      # per-batch (double-buffered with the pipeline)
-        self.early_agg = True
+        self.early_agg = os.environ.get("GSB_EARLY_AGG", "1") != "0"   # A/B knob (NC)
         self.dacat = torch.empty(max(self.sampler.acat_floats(l, self.d_in[l]) for l in range(self.L)),
                                  dtype=torch.float32, device=dev)
         self.dh = [torch.empty((self.sampler.dst_rows(l), hidden), dtype=torch.float32, device=dev)
