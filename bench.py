@@ -491,7 +491,9 @@ def run_gsb(args, cfg):
     # stream, batch i+1) and of the compute phase (+ Adam) of batch i; otherwise ONE graph of
     # the whole step.  Replays advance the RNG step word and Adam's t on the device; inputs
     # are copied into the graphs' fixed buffers.
-    use_graph = not args.no_graph and tr.exchange is None   # all-to-all sizes are host-synced
+    # all-to-all exchange modes (host-synced sizes): only the pipelined path, whose sample phase
+    # then runs eagerly beside the captured compute graph
+    use_graph = not args.no_graph and (tr.exchange is None or args.pipeline == "on")
     pipelined = use_graph and args.pipeline == "on"
 
     def inputs(i):
@@ -522,8 +524,12 @@ def run_gsb(args, cfg):
     launches0 = _lib.lib().gsb_launch_count()
     if tr.exchange is not None:
         tr.exchange.bytes_sent = 0
-    if getattr(tr, "_sx", None) is not None:
-        tr._sx.bytes_sent = 0
+    # frontier exchanges: one per pipeline buffer's sampler (MiniBatchSampler.twin attaches its own)
+    sxs = [b["sampler"]._sx for b in (tr._bufs or []) if getattr(b["sampler"], "_sx", None) is not None] \
+        or ([tr._sx] if getattr(tr, "_sx", None) is not None else [])
+    for sx in sxs:
+        sx.bytes_sent = 0
+        sx.host_s = {}
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -542,10 +548,18 @@ def run_gsb(args, cfg):
         dist.barrier()
     launches = _lib.lib().gsb_launch_count() - launches0
     nv_bytes = tr.exchange.bytes_sent / args.steps if tr.exchange is not None else 0
-    if getattr(tr, "_sx", None) is not None:
-        nv_bytes += tr._sx.bytes_sent / args.steps      # C2/C3 frontier exchange
+    nv_bytes += sum(sx.bytes_sent for sx in sxs) / args.steps      # C2/C3 frontier exchange
+    if sxs and os.environ.get("GSB_XPROF") and rank == 0:
+        tot = {}
+        for sx in sxs:
+            for k, v in sx.host_s.items():
+                tot[k] = tot.get(k, 0.0) + v
+        print("[xprof] host ms per step in the exchange callbacks (timed region):",
+              {k: round(v * 1e3 / max(args.steps, 1), 3) for k, v in tot.items()}, "host enqueue ms/step",
+              round(host_enqueue_ms / args.steps, 3), file=sys.stderr)
     if use_graph:   # kernels inside a replayed graph are not re-counted by the library
-        launches = launches_per_step_graph(tr, cfg) * args.steps
+        eager = launches if (pipelined and tr.pipe_graphs and tr.pipe_graphs.get("sample") is None) else 0
+        launches = launches_per_step_graph(tr, cfg) * args.steps + eager   # + eager sample-phase kernels
     ms = e0.elapsed_time(e1)
     if dist is not None:
         t = torch.tensor([ms], device=device)
@@ -561,6 +575,8 @@ def run_gsb(args, cfg):
         torch.cuda.synchronize()
         phase_ms = {}
         for kind in ("sample", "compute"):
+            if tr.pipe_graphs.get(kind) is None:   # eager sample phase (host-synced exchanges)
+                continue
             g = tr.pipe_graphs[kind][0]
             tr._use(0)
             g.replay()

@@ -74,10 +74,12 @@ class FeatureExchange:
         except Exception:
             pass
 
-    def gather(self, gids: torch.Tensor, n: int, out: Optional[torch.Tensor] = None):
+    def gather(self, gids: torch.Tensor, n: int, out: Optional[torch.Tensor] = None,
+               rows_out: Optional[torch.Tensor] = None, perm_out: Optional[torch.Tensor] = None):
         """Rows of gids[:n].  With `out`, unpacks into out (gid order) and returns it; without,
         returns (rows in exchange order, perm) so that row i of the request is rows[perm[i]]
-        (the consumer reads through perm -- no unpack pass)."""
+        (the consumer reads through perm -- no unpack pass).  rows_out / perm_out: fixed
+        buffers (>= n rows) to receive them, so a captured compute graph can read them."""
         import ctypes as C
         import torch.distributed as dist
         from ._lib import call
@@ -85,7 +87,7 @@ class FeatureExchange:
         s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         dev = gids.device
         send_gid = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
-        perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        perm = perm_out if perm_out is not None else torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         call("gsb_bucket_by_owner", self.h, P(gids), None, n, P(send_gid), P(perm), P(self.counts_dev), P(self.ws), s)
         recv_counts = torch.empty_like(self.counts_dev)
         dist.all_to_all_single(recv_counts, self.counts_dev, group=self.group)          # C1
@@ -95,7 +97,7 @@ class FeatureExchange:
         dist.all_to_all_single(recv_gid, send_gid[:n], recv_splits, send_splits, group=self.group)   # C4
         rows = torch.empty((max(sum(recv_splits), 1), self.dim), dtype=self.dtype, device=dev)
         call("gsb_shard_gather", self.h, P(recv_gid), recv_gid.numel(), P(rows), s)
-        back = torch.empty((max(n, 1), self.dim), dtype=self.dtype, device=dev)
+        back = rows_out if rows_out is not None else torch.empty((max(n, 1), self.dim), dtype=self.dtype, device=dev)
         dist.all_to_all_single(back[:n], rows[:sum(recv_splits)], send_splits, recv_splits, group=self.group)  # C5
         self.bytes_sent += (n - send_splits[self.rank]) * 8 + (sum(recv_splits) - recv_splits[self.rank]) * self.dim * self.esize
         if out is None:
@@ -267,12 +269,23 @@ class SampleExchange:
         self.bytes_sent = 0
         call("gsb_blocks_set_exchange", sampler.h, world, rank, first_hop, C.byref(b), self._fn, None)
         self.sampler = sampler
+        self.first_hop = first_hop
+        self.host_s = {}                # host seconds spent in the callback, per phase (tools)
+        sampler._sx = self              # kept alive with the sampler; twin() attaches its own
 
     def _a2a(self, out, inp, out_splits, in_splits):
         import torch.distributed as dist
         dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
 
     def _callback(self, user, phase, hop, stream, counts):
+        import time
+        t0 = time.perf_counter()
+        try:
+            return self._callback_body(phase, stream, counts)
+        finally:
+            self.host_s[phase] = self.host_s.get(phase, 0.0) + time.perf_counter() - t0
+
+    def _callback_body(self, phase, stream, counts):
         try:
             st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
             with torch.cuda.stream(st):

@@ -197,8 +197,15 @@ class MiniBatchSampler:
         self.fanouts = list(fanouts)
 
     def twin(self) -> "MiniBatchSampler":
-        """A second sampler of the same shape (own handle + arena), for double buffering."""
-        return MiniBatchSampler(self.store, self.fanouts, self.max_seeds, self.max_excl)
+        """A second sampler of the same shape (own handle + arena), for double buffering; a
+        frontier exchange attached to this sampler (dist.SampleExchange) is attached to the twin
+        too, with its own buffers."""
+        tw = MiniBatchSampler(self.store, self.fanouts, self.max_seeds, self.max_excl)
+        sx = getattr(self, "_sx", None)
+        if sx is not None:
+            from .dist import SampleExchange
+            SampleExchange(tw, sx.world, sx.rank, first_hop=sx.first_hop, group=sx.group)
+        return tw
 
     def __del__(self):
         try:
@@ -326,6 +333,7 @@ class _TrainerBase:
         self.emb: Dict[int, tuple] = {}
         nin = self.sampler.input_rows()
         self.x0 = torch.empty((0 if self.enc_types else nin, d0), dtype=store.feat_dtype, device=dev)
+        self.xperm = torch.empty(max(nin, 1), dtype=torch.int32, device=dev)   # C4/C5 bucketing permutation
         if self.enc_types:
             self.H0 = torch.empty((nin, d0), dtype=torch.float32, device=dev)
             self.dH0 = torch.empty((nin, d0), dtype=torch.float32, device=dev)
@@ -470,6 +478,12 @@ class _TrainerBase:
         if not self.fuse_gather and self.exchange is None and not self.enc_types:
             sm = self.sampler
             call("gsb_gather_block_inputs", sm.h, _ptr(sm.arena), _ptr(self.x0), s)
+        if self.exchange is not None and not self.enc_types:
+            # partitioned features, NCCL all-to-all fetch (C4/C5) into this buffer's x0 / xperm:
+            # host-synced sizes, so part of the (eager) sample phase; the compute phase reads
+            # the rows through the bucketing permutation
+            gids, n = self.sampler.input_gids()
+            self.exchange.gather(gids, n, rows_out=self.x0, perm_out=self.xperm)
         if self._early():
             sm = self.sampler
             h = None if self.fuse_gather else self.x0
@@ -494,10 +508,8 @@ class _TrainerBase:
                 else:
                     call("gsb_sparse_emb_fwd", sm.h, _ptr(sm.arena), t, _ptr(E), self.d_in[0], _ptr(self.H0), s)
             h = self.H0
-        elif self.exchange is not None:   # partitioned features: NCCL all-to-all fetch (C4/C5)
-            gids, n = sm.input_gids()
-            h, rowmap = self.exchange.gather(gids, n)   # layer 0 reads rows through perm
-            self._keep = (h, rowmap)
+        elif self.exchange is not None:   # partitioned features fetched in the sample phase (C4/C5)
+            h, rowmap = self.x0, self.xperm    # layer 0 reads rows through the bucketing permutation
         elif self.fuse_gather:
             h = None
         else:
@@ -623,7 +635,7 @@ class _TrainerBase:
         self.t += 1
 
     # double-buffered pipeline: sample batch i+1 while batch i computes ---------------------
-    _BUFFERED = ("sampler", "x0", "acat0")     # per-batch state; subclasses add their input buffers
+    _BUFFERED = ("sampler", "x0", "acat0", "xperm")   # per-batch state; subclasses add their input buffers
 
     def enable_prefetch(self):
         """Allocate a second copy of every per-batch buffer (sampler handle + arena, input
@@ -667,8 +679,8 @@ class _TrainerBase:
         each compute graph, NCCL being kept out of capture), then load `inputs` (the first
         batch) into buffer 0 and sample it with RNG step word `step`.  Each pipeline_step()
         computes the pending batch and samples the next one (step word + ws)."""
-        if self.exchange is not None:
-            raise GsbError("pipeline needs device-resident sizes (no all-to-all exchange mode)")
+        if self.exchange is not None:   # host-synced all-to-all sizes: eager sample phase
+            self.sample_graph = False
         self.enable_prefetch()
         self.pipe_ws, self.pipe_allreduce = ws, allreduce
         self._sync_images(_stream())   # images current before capture (none captured)
@@ -789,7 +801,7 @@ class RGCNTrainer(_TrainerBase):
         self.row_loss = torch.zeros(batch + 640, dtype=torch.float32, device=dev)   # + fused-mean scratch
         self.seeds_dev = torch.empty(batch, dtype=torch.int64, device=dev)
 
-    _BUFFERED = ("sampler", "x0", "acat0", "seeds_dev")
+    _BUFFERED = ("sampler", "x0", "acat0", "xperm", "seeds_dev")
 
     def _load_inputs(self, d, seeds: torch.Tensor):
         d["seeds_dev"][:seeds.numel()].copy_(seeds, non_blocking=True)
@@ -904,7 +916,7 @@ class LPTrainer(_TrainerBase):
         self.group_base = 0
         self.pos_base = 0
 
-    _BUFFERED = ("sampler", "x0", "acat0", "pos_u", "pos_v", "neg", "seeds", "n_seeds", "iu", "iv", "ineg",
+    _BUFFERED = ("sampler", "x0", "acat0", "xperm", "pos_u", "pos_v", "neg", "seeds", "n_seeds", "iu", "iv", "ineg",
                  "seeds_ws")
 
     def _load_inputs(self, d, u: torch.Tensor, v: torch.Tensor):
