@@ -26,9 +26,21 @@ using umma::cp_commit;
 using umma::cp_wait;
 
 constexpr int EN_PANEL = 16384;            // 128 x 64 bf16 (fwd) / 128 MN x 64 K bf16 (dW)
-constexpr int EN_STAGE = 3 * EN_PANEL;     // A, B_hi, B_lo
-constexpr int EN_STAGES = 4;
-constexpr int EN_SMEM = EN_STAGES * EN_STAGE + 1024;
+// decoupled rings: the gathered A panels (HBM-latency bound, deep ring) and the dense B panels
+// (W^T / dH0 hi + lo by TMA, mostly L2 hits, shallow ring)
+#ifndef GSB_ENC_AF
+#define GSB_ENC_AF 8      // forward: A stages (B = W^T panels, 2 stages: L2 hits)
+#endif
+#ifndef GSB_ENC_AB
+#define GSB_ENC_AB 4      // weight gradient: A stages (B = dH0 panels, 4 stages)
+#endif
+template <bool BWD>
+struct EnRing {
+    static constexpr int A = BWD ? GSB_ENC_AB : GSB_ENC_AF;
+    static constexpr int B = (192 - 16 * A) / 32;
+};
+constexpr int EN_B_STAGE = 2 * EN_PANEL;   // B_hi, B_lo
+constexpr int EN_SMEM = 192 * 1024 + 1024;
 
 struct EncDev {
     int T, d_out;
@@ -129,13 +141,14 @@ __device__ __forceinline__ void dw_decode(const EncDev& e, const HopMeta* m, int
 }
 
 // ---- the warp-specialized pipelined kernel (BWD = false: forward, true: weight gradient) --
-// warps 0-3: producers (cp.async gathers of operand panels into a ring of EN_STAGES stages;
-//            completion is signalled per stage with cp.async.mbarrier.arrive.noinc)
+// warps 0-3: A producers (cp.async gathers of the feature panels into a ring of EN_A_STAGES
+//            stages; completion is signalled per stage with cp.async.mbarrier.arrive.noinc)
 // warps 4-7: epilogue (TMEM -> registers -> H0 rows / red.add into dW), warp w drains TMEM
 //            lanes 32*(w%4)..; two TMEM accumulators so a tile's epilogue overlaps the next
 //            tile's MMAs
-// warp 8:    one thread issues the tcgen05 MMAs and commits stage / accumulator barriers
-constexpr int EN_WS_THREADS = 288;
+// warp 8:    lane 0 issues the tcgen05 MMAs and commits stage / accumulator barriers
+// warp 9:    lane 0 is the B producer (TMA boxes of W^T / dH0 hi + lo into a ring of EN_B_STAGES)
+constexpr int EN_WS_THREADS = 320;
 
 __device__ __forceinline__ void cp_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(umma::smem_u32(bar)) : "memory");
@@ -153,14 +166,23 @@ __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, 
     GSB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t full[EN_STAGES], empty[EN_STAGES], tfull[2], tempty[2];
+    constexpr int EN_A_STAGES = EnRing<BWD>::A, EN_B_STAGES = EnRing<BWD>::B;
+    static_assert(EN_A_STAGES * EN_PANEL + EN_B_STAGES * EN_B_STAGE <= 192 * 1024, "encoder rings exceed 192 KB");
+    __shared__ __align__(8) uint64_t fullA[EN_A_STAGES], emptyA[EN_A_STAGES], fullB[EN_B_STAGES], emptyB[EN_B_STAGES];
+    __shared__ __align__(8) uint64_t tfull[2], tempty[2];
     __shared__ uint32_t tmem_sh;
+    uint8_t* ringA = smem;
+    uint8_t* ringB = smem + EN_A_STAGES * EN_PANEL;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (warp == 0) umma::tmem_alloc<256>(&tmem_sh);
     if (tid == 0) {
-        for (int s = 0; s < EN_STAGES; ++s) {
-            umma::mbar_init(&full[s], 128 + (maps.use ? 1 : 0));
-            umma::mbar_init(&empty[s], 1);
+        for (int s = 0; s < EN_A_STAGES; ++s) {
+            umma::mbar_init(&fullA[s], 128);
+            umma::mbar_init(&emptyA[s], 1);
+        }
+        for (int s = 0; s < EN_B_STAGES; ++s) {
+            umma::mbar_init(&fullB[s], 1);
+            umma::mbar_init(&emptyB[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             umma::mbar_init(&tfull[a], 1);
@@ -197,31 +219,18 @@ __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, 
                     const int64_t row = c.row0 + rg + 16 * i;
                     arow[i] = row < c.rlim ? reinterpret_cast<const char*>(feat_row(g, __ldg(src_gid + row))) : nullptr;
                 }
-                const __nv_bfloat16* whi = e.wt_hi[c.t];
-                const __nv_bfloat16* wlo = e.wt_lo[c.t];
-                const int dim = e.dim[c.t];
+                const char* zsrc = reinterpret_cast<const char*>(e.wt_hi[c.t]);   // any valid address (0-byte copies)
                 for (int pn = 0; pn < c.KP; ++pn, ++it) {
-                    const int st = (int)(it % EN_STAGES);
-                    if (it >= EN_STAGES) umma::mbar_wait(&empty[st], (uint32_t)((it / EN_STAGES) - 1) & 1u);
-                    const uint32_t sA = umma::smem_u32(smem + st * EN_STAGE), sBh = sA + EN_PANEL, sBl = sA + 2 * EN_PANEL;
-                    if (maps.use && p == 0) {      // W_t^T hi / lo panels: two TMA boxes
-                        tma::mbar_expect_tx(&full[st], 2 * EN_PANEL);
-                        tma::load_2d(sBh, &maps.hi[c.t], pn * 64, c.n0, &full[st]);
-                        tma::load_2d(sBl, &maps.lo[c.t], pn * 64, c.n0, &full[st]);
-                    }
+                    const int st = (int)(it % EN_A_STAGES);
+                    if (it >= EN_A_STAGES) umma::mbar_wait(&emptyA[st], (uint32_t)((it / EN_A_STAGES) - 1) & 1u);
+                    const uint32_t sA = umma::smem_u32(ringA + st * EN_PANEL);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int r = rg + 16 * i;
                         const uint32_t o = umma::kmaj16_chunk(r, ch);
-                        cp16(sA + o, arow[i] ? arow[i] + pn * 128 + ch * 16 : reinterpret_cast<const char*>(whi),
-                             arow[i] ? 16 : 0);
-                        if (!maps.use) {
-                            const size_t off = (size_t)(c.n0 + r) * dim + pn * 64 + ch * 8;
-                            cp16(sBh + o, whi + off, 16);
-                            cp16(sBl + o, wlo + off, 16);
-                        }
+                        cp16(sA + o, arow[i] ? arow[i] + pn * 128 + ch * 16 : zsrc, arow[i] ? 16 : 0);
                     }
-                    cp_arrive_noinc(&full[st]);
+                    cp_arrive_noinc(&fullA[st]);
                 }
             } else {
                 // K rows kr = (p >> 4) + 8 i (i < 8) of the 64-row panel, 16-B chunk c of the 128-wide slice
@@ -240,39 +249,51 @@ __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, 
 #pragma unroll
                     for (int i = 0; i < 8; ++i) gid[i] = gid_next[i];
                     if (pn + 1 < c.KP) load_gids(pn + 1);       // prefetch the next panel's ids
-                    const int st = (int)(it % EN_STAGES);
-                    if (it >= EN_STAGES) umma::mbar_wait(&empty[st], (uint32_t)((it / EN_STAGES) - 1) & 1u);
-                    const uint32_t sA = umma::smem_u32(smem + st * EN_STAGE), sBh = sA + EN_PANEL, sBl = sA + 2 * EN_PANEL;
-                    if (maps.use && p == 0) {      // dH0 hi / lo rows of this panel: 2 x 2 TMA boxes
-                        const int32_t r0 = (int32_t)(c.row0 + (int64_t)pn * 64);
-                        tma::mbar_expect_tx(&full[st], 2 * EN_PANEL);
-                        tma::load_2d(sBh, &maps.hi[0], c.n0, r0, &full[st]);
-                        tma::load_2d(sBh + 8192, &maps.hi[0], c.n0 + 64, r0, &full[st]);
-                        tma::load_2d(sBl, &maps.lo[0], c.n0, r0, &full[st]);
-                        tma::load_2d(sBl + 8192, &maps.lo[0], c.n0 + 64, r0, &full[st]);
-                    }
+                    const int st = (int)(it % EN_A_STAGES);
+                    if (it >= EN_A_STAGES) umma::mbar_wait(&emptyA[st], (uint32_t)((it / EN_A_STAGES) - 1) & 1u);
+                    const uint32_t sA = umma::smem_u32(ringA + st * EN_PANEL);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int kr = kb + 8 * i;
-                        const int64_t row = c.row0 + (int64_t)pn * 64 + kr;
                         const bool ok = gid[i] >= 0;
                         const uint32_t o = umma::mnmaj16_chunk(cc * 8, kr);
                         const char* src = ok ? reinterpret_cast<const char*>(feat_row(g, gid[i])) + (size_t)(c.m0 + cc * 8) * 2
                                              : reinterpret_cast<const char*>(e.d_hi);
                         cp16(sA + o, src, ok ? 16 : 0);
-                        if (!maps.use) {
-                            const size_t off = (size_t)(ok ? row : 0) * e.d_out + c.n0 + cc * 8;
-                            cp16(sBh + o, e.d_hi + off, ok ? 16 : 0);
-                            cp16(sBl + o, e.d_lo + off, ok ? 16 : 0);
-                        }
                     }
-                    cp_arrive_noinc(&full[st]);
+                    cp_arrive_noinc(&fullA[st]);
+                }
+            }
+        }
+    } else if (warp == 9) {
+        if (lane == 0) {
+            // -------------------------------------------------------------- B producer (TMA)
+            int64_t it = 0;
+            for (int64_t tile = blockIdx.x; tile < total; tile += grid) {
+                EnCursor c;
+                c.tile = tile;
+                decode(c);
+                for (int pn = 0; pn < c.KP; ++pn, ++it) {
+                    const int sb = (int)(it % EN_B_STAGES);
+                    if (it >= EN_B_STAGES) umma::mbar_wait(&emptyB[sb], (uint32_t)((it / EN_B_STAGES) - 1) & 1u);
+                    const uint32_t bh = umma::smem_u32(ringB + sb * EN_B_STAGE), bl = bh + EN_PANEL;
+                    tma::mbar_expect_tx(&fullB[sb], 2 * EN_PANEL);
+                    if (!BWD) {            // W_t^T hi / lo panels: two TMA boxes {64, 128}
+                        tma::load_2d(bh, &maps.hi[c.t], pn * 64, c.n0, &fullB[sb]);
+                        tma::load_2d(bl, &maps.lo[c.t], pn * 64, c.n0, &fullB[sb]);
+                    } else {               // dH0 hi / lo rows of this panel: 2 x 2 boxes {64, 64}
+                        const int32_t r0 = (int32_t)(c.row0 + (int64_t)pn * 64);
+                        tma::load_2d(bh, &maps.hi[0], c.n0, r0, &fullB[sb]);
+                        tma::load_2d(bh + 8192, &maps.hi[0], c.n0 + 64, r0, &fullB[sb]);
+                        tma::load_2d(bl, &maps.lo[0], c.n0, r0, &fullB[sb]);
+                        tma::load_2d(bl + 8192, &maps.lo[0], c.n0 + 64, r0, &fullB[sb]);
+                    }
                 }
             }
         }
     } else if (warp == 8) {
-        // ------------------------------------------------------------------ MMA issuer
         if (lane == 0) {
+            // -------------------------------------------------------------- MMA issuer
             constexpr uint32_t IDESC = umma::idesc_bf16(128, BWD, BWD);
             int64_t it = 0, j = 0;
             for (int64_t tile = blockIdx.x; tile < total; tile += grid, ++j) {
@@ -284,32 +305,32 @@ __global__ void __launch_bounds__(EN_WS_THREADS, 1) enc_umma_kernel(GraphDev g, 
                 umma::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * 128);
                 for (int pn = 0; pn < c.KP; ++pn, ++it) {
-                    const int st = (int)(it % EN_STAGES);
-                    umma::mbar_wait(&full[st], (uint32_t)(it / EN_STAGES) & 1u);
+                    const int st = (int)(it % EN_A_STAGES), sb = (int)(it % EN_B_STAGES);
+                    umma::mbar_wait(&fullA[st], (uint32_t)(it / EN_A_STAGES) & 1u);
+                    umma::mbar_wait(&fullB[sb], (uint32_t)(it / EN_B_STAGES) & 1u);
                     umma::fence_proxy_async_smem();
                     umma::tc_fence_after();
-                    const uint32_t a = umma::smem_u32(smem + st * EN_STAGE), bh = a + EN_PANEL, bl = a + 2 * EN_PANEL;
+                    const uint32_t a = umma::smem_u32(ringA + st * EN_PANEL);
+                    const uint32_t bh = umma::smem_u32(ringB + sb * EN_B_STAGE), bl = bh + EN_PANEL;
 #pragma unroll
                     for (int ks = 0; ks < 4; ++ks) {
                         const uint32_t o = BWD ? ks * 4096u : ks * 32u;
                         const uint64_t da = BWD ? umma::desc_mnmajor16(a + o) : umma::desc_kmajor(a + o);
                         // backward B from TMA boxes: MN atoms 8192 B apart, 8-row K groups 1024 B, k-step 2048 B
-                        const uint64_t dbh = !BWD ? umma::desc_kmajor(bh + o)
-                                             : maps.use ? umma::desc_encode(bh + ks * 2048u, 8192, 1024, 2)
-                                                        : umma::desc_mnmajor16(bh + o);
-                        const uint64_t dbl = !BWD ? umma::desc_kmajor(bl + o)
-                                             : maps.use ? umma::desc_encode(bl + ks * 2048u, 8192, 1024, 2)
-                                                        : umma::desc_mnmajor16(bl + o);
+                        const uint64_t dbh = !BWD ? umma::desc_kmajor(bh + o) : umma::desc_encode(bh + ks * 2048u, 8192, 1024, 2);
+                        const uint64_t dbl = !BWD ? umma::desc_kmajor(bl + o) : umma::desc_encode(bl + ks * 2048u, 8192, 1024, 2);
                         umma::mma_f16(d, da, dbh, IDESC, (pn > 0 || ks > 0) ? 1u : 0u);
                         umma::mma_f16(d, da, dbl, IDESC, 1u);
                     }
-                    umma::mma_commit(&empty[st]);
+                    umma::mma_commit(&emptyA[st]);
+                    umma::mma_commit(&emptyB[sb]);
                 }
                 umma::mma_commit(&tfull[acc]);
             }
         }
     } else {
         // ------------------------------------------------------------------ epilogue (warps 4-7)
+        static_assert(EN_WS_THREADS == 320, "warp roles: 0-3 A producers, 4-7 epilogue, 8 MMA, 9 B producer");
         const int q = warp & 3;
         const int r = q * 32 + lane;
         int64_t j = 0;
@@ -467,8 +488,7 @@ static gsb_status enc_check(const Blocks* B, const float* const* W, int d_out) {
     return GSB_OK;
 }
 
-// B operand by TMA unless GSB_ENC_TMA=0 or a map cannot be encoded (then every producer thread
-// copies its B chunks with cp.async as well)
+// B operand by TMA (the kernel has no other B path: a map that cannot be encoded is an error)
 template <bool BWD>
 static gsb_status launch_enc(const char* name, const GraphDev& g, const EncDev& e, const HopMeta* m,
                              const int64_t* src_gid, float* H0, const EncOut& out, int64_t cap_rows, cudaStream_t s) {
@@ -477,10 +497,9 @@ static gsb_status launch_enc(const char* name, const GraphDev& g, const EncDev& 
         GSB_CUDA(cudaFuncSetAttribute(enc_umma_kernel<BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, EN_SMEM));
         attr = true;
     }
-    static const bool want = !(getenv("GSB_ENC_TMA") && strcmp(getenv("GSB_ENC_TMA"), "0") == 0);
     EncMaps maps;
     memset(&maps, 0, sizeof(maps));
-    bool ok = want;
+    bool ok = true;
     if (ok && !BWD) {
         for (int t = 0; t < e.T && ok; ++t)
             if (e.proj[t])
@@ -490,7 +509,8 @@ static gsb_status launch_enc(const char* name, const GraphDev& g, const EncDev& 
         ok = encode_tmap_bf16_2d(&maps.hi[0], e.d_hi, e.d_out, cap_rows, e.d_out, 64, 64) &&
              encode_tmap_bf16_2d(&maps.lo[0], e.d_lo, e.d_out, cap_rows, e.d_out, 64, 64);
     }
-    maps.use = ok ? 1 : 0;
+    GSB_CHECK_ARG(ok, "%s: TMA descriptors of the B operand could not be encoded", name);
+    maps.use = 1;
     GSB_LAUNCH(name, enc_umma_kernel<BWD>, kNumSMs, EN_WS_THREADS, EN_SMEM, s, g, e, m, src_gid, H0, out, maps);
     return GSB_OK;
 }
