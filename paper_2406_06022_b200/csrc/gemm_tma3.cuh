@@ -26,7 +26,6 @@
 #pragma once
 #include <cuda.h>
 
-#include "gemm_simt.cuh"
 #include "gemm_tma.cuh"
 
 namespace gsb {
@@ -122,11 +121,8 @@ __device__ __forceinline__ T3Off t3_offsets(int t) {
 // for ONE of the two operands: with both his truncated the dropped lo_A lo_B term has the sign
 // of every product (both residuals carry the sign of their x) and accumulates like the result
 // itself; one round-to-nearest residual makes it zero-mean (the 3xTF32 accuracy of an rna split)
-// hm (TN B only, optional): the ReLU mask source h at the same (row, column)s; values whose h
-// is not > 0 are zeroed (dZ = dh * 1[h > 0] folded into the weight-gradient GEMM)
 template <bool MN, bool ZERO, bool CS, bool HI>
-__device__ __forceinline__ void t3_split(uint32_t raw, uint32_t lo, const T3Off& o, int klim, double4& cs,
-                                         const float4* hm = nullptr) {
+__device__ __forceinline__ void t3_split(uint32_t raw, uint32_t lo, const T3Off& o, int klim, double4& cs) {
     float4 v[T3_PER];
 #pragma unroll
     for (int i = 0; i < T3_PER; ++i) v[i] = lds128(raw + (MN ? o.m[i] : o.k[i]));
@@ -136,12 +132,6 @@ __device__ __forceinline__ void t3_split(uint32_t raw, uint32_t lo, const T3Off&
         if (ZERO && o.kk[i] >= klim) {
             v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (!HI) sts128(raw + off, 0u, 0u, 0u, 0u);
-        }
-        if (hm) {
-            v[i].x = hm[i].x > 0.f ? v[i].x : 0.f;
-            v[i].y = hm[i].y > 0.f ? v[i].y : 0.f;
-            v[i].z = hm[i].z > 0.f ? v[i].z : 0.f;
-            v[i].w = hm[i].w > 0.f ? v[i].w : 0.f;
         }
         if (CS) { cs.x += v[i].x; cs.y += v[i].y; cs.z += v[i].z; cs.w += v[i].w; }   // fp64: exact-ish sums
         if (HI) {
@@ -384,21 +374,12 @@ __global__ void __launch_bounds__(T3_THREADS, 1) tma3_gemm_kernel(const __grid_c
             } else if (MODE == UMMA_TN) {
                 const int64_t rb = c.row0 + (int64_t)c.p * 32;
                 const int klim = (int)min((int64_t)32, c.rlim - rb);
-                float4 hm[T3_PER];
-                if (P.H) {          // ReLU mask of dZ from h (P.H [rows][N]), rows past the chunk unread
-                    const float* hp = P.H + c.n0 + 4 * (t & 31);
-#pragma unroll
-                    for (int i = 0; i < T3_PER; ++i)
-                        hm[i] = (o.kk[i] < klim && c.n0 + 4 * (t & 31) < P.N)
-                                    ? __ldg(reinterpret_cast<const float4*>(hp + (rb + o.kk[i]) * (int64_t)P.N))
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
                 if (klim < 32) {
                     t3_split<true, true, false, false>(a, a + UM_PANEL, o, klim, cs);
-                    t3_split<true, true, true, true>(b, b + UM_PANEL, o, klim, cs, P.H ? hm : nullptr);
+                    t3_split<true, true, true, true>(b, b + UM_PANEL, o, klim, cs);
                 } else {
                     t3_split<true, false, false, false>(a, a + UM_PANEL, o, 32, cs);
-                    t3_split<true, false, true, true>(b, b + UM_PANEL, o, 32, cs, P.H ? hm : nullptr);
+                    t3_split<true, false, true, true>(b, b + UM_PANEL, o, 32, cs);
                 }
             } else if (MODE == UMMA_NN) {
                 t3_split<false, false, false, false>(a, a + UM_PANEL, o, 32, cs);
@@ -632,14 +613,6 @@ template <int MODE>
 inline gsb_status launch_gemm_v(const char* name, UProb P, int64_t tiles_upper, int64_t a_rows, int64_t a_w,
                                 int64_t b_rows, int64_t b_w, cudaStream_t s) {
     const int ver = gemm_version();
-    // SIMT small-problem path: opt-in (GSB_SIMT=1); its K chunks are load-latency bound and it
-    // measured slower than the tcgen05 kernel in the step (profiles/round2_gemm_tma3.md)
-    static const bool simt = getenv("GSB_SIMT") && strcmp(getenv("GSB_SIMT"), "1") == 0;
-    if (simt && ver == 3) {
-        bool launched = false;
-        const gsb_status st = launch_simt_gemm<MODE>(name, P, a_rows, s, &launched);
-        if (st != GSB_OK || launched) return st;
-    }
     if (ver == 3) {
         UProb Q = P;
         if (Q.ksplit < 1) Q.ksplit = 1;
@@ -679,7 +652,6 @@ inline gsb_status launch_gemm_v(const char* name, UProb P, int64_t tiles_upper, 
             if (st != GSB_OK || launched) return st;
         }
     }
-    GSB_CHECK_ARG(!P.H, "%s: the fused ReLU mask needs the TMA GEMM (tma3_tn_ready)", name);
     return launch_gemm<MODE>(name, P, tiles_upper, a_rows, a_w, b_rows, b_w, s);
 }
 

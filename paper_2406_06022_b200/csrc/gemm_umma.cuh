@@ -54,7 +54,6 @@ struct UProb {
     const float* B;        // NN/NT: W ; TN: dH
     int64_t ldb;
     int64_t bslot;         // W slot stride (elements); 0 for a single matrix
-    const float* H;        // relu mask source for dZ (NT: with A, TN: with B), may be null
     int relu;
     int d_in;              // K per slot (NN), output cols per slot (NT), output rows per slot (TN)
     int N;                 // output cols (NN, TN) / reduction length (NT)

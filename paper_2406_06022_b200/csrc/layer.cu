@@ -255,148 +255,6 @@ static gsb_status launch_agg_seg(const char* name, cudaStream_t s, const GraphDe
     return GSB_OK;
 }
 
-// ------------------------------------------------------------------------------------
-// aggregation, row-streaming (default for layer 0): warp per dst row, the whole warp on one
-// source row at a time (lane = row_bytes / 32 bytes of it: 8 B = 4 bf16 of a 128-d bf16 row),
-// U source rows in flight.  A row's edges of all its slots are contiguous, [seg_ptr[j*S],
-// seg_ptr[j*S + St]), so one coalesced key load per 32 edges and one stream of row loads
-// cover every slot; the slot boundary is warp-uniform, so a finished slot's mean is stored
-// (16 B per lane) without any cross-lane reduction, and empty slots cost one store.
-// ------------------------------------------------------------------------------------
-template <int BPL>
-struct LaneChunk;                       // BPL bytes of a row per lane
-template <>
-struct LaneChunk<4> { using T = uint32_t; };
-template <>
-struct LaneChunk<8> { using T = uint2; };
-template <>
-struct LaneChunk<16> { using T = uint4; };
-
-template <bool BF16, int BPL>
-__device__ __forceinline__ void lane_acc(float* acc, const typename LaneChunk<BPL>::T& x) {
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(&x);
-#pragma unroll
-    for (int i = 0; i < BPL / 4; ++i) {
-        if (BF16) {
-            acc[2 * i] += bf16_lo(w[i]);
-            acc[2 * i + 1] += bf16_hi(w[i]);
-        } else {
-            acc[i] += __uint_as_float(w[i]);
-        }
-    }
-}
-
-template <bool FEAT, bool BF16, int BPL>
-__global__ void __launch_bounds__(256, 4) agg_row_kernel(GraphDev g, const HopMeta* __restrict__ m,
-                                                      const int64_t* __restrict__ seg_ptr,
-                                                      const int32_t* __restrict__ e_src,
-                                                      const int64_t* __restrict__ e_src_gid,
-                                                      const int64_t* __restrict__ dst_gid, const char* __restrict__ h,
-                                                      int row_bytes, int d, float* __restrict__ acat, int64_t lda,
-                                                      const int32_t* __restrict__ rowmap, int64_t seg_cap) {
-    GSB_PDL_ENTRY();
-    using CT = typename LaneChunk<BPL>::T;
-    constexpr int V = BF16 ? BPL / 2 : BPL / 4;      // floats per lane
-    constexpr int U = 8;                              // source rows in flight
-    __shared__ int64_t s_dst_off[kMaxT + 1], s_src_off[kMaxT + 1];
-    if (threadIdx.x <= (unsigned)g.T) {
-        s_dst_off[threadIdx.x] = m->dst_off[threadIdx.x];
-        s_src_off[threadIdx.x] = m->src_off[threadIdx.x];
-    }
-    const int64_t n = m->n_dst;
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int S = g.S;
-    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < n; j += warps) {
-        int t = 0;
-        for (int k = 1; k < g.T; ++k) t += (j >= s_dst_off[k]) ? 1 : 0;
-        const int St = g.n_slots[t];
-        float* out = acat + j * lda + lane * V;
-        const int64_t bl = (lane <= St) ? seg_ptr[j * S + lane] : 0;    // slot boundaries
-        const int64_t E0 = __shfl_sync(0xffffffffu, bl, 0), E1 = __shfl_sync(0xffffffffu, bl, St);
-        // the self row's chunk, loaded while the edges stream
-        const char* ps = reinterpret_cast<const char*>(
-            src_row<FEAT>(g, h, row_bytes, FEAT ? dst_gid[j] : s_src_off[t] + (j - s_dst_off[t]), rowmap));
-        const CT xs = *reinterpret_cast<const CT*>(ps + lane * BPL);
-        int slot = 0;
-        int64_t b0 = E0, b1 = __shfl_sync(0xffffffffu, bl, 1);   // current slot [b0, b1)
-        float acc[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) acc[v] = 0.f;
-        auto flush = [&]() {    // mean of slot `slot` (warp-uniform), then the next slot
-            const float inv = (b1 > b0) ? 1.f / (float)(b1 - b0) : 0.f;
-            float* o = out + (int64_t)slot * d;
-#pragma unroll
-            for (int v = 0; v < V; v += 4)
-                if (v + 3 < V) *reinterpret_cast<float4*>(o + v) = make_float4(acc[v] * inv, acc[v + 1] * inv,
-                                                                               acc[v + 2] * inv, acc[v + 3] * inv);
-                else
-                    for (int q = v; q < V; ++q) o[q] = acc[q] * inv;
-#pragma unroll
-            for (int v = 0; v < V; ++v) acc[v] = 0.f;
-            ++slot;
-            b0 = b1;
-            b1 = __shfl_sync(0xffffffffu, bl, min(slot + 1, St));
-        };
-        while (slot < St && b1 == b0) flush();            // leading empty slots
-        for (int64_t cb = E0; cb < E1; cb += 32) {
-            const int64_t ek = cb + lane;
-            const char* pk = (ek < E1) ? reinterpret_cast<const char*>(src_row<FEAT>(
-                                             g, h, row_bytes, FEAT ? e_src_gid[ek] : (int64_t)e_src[ek], rowmap))
-                                       : nullptr;
-            const int cnt = (int)min((int64_t)32, E1 - cb);
-            for (int k = 0; k < cnt; k += U) {
-                CT x[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const uint64_t pu = __shfl_sync(0xffffffffu, (uint64_t)pk, (k + u) & 31);
-                    if (k + u < cnt) x[u] = __ldg(reinterpret_cast<const CT*>(pu + lane * BPL));
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (k + u < cnt) {
-                        // a long segment is capped (fanout ALL hubs): heavy_kernel adds the tail
-                        if (cb + k + u - b0 < seg_cap) lane_acc<BF16, BPL>(acc, x[u]);
-                        if (cb + k + u + 1 == b1)
-                            do flush(); while (slot < St && b1 == b0);
-                    }
-                }
-            }
-        }
-        while (slot < St) flush();                          // trailing empty slots
-        float r[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) r[v] = 0.f;
-        lane_acc<BF16, BPL>(r, xs);
-        float* o = out + (int64_t)St * d;
-#pragma unroll
-        for (int v = 0; v < V; v += 4)
-            if (v + 3 < V) *reinterpret_cast<float4*>(o + v) = make_float4(r[v], r[v + 1], r[v + 2], r[v + 3]);
-            else
-                for (int q = v; q < V; ++q) o[q] = r[q];
-    }
-}
-
-template <bool FEAT, bool BF16>
-static gsb_status launch_agg_row(const char* name, cudaStream_t s, const GraphDev& g, const HopBufs& hb, const char* h,
-                                 int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap,
-                                 int64_t seg_cap) {
-    static const int bps = getenv("GSB_AGG_BPS") ? atoi(getenv("GSB_AGG_BPS")) : 4;   // one wave at 4 blocks / SM
-    const int grid = grid_for(hb.cap_dst * 32, 256, kNumSMs * bps);
-    const int bpl = row_bytes / 32;
-    if (bpl == 4)
-        GSB_LAUNCH(name, (agg_row_kernel<FEAT, BF16, 4>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,
-                   hb.e_src_gid, hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
-    else if (bpl == 8)
-        GSB_LAUNCH(name, (agg_row_kernel<FEAT, BF16, 8>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,
-                   hb.e_src_gid, hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
-    else
-        GSB_LAUNCH(name, (agg_row_kernel<FEAT, BF16, 16>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src,
-                   hb.e_src_gid, hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
-    return GSB_OK;
-}
-
 template <bool FEAT, bool BF16>
 static gsb_status launch_agg_lpe(const char* name, int grid, cudaStream_t s, const GraphDev& g, const HopBufs& hb,
                                  const char* h, int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap,
@@ -523,220 +381,6 @@ static gsb_status launch_heavy(cudaStream_t s, const GraphDev& g, const HopBufs&
     return GSB_OK;
 }
 
-// ------------------------------------------------------------------------------------
-// aggregation through a shared-memory ring filled by bulk async copies (cp.async.bulk, the
-// TMA engine): one producer warp walks the CTA's dst rows in items of AB_R rows and copies
-// every source row of the items' segments plus their self rows into the ring (one 16-B
-// aligned bulk copy per row, completion by mbarrier transaction count); AB_W consumer warps
-// take the items round-robin, sum each segment's rows out of shared memory (lane l owns bytes
-// [l*LB, (l+1)*LB) of a row) and store the means and the self row.  Bytes in flight are
-// bounded by the ring (up to ~200 KB per SM), not by registers: the gather is issued far ahead
-// of the arithmetic.  Items are released in any order; the producer reclaims ring space in
-// item order.  Requires fanout >= 0 (an item must fit the ring).
-// ------------------------------------------------------------------------------------
-constexpr int AB_W = 8;       // consumer warps
-constexpr int AB_NI = 16;     // items in flight per CTA
-constexpr int AB_R = 2;       // dst rows per item
-
-struct AbItem {
-    int64_t j0, e0, start;    // first dst row, first edge, ring position (monotonic rows)
-    int32_t ne, nr;           // edges, rows (edges + self rows)
-    int32_t pos;              // start % cap
-};
-
-template <bool BF16, int LB>
-__device__ __forceinline__ void ab_acc(float* acc, const uint8_t* p) {
-    if (LB == 16) {
-        const uint4 x = *reinterpret_cast<const uint4*>(p);
-        chunk_acc<BF16>(acc, x);
-    } else if (LB == 8) {
-        const uint2 x = *reinterpret_cast<const uint2*>(p);
-        if (BF16) {
-            acc[0] += bf16_lo(x.x); acc[1] += bf16_hi(x.x); acc[2] += bf16_lo(x.y); acc[3] += bf16_hi(x.y);
-        } else {
-            acc[0] += __uint_as_float(x.x); acc[1] += __uint_as_float(x.y);
-        }
-    } else {
-        const uint32_t x = *reinterpret_cast<const uint32_t*>(p);
-        if (BF16) {
-            acc[0] += bf16_lo(x); acc[1] += bf16_hi(x);
-        } else {
-            acc[0] += __uint_as_float(x);
-        }
-    }
-}
-
-template <bool FEAT, bool BF16, int LB>
-__global__ void __launch_bounds__(32 * (AB_W + 1), 1) agg_bulk_kernel(
-    GraphDev g, const HopMeta* __restrict__ m, const int64_t* __restrict__ seg_ptr, const int32_t* __restrict__ e_src,
-    const int64_t* __restrict__ e_src_gid, const int64_t* __restrict__ dst_gid, const char* __restrict__ h, int rb,
-    int d, float* __restrict__ acat, int64_t lda, const int32_t* __restrict__ rowmap, int cap) {
-    GSB_PDL_ENTRY();
-    constexpr int EPL = BF16 ? LB / 2 : LB / 4;      // elements per lane
-    extern __shared__ __align__(128) uint8_t ring[];
-    __shared__ __align__(8) uint64_t full[AB_NI], empty[AB_NI];
-    __shared__ AbItem info[AB_NI];
-    __shared__ int64_t s_dst_off[kMaxT + 1], s_src_off[kMaxT + 1];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid <= g.T) {
-        s_dst_off[tid] = m->dst_off[tid];
-        s_src_off[tid] = m->src_off[tid];
-    }
-    if (tid == 0) {
-        for (int i = 0; i < AB_NI; ++i) {
-            umma::mbar_init(&full[i], 1);
-            umma::mbar_init(&empty[i], 1);
-        }
-        umma::fence_barrier_init();
-    }
-    __syncthreads();
-    const int64_t n = m->n_dst;
-    const int S = g.S;
-    const int64_t items = (n + AB_R - 1) / AB_R;
-    const int64_t i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
-    const int nq = (int)(i1 - i0);
-    auto row_type = [&](int64_t j) {
-        int t = 0;
-        for (int k = 1; k < g.T; ++k) t += (j >= s_dst_off[k]) ? 1 : 0;
-        return t;
-    };
-    if (warp == 0) {
-        // ------------------------------------------------------------- producer
-        int64_t head = 0;
-        int hpos = 0;                                 // head % cap
-        int oldest = 0;
-        for (int q = 0; q < nq; ++q) {
-            const int64_t j0 = (i0 + q) * AB_R, j1 = min(n, j0 + AB_R);
-            const int64_t E0 = seg_ptr[j0 * S], E1 = seg_ptr[j1 * S];
-            const int ne = (int)(E1 - E0), nr = ne + (int)(j1 - j0);
-            // a free item slot and ring space: reclaim released items in order
-            while (oldest < q && (q - oldest >= AB_NI || head + nr - info[oldest % AB_NI].start > cap)) {
-                umma::mbar_wait(&empty[oldest % AB_NI], (uint32_t)((oldest / AB_NI) & 1));
-                ++oldest;
-            }
-            const int slot = q % AB_NI;
-            if (lane == 0) {
-                AbItem it;
-                it.j0 = j0; it.e0 = E0; it.start = head; it.ne = ne; it.nr = nr; it.pos = hpos;
-                info[slot] = it;
-                tma::mbar_expect_tx(&full[slot], (uint32_t)nr * (uint32_t)rb);
-            }
-            __syncwarp();
-            for (int i = lane; i < nr; i += 32) {
-                const char* src;
-                if (i < ne) {
-                    if (FEAT) src = reinterpret_cast<const char*>(feat_row(g, e_src_gid[E0 + i]));
-                    else {
-                        const int64_t k = e_src[E0 + i];
-                        src = h + (rowmap ? (int64_t)rowmap[k] : k) * rb;
-                    }
-                } else {
-                    const int64_t j = j0 + (i - ne);
-                    if (FEAT) src = reinterpret_cast<const char*>(feat_row(g, dst_gid[j]));
-                    else {
-                        const int t = row_type(j);
-                        const int64_t k = s_src_off[t] + (j - s_dst_off[t]);
-                        src = h + (rowmap ? (int64_t)rowmap[k] : k) * rb;
-                    }
-                }
-                int p = hpos + i;
-                if (p >= cap) p -= cap;
-                const uint32_t dst = umma::smem_u32(ring + (size_t)p * rb);
-                asm volatile(
-                    "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                    "l"(src), "r"(rb), "r"(umma::smem_u32(&full[slot]))
-                    : "memory");
-            }
-            head += nr;
-            hpos += nr;
-            if (hpos >= cap) hpos -= cap;
-        }
-    } else {
-        // ------------------------------------------------------------- consumers
-        const int cw = warp - 1;
-        for (int q = cw; q < nq; q += AB_W) {
-            const int slot = q % AB_NI;
-            umma::mbar_wait(&full[slot], (uint32_t)((q / AB_NI) & 1));
-            const AbItem it = info[slot];
-            const int64_t j1 = min(n, it.j0 + AB_R);
-            for (int64_t j = it.j0; j < j1; ++j) {
-                const int t = row_type(j);
-                const int St = g.n_slots[t];
-                const int64_t bl = (lane <= St) ? seg_ptr[j * S + lane] : 0;
-                float* out = acat + j * lda + lane * EPL;
-                for (int sl = 0; sl < St; ++sl) {
-                    const int64_t e0 = __shfl_sync(0xffffffffu, bl, sl), e1 = __shfl_sync(0xffffffffu, bl, sl + 1);
-                    float acc[EPL];
-#pragma unroll
-                    for (int v = 0; v < EPL; ++v) acc[v] = 0.f;
-                    int pos = it.pos + (int)(e0 - it.e0);
-                    if (pos >= cap) pos -= cap;
-                    const int cnt = (int)(e1 - e0);
-#pragma unroll 4
-                    for (int e = 0; e < cnt; ++e) {
-                        ab_acc<BF16, LB>(acc, ring + (size_t)pos * rb + lane * LB);
-                        if (++pos == cap) pos = 0;
-                    }
-                    const float inv = (e1 > e0) ? 1.f / (float)(e1 - e0) : 0.f;
-                    float* o = out + (int64_t)sl * d;
-                    if (EPL == 4) *reinterpret_cast<float4*>(o) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-                    else if (EPL == 2) *reinterpret_cast<float2*>(o) = make_float2(acc[0] * inv, acc[1] * inv);
-                    else
-#pragma unroll
-                        for (int v = 0; v < EPL; ++v) o[v] = acc[v] * inv;
-                }
-                float r[EPL];
-#pragma unroll
-                for (int v = 0; v < EPL; ++v) r[v] = 0.f;
-                int ps = it.pos + it.ne + (int)(j - it.j0);
-                if (ps >= cap) ps -= cap;
-                ab_acc<BF16, LB>(r, ring + (size_t)ps * rb + lane * LB);
-                float* o = out + (int64_t)St * d;
-                if (EPL == 4) *reinterpret_cast<float4*>(o) = make_float4(r[0], r[1], r[2], r[3]);
-                else if (EPL == 2) *reinterpret_cast<float2*>(o) = make_float2(r[0], r[1]);
-                else
-#pragma unroll
-                    for (int v = 0; v < EPL; ++v) o[v] = r[v];
-            }
-            __syncwarp();
-            if (lane == 0) tma::mbar_arrive(&empty[slot]);
-        }
-    }
-}
-
-// ring of up to ~200 KB per CTA, one CTA per SM; false when an item cannot fit (fanout ALL,
-// wide rows) or the row layout does not suit 16-B bulk copies / 32 lanes
-template <bool FEAT, bool BF16>
-static bool launch_agg_bulk(const char* name, cudaStream_t s, const GraphDev& g, const HopBufs& hb, const char* h,
-                            int rb, int d, float* acat, int64_t lda, const int32_t* rowmap, int fanout,
-                            gsb_status* st) {
-    const int lb = rb / 32;
-    if (fanout < 0 || rb % 16 != 0 || rb % 32 != 0 || (lb != 4 && lb != 8 && lb != 16) || (lda & 3) != 0 || d % 32)
-        return false;
-    if (!FEAT && (reinterpret_cast<uintptr_t>(h) & 15) != 0) return false;
-    const int smem = 200 * 1024;
-    const int cap = smem / rb;
-    if ((int64_t)AB_R * ((int64_t)g.S * fanout + 1) > cap) return false;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(agg_bulk_kernel<FEAT, BF16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(agg_bulk_kernel<FEAT, BF16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(agg_bulk_kernel<FEAT, BF16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
-    const int grid = kNumSMs;
-    *st = GSB_OK;
-    auto go = [&](auto kern) -> gsb_status {
-        GSB_LAUNCH(name, kern, grid, 32 * (AB_W + 1), cap * rb, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
-                   hb.dst_gid, h, rb, d, acat, lda, rowmap, cap);
-        return GSB_OK;
-    };
-    if (lb == 4) *st = go(agg_bulk_kernel<FEAT, BF16, 4>);
-    else if (lb == 8) *st = go(agg_bulk_kernel<FEAT, BF16, 8>);
-    else *st = go(agg_bulk_kernel<FEAT, BF16, 16>);
-    return true;
-}
-
 // fanout: the hop's fanout (-1 = ALL); segments can exceed kSegCap only when it does
 static gsb_status launch_agg(const char* name, bool feat, int dtype, cudaStream_t s, const GraphDev& g,
                              const HopBufs& hb, const void* h, int d, float* acat, int64_t lda, const int32_t* rowmap,
@@ -752,36 +396,11 @@ static gsb_status launch_agg(const char* name, bool feat, int dtype, cudaStream_
     // address resolution beats the per-lane one there (profiles/round2_agg_ab.md).  GSB_AGG=warp /
     // seg forces either (A/B).  32-byte lanes: rows of 4..32 such chunks, 32-B aligned.
     const char* am = getenv("GSB_AGG");
-    static const int agg_mode = !am ? 0
-                                    : (strcmp(am, "warp") == 0 ? 1
-                                       : (strcmp(am, "seg") == 0 ? 2 : (strcmp(am, "bulk") == 0 ? 4 : 3)));
-    if (agg_mode == 4) {
-        bool done = false;
-        st = GSB_OK;
-        if (feat)
-            done = dtype == GSB_BF16 ? launch_agg_bulk<true, true>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, fanout, &st)
-                                     : launch_agg_bulk<true, false>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, fanout, &st);
-        else
-            done = dtype == GSB_BF16 ? launch_agg_bulk<false, true>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, fanout, &st)
-                                     : launch_agg_bulk<false, false>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, fanout, &st);
-        if (done) return st;
-    }
+    static const int agg_mode = !am ? 0 : (strcmp(am, "warp") == 0 ? 1 : (strcmp(am, "seg") == 0 ? 2 : 0));
     const bool want_seg = agg_mode == 2 || (agg_mode == 0 && !feat);
     const bool use_seg = want_seg && rb % 32 == 0 && rb / 32 >= 4 && rb / 32 <= 32 && d % 4 == 0 &&
                          (feat || (reinterpret_cast<uintptr_t>(h) & 31) == 0);
-    // row-streaming kernel: opt-in (GSB_AGG=row); on the mag step's layer 0 it measured 44.0 us vs
-    // 35.9 for the warp kernel (profiles/round2_agg_ab.md)
-    const bool want_row = agg_mode == 3;
-    const bool use_row = want_row && !use_seg && (rb == 128 || rb == 256 || rb == 512) && d % 4 == 0 &&
-                         (feat || (reinterpret_cast<uintptr_t>(h) & 15) == 0);
-    if (use_row) {
-        if (feat)
-            st = dtype == GSB_BF16 ? launch_agg_row<true, true>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
-                                   : launch_agg_row<true, false>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
-        else
-            st = dtype == GSB_BF16 ? launch_agg_row<false, true>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
-                                   : launch_agg_row<false, false>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
-    } else if (use_seg) {
+    if (use_seg) {
         if (feat)
             st = dtype == GSB_BF16 ? launch_agg_seg<true, true>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap)
                                    : launch_agg_seg<true, false>(name, s, g, hb, hc, rb, d, acat, lda, rowmap, cap);
@@ -1339,14 +958,9 @@ gsb_status gsb_rgcn_layer_bwd(gsb_blocks_t b, const void* arena, int32_t layer, 
     Pw.rg = rg; Pw.A = acat; Pw.lda = lda; Pw.B = dh_dst; Pw.ldb = d_out;
     Pw.d_in = d_in; Pw.N = d_out; Pw.C = dW; Pw.ldc = d_out; Pw.bslot = (int64_t)d_in * d_out; Pw.db = db;
     Pw.rows_per_chunk = rpc;
-    // dZ = dh * 1[h > 0] once in place before the GEMMs; opt-in (GSB_RELU_FUSE=1): folded into
-    // the weight-gradient GEMM's B split when dZ has no other reader -- measured slower (the mask
-    // loads lengthen the split: dW_l0 29.3 -> 33.3 us, step 0.2030 -> 0.2060 ms, gpurun_out/rf2)
-    static const bool fuse_ok = getenv("GSB_RELU_FUSE") && strcmp(getenv("GSB_RELU_FUSE"), "1") == 0;
-    const bool fuse_mask = fuse_ok && relu && !dh_src && tma3_tn_ready(Pw);
-    if (fuse_mask) {
-        Pw.H = h_dst;
-    } else if (relu) {
+    // dZ = dh * 1[h > 0] once in place before the GEMMs (folding the mask into the weight-gradient
+    // GEMM's B split measured slower: dW_l0 29.3 -> 33.3 us, profiles/round2_gemm_tma3.md)
+    if (relu) {
         GSB_LAUNCH(lname("relu_bwd", layer), relu_bwd_kernel, grid_for(hb.cap_dst * d_out / 4, 256, kNumSMs * 8), 256, 0, s,
                    hb.meta, dh_dst, h_dst, d_out);
     }
