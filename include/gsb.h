@@ -357,6 +357,16 @@ gsb_status gsb_gemm_trace(uint64_t* out, int32_t n);
 gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, const float* bc, int32_t C,
                        const int32_t* labels, const int64_t* seed_gid, int64_t label_gid_base, float* logits_ws,
                        float* row_loss_ws, float* loss, float* dh, float* dWc, float* dbc, void* stream);
+/* The decoder weight gradient on its own: dWc [d][C] = h^T dlogits, dbc [C] = column sums of
+ * dlogits, where dlogits is what gsb_nc_loss left in logits_ws (same h, n, d, C; call it after
+ * gsb_nc_loss in stream order -- e.g. on a second stream that waits for it -- when gsb_nc_loss
+ * was given dWc = dbc = NULL).  Lets the caller overlap dWc with the layers' backward instead of
+ * gsb_nc_loss joining it before returning.  pad_ws: optional device fp32 scratch of
+ * d * ceil4(C) floats, 16-B aligned (NULL allowed): with C % 4 != 0 the GEMM's partials are
+ * reduce-added into it by TMA and copied to dWc (else per-thread atomics into dWc).  dWc, dbc
+ * overwritten; EINVAL on null / bad dims. */
+gsb_status gsb_nc_loss_dw(const float* h, int64_t n, int32_t d, const float* logits_ws, int32_t C, float* dWc,
+                          float* dbc, float* pad_ws, void* stream);
 
 /* ======================================================================================
  * Full-graph inference (P:L393 layer-wise inference, P:L403 embedding

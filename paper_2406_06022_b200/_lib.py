@@ -96,6 +96,7 @@ SIGS = {
     "gsb_exchange_sizes": [P, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64),
                            C.POINTER(i64)],
     "gsb_nc_loss": [P, i64, i32, P, P, i32, P, P, i64, P, P, P, P, P, P, P],
+    "gsb_nc_loss_dw": [P, i64, i32, P, i32, P, P, P, P],
     "gsb_adam_step": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P],
     "gsb_adam_step_split": [P, P, P, P, i64, f32, f32, f32, f32, i32, P, P, P, i64, i32, i32, i32, P, P, P],
     "gsb_counter_add": [P, i32, P],

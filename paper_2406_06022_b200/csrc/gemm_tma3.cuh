@@ -601,14 +601,6 @@ inline int gemm_version() {
     return ver;
 }
 
-// true when launch_gemm_v takes the TMA-everything kernel for this TN problem: the caller may
-// then fold dZ's ReLU mask into it (UProb::H = h, [rows][N]) instead of a separate pass
-inline bool tma3_tn_ready(const UProb& P) {
-    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    return gemm_version() == 3 && al(P.A) && al(P.B) && (P.lda & 3) == 0 && (P.ldb & 3) == 0 &&
-           P.rows_per_chunk % 32 == 0 && (P.N & 3) == 0 && P.ldb == P.N;
-}
-
 template <int MODE>
 inline gsb_status launch_gemm_v(const char* name, UProb P, int64_t tiles_upper, int64_t a_rows, int64_t a_w,
                                 int64_t b_rows, int64_t b_w, cudaStream_t s) {

@@ -1030,6 +1030,61 @@ gsb_status gsb_gemm(int32_t mode, const float* A, int64_t lda, const float* B, i
     return GSB_EINVAL;
 }
 
+// dWc = h^T dlogits, dbc = column sums of dlogits (dlogits: what nc_ce / nc_fused left in
+// logits_ws); fused: the SIMT kernel of the GSB_NC=fused decoder, else the tcgen05 TN GEMM
+__global__ void pad_copy_kernel(const float* __restrict__ src, int64_t ld, int64_t rows, int cols,
+                                float* __restrict__ dst) {
+    GSB_PDL_ENTRY();
+    const int64_t total = rows * cols;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / cols;
+        dst[i] = src[r * ld + (i - r * cols)];
+    }
+}
+
+// pad_ws (optional, [d][ldl] fp32): when C's rows are not 16-B multiples, the TN GEMM
+// reduce-adds its row-chunk partials into pad_ws with TMA (instead of 16k per-thread atomics
+// per CTA into the unaligned dWc) and one copy kernel writes dWc
+static gsb_status nc_dw(const float* h, int64_t n, int32_t d, const float* logits_ws, int64_t ldl, int32_t C,
+                        float* dWc, float* dbc, bool fused, cudaStream_t s, float* pad_ws = nullptr) {
+    const bool padded = !fused && pad_ws && ldl != C && (reinterpret_cast<uintptr_t>(pad_ws) & 15) == 0;
+    float* dst = padded ? pad_ws : dWc;
+    const int64_t ldd = padded ? ldl : C;
+    GSB_CUDA(cudaMemsetAsync(dst, 0, sizeof(float) * (size_t)d * ldd, s));
+    GSB_CUDA(cudaMemsetAsync(dbc, 0, sizeof(float) * (size_t)C, s));
+    if (fused) {
+        const int nkt = (d + kNcKT - 1) / kNcKT;
+        GSB_LAUNCH("nc_dwc", nc_dwc_kernel, (int)(nkt * ((n + kNcRC - 1) / kNcRC)), 256, 0, s, h, n, d, logits_ws, ldl,
+                   C, dWc, dbc);
+        return GSB_OK;
+    }
+    UProb P{};
+    P.rg = single_group(n);
+    P.A = h; P.lda = d; P.B = logits_ws; P.ldb = ldl; P.d_in = d; P.N = C; P.C = dst; P.ldc = ldd;
+    static const int rpc = getenv("GSB_DWC_RPC") ? atoi(getenv("GSB_DWC_RPC")) : 64;   // A/B knob
+    P.bslot = 0; P.db = dbc; P.rows_per_chunk = rpc;
+    gsb_status st = launch_gemm_v<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, rpc) * ceil_div(d, 128) * ceil_div(C, 128), n,
+                                           d, n, C, s);
+    if (st != GSB_OK || !padded) return st;
+    GSB_LAUNCH("nc_dwc_copy", pad_copy_kernel, grid_for((int64_t)d * C, 256, kNumSMs * 2), 256, 0, s, pad_ws, ldl,
+               (int64_t)d, C, dWc);
+    return GSB_OK;
+}
+
+static bool nc_fused_mode() {
+    static const bool f = getenv("GSB_NC") && strcmp(getenv("GSB_NC"), "fused") == 0;
+    return f;
+}
+
+gsb_status gsb_nc_loss_dw(const float* h, int64_t n, int32_t d, const float* logits_ws, int32_t C, float* dWc,
+                          float* dbc, float* pad_ws, void* stream) {
+    GSB_CHECK_ARG(h && logits_ws && dWc && dbc, "null argument");
+    GSB_CHECK_ARG(n >= 1 && d > 0 && d % BK == 0 && C >= 1, "bad dims (d %% %d == 0 required)", BK);
+    const int64_t ldl = (C + 3) / 4 * 4;
+    const bool fused = nc_fused_mode() && sizeof(float) * (size_t)kNcTR * (d + ldl) <= 48 * 1024;
+    return nc_dw(h, n, d, logits_ws, ldl, C, dWc, dbc, fused, (cudaStream_t)stream, pad_ws);
+}
+
 gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, const float* bc, int32_t C,
                        const int32_t* labels, const int64_t* seed_gid, int64_t label_gid_base, float* logits_ws,
                        float* row_loss_ws, float* loss, float* dh, float* dWc, float* dbc, void* stream) {
@@ -1040,7 +1095,7 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
     const int64_t ldl = (C + 3) / 4 * 4;   // padded logits row (16-B aligned rows)
     // fused SIMT decoder: opt-in (GSB_NC=fused); measured slower than the tcgen05 GEMMs + CE on the
     // mag step (69.6 + 45.8 us vs 16.4 + 9.8 + 20.3 || 16.4 us, profiles/round2_decoder_scatter.md)
-    const bool nc_fused = getenv("GSB_NC") && strcmp(getenv("GSB_NC"), "fused") == 0;
+    const bool nc_fused = nc_fused_mode();
     const size_t fsm = sizeof(float) * (size_t)kNcTR * (d + ldl);
     if (nc_fused && fsm <= 48 * 1024) {
         float* part = row_loss_ws + ((n + 31) / 32) * 32;
@@ -1050,11 +1105,7 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
                    label_gid_base, logits_ws, row_loss_ws, part, ticket, loss, dh);
         if (dWc || dbc) {
             GSB_CHECK_ARG(dWc && dbc, "dWc and dbc go together");
-            GSB_CUDA(cudaMemsetAsync(dWc, 0, sizeof(float) * (size_t)d * C, s));
-            GSB_CUDA(cudaMemsetAsync(dbc, 0, sizeof(float) * (size_t)C, s));
-            const int nkt = (d + kNcKT - 1) / kNcKT;
-            GSB_LAUNCH("nc_dwc", nc_dwc_kernel, (int)(nkt * ((n + kNcRC - 1) / kNcRC)), 256, 0, s, h, n, d, logits_ws,
-                       ldl, C, dWc, dbc);
+            return nc_dw(h, n, d, logits_ws, ldl, C, dWc, dbc, true, s);
         }
         return GSB_OK;
     }
@@ -1081,14 +1132,7 @@ gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, co
     if (dWc && dh) s = fork_begin(s_main);   // dWc on the side stream, overlapping dh
     if (dWc || dbc) {
         GSB_CHECK_ARG(dWc && dbc, "dWc and dbc go together");
-        GSB_CUDA(cudaMemsetAsync(dWc, 0, sizeof(float) * (size_t)d * C, s));
-        GSB_CUDA(cudaMemsetAsync(dbc, 0, sizeof(float) * (size_t)C, s));
-        UProb P{};
-        P.rg = rg; P.A = h; P.lda = d; P.B = logits_ws; P.ldb = ldl; P.d_in = d; P.N = C; P.C = dWc; P.ldc = C;
-        static const int rpc = getenv("GSB_DWC_RPC") ? atoi(getenv("GSB_DWC_RPC")) : 64;   // A/B knob
-        P.bslot = 0; P.db = dbc; P.rows_per_chunk = rpc;
-        gsb_status st = launch_gemm_v<UMMA_TN>("nc_gemm_dWc", P, ceil_div(n, rpc) * ceil_div(d, 128) * ceil_div(C, 128),
-                                             n, d, n, C, s);
+        gsb_status st = nc_dw(h, n, d, logits_ws, ldl, C, dWc, dbc, false, s);
         if (st != GSB_OK) return st;
     }
     cudaStream_t s_side = s;

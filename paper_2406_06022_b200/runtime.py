@@ -800,6 +800,12 @@ class RGCNTrainer(_TrainerBase):
         self.logits = torch.empty((batch, (max(num_classes, 1) + 3) // 4 * 4), dtype=torch.float32, device=dev)
         self.row_loss = torch.zeros(batch + 640, dtype=torch.float32, device=dev)   # + fused-mean scratch
         self.seeds_dev = torch.empty(batch, dtype=torch.int64, device=dev)
+        # the decoder weight gradient (gsb_nc_loss_dw) on a stream of its own, joined after the
+        # layers' backward instead of inside gsb_nc_loss (GSB_DWC_SIDE=0: joined inside)
+        self.dwc_stream = (torch.cuda.Stream(device=dev) if os.environ.get("GSB_DWC_SIDE", "1") != "0"
+                           else None)
+        self.dwc_ws = (torch.empty(hidden * self.logits.shape[1], dtype=torch.float32, device=dev)
+                       if os.environ.get("GSB_DWC_PAD", "1") != "0" else None)
 
     _BUFFERED = ("sampler", "x0", "acat0", "xperm", "seeds_dev")
 
@@ -818,10 +824,18 @@ class RGCNTrainer(_TrainerBase):
         n = seeds.numel()
         h = self._encode(s)
         top = self.L - 1
+        side = self.dwc_stream
         call("gsb_nc_loss", _ptr(h), n, self.hidden, self._pp("Wc"), self._pp("bc"), self.C, _ptr(self.labels),
              _ptr(seeds), self.label_base, _ptr(self.logits), _ptr(self.row_loss), _ptr(self.loss),
-             _ptr(self.dh[top]), self._pp("Wc", "g"), self._pp("bc", "g"), s)
+             _ptr(self.dh[top]), None if side else self._pp("Wc", "g"), None if side else self._pp("bc", "g"), s)
+        if side is not None:
+            main = stream if stream is not None else torch.cuda.current_stream()
+            side.wait_stream(main)
+            call("gsb_nc_loss_dw", _ptr(h), n, self.hidden, _ptr(self.logits), self.C, self._pp("Wc", "g"),
+                 self._pp("bc", "g"), _ptr(self.dwc_ws), _stream(side))
         self._backward_layers(s)
+        if side is not None:
+            main.wait_stream(side)
 
     def forward_backward(self, seeds: torch.Tensor, step: int, stream=None):
         """Sample -> gather -> layers (input layer first) -> NC loss -> backward."""

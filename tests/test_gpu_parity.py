@@ -386,6 +386,20 @@ def test_nc_loss_parity(torch_cuda, n, d, C):
     close(dh.cpu().numpy(), odh, what="dh")
     close(dWc.cpu().numpy(), odW, what="dWc")
     close(dbc.cpu().numpy(), odb, what="dbc")
+    # split form: gsb_nc_loss without dWc / dbc, then gsb_nc_loss_dw on a second stream that
+    # waits for it (what the trainer does): the same kernels as the joined call
+    dWc2 = torch.full((d, C), 7.0, dtype=torch.float32, device="cuda")
+    dbc2 = torch.full((C,), 7.0, dtype=torch.float32, device="cuda")
+    side = torch.cuda.Stream()
+    call("gsb_nc_loss", P(ht), n, d, P(Wt), P(bt), C, P(yt), P(gid), 0, P(logits), P(rl), P(loss), P(dh), None, None,
+         None)
+    side.wait_stream(torch.cuda.current_stream())
+    pad = torch.empty(d * ldl, dtype=torch.float32, device="cuda")
+    call("gsb_nc_loss_dw", P(ht), n, d, P(logits), C, P(dWc2), P(dbc2), P(pad), C_.c_void_p(side.cuda_stream))
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    close(dWc2.cpu().numpy(), odW, what="dWc (gsb_nc_loss_dw)")
+    close(dbc2.cpu().numpy(), odb, what="dbc (gsb_nc_loss_dw)")
 
 
 @pytest.mark.parametrize("name,batch", [("mag_small", 2600), ("mag_small", 3000), ("mag_small", 3200),
