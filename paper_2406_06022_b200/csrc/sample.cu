@@ -391,8 +391,11 @@ __global__ void __launch_bounds__(kCntThreads) count_scan_kernel(const int64_t* 
 // ------------------------------------------------------------------------------------
 // fill: one group of G lanes per segment (G >= fanout: 8, 16 or 32)
 // ------------------------------------------------------------------------------------
+#ifndef GSB_FILL_MINB
+#define GSB_FILL_MINB 8      // 32 registers: 8 blocks / SM (46 registers at 5: sample_fill 42.4 -> 39.7 us in the step)
+#endif
 template <int G>
-__global__ void __launch_bounds__(256) fill_kernel(GraphDev g, const HopMeta* __restrict__ m,
+__global__ void __launch_bounds__(256, GSB_FILL_MINB) fill_kernel(GraphDev g, const HopMeta* __restrict__ m,
                                                    const int64_t* __restrict__ dst_gid, int64_t cap_dst,
                                                    const int64_t* __restrict__ seg_ptr, int fanout, Excl ex,
                                                    uint64_t seed, uint32_t step_host, const uint32_t* step_dev, int hop,
