@@ -208,6 +208,7 @@ struct HopMeta {
 // Per-hop device buffers inside the arena.
 struct HopBufs {
     int64_t cap_dst, cap_edges, cap_src;
+    int64_t cap_seeds;    // the batch's seed capacity (hop 1's cap_dst): a host-side size hint
     HopMeta* meta;
     int64_t* dst_gid;     // [cap_dst]   (hop 1: seed copy; else previous hop's src_gid)
     int64_t* cnt;         // [cap_dst*S + 1]

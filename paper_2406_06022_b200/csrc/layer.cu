@@ -119,6 +119,91 @@ __global__ void __launch_bounds__(256, GSB_AGG_MINB) agg_kernel(GraphDev g, cons
 }
 
 // ------------------------------------------------------------------------------------
+// aggregation, half-warp per dst row (layer 0, rows of >= 256 B): the two 16-lane halves of a
+// warp run two dst rows side by side, so the dependent chain of each segment (key load ->
+// row address -> row loads) of one row overlaps the other's; 16 lanes x 16 B cover 256 B of
+// a source row per pass, 4 source rows in flight per lane, no cross-lane reduction.  The
+// halves diverge freely (own loop trip counts); every shuffle names only its half.
+// Requires S < 16 (a row's slot boundaries live in one lane each of its half).  Taken for
+// 256-B rows of large batches (launch_agg_lpe).
+// ------------------------------------------------------------------------------------
+#ifndef GSB_AGG_HALF
+#define GSB_AGG_HALF 1
+#endif
+template <bool FEAT, bool BF16>
+__global__ void __launch_bounds__(256, GSB_AGG_MINB) agg_half_kernel(
+    GraphDev g, const HopMeta* __restrict__ m, const int64_t* __restrict__ seg_ptr, const int32_t* __restrict__ e_src,
+    const int64_t* __restrict__ e_src_gid, const int64_t* __restrict__ dst_gid, const char* __restrict__ h,
+    int row_bytes, int d, float* __restrict__ acat, int64_t lda, const int32_t* __restrict__ rowmap, int64_t seg_cap) {
+    GSB_PDL_ENTRY();
+    constexpr int V = Chunk<BF16>::kVec;
+    __shared__ int64_t s_dst_off[kMaxT + 1], s_src_off[kMaxT + 1];
+    if (threadIdx.x <= (unsigned)g.T) {
+        s_dst_off[threadIdx.x] = m->dst_off[threadIdx.x];
+        s_src_off[threadIdx.x] = m->src_off[threadIdx.x];
+    }
+    const int64_t n = m->n_dst;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, hl = lane & 15;
+    const unsigned hmask = (lane < 16) ? 0x0000ffffu : 0xffff0000u;
+    const int S = g.S;
+    const int64_t halves = ((int64_t)gridDim.x * blockDim.x) >> 4;
+    const int cpr = row_bytes >> 4;
+    for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4; j < n; j += halves) {
+        int t = 0;
+        for (int k = 1; k < g.T; ++k) t += (j >= s_dst_off[k]) ? 1 : 0;
+        const int St = g.n_slots[t];
+        float* out = acat + j * lda;
+        const int64_t bl = (hl <= St) ? seg_ptr[j * S + hl] : 0;
+        const uint4* ps = src_row<FEAT>(g, h, row_bytes, FEAT ? dst_gid[j] : s_src_off[t] + (j - s_dst_off[t]), rowmap);
+        for (int s = 0; s < St; ++s) {
+            const int64_t e0 = __shfl_sync(hmask, bl, s, 16), e1 = __shfl_sync(hmask, bl, s + 1, 16);
+            const float inv = (e1 > e0) ? 1.f / (float)(e1 - e0) : 0.f;
+            const int64_t ec = (e1 - e0 > seg_cap) ? e0 + seg_cap : e1;
+            for (int c0 = 0; c0 < cpr; c0 += 16) {
+                const int c = c0 + hl;
+                const bool cl = c < cpr;
+                float acc[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] = 0.f;
+                for (int64_t cb = e0; cb < ec; cb += 16) {
+                    const uint4* prow = (cb + hl < ec)
+                        ? src_row<FEAT>(g, h, row_bytes, FEAT ? e_src_gid[cb + hl] : (int64_t)e_src[cb + hl], rowmap)
+                        : nullptr;
+                    const int cnt = (int)min((int64_t)16, ec - cb);
+                    for (int k = 0; k < cnt; k += 4) {
+                        uint4 x[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint64_t pu = __shfl_sync(hmask, (uint64_t)prow, (k + u) & 15, 16);
+                            x[u] = make_uint4(0u, 0u, 0u, 0u);
+                            if (cl && k + u < cnt) x[u] = __ldg(reinterpret_cast<const uint4*>(pu) + c);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) chunk_acc<BF16>(acc, x[u]);
+                    }
+                }
+                if (cl) {
+                    float4* o4 = reinterpret_cast<float4*>(out + (int64_t)s * d + (int64_t)c * V);
+#pragma unroll
+                    for (int v = 0; v < V; v += 4)
+                        o4[v / 4] = make_float4(acc[v] * inv, acc[v + 1] * inv, acc[v + 2] * inv, acc[v + 3] * inv);
+                }
+            }
+        }
+        for (int c = hl; c < cpr; c += 16) {
+            float r[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) r[v] = 0.f;
+            chunk_acc<BF16>(r, __ldg(ps + c));
+            float4* o4 = reinterpret_cast<float4*>(out + (int64_t)St * d + (int64_t)c * V);
+#pragma unroll
+            for (int v = 0; v < V; v += 4) o4[v / 4] = make_float4(r[v], r[v + 1], r[v + 2], r[v + 3]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // aggregation, segment-parallel (default): a group of LPE lanes owns one (dst row j, slot s)
 // unit -- a relation's segment (its mean) or the self slot (the dst's own row) -- and each
 // lane owns 32 bytes of the row (LPE = row bytes / 32: 8 lanes for 128-d bf16 or 64-d fp32,
@@ -260,6 +345,18 @@ static gsb_status launch_agg_lpe(const char* name, int grid, cudaStream_t s, con
                                  const char* h, int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap,
                                  int64_t seg_cap) {
     const int cpr = row_bytes / 16;
+    const char* hk = getenv("GSB_AGG_HALF");   // 0: warp kernel, 2: half kernel whenever it applies (A/B, tests)
+    const bool half_off = hk && strcmp(hk, "0") == 0, half_force = hk && strcmp(hk, "2") == 0;
+    // half-warp rows for 256-B feature rows when the batch is large (amazon_lp, 4096 positives:
+    // layer 0 290 -> 223 us); with 1024 seeds (mag: ~3 rows per warp, 35.3 vs 36.2 us) and for
+    // 512-B rows (two passes per segment: 45.5 vs 55.8 us) the warp kernel stays
+    // (profiles/round2_agg_ab.md).  The seed capacity is the host-side proxy for the row count.
+    const bool many_rows = hb.cap_seeds >= 4 * (int64_t)kNumSMs * 8;
+    if (GSB_AGG_HALF && !half_off && FEAT && cpr == 16 && g.S < 16 && (many_rows || half_force)) {
+        GSB_LAUNCH(name, (agg_half_kernel<FEAT, BF16>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
+                   hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
+        return GSB_OK;
+    }
     if (cpr <= 4) {
         GSB_LAUNCH(name, (agg_kernel<FEAT, BF16, 4>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
                    hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
@@ -1071,9 +1168,9 @@ static gsb_status nc_dw(const float* h, int64_t n, int32_t d, const float* logit
     return GSB_OK;
 }
 
-static bool nc_fused_mode() {
-    static const bool f = getenv("GSB_NC") && strcmp(getenv("GSB_NC"), "fused") == 0;
-    return f;
+static bool nc_fused_mode() {   // read per call: tests switch it inside one process
+    const char* e = getenv("GSB_NC");
+    return e && strcmp(e, "fused") == 0;
 }
 
 gsb_status gsb_nc_loss_dw(const float* h, int64_t n, int32_t d, const float* logits_ws, int32_t C, float* dWc,

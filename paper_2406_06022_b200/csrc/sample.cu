@@ -1063,6 +1063,7 @@ static int64_t* rank_flags(const Blocks* B, void* arena) {
 HopBufs Blocks::hop(int h, void* arena) const {
     HopBufs b;
     b.cap_dst = cap_dst[h];
+    b.cap_seeds = cap_dst[1];
     b.cap_edges = cap_edges[h];
     b.cap_src = cap_dst[h + 1];
     b.meta = at<HopMeta>(arena, off_meta[h]);

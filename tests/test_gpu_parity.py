@@ -446,14 +446,16 @@ def test_gcn_homogeneous_step_parity(torch_cuda):
         check_grads(tr, res, cfg, step)
 
 
-@pytest.mark.parametrize("knob", ["GSB_TCSR", "GSB_NC"])
-def test_optin_paths_parity(torch_cuda, knob, monkeypatch):
-    """The opt-in paths keep parity: GSB_TCSR=1 (by-source transposed CSR per block + the
-    deterministic gather scatter of the hidden layer's input gradient, §8(a) a4) and GSB_NC=fused
-    (the fused SIMT decoder: logits, softmax-CE, dh, dWc, dbc)."""
+@pytest.mark.parametrize("knob,value,case", [("GSB_TCSR", "1", "mag_small"), ("GSB_NC", "fused", "mag_small"),
+                                             ("GSB_AGG_HALF", "2", "mag_small_bf16")])
+def test_optin_paths_parity(torch_cuda, knob, value, case, monkeypatch):
+    """The opt-in / size-selected paths keep parity: GSB_TCSR=1 (by-source transposed CSR per
+    block + the deterministic gather scatter of the hidden layer's input gradient, §8(a) a4),
+    GSB_NC=fused (the fused SIMT decoder: logits, softmax-CE, dh, dWc, dbc) and GSB_AGG_HALF=2
+    (the half-warp-per-row layer-0 aggregation that large batches take, forced at a small one)."""
     import torch
-    monkeypatch.setenv(knob, "1" if knob == "GSB_TCSR" else "fused")
-    cfg = CASES["mag_small"]()
+    monkeypatch.setenv(knob, value)
+    cfg = CASES[case]()
     st, og = gpu_store(cfg), oracle_graph(cfg)
     tr = _gpu_trainer(cfg, st)
     params = {k: v.astype(np.float64) for k, v in synth.init_params(cfg).items()}
