@@ -340,6 +340,89 @@ static gsb_status launch_agg_seg(const char* name, cudaStream_t s, const GraphDe
     return GSB_OK;
 }
 
+// quarter-warp per dst row (256-B rows): 8 lanes x 32 B (256-bit loads) cover a source row,
+// four dst rows per warp side by side -- four dependent segment chains in flight per warp for
+// batches with few rows per warp (mag: ~3).  More registers (x: 4 x 8 words per lane), so
+// 3 blocks / SM.
+#ifndef GSB_AGG_QMINB
+#define GSB_AGG_QMINB 3
+#endif
+template <bool FEAT, bool BF16>
+__global__ void __launch_bounds__(256, GSB_AGG_QMINB) agg_quarter_kernel(
+    GraphDev g, const HopMeta* __restrict__ m, const int64_t* __restrict__ seg_ptr, const int32_t* __restrict__ e_src,
+    const int64_t* __restrict__ e_src_gid, const int64_t* __restrict__ dst_gid, const char* __restrict__ h,
+    int row_bytes, int d, float* __restrict__ acat, int64_t lda, const int32_t* __restrict__ rowmap, int64_t seg_cap) {
+    GSB_PDL_ENTRY();
+    constexpr int L = 8;
+    constexpr int V = 2 * Chunk<BF16>::kVec;      // values per lane (32 B)
+    __shared__ int64_t s_dst_off[kMaxT + 1], s_src_off[kMaxT + 1];
+    if (threadIdx.x <= (unsigned)g.T) {
+        s_dst_off[threadIdx.x] = m->dst_off[threadIdx.x];
+        s_src_off[threadIdx.x] = m->src_off[threadIdx.x];
+    }
+    const int64_t n = m->n_dst;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, ql = lane & (L - 1);
+    const unsigned qmask = 0xffu << (lane & ~(L - 1));
+    const int S = g.S;
+    const int64_t quarters = ((int64_t)gridDim.x * blockDim.x) / L;
+    for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / L; j < n; j += quarters) {
+        int t = 0;
+        for (int k = 1; k < g.T; ++k) t += (j >= s_dst_off[k]) ? 1 : 0;
+        const int St = g.n_slots[t];
+        float* out = acat + j * lda;
+        const int64_t bl = (ql <= St) ? seg_ptr[j * S + ql] : 0;
+        const char* ps = reinterpret_cast<const char*>(
+            src_row<FEAT>(g, h, row_bytes, FEAT ? dst_gid[j] : s_src_off[t] + (j - s_dst_off[t]), rowmap));
+        for (int s = 0; s < St; ++s) {
+            const int64_t e0 = __shfl_sync(qmask, bl, s, L), e1 = __shfl_sync(qmask, bl, s + 1, L);
+            const float inv = (e1 > e0) ? 1.f / (float)(e1 - e0) : 0.f;
+            const int64_t ec = (e1 - e0 > seg_cap) ? e0 + seg_cap : e1;
+            float acc[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[v] = 0.f;
+            for (int64_t cb = e0; cb < ec; cb += L) {
+                const char* prow = (cb + ql < ec)
+                    ? reinterpret_cast<const char*>(src_row<FEAT>(g, h, row_bytes,
+                                                                  FEAT ? e_src_gid[cb + ql] : (int64_t)e_src[cb + ql], rowmap))
+                    : nullptr;
+                const int cnt = (int)min((int64_t)L, ec - cb);
+                for (int k = 0; k < cnt; k += 4) {
+                    uint32_t x[4][8];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint64_t pu = __shfl_sync(qmask, (uint64_t)prow, (k + u) & (L - 1), L);
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) x[u][w] = 0u;
+                        if (k + u < cnt) ldg256(reinterpret_cast<const char*>(pu) + 32 * ql, x[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        chunk_acc<BF16>(acc, make_uint4(x[u][0], x[u][1], x[u][2], x[u][3]));
+                        chunk_acc<BF16>(acc + V / 2, make_uint4(x[u][4], x[u][5], x[u][6], x[u][7]));
+                    }
+                }
+            }
+            float4* o4 = reinterpret_cast<float4*>(out + (int64_t)s * d + (int64_t)ql * V);
+#pragma unroll
+            for (int v = 0; v < V; v += 4)
+                o4[v / 4] = make_float4(acc[v] * inv, acc[v + 1] * inv, acc[v + 2] * inv, acc[v + 3] * inv);
+        }
+        {
+            uint32_t x[8];
+            ldg256(ps + 32 * ql, x);
+            float r[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) r[v] = 0.f;
+            chunk_acc<BF16>(r, make_uint4(x[0], x[1], x[2], x[3]));
+            chunk_acc<BF16>(r + V / 2, make_uint4(x[4], x[5], x[6], x[7]));
+            float4* o4 = reinterpret_cast<float4*>(out + (int64_t)St * d + (int64_t)ql * V);
+#pragma unroll
+            for (int v = 0; v < V; v += 4) o4[v / 4] = make_float4(r[v], r[v + 1], r[v + 2], r[v + 3]);
+        }
+    }
+}
+
 template <bool FEAT, bool BF16>
 static gsb_status launch_agg_lpe(const char* name, int grid, cudaStream_t s, const GraphDev& g, const HopBufs& hb,
                                  const char* h, int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap,
@@ -352,6 +435,12 @@ static gsb_status launch_agg_lpe(const char* name, int grid, cudaStream_t s, con
     // 512-B rows (two passes per segment: 45.5 vs 55.8 us) the warp kernel stays
     // (profiles/round2_agg_ab.md).  The seed capacity is the host-side proxy for the row count.
     const bool many_rows = hb.cap_seeds >= 4 * (int64_t)kNumSMs * 8;
+    const bool quarter = hk && strcmp(hk, "4") == 0;
+    if (quarter && FEAT && cpr == 16 && g.S < 8 && (reinterpret_cast<uintptr_t>(acat) & 15) == 0 && (lda & 3) == 0) {
+        GSB_LAUNCH(name, (agg_quarter_kernel<FEAT, BF16>), kNumSMs * GSB_AGG_QMINB, 256, 0, s, g, hb.meta, hb.seg_ptr,
+                   hb.e_src, hb.e_src_gid, hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
+        return GSB_OK;
+    }
     if (GSB_AGG_HALF && !half_off && FEAT && cpr == 16 && g.S < 16 && (many_rows || half_force)) {
         GSB_LAUNCH(name, (agg_half_kernel<FEAT, BF16>), grid, 256, 0, s, g, hb.meta, hb.seg_ptr, hb.e_src, hb.e_src_gid,
                    hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);
