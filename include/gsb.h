@@ -353,6 +353,9 @@ gsb_status gsb_gemm_trace(uint64_t* out, int32_t n);
  * Writes: logits_ws [n][ceil4(C)] (scratch, rows padded to a multiple of 4), loss (device fp32 scalar), dh [n][d], dWc [d][C],
  * dbc [C] (overwritten).  row_loss_ws: device fp32 [n + 640] scratch (row losses, then the
  * fused mean's block partials and ticket word); zero-fill it once before the first call.
+ * dh may be NULL (no input gradient); dWc and dbc are both NULL (then logits_ws holds dlogits
+ * for gsb_nc_loss_dw) or both set (computed on the library's side stream and joined into
+ * `stream` before the call returns).  EINVAL on null inputs / bad dims.
  * ==================================================================================== */
 gsb_status gsb_nc_loss(const float* h, int64_t n, int32_t d, const float* Wc, const float* bc, int32_t C,
                        const int32_t* labels, const int64_t* seed_gid, int64_t label_gid_base, float* logits_ws,
