@@ -341,11 +341,12 @@ static gsb_status launch_agg_seg(const char* name, cudaStream_t s, const GraphDe
 }
 
 // quarter-warp per dst row (256-B rows): 8 lanes x 32 B (256-bit loads) cover a source row,
-// four dst rows per warp side by side -- four dependent segment chains in flight per warp for
-// batches with few rows per warp (mag: ~3).  More registers (x: 4 x 8 words per lane), so
-// 3 blocks / SM.
+// four dst rows per warp side by side -- four dependent segment chains in flight per warp
+// (mag: ~3 rows per warp of the warp kernel's grid).  Default for 256-B feature rows with
+// S < 8: mag layer 0 34.2 us (0.417 of HBM) vs 35.2 for the warp kernel, step 0.2009-0.2012 vs
+// 0.2036-0.2040 ms (profiles/round2_agg_ab.md).
 #ifndef GSB_AGG_QMINB
-#define GSB_AGG_QMINB 3
+#define GSB_AGG_QMINB 4       // 64 registers (3: 76-80, slower kernel: 38.5 vs 34.2 us on mag)
 #endif
 template <bool FEAT, bool BF16>
 __global__ void __launch_bounds__(256, GSB_AGG_QMINB) agg_quarter_kernel(
@@ -428,14 +429,16 @@ static gsb_status launch_agg_lpe(const char* name, int grid, cudaStream_t s, con
                                  const char* h, int row_bytes, int d, float* acat, int64_t lda, const int32_t* rowmap,
                                  int64_t seg_cap) {
     const int cpr = row_bytes / 16;
-    const char* hk = getenv("GSB_AGG_HALF");   // 0: warp kernel, 2: half kernel whenever it applies (A/B, tests)
+    // GSB_AGG_HALF (A/B, tests): unset = the choice below, 0 = warp kernel, 2 = half-warp kernel
+    // whenever it applies, 4 = quarter-warp kernel whenever it applies.  256-B feature rows with
+    // S < 8 take the quarter-warp kernel; else 256-B rows of large batches the half-warp kernel
+    // (amazon_lp 290 -> 223 us; the seed capacity is the host-side proxy for the row count);
+    // 512-B rows (two passes per segment in the narrower kernels: 45.5 vs 55.8 us) and the rest
+    // the warp kernel (profiles/round2_agg_ab.md).
+    const char* hk = getenv("GSB_AGG_HALF");
     const bool half_off = hk && strcmp(hk, "0") == 0, half_force = hk && strcmp(hk, "2") == 0;
-    // half-warp rows for 256-B feature rows when the batch is large (amazon_lp, 4096 positives:
-    // layer 0 290 -> 223 us); with 1024 seeds (mag: ~3 rows per warp, 35.3 vs 36.2 us) and for
-    // 512-B rows (two passes per segment: 45.5 vs 55.8 us) the warp kernel stays
-    // (profiles/round2_agg_ab.md).  The seed capacity is the host-side proxy for the row count.
     const bool many_rows = hb.cap_seeds >= 4 * (int64_t)kNumSMs * 8;
-    const bool quarter = hk && strcmp(hk, "4") == 0;
+    const bool quarter = !hk || strcmp(hk, "4") == 0;     // default (GSB_AGG_HALF=0 / 2 select the others)
     if (quarter && FEAT && cpr == 16 && g.S < 8 && (reinterpret_cast<uintptr_t>(acat) & 15) == 0 && (lda & 3) == 0) {
         GSB_LAUNCH(name, (agg_quarter_kernel<FEAT, BF16>), kNumSMs * GSB_AGG_QMINB, 256, 0, s, g, hb.meta, hb.seg_ptr,
                    hb.e_src, hb.e_src_gid, hb.dst_gid, h, row_bytes, d, acat, lda, rowmap, seg_cap);

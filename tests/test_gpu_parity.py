@@ -448,12 +448,14 @@ def test_gcn_homogeneous_step_parity(torch_cuda):
 
 @pytest.mark.parametrize("knob,value,case", [("GSB_TCSR", "1", "mag_small"), ("GSB_NC", "fused", "mag_small"),
                                              ("GSB_AGG_HALF", "2", "mag_small_bf16"),
-                                             ("GSB_AGG_HALF", "4", "mag_small_bf16")])
+                                             ("GSB_AGG_HALF", "0", "mag_small_bf16")])
 def test_optin_paths_parity(torch_cuda, knob, value, case, monkeypatch):
     """The opt-in / size-selected paths keep parity: GSB_TCSR=1 (by-source transposed CSR per
     block + the deterministic gather scatter of the hidden layer's input gradient, §8(a) a4),
-    GSB_NC=fused (the fused SIMT decoder: logits, softmax-CE, dh, dWc, dbc) and GSB_AGG_HALF=2
-    (the half-warp-per-row layer-0 aggregation that large batches take, forced at a small one)."""
+    GSB_NC=fused (the fused SIMT decoder: logits, softmax-CE, dh, dWc, dbc), GSB_AGG_HALF=2 (the
+    half-warp-per-row layer-0 aggregation that large batches take, forced at a small one) and
+    GSB_AGG_HALF=0 (the warp-per-row kernel, which the default quarter-warp kernel replaces for
+    256-B rows)."""
     import torch
     monkeypatch.setenv(knob, value)
     cfg = CASES[case]()
