@@ -18,7 +18,7 @@ CMD="python bench.py --no-cpu-baseline --steps 3 --warmup 3 --profile-steps 2 --
 timeout 900 ncu --nvtx --print-nvtx-rename kernel --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   --print-units base --clock-control none --csv --log-file gpurun_out/${T}_traffic.csv $CMD > gpurun_out/${T}_ncu_traffic.log 2>&1; echo traffic rc $?
 timeout 900 ncu --set full --import-source on --clock-control none --nvtx --print-nvtx-rename kernel \
-  -k regex:"agg_kernel|agg_seg_kernel|tma3_gemm_kernel|fill_kernel" -s 12 -c 6 -o gpurun_out/${T}_full $CMD > gpurun_out/${T}_ncu_full.log 2>&1; echo full rc $?
+  -k regex:"agg_kernel|agg_quarter_kernel|agg_half_kernel|agg_seg_kernel|tma3_gemm_kernel|fill_kernel" -s 12 -c 6 -o gpurun_out/${T}_full $CMD > gpurun_out/${T}_ncu_full.log 2>&1; echo full rc $?
 cuobjdump -sass paper_2406_06022_b200/libgsb.so > /tmp/sass.txt 2>/dev/null
 for m in UTCHMMA UTCBAR UTMALDG UBLKCP LDTM LDG.E.ENL2.256 SYNCS; do echo "$m $(grep -c "$m" /tmp/sass.txt)"; done > gpurun_out/${T}_sass_counts.txt
 grep -n "Function : \|UTMALDG\|UTCHMMA" /tmp/sass.txt | grep -B1 "UTMALDG\|UTCHMMA" | head -60 > gpurun_out/${T}_sass_excerpt.txt
